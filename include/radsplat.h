@@ -1,0 +1,183 @@
+/* radsplat.h -- C ABI of the B200-native RadSplat render-and-prune hot path.
+ *
+ * The reference (fieldsplat, pure NumPy) has no FFI: its boundary is the
+ * Python API re-exported at pkg/src/fieldsplat/__init__.py:39-65. Each entry
+ * point below replaces one piece of that API's compute; the Python package
+ * paper_2403_13806_b200 re-implements the reference signatures on top of it.
+ *
+ *   rs_render            <- render.py:225-287 `_forward` as used by
+ *                           rasterize (render.py:290-293),
+ *                           rasterize_with_contributions (render.py:296-308;
+ *                           max-merge render.py:84-88) and
+ *                           rasterize_filtered (render.py:311-315, :241-244)
+ *   rs_project           <- render.py:95-158 `_project_arrays`
+ *   rs_bin               <- render.py:218-222 `_composite_order` (re-expressed
+ *                           as per-tile (depth, index) lists)
+ *   rs_blend             <- render.py:246-283 compositing loop
+ *   rs_compact /
+ *   rs_compact_bits      <- np.nonzero of visibility.py:204 indicators /
+ *                           io.py:198-243 LSB-first RVIS bitsets
+ *   rs_check_finite      <- core.py:522-525 GaussianScene.is_finite
+ *   rs_max_merge         <- render.py:84-85 ContributionAccumulator.update
+ *
+ * Conventions
+ *   - All data pointers are DEVICE pointers owned by the caller; the library
+ *     never allocates or frees caller memory. Scratch lives in a caller-provided
+ *     workspace sized by rs_workspace_size().
+ *   - Every call is stream-ordered on `stream` (a cudaStream_t passed as void*,
+ *     NULL = legacy default stream) and never synchronizes the host, so a frame
+ *     (rs_render) can be captured into a CUDA graph.
+ *   - Re-entrant per workspace; no global mutable state.
+ *   - Return value: RS_OK or an RS_E* code (mapped to the reference exception
+ *     classes in paper_2403_13806_b200/_native.py).
+ *   - Arithmetic is fp32 with the operation order of the Tier-A contract
+ *     (oracle/cpu_ref.cpp); results are bit-identical to that oracle.
+ */
+#ifndef RADSPLAT_H
+#define RADSPLAT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RS_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define RS_API __attribute__((visibility("default")))
+#else
+#define RS_API
+#endif
+
+enum {
+  RS_OK = 0,
+  RS_EINVAL = 1,            /* bad argument (InvalidParameterError)              */
+  RS_ENONFINITE = 2,        /* non-finite scene (InvalidSceneError)              */
+  RS_ENOMEM_WORKSPACE = 3,  /* workspace too small for n / width / height        */
+  RS_ECUDA = 4,             /* CUDA launch error                                 */
+  RS_EOVERFLOW = 5          /* more tile pairs than the workspace's pair capacity */
+};
+
+/* Scene in device memory: 59 planes of `plane_stride` floats each
+ *   planes 0-2  positions x,y,z          (core.py:478)
+ *   plane  3    opacity logit            (core.py:479; opacity = sigmoid)
+ *   planes 4-6  log scales x,y,z         (core.py:481; scale = exp)
+ *   planes 7-10 quaternion w,x,y,z       (core.py:482; normalized on device)
+ *   planes 11-58 SH coefficient [c][b] at plane 11 + 16*c + b (core.py:480,
+ *               channel-major (N,3,16)); only 11 + 16*c + b < 11+16*c+nb read.
+ */
+typedef struct rs_scene {
+  const float* planes;
+  int64_t n;
+  int64_t plane_stride;
+  int32_t sh_degree; /* 0..3 */
+  int32_t _pad;
+} rs_scene;
+
+/* Pinhole camera (core.py:316-374): p_cam = R p + t, row-major R. `center`
+ * = -R^T t, computed by the caller in fp64 and rounded to fp32. */
+typedef struct rs_camera {
+  int32_t width, height;
+  float fx, fy, cx, cy;
+  float R[9];
+  float t[3];
+  float center[3];
+} rs_camera;
+
+/* RasterizeOptions (render.py:37-46). */
+typedef struct rs_options {
+  float alpha_max, alpha_cut, tau_stop, near_limit, lowpass, sigma_bound;
+} rs_options;
+
+/* Per-frame counters (device side; copied out by rs_read_stats). */
+typedef struct rs_stats {
+  uint32_t n_items;     /* Gaussians projected (N, or M for a filtered render) */
+  uint32_t n_visible;   /* valid after near / bbox culling                     */
+  uint32_t n_pairs;     /* Gaussian-tile overlaps used (min(P, capacity))      */
+  uint32_t overflow;    /* 1 if P exceeded the pair capacity: re-run bigger     */
+  uint64_t evals;       /* E: bbox-gated evaluations with tau >= tau_stop (only
+                           counted when RS_FLAG_COUNT_EVALS is set)            */
+  uint64_t composites;  /* C: composited (pixel, Gaussian) pairs (same flag)   */
+  uint64_t pairs_needed;/* P, the pair capacity this frame needs               */
+} rs_stats;
+
+/* Device pointers into a workspace, for inspection / parity tests. */
+typedef struct rs_buffers {
+  const void* records;          /* n_cap x 64 B projected records, item order:
+                                   {mx,my,na,nb},{nc,opacity,cut2,depth},
+                                   {r,g,b,gid},{x0,x1,y0,y1}                  */
+  const uint32_t* items_sorted; /* n_items item ids in (depth, index) order   */
+  const uint32_t* pair_items;   /* n_pairs item ids, grouped by tile           */
+  const uint32_t* ranges;       /* tiles x 2 : [start, end) into pair_items    */
+  const uint32_t* counters;     /* device counters (first words = rs_stats)    */
+  int32_t tiles_x, tiles_y;
+} rs_buffers;
+
+/* Opaque host-side handle over a caller-allocated device workspace. */
+typedef struct rs_workspace rs_workspace;
+
+#define RS_FLAG_COUNT_EVALS 1u /* count E and C (slower; for roofline accounting) */
+
+RS_API int32_t rs_abi_version(void);
+RS_API const char* rs_status_string(int32_t status);
+
+/* Bytes of device workspace for scenes of <= n_cap items, <= pair_cap tile
+ * pairs and images of <= width x height (tiles_x * tiles_y <= 65536). */
+RS_API size_t rs_workspace_size(int64_t n_cap, int64_t pair_cap, int32_t width, int32_t height);
+
+/* Bind a handle to `device_mem` (>= rs_workspace_size bytes, 256-B aligned,
+ * owned by the caller). The handle itself is freed by rs_workspace_destroy. */
+RS_API int32_t rs_workspace_create(void* device_mem, size_t bytes, int64_t n_cap, int64_t pair_cap, int32_t width,
+                            int32_t height, rs_workspace** out);
+RS_API void rs_workspace_destroy(rs_workspace* ws);
+
+/* One full frame: project -> depth sort -> tile binning -> blend.
+ *   active_idx: optional ascending list of m scene indices (filtered render:
+ *               only listed Gaussians are projected); NULL = all scene->n.
+ *   out_rgb (H*W*3), out_alpha, out_depth (H*W), out_count (H*W int32): may
+ *               all be NULL for a score-only (importance) pass.
+ *   scores:     optional n floats (as uint32 bit patterns of non-negative
+ *               floats) max-merged with each Gaussian's max alpha*tau.
+ */
+RS_API int32_t rs_render(rs_workspace* ws, const rs_scene* scene, const int32_t* active_idx, int64_t m, const rs_camera* cam,
+                  const rs_options* opts, float* out_rgb, float* out_alpha, float* out_depth, int32_t* out_count,
+                  uint32_t* scores, uint32_t flags, void* stream);
+
+/* Stages of rs_render, callable separately (same workspace state machine). */
+RS_API int32_t rs_project(rs_workspace* ws, const rs_scene* scene, const int32_t* active_idx, int64_t m, const rs_camera* cam,
+                   const rs_options* opts, void* stream);
+RS_API int32_t rs_bin(rs_workspace* ws, void* stream);
+/* rs_project that also writes, per item (culled included), the reference's
+ * ProjectedGaussian fields (render.py:49-59) as 16 floats
+ * {mx, my, a, b, c, inv_a, inv_b, inv_c, radius, depth, r, g, b, opacity,
+ *  valid, 0} to out_proj and {x0, x1, y0, y1} to out_bbox (render.py:161-211). */
+RS_API int32_t rs_project_full(rs_workspace* ws, const rs_scene* scene, const int32_t* active_idx, int64_t m,
+                        const rs_camera* cam, const rs_options* opts, float* out_proj, int32_t* out_bbox,
+                        void* stream);
+RS_API int32_t rs_blend(rs_workspace* ws, const rs_options* opts, float* out_rgb, float* out_alpha, float* out_depth,
+                 int32_t* out_count, uint32_t* scores, uint32_t flags, void* stream);
+
+/* Copy the device counters to host memory (synchronizes `stream`). */
+RS_API int32_t rs_read_stats(rs_workspace* ws, rs_stats* out, void* stream);
+RS_API int32_t rs_get_buffers(rs_workspace* ws, rs_buffers* out);
+
+/* Stable compaction: indices i (ascending) with flags[i] != 0, count -> *out_count (device). */
+RS_API size_t rs_compact_workspace_size(int64_t n);
+RS_API int32_t rs_compact(const uint8_t* flags, int64_t n, int32_t* out_idx, uint32_t* out_count, void* scratch,
+                   size_t scratch_bytes, void* stream);
+/* Same from an LSB-first bitset (bit i of byte i/8; io.py:205-206). */
+RS_API int32_t rs_compact_bits(const uint8_t* bits, int64_t n, int32_t* out_idx, uint32_t* out_count, void* scratch,
+                        size_t scratch_bytes, void* stream);
+
+/* *out_bad (device) = number of non-finite values over all 59 planes (0 = finite). */
+RS_API int32_t rs_check_finite(const rs_scene* scene, uint32_t* out_bad, void* stream);
+
+/* dst[i] = max(dst[i], src[i]) over n non-negative floats. */
+RS_API int32_t rs_max_merge(float* dst, const float* src, int64_t n, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RADSPLAT_H */

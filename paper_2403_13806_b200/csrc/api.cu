@@ -1,0 +1,366 @@
+// api.cu -- the C ABI (include/radsplat.h): workspace layout and the frame
+// pipeline  project -> depth sort -> pair emission -> tile sort -> blend.
+//
+// One translation unit: the kernels live in the .cuh files next to this one.
+// Build: see paper_2403_13806_b200/build.py (nvcc -gencode arch=compute_100a,
+// code=sm_100a -fmad=false -lineinfo, static cudart).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+
+#include "bin.cuh"
+#include "blend.cuh"
+#include "compact.cuh"
+#include "project.cuh"
+#include "sort.cuh"
+
+using namespace rs;
+
+namespace {
+
+size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+struct Layout {
+  // per-frame zeroed region [0, frame_bytes)
+  size_t ctr, hist, diff, emit_lb, frame_bytes;
+  size_t ranges, recs, keysA, keysB, valsA, valsB, ptileA, ptileB, pitemA, pitemB, lbA, lbB, total;
+};
+
+int tiles_x(int w) { return (w + kTile - 1) / kTile; }
+
+Layout make_layout(int64_t n_cap, int64_t pair_cap, int W, int H) {
+  Layout L{};
+  const size_t TW = tiles_x(W), TH = tiles_x(H);
+  size_t o = 0;
+  auto take = [&](size_t bytes) { const size_t at = o; o = align_up(o + bytes); return at; };
+  L.ctr = take(sizeof(Counters));
+  L.hist = take(8 * 256 * sizeof(uint32_t));  // depth passes 0-3, tile passes 4-5
+  L.diff = take((TW + 1) * (TH + 1) * sizeof(int32_t));
+  L.emit_lb = take(((size_t)n_cap / 256 + 1) * sizeof(unsigned long long));
+  L.frame_bytes = o;
+  L.ranges = take(TW * TH * sizeof(uint2));
+  L.recs = take((size_t)n_cap * sizeof(Rec));
+  L.keysA = take((size_t)n_cap * 4);
+  L.keysB = take((size_t)n_cap * 4);
+  L.valsA = take((size_t)n_cap * 4);
+  L.valsB = take((size_t)n_cap * 4);
+  L.ptileA = take((size_t)pair_cap * 2);
+  L.ptileB = take((size_t)pair_cap * 2);
+  L.pitemA = take((size_t)pair_cap * 4);
+  L.pitemB = take((size_t)pair_cap * 4);
+  const size_t chunks = (size_t)(std::max(n_cap, pair_cap) + kChunk - 1) / kChunk + 1;
+  L.lbA = take(chunks * 256 * 4);
+  L.lbB = take(chunks * 256 * 4);
+  L.total = o;
+  return L;
+}
+
+}  // namespace
+
+struct rs_workspace {
+  unsigned char* base;
+  size_t bytes;
+  Layout L;
+  int64_t n_cap, pair_cap;
+  int W_cap, H_cap;
+  int sms;
+  // current frame (set by rs_project)
+  uint32_t n_items;
+  int W, H, TW, TH;
+  int tile_passes;
+  bool binned;
+
+  template <typename T> T* at(size_t off) const { return reinterpret_cast<T*>(base + off); }
+  Counters* ctr() const { return at<Counters>(L.ctr); }
+};
+
+namespace {
+
+cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int32_t cuda_status() { return cudaGetLastError() == cudaSuccess ? RS_OK : RS_ECUDA; }
+
+template <typename K>
+void run_sort(rs_workspace* ws, const K* keys0, K* keysA, K* keysB, const uint32_t* vals0, uint32_t* valsA,
+              uint32_t* valsB, const uint32_t* n_ptr, uint32_t n_static, uint32_t n_bound, int passes, int hist_slot,
+              int ticket_slot, bool last_keys, cudaStream_t st, const K** keys_res, const uint32_t** vals_res) {
+  Counters* ctr = ws->ctr();
+  uint32_t* hist = ws->at<uint32_t>(ws->L.hist) + hist_slot * 256;
+  uint32_t* lb[2] = {ws->at<uint32_t>(ws->L.lbA), ws->at<uint32_t>(ws->L.lbB)};
+  const int hist_blocks = (int)std::max<uint32_t>(1, std::min<uint32_t>((n_bound + 255) / 256, ws->sms * 8));
+  radix_hist_kernel<K><<<hist_blocks, 256, 0, st>>>(keys0, n_ptr, n_static, passes, 0, hist, lb[0],
+                                                    ctr->tickets + ticket_slot);
+  const int smem = (int)sizeof(OnesweepSmem<K>);
+  const int chunks = (int)((n_bound + kChunk - 1) / kChunk);
+  const int grid = std::max(1, std::min(chunks, ws->sms * 4));
+  const K* kin = keys0;
+  const uint32_t* vin = vals0;
+  for (int p = 0; p < passes; ++p) {
+    K* kout = (p % 2 == 0) ? keysB : keysA;
+    uint32_t* vout = (p % 2 == 0) ? valsB : valsA;
+    const bool last = p == passes - 1;
+    onesweep_kernel<K><<<grid, kSortThreads, smem, st>>>(kin, vin, kout, vout, n_ptr, n_static, hist + p * 256,
+                                                         lb[p % 2], last ? nullptr : lb[(p + 1) % 2],
+                                                         ctr->tickets + ticket_slot + p, 8 * p,
+                                                         (!last || last_keys) ? 1 : 0);
+    kin = kout;
+    vin = vout;
+  }
+  *keys_res = kin;
+  *vals_res = vin;
+}
+
+void configure_kernels() {  // per device; idempotent
+  cudaFuncSetAttribute(onesweep_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)sizeof(OnesweepSmem<uint32_t>));
+  cudaFuncSetAttribute(onesweep_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)sizeof(OnesweepSmem<uint16_t>));
+  cudaFuncSetAttribute(ranges_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t rs_abi_version(void) { return RS_ABI_VERSION; }
+
+const char* rs_status_string(int32_t s) {
+  switch (s) {
+    case RS_OK: return "ok";
+    case RS_EINVAL: return "invalid argument";
+    case RS_ENONFINITE: return "scene contains non-finite parameters";
+    case RS_ENOMEM_WORKSPACE: return "workspace too small";
+    case RS_ECUDA: return "CUDA error";
+    case RS_EOVERFLOW: return "tile pair capacity exceeded";
+    default: return "unknown status";
+  }
+}
+
+size_t rs_workspace_size(int64_t n_cap, int64_t pair_cap, int32_t width, int32_t height) {
+  if (n_cap < 0 || pair_cap < 0 || width <= 0 || height <= 0) return 0;
+  return make_layout(n_cap, pair_cap, width, height).total;
+}
+
+int32_t rs_workspace_create(void* device_mem, size_t bytes, int64_t n_cap, int64_t pair_cap, int32_t width,
+                            int32_t height, rs_workspace** out) {
+  if (!out || !device_mem || n_cap < 0 || n_cap > 0x7fffffffLL || pair_cap < 0 || pair_cap > 0xffffffffLL ||
+      width <= 0 || height <= 0)
+    return RS_EINVAL;
+  const int TW = tiles_x(width), TH = tiles_x(height);
+  if ((int64_t)TW * TH > 65536 || (int64_t)(TW + 1) * (TH + 1) * 4 > 200 * 1024) return RS_EINVAL;
+  const Layout L = make_layout(n_cap, pair_cap, width, height);
+  if (bytes < L.total) return RS_ENOMEM_WORKSPACE;
+  rs_workspace* ws = new (std::nothrow) rs_workspace();
+  if (!ws) return RS_ECUDA;
+  ws->base = static_cast<unsigned char*>(device_mem);
+  ws->bytes = bytes;
+  ws->L = L;
+  ws->n_cap = n_cap;
+  ws->pair_cap = pair_cap;
+  ws->W_cap = width;
+  ws->H_cap = height;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (cudaDeviceGetAttribute(&ws->sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) ws->sms = 148;
+  configure_kernels();
+  *out = ws;
+  return cuda_status();
+}
+
+void rs_workspace_destroy(rs_workspace* ws) { delete ws; }
+
+static int32_t project_impl(rs_workspace* ws, const rs_scene* scene, const int32_t* active_idx, int64_t m,
+                            const rs_camera* cam, const rs_options* opts, float* full, int32_t* full_bbox,
+                            void* stream) {
+  if (!ws || !scene || !cam || !opts || !scene->planes || scene->sh_degree < 0 || scene->sh_degree > 3 ||
+      scene->n < 0 || scene->plane_stride < scene->n)
+    return RS_EINVAL;
+  const int64_t items = active_idx ? m : scene->n;
+  if (items < 0 || items > ws->n_cap || cam->width <= 0 || cam->height <= 0 || cam->width > ws->W_cap ||
+      cam->height > ws->H_cap)
+    return items > ws->n_cap ? RS_ENOMEM_WORKSPACE : RS_EINVAL;
+  const int TW = tiles_x(cam->width), TH = tiles_x(cam->height);
+  if ((int64_t)(TW + 1) * (TH + 1) > (int64_t)(tiles_x(ws->W_cap) + 1) * (tiles_x(ws->H_cap) + 1))
+    return RS_ENOMEM_WORKSPACE;
+  cudaStream_t st = S(stream);
+  ws->n_items = (uint32_t)items;
+  ws->W = cam->width;
+  ws->H = cam->height;
+  ws->TW = TW;
+  ws->TH = TH;
+  ws->tile_passes = (TW * TH <= 256) ? 1 : 2;
+  ws->binned = false;
+  // zero counters, histograms, difference array and emit look-back in one memset
+  cudaMemsetAsync(ws->base, 0, ws->L.frame_bytes, st);
+  if (items > 0) {
+    if (full)
+      project_kernel<true><<<(unsigned)((items + 127) / 128), 128, 0, st>>>(
+          scene->planes, scene->plane_stride, scene->sh_degree, active_idx, (uint32_t)items, *cam, *opts,
+          ws->at<Rec>(ws->L.recs), ws->at<uint32_t>(ws->L.keysA), ws->ctr(), full, reinterpret_cast<int4*>(full_bbox));
+    else
+      project_kernel<false><<<(unsigned)((items + 127) / 128), 128, 0, st>>>(
+          scene->planes, scene->plane_stride, scene->sh_degree, active_idx, (uint32_t)items, *cam, *opts,
+          ws->at<Rec>(ws->L.recs), ws->at<uint32_t>(ws->L.keysA), ws->ctr(), nullptr, nullptr);
+  }
+  return cuda_status();
+}
+
+int32_t rs_project(rs_workspace* ws, const rs_scene* scene, const int32_t* active_idx, int64_t m,
+                   const rs_camera* cam, const rs_options* opts, void* stream) {
+  return project_impl(ws, scene, active_idx, m, cam, opts, nullptr, nullptr, stream);
+}
+
+int32_t rs_project_full(rs_workspace* ws, const rs_scene* scene, const int32_t* active_idx, int64_t m,
+                        const rs_camera* cam, const rs_options* opts, float* out_proj, int32_t* out_bbox,
+                        void* stream) {
+  if (!out_proj || !out_bbox) return RS_EINVAL;
+  return project_impl(ws, scene, active_idx, m, cam, opts, out_proj, out_bbox, stream);
+}
+
+int32_t rs_bin(rs_workspace* ws, void* stream) {
+  if (!ws || ws->W <= 0) return RS_EINVAL;
+  cudaStream_t st = S(stream);
+  const uint32_t n = ws->n_items;
+  if (n > 0) {
+    const uint32_t *keys_res, *items_sorted;
+    run_sort<uint32_t>(ws, ws->at<uint32_t>(ws->L.keysA), ws->at<uint32_t>(ws->L.keysA),
+                       ws->at<uint32_t>(ws->L.keysB), nullptr, ws->at<uint32_t>(ws->L.valsA),
+                       ws->at<uint32_t>(ws->L.valsB), nullptr, n, n, 4, 0, 0, false, st, &keys_res, &items_sorted);
+    emit_kernel<<<(n + 255) / 256, 256, 0, st>>>(items_sorted, ws->at<Rec>(ws->L.recs), ws->ctr(), ws->TW,
+                                                 (uint32_t)ws->pair_cap, ws->at<uint16_t>(ws->L.ptileA),
+                                                 ws->at<uint32_t>(ws->L.pitemA), ws->at<int32_t>(ws->L.diff),
+                                                 ws->at<unsigned long long>(ws->L.emit_lb));
+    const uint16_t* tiles_res;
+    const uint32_t* pitems;
+    run_sort<uint16_t>(ws, ws->at<uint16_t>(ws->L.ptileA), ws->at<uint16_t>(ws->L.ptileA),
+                       ws->at<uint16_t>(ws->L.ptileB), ws->at<uint32_t>(ws->L.pitemA), ws->at<uint32_t>(ws->L.pitemA),
+                       ws->at<uint32_t>(ws->L.pitemB), &ws->ctr()->n_pairs, 0, (uint32_t)ws->pair_cap,
+                       ws->tile_passes, 4, 4, false, st, &tiles_res, &pitems);
+  }
+  const int nd = (ws->TW + 1) * (ws->TH + 1);
+  ranges_kernel<<<1, 1024, nd * 4, st>>>(ws->at<int32_t>(ws->L.diff), ws->TW, ws->TH, ws->at<uint2>(ws->L.ranges));
+  ws->binned = true;
+  return cuda_status();
+}
+
+static const uint32_t* final_pair_items(const rs_workspace* ws) {
+  // tile sort ping-pong: 1 pass -> B, 2 passes -> A
+  return ws->tile_passes == 1 ? ws->at<uint32_t>(ws->L.pitemB) : ws->at<uint32_t>(ws->L.pitemA);
+}
+
+int32_t rs_blend(rs_workspace* ws, const rs_options* opts, float* out_rgb, float* out_alpha, float* out_depth,
+                 int32_t* out_count, uint32_t* scores, uint32_t flags, void* stream) {
+  if (!ws || !opts || !ws->binned) return RS_EINVAL;
+  const bool color = out_rgb != nullptr;
+  if (color && (!out_alpha || !out_depth || !out_count)) return RS_EINVAL;
+  if (!color && !scores) return RS_EINVAL;
+  const bool stats = (flags & RS_FLAG_COUNT_EVALS) != 0;
+  cudaStream_t st = S(stream);
+  const int T = ws->TW * ws->TH;
+  const uint2* ranges = ws->at<uint2>(ws->L.ranges);
+  const uint32_t* items = final_pair_items(ws);
+  const Rec* recs = ws->at<Rec>(ws->L.recs);
+  Counters* ctr = ws->ctr();
+#define RS_BLEND(C, I, K)                                                                                        \
+  blend_kernel<C, I, K><<<T, kBlendThreads, 0, st>>>(ranges, items, recs, ctr, ws->W, ws->H, ws->TW, *opts, \
+                                                     out_rgb, out_alpha, out_depth, out_count, scores)
+  if (color && scores) {
+    if (stats) RS_BLEND(true, true, true); else RS_BLEND(true, true, false);
+  } else if (color) {
+    if (stats) RS_BLEND(true, false, true); else RS_BLEND(true, false, false);
+  } else {
+    if (stats) RS_BLEND(false, true, true); else RS_BLEND(false, true, false);
+  }
+#undef RS_BLEND
+  return cuda_status();
+}
+
+int32_t rs_render(rs_workspace* ws, const rs_scene* scene, const int32_t* active_idx, int64_t m,
+                  const rs_camera* cam, const rs_options* opts, float* out_rgb, float* out_alpha, float* out_depth,
+                  int32_t* out_count, uint32_t* scores, uint32_t flags, void* stream) {
+  int32_t s = rs_project(ws, scene, active_idx, m, cam, opts, stream);
+  if (s != RS_OK) return s;
+  if ((s = rs_bin(ws, stream)) != RS_OK) return s;
+  return rs_blend(ws, opts, out_rgb, out_alpha, out_depth, out_count, scores, flags, stream);
+}
+
+int32_t rs_read_stats(rs_workspace* ws, rs_stats* out, void* stream) {
+  if (!ws || !out) return RS_EINVAL;
+  Counters c;
+  if (cudaMemcpyAsync(&c, ws->ctr(), sizeof(c), cudaMemcpyDeviceToHost, S(stream)) != cudaSuccess) return RS_ECUDA;
+  if (cudaStreamSynchronize(S(stream)) != cudaSuccess) return RS_ECUDA;
+  out->n_items = c.n_items;
+  out->n_visible = c.n_visible;
+  out->n_pairs = c.n_pairs;
+  out->overflow = c.overflow;
+  out->evals = c.evals;
+  out->composites = c.composites;
+  out->pairs_needed = c.pairs_needed;
+  return RS_OK;
+}
+
+int32_t rs_get_buffers(rs_workspace* ws, rs_buffers* out) {
+  if (!ws || !out) return RS_EINVAL;
+  out->records = ws->at<void>(ws->L.recs);
+  out->items_sorted = ws->at<uint32_t>(ws->L.valsA);  // 4 depth passes end in A
+  out->pair_items = final_pair_items(ws);
+  out->ranges = ws->at<uint32_t>(ws->L.ranges);
+  out->counters = ws->at<uint32_t>(ws->L.ctr);
+  out->tiles_x = ws->TW;
+  out->tiles_y = ws->TH;
+  return RS_OK;
+}
+
+size_t rs_compact_workspace_size(int64_t n) {
+  return align_up(((size_t)std::max<int64_t>(n, 0) / kCompactPerBlock + 2) * 8 + 256);
+}
+
+static int32_t compact_impl(const uint8_t* flags, int64_t n, int32_t* out_idx, uint32_t* out_count, void* scratch,
+                            size_t scratch_bytes, void* stream, bool bits) {
+  if (n < 0 || !out_count || (n > 0 && (!flags || !out_idx)) || n > 0x7fffffffLL) return RS_EINVAL;
+  if (scratch_bytes < rs_compact_workspace_size(n) || !scratch) return RS_ENOMEM_WORKSPACE;
+  cudaStream_t st = S(stream);
+  cudaMemsetAsync(out_count, 0, 4, st);
+  if (n == 0) return cuda_status();
+  const int blocks = (int)((n + kCompactPerBlock - 1) / kCompactPerBlock);
+  cudaMemsetAsync(scratch, 0, (size_t)blocks * 8 + 256, st);
+  uint32_t* ticket = reinterpret_cast<uint32_t*>(scratch);
+  unsigned long long* status = reinterpret_cast<unsigned long long*>(static_cast<unsigned char*>(scratch) + 256);
+  if (bits)
+    compact_kernel<true><<<blocks, kCompactThreads, 0, st>>>(flags, n, out_idx, out_count, status, ticket);
+  else
+    compact_kernel<false><<<blocks, kCompactThreads, 0, st>>>(flags, n, out_idx, out_count, status, ticket);
+  return cuda_status();
+}
+
+int32_t rs_compact(const uint8_t* flags, int64_t n, int32_t* out_idx, uint32_t* out_count, void* scratch,
+                   size_t scratch_bytes, void* stream) {
+  return compact_impl(flags, n, out_idx, out_count, scratch, scratch_bytes, stream, false);
+}
+
+int32_t rs_compact_bits(const uint8_t* bits, int64_t n, int32_t* out_idx, uint32_t* out_count, void* scratch,
+                        size_t scratch_bytes, void* stream) {
+  return compact_impl(bits, n, out_idx, out_count, scratch, scratch_bytes, stream, true);
+}
+
+int32_t rs_check_finite(const rs_scene* scene, uint32_t* out_bad, void* stream) {
+  if (!scene || !out_bad || scene->n < 0 || (scene->n > 0 && !scene->planes) || scene->plane_stride < scene->n)
+    return RS_EINVAL;
+  cudaStream_t st = S(stream);
+  cudaMemsetAsync(out_bad, 0, 4, st);
+  if (scene->n > 0) finite_kernel<<<1184, 256, 0, st>>>(scene->planes, scene->n, scene->plane_stride, out_bad);
+  return cuda_status();
+}
+
+int32_t rs_max_merge(float* dst, const float* src, int64_t n, void* stream) {
+  if (n < 0 || (n > 0 && (!dst || !src))) return RS_EINVAL;
+  if (n > 0)
+    max_merge_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, S(stream)>>>(
+        reinterpret_cast<uint32_t*>(dst), reinterpret_cast<const uint32_t*>(src), n);
+  return cuda_status();
+}
+
+}  // extern "C"

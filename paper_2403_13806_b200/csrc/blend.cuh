@@ -1,0 +1,144 @@
+// blend.cuh -- per-tile front-to-back compositing (replaces render.py:246-283)
+// and its importance-scoring variant (render.py:267, :273-275 + pruning.py:86-92).
+//
+// One 256-thread CTA per 16x16 tile, one thread per pixel; warp w owns the 8x4
+// sub-rectangle (w%2, w/2) so that the per-Gaussian bbox test (oracles.py:36-38)
+// is usually warp-uniform. The tile's (depth, index)-ordered list is consumed
+// in batches of 256 records: each thread stages one 64-byte record into shared
+// memory with four 128-bit loads, then every warp walks the batch reading the
+// records as shared-memory broadcasts.
+//
+// Per pixel and Gaussian (Tier-A contract, bit-identical to oracle/cpu_ref.cpp):
+//   p2    = fma(na*dx, dx, fma(nb*dy, dx, (nc*dy)*dy))     (= -0.5*log2(e)*q)
+//   alpha = min(o * 2^p2, alpha_max)
+//   if alpha >= alpha_cut and tau >= tau_stop:   (render.py:261)
+//       w = alpha*tau; rgb += c*w; depth += z*w; count++; tau *= 1 - alpha
+// Pixels leave the loop once tau < tau_stop (nothing can composite after
+// that, render.py:261); the CTA stops when all 256 have (__syncthreads_and).
+// p2 < cut2 (a conservative per-Gaussian bound) proves alpha < alpha_cut
+// without evaluating 2^p2 -- the skip changes no result, only work.
+//
+// Importance: w is reduced across the warp with one REDUX.MAX on its fp32 bit
+// pattern (w >= 0, so the unsigned order is the float order), lane 0 folds it
+// into a per-batch shared slot, and each slot reaches the global score vector
+// with one atomicMax per (tile, Gaussian) -- max-merge is order independent
+// (render.py:71-76), so the result is deterministic.
+#pragma once
+#include "rs_common.cuh"
+#include "rs_math.cuh"
+
+namespace rs {
+
+template <bool COLOR, bool CONTRIB, bool STATS>
+__global__ void __launch_bounds__(kBlendThreads) blend_kernel(
+    const uint2* __restrict__ ranges, const uint32_t* __restrict__ pair_items, const Rec* __restrict__ recs,
+    Counters* __restrict__ ctr, int W, int H, int TW, rs_options o, float* __restrict__ out_rgb,
+    float* __restrict__ out_alpha, float* __restrict__ out_depth, int32_t* __restrict__ out_count,
+    uint32_t* __restrict__ scores) {
+  __shared__ float4 s_a[kBlendThreads];
+  __shared__ float4 s_b[kBlendThreads];
+  __shared__ float4 s_c[COLOR ? kBlendThreads : 1];
+  __shared__ int4 s_d[kBlendThreads];
+  __shared__ uint32_t s_w[CONTRIB ? kBlendThreads : 1];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tile = blockIdx.x;
+  const int tx = tile % TW, ty = tile / TW;
+  const int px = tx * kTile + (warp & 1) * 8 + (lane & 7);
+  const int py = ty * kTile + (warp >> 1) * 4 + (lane >> 3);
+  const bool inside = px < W && py < H;
+  const float xs = __fadd_rn((float)px, 0.5f), ys = __fadd_rn((float)py, 0.5f);
+  if (ctr->overflow) return;  // pair list incomplete: the host re-runs with a larger capacity
+  const uint2 rg = ranges[tile];
+  const uint32_t npairs = ctr->n_pairs;
+  const uint32_t end = rg.y < npairs ? rg.y : npairs;  // memory safety on overflow
+
+  float tau = 1.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f, cd = 0.0f;
+  int cnt = 0;
+  unsigned long long evals = 0;
+  bool done = !inside || !(1.0f >= o.tau_stop);
+
+  for (uint32_t base = rg.x; base < end; base += kBlendThreads) {
+    if (__syncthreads_and(done)) break;
+    const uint32_t idx = base + tid;
+    uint32_t gid = 0;
+    if (idx < end) {
+      const Rec* R = recs + __ldg(pair_items + idx);
+      s_a[tid] = __ldg(&R->a);
+      s_b[tid] = __ldg(&R->b);
+      const float4 c = __ldg(&R->c);
+      if (COLOR) s_c[tid] = c;
+      gid = (uint32_t)__float_as_int(c.w);
+      s_d[tid] = __ldg(&R->d);
+    }
+    if (CONTRIB) s_w[tid] = 0u;
+    __syncthreads();
+    const int n = (int)min((uint32_t)kBlendThreads, end - base);
+    if (!__all_sync(0xffffffffu, done)) {
+      for (int j = 0; j < n; ++j) {
+        const int4 bb = s_d[j];
+        const bool in = !done && px >= bb.x && px < bb.y && py >= bb.z && py < bb.w;
+        if (!__any_sync(0xffffffffu, in)) continue;
+        float w = 0.0f;
+        if (in) {
+          if (STATS) ++evals;
+          const float4 ga = s_a[j];
+          const float4 gb = s_b[j];
+          const float dx = __fsub_rn(xs, ga.x), dy = __fsub_rn(ys, ga.y);
+          const float p2 =
+              __fmaf_rn(__fmul_rn(ga.z, dx), dx, __fmaf_rn(__fmul_rn(ga.w, dy), dx, __fmul_rn(__fmul_rn(gb.x, dy), dy)));
+          if (p2 >= gb.z) {
+            const float e = (p2 >= -126.0f && p2 <= 127.0f) ? exp2_core(p2) : exp2_contract(p2);
+            const float alpha = fminf(__fmul_rn(gb.y, e), o.alpha_max);
+            if (alpha >= o.alpha_cut) {
+              w = __fmul_rn(alpha, tau);
+              if (COLOR) {
+                const float4 gc = s_c[j];
+                cr = __fmaf_rn(gc.x, w, cr);
+                cg = __fmaf_rn(gc.y, w, cg);
+                cb = __fmaf_rn(gc.z, w, cb);
+                cd = __fmaf_rn(gb.w, w, cd);
+              }
+              ++cnt;
+              tau = __fmul_rn(tau, __fsub_rn(1.0f, alpha));
+              done = tau < o.tau_stop;
+            }
+          }
+        }
+        if (CONTRIB) {
+          const uint32_t wm = __reduce_max_sync(0xffffffffu, __float_as_uint(w));
+          if (lane == 0 && wm) atomicMax(&s_w[j], wm);
+        }
+      }
+    }
+    __syncthreads();
+    if (CONTRIB && idx < end) {
+      const uint32_t v = s_w[tid];
+      if (v) atomicMax(scores + gid, v);
+    }
+  }
+
+  if (inside && COLOR) {
+    const size_t p = (size_t)py * W + px;
+    out_rgb[3 * p] = cr;
+    out_rgb[3 * p + 1] = cg;
+    out_rgb[3 * p + 2] = cb;
+    out_alpha[p] = __fsub_rn(1.0f, tau);
+    out_depth[p] = cd;
+    out_count[p] = cnt;
+  }
+  if (STATS) {
+    unsigned long long c = (unsigned long long)cnt;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      evals += __shfl_down_sync(0xffffffffu, evals, off);
+      c += __shfl_down_sync(0xffffffffu, c, off);
+    }
+    if (lane == 0) {
+      atomicAdd(&ctr->evals, evals);
+      atomicAdd(&ctr->composites, c);
+    }
+  }
+}
+
+}  // namespace rs

@@ -1,0 +1,199 @@
+// project.cuh -- per-Gaussian projection (replaces render.py:95-158).
+//
+// One thread per item. Reads the scene's fp32 planes with coalesced 4-byte
+// loads (59 independent loads in flight per thread at SH degree 3), evaluates
+// the Tier-A fp32 contract of oracle/cpu_ref.cpp:project_one() in the same
+// operation order (compiled with -fmad=false; explicit __fmaf_rn only where
+// the contract fuses), and writes
+//   * a 64-byte Rec for valid items (invalid items write nothing else), and
+//   * the 32-bit depth key (kInvalidKey for culled items) that the depth sort
+//     consumes; culled items sort last.
+// n_visible is counted with one atomic per warp.
+#pragma once
+#include "rs_common.cuh"
+#include "rs_math.cuh"
+
+namespace rs {
+
+__device__ __forceinline__ int floor_clip(float v, int hi) {
+  if (v != v) return 0;
+  const float f = floorf(v);
+  if (f <= 0.0f) return 0;
+  if (f >= (float)hi) return hi;
+  return (int)f;
+}
+
+__device__ __forceinline__ int ceil1_clip(float v, int hi) {
+  if (v != v) return 0;
+  const float f = ceilf(v);
+  if (f <= -1.0f) return 0;
+  if (f >= (float)hi) return hi;
+  const int r = (int)f + 1;
+  return r > hi ? hi : r;
+}
+
+// FULL additionally writes, for every item (culled ones included), the
+// ProjectedGaussian fields of render.py:49-59 as 16 floats
+// {mx, my, a, b, c, ia, ib, ic, radius, depth, r, g, b, opacity, valid, 0}
+// and the int4 bbox: the per-primitive API project_gaussian/project_scene.
+template <bool FULL>
+__global__ void __launch_bounds__(128) project_kernel(const float* __restrict__ planes, int64_t stride, int deg,
+                                                      const int32_t* __restrict__ active_idx, uint32_t n_items,
+                                                      rs_camera cam, rs_options o, Rec* __restrict__ recs,
+                                                      uint32_t* __restrict__ keys, Counters* __restrict__ ctr,
+                                                      float* __restrict__ full, int4* __restrict__ full_bbox) {
+  const uint32_t item = blockIdx.x * blockDim.x + threadIdx.x;
+  if (item == 0) ctr->n_items = n_items;
+  bool valid = false;
+  if (item < n_items) {
+    const int64_t i = active_idx ? (int64_t)__ldg(active_idx + item) : (int64_t)item;
+    const float* P = planes + i;
+    const float px = __ldg(P), py = __ldg(P + stride), pz = __ldg(P + 2 * stride);
+    // t = R p + T (render.py:100)
+    float t[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      t[k] = __fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(cam.R[3 * k], px), __fmul_rn(cam.R[3 * k + 1], py)),
+                                 __fmul_rn(cam.R[3 * k + 2], pz)),
+                       cam.t[k]);
+    const bool valid0 = t[2] > o.near_limit;
+    const float tz = valid0 ? t[2] : 1.0f;
+    const float mx = __fadd_rn(__fdiv_rn(__fmul_rn(cam.fx, t[0]), tz), cam.cx);  // render.py:104-105
+    const float my = __fadd_rn(__fdiv_rn(__fmul_rn(cam.fy, t[1]), tz), cam.cy);
+    const float depth = __fadd_rn(t[2], 0.0f);
+    // quaternion -> rotation (core.py:111-139)
+    float qw = __ldg(P + 7 * stride), qx = __ldg(P + 8 * stride), qy = __ldg(P + 9 * stride),
+          qz = __ldg(P + 10 * stride);
+    const float qn = __fsqrt_rn(
+        __fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(qw, qw), __fmul_rn(qx, qx)), __fmul_rn(qy, qy)), __fmul_rn(qz, qz)));
+    qw = __fdiv_rn(qw, qn); qx = __fdiv_rn(qx, qn); qy = __fdiv_rn(qy, qn); qz = __fdiv_rn(qz, qn);
+    float Rq[9];
+    Rq[0] = __fsub_rn(1.0f, __fmul_rn(2.0f, __fadd_rn(__fmul_rn(qy, qy), __fmul_rn(qz, qz))));
+    Rq[1] = __fmul_rn(2.0f, __fsub_rn(__fmul_rn(qx, qy), __fmul_rn(qw, qz)));
+    Rq[2] = __fmul_rn(2.0f, __fadd_rn(__fmul_rn(qx, qz), __fmul_rn(qw, qy)));
+    Rq[3] = __fmul_rn(2.0f, __fadd_rn(__fmul_rn(qx, qy), __fmul_rn(qw, qz)));
+    Rq[4] = __fsub_rn(1.0f, __fmul_rn(2.0f, __fadd_rn(__fmul_rn(qx, qx), __fmul_rn(qz, qz))));
+    Rq[5] = __fmul_rn(2.0f, __fsub_rn(__fmul_rn(qy, qz), __fmul_rn(qw, qx)));
+    Rq[6] = __fmul_rn(2.0f, __fsub_rn(__fmul_rn(qx, qz), __fmul_rn(qw, qy)));
+    Rq[7] = __fmul_rn(2.0f, __fadd_rn(__fmul_rn(qy, qz), __fmul_rn(qw, qx)));
+    Rq[8] = __fsub_rn(1.0f, __fmul_rn(2.0f, __fadd_rn(__fmul_rn(qx, qx), __fmul_rn(qy, qy))));
+    // Sigma = L L^T, L = Rq diag(exp(log_s)) (render.py:108-111)
+    float sc[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) sc[j] = exp_contract(__ldg(P + (4 + j) * stride));
+    float L[9];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) L[3 * r + j] = __fmul_rn(Rq[3 * r + j], sc[j]);
+    float S[9];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+        S[3 * r + k] = __fadd_rn(__fadd_rn(__fmul_rn(L[3 * r], L[3 * k]), __fmul_rn(L[3 * r + 1], L[3 * k + 1])),
+                                 __fmul_rn(L[3 * r + 2], L[3 * k + 2]));
+    // J and A = J R_cam (render.py:114-119)
+    const float tz2 = __fmul_rn(tz, tz);
+    const float j00 = __fdiv_rn(cam.fx, tz), j02 = __fdiv_rn(__fmul_rn(-cam.fx, t[0]), tz2);
+    const float j11 = __fdiv_rn(cam.fy, tz), j12 = __fdiv_rn(__fmul_rn(-cam.fy, t[1]), tz2);
+    float A[6];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      A[k] = __fadd_rn(__fmul_rn(j00, cam.R[k]), __fmul_rn(j02, cam.R[6 + k]));
+      A[3 + k] = __fadd_rn(__fmul_rn(j11, cam.R[3 + k]), __fmul_rn(j12, cam.R[6 + k]));
+    }
+    float MS[6];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+        MS[3 * r + k] = __fadd_rn(__fadd_rn(__fmul_rn(A[3 * r], S[k]), __fmul_rn(A[3 * r + 1], S[3 + k])),
+                                  __fmul_rn(A[3 * r + 2], S[6 + k]));
+    const float c00 = __fadd_rn(__fadd_rn(__fmul_rn(MS[0], A[0]), __fmul_rn(MS[1], A[1])), __fmul_rn(MS[2], A[2]));
+    const float c01 = __fadd_rn(__fadd_rn(__fmul_rn(MS[0], A[3]), __fmul_rn(MS[1], A[4])), __fmul_rn(MS[2], A[5]));
+    const float c11 = __fadd_rn(__fadd_rn(__fmul_rn(MS[3], A[3]), __fmul_rn(MS[4], A[4])), __fmul_rn(MS[5], A[5]));
+    const float a = __fadd_rn(c00, o.lowpass), b = c01, c = __fadd_rn(c11, o.lowpass);  // render.py:121-123
+    const float det = __fsub_rn(__fmul_rn(a, c), __fmul_rn(b, b));                       // render.py:125-128
+    const float ia = __fdiv_rn(c, det), ib = __fdiv_rn(-b, det), ic = __fdiv_rn(a, det);
+    const float amc = __fsub_rn(a, c);  // render.py:130-131
+    const float disc = __fadd_rn(__fmul_rn(0.25f, __fmul_rn(amc, amc)), __fmul_rn(b, b));
+    const float lam = __fadd_rn(__fmul_rn(0.5f, __fadd_rn(a, c)), __fsqrt_rn(disc > 0.0f ? disc : 0.0f));
+    const float radius = __fmul_rn(o.sigma_bound, __fsqrt_rn(lam > 0.0f ? lam : 0.0f));
+    const int x0 = floor_clip(__fsub_rn(mx, radius), cam.width);  // render.py:133-137
+    const int x1 = ceil1_clip(__fadd_rn(mx, radius), cam.width);
+    const int y0 = floor_clip(__fsub_rn(my, radius), cam.height);
+    const int y1 = ceil1_clip(__fadd_rn(my, radius), cam.height);
+    valid = valid0 && x1 > x0 && y1 > y0;
+    if (valid || FULL) {
+      // view-direction SH colour (render.py:139-149, core.py:207-239)
+      const float vx = __fsub_rn(px, cam.center[0]), vy = __fsub_rn(py, cam.center[1]),
+                  vz = __fsub_rn(pz, cam.center[2]);
+      float vn = __fsqrt_rn(__fadd_rn(__fadd_rn(__fmul_rn(vx, vx), __fmul_rn(vy, vy)), __fmul_rn(vz, vz)));
+      if (!(vn > 0.0f)) vn = 1.0f;
+      const float x = __fdiv_rn(vx, vn), y = __fdiv_rn(vy, vn), z = __fdiv_rn(vz, vn);
+      float Y[16];
+      Y[0] = (float)0.28209479177387814;
+      const float C1 = (float)0.4886025119029199;
+      Y[1] = __fmul_rn(-C1, y); Y[2] = __fmul_rn(C1, z); Y[3] = __fmul_rn(-C1, x);
+      const float xx = __fmul_rn(x, x), yy = __fmul_rn(y, y), zz = __fmul_rn(z, z);
+      const float xy = __fmul_rn(x, y), yz = __fmul_rn(y, z), xz = __fmul_rn(x, z);
+      Y[4] = __fmul_rn((float)1.0925484305920792, xy);
+      Y[5] = __fmul_rn((float)-1.0925484305920792, yz);
+      Y[6] = __fmul_rn((float)0.31539156525252005, __fsub_rn(__fsub_rn(__fmul_rn(2.0f, zz), xx), yy));
+      Y[7] = __fmul_rn((float)-1.0925484305920792, xz);
+      Y[8] = __fmul_rn((float)0.5462742152960396, __fsub_rn(xx, yy));
+      Y[9] = __fmul_rn(__fmul_rn((float)-0.5900435899266435, y), __fsub_rn(__fmul_rn(3.0f, xx), yy));
+      Y[10] = __fmul_rn(__fmul_rn((float)2.890611442640554, xy), z);
+      Y[11] = __fmul_rn(__fmul_rn((float)-0.4570457994644658, y), __fsub_rn(__fsub_rn(__fmul_rn(4.0f, zz), xx), yy));
+      Y[12] = __fmul_rn(__fmul_rn((float)0.3731763325901154, z),
+                        __fsub_rn(__fsub_rn(__fmul_rn(2.0f, zz), __fmul_rn(3.0f, xx)), __fmul_rn(3.0f, yy)));
+      Y[13] = __fmul_rn(__fmul_rn((float)-0.4570457994644658, x), __fsub_rn(__fsub_rn(__fmul_rn(4.0f, zz), xx), yy));
+      Y[14] = __fmul_rn(__fmul_rn((float)1.445305721320277, z), __fsub_rn(xx, yy));
+      Y[15] = __fmul_rn(__fmul_rn((float)-0.5900435899266435, x), __fsub_rn(xx, __fmul_rn(3.0f, yy)));
+      const int nb = deg == 0 ? 1 : deg == 1 ? 4 : deg == 2 ? 9 : 16;
+      float col[3];
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch) {
+        const float* shc = P + (int64_t)(11 + 16 * ch) * stride;
+        float acc = __fmul_rn(__ldg(shc), Y[0]);
+#pragma unroll
+        for (int bnd = 1; bnd < 16; ++bnd)
+          if (bnd < nb) acc = __fadd_rn(acc, __fmul_rn(__ldg(shc + bnd * stride), Y[bnd]));
+        const float pre = __fadd_rn(0.5f, acc);
+        col[ch] = pre < 0.0f ? 0.0f : (pre > 1.0f ? 1.0f : pre);
+      }
+      // opacity = sigmoid(logit) (core.py:419-421)
+      const float lg = __ldg(P + 3 * stride);
+      float op;
+      if (lg >= 0.0f) {
+        op = __fdiv_rn(1.0f, __fadd_rn(1.0f, exp_contract(-lg)));
+      } else {
+        const float e = exp_contract(lg);
+        op = __fdiv_rn(e, __fadd_rn(1.0f, e));
+      }
+      const float K = fbits(0xbf38aa3bu);  // -0.5*log2(e)
+      // conservative skip threshold: p2 < cut2 => alpha < alpha_cut
+      const float cut2 = o.alpha_cut > 0.0f ? __fsub_rn(log2f(o.alpha_cut / op), 1e-3f) : -INFINITY;
+      Rec rec;
+      rec.a = make_float4(mx, my, __fmul_rn(K, ia), __fmul_rn(__fmul_rn(2.0f, K), ib));
+      rec.b = make_float4(__fmul_rn(K, ic), op, cut2, depth);
+      rec.c = make_float4(col[0], col[1], col[2], __int_as_float((int)i));
+      rec.d = make_int4(x0, x1, y0, y1);
+      if (valid) recs[item] = rec;
+      if (FULL) {
+        float4* f = reinterpret_cast<float4*>(full + 16 * (size_t)item);
+        f[0] = make_float4(mx, my, a, b);
+        f[1] = make_float4(c, ia, ib, ic);
+        f[2] = make_float4(radius, depth, col[0], col[1]);
+        f[3] = make_float4(col[2], op, valid ? 1.0f : 0.0f, 0.0f);
+        full_bbox[item] = rec.d;
+      }
+    }
+    keys[item] = valid ? depth_key(depth) : kInvalidKey;
+  }
+  const unsigned vb = __ballot_sync(0xffffffffu, valid);
+  if ((threadIdx.x & 31) == 0 && vb) atomicAdd(&ctr->n_visible, (uint32_t)__popc(vb));
+}
+
+}  // namespace rs

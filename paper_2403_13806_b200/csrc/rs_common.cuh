@@ -1,0 +1,38 @@
+// rs_common.cuh -- shared device types of the render-and-prune path.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "../../include/radsplat.h"
+
+namespace rs {
+
+constexpr int kTile = 16;          // 16x16 pixel tiles, one CTA of 256 threads each
+constexpr int kBlendThreads = 256;
+constexpr uint32_t kInvalidKey = 0xffffffffu;
+constexpr int kPlanes = 59;
+
+// Projected Gaussian, 64 B = 4 x 16 B so a batch is staged with four
+// 128-bit loads per thread and read back from shared memory as broadcasts.
+//   a = {mean x, mean y, na, nb}   na,nb,nc = -0.5*log2(e) * (ia, 2*ib, ic)
+//   b = {nc, opacity, cut2, depth} cut2: log2 power below which alpha < alpha_cut
+//   c = {r, g, b, gid bits}        gid = scene index (for importance scatter)
+//   d = {x0, x1, y0, y1}           half-open pixel bbox (render.py:133-137)
+struct __align__(16) Rec {
+  float4 a, b, c;
+  int4 d;
+};
+static_assert(sizeof(Rec) == 64, "record must be 64 B");
+
+// Device-side counters, mirrors rs_stats (first four words) + sort bookkeeping.
+struct Counters {
+  uint32_t n_items, n_visible, n_pairs, overflow;  // n_pairs = min(P, pair capacity)
+  unsigned long long evals, composites;
+  unsigned long long pairs_needed;                 // true P (sizing hint after overflow)
+  uint32_t tickets[16];  // onesweep chunk tickets, one per pass
+  uint32_t emit_ctr;     // decoupled look-back ticket of the pair emitter
+  uint32_t pad[5];
+};
+static_assert(sizeof(Counters) == 128, "Counters is 128 B");
+
+}  // namespace rs

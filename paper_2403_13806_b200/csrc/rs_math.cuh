@@ -1,0 +1,84 @@
+// rs_math.cuh -- fp32 arithmetic of the parity contract, device side.
+//
+// Every function here is the device twin of the same-named function in
+// oracle/cpu_ref.cpp and must stay operation-for-operation identical: only
+// IEEE-rounded add/mul/div/sqrt and explicit fused multiply-adds, so the GPU
+// result equals the CPU oracle bit for bit. The library is compiled with
+// -fmad=false so the compiler cannot contract a*b+c behind our back; every
+// intended fusion is an explicit __fmaf_rn.
+#pragma once
+#include <cstdint>
+
+namespace rs {
+
+__device__ __forceinline__ float fbits(uint32_t u) { return __uint_as_float(u); }
+
+constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
+
+__device__ __forceinline__ float pow2i(int n) { return __int_as_float((n + 127) << 23); }
+
+__device__ __forceinline__ float scale2(float p, int n) {
+  if (n >= -126 && n <= 127) return __fmul_rn(p, pow2i(n));
+  const int h = n / 2;
+  return __fmul_rn(__fmul_rn(p, pow2i(h)), pow2i(n - h));
+}
+
+__device__ __forceinline__ float exp2_poly(float r) {
+  float p = fbits(0x3920e999u);
+  p = __fmaf_rn(p, r, fbits(0x3aafa2b5u));
+  p = __fmaf_rn(p, r, fbits(0x3c1d96deu));
+  p = __fmaf_rn(p, r, fbits(0x3d63576au));
+  p = __fmaf_rn(p, r, fbits(0x3e75fdedu));
+  p = __fmaf_rn(p, r, fbits(0x3f317218u));
+  p = __fmaf_rn(p, r, 1.0f);
+  return p;
+}
+
+// 2^x (oracle: exp2_contract)
+__device__ __forceinline__ float exp2_contract(float x) {
+  if (x != x) return x;
+  if (x >= 128.0f) return __int_as_float(0x7f800000);
+  if (x < -150.0f) return 0.0f;
+  const float t = __fadd_rn(x, kMagic);
+  const float n = __fsub_rn(t, kMagic);
+  const float r = __fsub_rn(x, n);
+  return scale2(exp2_poly(r), (int)n);
+}
+
+// Hot-loop form, valid (and identical to exp2_contract) for x in [-126, 127]:
+// the integer part is read straight out of t's mantissa, 2^n built with one
+// shift+add, no conversion-pipe instructions.
+__device__ __forceinline__ float exp2_core(float x) {
+  const float t = __fadd_rn(x, kMagic);
+  const float n = __fsub_rn(t, kMagic);
+  const float r = __fsub_rn(x, n);
+  const float s = __int_as_float((__float_as_int(t) << 23) + 0x3f800000);
+  return __fmul_rn(exp2_poly(r), s);
+}
+
+// e^x (oracle: exp_contract)
+__device__ __forceinline__ float exp_contract(float x) {
+  if (x != x) return x;
+  if (x >= 89.0f) return __int_as_float(0x7f800000);
+  if (x < -104.0f) return 0.0f;
+  const float t = __fmaf_rn(x, fbits(0x3fb8aa3bu), kMagic);
+  const float n = __fsub_rn(t, kMagic);
+  float r = __fmaf_rn(n, -fbits(0x3f317200u), x);
+  r = __fmaf_rn(n, -fbits(0x35bfbe8eu), r);
+  float p = fbits(0x3ab55cb8u);
+  p = __fmaf_rn(p, r, fbits(0x3c09368du));
+  p = __fmaf_rn(p, r, fbits(0x3d2aac4du));
+  p = __fmaf_rn(p, r, fbits(0x3e2aaa05u));
+  p = __fmaf_rn(p, r, fbits(0x3efffffdu));
+  p = __fmaf_rn(p, r, 1.0f);
+  p = __fmaf_rn(p, r, 1.0f);
+  return scale2(p, (int)n);
+}
+
+// order-preserving 32-bit key of an fp32 depth (-0 folded into +0)
+__device__ __forceinline__ uint32_t depth_key(float d) {
+  const uint32_t u = __float_as_uint(__fadd_rn(d, 0.0f));
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+}  // namespace rs

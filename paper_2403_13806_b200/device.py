@@ -1,0 +1,257 @@
+"""Device residency: scenes in HBM, workspaces, and the frame launcher.
+
+* ``DeviceScene`` -- the scene as 59 fp32 planes of N floats in HBM (the
+  layout ``rs_scene`` documents). Reference scenes are immutable and carry a
+  ``generation`` tag (core.py:467-485), so an uploaded copy is cached per
+  (object, generation) and reused by every later call on the same scene.
+* ``Renderer`` -- one per device: owns the workspace (grown on demand; a pair
+  overflow re-runs the frame with the capacity the device reported), the
+  stream, and launches ``rs_render`` / ``rs_project_full`` / ``rs_compact``.
+
+Everything here calls the CUDA library; nothing computes on the CPU.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import weakref
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .core import InvalidParameterError, InvalidSceneError
+
+PLANES = 59
+
+
+def pack_planes(scene) -> np.ndarray:
+    """(59, N) float32 plane-major copy of a scene-like object."""
+    pos = np.asarray(scene.positions)
+    n = pos.shape[0]
+    out = np.empty((PLANES, n), np.float32)
+    out[0:3] = pos.reshape(n, 3).T
+    out[3] = np.asarray(scene.opacity_logits).reshape(n)
+    out[4:7] = np.asarray(scene.log_scales).reshape(n, 3).T
+    out[7:11] = np.asarray(scene.quaternions).reshape(n, 4).T
+    out[11:59] = np.asarray(scene.sh).reshape(n, 48).T
+    return out
+
+
+class DeviceScene:
+    """A scene resident in HBM (fp32 planes) plus its ``rs_scene`` descriptor."""
+
+    def __init__(self, scene, device: torch.device | None = None, check_finite: bool = True):
+        lib = N.load()
+        self.device = torch.device(device or torch.device("cuda", torch.cuda.current_device()))
+        host = torch.from_numpy(pack_planes(scene))
+        self.n = int(host.shape[1])
+        self.sh_degree = int(scene.active_sh_degree)
+        if not 0 <= self.sh_degree <= 3:
+            raise InvalidParameterError("active SH degree must be in 0..3")
+        self.generation = getattr(scene, "generation", None)
+        with torch.cuda.device(self.device):
+            self.planes = (host.pin_memory().to(self.device, non_blocking=True) if self.n
+                           else torch.zeros((PLANES, 1), dtype=torch.float32, device=self.device))
+        self.struct = N.RsScene(self.planes.data_ptr(), self.n, max(self.n, 1), self.sh_degree, 0)
+        if check_finite and self.n:
+            with torch.cuda.device(self.device):
+                bad = torch.zeros(1, dtype=torch.int32, device=self.device)
+                N.check(lib.rs_check_finite(C.byref(self.struct), bad.data_ptr(),
+                                            torch.cuda.current_stream(self.device).cuda_stream), "check_finite")
+                if int(bad.item()) != 0:
+                    raise InvalidSceneError("scene contains non-finite parameters")
+
+    def __len__(self):
+        return self.n
+
+
+_scene_cache: dict = {}
+
+
+def device_scene(scene, device: torch.device | None = None) -> DeviceScene:
+    """Upload once per (scene object, generation, device); later calls reuse it."""
+    if isinstance(scene, DeviceScene):
+        return scene
+    dev = torch.device(device or torch.device("cuda", torch.cuda.current_device()))
+    key = (id(scene), dev)
+    hit = _scene_cache.get(key)
+    gen = getattr(scene, "generation", None)
+    if hit is not None and hit.generation == gen and hit.n == len(scene.positions):
+        return hit
+    ds = DeviceScene(scene, dev)
+    _scene_cache[key] = ds
+    try:
+        weakref.finalize(scene, _scene_cache.pop, key, None)
+    except TypeError:  # not weak-referenceable: keep only the latest such scene
+        pass
+    return ds
+
+
+def camera_struct(cam) -> N.RsCamera:
+    """fp32 camera packet; the centre -R^T t is formed in fp64, then rounded."""
+    R = np.asarray(cam.rotation, np.float64).reshape(3, 3)
+    t = np.asarray(cam.translation, np.float64).reshape(3)
+    c = -R.T @ t
+    s = N.RsCamera()
+    s.width, s.height = int(cam.width), int(cam.height)
+    s.fx, s.fy, s.cx, s.cy = (float(np.float32(v)) for v in (cam.fx, cam.fy, cam.cx, cam.cy))
+    s.R[:] = [float(v) for v in R.ravel().astype(np.float32)]
+    s.t[:] = [float(v) for v in t.astype(np.float32)]
+    s.center[:] = [float(v) for v in c.astype(np.float32)]
+    return s
+
+
+def options_struct(opts) -> N.RsOptions:
+    return N.RsOptions(*(float(np.float32(getattr(opts, k))) for k in
+                         ("alpha_max", "alpha_cut", "tau_stop", "near_limit", "lowpass", "sigma_bound")))
+
+
+class Renderer:
+    """Frame launcher bound to one CUDA device."""
+
+    def __init__(self, device: torch.device | None = None):
+        self.lib = N.load()
+        self.device = torch.device(device or torch.device("cuda", torch.cuda.current_device()))
+        self.buf = None
+        self.handle = C.c_void_p()
+        self.caps = (0, 0, 0, 0)
+
+    # -- workspace ---------------------------------------------------------
+    def ensure(self, n: int, pairs: int, width: int, height: int) -> None:
+        cn, cp, cw, ch = self.caps
+        if n <= cn and pairs <= cp and width <= cw and height <= ch:
+            return
+        caps = (max(n, cn, 1), max(pairs, cp, 1 << 16), max(width, cw), max(height, ch))
+        size = self.lib.rs_workspace_size(*caps)
+        if size == 0:
+            raise InvalidParameterError(f"unsupported workspace shape {caps}")
+        self.close()
+        with torch.cuda.device(self.device):
+            self.buf = torch.empty(size, dtype=torch.uint8, device=self.device)
+        N.check(self.lib.rs_workspace_create(self.buf.data_ptr(), size, *caps, C.byref(self.handle)),
+                "workspace_create")
+        self.caps = caps
+
+    def close(self) -> None:
+        if self.handle:
+            torch.cuda.synchronize(self.device)
+            self.lib.rs_workspace_destroy(self.handle)
+            self.handle = C.c_void_p()
+        self.buf = None
+        self.caps = (0, 0, 0, 0)
+
+    def __del__(self):
+        try:
+            if self.handle:
+                self.lib.rs_workspace_destroy(self.handle)
+        except Exception:
+            pass
+
+    @property
+    def stream(self) -> int:
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def stats(self) -> N.RsStats:
+        st = N.RsStats()
+        N.check(self.lib.rs_read_stats(self.handle, C.byref(st), self.stream), "read_stats")
+        return st
+
+    def buffers(self) -> N.RsBuffers:
+        b = N.RsBuffers()
+        N.check(self.lib.rs_get_buffers(self.handle, C.byref(b)), "get_buffers")
+        return b
+
+    def view(self, ptr: int, count: int, dtype: torch.dtype) -> torch.Tensor:
+        """A tensor view of `count` elements at device pointer `ptr` inside the workspace."""
+        off = int(ptr) - self.buf.data_ptr()
+        size = torch.empty((), dtype=dtype).element_size()
+        assert 0 <= off and off + count * size <= self.buf.numel()
+        return self.buf[off:off + count * size].view(dtype)
+
+    def frame_arrays(self) -> dict:
+        """Binning state of the last frame, copied to host (parity tests)."""
+        st, b = self.stats(), self.buffers()
+        T = b.tiles_x * b.tiles_y
+        return dict(
+            stats=st, tiles_x=b.tiles_x, tiles_y=b.tiles_y,
+            records=self.view(b.records, 16 * st.n_items, torch.float32).view(-1, 16).cpu().numpy(),
+            items_sorted=self.view(b.items_sorted, st.n_items, torch.int32).cpu().numpy().view(np.uint32),
+            pair_items=self.view(b.pair_items, st.n_pairs, torch.int32).cpu().numpy().view(np.uint32),
+            ranges=self.view(b.ranges, 2 * T, torch.int32).cpu().numpy().view(np.uint32).reshape(T, 2))
+
+    # -- frames --------------------------------------------------------------
+    def alloc_outputs(self, cam, color: bool = True) -> dict:
+        H, W = int(cam.height), int(cam.width)
+        if not color:
+            return {}
+        d = self.device
+        return dict(rgb=torch.empty((H, W, 3), dtype=torch.float32, device=d),
+                    alpha=torch.empty((H, W), dtype=torch.float32, device=d),
+                    depth=torch.empty((H, W), dtype=torch.float32, device=d),
+                    count=torch.empty((H, W), dtype=torch.int32, device=d))
+
+    def launch(self, ds: DeviceScene, cam_s: N.RsCamera, opt_s: N.RsOptions, out: dict,
+               scores: torch.Tensor | None = None, active_idx: torch.Tensor | None = None,
+               m: int = 0, flags: int = 0) -> None:
+        """Enqueue one frame (no host synchronization)."""
+        ptr = lambda k: out[k].data_ptr() if k in out else None  # noqa: E731
+        N.check(self.lib.rs_render(
+            self.handle, C.byref(ds.struct), active_idx.data_ptr() if active_idx is not None else None,
+            int(m), C.byref(cam_s), C.byref(opt_s), ptr("rgb"), ptr("alpha"), ptr("depth"), ptr("count"),
+            scores.data_ptr() if scores is not None else None, flags, self.stream), "render")
+
+    def render(self, ds: DeviceScene, cam, opts, *, color: bool = True, scores: torch.Tensor | None = None,
+               active_idx: torch.Tensor | None = None, m: int | None = None, count_evals: bool = False,
+               out: dict | None = None) -> tuple[dict, N.RsStats]:
+        """One frame with overflow handling (reads the counters: synchronizes)."""
+        items = ds.n if active_idx is None else int(m if m is not None else active_idx.numel())
+        W, H = int(cam.width), int(cam.height)
+        self.ensure(items, self.caps[1] or max(4 * items, 1 << 20), W, H)
+        cam_s, opt_s = camera_struct(cam), options_struct(opts)
+        out = out if out is not None else self.alloc_outputs(cam, color)
+        flags = N.RS_FLAG_COUNT_EVALS if count_evals else 0
+        snapshot = scores.clone() if scores is not None else None
+        for _ in range(4):
+            self.launch(ds, cam_s, opt_s, out, scores, active_idx, items, flags)
+            st = self.stats()
+            if not st.overflow:
+                return out, st
+            self.ensure(items, int(st.pairs_needed * 1.15) + 1024, W, H)
+            if snapshot is not None:
+                scores.copy_(snapshot)
+        raise N.PairOverflow("tile pair capacity could not be satisfied")
+
+    def project_full(self, ds: DeviceScene, cam, opts) -> tuple[np.ndarray, np.ndarray]:
+        """ProjectedGaussian fields for every Gaussian (render.py:161-211)."""
+        self.ensure(ds.n, self.caps[1] or (1 << 16), int(cam.width), int(cam.height))
+        n = max(ds.n, 1)
+        full = torch.empty((n, 16), dtype=torch.float32, device=self.device)
+        bbox = torch.empty((n, 4), dtype=torch.int32, device=self.device)
+        N.check(self.lib.rs_project_full(self.handle, C.byref(ds.struct), None, 0, C.byref(camera_struct(cam)),
+                                         C.byref(options_struct(opts)), full.data_ptr(), bbox.data_ptr(),
+                                         self.stream), "project_full")
+        return full[:ds.n].cpu().numpy(), bbox[:ds.n].cpu().numpy()
+
+    def compact(self, flags: torch.Tensor, bits: bool = False, n: int | None = None) -> torch.Tensor:
+        """Ascending indices of non-zero flags (or set bits), on device."""
+        n = int(flags.numel() if n is None else n)
+        nbytes = self.lib.rs_compact_workspace_size(n)
+        scratch = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
+        idx = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
+        cnt = torch.empty(1, dtype=torch.int32, device=self.device)
+        fn = self.lib.rs_compact_bits if bits else self.lib.rs_compact
+        N.check(fn(flags.data_ptr() if n else None, n, idx.data_ptr(), cnt.data_ptr(), scratch.data_ptr(),
+                   scratch.numel(), self.stream), "compact")
+        return idx[:int(cnt.item())]
+
+
+_renderers: dict = {}
+
+
+def renderer(device: torch.device | None = None) -> Renderer:
+    dev = torch.device(device or torch.device("cuda", torch.cuda.current_device()))
+    r = _renderers.get(dev)
+    if r is None:
+        r = _renderers[dev] = Renderer(dev)
+    return r

@@ -1,0 +1,81 @@
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+GOLDEN = ROOT / "tests" / "golden"
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and the built library")
+
+
+def pytest_collection_modifyitems(config, items):
+    try:
+        import torch
+        has_cuda = torch.cuda.is_available()
+    except Exception:
+        has_cuda = False
+    if has_cuda:
+        return
+    skip = pytest.mark.skip(reason="no CUDA device in this container")
+    for it in items:
+        if "gpu" in it.keywords:
+            it.add_marker(skip)
+
+
+_cache = {}
+
+
+def golden(name: str):
+    if name not in _cache:
+        _cache[name] = dict(np.load(GOLDEN / f"{name}.npz"))
+    return _cache[name]
+
+
+def load_case(d, p):
+    """(scene, camera, RasterizeOptions-like values) from a golden npz prefix."""
+    from paper_2403_13806_b200.core import GaussianScene, PinholeCamera
+    scene = GaussianScene(positions=d[p + "pos"], opacity_logits=d[p + "logit"], sh=d[p + "sh"],
+                          log_scales=d[p + "ls"], quaternions=d[p + "quat"], active_sh_degree=int(d[p + "deg"]))
+    cam = load_cam(d, p)
+    opts = d.get(p + "opts")
+    return scene, cam, opts
+
+
+def load_cam(d, p):
+    from paper_2403_13806_b200.core import PinholeCamera
+    W, H = (int(v) for v in d[p + "wh"])
+    fx, fy, cx, cy = (float(v) for v in d[p + "intr"])
+    return PinholeCamera(width=W, height=H, fx=fx, fy=fy, cx=cx, cy=cy, rotation=d[p + "R"],
+                         translation=d[p + "t"])
+
+
+def options_from(vals):
+    from types import SimpleNamespace
+    if vals is None:
+        vals = [0.99, 1.0 / 255.0, 1e-4, 0.01, 0.3, 3.0]
+    keys = ("alpha_max", "alpha_cut", "tau_stop", "near_limit", "lowpass", "sigma_bound")
+    return SimpleNamespace(**dict(zip(keys, (float(v) for v in vals))))
+
+
+def render_cases():
+    """(name, scene, cam, opts) for every golden render case."""
+    out = []
+    for f in ("suite50", "accept50"):
+        d = golden(f)
+        for c in range(int(d["n_cases"])):
+            s, cam, o = load_case(d, f"c{c}_")
+            out.append((f"{f}-{c}", s, cam, options_from(o), d, f"c{c}_"))
+    d = golden("known")
+    for name in ("single", "twolayer", "tie", "iso", "lowpass", "occluder", "occluder1", "behind",
+                 "offscreen", "ragged"):
+        s, cam, o = load_case(d, name + "_")
+        out.append((name, s, cam, options_from(o), d, name + "_"))
+    d = golden("config0")
+    s, cam, o = load_case(d, "cfg0_")
+    out.append(("config0", s, cam, options_from(o), d, "cfg0_"))
+    return out
