@@ -1,0 +1,404 @@
+#!/usr/bin/env python
+"""Benchmark: RadSplat render FPS at 1256x828 (BASELINE configs[1]) and
+importance-score views/s (configs[2]) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload render|score]
+                    [--impl b200|reference] [--no-cpu-baseline]
+
+One JSON line on rank 0 (contract in the task brief):
+* render (default): a step = one 500k-Gaussian 1256x828 frame per rank along
+  the 1000-frame orbit (rank r renders frame (s*N + r) mod 1000): weak scaling,
+  value = frames/s over all ranks. Per-stage device times (preprocess / sort /
+  blend) come from CUDA events on the launching stream around the three C-ABI
+  stages; L2 is flushed (256 MB memset) between timed steps, outside the events.
+* score: a step = one full scoring pass of configs[2] (3M Gaussians, 200
+  Fibonacci views, 1256x828): views sharded contiguously across ranks, one
+  NCCL MAX all-reduce; strong scaling, value = views/s.
+* --impl reference: the CPU oracle port (oracle/cpu_ref.cpp, the restated
+  reference algorithm; the reference itself is pure NumPy and cannot travel)
+  on all host cores, same metric and config, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC_RENDER = "render FPS at 1256x828, 500k Gaussians (configs[1] orbit), 1 frame per GPU per step"
+METRIC_SCORE = "importance-score views/s, 3M Gaussians x 200 views at 1256x828 (configs[2])"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", choices=("render", "score"), default="render")
+    ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--n-gaussians", type=int, default=None, help="override N (debug only)")
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+# ---------------------------------------------------------------------------
+# clocks
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi -lms 200 during the timed region (clocks + throttle reasons)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-i", str(self.index), "-lms", "200"], stdout=subprocess.PIPE,
+                                      stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.p:
+            time.sleep(0.25)
+            self.p.terminate()
+            try:
+                out, _ = self.p.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.p.kill()
+                out, _ = self.p.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self) -> dict:
+        sm, mx, reasons, util_sm = [], None, set(), []
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in getattr(self, "lines", []):
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                s, m, u = float(f[1]), float(f[2]), float(f[8])
+            except ValueError:
+                continue
+            mx = m
+            if u > 0:
+                util_sm.append(s)
+            for nm, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+            sm.append(s)
+        use = util_sm or sm
+        return {"sm_mhz": statistics.median(use) if use else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm), "samples_under_load": len(util_sm)}
+
+
+def peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "_fallback": True}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline (oracle port, all host cores)
+# ---------------------------------------------------------------------------
+def cpu_views(scene, cams, images: bool, threads: int | None = None):
+    from oracle import oracle as O
+    O.build()
+    t0 = time.perf_counter()
+    r = O.views(scene, cams, dict_opts(), np.float32, threads=threads, scores=not images, images=images)
+    return time.perf_counter() - t0, r
+
+
+def dict_opts():
+    from paper_2403_13806_b200.render import RasterizeOptions
+    return RasterizeOptions(near_limit=0.2)
+
+
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ---------------------------------------------------------------------------
+# workloads
+# ---------------------------------------------------------------------------
+def make_workload(kind: str, n_override=None):
+    from paper_2403_13806_b200 import synth
+    if kind == "render":
+        scene, cams = synth.config1(0, n=n_override or 500_000)
+        return scene, cams
+    scene, cams = synth.config2(0, n=n_override or 3_000_000)
+    return scene, cams
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    scene, cams = make_workload(args.workload, args.n_gaussians)
+    threads = os.cpu_count() or 1
+    images = args.workload == "render"
+    # a step = one frame (or view) rendered by all host threads (bounded sample);
+    # a wall-clock guard keeps the whole arm within a few minutes on small hosts
+    for s in range(args.warmup):
+        cpu_views(scene, cams[s:s + 1], images, threads=threads)
+    total_t, done, budget = 0.0, 0, float(os.environ.get("RADSPLAT_REF_BUDGET_S", 240))
+    for s in range(args.steps):
+        dt, _ = cpu_views(scene, [cams[s % len(cams)]], images, threads=threads)
+        total_t += dt
+        done += 1
+        if total_t > budget:
+            break
+    value = done / total_t
+    unit = "frames/s" if images else "views/s"
+    line = {
+        "metric": METRIC_RENDER if images else METRIC_SCORE, "impl": "reference", "value": value, "unit": unit,
+        "n_gpus": world, "steps": args.steps, "steps_completed": done, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total_t / done,
+        "higher_is_better": True, "scaling": "weak" if images else "strong", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic (seeded, BASELINE configs distributions)",
+        "config": {"workload": "configs[1] render" if images else "configs[2] scoring",
+                   "n_gaussians": len(scene), "width": 1256, "height": 828},
+        "cpu_baseline": {"value": value, "unit": unit, "cores": threads, "kind": "port",
+                         "sample": f"1 {'frame' if images else 'view'} per step on {threads} threads "
+                                   f"(oracle/cpu_ref.cpp fp32 restatement, tile-parallel); CPU {cpu_model()}"},
+        "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def bytes_alg_render(n_in, n_vis, P, HW):
+    """SURVEY §8d per-frame algorithmic bytes."""
+    return 236 * n_in + 2 * 48 * n_vis + 2 * 12 * P + 4 * P + 20 * HW
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    from paper_2403_13806_b200 import _native as N
+    from paper_2403_13806_b200.device import camera_struct, device_scene, options_struct, renderer
+    from paper_2403_13806_b200.dist import all_reduce_max, shard_range
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    opts = dict_opts()
+    scene, cams = make_workload(args.workload, args.n_gaussians)
+    ds = device_scene(scene, dev)
+    r = renderer(dev)
+    lib = r.lib
+    opt_s = options_struct(opts)
+    stream = torch.cuda.current_stream(dev)
+    sptr = stream.cuda_stream
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    pk = peaks()
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    W_, H_ = cams[0].width, cams[0].height
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    result = {}
+    if args.workload == "render":
+        frames = lambda s: cams[(s * world + rank) % len(cams)]  # noqa: E731
+        out = r.alloc_outputs(cams[0])
+        # untimed pre-pass over every frame the timed loop will render: sizes the
+        # pair capacity (overflow-checked) and counts E / C for the roofline
+        E = C_ = P_ = NV = 0
+        for s in range(args.steps):
+            _, st = r.render(ds, frames(s), opts, out=out, count_evals=True)
+            E += st.evals
+            C_ += st.composites
+            P_ += st.n_pairs
+            NV += st.n_visible
+        cam_structs = [camera_struct(frames(s)) for s in range(args.steps)]
+        ptr = {k: v.data_ptr() for k, v in out.items()}
+
+        def step(cs, evs):
+            evs[0].record(stream)
+            N.check(lib.rs_project(r.handle, C.byref(ds.struct), None, 0, C.byref(cs), C.byref(opt_s), sptr))
+            evs[1].record(stream)
+            N.check(lib.rs_bin(r.handle, sptr))
+            evs[2].record(stream)
+            N.check(lib.rs_blend(r.handle, C.byref(opt_s), ptr["rgb"], ptr["alpha"], ptr["depth"], ptr["count"],
+                                 None, 0, sptr))
+            evs[3].record(stream)
+
+        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+        for s in range(args.warmup):
+            step(camera_struct(frames(s)), ev[0])
+        barrier()
+        with ClockSampler(local) as clk:
+            barrier()
+            t0 = time.perf_counter()
+            for s in range(args.steps):
+                flush.zero_()
+                step(cam_structs[s], ev[s])
+            barrier()
+            wall = time.perf_counter() - t0
+        st = r.stats()
+        assert not st.overflow
+        stage = np.array([[ev[s][i].elapsed_time(ev[s][i + 1]) for i in range(3)] for s in range(args.steps)])
+        t_frames = float(stage.sum())  # ms, device time of the K frames
+        t_local = torch.tensor([t_frames], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+        t_max = float(t_local.item())
+        value = world * args.steps / (t_max / 1e3)
+        blend_ms = float(stage[:, 2].sum())
+        fp32_peak = sms * 128 * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+        flops = 16 * E + 11 * C_
+        achieved = flops / (blend_ms / 1e3) / 1e12
+        hw = W_ * H_
+        frame_bytes = bytes_alg_render(len(scene), NV / args.steps, P_ / args.steps, hw)
+        result.update({
+            "metric": METRIC_RENDER, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded configs[1]: 500k Gaussians in 32 clusters, SH deg 3; no dataset offline)",
+            "config": {"workload": "configs[1] orbit render", "n_gaussians": len(scene), "width": W_, "height": H_,
+                       "tile": 16, "frames": args.steps, "l2": "flushed (256 MB memset) between timed steps",
+                       "parallelism": f"frames split across {world} GPU(s), no communication"},
+            "stages_ms": {"preprocess": float(stage[:, 0].mean()), "sort": float(stage[:, 1].mean()),
+                          "blend": float(stage[:, 2].mean())},
+            "wall_fps": world * args.steps / wall,
+            "workload_stats": {"visible_mean": NV / args.steps, "pairs_mean": P_ / args.steps,
+                               "evals_per_px": E / args.steps / hw, "composites_per_px": C_ / args.steps / hw},
+            "roofline": {"kernel": "blend_kernel<COLOR>", "bound": "fp32", "achieved": achieved,
+                         "peak": fp32_peak, "unit": "TFLOP/s", "frac": achieved / fp32_peak,
+                         "traffic": None, "algorithmic": "16*E + 11*C flops per frame (SURVEY §8d)",
+                         "peak_source": "computed: SMs x 128 FP32 lanes x 2 x sm_max_mhz"},
+            "frame_roofline": {"bytes_alg_per_frame": frame_bytes,
+                               "achieved_gbs": frame_bytes / (t_max / args.steps / 1e3) / 1e9,
+                               "peak_gbs": pk.get("hbm_gbs"),
+                               "frac": frame_bytes / (t_max / args.steps / 1e3) / 1e9 / pk.get("hbm_gbs", 6548.8)},
+            "gpu_launches": args.steps * (1 + 5 + 1 + 1 + r_tile_passes(W_, H_) + 1 + 1),
+            "clocks": clk.summary(),
+        })
+        # e2e: the reference-facing call (rasterize -> RenderOutput with host numpy
+        # fp64 arrays), camera in, image + alpha + count + depth out, every step
+        from paper_2403_13806_b200.render import rasterize
+        ke = min(args.steps, 30)
+        for s in range(2):
+            rasterize(scene, frames(s), opts)
+        barrier()
+        t0 = time.perf_counter()
+        for s in range(ke):
+            rasterize(scene, frames(s), opts)
+        barrier()
+        te = time.perf_counter() - t0
+        te_t = torch.tensor([te], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te_t, op=dist.ReduceOp.MAX)
+        result["e2e"] = {"value": world * ke / float(te_t.item()), "unit": "frames/s",
+                         "h2d_bytes_per_step": C.sizeof(N.RsCamera) + C.sizeof(N.RsOptions),
+                         "d2h_bytes_per_step": hw * (12 + 4 + 4 + 4),
+                         "api": "paper_2403_13806_b200.render.rasterize (scene resident in HBM after first call)"}
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            threads = os.cpu_count() or 1
+            sel = [frames(s) for s in range(4)]
+            dt, _ = cpu_views(scene, sel, True, threads=threads)
+            result["cpu_baseline"] = {"value": len(sel) / dt, "unit": "frames/s", "cores": threads, "kind": "port",
+                                      "sample": f"{len(sel)} orbit frames, each on {threads} threads "
+                                                f"(oracle/cpu_ref.cpp fp32, tile-parallel), CPU {cpu_model()}"}
+    else:
+        n = len(cams)
+        lo, hi = shard_range(n, rank, world)
+        mine = [camera_struct(c) for c in cams[lo:hi]]
+        scores = torch.zeros(len(scene), dtype=torch.float32, device=dev)
+        # pre-pass: overflow-checked capacity sizing over this rank's views
+        P_ = 0
+        for c in cams[lo:hi]:
+            _, st = r.render(ds, c, opts, color=False, scores=scores.view(torch.int32))
+            P_ += st.n_pairs
+        sc_ptr = scores.data_ptr()
+
+        def one_pass():
+            scores.zero_()
+            for cs in mine:
+                N.check(lib.rs_render(r.handle, C.byref(ds.struct), None, 0, C.byref(cs), C.byref(opt_s), None, None,
+                                      None, None, sc_ptr, 0, sptr))
+            all_reduce_max(scores)
+
+        for _ in range(args.warmup):
+            one_pass()
+        barrier()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        with ClockSampler(local) as clk:
+            barrier()
+            t0 = time.perf_counter()
+            for s in range(args.steps):
+                flush.zero_()
+                evs[s][0].record(stream)
+                one_pass()
+                evs[s][1].record(stream)
+            barrier()
+            wall = time.perf_counter() - t0
+        assert not r.stats().overflow
+        t_local = torch.tensor([sum(a.elapsed_time(b) for a, b in evs)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+        t_max = float(t_local.item())
+        value = args.steps * n / (t_max / 1e3)
+        kept = int((scores >= 0.01).sum().item())
+        result.update({
+            "metric": METRIC_SCORE, "value": value, "unit": "views/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded configs[2]: 3M Gaussians, log-scale N(-4,0.6); no dataset offline)",
+            "config": {"workload": "configs[2] importance scoring", "n_gaussians": len(scene), "views": n,
+                       "width": W_, "height": H_, "l2": "flushed (256 MB memset) between timed passes",
+                       "parallelism": f"views sharded over {world} GPU(s) + NCCL all_reduce(MAX)"},
+            "kept_at_0.01": kept, "wall_views_per_s": args.steps * n / wall,
+            "gpu_launches": args.steps * len(mine) * (1 + 5 + 1 + 1 + r_tile_passes(W_, H_) + 1 + 1),
+            "clocks": clk.summary(),
+        })
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def r_tile_passes(W, H):
+    T = ((W + 15) // 16) * ((H + 15) // 16)
+    return 1 if T <= 256 else 2
+
+
+if __name__ == "__main__":
+    main()

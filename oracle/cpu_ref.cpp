@@ -293,6 +293,14 @@ std::vector<int64_t> composite_order(const std::vector<PG<T>>& pg, const uint8_t
 
 struct Counters { int64_t E = 0, C = 0; };
 
+// max-merge that is safe when several threads composite different tiles
+template <typename T> inline void atomic_max(T* p, T v) {
+  std::atomic_ref<T> a(*p);
+  T cur = a.load(std::memory_order_relaxed);
+  while (v > cur && !a.compare_exchange_weak(cur, v, std::memory_order_relaxed)) {
+  }
+}
+
 // Per-pixel evaluation of one Gaussian: returns alpha (render.py:255-259).
 template <typename T> inline T pixel_alpha(const PG<T>& g, T xs, T ys, T alpha_max);
 template <> inline double pixel_alpha<double>(const PG<double>& g, double xs, double ys, double alpha_max) {
@@ -339,7 +347,7 @@ inline void composite_pixel(const std::vector<PG<T>>& pg, const int64_t* list, s
       gg = mac<T>(g.color[1], w, gg);
       b = mac<T>(g.color[2], w, b);
       d = mac<T>(g.depth, w, d);
-      if (contrib && w > contrib[list[j]]) contrib[list[j]] = w;  // render.py:273-275
+      if (contrib) atomic_max(contrib + list[j], w);  // render.py:273-275
       ++c;
       ++k.C;
       tau = tau * ((T)1 - alpha);  // render.py:281
@@ -381,16 +389,40 @@ int64_t bin_tiles(const std::vector<PG<T>>& pg, const uint8_t* active, int W, in
   return (int64_t)pairs.size();
 }
 
-// Full render of one view. method 0 = tiled lists, 1 = global list per pixel.
+// Run fn(worker) on `threads` workers (worker 0 is the caller).
+template <typename F> void parallel(int threads, F fn) {
+  if (threads <= 1) { fn(0); return; }
+  std::vector<std::thread> pool;
+  for (int t = 1; t < threads; ++t) pool.emplace_back(fn, t);
+  fn(0);
+  for (auto& th : pool) th.join();
+}
+
+template <typename T>
+std::vector<PG<T>> project_par(const Scene<T>& s, const Cam<T>& cam, const Opts<T>& o, int threads) {
+  std::vector<PG<T>> v((size_t)s.n);
+  const int64_t per = (s.n + threads - 1) / std::max(threads, 1);
+  parallel(threads, [&](int t) {
+    const int64_t lo = t * per, hi = std::min<int64_t>(s.n, lo + per);
+    for (int64_t i = lo; i < hi; ++i) v[(size_t)i] = project_one(s, i, cam, o);
+  });
+  return v;
+}
+
+// Full render of one view. method 0 = per-tile lists (the global (depth, index)
+// order restricted to each tile: identical per-pixel walk), 1 = the global
+// list per pixel (oracles.py literal). `threads` splits projection, tile-list
+// construction (bands of tile rows) and compositing (tiles); contributions
+// merge by an atomic max, which is order independent (render.py:71-76).
 template <typename T>
 void render(const Scene<T>& s, const T* camp, const T* optp, const uint8_t* active, int method, Out out,
-            Counters* kc) {
+            Counters* kc, int threads = 1) {
   const Cam<T> cam(camp);
   const Opts<T> o(optp);
-  const std::vector<PG<T>> pg = project_all(s, cam, o);
+  threads = std::max(threads, 1);
+  const std::vector<PG<T>> pg = project_par(s, cam, o, threads);
   T* contrib = (T*)out.contrib;
   const int W = cam.W, H = cam.H;
-  Counters k;
   auto store = [&](int x, int y, const T* rgbd, T tau, int32_t c) {
     const size_t p = (size_t)y * W + x;
     if (out.img) { T* im = (T*)out.img; im[3 * p] = rgbd[0]; im[3 * p + 1] = rgbd[1]; im[3 * p + 2] = rgbd[2]; }
@@ -398,32 +430,50 @@ void render(const Scene<T>& s, const T* camp, const T* optp, const uint8_t* acti
     if (out.depth) ((T*)out.depth)[p] = rgbd[3];
     if (out.count) out.count[p] = c;
   };
-  T rgbd[4], tau;
-  int32_t c;
+  const std::vector<int64_t> order = composite_order(pg, active);
+  std::vector<Counters> kk(threads);
   if (method == 1) {
-    const std::vector<int64_t> order = composite_order(pg, active);
-    for (int y = 0; y < H; ++y)
-      for (int x = 0; x < W; ++x) {
-        composite_pixel(pg, order.data(), order.size(), x, y, o, rgbd, tau, c, contrib, k);
-        store(x, y, rgbd, tau, c);
-      }
-  } else {
-    std::vector<uint64_t> keys;
-    std::vector<uint32_t> vals, ranges;
-    bin_tiles(pg, active, W, H, &keys, &vals, &ranges);
-    const int TW = (W + TILE - 1) / TILE, TH = (H + TILE - 1) / TILE;
-    std::vector<int64_t> list;
-    for (int t = 0; t < TW * TH; ++t) {
-      list.assign(vals.begin() + ranges[2 * t], vals.begin() + ranges[2 * t + 1]);
-      const int tx = t % TW, ty = t / TW;
-      for (int y = ty * TILE; y < std::min(H, ty * TILE + TILE); ++y)
-        for (int x = tx * TILE; x < std::min(W, tx * TILE + TILE); ++x) {
-          composite_pixel(pg, list.data(), list.size(), x, y, o, rgbd, tau, c, contrib, k);
+    std::atomic<int> next(0);
+    parallel(threads, [&](int t) {
+      T rgbd[4], tau;
+      int32_t c;
+      for (int y; (y = next.fetch_add(1)) < H;)
+        for (int x = 0; x < W; ++x) {
+          composite_pixel(pg, order.data(), order.size(), x, y, o, rgbd, tau, c, contrib, kk[t]);
           store(x, y, rgbd, tau, c);
         }
-    }
+    });
+  } else {
+    const int TW = (W + TILE - 1) / TILE, TH = (H + TILE - 1) / TILE;
+    std::vector<std::vector<int64_t>> lists((size_t)TW * TH);
+    const int rows_per = (TH + threads - 1) / threads;
+    parallel(threads, [&](int t) {
+      const int r0 = t * rows_per, r1 = std::min(TH, r0 + rows_per);
+      if (r0 >= r1) return;
+      for (const int64_t g : order) {
+        const PG<T>& q = pg[(size_t)g];
+        const int ty0 = std::max(q.y0 / TILE, r0), ty1 = std::min((q.y1 - 1) / TILE, r1 - 1);
+        for (int ty = ty0; ty <= ty1; ++ty)
+          for (int tx = q.x0 / TILE; tx <= (q.x1 - 1) / TILE; ++tx) lists[(size_t)ty * TW + tx].push_back(g);
+      }
+    });
+    std::atomic<int> next(0);
+    parallel(threads, [&](int t) {
+      T rgbd[4], tau;
+      int32_t c;
+      for (int tile; (tile = next.fetch_add(1)) < TW * TH;) {
+        const std::vector<int64_t>& list = lists[(size_t)tile];
+        const int tx = tile % TW, ty = tile / TW;
+        for (int y = ty * TILE; y < std::min(H, ty * TILE + TILE); ++y)
+          for (int x = tx * TILE; x < std::min(W, tx * TILE + TILE); ++x) {
+            composite_pixel(pg, list.data(), list.size(), x, y, o, rgbd, tau, c, contrib, kk[t]);
+            store(x, y, rgbd, tau, c);
+          }
+      }
+    });
   }
-  if (kc) { kc->E += k.E; kc->C += k.C; }
+  if (kc)
+    for (const Counters& k : kk) { kc->E += k.E; kc->C += k.C; }
 }
 
 template <typename T> Scene<T> mkscene(const T* pos, const T* logit, const T* sh, const T* ls, const T* quat, int64_t n, int deg) {
@@ -431,44 +481,27 @@ template <typename T> Scene<T> mkscene(const T* pos, const T* logit, const T* sh
   return s;
 }
 
-// Per-view parallel driver (CPU baseline): views are independent and merge by
-// an order-independent max (pruning.py:80-82), so threads split the views.
+// CPU-baseline driver: views one after another, each rendered by all threads
+// (so a bounded sample of a few views still uses every core); scores merge by
+// max across views (pruning.py:80-82).
 template <typename T>
 void views(const Scene<T>& s, const T* cams, int64_t n_views, const T* optp, int threads, int want_images,
            T* contrib, T* img_last, int64_t* counters) {
-  if (threads < 1) threads = 1;
-  std::atomic<int64_t> next(0);
-  std::vector<std::vector<T>> local(threads);
-  std::vector<Counters> kc(threads);
-  auto work = [&](int tid) {
-    std::vector<T>& acc = local[tid];
-    if (contrib) acc.assign((size_t)s.n, (T)0);
-    std::vector<T> img;
-    for (;;) {
-      const int64_t v = next.fetch_add(1);
-      if (v >= n_views) break;
-      const T* cp = cams + 21 * v;
-      const int W = (int)cp[0], H = (int)cp[1];
-      Out out{};
-      if (want_images) {
-        img.assign((size_t)W * H * 3, (T)0);
-        out.img = img.data();
-      }
-      out.contrib = contrib ? acc.data() : nullptr;
-      render<T>(s, cp, optp, nullptr, 0, out, &kc[tid]);
-      if (img_last && v == n_views - 1) std::memcpy(img_last, img.data(), img.size() * sizeof(T));
+  Counters kc;
+  std::vector<T> img;
+  for (int64_t v = 0; v < n_views; ++v) {
+    const T* cp = cams + 21 * v;
+    const int W = (int)cp[0], H = (int)cp[1];
+    Out out{};
+    if (want_images) {
+      img.assign((size_t)W * H * 3, (T)0);
+      out.img = img.data();
     }
-  };
-  std::vector<std::thread> pool;
-  for (int t = 1; t < threads; ++t) pool.emplace_back(work, t);
-  work(0);
-  for (auto& th : pool) th.join();
-  if (contrib)
-    for (int t = 0; t < threads; ++t)
-      for (int64_t i = 0; i < s.n; ++i) contrib[i] = std::max(contrib[i], local[t][(size_t)i]);
-  if (counters) {
-    for (int t = 0; t < threads; ++t) { counters[0] += kc[t].E; counters[1] += kc[t].C; }
+    out.contrib = contrib;
+    render<T>(s, cp, optp, nullptr, 0, out, &kc, threads);
+    if (img_last && v == n_views - 1) std::memcpy(img_last, img.data(), img.size() * sizeof(T));
   }
+  if (counters) { counters[0] += kc.E; counters[1] += kc.C; }
 }
 
 // flat projection export for the tests (ctypes)

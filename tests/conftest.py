@@ -79,3 +79,30 @@ def render_cases():
     s, cam, o = load_case(d, "cfg0_")
     out.append(("config0", s, cam, options_from(o), d, "cfg0_"))
     return out
+
+
+def tier_b_check(name, img, alpha, count, contrib, d, p, thresholds=(0.001, 0.01, 0.05)):
+    """fp32 result vs the fp64 reference's golden output (Tier B budget).
+
+    * count flips (a threshold decision alpha >= 1/255 or tau >= 1e-4 taken the
+      other way in fp32) are rare: <= max(4, pixels / 10^4);
+    * every pixel that is not a flip pixel is within the north-star 1e-4 (RGB
+      and alpha); flip pixels may differ by up to alpha_cut * tau;
+    * importance: >= 99.5% of Gaussians within 1e-5 relative (fp32 tau after
+      many near-opaque layers carries ~6e-8 * o/(1-o) relative error per layer);
+    * prune / visibility masks identical except where |h - t| <= 1e-4 * t.
+    """
+    ref_count = d[p + "count"]
+    flips = count != ref_count
+    assert flips.sum() <= max(4, ref_count.size // 10000), (name, int(flips.sum()))
+    err = np.abs(img - d[p + "img"]).max(axis=-1)
+    assert np.all(err[~flips] <= 1e-4), (name, float(err[~flips].max()))
+    aerr = np.abs(alpha - d[p + "alpha"])
+    assert np.all(aerr[~flips] <= 1e-4), (name, float(aerr[~flips].max()))
+    ref = d[p + "contrib"]
+    rel = np.abs(contrib - ref) / np.maximum(ref, 1e-30)
+    assert np.mean(rel <= 1e-5) >= 0.995, (name, float(rel.max()))
+    assert np.all(rel <= 1e-3) or flips.any(), (name, float(rel.max()))
+    for t in thresholds:
+        diff = (contrib >= t) != (ref >= t)
+        assert np.all(np.abs(ref[diff] - t) <= 1e-4 * t), (name, t)

@@ -1,0 +1,127 @@
+"""Pin the CPU oracle against the reference's own outputs (CPU only).
+
+The golden vectors in tests/golden were produced by the unmodified reference
+(fieldsplat) by tests/golden/make_golden.py: the two 50-scene bit-exact
+suites of the reference tests, the known-answer cases, the two-room
+visibility fixture, the viewer parity bundle and BASELINE configs[0].
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden, load_case, options_from, render_cases, tier_b_check
+
+CASES = render_cases()
+IDS = [c[0] for c in CASES]
+
+
+@pytest.fixture(scope="module")
+def O():
+    from oracle import oracle
+    oracle.build()
+    return oracle
+
+
+@pytest.mark.parametrize("case", CASES, ids=IDS)
+def test_fp64_oracle_matches_reference(O, case):
+    """Tier B: the fp64 restatement reproduces the reference to ~1 ulp."""
+    name, scene, cam, opts, d, p = case
+    for method in (0, 1):  # tiled lists and the literal per-pixel global order
+        r = O.render(scene, cam, opts, np.float64, method=method)
+        assert np.abs(r["img"] - d[p + "img"]).max() <= 1e-12, name
+        assert np.abs(r["alpha"] - d[p + "alpha"]).max() <= 1e-12, name
+        assert np.array_equal(r["count"], d[p + "count"]), name
+        assert np.abs(r["contrib"] - d[p + "contrib"]).max() <= 1e-12, name
+
+
+@pytest.mark.parametrize("case", CASES, ids=IDS)
+def test_fp64_projection_and_order(O, case):
+    name, scene, cam, opts, d, p = case
+    pr = O.project(scene, cam, opts, np.float64)
+    assert np.array_equal(pr["valid"], d[p + "proj_valid"])
+    for k in ("x0", "x1", "y0", "y1"):
+        assert np.array_equal(pr[k].astype(np.int64), d[p + "proj_" + k]), (name, k)
+    for k, rk in (("mx", "mx"), ("my", "my"), ("a", "a"), ("b", "b"), ("c", "c"), ("ia", "inv_a"),
+                  ("ib", "inv_b"), ("ic", "inv_c"), ("depth", "depth"), ("opacity", "opacity"),
+                  ("color", "color"), ("radius", "radius")):
+        ref = d[p + "proj_" + rk]
+        assert np.allclose(pr[k], ref, rtol=1e-12, atol=1e-12), (name, k)
+    assert np.array_equal(O.order(scene, cam, opts, np.float64), d[p + "order"])
+
+
+@pytest.mark.parametrize("case", CASES, ids=IDS)
+def test_fp32_oracle_within_budget_of_reference(O, case):
+    """Tier A vs the fp64 reference: fp32 rounding, rare threshold flips only."""
+    name, scene, cam, opts, d, p = case
+    r = O.render(scene, cam, opts, np.float32)
+    tier_b_check(name, r["img"], r["alpha"], r["count"], r["contrib"], d, p)
+
+
+@pytest.mark.parametrize("case", CASES, ids=IDS)
+def test_tiled_equals_global_order(O, case):
+    """The tile lists reproduce the reference's global (depth, index) walk exactly."""
+    name, scene, cam, opts, d, p = case
+    for dt in (np.float32, np.float64):
+        a = O.render(scene, cam, opts, dt, method=0)
+        b = O.render(scene, cam, opts, dt, method=1)
+        for k in ("img", "alpha", "depth", "count", "contrib"):
+            assert np.array_equal(a[k], b[k]), (name, k)
+        assert a["E"] == b["E"] and a["C"] == b["C"]
+        assert a["C"] == int(a["count"].sum())
+
+
+def test_binning_structure(O):
+    d = golden("config0")
+    scene, cam, o = load_case(d, "cfg0_")
+    opts = options_from(o)
+    b = O.bin_tiles(scene, cam, opts, np.float32)
+    keys, vals, ranges = b["keys"], b["vals"], b["ranges"]
+    assert np.all(np.diff(keys.astype(np.float64)) >= 0) and np.all(keys[1:] >= keys[:-1])
+    assert ranges[0, 0] == 0 and ranges[-1, 1] == b["P"]
+    nonempty = ranges[:, 1] > ranges[:, 0]
+    assert np.all(ranges[nonempty, 0][1:] == ranges[nonempty, 1][:-1])
+    order = O.order(scene, cam, opts, np.float32)
+    rank = np.empty(len(scene), np.int64)
+    rank[order] = np.arange(len(order))
+    for t in range(len(ranges)):
+        lst = vals[ranges[t, 0]:ranges[t, 1]]
+        assert np.all(np.diff(rank[lst]) > 0)  # per-tile order = global order restricted
+    assert b["P"] == 13613  # configs[0] tile pairs (fp64 reference projection)
+    r = O.render(scene, cam, opts, np.float32)
+    assert r["E"] == 883773  # E_alg = 53.9 per pixel
+
+
+def test_exp_contract_accuracy(O):
+    x = np.linspace(-100, 80, 2_000_001, dtype=np.float32)
+    y = O.exp_contract(x).astype(np.float64)
+    t = np.exp(x.astype(np.float64))
+    ok = t > 1e-37
+    assert np.max(np.abs(y[ok] - t[ok]) / t[ok]) < 3 * 2.0 ** -24
+    x2 = np.linspace(-140, 120, 2_000_001, dtype=np.float32)
+    y2 = O.exp2_contract(x2).astype(np.float64)
+    t2 = np.exp2(x2.astype(np.float64))
+    ok = t2 > 1e-37
+    assert np.max(np.abs(y2[ok] - t2[ok]) / t2[ok]) < 3 * 2.0 ** -24
+    assert O.exp2_contract(np.array([0.0, 1.0, -1.0, 200.0, -200.0, np.nan], np.float32)).tolist()[:5] == \
+        [1.0, 2.0, 0.5, np.inf, 0.0]
+
+
+def test_depth_key_order(O):
+    vals = np.array([-np.inf, -3.0, -1e-30, -0.0, 0.0, 1e-30, 0.2, 0.2000001, 5.0, np.inf], np.float32)
+    keys = [O.depth_key(float(v)) for v in vals]
+    assert keys[3] == keys[4]  # -0 folded into +0
+    assert all(a <= b for a, b in zip(keys, keys[1:]))
+
+
+def test_viewer_parity_bundle(O):
+    """Reference viewer fixture (make_fixtures.py): fp32 frames of the reference renderer."""
+    from paper_2403_13806_b200.core import GaussianScene
+    from conftest import load_cam
+    d = golden("viewer_parity")
+    scene = GaussianScene(positions=d["pos"], opacity_logits=d["logit"], sh=d["sh"], log_scales=d["ls"],
+                          quaternions=d["quat"], active_sh_degree=int(d["deg"]))
+    for i in range(5):
+        cam = load_cam(d, f"pose{i}_")
+        r = O.render(scene, cam, None, np.float32)
+        mse = np.mean((r["img"].astype(np.float64) - d[f"pose{i}_frame"]) ** 2)
+        assert mse == 0 or 10 * np.log10(1.0 / mse) >= 80.0  # the viewer suite's bar is 30 dB
