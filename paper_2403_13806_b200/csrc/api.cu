@@ -25,8 +25,8 @@ size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
 struct Layout {
   // per-frame zeroed region [0, frame_bytes)
-  size_t ctr, hist, diff, emit_lb, frame_bytes;
-  size_t ranges, recs, keysA, keysB, valsA, valsB, ptileA, ptileB, pitemA, pitemB, lbA, lbB, total;
+  size_t ctr, hist, emit_lb, ranges, frame_bytes;
+  size_t recs, keysA, keysB, valsA, valsB, offsets, owners, ptileA, ptileB, pitemA, pitemB, lbA, lbB, total;
 };
 
 int tiles_x(int w) { return (w + kTile - 1) / kTile; }
@@ -38,20 +38,21 @@ Layout make_layout(int64_t n_cap, int64_t pair_cap, int W, int H) {
   auto take = [&](size_t bytes) { const size_t at = o; o = align_up(o + bytes); return at; };
   L.ctr = take(sizeof(Counters));
   L.hist = take(8 * 256 * sizeof(uint32_t));  // depth passes 0-3, tile passes 4-5
-  L.diff = take((TW + 1) * (TH + 1) * sizeof(int32_t));
   L.emit_lb = take(((size_t)n_cap / 256 + 1) * sizeof(unsigned long long));
-  L.frame_bytes = o;
   L.ranges = take(TW * TH * sizeof(uint2));
+  L.frame_bytes = o;
   L.recs = take((size_t)n_cap * sizeof(Rec));
   L.keysA = take((size_t)n_cap * 4);
   L.keysB = take((size_t)n_cap * 4);
   L.valsA = take((size_t)n_cap * 4);
   L.valsB = take((size_t)n_cap * 4);
+  L.offsets = take((size_t)n_cap * 4);
+  L.owners = take(((size_t)pair_cap / kEmitPairs + 2) * 4);
   L.ptileA = take((size_t)pair_cap * 2);
   L.ptileB = take((size_t)pair_cap * 2);
   L.pitemA = take((size_t)pair_cap * 4);
   L.pitemB = take((size_t)pair_cap * 4);
-  const size_t chunks = (size_t)(std::max(n_cap, pair_cap) + kChunk - 1) / kChunk + 1;
+  const size_t chunks = (size_t)(std::max(n_cap, pair_cap) + kMinChunk - 1) / kMinChunk + 1;
   L.lbA = take(chunks * 256 * 4);
   L.lbB = take(chunks * 256 * 4);
   L.total = o;
@@ -70,7 +71,7 @@ struct rs_workspace {
   // current frame (set by rs_project)
   uint32_t n_items;
   int W, H, TW, TH;
-  int tile_passes;
+  int tile_bits, tile_passes;
   bool binned;
 
   template <typename T> T* at(size_t off) const { return reinterpret_cast<T*>(base + off); }
@@ -83,29 +84,33 @@ cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 int32_t cuda_status() { return cudaGetLastError() == cudaSuccess ? RS_OK : RS_ECUDA; }
 
-template <typename K>
+constexpr int kDepthItems = 8;   // 2048-key chunks: more CTAs for the small depth sort
+constexpr int kTileItems = 16;   // 4096-pair chunks for the large tile sort
+
+// LSD passes of one sort over `bits` key bits; the digit histograms
+// (hist_slot) and the first pass's zeroed look-back words were produced by
+// the key-producing kernel.
+template <typename K, int ITEMS>
 void run_sort(rs_workspace* ws, const K* keys0, K* keysA, K* keysB, const uint32_t* vals0, uint32_t* valsA,
-              uint32_t* valsB, const uint32_t* n_ptr, uint32_t n_static, uint32_t n_bound, int passes, int hist_slot,
+              uint32_t* valsB, const uint32_t* n_ptr, uint32_t n_static, uint32_t n_bound, int bits, int hist_slot,
               int ticket_slot, bool last_keys, cudaStream_t st, const K** keys_res, const uint32_t** vals_res) {
   Counters* ctr = ws->ctr();
   uint32_t* hist = ws->at<uint32_t>(ws->L.hist) + hist_slot * 256;
   uint32_t* lb[2] = {ws->at<uint32_t>(ws->L.lbA), ws->at<uint32_t>(ws->L.lbB)};
-  const int hist_blocks = (int)std::max<uint32_t>(1, std::min<uint32_t>((n_bound + 255) / 256, ws->sms * 8));
-  radix_hist_kernel<K><<<hist_blocks, 256, 0, st>>>(keys0, n_ptr, n_static, passes, 0, hist, lb[0],
-                                                    ctr->tickets + ticket_slot);
-  const int smem = (int)sizeof(OnesweepSmem<K>);
-  const int chunks = (int)((n_bound + kChunk - 1) / kChunk);
-  const int grid = std::max(1, std::min(chunks, ws->sms * 4));
+  const int smem = (int)sizeof(OnesweepSmem<K, ITEMS>);
+  constexpr uint32_t CHUNK = kSortThreads * ITEMS;
+  const int grid = std::max(1, (int)((n_bound + CHUNK - 1) / CHUNK));  // one CTA per chunk, ticket order
+  const int passes = (bits + 7) / 8;
   const K* kin = keys0;
   const uint32_t* vin = vals0;
   for (int p = 0; p < passes; ++p) {
     K* kout = (p % 2 == 0) ? keysB : keysA;
     uint32_t* vout = (p % 2 == 0) ? valsB : valsA;
     const bool last = p == passes - 1;
-    onesweep_kernel<K><<<grid, kSortThreads, smem, st>>>(kin, vin, kout, vout, n_ptr, n_static, hist + p * 256,
-                                                         lb[p % 2], last ? nullptr : lb[(p + 1) % 2],
-                                                         ctr->tickets + ticket_slot + p, 8 * p,
-                                                         (!last || last_keys) ? 1 : 0);
+    const int nbits = std::min(8, bits - 8 * p);
+    onesweep_kernel<K, ITEMS><<<grid, kSortThreads, smem, st>>>(
+        kin, vin, kout, vout, n_ptr, n_static, hist + p * 256, lb[p % 2], last ? nullptr : lb[(p + 1) % 2],
+        ctr->tickets + ticket_slot + p, 8 * p, nbits, (!last || last_keys) ? 1 : 0);
     kin = kout;
     vin = vout;
   }
@@ -114,11 +119,10 @@ void run_sort(rs_workspace* ws, const K* keys0, K* keysA, K* keysB, const uint32
 }
 
 void configure_kernels() {  // per device; idempotent
-  cudaFuncSetAttribute(onesweep_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)sizeof(OnesweepSmem<uint32_t>));
-  cudaFuncSetAttribute(onesweep_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)sizeof(OnesweepSmem<uint16_t>));
-  cudaFuncSetAttribute(ranges_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(onesweep_kernel<uint32_t, kDepthItems>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)sizeof(OnesweepSmem<uint32_t, kDepthItems>));
+  cudaFuncSetAttribute(onesweep_kernel<uint16_t, kTileItems>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)sizeof(OnesweepSmem<uint16_t, kTileItems>));
 }
 
 }  // namespace
@@ -150,7 +154,7 @@ int32_t rs_workspace_create(void* device_mem, size_t bytes, int64_t n_cap, int64
       width <= 0 || height <= 0)
     return RS_EINVAL;
   const int TW = tiles_x(width), TH = tiles_x(height);
-  if ((int64_t)TW * TH > 65536 || (int64_t)(TW + 1) * (TH + 1) * 4 > 200 * 1024) return RS_EINVAL;
+  if ((int64_t)TW * TH > 65536) return RS_EINVAL;
   const Layout L = make_layout(n_cap, pair_cap, width, height);
   if (bytes < L.total) return RS_ENOMEM_WORKSPACE;
   rs_workspace* ws = new (std::nothrow) rs_workspace();
@@ -191,17 +195,20 @@ static int32_t project_impl(rs_workspace* ws, const rs_scene* scene, const int32
   ws->H = cam->height;
   ws->TW = TW;
   ws->TH = TH;
-  ws->tile_passes = (TW * TH <= 256) ? 1 : 2;
+  ws->tile_bits = 1;
+  while ((1 << ws->tile_bits) < TW * TH) ++ws->tile_bits;
+  ws->tile_passes = (ws->tile_bits + 7) / 8;
   ws->binned = false;
   // zero counters, histograms, difference array and emit look-back in one memset
   cudaMemsetAsync(ws->base, 0, ws->L.frame_bytes, st);
   if (items > 0) {
+    const unsigned grid = (unsigned)((items + 127) / 128);
     if (full)
-      project_kernel<true><<<(unsigned)((items + 127) / 128), 128, 0, st>>>(
+      project_kernel<true><<<grid, 128, 0, st>>>(
           scene->planes, scene->plane_stride, scene->sh_degree, active_idx, (uint32_t)items, *cam, *opts,
           ws->at<Rec>(ws->L.recs), ws->at<uint32_t>(ws->L.keysA), ws->ctr(), full, reinterpret_cast<int4*>(full_bbox));
     else
-      project_kernel<false><<<(unsigned)((items + 127) / 128), 128, 0, st>>>(
+      project_kernel<false><<<grid, 128, 0, st>>>(
           scene->planes, scene->plane_stride, scene->sh_degree, active_idx, (uint32_t)items, *cam, *opts,
           ws->at<Rec>(ws->L.recs), ws->at<uint32_t>(ws->L.keysA), ws->ctr(), nullptr, nullptr);
   }
@@ -225,23 +232,34 @@ int32_t rs_bin(rs_workspace* ws, void* stream) {
   cudaStream_t st = S(stream);
   const uint32_t n = ws->n_items;
   if (n > 0) {
+    radix_hist_kernel<<<std::max(1, std::min((int)((n + 255) / 256), ws->sms * 2)), 256, 0, st>>>(
+        ws->at<uint32_t>(ws->L.keysA), n, 4, kSortThreads * kDepthItems, ws->at<uint32_t>(ws->L.hist),
+        ws->at<uint32_t>(ws->L.lbA));
     const uint32_t *keys_res, *items_sorted;
-    run_sort<uint32_t>(ws, ws->at<uint32_t>(ws->L.keysA), ws->at<uint32_t>(ws->L.keysA),
-                       ws->at<uint32_t>(ws->L.keysB), nullptr, ws->at<uint32_t>(ws->L.valsA),
-                       ws->at<uint32_t>(ws->L.valsB), nullptr, n, n, 4, 0, 0, false, st, &keys_res, &items_sorted);
-    emit_kernel<<<(n + 255) / 256, 256, 0, st>>>(items_sorted, ws->at<Rec>(ws->L.recs), ws->ctr(), ws->TW,
-                                                 (uint32_t)ws->pair_cap, ws->at<uint16_t>(ws->L.ptileA),
-                                                 ws->at<uint32_t>(ws->L.pitemA), ws->at<int32_t>(ws->L.diff),
-                                                 ws->at<unsigned long long>(ws->L.emit_lb));
+    run_sort<uint32_t, kDepthItems>(ws, ws->at<uint32_t>(ws->L.keysA), ws->at<uint32_t>(ws->L.keysA),
+                                    ws->at<uint32_t>(ws->L.keysB), nullptr, ws->at<uint32_t>(ws->L.valsA),
+                                    ws->at<uint32_t>(ws->L.valsB), nullptr, n, n, 32, 0, 0, false, st, &keys_res,
+                                    &items_sorted);
+    count_kernel<<<(n + 255) / 256, 256, 0, st>>>(items_sorted, ws->at<Rec>(ws->L.recs), ws->ctr(), ws->TW,
+                                                  (uint32_t)ws->pair_cap, ws->at<uint32_t>(ws->L.offsets),
+                                                  ws->at<uint32_t>(ws->L.owners),
+                                                  ws->at<unsigned long long>(ws->L.emit_lb));
+    const unsigned egrid = (unsigned)std::max<int64_t>(1, (ws->pair_cap + kEmitPairs - 1) / kEmitPairs);
+    emit_kernel<<<egrid, 256, 0, st>>>(items_sorted, ws->at<Rec>(ws->L.recs), ws->at<uint32_t>(ws->L.offsets),
+                                       ws->at<uint32_t>(ws->L.owners), ws->ctr(), ws->TW,
+                                       ws->at<uint16_t>(ws->L.ptileA), ws->at<uint32_t>(ws->L.pitemA),
+                                       ws->at<uint32_t>(ws->L.hist) + 4 * 256, ws->at<uint32_t>(ws->L.lbA),
+                                       kSortThreads * kTileItems);
     const uint16_t* tiles_res;
     const uint32_t* pitems;
-    run_sort<uint16_t>(ws, ws->at<uint16_t>(ws->L.ptileA), ws->at<uint16_t>(ws->L.ptileA),
-                       ws->at<uint16_t>(ws->L.ptileB), ws->at<uint32_t>(ws->L.pitemA), ws->at<uint32_t>(ws->L.pitemA),
-                       ws->at<uint32_t>(ws->L.pitemB), &ws->ctr()->n_pairs, 0, (uint32_t)ws->pair_cap,
-                       ws->tile_passes, 4, 4, false, st, &tiles_res, &pitems);
+    run_sort<uint16_t, kTileItems>(ws, ws->at<uint16_t>(ws->L.ptileA), ws->at<uint16_t>(ws->L.ptileA),
+                                   ws->at<uint16_t>(ws->L.ptileB), ws->at<uint32_t>(ws->L.pitemA),
+                                   ws->at<uint32_t>(ws->L.pitemA), ws->at<uint32_t>(ws->L.pitemB),
+                                   &ws->ctr()->n_pairs, 0, (uint32_t)ws->pair_cap, ws->tile_bits, 4, 4, true, st,
+                                   &tiles_res, &pitems);
+    const unsigned rgrid = (unsigned)std::max<int64_t>(1, (ws->pair_cap + 2047) / 2048);
+    ranges_kernel<<<rgrid, 256, 0, st>>>(tiles_res, ws->ctr(), ws->at<uint2>(ws->L.ranges));
   }
-  const int nd = (ws->TW + 1) * (ws->TH + 1);
-  ranges_kernel<<<1, 1024, nd * 4, st>>>(ws->at<int32_t>(ws->L.diff), ws->TW, ws->TH, ws->at<uint2>(ws->L.ranges));
   ws->binned = true;
   return cuda_status();
 }

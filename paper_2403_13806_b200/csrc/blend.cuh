@@ -2,11 +2,13 @@
 // and its importance-scoring variant (render.py:267, :273-275 + pruning.py:86-92).
 //
 // One 256-thread CTA per 16x16 tile, one thread per pixel; warp w owns the 8x4
-// sub-rectangle (w%2, w/2) so that the per-Gaussian bbox test (oracles.py:36-38)
-// is usually warp-uniform. The tile's (depth, index)-ordered list is consumed
+// sub-rectangle (w%2, w/2). The tile's (depth, index)-ordered list is consumed
 // in batches of 256 records: each thread stages one 64-byte record into shared
-// memory with four 128-bit loads, then every warp walks the batch reading the
-// records as shared-memory broadcasts.
+// memory with four 128-bit loads and tags it with the 8-bit set of warps whose
+// sub-rectangle its bbox touches; each warp then compacts (ballot + popc) its
+// own ordered entry list and walks only that, reading records as shared-memory
+// broadcasts and stopping as soon as all 32 of its pixels have terminated. The
+// per-pixel bbox gate (oracles.py:36-38) is still applied exactly.
 //
 // Per pixel and Gaussian (Tier-A contract, bit-identical to oracle/cpu_ref.cpp):
 //   p2    = fma(na*dx, dx, fma(nb*dy, dx, (nc*dy)*dy))     (= -0.5*log2(e)*q)
@@ -40,18 +42,22 @@ __global__ void __launch_bounds__(kBlendThreads) blend_kernel(
   __shared__ float4 s_c[COLOR ? kBlendThreads : 1];
   __shared__ int4 s_d[kBlendThreads];
   __shared__ uint32_t s_w[CONTRIB ? kBlendThreads : 1];
+  __shared__ uint8_t s_mask[kBlendThreads];             // which warps' 8x4 sub-rectangles the entry touches
+  __shared__ uint8_t s_list[kBlendThreads / 32][kBlendThreads];  // per-warp compacted entry lists
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int tile = blockIdx.x;
   const int tx = tile % TW, ty = tile / TW;
-  const int px = tx * kTile + (warp & 1) * 8 + (lane & 7);
-  const int py = ty * kTile + (warp >> 1) * 4 + (lane >> 3);
+  const int ox = tx * kTile, oy = ty * kTile;
+  const int px = ox + (warp & 1) * 8 + (lane & 7);
+  const int py = oy + (warp >> 1) * 4 + (lane >> 3);
   const bool inside = px < W && py < H;
   const float xs = __fadd_rn((float)px, 0.5f), ys = __fadd_rn((float)py, 0.5f);
   if (ctr->overflow) return;  // pair list incomplete: the host re-runs with a larger capacity
   const uint2 rg = ranges[tile];
   const uint32_t npairs = ctr->n_pairs;
   const uint32_t end = rg.y < npairs ? rg.y : npairs;  // memory safety on overflow
+  const uint32_t lt = (1u << lane) - 1u;
 
   float tau = 1.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f, cd = 0.0f;
   int cnt = 0;
@@ -69,16 +75,34 @@ __global__ void __launch_bounds__(kBlendThreads) blend_kernel(
       const float4 c = __ldg(&R->c);
       if (COLOR) s_c[tid] = c;
       gid = (uint32_t)__float_as_int(c.w);
-      s_d[tid] = __ldg(&R->d);
+      const int4 d = __ldg(&R->d);
+      s_d[tid] = d;
+      // bbox x sub-rectangle overlap: 2 column halves x 4 row quarters -> bit w = (w%2, w/2)
+      const unsigned col = (d.x < ox + 8 && d.y > ox ? 1u : 0u) | (d.x < ox + 16 && d.y > ox + 8 ? 2u : 0u);
+      unsigned m = 0;
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        if (d.z < oy + 4 * r + 4 && d.w > oy + 4 * r) m |= col << (2 * r);
+      s_mask[tid] = (uint8_t)m;
     }
     if (CONTRIB) s_w[tid] = 0u;
     __syncthreads();
     const int n = (int)min((uint32_t)kBlendThreads, end - base);
     if (!__all_sync(0xffffffffu, done)) {
-      for (int j = 0; j < n; ++j) {
+      // this warp's entries, in list order
+      int cntw = 0;
+      for (int c0 = 0; c0 < n; c0 += 32) {
+        const int e = c0 + lane;
+        const bool has = e < n && ((s_mask[e] >> warp) & 1u);
+        const unsigned bal = __ballot_sync(0xffffffffu, has);
+        if (has) s_list[warp][cntw + __popc(bal & lt)] = (uint8_t)e;
+        cntw += __popc(bal);
+      }
+      __syncwarp();
+      for (int q = 0; q < cntw; ++q) {
+        const int j = s_list[warp][q];
         const int4 bb = s_d[j];
         const bool in = !done && px >= bb.x && px < bb.y && py >= bb.z && py < bb.w;
-        if (!__any_sync(0xffffffffu, in)) continue;
         float w = 0.0f;
         if (in) {
           if (STATS) ++evals;
@@ -109,6 +133,7 @@ __global__ void __launch_bounds__(kBlendThreads) blend_kernel(
           const uint32_t wm = __reduce_max_sync(0xffffffffu, __float_as_uint(w));
           if (lane == 0 && wm) atomicMax(&s_w[j], wm);
         }
+        if (__all_sync(0xffffffffu, done)) break;  // every pixel of the warp terminated
       }
     }
     __syncthreads();
