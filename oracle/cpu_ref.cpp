@@ -312,7 +312,8 @@ template <> inline double pixel_alpha<double>(const PG<double>& g, double xs, do
 template <> inline float pixel_alpha<float>(const PG<float>& g, float xs, float ys, float alpha_max) {
   const float dx = xs - g.mx, dy = ys - g.my;
   const float p2 = std::fma(g.na * dx, dx, std::fma(g.nb * dy, dx, (g.nc * dy) * dy));
-  const float raw = g.opacity * exp2_contract(p2);
+  // 2^min(p2, 127): an overflow guard (o * 2^127 saturates alpha_max for any o >= 5.8e-39)
+  const float raw = g.opacity * exp2_contract(p2 < 127.0f || p2 != p2 ? p2 : 127.0f);
   return (raw != raw || raw < alpha_max) ? raw : alpha_max;  // np.minimum propagates NaN
 }
 

@@ -282,16 +282,21 @@ int32_t rs_blend(rs_workspace* ws, const rs_options* opts, float* out_rgb, float
   const uint32_t* items = final_pair_items(ws);
   const Rec* recs = ws->at<Rec>(ws->L.recs);
   Counters* ctr = ws->ctr();
-#define RS_BLEND(C, I, K)                                                                                        \
-  blend_kernel<C, I, K><<<T, kBlendThreads, 0, st>>>(ranges, items, recs, ctr, ws->W, ws->H, ws->TW, *opts, \
-                                                     out_rgb, out_alpha, out_depth, out_count, scores)
+#define RS_BLEND(C, I, K, F)                                                                        \
+  blend_kernel<C, I, K, F><<<T, kBlendThreads, 0, st>>>(ranges, items, recs, ctr, ws->W, ws->H, ws->TW, *opts, \
+                                                        out_rgb, out_alpha, out_depth, out_count, scores)
+#define RS_BLEND_F(C, I, K) \
+  if (fast) RS_BLEND(C, I, K, true); else RS_BLEND(C, I, K, false)
+  // exact-range exp2 is only needed for degenerate options (see blend.cuh FAST)
+  const bool fast = opts->alpha_cut >= 1e-30f;
   if (color && scores) {
-    if (stats) RS_BLEND(true, true, true); else RS_BLEND(true, true, false);
+    if (stats) { RS_BLEND_F(true, true, true); } else { RS_BLEND_F(true, true, false); }
   } else if (color) {
-    if (stats) RS_BLEND(true, false, true); else RS_BLEND(true, false, false);
+    if (stats) { RS_BLEND_F(true, false, true); } else { RS_BLEND_F(true, false, false); }
   } else {
-    if (stats) RS_BLEND(false, true, true); else RS_BLEND(false, true, false);
+    if (stats) { RS_BLEND_F(false, true, true); } else { RS_BLEND_F(false, true, false); }
   }
+#undef RS_BLEND_F
 #undef RS_BLEND
   return cuda_status();
 }

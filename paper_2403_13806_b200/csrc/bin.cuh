@@ -134,8 +134,9 @@ __global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ 
   const uint32_t k1 = min(P, k0 + kEmitPairs);
   for (int i = tid; i < 512; i += 256) (&s_hist[0][0])[i] = 0;
   const uint32_t r0 = chunk_owner[blockIdx.x];
-  // owners of [k0, k1): at most k1 - k0 consecutive ranks (every rank has >= 1 pair)
-  const uint32_t nown = min((uint32_t)kEmitPairs, nvis - r0);
+  // owners of [k0, k1): ranks r0 .. owner(k1 - 1) <= chunk_owner[next chunk]; at most k1 - k0 of them
+  const uint32_t rlast = k1 < P ? chunk_owner[blockIdx.x + 1] : nvis - 1;
+  const uint32_t nown = min((uint32_t)kEmitPairs, rlast - r0 + 1);
   for (uint32_t i = tid; i < nown; i += 256) {
     const uint32_t o = offsets[r0 + i];
     s_off[i] = o;

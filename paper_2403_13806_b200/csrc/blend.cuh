@@ -12,7 +12,7 @@
 //
 // Per pixel and Gaussian (Tier-A contract, bit-identical to oracle/cpu_ref.cpp):
 //   p2    = fma(na*dx, dx, fma(nb*dy, dx, (nc*dy)*dy))     (= -0.5*log2(e)*q)
-//   alpha = min(o * 2^p2, alpha_max)
+//   alpha = min(o * 2^min(p2, 127), alpha_max)
 //   if alpha >= alpha_cut and tau >= tau_stop:   (render.py:261)
 //       w = alpha*tau; rgb += c*w; depth += z*w; count++; tau *= 1 - alpha
 // Pixels leave the loop once tau < tau_stop (nothing can composite after
@@ -31,16 +31,16 @@
 
 namespace rs {
 
-template <bool COLOR, bool CONTRIB, bool STATS>
+// FAST: the host guarantees alpha_cut >= 1e-30, so every evaluated p2 is >=
+// cut2 >= -126 (projection clamps it) and, after the contract's clamp at 127,
+// inside exp2_core's exact range: the range-checked exp2_contract is not needed.
+template <bool COLOR, bool CONTRIB, bool STATS, bool FAST>
 __global__ void __launch_bounds__(kBlendThreads) blend_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ pair_items, const Rec* __restrict__ recs,
     Counters* __restrict__ ctr, int W, int H, int TW, rs_options o, float* __restrict__ out_rgb,
     float* __restrict__ out_alpha, float* __restrict__ out_depth, int32_t* __restrict__ out_count,
     uint32_t* __restrict__ scores) {
-  __shared__ float4 s_a[kBlendThreads];
-  __shared__ float4 s_b[kBlendThreads];
-  __shared__ float4 s_c[COLOR ? kBlendThreads : 1];
-  __shared__ int4 s_d[kBlendThreads];
+  __shared__ Rec s_rec[kBlendThreads];  // one 64-byte record per entry: one base address per iteration
   __shared__ uint32_t s_w[CONTRIB ? kBlendThreads : 1];
   __shared__ uint8_t s_mask[kBlendThreads];             // which warps' 8x4 sub-rectangles the entry touches
   __shared__ uint8_t s_list[kBlendThreads / 32][kBlendThreads];  // per-warp compacted entry lists
@@ -70,13 +70,13 @@ __global__ void __launch_bounds__(kBlendThreads) blend_kernel(
     uint32_t gid = 0;
     if (idx < end) {
       const Rec* R = recs + __ldg(pair_items + idx);
-      s_a[tid] = __ldg(&R->a);
-      s_b[tid] = __ldg(&R->b);
+      s_rec[tid].a = __ldg(&R->a);
+      s_rec[tid].b = __ldg(&R->b);
       const float4 c = __ldg(&R->c);
-      if (COLOR) s_c[tid] = c;
+      if (COLOR || CONTRIB) s_rec[tid].c = c;
       gid = (uint32_t)__float_as_int(c.w);
       const int4 d = __ldg(&R->d);
-      s_d[tid] = d;
+      s_rec[tid].d = d;
       // bbox x sub-rectangle overlap: 2 column halves x 4 row quarters -> bit w = (w%2, w/2)
       const unsigned col = (d.x < ox + 8 && d.y > ox ? 1u : 0u) | (d.x < ox + 16 && d.y > ox + 8 ? 2u : 0u);
       unsigned m = 0;
@@ -100,24 +100,25 @@ __global__ void __launch_bounds__(kBlendThreads) blend_kernel(
       }
       __syncwarp();
       for (int q = 0; q < cntw; ++q) {
-        const int j = s_list[warp][q];
-        const int4 bb = s_d[j];
+        const Rec& E = s_rec[s_list[warp][q]];
+        const int4 bb = E.d;
         const bool in = !done && px >= bb.x && px < bb.y && py >= bb.z && py < bb.w;
         float w = 0.0f;
         if (in) {
           if (STATS) ++evals;
-          const float4 ga = s_a[j];
-          const float4 gb = s_b[j];
+          const float4 ga = E.a;
+          const float4 gb = E.b;
           const float dx = __fsub_rn(xs, ga.x), dy = __fsub_rn(ys, ga.y);
           const float p2 =
               __fmaf_rn(__fmul_rn(ga.z, dx), dx, __fmaf_rn(__fmul_rn(ga.w, dy), dx, __fmul_rn(__fmul_rn(gb.x, dy), dy)));
           if (p2 >= gb.z) {
-            const float e = (p2 >= -126.0f && p2 <= 127.0f) ? exp2_core(p2) : exp2_contract(p2);
+            const float pc = fminf(p2, 127.0f);  // contract: exp2 argument clamped at 127 (oracle does the same)
+            const float e = FAST ? exp2_core(pc) : exp2_contract(pc);
             const float alpha = fminf(__fmul_rn(gb.y, e), o.alpha_max);
             if (alpha >= o.alpha_cut) {
               w = __fmul_rn(alpha, tau);
               if (COLOR) {
-                const float4 gc = s_c[j];
+                const float4 gc = E.c;
                 cr = __fmaf_rn(gc.x, w, cr);
                 cg = __fmaf_rn(gc.y, w, cg);
                 cb = __fmaf_rn(gc.z, w, cb);
@@ -131,7 +132,7 @@ __global__ void __launch_bounds__(kBlendThreads) blend_kernel(
         }
         if (CONTRIB) {
           const uint32_t wm = __reduce_max_sync(0xffffffffu, __float_as_uint(w));
-          if (lane == 0 && wm) atomicMax(&s_w[j], wm);
+          if (lane == 0 && wm) atomicMax(&s_w[s_list[warp][q]], wm);
         }
         if (__all_sync(0xffffffffu, done)) break;  // every pixel of the warp terminated
       }

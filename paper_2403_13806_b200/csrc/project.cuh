@@ -174,7 +174,11 @@ __global__ void __launch_bounds__(128) project_kernel(const float* __restrict__ 
       }
       const float K = fbits(0xbf38aa3bu);  // -0.5*log2(e)
       // conservative skip threshold: p2 < cut2 => alpha < alpha_cut
-      const float cut2 = o.alpha_cut > 0.0f ? __fsub_rn(log2f(o.alpha_cut / op), 1e-3f) : -INFINITY;
+      // (clamped at -126: p2 < -126 gives alpha < 2^-126 < alpha_cut whenever the fast
+      // blend path is used, i.e. alpha_cut >= 1e-30; the exact path ignores the clamp's effect
+      // only through the skip, which stays conservative)
+      float cut2 = o.alpha_cut > 0.0f ? __fsub_rn(log2f(o.alpha_cut / op), 1e-3f) : -INFINITY;
+      if (o.alpha_cut >= 1e-30f && cut2 < -126.0f) cut2 = -126.0f;
       Rec rec;
       rec.a = make_float4(mx, my, __fmul_rn(K, ia), __fmul_rn(__fmul_rn(2.0f, K), ib));
       rec.b = make_float4(__fmul_rn(K, ic), op, cut2, depth);

@@ -59,10 +59,17 @@ __global__ void __launch_bounds__(256) radix_hist_kernel(const uint32_t* __restr
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < words; i += stride) lookback0[i] = 0;
 }
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, uint32_t src_bytes) {
+  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
 template <typename K, int ITEMS>
 struct OnesweepSmem {
   K keys[kSortThreads * ITEMS];
   uint32_t vals[kSortThreads * ITEMS];
+  uint32_t vstage[kSortThreads * ITEMS];  // this chunk's values in input order (cp.async prefetch)
   uint32_t whist[8][256];   // per-warp digit counts, then per-warp exclusive offsets
   uint32_t gbase[256];      // global exclusive digit offsets of this pass
   uint32_t lstart[256];     // chunk-local exclusive digit starts
@@ -114,6 +121,14 @@ __global__ void __launch_bounds__(kSortThreads, 3) onesweep_kernel(
   const uint32_t cbase = c * CHUNK;
   const uint32_t wbase = cbase + warp * 32 * ITEMS;
   const uint32_t lt = lanemask_lt();
+  const uint32_t m = min(CHUNK, n - cbase);
+  if (vals_in) {  // prefetch the chunk's values (16-byte cp.async, zero-filled tail) behind the ranking
+    for (uint32_t q = tid; q < CHUNK / 4; q += kSortThreads) {
+      const uint32_t e = 4 * q;
+      const uint32_t bytes = e < m ? min(16u, 4 * (m - e)) : 0u;
+      cp_async16(&S.vstage[e], vals_in + cbase + (bytes ? e : 0), bytes);
+    }
+  }
   uint32_t kk[ITEMS], rk[ITEMS];
 #pragma unroll
   for (int it = 0; it < ITEMS; ++it) {
@@ -185,6 +200,7 @@ __global__ void __launch_bounds__(kSortThreads, 3) onesweep_kernel(
     S.lstart[tid] = ls;
     S.gout[tid] = S.gbase[tid] + excl - ls;
   }
+  if (vals_in) cp_async_wait_all();
   __syncthreads();
 #pragma unroll
   for (int it = 0; it < ITEMS; ++it) {  // scatter into shared memory in chunk-sorted order
@@ -193,11 +209,10 @@ __global__ void __launch_bounds__(kSortThreads, 3) onesweep_kernel(
       const uint32_t d = (kk[it] >> shift) & dmask;
       const uint32_t pos = S.lstart[d] + S.whist[warp][d] + rk[it];
       S.keys[pos] = (K)kk[it];
-      S.vals[pos] = vals_in ? vals_in[i] : i;
+      S.vals[pos] = vals_in ? S.vstage[i - cbase] : i;
     }
   }
   __syncthreads();
-  const uint32_t m = min(CHUNK, n - cbase);
   for (uint32_t p = tid; p < m; p += kSortThreads) {
     const K k = S.keys[p];
     const uint32_t g = S.gout[((uint32_t)k >> shift) & dmask] + p;
