@@ -172,20 +172,23 @@ __global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ 
     }
   }
   __syncthreads();
-  // coalesced copy-out + digit histograms of the tile sort
-  for (uint32_t p = tid; p < k1 - k0; p += 256) {
-    const uint32_t tile = s_tile_out[p];
-    pair_tiles[k0 + p] = (uint16_t)tile;
-    pair_items[k0 + p] = s_item_out[p];
-    atomicAdd(&s_hist[0][tile & 255], 1u);
-    // high digit: consecutive pairs mostly share it -> one atomic per run inside the warp
-    const uint32_t hi8 = tile >> 8;
-    const unsigned act = __activemask();
-    const uint32_t prev = __shfl_up_sync(act, hi8, 1);
-    const uint32_t next = __shfl_down_sync(act, hi8, 1);
-    const bool has_next = lane < 31 && ((act >> (lane + 1)) & 1u);
-    const unsigned starts = __ballot_sync(act, lane == 0 || prev != hi8);
-    if (!has_next || next != hi8) {
+  // coalesced copy-out + digit histograms of the tile sort (uniform trip count: full-warp votes)
+  const uint32_t npair = k1 - k0;
+  for (uint32_t p0 = 0; p0 < npair; p0 += 256) {
+    const uint32_t p = p0 + tid;
+    const bool ok = p < npair;
+    const uint32_t tile = ok ? (uint32_t)s_tile_out[p] : 0u;
+    if (ok) {
+      pair_tiles[k0 + p] = (uint16_t)tile;
+      pair_items[k0 + p] = s_item_out[p];
+      atomicAdd(&s_hist[0][tile & 255], 1u);
+    }
+    // high digit: consecutive pairs mostly share it -> one shared atomic per run of equal digits
+    const uint32_t hi8 = ok ? tile >> 8 : 0xffffffffu;
+    const uint32_t prev = __shfl_up_sync(0xffffffffu, hi8, 1);
+    const uint32_t next = __shfl_down_sync(0xffffffffu, hi8, 1);
+    const unsigned starts = __ballot_sync(0xffffffffu, lane == 0 || prev != hi8);
+    if (ok && (lane == 31 || next != hi8)) {
       const int run_start = 31 - __clz(starts & ((2u << lane) - 1u));
       atomicAdd(&s_hist[1][hi8], (uint32_t)(lane - run_start + 1));
     }

@@ -73,6 +73,7 @@ def device_scene(scene, device: torch.device | None = None) -> DeviceScene:
     """Upload once per (scene object, generation, device); later calls reuse it."""
     if isinstance(scene, DeviceScene):
         return scene
+    N.load()  # raises NativeUnavailable without the library or a CUDA device (no CPU fallback)
     dev = torch.device(device or torch.device("cuda", torch.cuda.current_device()))
     key = (id(scene), dev)
     hit = _scene_cache.get(key)
@@ -250,6 +251,7 @@ _renderers: dict = {}
 
 
 def renderer(device: torch.device | None = None) -> Renderer:
+    N.load()
     dev = torch.device(device or torch.device("cuda", torch.cuda.current_device()))
     r = _renderers.get(dev)
     if r is None:
