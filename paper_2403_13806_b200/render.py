@@ -49,12 +49,20 @@ class ProjectedGaussian:
     bbox: tuple
 
 
-@dataclass
 class RenderOutput:
-    color: ImageBuffer
-    alpha: np.ndarray   # (H, W) float64
-    count: np.ndarray   # (H, W) int64
-    depth: np.ndarray | None = None  # (H, W) sum of w * camera z (not in the reference)
+    """color (ImageBuffer, (H,W,3) float64), alpha (H,W) float64, count (H,W) int64,
+    plus ``depth`` (H,W) = sum of w * camera z -- not in the reference; copied from
+    the device on first access only."""
+
+    def __init__(self, color: ImageBuffer, alpha: np.ndarray, count: np.ndarray, depth=None):
+        self.color, self.alpha, self.count = color, alpha, count
+        self._depth = depth
+
+    @property
+    def depth(self):
+        if isinstance(self._depth, torch.Tensor):
+            self._depth = self._depth.double().cpu().numpy()
+        return self._depth
 
 
 class ContributionAccumulator:
@@ -95,11 +103,16 @@ def render_device(scene, camera, options: RasterizeOptions = RasterizeOptions(),
 
 
 def _to_output(out: dict) -> RenderOutput:
-    rgb = out["rgb"].cpu().numpy().astype(np.float64)
-    alpha = out["alpha"].cpu().numpy().astype(np.float64)
-    return RenderOutput(color=ImageBuffer(rgb), alpha=alpha,
-                        count=out["count"].cpu().numpy().astype(np.int64),
-                        depth=out["depth"].cpu().numpy().astype(np.float64))
+    """Reference-typed host result: widened to float64 / int64 on the device, then
+    one device-to-host copy per array straight into fresh numpy buffers."""
+    H, W = out["alpha"].shape
+    rgb = np.empty((H, W, 3), np.float64)
+    alpha = np.empty((H, W), np.float64)
+    count = np.empty((H, W), np.int64)
+    torch.from_numpy(rgb).copy_(out["rgb"].double())
+    torch.from_numpy(alpha).copy_(out["alpha"].double())
+    torch.from_numpy(count).copy_(out["count"].long())
+    return RenderOutput(color=ImageBuffer.trusted(rgb), alpha=alpha, count=count, depth=out["depth"])
 
 
 def rasterize(scene, camera, options: RasterizeOptions = RasterizeOptions()) -> RenderOutput:
