@@ -85,7 +85,7 @@ cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 int32_t cuda_status() { return cudaGetLastError() == cudaSuccess ? RS_OK : RS_ECUDA; }
 
 constexpr int kDepthItems = 8;   // 2048-key chunks: more CTAs for the small depth sort
-constexpr int kTileItems = 16;   // 4096-pair chunks for the large tile sort
+constexpr int kTileItems = 16;   // 4096-pair chunks for the tile sort
 
 // LSD passes of one sort over `bits` key bits; the digit histograms
 // (hist_slot) and the first pass's zeroed look-back words were produced by
@@ -108,9 +108,23 @@ void run_sort(rs_workspace* ws, const K* keys0, K* keysA, K* keysB, const uint32
     uint32_t* vout = (p % 2 == 0) ? valsB : valsA;
     const bool last = p == passes - 1;
     const int nbits = std::min(8, bits - 8 * p);
-    onesweep_kernel<K, ITEMS><<<grid, kSortThreads, smem, st>>>(
-        kin, vin, kout, vout, n_ptr, n_static, hist + p * 256, lb[p % 2], last ? nullptr : lb[(p + 1) % 2],
-        ctr->tickets + ticket_slot + p, 8 * p, nbits, (!last || last_keys) ? 1 : 0);
+    uint32_t* lb_next = last ? nullptr : lb[(p + 1) % 2];
+    const int wk = (!last || last_keys) ? 1 : 0;
+#define RS_PASS(NB)                                                                                       \
+  onesweep_kernel<K, ITEMS, NB><<<grid, kSortThreads, smem, st>>>(kin, vin, kout, vout, n_ptr, n_static,   \
+                                                                  hist + p * 256, lb[p % 2], lb_next,      \
+                                                                  ctr->tickets + ticket_slot + p, 8 * p, wk)
+    switch (nbits) {
+      case 1: RS_PASS(1); break;
+      case 2: RS_PASS(2); break;
+      case 3: RS_PASS(3); break;
+      case 4: RS_PASS(4); break;
+      case 5: RS_PASS(5); break;
+      case 6: RS_PASS(6); break;
+      case 7: RS_PASS(7); break;
+      default: RS_PASS(8); break;
+    }
+#undef RS_PASS
     kin = kout;
     vin = vout;
   }
@@ -118,11 +132,19 @@ void run_sort(rs_workspace* ws, const K* keys0, K* keysA, K* keysB, const uint32
   *vals_res = vin;
 }
 
+template <typename K, int ITEMS, int NB>
+void set_smem() {
+  cudaFuncSetAttribute(onesweep_kernel<K, ITEMS, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)sizeof(OnesweepSmem<K, ITEMS>));
+}
+template <typename K, int ITEMS>
+void set_smem_all() {
+  set_smem<K, ITEMS, 1>(); set_smem<K, ITEMS, 2>(); set_smem<K, ITEMS, 3>(); set_smem<K, ITEMS, 4>();
+  set_smem<K, ITEMS, 5>(); set_smem<K, ITEMS, 6>(); set_smem<K, ITEMS, 7>(); set_smem<K, ITEMS, 8>();
+}
 void configure_kernels() {  // per device; idempotent
-  cudaFuncSetAttribute(onesweep_kernel<uint32_t, kDepthItems>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)sizeof(OnesweepSmem<uint32_t, kDepthItems>));
-  cudaFuncSetAttribute(onesweep_kernel<uint16_t, kTileItems>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)sizeof(OnesweepSmem<uint16_t, kTileItems>));
+  set_smem_all<uint32_t, kDepthItems>();
+  set_smem_all<uint16_t, kTileItems>();
 }
 
 }  // namespace

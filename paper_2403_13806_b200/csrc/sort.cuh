@@ -78,20 +78,21 @@ struct OnesweepSmem {
   uint32_t chunk;
 };
 
-// One pass over bits [shift, shift + nbits), nbits <= 8.
-template <typename K, int ITEMS>
-__global__ void __launch_bounds__(kSortThreads, 3) onesweep_kernel(
+// One pass over bits [shift, shift + NBITS), NBITS <= 8 (compile-time: the
+// per-bit ballots unroll into a straight SHF/VOTE/LOP3 sequence).
+template <typename K, int ITEMS, int NBITS>
+__global__ void __launch_bounds__(kSortThreads, 4) onesweep_kernel(
     const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, K* __restrict__ keys_out,
     uint32_t* __restrict__ vals_out, const uint32_t* __restrict__ n_ptr, uint32_t n_static,
     const uint32_t* __restrict__ pass_hist, uint32_t* __restrict__ lookback, uint32_t* __restrict__ lookback_next,
-    uint32_t* __restrict__ ticket, int shift, int nbits, int write_keys) {
+    uint32_t* __restrict__ ticket, int shift, int write_keys) {
   constexpr uint32_t CHUNK = kSortThreads * ITEMS;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   OnesweepSmem<K, ITEMS>& S = *reinterpret_cast<OnesweepSmem<K, ITEMS>*>(smem_raw);
   const uint32_t n = n_ptr ? *n_ptr : n_static;
   const uint32_t chunks = (n + CHUNK - 1) / CHUNK;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t dmask = (1u << nbits) - 1u;
+  constexpr uint32_t dmask = (1u << NBITS) - 1u;
 
   if (tid == 0) S.chunk = atomicAdd(ticket, 1u);
 #pragma unroll
@@ -142,10 +143,10 @@ __global__ void __launch_bounds__(kSortThreads, 3) onesweep_kernel(
     const bool ok = i < n;
     const uint32_t d = (kk[it] >> shift) & dmask;
     uint32_t peers = __ballot_sync(0xffffffffu, ok);
-    for (int b = 0; b < nbits; ++b) {
-      const bool bit = (d >> b) & 1u;
-      const uint32_t bal = __ballot_sync(0xffffffffu, bit);
-      peers &= bit ? bal : ~bal;
+#pragma unroll
+    for (int b = 0; b < NBITS; ++b) {
+      const uint32_t bal = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+      peers &= ((d >> b) & 1u) ? bal : ~bal;
     }
     uint32_t base = 0;
     if (ok) base = S.whist[warp][d];
@@ -162,25 +163,33 @@ __global__ void __launch_bounds__(kSortThreads, 3) onesweep_kernel(
     S.whist[w][tid] = cnt;
     cnt += t;
   }
-  // publish the aggregate, then look back (4 predecessors per round) for the exclusive prefix
+  // publish the aggregate, then look back for the exclusive prefix: each digit thread
+  // reads LB predecessors per round trip (independent loads), then folds them in order
   volatile uint32_t* lb = lookback;
   lb[c * 256 + tid] = (c == 0 ? (uint32_t)kFlagInc : (uint32_t)kFlagAgg) | cnt;
   uint32_t excl = 0;
   if (c > 0) {
+    constexpr int LB = 4;
     int j = (int)c - 1;
     for (;;) {
-      uint32_t s[4];
+      uint32_t s[LB];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) s[q] = j - q >= 0 ? lb[(j - q) * 256 + tid] : (uint32_t)kFlagInc;
+      for (int q = 0; q < LB; ++q) s[q] = j - q >= 0 ? lb[(j - q) * 256 + tid] : (uint32_t)kFlagInc;
       int q = 0;
       bool fin = false;
-      for (; q < 4; ++q) {
-        if ((s[q] & ~(uint32_t)kValMask) == 0) break;  // not published yet: re-read from here
-        excl += s[q] & kValMask;
-        if (s[q] & kFlagInc) { fin = true; break; }
+#pragma unroll
+      for (int qq = 0; qq < LB; ++qq) {
+        if (!fin && q == qq) {
+          if ((s[qq] & ~(uint32_t)kValMask) == 0) {
+            q = -1 - qq;  // not published yet: resume from here
+          } else {
+            excl += s[qq] & kValMask;
+            if (s[qq] & kFlagInc) fin = true; else q = qq + 1;
+          }
+        }
       }
       if (fin) break;
-      j -= q;
+      j -= q >= 0 ? q : (-1 - q);
     }
     lb[c * 256 + tid] = kFlagInc | (excl + cnt);
   }

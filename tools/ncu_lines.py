@@ -6,7 +6,7 @@ import sys
 
 rep, kern = sys.argv[1], sys.argv[2]
 txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name", f"regex:{kern}",
-                      "--launch-count", "1"], capture_output=True, text=True).stdout
+                      "--launch-skip", sys.argv[4] if len(sys.argv) > 4 else "0", "--launch-count", "1"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(txt)))
 hdr = next(r for r in rows if "Address" in r and "Source" in r)
 data = [dict(zip(hdr, r)) for r in rows[rows.index(hdr) + 1:] if len(r) == len(hdr)]
