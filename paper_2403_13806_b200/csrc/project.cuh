@@ -183,7 +183,31 @@ __global__ void __launch_bounds__(128) project_kernel(const float* __restrict__ 
       rec.a = make_float4(mx, my, __fmul_rn(K, ia), __fmul_rn(__fmul_rn(2.0f, K), ib));
       rec.b = make_float4(__fmul_rn(K, ic), op, cut2, depth);
       rec.c = make_float4(col[0], col[1], col[2], __int_as_float((int)i));
-      rec.d = make_int4(x0, x1, y0, y1);
+      // culling box: pixels whose centre lies outside the ellipse {p2 >= cut2}, widened by
+      // 1% + 0.5 px, cannot reach alpha_cut even with fp32 rounding of p2 (bounded by
+      // 6*2^-24*kappa*|cut2| for condition number kappa <= 1e4; worse-conditioned
+      // Gaussians keep the full bbox). Double precision: once per Gaussian.
+      int cx0 = x0, cx1 = x1, cy0 = y0, cy1 = y1;
+      {
+        const double Na = __fmul_rn(K, ia), Nb = __fmul_rn(__fmul_rn(2.0f, K), ib), Nc = __fmul_rn(K, ic);
+        const double C2 = cut2;
+        const double D = 4.0 * Na * Nc - Nb * Nb;
+        const double tr = Na + Nc, sq = sqrt((Na - Nc) * (Na - Nc) + Nb * Nb);
+        const double l1 = 0.5 * (tr - sq), l2 = 0.5 * (tr + sq);  // eigenvalues, both < 0 if definite
+        if (!(C2 < 0.0)) {
+          cx1 = cx0;  // opacity below alpha_cut (or cut2 = +inf): nothing can composite
+          cy1 = cy0;
+        } else if (C2 > -1e30 && D > 0.0 && l2 < 0.0 && l1 >= 1e4 * l2) {
+          const double hx = sqrt(C2 * 4.0 * Nc / D) * 1.01 + 0.5, hy = sqrt(C2 * 4.0 * Na / D) * 1.01 + 0.5;
+          cx0 = max(x0, (int)fmax(floor((double)mx - hx - 0.5), -1.0));
+          cx1 = min(x1, (int)fmin(floor((double)mx + hx - 0.5) + 1.0, 65535.0));
+          cy0 = max(y0, (int)fmax(floor((double)my - hy - 0.5), -1.0));
+          cy1 = min(y1, (int)fmin(floor((double)my + hy - 0.5) + 1.0, 65535.0));
+          if (cx1 < cx0) cx1 = cx0;
+          if (cy1 < cy0) cy1 = cy0;
+        }
+      }
+      rec.d = make_int4(x0 | (x1 << 16), y0 | (y1 << 16), cx0 | (cx1 << 16), cy0 | (cy1 << 16));
       if (valid) recs[item] = rec;
       if (FULL) {
         float4* f = reinterpret_cast<float4*>(full + 16 * (size_t)item);
@@ -191,7 +215,7 @@ __global__ void __launch_bounds__(128) project_kernel(const float* __restrict__ 
         f[1] = make_float4(c, ia, ib, ic);
         f[2] = make_float4(radius, depth, col[0], col[1]);
         f[3] = make_float4(col[2], op, valid ? 1.0f : 0.0f, 0.0f);
-        full_bbox[item] = rec.d;
+        full_bbox[item] = make_int4(x0, x1, y0, y1);
       }
     }
     keys[item] = valid ? depth_key(depth) : kInvalidKey;

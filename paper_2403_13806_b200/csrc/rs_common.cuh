@@ -17,12 +17,20 @@ constexpr int kPlanes = 59;
 //   a = {mean x, mean y, na, nb}   na,nb,nc = -0.5*log2(e) * (ia, 2*ib, ic)
 //   b = {nc, opacity, cut2, depth} cut2: log2 power below which alpha < alpha_cut
 //   c = {r, g, b, gid bits}        gid = scene index (for importance scatter)
-//   d = {x0, x1, y0, y1}           half-open pixel bbox (render.py:133-137)
+//   d = {x0 | x1<<16, y0 | y1<<16, cx0 | cx1<<16, cy0 | cy1<<16}
+//       [x0,x1)x[y0,y1): the half-open 3-sigma pixel bbox of render.py:133-137;
+//       [cx0,cx1)x[cy0,cy1): a sub-box outside which no pixel can reach
+//       alpha >= alpha_cut (culling only -- never changes a result, §4 DESIGN.md)
 struct __align__(16) Rec {
   float4 a, b, c;
   int4 d;
 };
 static_assert(sizeof(Rec) == 64, "record must be 64 B");
+
+__device__ __forceinline__ int lo16(int v) { return v & 0xffff; }
+__device__ __forceinline__ int hi16(int v) { return (int)((unsigned)v >> 16); }
+__device__ __forceinline__ int4 bbox_of(const int4 d) { return make_int4(lo16(d.x), hi16(d.x), lo16(d.y), hi16(d.y)); }
+__device__ __forceinline__ int4 cullbox_of(const int4 d) { return make_int4(lo16(d.z), hi16(d.z), lo16(d.w), hi16(d.w)); }
 
 // Device-side counters, mirrors rs_stats (first four words) + sort bookkeeping.
 struct Counters {
