@@ -95,6 +95,27 @@ inline float exp_contract(float x) {
   return scale2(p, (int)n);
 }
 
+// log2(x) for normal x > 0 (~1e-7 relative); used only for the conservative
+// skip threshold cut2, but it also fixes the culling box that the tile binning
+// uses, so it must be reproducible: add/mul/div/fma only (device twin in rs_math.cuh).
+inline float log2_contract(float x) {
+  if (x != x) return x;
+  if (x <= 0.0f) return -INFINITY;
+  if (x == INFINITY) return INFINITY;
+  if (x < 1.17549435e-38f) return -150.0f;  // subnormal: a lower bound is enough (conservative)
+  const uint32_t u = ubits(x);
+  int e = (int)((u >> 23) & 0xffu) - 127;
+  float m = fbits((u & 0x7fffffu) | 0x3f800000u);
+  if (m > 1.41421356f) { m = m * 0.5f; e += 1; }
+  const float t = (m - 1.0f) / (m + 1.0f);
+  const float t2 = t * t;
+  float p = std::fma(t2, 0.111111112f, 0.142857149f);
+  p = std::fma(p, t2, 0.200000003f);
+  p = std::fma(p, t2, 0.333333343f);
+  p = std::fma(p, t2, 1.0f);
+  return std::fma(t * p, 2.88539004f, (float)e);
+}
+
 template <typename T> struct M;
 template <> struct M<double> {
   static double exp(double x) { return std::exp(x); }
@@ -138,6 +159,9 @@ template <typename T> struct PG {
   T mx, my, a, b, c, ia, ib, ic, radius, depth, color[3], opacity;
   int32_t x0, x1, y0, y1;
   float na, nb, nc;  // fp32 contract: -0.5*log2(e) * (ia, 2*ib, ic)
+  float cut2;        // fp32 contract: p2 < cut2 => alpha < alpha_cut
+  int32_t cx0, cx1, cy0, cy1;  // culling box (fp32 contract); == bbox for T = double
+  uint8_t bin;       // binned: valid and the culling box is non-empty
 };
 
 template <typename T> inline int64_t floor_clip(T v, int hi) {
@@ -155,6 +179,36 @@ template <typename T> inline int64_t ceil1_clip(T v, int hi) {
   if (f <= (T)-1) return 0;
   if (f >= (T)hi) return hi;
   return (int64_t)f + 1 > hi ? hi : (int64_t)f + 1;
+}
+
+// Culling box of the fp32 contract (device twin: project.cuh). cut2 is a
+// conservative bound (p2 < cut2 => o*2^p2 < alpha_cut); outside the ellipse
+// {p2 >= cut2} widened by 1% + 0.5 px no pixel can reach alpha_cut even with
+// the fp32 rounding of p2 (condition number <= 1e4; else the full bbox). The
+// tile binning uses this box; Gaussians with an empty box are not binned.
+template <typename T> inline void cull_box(PG<T>& g, float alpha_cut) {
+  const float op = (float)g.opacity;
+  float cut2 = alpha_cut > 0.0f ? log2_contract(alpha_cut / op) - 1e-3f : -INFINITY;
+  if (alpha_cut >= 1e-30f && cut2 < -126.0f) cut2 = -126.0f;
+  g.cut2 = cut2;
+  const double Na = g.na, Nb = g.nb, Nc = g.nc, C2 = cut2;
+  const double D = 4.0 * Na * Nc - Nb * Nb;
+  const double tr = Na + Nc, sq = std::sqrt((Na - Nc) * (Na - Nc) + Nb * Nb);
+  const double l1 = 0.5 * (tr - sq), l2 = 0.5 * (tr + sq);
+  if (!(C2 < 0.0)) {
+    g.cx1 = g.cx0;
+    g.cy1 = g.cy0;
+  } else if (C2 > -1e30 && D > 0.0 && l2 < 0.0 && l1 >= 1e4 * l2) {
+    const double hx = std::sqrt(C2 * 4.0 * Nc / D) * 1.01 + 0.5, hy = std::sqrt(C2 * 4.0 * Na / D) * 1.01 + 0.5;
+    const double mx = (float)g.mx, my = (float)g.my;
+    g.cx0 = std::max(g.x0, (int32_t)std::fmax(std::floor(mx - hx - 0.5), -1.0));
+    g.cx1 = std::min(g.x1, (int32_t)std::fmin(std::floor(mx + hx - 0.5) + 1.0, 65535.0));
+    g.cy0 = std::max(g.y0, (int32_t)std::fmax(std::floor(my - hy - 0.5), -1.0));
+    g.cy1 = std::min(g.y1, (int32_t)std::fmin(std::floor(my + hy - 0.5) + 1.0, 65535.0));
+    if (g.cx1 < g.cx0) g.cx1 = g.cx0;
+    if (g.cy1 < g.cy0) g.cy1 = g.cy0;
+  }
+  g.bin = g.valid && g.cx1 > g.cx0 && g.cy1 > g.cy0;
 }
 
 template <typename T>
@@ -271,6 +325,10 @@ PG<T> project_one(const Scene<T>& s, int64_t i, const Cam<T>& cam, const Opts<T>
   g.na = K * (float)g.ia;
   g.nb = (2.0f * K) * (float)g.ib;
   g.nc = K * (float)g.ic;
+  g.cx0 = g.x0; g.cx1 = g.x1; g.cy0 = g.y0; g.cy1 = g.y1;
+  g.cut2 = -INFINITY;
+  g.bin = g.valid;
+  if (sizeof(T) == 4 && g.valid) cull_box(g, (float)o.alpha_cut);
   return g;
 }
 
@@ -286,7 +344,7 @@ template <typename T>
 std::vector<int64_t> composite_order(const std::vector<PG<T>>& pg, const uint8_t* active) {
   std::vector<int64_t> idx;
   for (size_t i = 0; i < pg.size(); ++i)
-    if (pg[i].valid && (!active || active[i])) idx.push_back((int64_t)i);
+    if (pg[i].bin && (!active || active[i])) idx.push_back((int64_t)i);
   std::stable_sort(idx.begin(), idx.end(), [&](int64_t a, int64_t b) { return pg[a].depth < pg[b].depth; });
   return idx;
 }
@@ -339,7 +397,9 @@ inline void composite_pixel(const std::vector<PG<T>>& pg, const int64_t* list, s
   for (size_t j = 0; j < len; ++j) {
     if (tau < o.tau_stop) break;  // nothing composites once tau < tau_stop (render.py:261)
     const PG<T>& g = pg[(size_t)list[j]];
-    if (!(g.x0 <= x && x < g.x1 && g.y0 <= y && y < g.y1)) continue;  // oracles.py:36-38
+    // bbox gate (oracles.py:36-38); the culling box lies inside the bbox and only drops
+    // pixels that cannot reach alpha_cut, so gating with it changes no result
+    if (!(g.cx0 <= x && x < g.cx1 && g.cy0 <= y && y < g.cy1)) continue;
     ++k.E;
     const T alpha = pixel_alpha<T>(g, xs, ys, o.alpha_max);
     if (alpha >= o.alpha_cut && tau >= o.tau_stop) {
@@ -368,10 +428,10 @@ int64_t bin_tiles(const std::vector<PG<T>>& pg, const uint8_t* active, int W, in
   std::vector<std::pair<uint64_t, uint32_t>> pairs;
   for (size_t i = 0; i < pg.size(); ++i) {
     const PG<T>& g = pg[i];
-    if (!g.valid || (active && !active[i])) continue;
+    if (!g.bin || (active && !active[i])) continue;
     const uint64_t dk = depth_key((float)g.depth);
-    for (int ty = g.y0 / TILE; ty <= (g.y1 - 1) / TILE; ++ty)
-      for (int tx = g.x0 / TILE; tx <= (g.x1 - 1) / TILE; ++tx)
+    for (int ty = g.cy0 / TILE; ty <= (g.cy1 - 1) / TILE; ++ty)
+      for (int tx = g.cx0 / TILE; tx <= (g.cx1 - 1) / TILE; ++tx)
         pairs.emplace_back(((uint64_t)(ty * TW + tx) << 32) | dk, (uint32_t)i);
   }
   std::stable_sort(pairs.begin(), pairs.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
@@ -453,9 +513,9 @@ void render(const Scene<T>& s, const T* camp, const T* optp, const uint8_t* acti
       if (r0 >= r1) return;
       for (const int64_t g : order) {
         const PG<T>& q = pg[(size_t)g];
-        const int ty0 = std::max(q.y0 / TILE, r0), ty1 = std::min((q.y1 - 1) / TILE, r1 - 1);
+        const int ty0 = std::max(q.cy0 / TILE, r0), ty1 = std::min((q.cy1 - 1) / TILE, r1 - 1);
         for (int ty = ty0; ty <= ty1; ++ty)
-          for (int tx = q.x0 / TILE; tx <= (q.x1 - 1) / TILE; ++tx) lists[(size_t)ty * TW + tx].push_back(g);
+          for (int tx = q.cx0 / TILE; tx <= (q.cx1 - 1) / TILE; ++tx) lists[(size_t)ty * TW + tx].push_back(g);
       }
     });
     std::atomic<int> next(0);
@@ -509,7 +569,9 @@ void views(const Scene<T>& s, const T* cams, int64_t n_views, const T* optp, int
 struct ProjOut {
   uint8_t* valid; void *mx, *my, *a, *b, *c, *ia, *ib, *ic, *radius, *depth, *color, *opacity;
   int32_t *x0, *x1, *y0, *y1;
-  float *na, *nb, *nc;
+  float *na, *nb, *nc, *cut2;
+  int32_t *cx0, *cx1, *cy0, *cy1;
+  uint8_t* bin;
 };
 
 template <typename T>
@@ -524,7 +586,8 @@ void export_proj(const std::vector<PG<T>>& pg, ProjOut* po) {
     for (int c = 0; c < 3; ++c) ((T*)po->color)[3 * i + c] = g.color[c];
     ((T*)po->opacity)[i] = g.opacity;
     po->x0[i] = g.x0; po->x1[i] = g.x1; po->y0[i] = g.y0; po->y1[i] = g.y1;
-    po->na[i] = g.na; po->nb[i] = g.nb; po->nc[i] = g.nc;
+    po->na[i] = g.na; po->nb[i] = g.nb; po->nc[i] = g.nc; po->cut2[i] = g.cut2;
+    po->cx0[i] = g.cx0; po->cx1[i] = g.cx1; po->cy0[i] = g.cy0; po->cy1[i] = g.cy1; po->bin[i] = g.bin;
   }
 }
 
@@ -581,3 +644,6 @@ extern "C" void orc_exp_contract(const float* x, float* y, int64_t n) {
   for (int64_t i = 0; i < n; ++i) y[i] = exp_contract(x[i]);
 }
 extern "C" uint32_t orc_depth_key(float d) { return depth_key(d); }
+extern "C" void orc_log2_contract(const float* x, float* y, int64_t n) {
+  for (int64_t i = 0; i < n; ++i) y[i] = log2_contract(x[i]);
+}

@@ -30,7 +30,7 @@ def build(force: bool = False) -> Path:
 class ProjOut(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in (
         "valid", "mx", "my", "a", "b", "c", "ia", "ib", "ic", "radius", "depth", "color",
-        "opacity", "x0", "x1", "y0", "y1", "na", "nb", "nc")]
+        "opacity", "x0", "x1", "y0", "y1", "na", "nb", "nc", "cut2", "cx0", "cx1", "cy0", "cy1", "bin")]
 
 
 _lib = None
@@ -53,6 +53,7 @@ def lib():
             getattr(_lib, f"orc_views_{suf}").argtypes = [vp] * 5 + [i64, i32, vp, i64, vp, i32, i32, vp, vp, vp]
         _lib.orc_exp2_contract.argtypes = [vp, vp, i64]
         _lib.orc_exp_contract.argtypes = [vp, vp, i64]
+        _lib.orc_log2_contract.argtypes = [vp, vp, i64]
         _lib.orc_depth_key.argtypes = [C.c_float]
         _lib.orc_depth_key.restype = C.c_uint32
     return _lib
@@ -106,7 +107,9 @@ def project(scene, cam, opts=None, dtype=np.float32) -> dict:
     n = s.n
     out = dict(valid=np.zeros(n, np.uint8), x0=np.zeros(n, np.int32), x1=np.zeros(n, np.int32),
                y0=np.zeros(n, np.int32), y1=np.zeros(n, np.int32), color=np.zeros((n, 3), dtype),
-               na=np.zeros(n, np.float32), nb=np.zeros(n, np.float32), nc=np.zeros(n, np.float32))
+               na=np.zeros(n, np.float32), nb=np.zeros(n, np.float32), nc=np.zeros(n, np.float32),
+               cut2=np.zeros(n, np.float32), cx0=np.zeros(n, np.int32), cx1=np.zeros(n, np.int32),
+               cy0=np.zeros(n, np.int32), cy1=np.zeros(n, np.int32), bin=np.zeros(n, np.uint8))
     for k in ("mx", "my", "a", "b", "c", "ia", "ib", "ic", "radius", "depth", "opacity"):
         out[k] = np.zeros(n, dtype)
     po = ProjOut()
@@ -115,6 +118,7 @@ def project(scene, cam, opts=None, dtype=np.float32) -> dict:
     getattr(lib(), f"orc_project_{_suf(dtype)}")(*s.args(), _p(pack_camera(cam, dtype)),
                                                    _p(pack_options(opts, dtype)), C.byref(po))
     out["valid"] = out["valid"].astype(bool)
+    out["bin"] = out["bin"].astype(bool)
     return out
 
 
@@ -185,6 +189,13 @@ def exp_contract(x: np.ndarray) -> np.ndarray:
     x = np.ascontiguousarray(x, np.float32)
     y = np.empty_like(x)
     lib().orc_exp_contract(_p(x), _p(y), x.size)
+    return y
+
+
+def log2_contract(x: np.ndarray) -> np.ndarray:
+    x = np.ascontiguousarray(x, np.float32)
+    y = np.empty_like(x)
+    lib().orc_log2_contract(_p(x), _p(y), x.size)
     return y
 
 

@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(256) count_kernel(const uint32_t* __restrict__
   const uint32_t r = b * 256 + tid;
   uint32_t nt = 0;
   if (r < nvis) {
-    const int4 d = bbox_of(recs[items_sorted[r]].d);
+    const int4 d = cullbox_of(recs[items_sorted[r]].d);
     const int tx0 = d.x / kTile, tx1 = (d.y - 1) / kTile, ty0 = d.z / kTile, ty1 = (d.w - 1) / kTile;
     nt = (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
   }
@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ 
     s_off[i] = o;
     if (o < k1) {
       const uint32_t it = items_sorted[r0 + i];
-      const int4 d = bbox_of(recs[it].d);
+      const int4 d = cullbox_of(recs[it].d);
       const int tx0 = d.x / kTile, tx1 = (d.y - 1) / kTile;
       s_tx0[i] = (uint16_t)tx0; s_ty0[i] = (uint16_t)(d.z / kTile); s_tw[i] = (uint16_t)(tx1 - tx0 + 1);
       s_item[i] = it;

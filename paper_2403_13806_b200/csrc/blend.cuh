@@ -75,9 +75,8 @@ __global__ void __launch_bounds__(kBlendThreads) blend_kernel(
       const float4 c = __ldg(&R->c);
       if (COLOR || CONTRIB) s_rec[tid].c = c;
       gid = (uint32_t)__float_as_int(c.w);
-      // STATS counts the reference's bbox-gated evaluations; otherwise gate with the
-      // (smaller, exact-conservative) culling box
-      const int4 d = STATS ? bbox_of(__ldg(&R->d)) : cullbox_of(__ldg(&R->d));
+      // gate with the culling box: inside the bbox, and only pixels that can reach alpha_cut
+      const int4 d = cullbox_of(__ldg(&R->d));
       s_rec[tid].d = d;
       // bbox x sub-rectangle overlap: 2 column halves x 4 row quarters -> bit w = (w%2, w/2)
       const unsigned col = (d.x < ox + 8 && d.y > ox ? 1u : 0u) | (d.x < ox + 16 && d.y > ox + 8 ? 2u : 0u);

@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(128) project_kernel(const float* __restrict__ 
                                                       float* __restrict__ full, int4* __restrict__ full_bbox) {
   const uint32_t item = blockIdx.x * blockDim.x + threadIdx.x;
   if (item == 0) ctr->n_items = n_items;
-  bool valid = false;
+  bool valid = false, binned = false;
   if (item < n_items) {
     const int64_t i = active_idx ? (int64_t)__ldg(active_idx + item) : (int64_t)item;
     const float* P = planes + i;
@@ -173,54 +173,56 @@ __global__ void __launch_bounds__(128) project_kernel(const float* __restrict__ 
         op = __fdiv_rn(e, __fadd_rn(1.0f, e));
       }
       const float K = fbits(0xbf38aa3bu);  // -0.5*log2(e)
-      // conservative skip threshold: p2 < cut2 => alpha < alpha_cut
-      // (clamped at -126: p2 < -126 gives alpha < 2^-126 < alpha_cut whenever the fast
-      // blend path is used, i.e. alpha_cut >= 1e-30; the exact path ignores the clamp's effect
-      // only through the skip, which stays conservative)
-      float cut2 = o.alpha_cut > 0.0f ? __fsub_rn(log2f(o.alpha_cut / op), 1e-3f) : -INFINITY;
+      // conservative skip threshold: p2 < cut2 => alpha < alpha_cut; clamped at
+      // -126 (p2 < -126 gives alpha < 2^-126 < alpha_cut whenever alpha_cut >= 1e-30)
+      float cut2 = o.alpha_cut > 0.0f ? __fsub_rn(log2_contract(__fdiv_rn(o.alpha_cut, op)), 1e-3f) : -INFINITY;
       if (o.alpha_cut >= 1e-30f && cut2 < -126.0f) cut2 = -126.0f;
       Rec rec;
       rec.a = make_float4(mx, my, __fmul_rn(K, ia), __fmul_rn(__fmul_rn(2.0f, K), ib));
       rec.b = make_float4(__fmul_rn(K, ic), op, cut2, depth);
       rec.c = make_float4(col[0], col[1], col[2], __int_as_float((int)i));
-      // culling box: pixels whose centre lies outside the ellipse {p2 >= cut2}, widened by
-      // 1% + 0.5 px, cannot reach alpha_cut even with fp32 rounding of p2 (bounded by
-      // 6*2^-24*kappa*|cut2| for condition number kappa <= 1e4; worse-conditioned
-      // Gaussians keep the full bbox). Double precision: once per Gaussian.
+      // culling box (oracle: cull_box): pixels outside the ellipse {p2 >= cut2} widened by
+      // 1% + 0.5 px cannot reach alpha_cut even with the fp32 rounding of p2 (bounded for
+      // condition number <= 1e4; worse-conditioned Gaussians keep the full bbox). The tile
+      // binning uses this box; double precision, IEEE ops only (reproducible on the CPU).
       int cx0 = x0, cx1 = x1, cy0 = y0, cy1 = y1;
-      {
-        const double Na = __fmul_rn(K, ia), Nb = __fmul_rn(__fmul_rn(2.0f, K), ib), Nc = __fmul_rn(K, ic);
+      if (valid) {
+        const double Na = rec.a.z, Nb = rec.a.w, Nc = rec.b.x;
         const double C2 = cut2;
-        const double D = 4.0 * Na * Nc - Nb * Nb;
-        const double tr = Na + Nc, sq = sqrt((Na - Nc) * (Na - Nc) + Nb * Nb);
-        const double l1 = 0.5 * (tr - sq), l2 = 0.5 * (tr + sq);  // eigenvalues, both < 0 if definite
+        const double D = __dsub_rn(__dmul_rn(__dmul_rn(4.0, Na), Nc), __dmul_rn(Nb, Nb));
+        const double tr = __dadd_rn(Na, Nc);
+        const double sq = __dsqrt_rn(__dadd_rn(__dmul_rn(__dsub_rn(Na, Nc), __dsub_rn(Na, Nc)), __dmul_rn(Nb, Nb)));
+        const double l1 = __dmul_rn(0.5, __dsub_rn(tr, sq)), l2 = __dmul_rn(0.5, __dadd_rn(tr, sq));
         if (!(C2 < 0.0)) {
-          cx1 = cx0;  // opacity below alpha_cut (or cut2 = +inf): nothing can composite
+          cx1 = cx0;
           cy1 = cy0;
-        } else if (C2 > -1e30 && D > 0.0 && l2 < 0.0 && l1 >= 1e4 * l2) {
-          const double hx = sqrt(C2 * 4.0 * Nc / D) * 1.01 + 0.5, hy = sqrt(C2 * 4.0 * Na / D) * 1.01 + 0.5;
-          cx0 = max(x0, (int)fmax(floor((double)mx - hx - 0.5), -1.0));
-          cx1 = min(x1, (int)fmin(floor((double)mx + hx - 0.5) + 1.0, 65535.0));
-          cy0 = max(y0, (int)fmax(floor((double)my - hy - 0.5), -1.0));
-          cy1 = min(y1, (int)fmin(floor((double)my + hy - 0.5) + 1.0, 65535.0));
+        } else if (C2 > -1e30 && D > 0.0 && l2 < 0.0 && l1 >= __dmul_rn(1e4, l2)) {
+          const double hx = __dadd_rn(__dmul_rn(__dsqrt_rn(__ddiv_rn(__dmul_rn(__dmul_rn(C2, 4.0), Nc), D)), 1.01), 0.5);
+          const double hy = __dadd_rn(__dmul_rn(__dsqrt_rn(__ddiv_rn(__dmul_rn(__dmul_rn(C2, 4.0), Na), D)), 1.01), 0.5);
+          const double dmx = mx, dmy = my;
+          cx0 = max(x0, (int)fmax(floor(__dsub_rn(__dsub_rn(dmx, hx), 0.5)), -1.0));
+          cx1 = min(x1, (int)fmin(__dadd_rn(floor(__dsub_rn(__dadd_rn(dmx, hx), 0.5)), 1.0), 65535.0));
+          cy0 = max(y0, (int)fmax(floor(__dsub_rn(__dsub_rn(dmy, hy), 0.5)), -1.0));
+          cy1 = min(y1, (int)fmin(__dadd_rn(floor(__dsub_rn(__dadd_rn(dmy, hy), 0.5)), 1.0), 65535.0));
           if (cx1 < cx0) cx1 = cx0;
           if (cy1 < cy0) cy1 = cy0;
         }
       }
+      binned = valid && cx1 > cx0 && cy1 > cy0;
       rec.d = make_int4(x0 | (x1 << 16), y0 | (y1 << 16), cx0 | (cx1 << 16), cy0 | (cy1 << 16));
-      if (valid) recs[item] = rec;
+      if (binned) recs[item] = rec;
       if (FULL) {
         float4* f = reinterpret_cast<float4*>(full + 16 * (size_t)item);
         f[0] = make_float4(mx, my, a, b);
         f[1] = make_float4(c, ia, ib, ic);
         f[2] = make_float4(radius, depth, col[0], col[1]);
-        f[3] = make_float4(col[2], op, valid ? 1.0f : 0.0f, 0.0f);
+        f[3] = make_float4(col[2], op, valid ? 1.0f : 0.0f, cut2);
         full_bbox[item] = make_int4(x0, x1, y0, y1);
       }
     }
-    keys[item] = valid ? depth_key(depth) : kInvalidKey;
+    keys[item] = binned ? depth_key(depth) : kInvalidKey;
   }
-  const unsigned vb = __ballot_sync(0xffffffffu, valid);
+  const unsigned vb = __ballot_sync(0xffffffffu, binned);
   if ((threadIdx.x & 31) == 0 && vb) atomicAdd(&ctr->n_visible, (uint32_t)__popc(vb));
 }
 

@@ -75,6 +75,26 @@ __device__ __forceinline__ float exp_contract(float x) {
   return scale2(p, (int)n);
 }
 
+// log2(x) (oracle: log2_contract): fixes cut2, which fixes the culling box
+// that the tile binning uses -- hence reproducible add/mul/div/fma only.
+__device__ __forceinline__ float log2_contract(float x) {
+  if (x != x) return x;
+  if (x <= 0.0f) return -INFINITY;
+  if (x == INFINITY) return INFINITY;
+  if (x < 1.17549435e-38f) return -150.0f;
+  const uint32_t u = __float_as_uint(x);
+  int e = (int)((u >> 23) & 0xffu) - 127;
+  float m = __uint_as_float((u & 0x7fffffu) | 0x3f800000u);
+  if (m > 1.41421356f) { m = __fmul_rn(m, 0.5f); e += 1; }
+  const float t = __fdiv_rn(__fsub_rn(m, 1.0f), __fadd_rn(m, 1.0f));
+  const float t2 = __fmul_rn(t, t);
+  float p = __fmaf_rn(t2, 0.111111112f, 0.142857149f);
+  p = __fmaf_rn(p, t2, 0.200000003f);
+  p = __fmaf_rn(p, t2, 0.333333343f);
+  p = __fmaf_rn(p, t2, 1.0f);
+  return __fmaf_rn(__fmul_rn(t, p), 2.88539004f, (float)e);
+}
+
 // order-preserving 32-bit key of an fp32 depth (-0 folded into +0)
 __device__ __forceinline__ uint32_t depth_key(float d) {
   const uint32_t u = __float_as_uint(__fadd_rn(d, 0.0f));

@@ -86,9 +86,44 @@ def test_binning_structure(O):
     for t in range(len(ranges)):
         lst = vals[ranges[t, 0]:ranges[t, 1]]
         assert np.all(np.diff(rank[lst]) > 0)  # per-tile order = global order restricted
-    assert b["P"] == 13613  # configs[0] tile pairs (fp64 reference projection)
+    # the 3-sigma bboxes give SURVEY §6's configs[0] pair count; the binning uses the
+    # (exact-conservative) culling boxes inside them, so it emits fewer pairs
+    pr = O.project(scene, cam, opts, np.float32)
+    v = pr["valid"]
+    T = lambda a0, a1, b0, b1: ((a1 - 1) // 16 - a0 // 16 + 1) * ((b1 - 1) // 16 - b0 // 16 + 1)  # noqa: E731
+    assert int(T(pr["x0"][v], pr["x1"][v], pr["y0"][v], pr["y1"][v]).sum()) == 13613
+    bn = pr["bin"]
+    assert b["P"] == int(T(pr["cx0"][bn], pr["cx1"][bn], pr["cy0"][bn], pr["cy1"][bn]).sum()) < 13613
+    assert np.all(pr["cx0"][bn] >= pr["x0"][bn]) and np.all(pr["cx1"][bn] <= pr["x1"][bn])
     r = O.render(scene, cam, opts, np.float32)
-    assert r["E"] == 883773  # E_alg = 53.9 per pixel
+    r64 = O.render(scene, cam, opts, np.float64)
+    assert r64["E"] == 883773  # E_alg = 53.9 per pixel with the reference's bbox gate
+    assert r["E"] < r64["E"]     # culled evaluations only drop pixels that cannot composite
+
+
+def test_culling_box_is_conservative(O):
+    """No pixel outside a Gaussian's culling box reaches alpha_cut (checked exhaustively
+    over the 3-sigma bbox of every Gaussian of configs[0] and a ragged random scene)."""
+    for name in ("config0", "known"):
+        d = golden(name)
+        p = "cfg0_" if name == "config0" else "ragged_"
+        scene, cam, o = load_case(d, p)
+        opts = options_from(o)
+        pr = O.project(scene, cam, opts, np.float32)
+        for i in np.nonzero(pr["valid"])[0]:
+            ys, xs = np.mgrid[pr["y0"][i]:pr["y1"][i], pr["x0"][i]:pr["x1"][i]]
+            dx = (xs.astype(np.float32) + np.float32(0.5)) - pr["mx"][i]
+            dy = (ys.astype(np.float32) + np.float32(0.5)) - pr["my"][i]
+            p2 = pr["na"][i] * dx * dx + pr["nb"][i] * dy * dx + pr["nc"][i] * dy * dy  # fp32, close to contract
+            outside = ~((xs >= pr["cx0"][i]) & (xs < pr["cx1"][i]) & (ys >= pr["cy0"][i]) & (ys < pr["cy1"][i]))
+            alpha = pr["opacity"][i] * np.exp2(p2.astype(np.float64))
+            assert not np.any(outside & (alpha >= opts.alpha_cut * 0.999)), (name, i)
+
+
+def test_log2_contract(O):
+    x = np.float32(10.0) ** np.linspace(-37, 38, 200001).astype(np.float32)
+    y = O.log2_contract(x).astype(np.float64)
+    assert np.max(np.abs(y - np.log2(x.astype(np.float64)))) < 2e-5
 
 
 def test_exp_contract_accuracy(O):
