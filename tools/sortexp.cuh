@@ -1,88 +1,10 @@
-// sort.cuh -- hand-written stable LSD radix sort (onesweep, 8-bit digits).
-//
-// Replaces np.lexsort (render.py:218-222) twice per frame:
-//   * depth sort: 32-bit depth keys of all n items (culled = 0xffffffff, last),
-//     values = item index (implicit on the first pass), 4 passes;
-//   * tile sort:  16-bit tile ids of the P Gaussian-tile pairs emitted in
-//     (depth, index) order, values = item id, ceil(tile_bits/8) passes.
-// Stability makes the per-tile order exactly the reference's (depth, index)
-// order restricted to the tile.
-//
-// Digit histograms of every pass come from the key producer (radix_hist_kernel
-// for depth keys, emit_kernel for tile ids), so each pass is ONE kernel: CTAs
-// take chunks of 256*ITEMS keys in launch order from an atomic ticket, rank
-// keys inside the chunk with a warp multisplit (match_any for narrow digits,
-// per-bit ballots for 7-8 bit digits, whichever measured faster), publish
-// the chunk's digit counts right after loading (before ranking, so successors
-// never wait on it), get the chunk's global digit offsets by decoupled
-// look-back over earlier chunks (4 predecessors per load round), and scatter
-// through shared memory so global writes are contiguous runs per digit.
-// Keys and values are read once and written once per pass; sizes come from
-// device memory, so a frame has no host synchronization.
 #pragma once
-#include "rs_common.cuh"
-
+#include "../paper_2403_13806_b200/csrc/sort.cuh"
 namespace rs {
-
-constexpr int kSortThreads = 256;
-constexpr int kMinChunk = kSortThreads * 8;  // smallest chunk used (look-back region sizing)
-enum : uint32_t { kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kValMask = (1u << 30) - 1 };
-
-__device__ __forceinline__ uint32_t lanemask_lt() {
-  uint32_t m;
-  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
-  return m;
-}
-
-// Digit histograms of all passes of a 32-bit key sort (per-warp shared
-// sub-histograms), plus zeroing of the first pass's look-back words.
-// hist must be zero on entry.
-__global__ void __launch_bounds__(256) radix_hist_kernel(const uint32_t* __restrict__ keys, uint32_t n, int passes,
-                                                         uint32_t chunk, uint32_t* __restrict__ hist,
-                                                         uint32_t* __restrict__ lookback0) {
-  __shared__ uint32_t sh[8][4][256];
-  const int warp = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < 8 * 4 * 256; i += blockDim.x) (&sh[0][0][0])[i] = 0;
-  __syncthreads();
-  const uint32_t stride = gridDim.x * blockDim.x;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const uint32_t k = keys[i];
-    for (int p = 0; p < passes; ++p) atomicAdd(&sh[warp][p][(k >> (8 * p)) & 0xffu], 1u);
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < passes * 256; i += blockDim.x) {
-    uint32_t v = 0;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) v += (&sh[w][0][0])[i];
-    if (v) atomicAdd(&hist[i], v);
-  }
-  const uint32_t words = (n + chunk - 1) / chunk * 256u;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < words; i += stride) lookback0[i] = 0;
-}
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, uint32_t src_bytes) {
-  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
-
-template <typename K, int ITEMS>
-struct OnesweepSmem {
-  K keys[kSortThreads * ITEMS];
-  uint32_t vals[kSortThreads * ITEMS];
-  uint32_t vstage[kSortThreads * ITEMS];  // this chunk's values in input order (cp.async prefetch)
-  uint32_t whist[8][256];   // per-warp digit counts, then per-warp exclusive offsets
-  uint32_t gbase[256];      // global exclusive digit offsets of this pass
-  uint32_t lstart[256];     // chunk-local exclusive digit starts
-  uint32_t gout[256];       // global position of local slot 0 for each digit
-  uint32_t ccnt[256];       // this chunk's digit counts
-  uint32_t wsum[8];
-  uint32_t chunk;
-};
-
-// One pass over bits [shift, shift + NBITS), NBITS <= 8.
-template <typename K, int ITEMS, int NBITS>
-__global__ void __launch_bounds__(kSortThreads, 4) onesweep_kernel(
+// One pass over bits [shift, shift + NBITS), NBITS <= 8 (compile-time: the
+// per-bit ballots unroll into a straight SHF/VOTE/LOP3 sequence).
+template <typename K, int ITEMS, int NBITS, int MODE>
+__global__ void __launch_bounds__(kSortThreads, 4) exp_kernel(
     const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, K* __restrict__ keys_out,
     uint32_t* __restrict__ vals_out, const uint32_t* __restrict__ n_ptr, uint32_t n_static,
     const uint32_t* __restrict__ pass_hist, uint32_t* __restrict__ lookback, uint32_t* __restrict__ lookback_next,
@@ -149,7 +71,7 @@ __global__ void __launch_bounds__(kSortThreads, 4) onesweep_kernel(
   lb[c * 256 + tid] = (c == 0 ? (uint32_t)kFlagInc : (uint32_t)kFlagAgg) | cnt;
   // decoupled look-back for the exclusive prefix (LB predecessors per round trip)
   uint32_t excl = 0;
-  if (c > 0) {
+  if (c > 0 && !(MODE & 1)) {
     constexpr int LB = 4;
     int j = (int)c - 1;
     for (;;) {
@@ -177,13 +99,14 @@ __global__ void __launch_bounds__(kSortThreads, 4) onesweep_kernel(
   // warp multisplit ranking in key order (item-major, lane-minor)
 #pragma unroll
   for (int it = 0; it < ITEMS; ++it) {
+    if (MODE & 2) { rk[it] = it * 32 + lane; continue; }
     const uint32_t i = wbase + it * 32 + lane;
     const bool ok = i < n;
     const uint32_t d = (kk[it] >> shift) & dmask;
     uint32_t peers;
-    if (NBITS <= 6) {  // few distinct digits per warp: one MATCH is cheapest
+    if (MODE & 8) {
       peers = __match_any_sync(0xffffffffu, ok ? d : 0x100u + lane);
-    } else {           // many distinct digits: MATCH serialises, per-bit ballots do not
+    } else {
       peers = __ballot_sync(0xffffffffu, ok);
 #pragma unroll
       for (int b = 0; b < NBITS; ++b) {
@@ -191,12 +114,32 @@ __global__ void __launch_bounds__(kSortThreads, 4) onesweep_kernel(
         peers &= ((d >> b) & 1u) ? bal : ~bal;
       }
     }
+    if (MODE & 16) {
+      const int leader = 31 - __clz(peers);
+      uint32_t base = 0;
+      if (ok && leader == lane) base = atomicAdd(&S.whist[warp][d], (uint32_t)__popc(peers));
+      rk[it] = __popc(peers & lt) + (ok ? 0u : 0u);
+      kk[it] |= 0;  // keep
+      // broadcast deferred: store leader in rk high bits? use separate pass below
+      rk[it] = (rk[it] & 0xffffu) | ((uint32_t)leader << 16);
+      S.vals[it * 256 + tid] = base;  // temp: leader's base (vals array reused before scatter)
+    } else {
     uint32_t base = 0;
     if (ok) base = S.whist[warp][d];
     __syncwarp();
     if (ok && (31 - __clz(peers)) == lane) S.whist[warp][d] = base + __popc(peers);
     __syncwarp();
     rk[it] = base + __popc(peers & lt);
+    }
+  }
+  if (MODE & 16) {
+    __syncwarp();
+#pragma unroll
+    for (int it = 0; it < ITEMS; ++it) {
+      const uint32_t leader = rk[it] >> 16;
+      const uint32_t base = S.vals[it * 256 + warp * 32 + leader];
+      rk[it] = (rk[it] & 0xffffu) + base;
+    }
   }
   __syncthreads();
   {  // per digit: per-warp exclusive offsets
@@ -240,9 +183,10 @@ __global__ void __launch_bounds__(kSortThreads, 4) onesweep_kernel(
   for (uint32_t p = tid; p < m; p += kSortThreads) {
     const K k = S.keys[p];
     const uint32_t g = S.gout[((uint32_t)k >> shift) & dmask] + p;
+    if (MODE & 4) { if (g == 0xffffffffu) vals_out[0] = k; continue; }
     if (write_keys) keys_out[g] = k;
     vals_out[g] = S.vals[p];
   }
 }
 
-}  // namespace rs
+}
