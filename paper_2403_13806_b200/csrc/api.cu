@@ -38,7 +38,7 @@ Layout make_layout(int64_t n_cap, int64_t pair_cap, int W, int H) {
   auto take = [&](size_t bytes) { const size_t at = o; o = align_up(o + bytes); return at; };
   L.ctr = take(sizeof(Counters));
   L.hist = take(8 * 256 * sizeof(uint32_t));  // depth passes 0-3, tile passes 4-5
-  L.emit_lb = take(((size_t)n_cap / 256 + 1) * sizeof(unsigned long long));
+  L.emit_lb = take(((size_t)n_cap / kCountThreads + 2) * sizeof(unsigned long long));
   L.ranges = take(TW * TH * sizeof(uint2));
   L.frame_bytes = o;
   L.recs = take((size_t)n_cap * sizeof(Rec));
@@ -262,7 +262,7 @@ int32_t rs_bin(rs_workspace* ws, void* stream) {
                                     ws->at<uint32_t>(ws->L.keysB), nullptr, ws->at<uint32_t>(ws->L.valsA),
                                     ws->at<uint32_t>(ws->L.valsB), nullptr, n, n, 32, 0, 0, false, st, &keys_res,
                                     &items_sorted);
-    count_kernel<<<(n + 255) / 256, 256, 0, st>>>(items_sorted, ws->at<Rec>(ws->L.recs), ws->ctr(), ws->TW,
+    count_kernel<<<(n + kCountThreads - 1) / kCountThreads, kCountThreads, 0, st>>>(items_sorted, ws->at<Rec>(ws->L.recs), ws->ctr(), ws->TW,
                                                   (uint32_t)ws->pair_cap, ws->at<uint32_t>(ws->L.offsets),
                                                   ws->at<uint32_t>(ws->L.owners),
                                                   ws->at<unsigned long long>(ws->L.emit_lb));

@@ -11,7 +11,7 @@
 //
 // Two kernels, so that work is balanced over PAIRS, not Gaussians (near
 // Gaussians are both first in depth order and the largest on screen):
-//   count_kernel  one thread per depth rank: tile count, block scan, decoupled
+//   count_kernel  one thread per depth rank (1024-rank CTAs): tile count, block scan, decoupled
 //                 look-back (logical block ids from an atomic ticket) ->
 //                 exclusive pair offset per rank; total P.
 //   emit_kernel   one CTA per 2048 consecutive pairs: the owning ranks of the
@@ -27,6 +27,7 @@ namespace rs {
 
 enum : unsigned long long { kLbAgg = 1ull << 62, kLbInc = 2ull << 62, kLbMask = (1ull << 62) - 1 };
 constexpr int kEmitPairs = 2048;  // pairs per emit CTA
+constexpr int kCountThreads = 1024;  // ranks per count CTA (few CTAs: short look-back chains)
 
 // Decoupled look-back over 64-bit status words (flag in the top 2 bits);
 // one warp reads 32 predecessors per step.
@@ -34,37 +35,41 @@ __device__ __forceinline__ unsigned long long warp_lookback(volatile unsigned lo
   unsigned long long excl = 0;
   int j = (int)b - 1;
   while (j >= 0) {
-    const int k = j - lane;
-    unsigned long long s = k >= 0 ? st[k] : kLbInc;  // before block 0: an inclusive zero
-    const unsigned ready = __ballot_sync(0xffffffffu, (s & ~kLbMask) != 0);
-    if (ready != 0xffffffffu) continue;  // wait until the 32-wide window is published
-    const unsigned inc = __ballot_sync(0xffffffffu, (s & kLbInc) != 0);
-    const int first = __ffs(inc) - 1;  // nearest inclusive predecessor in the window (lane order = j, j-1, ...)
-    unsigned long long v = (inc && lane <= first) || !inc ? (s & kLbMask) : 0ull;
-    if (k < 0) v = 0;
+    const int k = j - lane;  // lane 0 = nearest predecessor
+    const unsigned long long s = k >= 0 ? st[k] : (unsigned long long)kLbInc;  // before block 0: inclusive zero
+    const unsigned ready = __ballot_sync(0xffffffffu, (s & ~(unsigned long long)kLbMask) != 0);
+    const unsigned inc = __ballot_sync(0xffffffffu, (s & (unsigned long long)kLbInc) != 0) & ready;
+    const unsigned notready = ~ready;
+    // use the window up to (and including) the nearest inclusive entry, or up to the first
+    // unpublished entry, whichever comes first
+    const int first_inc = inc ? __ffs(inc) - 1 : 32;
+    const int first_nr = notready ? __ffs(notready) - 1 : 32;
+    const int take = first_inc < first_nr ? first_inc + 1 : first_nr;  // lanes [0, take)
+    unsigned long long v = (lane < take && k >= 0) ? (s & (unsigned long long)kLbMask) : 0ull;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     excl += v;
-    if (inc) break;
-    j -= 32;
+    if (first_inc < first_nr) break;
+    j -= take;
   }
   return excl;
 }
 
-__global__ void __launch_bounds__(256) count_kernel(const uint32_t* __restrict__ items_sorted,
+__global__ void __launch_bounds__(kCountThreads) count_kernel(const uint32_t* __restrict__ items_sorted,
                                                     const Rec* __restrict__ recs, Counters* __restrict__ ctr, int TW,
                                                     uint32_t pair_cap, uint32_t* __restrict__ offsets,
                                                     uint32_t* __restrict__ chunk_owner,
                                                     unsigned long long* __restrict__ status) {
   __shared__ uint32_t s_block;
-  __shared__ uint32_t s_wsum[8];
+  __shared__ uint32_t s_wsum[kCountThreads / 32];
   __shared__ unsigned long long s_base;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) s_block = atomicAdd(&ctr->emit_ctr, 1u);
   __syncthreads();
   const uint32_t b = s_block;
   const uint32_t nvis = ctr->n_visible;
-  const uint32_t r = b * 256 + tid;
+  if (b * kCountThreads >= nvis && b > 0) return;  // no ranks here, and no later block needs this status
+  const uint32_t r = b * kCountThreads + tid;
   uint32_t nt = 0;
   if (r < nvis) {
     const int4 d = cullbox_of(recs[items_sorted[r]].d);
@@ -81,7 +86,7 @@ __global__ void __launch_bounds__(256) count_kernel(const uint32_t* __restrict__
   __syncthreads();
   uint32_t off = 0, total = 0;
 #pragma unroll
-  for (int w = 0; w < 8; ++w) {
+  for (int w = 0; w < kCountThreads / 32; ++w) {
     off += w < warp ? s_wsum[w] : 0u;
     total += s_wsum[w];
   }
@@ -92,7 +97,7 @@ __global__ void __launch_bounds__(256) count_kernel(const uint32_t* __restrict__
     if (lane == 0) {
       if (b) st[b] = kLbInc | (excl + total);
       s_base = excl;
-      if (nvis > 0 && b == (nvis - 1) / 256) {
+      if (nvis > 0 && b == (nvis - 1) / kCountThreads) {
         const unsigned long long end = excl + total;
         ctr->pairs_needed = end;
         ctr->n_pairs = (uint32_t)(end < pair_cap ? end : pair_cap);
@@ -121,10 +126,15 @@ __global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ 
   __shared__ uint32_t s_off[kEmitPairs + 1];
   __shared__ uint16_t s_tx0[kEmitPairs], s_ty0[kEmitPairs], s_tw[kEmitPairs];
   __shared__ uint32_t s_item[kEmitPairs];
-  __shared__ uint16_t s_tile_out[kEmitPairs];
-  __shared__ uint32_t s_item_out[kEmitPairs];
+  __shared__ __align__(16) uint16_t s_tile_out[kEmitPairs];
+  // s_start (owner start marks) and s_item_out share storage (a barrier separates the
+  // last mark read from the first item write)
+  __shared__ __align__(16) int s_start_item[kEmitPairs];
+  int* const s_start = s_start_item;
+  uint32_t* const s_item_out = reinterpret_cast<uint32_t*>(s_start_item);
   __shared__ uint32_t s_hist[2][256];
-  const int tid = threadIdx.x, lane = tid & 31;
+  __shared__ int s_wmax[8];
+  const int tid = threadIdx.x;
   const uint32_t P = ctr->n_pairs, nvis = ctr->n_visible;
   // zero the tile sort's first-pass look-back words
   const uint32_t lb_words = (P + sort_chunk - 1) / sort_chunk * 256u;
@@ -133,6 +143,7 @@ __global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ 
   if (k0 >= P) return;
   const uint32_t k1 = min(P, k0 + kEmitPairs);
   for (int i = tid; i < 512; i += 256) (&s_hist[0][0])[i] = 0;
+  for (int i = tid; i < kEmitPairs; i += 256) s_start[i] = -1;
   const uint32_t r0 = chunk_owner[blockIdx.x];
   // owners of [k0, k1): ranks r0 .. owner(k1 - 1) <= chunk_owner[next chunk]; at most k1 - k0 of them
   const uint32_t rlast = k1 < P ? chunk_owner[blockIdx.x + 1] : nvis - 1;
@@ -148,29 +159,67 @@ __global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ 
       s_item[i] = it;
     }
   }
-  if (tid == 0) s_off[nown] = 0xffffffffu;
   __syncthreads();
-  // each thread emits 8 consecutive pairs into shared memory: one binary search, then a forward walk
-  const uint32_t q0 = k0 + 8 * tid;
-  if (q0 < k1) {
-    uint32_t lo = 0, hi = nown - 1;
-    while (lo < hi) {
-      const uint32_t mid = (lo + hi + 1) >> 1;
-      if (s_off[mid] <= q0) lo = mid; else hi = mid - 1;
-    }
-    uint32_t j = lo;
+  // owner of every pair slot without a search: mark where each owner's pairs start in this
+  // CTA's window, then a block-wide running max carries the owner index forward
+  for (uint32_t i = tid; i < nown; i += 256) {
+    const uint32_t o = s_off[i];
+    if (o < k1) s_start[o > k0 ? o - k0 : 0] = (int)i;
+  }
+  __syncthreads();
+  const uint32_t q0 = 8 * tid;  // this thread's 8 consecutive pair slots
+  int own[8];
+  {  // two 128-bit shared loads per thread (no bank conflicts at an 8-word stride)
+    const int4 m0 = reinterpret_cast<const int4*>(s_start)[2 * tid];
+    const int4 m1 = reinterpret_cast<const int4*>(s_start)[2 * tid + 1];
+    own[0] = m0.x; own[1] = m0.y; own[2] = m0.z; own[3] = m0.w;
+    own[4] = m1.x; own[5] = m1.y; own[6] = m1.z; own[7] = m1.w;
+  }
+  int run = -1;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const uint32_t k = q0 + q;
-      if (k >= k1) break;
-      while (s_off[j + 1] <= k) ++j;
-      const uint32_t local = k - s_off[j];
-      const uint32_t tw = s_tw[j];
-      const uint32_t row = local / tw;
-      s_tile_out[8 * tid + q] = (uint16_t)((s_ty0[j] + row) * TW + s_tx0[j] + (local - row * tw));
-      s_item_out[8 * tid + q] = s_item[j];
+  for (int q = 0; q < 8; ++q) {
+    run = max(run, own[q]);
+    own[q] = run;
+  }
+  // exclusive max-scan of the per-thread last owner across the block
+  const int lane = tid & 31, warp = tid >> 5;
+  int x = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) x = max(x, __shfl_up_sync(0xffffffffu, x, o));
+  if (lane == 31) s_wmax[warp] = x;
+  __syncthreads();
+  int carry = __shfl_up_sync(0xffffffffu, x, 1);
+  if (lane == 0) carry = -1;
+  for (int w = 0; w < warp; ++w) carry = max(carry, s_wmax[w]);
+  uint32_t row = 0, col = 0, tw = 1;
+  int cur = -2;
+  uint32_t tl[8], itm[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const uint32_t k = k0 + q0 + q;
+    tl[q] = 0;
+    itm[q] = 0;
+    if (k < k1) {
+      const int j = max(own[q], carry);
+      if (j != cur) {  // new owner: one division, then walk the rectangle row-major
+        cur = j;
+        tw = s_tw[j];
+        const uint32_t local = k - s_off[j];
+        row = local / tw;
+        col = local - row * tw;
+      } else if (++col == tw) {
+        col = 0;
+        ++row;
+      }
+      tl[q] = (s_ty0[j] + row) * TW + s_tx0[j] + col;
+      itm[q] = s_item[j];
     }
   }
+  __syncthreads();  // all owner marks read before the aliased item slots are written
+  reinterpret_cast<uint4*>(s_tile_out)[tid] =
+      make_uint4(tl[0] | (tl[1] << 16), tl[2] | (tl[3] << 16), tl[4] | (tl[5] << 16), tl[6] | (tl[7] << 16));
+  reinterpret_cast<uint4*>(s_item_out)[2 * tid] = make_uint4(itm[0], itm[1], itm[2], itm[3]);
+  reinterpret_cast<uint4*>(s_item_out)[2 * tid + 1] = make_uint4(itm[4], itm[5], itm[6], itm[7]);
   __syncthreads();
   // coalesced copy-out + digit histograms of the tile sort (uniform trip count: full-warp votes)
   const uint32_t npair = k1 - k0;
