@@ -134,6 +134,9 @@ RS_API int32_t rs_workspace_create(void* device_mem, size_t bytes, int64_t n_cap
 RS_API void rs_workspace_destroy(rs_workspace* ws);
 
 /* One full frame: project -> depth sort -> tile binning -> blend.
+ *   cam:        HOST pointer, uploaded with rs_set_camera; NULL reuses the camera
+ *               of the last rs_set_camera -- capture rs_render(cam = NULL) into a
+ *               CUDA graph and call rs_set_camera before each replay.
  *   active_idx: optional ascending list of m scene indices (filtered render:
  *               only listed Gaussians are projected); NULL = all scene->n.
  *   out_rgb (H*W*3), out_alpha, out_depth (H*W), out_count (H*W int32): may
@@ -144,6 +147,10 @@ RS_API void rs_workspace_destroy(rs_workspace* ws);
 RS_API int32_t rs_render(rs_workspace* ws, const rs_scene* scene, const int32_t* active_idx, int64_t m, const rs_camera* cam,
                   const rs_options* opts, float* out_rgb, float* out_alpha, float* out_depth, int32_t* out_count,
                   uint32_t* scores, uint32_t flags, void* stream);
+
+/* Stream-ordered camera upload into the workspace (also fixes the image size of
+ * the following frames); `cam` may be reused as soon as the call returns. */
+RS_API int32_t rs_set_camera(rs_workspace* ws, const rs_camera* cam, void* stream);
 
 /* Stages of rs_render, callable separately (same workspace state machine). */
 RS_API int32_t rs_project(rs_workspace* ws, const rs_scene* scene, const int32_t* active_idx, int64_t m, const rs_camera* cam,

@@ -72,6 +72,7 @@ SIGNATURES = {
     "rs_project_full": (_i32, [_vp, C.POINTER(RsScene), _vp, _i64, C.POINTER(RsCamera), C.POINTER(RsOptions),
                                _vp, _vp, _vp]),
     "rs_bin": (_i32, [_vp, _vp]),
+    "rs_set_camera": (_i32, [_vp, C.POINTER(RsCamera), _vp]),
     "rs_blend": (_i32, [_vp, C.POINTER(RsOptions), _vp, _vp, _vp, _vp, _vp, _u32, _vp]),
     "rs_read_stats": (_i32, [_vp, C.POINTER(RsStats), _vp]),
     "rs_get_buffers": (_i32, [_vp, C.POINTER(RsBuffers)]),

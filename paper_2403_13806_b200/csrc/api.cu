@@ -26,7 +26,7 @@ size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 struct Layout {
   // per-frame zeroed region [0, frame_bytes)
   size_t ctr, hist, emit_lb, ranges, frame_bytes;
-  size_t recs, keysA, keysB, valsA, valsB, offsets, owners, ptileA, ptileB, pitemA, pitemB, lbA, lbB, total;
+  size_t cam, recs, keysA, keysB, valsA, valsB, offsets, owners, ptileA, ptileB, pitemA, pitemB, lbA, lbB, total;
 };
 
 int tiles_x(int w) { return (w + kTile - 1) / kTile; }
@@ -41,6 +41,7 @@ Layout make_layout(int64_t n_cap, int64_t pair_cap, int W, int H) {
   L.emit_lb = take(((size_t)n_cap / kCountThreads + 2) * sizeof(unsigned long long));
   L.ranges = take(TW * TH * sizeof(uint2));
   L.frame_bytes = o;
+  L.cam = take(sizeof(rs_camera));
   L.recs = take((size_t)n_cap * sizeof(Rec));
   L.keysA = take((size_t)n_cap * 4);
   L.keysB = take((size_t)n_cap * 4);
@@ -72,7 +73,7 @@ struct rs_workspace {
   uint32_t n_items;
   int W, H, TW, TH;
   int tile_bits, tile_passes;
-  bool binned;
+  bool binned, have_cam;
 
   template <typename T> T* at(size_t off) const { return reinterpret_cast<T*>(base + off); }
   Counters* ctr() const { return at<Counters>(L.ctr); }
@@ -198,21 +199,10 @@ int32_t rs_workspace_create(void* device_mem, size_t bytes, int64_t n_cap, int64
 
 void rs_workspace_destroy(rs_workspace* ws) { delete ws; }
 
-static int32_t project_impl(rs_workspace* ws, const rs_scene* scene, const int32_t* active_idx, int64_t m,
-                            const rs_camera* cam, const rs_options* opts, float* full, int32_t* full_bbox,
-                            void* stream) {
-  if (!ws || !scene || !cam || !opts || !scene->planes || scene->sh_degree < 0 || scene->sh_degree > 3 ||
-      scene->n < 0 || scene->plane_stride < scene->n)
-    return RS_EINVAL;
-  const int64_t items = active_idx ? m : scene->n;
-  if (items < 0 || items > ws->n_cap || cam->width <= 0 || cam->height <= 0 || cam->width > ws->W_cap ||
-      cam->height > ws->H_cap)
-    return items > ws->n_cap ? RS_ENOMEM_WORKSPACE : RS_EINVAL;
+int32_t rs_set_camera(rs_workspace* ws, const rs_camera* cam, void* stream) {
+  if (!ws || !cam || cam->width <= 0 || cam->height <= 0) return RS_EINVAL;
+  if (cam->width > ws->W_cap || cam->height > ws->H_cap) return RS_ENOMEM_WORKSPACE;
   const int TW = tiles_x(cam->width), TH = tiles_x(cam->height);
-  if ((int64_t)(TW + 1) * (TH + 1) > (int64_t)(tiles_x(ws->W_cap) + 1) * (tiles_x(ws->H_cap) + 1))
-    return RS_ENOMEM_WORKSPACE;
-  cudaStream_t st = S(stream);
-  ws->n_items = (uint32_t)items;
   ws->W = cam->width;
   ws->H = cam->height;
   ws->TW = TW;
@@ -220,18 +210,42 @@ static int32_t project_impl(rs_workspace* ws, const rs_scene* scene, const int32
   ws->tile_bits = 1;
   while ((1 << ws->tile_bits) < TW * TH) ++ws->tile_bits;
   ws->tile_passes = (ws->tile_bits + 7) / 8;
-  ws->binned = false;
-  // zero counters, histograms, difference array and emit look-back in one memset
+  ws->have_cam = true;
+  // stream-ordered upload; from pageable memory the driver stages it at once, so the
+  // caller may reuse `cam` immediately (a captured frame graph then replays it)
+  cudaMemcpyAsync(ws->at<rs_camera>(ws->L.cam), cam, sizeof(rs_camera), cudaMemcpyHostToDevice, S(stream));
+  return cuda_status();
+}
+
+static int32_t project_impl(rs_workspace* ws, const rs_scene* scene, const int32_t* active_idx, int64_t m,
+                            const rs_camera* cam, const rs_options* opts, float* full, int32_t* full_bbox,
+                            void* stream) {
+  if (!ws || !scene || !opts || !scene->planes || scene->sh_degree < 0 || scene->sh_degree > 3 ||
+      scene->n < 0 || scene->plane_stride < scene->n)
+    return RS_EINVAL;
+  const int64_t items = active_idx ? m : scene->n;
+  if (items < 0) return RS_EINVAL;
+  if (items > ws->n_cap) return RS_ENOMEM_WORKSPACE;
+  cudaStream_t st = S(stream);
+  // zero counters, histograms, ranges and emit look-back in one memset
   cudaMemsetAsync(ws->base, 0, ws->L.frame_bytes, st);
+  if (cam) {
+    const int32_t s = rs_set_camera(ws, cam, stream);
+    if (s != RS_OK) return s;
+  } else if (!ws->have_cam) {
+    return RS_EINVAL;  // cam == NULL reuses the camera of the last rs_set_camera
+  }
+  ws->n_items = (uint32_t)items;
+  ws->binned = false;
   if (items > 0) {
     const unsigned grid = (unsigned)((items + 127) / 128);
     if (full)
       project_kernel<true><<<grid, 128, 0, st>>>(
-          scene->planes, scene->plane_stride, scene->sh_degree, active_idx, (uint32_t)items, *cam, *opts,
+          scene->planes, scene->plane_stride, scene->sh_degree, active_idx, (uint32_t)items, ws->at<rs_camera>(ws->L.cam), *opts,
           ws->at<Rec>(ws->L.recs), ws->at<uint32_t>(ws->L.keysA), ws->ctr(), full, reinterpret_cast<int4*>(full_bbox));
     else
       project_kernel<false><<<grid, 128, 0, st>>>(
-          scene->planes, scene->plane_stride, scene->sh_degree, active_idx, (uint32_t)items, *cam, *opts,
+          scene->planes, scene->plane_stride, scene->sh_degree, active_idx, (uint32_t)items, ws->at<rs_camera>(ws->L.cam), *opts,
           ws->at<Rec>(ws->L.recs), ws->at<uint32_t>(ws->L.keysA), ws->ctr(), nullptr, nullptr);
   }
   return cuda_status();

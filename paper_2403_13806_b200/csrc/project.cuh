@@ -39,11 +39,15 @@ __device__ __forceinline__ int ceil1_clip(float v, int hi) {
 template <bool FULL>
 __global__ void __launch_bounds__(128) project_kernel(const float* __restrict__ planes, int64_t stride, int deg,
                                                       const int32_t* __restrict__ active_idx, uint32_t n_items,
-                                                      rs_camera cam, rs_options o, Rec* __restrict__ recs,
+                                                      const rs_camera* __restrict__ camp, rs_options o,
+                                                      Rec* __restrict__ recs,
                                                       uint32_t* __restrict__ keys, Counters* __restrict__ ctr,
                                                       float* __restrict__ full, int4* __restrict__ full_bbox) {
   const uint32_t item = blockIdx.x * blockDim.x + threadIdx.x;
   if (item == 0) ctr->n_items = n_items;
+  // the camera lives in device memory (uploaded by a stream-ordered copy), so a captured
+  // CUDA graph of the frame replays with a new camera without re-instantiation
+  const rs_camera cam = *camp;
   bool valid = false, binned = false;
   if (item < n_items) {
     const int64_t i = active_idx ? (int64_t)__ldg(active_idx + item) : (int64_t)item;

@@ -223,6 +223,16 @@ class Renderer:
                 scores.copy_(snapshot)
         raise N.PairOverflow("tile pair capacity could not be satisfied")
 
+    def capture(self, ds: DeviceScene, cam, opts, *, color: bool = True, scores: torch.Tensor | None = None,
+                active_idx: torch.Tensor | None = None, pairs_hint: int | None = None) -> FrameGraph:
+        """Capture one frame into a CUDA graph (workspace sized first, no overflow check at
+        replay time: size it with ``pairs_hint`` or a checked ``render`` beforehand)."""
+        items = ds.n if active_idx is None else int(active_idx.numel())
+        self.ensure(items, max(self.caps[1], pairs_hint or 0, 1 << 16), int(cam.width), int(cam.height))
+        out = self.alloc_outputs(cam, color)
+        torch.cuda.synchronize(self.device)
+        return FrameGraph(self, ds, cam, opts, out, scores, active_idx, items)
+
     def project_full(self, ds: DeviceScene, cam, opts) -> tuple[np.ndarray, np.ndarray]:
         """ProjectedGaussian fields for every Gaussian (render.py:161-211)."""
         self.ensure(ds.n, self.caps[1] or (1 << 16), int(cam.width), int(cam.height))
@@ -245,6 +255,47 @@ class Renderer:
         N.check(fn(flags.data_ptr() if n else None, n, idx.data_ptr(), cnt.data_ptr(), scratch.data_ptr(),
                    scratch.numel(), self.stream), "compact")
         return idx[:int(cnt.item())]
+
+
+class FrameGraph:
+    """One frame (rs_render) captured into a CUDA graph.
+
+    The camera lives in the workspace (``rs_set_camera``, a stream-ordered copy
+    enqueued before each replay), so ``replay(cam)`` renders a new view without
+    re-capture: the whole frame (memset and ~12 kernels) is one graph launch.
+    """
+
+    def __init__(self, r: "Renderer", ds: DeviceScene, cam, opts, out: dict, scores=None,
+                 active_idx=None, m: int = 0):
+        self.r, self.ds, self.out, self.scores = r, ds, out, scores
+        self.buf = r.buf
+        self.width, self.height = int(cam.width), int(cam.height)
+        self.opt_s = options_struct(opts)
+        ptr = lambda k: out[k].data_ptr() if k in out else None  # noqa: E731
+        self.set_camera(cam)
+        side = torch.cuda.Stream(r.device)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.device(r.device):
+            side.wait_stream(torch.cuda.current_stream(r.device))
+            with torch.cuda.graph(self.graph, stream=side):
+                N.check(r.lib.rs_render(
+                    r.handle, C.byref(ds.struct), active_idx.data_ptr() if active_idx is not None else None,
+                    int(m), None, C.byref(self.opt_s), ptr("rgb"), ptr("alpha"), ptr("depth"), ptr("count"),
+                    scores.data_ptr() if scores is not None else None, 0, side.cuda_stream), "render(capture)")
+
+    def set_camera(self, cam) -> None:
+        if int(cam.width) != self.width or int(cam.height) != self.height:
+            raise InvalidParameterError("a captured frame graph is bound to its image size")
+        cs = camera_struct(cam)
+        N.check(self.r.lib.rs_set_camera(self.r.handle, C.byref(cs), self.r.stream), "set_camera")
+
+    def replay(self, cam=None) -> None:
+        """Enqueue the frame (optionally after uploading a new camera) on the current stream."""
+        if self.r.buf is not self.buf:
+            raise RuntimeError("the workspace was re-allocated after capture; capture again")
+        if cam is not None:
+            self.set_camera(cam)
+        self.graph.replay()
 
 
 _renderers: dict = {}
