@@ -177,7 +177,7 @@ int32_t rs_workspace_create(void* device_mem, size_t bytes, int64_t n_cap, int64
       width <= 0 || height <= 0)
     return RS_EINVAL;
   const int TW = tiles_x(width), TH = tiles_x(height);
-  if ((int64_t)TW * TH > 65536) return RS_EINVAL;
+  if ((int64_t)TW * TH > 65536 || width > 32767 || height > 32767) return RS_EINVAL;  // 15-bit box fields
   const Layout L = make_layout(n_cap, pair_cap, width, height);
   if (bytes < L.total) return RS_ENOMEM_WORKSPACE;
   rs_workspace* ws = new (std::nothrow) rs_workspace();

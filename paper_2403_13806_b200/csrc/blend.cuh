@@ -76,6 +76,7 @@ __global__ void __launch_bounds__(kBlendThreads) blend_kernel(
       if (COLOR || CONTRIB) s_rec[tid].c = c;
       gid = (uint32_t)__float_as_int(c.w);
       // gate with the culling box: inside the bbox, and only pixels that can reach alpha_cut
+      // (skipping the per-pixel test for "tight" boxes measured slower: the test is cheap ALU)
       const int4 d = cullbox_of(__ldg(&R->d));
       s_rec[tid].d = d;
       // bbox x sub-rectangle overlap: 2 column halves x 4 row quarters -> bit w = (w%2, w/2)

@@ -190,6 +190,7 @@ __global__ void __launch_bounds__(128) project_kernel(const float* __restrict__ 
       // condition number <= 1e4; worse-conditioned Gaussians keep the full bbox). The tile
       // binning uses this box; double precision, IEEE ops only (reproducible on the CPU).
       int cx0 = x0, cx1 = x1, cy0 = y0, cy1 = y1;
+      bool tight = false;  // box derived from the ellipse: outside it p2 < cut2 is guaranteed
       if (valid) {
         const double Na = rec.a.z, Nb = rec.a.w, Nc = rec.b.x;
         const double C2 = cut2;
@@ -204,16 +205,25 @@ __global__ void __launch_bounds__(128) project_kernel(const float* __restrict__ 
           const double hx = __dadd_rn(__dmul_rn(__dsqrt_rn(__ddiv_rn(__dmul_rn(__dmul_rn(C2, 4.0), Nc), D)), 1.01), 0.5);
           const double hy = __dadd_rn(__dmul_rn(__dsqrt_rn(__ddiv_rn(__dmul_rn(__dmul_rn(C2, 4.0), Na), D)), 1.01), 0.5);
           const double dmx = mx, dmy = my;
-          cx0 = max(x0, (int)fmax(floor(__dsub_rn(__dsub_rn(dmx, hx), 0.5)), -1.0));
-          cx1 = min(x1, (int)fmin(__dadd_rn(floor(__dsub_rn(__dadd_rn(dmx, hx), 0.5)), 1.0), 65535.0));
-          cy0 = max(y0, (int)fmax(floor(__dsub_rn(__dsub_rn(dmy, hy), 0.5)), -1.0));
-          cy1 = min(y1, (int)fmin(__dadd_rn(floor(__dsub_rn(__dadd_rn(dmy, hy), 0.5)), 1.0), 65535.0));
+          const int ex0 = (int)fmax(floor(__dsub_rn(__dsub_rn(dmx, hx), 0.5)), -1.0);
+          const int ex1 = (int)fmin(__dadd_rn(floor(__dsub_rn(__dadd_rn(dmx, hx), 0.5)), 1.0), 65535.0);
+          const int ey0 = (int)fmax(floor(__dsub_rn(__dsub_rn(dmy, hy), 0.5)), -1.0);
+          const int ey1 = (int)fmin(__dadd_rn(floor(__dsub_rn(__dadd_rn(dmy, hy), 0.5)), 1.0), 65535.0);
+          cx0 = max(x0, ex0);
+          cx1 = min(x1, ex1);
+          cy0 = max(y0, ey0);
+          cy1 = min(y1, ey1);
+          // the ellipse box is the binding bound on every side (or that side is the image edge):
+          // then no pixel outside the culling box can composite, bbox gate included
+          tight = (ex0 >= x0 || x0 == 0) && (ex1 <= x1 || x1 == cam.width) && (ey0 >= y0 || y0 == 0) &&
+                  (ey1 <= y1 || y1 == cam.height);
           if (cx1 < cx0) cx1 = cx0;
           if (cy1 < cy0) cy1 = cy0;
         }
       }
       binned = valid && cx1 > cx0 && cy1 > cy0;
-      rec.d = make_int4(x0 | (x1 << 16), y0 | (y1 << 16), cx0 | (cx1 << 16), cy0 | (cy1 << 16));
+      rec.d = make_int4(x0 | (x1 << 16), y0 | (y1 << 16), cx0 | (cx1 << 16) | (tight ? (int)0x80000000 : 0),
+                        cy0 | (cy1 << 16));
       if (binned) recs[item] = rec;
       if (FULL) {
         float4* f = reinterpret_cast<float4*>(full + 16 * (size_t)item);

@@ -17,7 +17,7 @@ constexpr int kPlanes = 59;
 //   a = {mean x, mean y, na, nb}   na,nb,nc = -0.5*log2(e) * (ia, 2*ib, ic)
 //   b = {nc, opacity, cut2, depth} cut2: log2 power below which alpha < alpha_cut
 //   c = {r, g, b, gid bits}        gid = scene index (for importance scatter)
-//   d = {x0 | x1<<16, y0 | y1<<16, cx0 | cx1<<16, cy0 | cy1<<16}
+//   d = {x0 | x1<<16, y0 | y1<<16, cx0 | cx1<<16 | tight<<31, cy0 | cy1<<16}
 //       [x0,x1)x[y0,y1): the half-open 3-sigma pixel bbox of render.py:133-137;
 //       [cx0,cx1)x[cy0,cy1): a sub-box outside which no pixel can reach
 //       alpha >= alpha_cut (culling only -- never changes a result, §4 DESIGN.md)
@@ -30,7 +30,12 @@ static_assert(sizeof(Rec) == 64, "record must be 64 B");
 __device__ __forceinline__ int lo16(int v) { return v & 0xffff; }
 __device__ __forceinline__ int hi16(int v) { return (int)((unsigned)v >> 16); }
 __device__ __forceinline__ int4 bbox_of(const int4 d) { return make_int4(lo16(d.x), hi16(d.x), lo16(d.y), hi16(d.y)); }
-__device__ __forceinline__ int4 cullbox_of(const int4 d) { return make_int4(lo16(d.z), hi16(d.z), lo16(d.w), hi16(d.w)); }
+// culling box; bit 31 of d.z flags a box derived from the ellipse (then every pixel
+// outside it has p2 < cut2, so a per-pixel box test is redundant)
+__device__ __forceinline__ int4 cullbox_of(const int4 d) {
+  return make_int4(lo16(d.z), hi16(d.z) & 0x7fff, lo16(d.w), hi16(d.w));
+}
+__device__ __forceinline__ bool cullbox_tight(const int4 d) { return d.z < 0; }
 
 // Device-side counters, mirrors rs_stats (first four words) + sort bookkeeping.
 struct Counters {
