@@ -60,16 +60,19 @@ enum {
   RS_EOVERFLOW = 5          /* more tile pairs than the workspace's pair capacity */
 };
 
-/* Scene in device memory: 59 planes of `plane_stride` floats each
- *   planes 0-2  positions x,y,z          (core.py:478)
- *   plane  3    opacity logit            (core.py:479; opacity = sigmoid)
- *   planes 4-6  log scales x,y,z         (core.py:481; scale = exp)
- *   planes 7-10 quaternion w,x,y,z       (core.py:482; normalized on device)
- *   planes 11-58 SH coefficient [c][b] at plane 11 + 16*c + b (core.py:480,
- *               channel-major (N,3,16)); only 11 + 16*c + b < 11+16*c+nb read.
+/* Scene in device memory (236 B per Gaussian):
+ *   planes: 11 planes of `plane_stride` floats (coalesced per-plane loads)
+ *     planes 0-2  positions x,y,z          (core.py:478)
+ *     plane  3    opacity logit            (core.py:479; opacity = sigmoid)
+ *     planes 4-6  log scales x,y,z         (core.py:481; scale = exp)
+ *     planes 7-10 quaternion w,x,y,z       (core.py:482; normalized on device)
+ *   sh: n rows of 48 floats, [c][b] at 16*c + b (core.py:480, channel-major
+ *     (N,3,16)); each row is read with 128-bit loads, only for visible
+ *     Gaussians of frames that produce colour. 16-byte aligned.
  */
 typedef struct rs_scene {
   const float* planes;
+  const float* sh;
   int64_t n;
   int64_t plane_stride;
   int32_t sh_degree; /* 0..3 */
@@ -178,7 +181,7 @@ RS_API int32_t rs_compact(const uint8_t* flags, int64_t n, int32_t* out_idx, uin
 RS_API int32_t rs_compact_bits(const uint8_t* bits, int64_t n, int32_t* out_idx, uint32_t* out_count, void* scratch,
                         size_t scratch_bytes, void* stream);
 
-/* *out_bad (device) = number of non-finite values over all 59 planes (0 = finite). */
+/* *out_bad (device) = number of non-finite scene values (planes and SH rows; 0 = finite). */
 RS_API int32_t rs_check_finite(const rs_scene* scene, uint32_t* out_bad, void* stream);
 
 /* dst[i] = max(dst[i], src[i]) over n non-negative floats. */

@@ -31,7 +31,7 @@ class PairOverflow(RuntimeError):
 
 
 class RsScene(C.Structure):
-    _fields_ = [("planes", C.c_void_p), ("n", C.c_int64), ("plane_stride", C.c_int64),
+    _fields_ = [("planes", C.c_void_p), ("sh", C.c_void_p), ("n", C.c_int64), ("plane_stride", C.c_int64),
                 ("sh_degree", C.c_int32), ("_pad", C.c_int32)]
 
 

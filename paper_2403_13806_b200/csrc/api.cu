@@ -73,7 +73,7 @@ struct rs_workspace {
   uint32_t n_items;
   int W, H, TW, TH;
   int tile_bits, tile_passes;
-  bool binned, have_cam;
+  bool binned, have_cam, has_color;
 
   template <typename T> T* at(size_t off) const { return reinterpret_cast<T*>(base + off); }
   Counters* ctr() const { return at<Counters>(L.ctr); }
@@ -219,9 +219,9 @@ int32_t rs_set_camera(rs_workspace* ws, const rs_camera* cam, void* stream) {
 
 static int32_t project_impl(rs_workspace* ws, const rs_scene* scene, const int32_t* active_idx, int64_t m,
                             const rs_camera* cam, const rs_options* opts, float* full, int32_t* full_bbox,
-                            void* stream) {
-  if (!ws || !scene || !opts || !scene->planes || scene->sh_degree < 0 || scene->sh_degree > 3 ||
-      scene->n < 0 || scene->plane_stride < scene->n)
+                            bool color, void* stream) {
+  if (!ws || !scene || !opts || !scene->planes || !scene->sh || scene->sh_degree < 0 || scene->sh_degree > 3 ||
+      scene->n < 0 || scene->plane_stride < scene->n || (reinterpret_cast<uintptr_t>(scene->sh) & 15))
     return RS_EINVAL;
   const int64_t items = active_idx ? m : scene->n;
   if (items < 0) return RS_EINVAL;
@@ -237,15 +237,16 @@ static int32_t project_impl(rs_workspace* ws, const rs_scene* scene, const int32
   }
   ws->n_items = (uint32_t)items;
   ws->binned = false;
+  ws->has_color = color || full;
   if (items > 0) {
     const unsigned grid = (unsigned)((items + 127) / 128);
     if (full)
-      project_kernel<true><<<grid, 128, 0, st>>>(
-          scene->planes, scene->plane_stride, scene->sh_degree, active_idx, (uint32_t)items, ws->at<rs_camera>(ws->L.cam), *opts,
+      project_kernel<true, true><<<grid, 128, 0, st>>>(
+          scene->planes, scene->sh, scene->plane_stride, scene->sh_degree, active_idx, (uint32_t)items, ws->at<rs_camera>(ws->L.cam), *opts,
           ws->at<Rec>(ws->L.recs), ws->at<uint32_t>(ws->L.keysA), ws->ctr(), full, reinterpret_cast<int4*>(full_bbox));
     else
-      project_kernel<false><<<grid, 128, 0, st>>>(
-          scene->planes, scene->plane_stride, scene->sh_degree, active_idx, (uint32_t)items, ws->at<rs_camera>(ws->L.cam), *opts,
+      (color ? project_kernel<false, true> : project_kernel<false, false>)<<<grid, 128, 0, st>>>(
+          scene->planes, scene->sh, scene->plane_stride, scene->sh_degree, active_idx, (uint32_t)items, ws->at<rs_camera>(ws->L.cam), *opts,
           ws->at<Rec>(ws->L.recs), ws->at<uint32_t>(ws->L.keysA), ws->ctr(), nullptr, nullptr);
   }
   return cuda_status();
@@ -253,14 +254,14 @@ static int32_t project_impl(rs_workspace* ws, const rs_scene* scene, const int32
 
 int32_t rs_project(rs_workspace* ws, const rs_scene* scene, const int32_t* active_idx, int64_t m,
                    const rs_camera* cam, const rs_options* opts, void* stream) {
-  return project_impl(ws, scene, active_idx, m, cam, opts, nullptr, nullptr, stream);
+  return project_impl(ws, scene, active_idx, m, cam, opts, nullptr, nullptr, true, stream);
 }
 
 int32_t rs_project_full(rs_workspace* ws, const rs_scene* scene, const int32_t* active_idx, int64_t m,
                         const rs_camera* cam, const rs_options* opts, float* out_proj, int32_t* out_bbox,
                         void* stream) {
   if (!out_proj || !out_bbox) return RS_EINVAL;
-  return project_impl(ws, scene, active_idx, m, cam, opts, out_proj, out_bbox, stream);
+  return project_impl(ws, scene, active_idx, m, cam, opts, out_proj, out_bbox, true, stream);
 }
 
 int32_t rs_bin(rs_workspace* ws, void* stream) {
@@ -309,6 +310,7 @@ int32_t rs_blend(rs_workspace* ws, const rs_options* opts, float* out_rgb, float
                  int32_t* out_count, uint32_t* scores, uint32_t flags, void* stream) {
   if (!ws || !opts || !ws->binned) return RS_EINVAL;
   const bool color = out_rgb != nullptr;
+  if (color && !ws->has_color) return RS_EINVAL;  // projected by a score-only rs_render
   if (color && (!out_alpha || !out_depth || !out_count)) return RS_EINVAL;
   if (!color && !scores) return RS_EINVAL;
   const bool stats = (flags & RS_FLAG_COUNT_EVALS) != 0;
@@ -340,7 +342,8 @@ int32_t rs_blend(rs_workspace* ws, const rs_options* opts, float* out_rgb, float
 int32_t rs_render(rs_workspace* ws, const rs_scene* scene, const int32_t* active_idx, int64_t m,
                   const rs_camera* cam, const rs_options* opts, float* out_rgb, float* out_alpha, float* out_depth,
                   int32_t* out_count, uint32_t* scores, uint32_t flags, void* stream) {
-  int32_t s = rs_project(ws, scene, active_idx, m, cam, opts, stream);
+  // a score-only frame (no image outputs) projects without the SH colour
+  int32_t s = project_impl(ws, scene, active_idx, m, cam, opts, nullptr, nullptr, out_rgb != nullptr, stream);
   if (s != RS_OK) return s;
   if ((s = rs_bin(ws, stream)) != RS_OK) return s;
   return rs_blend(ws, opts, out_rgb, out_alpha, out_depth, out_count, scores, flags, stream);
@@ -406,11 +409,12 @@ int32_t rs_compact_bits(const uint8_t* bits, int64_t n, int32_t* out_idx, uint32
 }
 
 int32_t rs_check_finite(const rs_scene* scene, uint32_t* out_bad, void* stream) {
-  if (!scene || !out_bad || scene->n < 0 || (scene->n > 0 && !scene->planes) || scene->plane_stride < scene->n)
+  if (!scene || !out_bad || scene->n < 0 || (scene->n > 0 && (!scene->planes || !scene->sh)) ||
+      scene->plane_stride < scene->n)
     return RS_EINVAL;
   cudaStream_t st = S(stream);
   cudaMemsetAsync(out_bad, 0, 4, st);
-  if (scene->n > 0) finite_kernel<<<1184, 256, 0, st>>>(scene->planes, scene->n, scene->plane_stride, out_bad);
+  if (scene->n > 0) finite_kernel<<<1184, 256, 0, st>>>(scene->planes, scene->sh, scene->n, scene->plane_stride, out_bad);
   return cuda_status();
 }
 

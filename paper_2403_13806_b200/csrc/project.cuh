@@ -1,7 +1,8 @@
 // project.cuh -- per-Gaussian projection (replaces render.py:95-158).
 //
-// One thread per item. Reads the scene's fp32 planes with coalesced 4-byte
-// loads (59 independent loads in flight per thread at SH degree 3), evaluates
+// One thread per item. Reads the 11 geometry planes with coalesced 4-byte loads
+// and, for visible Gaussians of colour frames, the 192-byte SH row with twelve
+// 128-bit loads issued together; evaluates
 // the Tier-A fp32 contract of oracle/cpu_ref.cpp:project_one() in the same
 // operation order (compiled with -fmad=false; explicit __fmaf_rn only where
 // the contract fuses), and writes
@@ -36,8 +37,11 @@ __device__ __forceinline__ int ceil1_clip(float v, int hi) {
 // ProjectedGaussian fields of render.py:49-59 as 16 floats
 // {mx, my, a, b, c, ia, ib, ic, radius, depth, r, g, b, opacity, valid, 0}
 // and the int4 bbox: the per-primitive API project_gaussian/project_scene.
-template <bool FULL>
-__global__ void __launch_bounds__(128) project_kernel(const float* __restrict__ planes, int64_t stride, int deg,
+// COLOR = false skips the SH colour (score-only frames never read it: 192 B per
+// visible Gaussian less traffic, SURVEY §8d "44 B without SH in score mode").
+template <bool FULL, bool COLOR>
+__global__ void __launch_bounds__(128) project_kernel(const float* __restrict__ planes,
+                                                      const float* __restrict__ sh, int64_t stride, int deg,
                                                       const int32_t* __restrict__ active_idx, uint32_t n_items,
                                                       const rs_camera* __restrict__ camp, rs_options o,
                                                       Rec* __restrict__ recs,
@@ -130,6 +134,8 @@ __global__ void __launch_bounds__(128) project_kernel(const float* __restrict__ 
     const int y1 = ceil1_clip(__fadd_rn(my, radius), cam.height);
     valid = valid0 && x1 > x0 && y1 > y0;
     if (valid || FULL) {
+      float col[3] = {0.0f, 0.0f, 0.0f};
+      if (COLOR || FULL) {
       // view-direction SH colour (render.py:139-149, core.py:207-239)
       const float vx = __fsub_rn(px, cam.center[0]), vy = __fsub_rn(py, cam.center[1]),
                   vz = __fsub_rn(pz, cam.center[2]);
@@ -156,17 +162,28 @@ __global__ void __launch_bounds__(128) project_kernel(const float* __restrict__ 
       Y[14] = __fmul_rn(__fmul_rn((float)1.445305721320277, z), __fsub_rn(xx, yy));
       Y[15] = __fmul_rn(__fmul_rn((float)-0.5900435899266435, x), __fsub_rn(xx, __fmul_rn(3.0f, yy)));
       const int nb = deg == 0 ? 1 : deg == 1 ? 4 : deg == 2 ? 9 : 16;
-      float col[3];
+      // the Gaussian's SH row: 128-bit loads, issued together (one round trip)
+      const float4* shr = reinterpret_cast<const float4*>(sh + 48 * i);
+      float c[48];
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (4 * v < nb) q = __ldg(shr + 4 * ch + v);
+          c[16 * ch + 4 * v] = q.x; c[16 * ch + 4 * v + 1] = q.y;
+          c[16 * ch + 4 * v + 2] = q.z; c[16 * ch + 4 * v + 3] = q.w;
+        }
 #pragma unroll
       for (int ch = 0; ch < 3; ++ch) {
-        const float* shc = P + (int64_t)(11 + 16 * ch) * stride;
-        float acc = __fmul_rn(__ldg(shc), Y[0]);
+        float acc = __fmul_rn(c[16 * ch], Y[0]);
 #pragma unroll
         for (int bnd = 1; bnd < 16; ++bnd)
-          if (bnd < nb) acc = __fadd_rn(acc, __fmul_rn(__ldg(shc + bnd * stride), Y[bnd]));
+          if (bnd < nb) acc = __fadd_rn(acc, __fmul_rn(c[16 * ch + bnd], Y[bnd]));
         const float pre = __fadd_rn(0.5f, acc);
         col[ch] = pre < 0.0f ? 0.0f : (pre > 1.0f ? 1.0f : pre);
       }
+      }  // COLOR
       // opacity = sigmoid(logit) (core.py:419-421)
       const float lg = __ldg(P + 3 * stride);
       float op;

@@ -1,7 +1,7 @@
 """Device residency: scenes in HBM, workspaces, and the frame launcher.
 
-* ``DeviceScene`` -- the scene as 59 fp32 planes of N floats in HBM (the
-  layout ``rs_scene`` documents). Reference scenes are immutable and carry a
+* ``DeviceScene`` -- the scene in HBM: 11 fp32 geometry planes of N floats
+  plus N SH rows of 48 floats (the layout ``rs_scene`` documents). Reference scenes are immutable and carry a
   ``generation`` tag (core.py:467-485), so an uploaded copy is cached per
   (object, generation) and reused by every later call on the same scene.
 * ``Renderer`` -- one per device: owns the workspace (grown on demand; a pair
@@ -22,11 +22,11 @@ import torch
 from . import _native as N
 from .core import InvalidParameterError, InvalidSceneError
 
-PLANES = 59
+PLANES = 11  # positions(3), opacity logit, log scales(3), quaternion(4); SH rows are separate
 
 
 def pack_planes(scene) -> np.ndarray:
-    """(59, N) float32 plane-major copy of a scene-like object."""
+    """(11, N) float32 plane-major geometry of a scene-like object."""
     pos = np.asarray(scene.positions)
     n = pos.shape[0]
     out = np.empty((PLANES, n), np.float32)
@@ -34,8 +34,13 @@ def pack_planes(scene) -> np.ndarray:
     out[3] = np.asarray(scene.opacity_logits).reshape(n)
     out[4:7] = np.asarray(scene.log_scales).reshape(n, 3).T
     out[7:11] = np.asarray(scene.quaternions).reshape(n, 4).T
-    out[11:59] = np.asarray(scene.sh).reshape(n, 48).T
     return out
+
+
+def pack_sh(scene) -> np.ndarray:
+    """(N, 48) float32 SH rows, channel-major [c][b] (core.py:480)."""
+    sh = np.asarray(scene.sh)
+    return np.ascontiguousarray(sh.reshape(sh.shape[0], 48), dtype=np.float32)
 
 
 class DeviceScene:
@@ -45,15 +50,21 @@ class DeviceScene:
         lib = N.load()
         self.device = torch.device(device or torch.device("cuda", torch.cuda.current_device()))
         host = torch.from_numpy(pack_planes(scene))
+        host_sh = torch.from_numpy(pack_sh(scene))
         self.n = int(host.shape[1])
         self.sh_degree = int(scene.active_sh_degree)
         if not 0 <= self.sh_degree <= 3:
             raise InvalidParameterError("active SH degree must be in 0..3")
         self.generation = getattr(scene, "generation", None)
         with torch.cuda.device(self.device):
-            self.planes = (host.pin_memory().to(self.device, non_blocking=True) if self.n
-                           else torch.zeros((PLANES, 1), dtype=torch.float32, device=self.device))
-        self.struct = N.RsScene(self.planes.data_ptr(), self.n, max(self.n, 1), self.sh_degree, 0)
+            if self.n:
+                self.planes = host.pin_memory().to(self.device, non_blocking=True)
+                self.sh = host_sh.pin_memory().to(self.device, non_blocking=True)
+            else:
+                self.planes = torch.zeros((PLANES, 1), dtype=torch.float32, device=self.device)
+                self.sh = torch.zeros((1, 48), dtype=torch.float32, device=self.device)
+        self.struct = N.RsScene(self.planes.data_ptr(), self.sh.data_ptr(), self.n, max(self.n, 1),
+                                self.sh_degree, 0)
         if check_finite and self.n:
             with torch.cuda.device(self.device):
                 bad = torch.zeros(1, dtype=torch.int32, device=self.device)

@@ -210,13 +210,15 @@ def test_contribution_accumulator_merge_commutative():
 # core types and the fp32 device packing
 # ---------------------------------------------------------------------------
 def test_plane_packing_roundtrip():
-    from paper_2403_13806_b200.device import pack_planes
+    from paper_2403_13806_b200.device import pack_planes, pack_sh
     s = _scene(7)
     p = pack_planes(s)
-    assert p.shape == (59, 7) and p.dtype == np.float32
+    assert p.shape == (11, 7) and p.dtype == np.float32
     assert np.array_equal(p[0:3].T, s.positions.astype(np.float32))
-    assert np.array_equal(p[11:59].T.reshape(7, 3, 16), s.sh.astype(np.float32))
     assert np.array_equal(p[7:11].T, s.quaternions.astype(np.float32))
+    sh = pack_sh(s)
+    assert sh.shape == (7, 48) and sh.flags.c_contiguous
+    assert np.array_equal(sh.reshape(7, 3, 16), s.sh.astype(np.float32))
 
 
 def test_camera_struct_center_in_fp64():
