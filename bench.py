@@ -40,18 +40,27 @@ sys.path.insert(0, str(ROOT))
 
 METRIC_RENDER = "render FPS at 1256x828, 500k Gaussians (configs[1] orbit), 1 frame per GPU per step"
 METRIC_SCORE = "importance-score views/s, 3M Gaussians x 200 views at 1256x828 (configs[2])"
+METRIC_HOUSE = "house-scale render FPS with visibility filtering, 6M Gaussians, 1920x1080 (configs[3])"
+METRIC_BATCH = "batched multi-view render frames/s, 1M heavy-tailed Gaussians, 1920x1080 (configs[4])"
+METRICS = {"render": METRIC_RENDER, "score": METRIC_SCORE, "house": METRIC_HOUSE, "batch": METRIC_BATCH}
+WORKLOADS = {"render": "configs[1] orbit render", "score": "configs[2] importance scoring",
+             "house": "configs[3] house trajectory", "batch": "configs[4] batched views"}
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="default: render 200 frames, score 5 passes, house 300 frames, batch 3 x 64 frames")
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", choices=("render", "score"), default="render")
+    ap.add_argument("--workload", choices=("render", "score", "house", "batch"), default="render")
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--n-gaussians", type=int, default=None, help="override N (debug only)")
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.steps is None:
+        a.steps = {"render": 200, "score": 5, "house": 300, "batch": 3}[a.workload]
+    return a
 
 
 def dist_env():
@@ -154,6 +163,11 @@ def cpu_model() -> str:
 # ---------------------------------------------------------------------------
 def make_workload(kind: str, n_override=None):
     from paper_2403_13806_b200 import synth
+    if kind == "house":
+        scene, _, traj = synth.config3(0, n=n_override or 6_000_000)
+        return scene, traj
+    if kind == "batch":
+        return synth.config4(0, n=n_override or 1_000_000)
     if kind == "render":
         scene, cams = synth.config1(0, n=n_override or 500_000)
         return scene, cams
@@ -167,7 +181,7 @@ def run_reference(args):
         return
     scene, cams = make_workload(args.workload, args.n_gaussians)
     threads = os.cpu_count() or 1
-    images = args.workload == "render"
+    images = args.workload != "score"
     # a step = one frame (or view) rendered by all host threads (bounded sample);
     # a wall-clock guard keeps the whole arm within a few minutes on small hosts
     for s in range(args.warmup):
@@ -182,13 +196,13 @@ def run_reference(args):
     value = done / total_t
     unit = "frames/s" if images else "views/s"
     line = {
-        "metric": METRIC_RENDER if images else METRIC_SCORE, "impl": "reference", "value": value, "unit": unit,
+        "metric": METRICS[args.workload], "impl": "reference", "value": value, "unit": unit,
         "n_gpus": world, "steps": args.steps, "steps_completed": done, "warmup": args.warmup,
         "ms_per_step": 1e3 * total_t / done,
         "higher_is_better": True, "scaling": "weak" if images else "strong", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic (seeded, BASELINE configs distributions)",
-        "config": {"workload": "configs[1] render" if images else "configs[2] scoring",
-                   "n_gaussians": len(scene), "width": 1256, "height": 828},
+        "config": {"workload": WORKLOADS[args.workload], "n_gaussians": len(scene), "width": cams[0].width,
+                   "height": cams[0].height},
         "cpu_baseline": {"value": value, "unit": unit, "cores": threads, "kind": "port",
                          "sample": f"1 {'frame' if images else 'view'} per step on {threads} threads "
                                    f"(oracle/cpu_ref.cpp fp32 restatement, tile-parallel); CPU {cpu_model()}"},
@@ -219,8 +233,6 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     opts = dict_opts()
-    scene, cams = make_workload(args.workload, args.n_gaussians)
-    ds = device_scene(scene, dev)
     r = renderer(dev)
     lib = r.lib
     opt_s = options_struct(opts)
@@ -229,13 +241,17 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     pk = peaks()
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    W_, H_ = cams[0].width, cams[0].height
 
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize(dev)
 
+    if args.workload in ("house", "batch"):
+        return run_trajectory(args, rank, world, local, dev, opts, r, opt_s, stream, flush, pk, barrier)
+    scene, cams = make_workload(args.workload, args.n_gaussians)
+    ds = device_scene(scene, dev)
+    W_, H_ = cams[0].width, cams[0].height
     result = {}
     if args.workload == "render":
         frames = lambda s: cams[(s * world + rank) % len(cams)]  # noqa: E731
@@ -304,7 +320,7 @@ def main():
         hw = W_ * H_
         frame_bytes = bytes_alg_render(len(scene), NV / args.steps, P_ / args.steps, hw)
         result.update({
-            "metric": METRIC_RENDER, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+            "metric": METRICS["render"], "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded configs[1]: 500k Gaussians in 32 clusters, SH deg 3; no dataset offline)",
@@ -346,7 +362,7 @@ def main():
             dist.all_reduce(te_t, op=dist.ReduceOp.MAX)
         result["e2e"] = {"value": world * ke / float(te_t.item()), "unit": "frames/s",
                          "h2d_bytes_per_step": C.sizeof(N.RsCamera) + C.sizeof(N.RsOptions),
-                         "d2h_bytes_per_step": hw * (12 + 4 + 4 + 4),
+                         "d2h_bytes_per_step": hw * (24 + 8 + 8),
                          "api": "paper_2403_13806_b200.render.rasterize (scene resident in HBM after first call)"}
         if rank == 0 and world == 1 and not args.no_cpu_baseline:
             threads = os.cpu_count() or 1
@@ -395,6 +411,21 @@ def main():
         t_max = float(t_local.item())
         value = args.steps * n / (t_max / 1e3)
         kept = int((scores >= 0.01).sum().item())
+        # e2e: the reference-facing compute_importance (cameras in, fp64 host table out)
+        from paper_2403_13806_b200.pruning import compute_importance
+        compute_importance(scene, cams, opts)
+        barrier()
+        t0 = time.perf_counter()
+        tab = compute_importance(scene, cams, opts)
+        barrier()
+        te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        assert int((tab.values >= 0.01).sum()) == kept
+        e2e = {"value": n / float(te.item()), "unit": "views/s",
+               "h2d_bytes_per_step": (hi - lo) * (C.sizeof(N.RsCamera) + C.sizeof(N.RsOptions)),
+               "d2h_bytes_per_step": 4 * len(scene),
+               "api": "paper_2403_13806_b200.pruning.compute_importance (one full pass of all views)"}
         result.update({
             "metric": METRIC_SCORE, "value": value, "unit": "views/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
@@ -404,9 +435,164 @@ def main():
                        "width": W_, "height": H_, "l2": "flushed (256 MB memset) between timed passes",
                        "parallelism": f"views sharded over {world} GPU(s) + NCCL all_reduce(MAX)"},
             "kept_at_0.01": kept, "wall_views_per_s": args.steps * n / wall,
+            "e2e": e2e,
             "gpu_launches": args.steps * len(mine) * (1 + 5 + 1 + 1 + r_tile_passes(W_, H_) + 1 + 1),
             "clocks": clk.summary(),
         })
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_trajectory(args, rank, world, local, dev, opts, r, opt_s, stream, flush, pk, barrier):
+    """configs[3] (house: 300-frame trajectory, FPS with vs without visibility
+    filtering) and configs[4] (batched multi-view render: 64 frames per GPU per
+    step). Frames are split across ranks with no communication (replicas); each
+    frame is one rs_render_ex launch sequence timed with CUDA events on the
+    launching stream, L2 flushed between frames (outside the events)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2403_13806_b200 import _native as N
+    from paper_2403_13806_b200 import synth
+    from paper_2403_13806_b200.device import camera_struct, device_scene
+    from paper_2403_13806_b200.visibility import _center, bake_visibility, cluster_cameras
+
+    house = args.workload == "house"
+    if house:
+        scene, train_cams, traj = synth.config3(0, n=args.n_gaussians or 6_000_000)
+        per_step = 1
+        frame_cams = lambda s: [traj[(s * world + rank) % len(traj)]]  # noqa: E731
+    else:
+        scene, traj = synth.config4(0, n=args.n_gaussians or 1_000_000)
+        per_step = 64
+        frame_cams = lambda s: [traj[((s * world + rank) * per_step + i) % len(traj)]  # noqa: E731
+                                for i in range(per_step)]
+    ds = device_scene(scene, dev)
+    W_, H_ = traj[0].width, traj[0].height
+    hw = W_ * H_
+    T = ((W_ + 15) // 16) * ((H_ + 15) // 16)
+    lib = r.lib
+    sptr = stream.cuda_stream
+    extra = {}
+    lists = {}
+    if house:
+        # bake: k-means (k=64) over the 512 training-camera centres, then one importance
+        # pass per cluster over its member cameras; list = {h > 0.01} (reference strict >,
+        # visibility.py:204; aux cameras 0 = "from that cluster's cameras")
+        clustering = cluster_cameras(np.array([_center(c) for c in train_cams]), 64, seed=0)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        vis = bake_visibility(scene, clustering, train_cams, t_cluster=0.01, aux_per_camera=0, seed=0,
+                              options=opts)
+        e1.record(stream)
+        barrier()
+        counts = vis.active_counts()
+        extra["bake"] = {"clusters": 64, "cameras": len(train_cams), "ms": e0.elapsed_time(e1),
+                         "active_mean": float(counts.mean()), "active_min": int(counts.min()),
+                         "active_max": int(counts.max()), "rule": "h > 0.01, member cameras only"}
+        clus = lambda cam: vis.nearest_cluster(_center(cam))  # noqa: E731
+        for j in range(vis.k):
+            lists[j] = vis.visible_indices(j, dev)
+    out = r.alloc_outputs(traj[0])
+    outs = r.outputs_struct(out)
+
+    arms = [("filtered", True), ("unfiltered", False)] if house else [("all", False)]
+    res_arms = {}
+    for arm, filt in arms:
+        # untimed checked pre-pass over every timed frame: pair capacity + E/C/P statistics
+        E = C_ = P_ = NV = NI = 0
+        nfr = 0
+        for s in range(args.steps):
+            for cam in frame_cams(s):
+                idx = lists[clus(cam)] if filt else None
+                _, st = r.render(ds, cam, opts, out=out, active_idx=idx, count_evals=True)
+                E += st.evals
+                C_ += st.composites
+                P_ += st.n_pairs
+                NV += st.n_visible
+                NI += st.n_items
+                nfr += 1
+        plan = []
+        for s in range(args.steps):
+            for cam in frame_cams(s):
+                idx = lists[clus(cam)] if filt else None
+                plan.append((camera_struct(cam), idx))
+
+        def launch(cs, idx):
+            N.check(lib.rs_render_ex(r.handle, C.byref(ds.struct), idx.data_ptr() if idx is not None else None,
+                                     int(idx.numel()) if idx is not None else 0, C.byref(cs), C.byref(opt_s),
+                                     C.byref(outs), None, 0, sptr))
+
+        for cs, idx in plan[:max(args.warmup, 1)]:
+            launch(cs, idx)
+        barrier()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in plan]
+        with ClockSampler(local) as clk:
+            barrier()
+            for (cs, idx), (a, b) in zip(plan, evs):
+                flush.zero_()
+                a.record(stream)
+                launch(cs, idx)
+                b.record(stream)
+            barrier()
+        assert not r.stats().overflow
+        t_local = torch.tensor([sum(a.elapsed_time(b) for a, b in evs)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+        t_max = float(t_local.item())
+        res_arms[arm] = {
+            "fps": world * nfr / (t_max / 1e3), "ms_per_frame": t_max / nfr, "clocks": clk.summary(),
+            "projected_mean": NI / nfr, "visible_mean": NV / nfr, "pairs_mean": P_ / nfr,
+            "pairs_per_tile_mean": P_ / nfr / T, "evals_per_px": E / nfr / hw, "composites_per_px": C_ / nfr / hw,
+            "bytes_alg_per_frame": bytes_alg_render(NI / nfr, NV / nfr, P_ / nfr, hw),
+            "frames": nfr * world}
+    main_arm = res_arms["filtered" if house else "all"]
+    t_max = main_arm["ms_per_frame"] * (main_arm["frames"] // world)
+    metric = METRICS[args.workload]
+    if house:
+        extra["fps_unfiltered"] = res_arms["unfiltered"]["fps"]
+        extra["filtering_speedup"] = res_arms["filtered"]["fps"] / res_arms["unfiltered"]["fps"]
+    value = main_arm["fps"]
+    result = {
+        "metric": metric, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32",
+        "data": f"synthetic (seeded configs[{3 if house else 4}]; no dataset offline)",
+        "config": {"workload": WORKLOADS[args.workload],
+                   "n_gaussians": len(scene), "width": W_, "height": H_, "tile": 16,
+                   "frames_per_gpu_per_step": per_step, "l2": "flushed (256 MB memset) between timed frames",
+                   "parallelism": f"frames split across {world} GPU(s), no communication"},
+        "arms": res_arms, "clocks": main_arm["clocks"],
+        "gpu_launches": sum(a["frames"] // world for a in res_arms.values()) * (1 + 5 + 1 + 1 + r_tile_passes(W_, H_) + 1 + 1),
+        "frame_roofline": {"bytes_alg_per_frame": main_arm["bytes_alg_per_frame"],
+                           "achieved_gbs": main_arm["bytes_alg_per_frame"] / (main_arm["ms_per_frame"] / 1e3) / 1e9,
+                           "peak_gbs": pk.get("hbm_gbs"),
+                           "frac": main_arm["bytes_alg_per_frame"] / (main_arm["ms_per_frame"] / 1e3) / 1e9
+                           / pk.get("hbm_gbs", 6548.8)},
+        **extra,
+    }
+    # e2e through the public API (host results every frame)
+    from paper_2403_13806_b200.render import rasterize
+    from paper_2403_13806_b200.visibility import render_from_viewpoint
+    sel = [c for s in range(args.steps) for c in frame_cams(s)][:8]
+    call = (lambda c: render_from_viewpoint(scene, vis, c, opts)) if house else (lambda c: rasterize(scene, c, opts))
+    call(sel[0])
+    barrier()
+    t0 = time.perf_counter()
+    for c in sel:
+        call(c)
+    barrier()
+    te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    result["e2e"] = {"value": world * len(sel) / float(te.item()), "unit": "frames/s",
+                     "h2d_bytes_per_step": per_step * (C.sizeof(N.RsCamera) + C.sizeof(N.RsOptions)),
+                     "d2h_bytes_per_step": per_step * hw * (24 + 8 + 8),
+                     "api": "paper_2403_13806_b200." + ("visibility.render_from_viewpoint" if house
+                                                        else "render.rasterize") + f" ({len(sel)} frames)"}
     if rank == 0:
         print(json.dumps(result), flush=True)
     if world > 1:

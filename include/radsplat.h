@@ -5,7 +5,7 @@
  * point below replaces one piece of that API's compute; the Python package
  * paper_2403_13806_b200 re-implements the reference signatures on top of it.
  *
- *   rs_render            <- render.py:225-287 `_forward` as used by
+ *   rs_render(_ex)       <- render.py:225-287 `_forward` as used by
  *                           rasterize (render.py:290-293),
  *                           rasterize_with_contributions (render.py:296-308;
  *                           max-merge render.py:84-88) and
@@ -13,7 +13,7 @@
  *   rs_project           <- render.py:95-158 `_project_arrays`
  *   rs_bin               <- render.py:218-222 `_composite_order` (re-expressed
  *                           as per-tile (depth, index) lists)
- *   rs_blend             <- render.py:246-283 compositing loop
+ *   rs_blend(_ex)        <- render.py:246-283 compositing loop
  *   rs_compact /
  *   rs_compact_bits      <- np.nonzero of visibility.py:204 indicators /
  *                           io.py:198-243 LSB-first RVIS bitsets
@@ -21,7 +21,8 @@
  *   rs_max_merge         <- render.py:84-85 ContributionAccumulator.update
  *
  * Conventions
- *   - All data pointers are DEVICE pointers owned by the caller; the library
+ *   - All data pointers are DEVICE pointers (rs_outputs' 64-bit images may be
+ *     mapped pinned host memory) owned by the caller; the library
  *     never allocates or frees caller memory. Scratch lives in a caller-provided
  *     workspace sized by rs_workspace_size().
  *   - Every call is stream-ordered on `stream` (a cudaStream_t passed as void*,
@@ -94,6 +95,24 @@ typedef struct rs_options {
   float alpha_max, alpha_cut, tau_stop, near_limit, lowpass, sigma_bound;
 } rs_options;
 
+/* Image outputs of a colour frame (rs_render_ex / rs_blend_ex). Every pointer
+ * may be NULL (that output is skipped); rgb, alpha and count go together.
+ *   rgb (H*W*3), alpha, depth (H*W) fp32 and count (H*W) int32: device images.
+ *   rgb64 (H*W*3), alpha64 (H*W) float64 and count64 (H*W) int64: the
+ *     reference's RenderOutput types (render.py:62-68, :236-239, :283); any
+ *     device-dereferenceable memory, typically mapped pinned HOST memory
+ *     (cudaHostAlloc; same pointer under UVA) so the blend writes the result
+ *     straight over the host link while other tiles are still compositing. */
+typedef struct rs_outputs {
+  float* rgb;
+  float* alpha;
+  float* depth;
+  int32_t* count;
+  double* rgb64;
+  double* alpha64;
+  int64_t* count64;
+} rs_outputs;
+
 /* Per-frame counters (device side; copied out by rs_read_stats). */
 typedef struct rs_stats {
   uint32_t n_items;     /* Gaussians projected (N, or M for a filtered render) */
@@ -151,6 +170,11 @@ RS_API int32_t rs_render(rs_workspace* ws, const rs_scene* scene, const int32_t*
                   const rs_options* opts, float* out_rgb, float* out_alpha, float* out_depth, int32_t* out_count,
                   uint32_t* scores, uint32_t flags, void* stream);
 
+/* rs_render with the image outputs of an rs_outputs (NULL = score-only frame). */
+RS_API int32_t rs_render_ex(rs_workspace* ws, const rs_scene* scene, const int32_t* active_idx, int64_t m,
+                            const rs_camera* cam, const rs_options* opts, const rs_outputs* out, uint32_t* scores,
+                            uint32_t flags, void* stream);
+
 /* Stream-ordered camera upload into the workspace (also fixes the image size of
  * the following frames); `cam` may be reused as soon as the call returns. */
 RS_API int32_t rs_set_camera(rs_workspace* ws, const rs_camera* cam, void* stream);
@@ -168,9 +192,17 @@ RS_API int32_t rs_project_full(rs_workspace* ws, const rs_scene* scene, const in
                         void* stream);
 RS_API int32_t rs_blend(rs_workspace* ws, const rs_options* opts, float* out_rgb, float* out_alpha, float* out_depth,
                  int32_t* out_count, uint32_t* scores, uint32_t flags, void* stream);
+RS_API int32_t rs_blend_ex(rs_workspace* ws, const rs_options* opts, const rs_outputs* out, uint32_t* scores,
+                           uint32_t flags, void* stream);
 
 /* Copy the device counters to host memory (synchronizes `stream`). */
 RS_API int32_t rs_read_stats(rs_workspace* ws, rs_stats* out, void* stream);
+/* Did any frame since the last reset overflow its pair capacity, and the
+ * largest P such a frame needed (synchronizes `stream`; reset != 0 clears
+ * the record). Lets a batch of frames -- a scoring pass -- run without a
+ * host sync per frame and be checked once. */
+RS_API int32_t rs_read_overflow(rs_workspace* ws, uint32_t* out_overflowed, uint64_t* out_pairs_needed_max,
+                                int32_t reset, void* stream);
 RS_API int32_t rs_get_buffers(rs_workspace* ws, rs_buffers* out);
 
 /* Stable compaction: indices i (ascending) with flags[i] != 0, count -> *out_count (device). */

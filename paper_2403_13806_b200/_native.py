@@ -46,6 +46,10 @@ class RsOptions(C.Structure):
                 ("alpha_max", "alpha_cut", "tau_stop", "near_limit", "lowpass", "sigma_bound")]
 
 
+class RsOutputs(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("rgb", "alpha", "depth", "count", "rgb64", "alpha64", "count64")]
+
+
 class RsStats(C.Structure):
     _fields_ = [("n_items", C.c_uint32), ("n_visible", C.c_uint32), ("n_pairs", C.c_uint32),
                 ("overflow", C.c_uint32), ("evals", C.c_uint64), ("composites", C.c_uint64),
@@ -68,13 +72,17 @@ SIGNATURES = {
     "rs_workspace_destroy": (None, [_vp]),
     "rs_render": (_i32, [_vp, C.POINTER(RsScene), _vp, _i64, C.POINTER(RsCamera), C.POINTER(RsOptions),
                          _vp, _vp, _vp, _vp, _vp, _u32, _vp]),
+    "rs_render_ex": (_i32, [_vp, C.POINTER(RsScene), _vp, _i64, C.POINTER(RsCamera), C.POINTER(RsOptions),
+                            C.POINTER(RsOutputs), _vp, _u32, _vp]),
     "rs_project": (_i32, [_vp, C.POINTER(RsScene), _vp, _i64, C.POINTER(RsCamera), C.POINTER(RsOptions), _vp]),
     "rs_project_full": (_i32, [_vp, C.POINTER(RsScene), _vp, _i64, C.POINTER(RsCamera), C.POINTER(RsOptions),
                                _vp, _vp, _vp]),
     "rs_bin": (_i32, [_vp, _vp]),
     "rs_set_camera": (_i32, [_vp, C.POINTER(RsCamera), _vp]),
     "rs_blend": (_i32, [_vp, C.POINTER(RsOptions), _vp, _vp, _vp, _vp, _vp, _u32, _vp]),
+    "rs_blend_ex": (_i32, [_vp, C.POINTER(RsOptions), C.POINTER(RsOutputs), _vp, _u32, _vp]),
     "rs_read_stats": (_i32, [_vp, C.POINTER(RsStats), _vp]),
+    "rs_read_overflow": (_i32, [_vp, C.POINTER(_u32), C.POINTER(C.c_uint64), _i32, _vp]),
     "rs_get_buffers": (_i32, [_vp, C.POINTER(RsBuffers)]),
     "rs_compact_workspace_size": (_sz, [_i64]),
     "rs_compact": (_i32, [_vp, _i64, _vp, _vp, _vp, _sz, _vp]),

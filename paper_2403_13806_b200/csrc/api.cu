@@ -26,7 +26,7 @@ size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 struct Layout {
   // per-frame zeroed region [0, frame_bytes)
   size_t ctr, hist, emit_lb, ranges, frame_bytes;
-  size_t cam, recs, keysA, keysB, valsA, valsB, offsets, owners, ptileA, ptileB, pitemA, pitemB, lbA, lbB, total;
+  size_t sticky, cam, recs, keysA, keysB, valsA, valsB, offsets, owners, ptileA, ptileB, pitemA, pitemB, lbA, lbB, total;
 };
 
 int tiles_x(int w) { return (w + kTile - 1) / kTile; }
@@ -41,6 +41,7 @@ Layout make_layout(int64_t n_cap, int64_t pair_cap, int W, int H) {
   L.emit_lb = take(((size_t)n_cap / kCountThreads + 2) * sizeof(unsigned long long));
   L.ranges = take(TW * TH * sizeof(uint2));
   L.frame_bytes = o;
+  L.sticky = take(sizeof(Sticky));
   L.cam = take(sizeof(rs_camera));
   L.recs = take((size_t)n_cap * sizeof(Rec));
   L.keysA = take((size_t)n_cap * 4);
@@ -193,6 +194,10 @@ int32_t rs_workspace_create(void* device_mem, size_t bytes, int64_t n_cap, int64
   cudaGetDevice(&dev);
   if (cudaDeviceGetAttribute(&ws->sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) ws->sms = 148;
   configure_kernels();
+  if (cudaMemset(ws->at<Sticky>(L.sticky), 0, sizeof(Sticky)) != cudaSuccess) {
+    delete ws;
+    return RS_ECUDA;
+  }
   *out = ws;
   return cuda_status();
 }
@@ -280,7 +285,8 @@ int32_t rs_bin(rs_workspace* ws, void* stream) {
     count_kernel<<<(n + kCountThreads - 1) / kCountThreads, kCountThreads, 0, st>>>(items_sorted, ws->at<Rec>(ws->L.recs), ws->ctr(), ws->TW,
                                                   (uint32_t)ws->pair_cap, ws->at<uint32_t>(ws->L.offsets),
                                                   ws->at<uint32_t>(ws->L.owners),
-                                                  ws->at<unsigned long long>(ws->L.emit_lb));
+                                                  ws->at<unsigned long long>(ws->L.emit_lb),
+                                                  ws->at<Sticky>(ws->L.sticky));
     const unsigned egrid = (unsigned)std::max<int64_t>(1, (ws->pair_cap + kEmitPairs - 1) / kEmitPairs);
     emit_kernel<<<egrid, 256, 0, st>>>(items_sorted, ws->at<Rec>(ws->L.recs), ws->at<uint32_t>(ws->L.offsets),
                                        ws->at<uint32_t>(ws->L.owners), ws->ctr(), ws->TW,
@@ -306,12 +312,16 @@ static const uint32_t* final_pair_items(const rs_workspace* ws) {
   return ws->tile_passes == 1 ? ws->at<uint32_t>(ws->L.pitemB) : ws->at<uint32_t>(ws->L.pitemA);
 }
 
-int32_t rs_blend(rs_workspace* ws, const rs_options* opts, float* out_rgb, float* out_alpha, float* out_depth,
-                 int32_t* out_count, uint32_t* scores, uint32_t flags, void* stream) {
+int32_t rs_blend_ex(rs_workspace* ws, const rs_options* opts, const rs_outputs* out_p, uint32_t* scores,
+                    uint32_t flags, void* stream) {
   if (!ws || !opts || !ws->binned) return RS_EINVAL;
-  const bool color = out_rgb != nullptr;
+  rs_outputs out{};
+  if (out_p) out = *out_p;
+  if ((out.rgb != nullptr) != (out.alpha != nullptr) || (out.rgb != nullptr) != (out.count != nullptr) ||
+      (out.rgb64 != nullptr) != (out.alpha64 != nullptr) || (out.rgb64 != nullptr) != (out.count64 != nullptr))
+    return RS_EINVAL;
+  const bool color = out.rgb || out.rgb64 || out.depth;
   if (color && !ws->has_color) return RS_EINVAL;  // projected by a score-only rs_render
-  if (color && (!out_alpha || !out_depth || !out_count)) return RS_EINVAL;
   if (!color && !scores) return RS_EINVAL;
   const bool stats = (flags & RS_FLAG_COUNT_EVALS) != 0;
   cudaStream_t st = S(stream);
@@ -322,7 +332,7 @@ int32_t rs_blend(rs_workspace* ws, const rs_options* opts, float* out_rgb, float
   Counters* ctr = ws->ctr();
 #define RS_BLEND(C, I, K, F)                                                                        \
   blend_kernel<C, I, K, F><<<T, kBlendThreads, 0, st>>>(ranges, items, recs, ctr, ws->W, ws->H, ws->TW, *opts, \
-                                                        out_rgb, out_alpha, out_depth, out_count, scores)
+                                                        out, scores)
 #define RS_BLEND_F(C, I, K) \
   if (fast) RS_BLEND(C, I, K, true); else RS_BLEND(C, I, K, false)
   // exact-range exp2 is only needed for degenerate options (see blend.cuh FAST)
@@ -339,14 +349,30 @@ int32_t rs_blend(rs_workspace* ws, const rs_options* opts, float* out_rgb, float
   return cuda_status();
 }
 
+int32_t rs_blend(rs_workspace* ws, const rs_options* opts, float* out_rgb, float* out_alpha, float* out_depth,
+                 int32_t* out_count, uint32_t* scores, uint32_t flags, void* stream) {
+  if (out_rgb && (!out_alpha || !out_depth || !out_count)) return RS_EINVAL;
+  const rs_outputs out{out_rgb, out_alpha, out_depth, out_count, nullptr, nullptr, nullptr};
+  return rs_blend_ex(ws, opts, &out, scores, flags, stream);
+}
+
+int32_t rs_render_ex(rs_workspace* ws, const rs_scene* scene, const int32_t* active_idx, int64_t m,
+                     const rs_camera* cam, const rs_options* opts, const rs_outputs* out, uint32_t* scores,
+                     uint32_t flags, void* stream) {
+  // a score-only frame (no image outputs) projects without the SH colour
+  const bool color = out && (out->rgb || out->rgb64 || out->depth);
+  int32_t s = project_impl(ws, scene, active_idx, m, cam, opts, nullptr, nullptr, color, stream);
+  if (s != RS_OK) return s;
+  if ((s = rs_bin(ws, stream)) != RS_OK) return s;
+  return rs_blend_ex(ws, opts, out, scores, flags, stream);
+}
+
 int32_t rs_render(rs_workspace* ws, const rs_scene* scene, const int32_t* active_idx, int64_t m,
                   const rs_camera* cam, const rs_options* opts, float* out_rgb, float* out_alpha, float* out_depth,
                   int32_t* out_count, uint32_t* scores, uint32_t flags, void* stream) {
-  // a score-only frame (no image outputs) projects without the SH colour
-  int32_t s = project_impl(ws, scene, active_idx, m, cam, opts, nullptr, nullptr, out_rgb != nullptr, stream);
-  if (s != RS_OK) return s;
-  if ((s = rs_bin(ws, stream)) != RS_OK) return s;
-  return rs_blend(ws, opts, out_rgb, out_alpha, out_depth, out_count, scores, flags, stream);
+  if (out_rgb && (!out_alpha || !out_depth || !out_count)) return RS_EINVAL;
+  const rs_outputs out{out_rgb, out_alpha, out_depth, out_count, nullptr, nullptr, nullptr};
+  return rs_render_ex(ws, scene, active_idx, m, cam, opts, &out, scores, flags, stream);
 }
 
 int32_t rs_read_stats(rs_workspace* ws, rs_stats* out, void* stream) {
@@ -361,6 +387,19 @@ int32_t rs_read_stats(rs_workspace* ws, rs_stats* out, void* stream) {
   out->evals = c.evals;
   out->composites = c.composites;
   out->pairs_needed = c.pairs_needed;
+  return RS_OK;
+}
+
+int32_t rs_read_overflow(rs_workspace* ws, uint32_t* out_overflowed, uint64_t* out_pairs_needed_max,
+                         int32_t reset, void* stream) {
+  if (!ws || !out_overflowed || !out_pairs_needed_max) return RS_EINVAL;
+  Sticky h;
+  Sticky* d = ws->at<Sticky>(ws->L.sticky);
+  if (cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, S(stream)) != cudaSuccess) return RS_ECUDA;
+  if (reset && cudaMemsetAsync(d, 0, sizeof(Sticky), S(stream)) != cudaSuccess) return RS_ECUDA;
+  if (cudaStreamSynchronize(S(stream)) != cudaSuccess) return RS_ECUDA;
+  *out_overflowed = h.overflowed;
+  *out_pairs_needed_max = h.pairs_needed_max;
   return RS_OK;
 }
 

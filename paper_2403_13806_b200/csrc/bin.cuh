@@ -59,7 +59,8 @@ __global__ void __launch_bounds__(kCountThreads) count_kernel(const uint32_t* __
                                                     const Rec* __restrict__ recs, Counters* __restrict__ ctr, int TW,
                                                     uint32_t pair_cap, uint32_t* __restrict__ offsets,
                                                     uint32_t* __restrict__ chunk_owner,
-                                                    unsigned long long* __restrict__ status) {
+                                                    unsigned long long* __restrict__ status,
+                                                    Sticky* __restrict__ sticky) {
   __shared__ uint32_t s_block;
   __shared__ uint32_t s_wsum[kCountThreads / 32];
   __shared__ unsigned long long s_base;
@@ -102,6 +103,10 @@ __global__ void __launch_bounds__(kCountThreads) count_kernel(const uint32_t* __
         ctr->pairs_needed = end;
         ctr->n_pairs = (uint32_t)(end < pair_cap ? end : pair_cap);
         ctr->overflow = end > pair_cap ? 1u : 0u;
+        if (end > pair_cap) {  // survives the next frame's counter reset (checked once per batch)
+          atomicOr(&sticky->overflowed, 1u);
+          atomicMax(&sticky->pairs_needed_max, end);
+        }
       }
     }
   }

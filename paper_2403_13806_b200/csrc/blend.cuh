@@ -37,8 +37,7 @@ namespace rs {
 template <bool COLOR, bool CONTRIB, bool STATS, bool FAST>
 __global__ void __launch_bounds__(kBlendThreads) blend_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ pair_items, const Rec* __restrict__ recs,
-    Counters* __restrict__ ctr, int W, int H, int TW, rs_options o, float* __restrict__ out_rgb,
-    float* __restrict__ out_alpha, float* __restrict__ out_depth, int32_t* __restrict__ out_count,
+    Counters* __restrict__ ctr, int W, int H, int TW, rs_options o, const rs_outputs out,
     uint32_t* __restrict__ scores) {
   __shared__ Rec s_rec[kBlendThreads];  // one 64-byte record per entry: one base address per iteration
   __shared__ uint32_t s_w[CONTRIB ? kBlendThreads : 1];
@@ -146,14 +145,44 @@ __global__ void __launch_bounds__(kBlendThreads) blend_kernel(
     }
   }
 
-  if (inside && COLOR) {
-    const size_t p = (size_t)py * W + px;
-    out_rgb[3 * p] = cr;
-    out_rgb[3 * p + 1] = cg;
-    out_rgb[3 * p + 2] = cb;
-    out_alpha[p] = __fsub_rn(1.0f, tau);
-    out_depth[p] = cd;
-    out_count[p] = cnt;
+  if (COLOR) {
+    if (inside && out.rgb) {
+      const size_t p = (size_t)py * W + px;
+      out.rgb[3 * p] = cr;
+      out.rgb[3 * p + 1] = cg;
+      out.rgb[3 * p + 2] = cb;
+      out.alpha[p] = __fsub_rn(1.0f, tau);
+      out.count[p] = cnt;
+    }
+    if (inside && out.depth) out.depth[(size_t)py * W + px] = cd;
+    if (out.rgb64) {
+      // reference-typed images (float64 colour/alpha, int64 count; render.py:236-239, :283),
+      // usually straight into mapped pinned host memory: stage the tile in shared memory
+      // (the record slots are free after the loop) and write whole tile rows, so each warp
+      // store is one contiguous run -- the host-link writes overlap the other tiles' blending
+      __syncthreads();
+      double* s_o = reinterpret_cast<double*>(s_rec);  // [0,768) rgb, [768,1024) alpha, [1024,1280) count
+      const int lp = ((warp >> 1) * 4 + (lane >> 3)) * kTile + (warp & 1) * 8 + (lane & 7);
+      s_o[3 * lp] = (double)cr;
+      s_o[3 * lp + 1] = (double)cg;
+      s_o[3 * lp + 2] = (double)cb;
+      s_o[768 + lp] = (double)__fsub_rn(1.0f, tau);
+      reinterpret_cast<long long*>(s_o)[1024 + lp] = (long long)cnt;
+      __syncthreads();
+      const int cols = min(kTile, W - ox);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const int i = tid + k * kBlendThreads;  // 16 rows x 48 values
+        const int row = i / (3 * kTile), c = i - row * (3 * kTile);
+        if (oy + row < H && c < 3 * cols) out.rgb64[((size_t)(oy + row) * W + ox) * 3 + c] = s_o[i];
+      }
+      const int row = tid / kTile, c = tid % kTile;
+      if (oy + row < H && c < cols) {
+        const size_t p = (size_t)(oy + row) * W + ox + c;
+        out.alpha64[p] = s_o[768 + tid];
+        out.count64[p] = reinterpret_cast<const long long*>(s_o)[1024 + tid];
+      }
+    }
   }
   if (STATS) {
     unsigned long long c = (unsigned long long)cnt;

@@ -48,4 +48,11 @@ struct Counters {
 };
 static_assert(sizeof(Counters) == 128, "Counters is 128 B");
 
+// Overflow record that outlives the per-frame counter reset: a batch of frames
+// (e.g. a scoring pass) is launched without host syncs and checked once.
+struct Sticky {
+  uint32_t overflowed, pad;
+  unsigned long long pairs_needed_max;
+};
+
 }  // namespace rs

@@ -169,6 +169,13 @@ class Renderer:
         N.check(self.lib.rs_read_stats(self.handle, C.byref(st), self.stream), "read_stats")
         return st
 
+    def read_overflow(self, reset: bool = True) -> tuple[bool, int]:
+        """(did any frame since the last reset overflow, largest P it needed); synchronizes."""
+        o, p = C.c_uint32(), C.c_uint64()
+        N.check(self.lib.rs_read_overflow(self.handle, C.byref(o), C.byref(p), int(reset), self.stream),
+                "read_overflow")
+        return bool(o.value), int(p.value)
+
     def buffers(self) -> N.RsBuffers:
         b = N.RsBuffers()
         N.check(self.lib.rs_get_buffers(self.handle, C.byref(b)), "get_buffers")
@@ -203,14 +210,21 @@ class Renderer:
                     depth=torch.empty((H, W), dtype=torch.float32, device=d),
                     count=torch.empty((H, W), dtype=torch.int32, device=d))
 
+    @staticmethod
+    def outputs_struct(out: dict) -> N.RsOutputs:
+        """rs_outputs over the image tensors present in ``out`` (fp32 device images
+        rgb/alpha/depth/count and/or reference-typed rgb64/alpha64/count64, which may
+        live in pinned host memory)."""
+        return N.RsOutputs(*(out[k].data_ptr() if k in out else None for k in
+                             ("rgb", "alpha", "depth", "count", "rgb64", "alpha64", "count64")))
+
     def launch(self, ds: DeviceScene, cam_s: N.RsCamera, opt_s: N.RsOptions, out: dict,
                scores: torch.Tensor | None = None, active_idx: torch.Tensor | None = None,
                m: int = 0, flags: int = 0) -> None:
         """Enqueue one frame (no host synchronization)."""
-        ptr = lambda k: out[k].data_ptr() if k in out else None  # noqa: E731
-        N.check(self.lib.rs_render(
+        N.check(self.lib.rs_render_ex(
             self.handle, C.byref(ds.struct), active_idx.data_ptr() if active_idx is not None else None,
-            int(m), C.byref(cam_s), C.byref(opt_s), ptr("rgb"), ptr("alpha"), ptr("depth"), ptr("count"),
+            int(m), C.byref(cam_s), C.byref(opt_s), C.byref(self.outputs_struct(out)),
             scores.data_ptr() if scores is not None else None, flags, self.stream), "render")
 
     def render(self, ds: DeviceScene, cam, opts, *, color: bool = True, scores: torch.Tensor | None = None,
@@ -232,6 +246,30 @@ class Renderer:
             self.ensure(items, int(st.pairs_needed * 1.15) + 1024, W, H)
             if snapshot is not None:
                 scores.copy_(snapshot)
+        raise N.PairOverflow("tile pair capacity could not be satisfied")
+
+    def score_views(self, ds: DeviceScene, cams, opts, scores: torch.Tensor) -> None:
+        """Score-only frames of every camera max-merged into ``scores`` (fp32 bits viewed
+        as int32), launched back to back with no host sync per view; the pass is checked
+        for pair overflow once and, if a view overflowed, re-run from a snapshot with the
+        capacity the device reported."""
+        cams = list(cams)
+        if not cams:
+            return
+        W, H = max(int(c.width) for c in cams), max(int(c.height) for c in cams)
+        self.ensure(ds.n, self.caps[1] or max(4 * ds.n, 1 << 20), W, H)
+        opt_s = options_struct(opts)
+        structs = [camera_struct(c) for c in cams]
+        snapshot = scores.clone()
+        self.read_overflow(reset=True)
+        for _ in range(4):
+            for cs in structs:
+                self.launch(ds, cs, opt_s, {}, scores)
+            over, need = self.read_overflow(reset=True)
+            if not over:
+                return
+            self.ensure(ds.n, int(need * 1.15) + 1024, W, H)
+            scores.copy_(snapshot)
         raise N.PairOverflow("tile pair capacity could not be satisfied")
 
     def capture(self, ds: DeviceScene, cam, opts, *, color: bool = True, scores: torch.Tensor | None = None,
@@ -282,16 +320,15 @@ class FrameGraph:
         self.buf = r.buf
         self.width, self.height = int(cam.width), int(cam.height)
         self.opt_s = options_struct(opts)
-        ptr = lambda k: out[k].data_ptr() if k in out else None  # noqa: E731
         self.set_camera(cam)
         side = torch.cuda.Stream(r.device)
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.device(r.device):
             side.wait_stream(torch.cuda.current_stream(r.device))
             with torch.cuda.graph(self.graph, stream=side):
-                N.check(r.lib.rs_render(
+                N.check(r.lib.rs_render_ex(
                     r.handle, C.byref(ds.struct), active_idx.data_ptr() if active_idx is not None else None,
-                    int(m), None, C.byref(self.opt_s), ptr("rgb"), ptr("alpha"), ptr("depth"), ptr("count"),
+                    int(m), None, C.byref(self.opt_s), C.byref(r.outputs_struct(out)),
                     scores.data_ptr() if scores is not None else None, 0, side.cuda_stream), "render(capture)")
 
     def set_camera(self, cam) -> None:

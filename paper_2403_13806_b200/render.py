@@ -102,23 +102,27 @@ def render_device(scene, camera, options: RasterizeOptions = RasterizeOptions(),
                     count_evals=count_evals)
 
 
-def _to_output(out: dict) -> RenderOutput:
-    """Reference-typed host result: widened to float64 / int64 on the device, then
-    one device-to-host copy per array straight into fresh numpy buffers."""
-    H, W = out["alpha"].shape
-    rgb = np.empty((H, W, 3), np.float64)
-    alpha = np.empty((H, W), np.float64)
-    count = np.empty((H, W), np.int64)
-    torch.from_numpy(rgb).copy_(out["rgb"].double())
-    torch.from_numpy(alpha).copy_(out["alpha"].double())
-    torch.from_numpy(count).copy_(out["count"].long())
-    return RenderOutput(color=ImageBuffer.trusted(rgb), alpha=alpha, count=count, depth=out["depth"])
+def _render_host(scene, camera, options, *, scores: torch.Tensor | None = None,
+                 active_idx: torch.Tensor | None = None) -> RenderOutput:
+    """One frame whose reference-typed results (float64 colour/alpha, int64 count)
+    the blend kernel writes straight into pinned host memory (no device-side
+    widening pass, no staging copy); depth stays on the device until read."""
+    ds = _check_scene(scene)
+    r = renderer(ds.device)
+    H, W = int(camera.height), int(camera.width)
+    out = dict(rgb64=torch.empty((H, W, 3), dtype=torch.float64, pin_memory=True),
+               alpha64=torch.empty((H, W), dtype=torch.float64, pin_memory=True),
+               count64=torch.empty((H, W), dtype=torch.int64, pin_memory=True),
+               depth=torch.empty((H, W), dtype=torch.float32, device=ds.device))
+    sc = scores.view(torch.int32) if scores is not None else None
+    r.render(ds, camera, options, scores=sc, active_idx=active_idx, out=out)  # synchronizes
+    return RenderOutput(color=ImageBuffer.trusted(out["rgb64"].numpy()), alpha=out["alpha64"].numpy(),
+                        count=out["count64"].numpy(), depth=out["depth"])
 
 
 def rasterize(scene, camera, options: RasterizeOptions = RasterizeOptions()) -> RenderOutput:
     """Render over a black background, front to back (render.py:290-293)."""
-    out, _ = render_device(scene, camera, options)
-    return _to_output(out)
+    return _render_host(scene, camera, options)
 
 
 def rasterize_with_contributions(scene, camera, accumulator: ContributionAccumulator,
@@ -128,9 +132,9 @@ def rasterize_with_contributions(scene, camera, accumulator: ContributionAccumul
         raise InvalidParameterError("accumulator length must equal scene size")
     ds = _check_scene(scene)
     scores = torch.zeros(max(ds.n, 1), dtype=torch.float32, device=ds.device)
-    out, _ = render_device(ds, camera, options, scores=scores)
+    res = _render_host(ds, camera, options, scores=scores)
     accumulator.update(scores[:ds.n].cpu().numpy().astype(np.float64))
-    return _to_output(out)
+    return res
 
 
 def active_indices(scene, active, device=None) -> torch.Tensor:
@@ -147,8 +151,7 @@ def active_indices(scene, active, device=None) -> torch.Tensor:
 def rasterize_filtered(scene, camera, active, options: RasterizeOptions = RasterizeOptions()) -> RenderOutput:
     """Render only the active Gaussians; only those are projected."""
     idx = active_indices(scene, active)
-    out, _ = render_device(scene, camera, options, active_idx=idx)
-    return _to_output(out)
+    return _render_host(scene, camera, options, active_idx=idx)
 
 
 def _project_all(scene, camera, options):

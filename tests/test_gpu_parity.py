@@ -216,3 +216,62 @@ def test_accumulator_length_and_active_shape_rejected():
         rasterize_with_contributions(s, cam, ContributionAccumulator(len(s) + 1))
     with pytest.raises(InvalidParameterError):
         rasterize_filtered(s, cam, np.ones(len(s) + 2, bool))
+
+
+@pytest.mark.parametrize("case", CASES[:12] + CASES[-4:], ids=IDS[:12] + IDS[-4:])
+def test_rasterize_host_outputs_equal_device_images(case):
+    """rasterize(): the blend writes float64 colour/alpha and int64 count straight into
+    pinned host memory (rs_outputs rgb64/alpha64/count64) -- exactly the widened fp32
+    device images, including partial edge tiles."""
+    from paper_2403_13806_b200.render import rasterize
+    name, scene, cam, opts, d, p = case
+    got, _, _ = _render_gpu(scene, cam, opts, scores=False)
+    res = rasterize(scene, cam, opts)
+    assert res.color.data.dtype == np.float64 and res.alpha.dtype == np.float64 and res.count.dtype == np.int64
+    assert not res.color.data.flags.writeable
+    assert np.array_equal(res.color.data, got["rgb"].astype(np.float64)), name
+    assert np.array_equal(res.alpha, got["alpha"].astype(np.float64)), name
+    assert np.array_equal(res.count, got["count"].astype(np.int64)), name
+    assert np.array_equal(res.depth, got["depth"].astype(np.float64)), name
+
+
+def test_rasterize_host_outputs_odd_sizes():
+    """Image sizes that are not tile multiples: the staged row writes clip at W and H."""
+    from oracle import oracle as O
+    from paper_2403_13806_b200.core import look_at_camera
+    from paper_2403_13806_b200.render import RasterizeOptions, rasterize
+    from paper_2403_13806_b200.synth import config0
+    scene, _ = config0(0)
+    opts = RasterizeOptions(near_limit=0.2)
+    for w, h in ((1, 1), (17, 5), (33, 47), (130, 97)):
+        cam = look_at_camera(np.array([0.0, -3.0, 0.4]), np.zeros(3), width=w, height=h, fov_deg=50.0)
+        res = rasterize(scene, cam, opts)
+        ref = O.render(scene, cam, opts, np.float32)
+        assert np.array_equal(res.color.data, ref["img"].astype(np.float64)), (w, h)
+        assert np.array_equal(res.alpha, ref["alpha"].astype(np.float64)), (w, h)
+        assert np.array_equal(res.count, ref["count"].astype(np.int64)), (w, h)
+
+
+def test_score_views_overflow_recovery_matches_per_view_renders():
+    """A scoring pass launched without per-view host syncs: a view that overflows the
+    pair capacity is detected once per pass (rs_read_overflow) and the pass re-run from a
+    snapshot -- the result equals the max over checked single-view renders."""
+    from paper_2403_13806_b200.device import Renderer, device_scene
+    from paper_2403_13806_b200.render import RasterizeOptions, render_device
+    from paper_2403_13806_b200.synth import config2
+    scene, cams = config2(0, n=60_000, n_views=6)
+    opts = RasterizeOptions(near_limit=0.2)
+    ds = device_scene(scene)
+    ref = torch.zeros(ds.n, dtype=torch.float32, device=ds.device)
+    for c in cams:
+        render_device(ds, c, opts, color=False, scores=ref)
+    r = Renderer(ds.device)
+    r.ensure(ds.n, 1 << 16, cams[0].width, cams[0].height)  # far below this pass's P
+    pre = torch.rand(ds.n, device=ds.device) * 1e-3  # an accumulator that already holds values
+    got = pre.clone()
+    r.score_views(ds, cams, opts, got.view(torch.int32))
+    assert r.caps[1] > (1 << 16)
+    assert torch.equal(got, torch.maximum(ref, pre))
+    over, _ = r.read_overflow()
+    assert not over
+    r.close()
