@@ -574,6 +574,17 @@ def run_trajectory(args, rank, world, local, dev, opts, r, opt_s, stream, flush,
                            / pk.get("hbm_gbs", 6548.8)},
         **extra,
     }
+    if house:
+        # quality of the filtered frames vs the full render (reference acceptance: PSNR,
+        # test_acceptance.py:303-329), on a sample of the timed frames
+        ps = []
+        for cam in [c for s in range(args.steps) for c in frame_cams(s)][:16]:
+            full, _ = r.render(ds, cam, opts)
+            full = full["rgb"].clone()
+            filt, _ = r.render(ds, cam, opts, active_idx=lists[clus(cam)])
+            mse = float(((filt["rgb"] - full) ** 2).mean().item())
+            ps.append(99.0 if mse == 0 else 10.0 * np.log10(1.0 / mse))
+        extra["psnr_filtered_vs_full_db"] = {"mean": float(np.mean(ps)), "min": float(np.min(ps)), "frames": len(ps)}
     # e2e through the public API (host results every frame)
     from paper_2403_13806_b200.render import rasterize
     from paper_2403_13806_b200.visibility import render_from_viewpoint

@@ -162,6 +162,8 @@ template <typename T> struct PG {
   float cut2;        // fp32 contract: p2 < cut2 => alpha < alpha_cut
   int32_t cx0, cx1, cy0, cy1;  // culling box (fp32 contract); == bbox for T = double
   uint8_t bin;       // binned: valid and the culling box is non-empty
+  uint8_t ell;       // the culling box came from the ellipse (then tile rows use row_span)
+  float rg_hy, rg_dyr, rg_ak4, rg_d, rg_bi, rg_i2a, rg_del;  // row_geom terms (ell only)
 };
 
 template <typename T> inline int64_t floor_clip(T v, int hi) {
@@ -180,6 +182,8 @@ template <typename T> inline int64_t ceil1_clip(T v, int hi) {
   if (f >= (T)hi) return hi;
   return (int64_t)f + 1 > hi ? hi : (int64_t)f + 1;
 }
+
+template <typename T> inline void row_geom(PG<T>& g);
 
 // Culling box of the fp32 contract (device twin: project.cuh). cut2 is a
 // conservative bound (p2 < cut2 => o*2^p2 < alpha_cut); outside the ellipse
@@ -207,8 +211,63 @@ template <typename T> inline void cull_box(PG<T>& g, float alpha_cut) {
     g.cy1 = std::min(g.y1, (int32_t)std::fmin(std::floor(my + hy - 0.5) + 1.0, 65535.0));
     if (g.cx1 < g.cx0) g.cx1 = g.cx0;
     if (g.cy1 < g.cy0) g.cy1 = g.cy0;
+    g.ell = 1;
+    row_geom(g);
   }
   g.bin = g.valid && g.cx1 > g.cx0 && g.cy1 > g.cy0;
+}
+
+// Tile columns [tx0, tx1] of tile row ty that a binned Gaussian is listed in
+// (device twin: rows.cuh). For an ellipse-derived culling box this is the
+// x-extent, over the strip of the row's pixel centres dilated by 0.5 px, of
+// the ellipse {p2 >= cut2} scaled by 1.01 (q = -p2 <= 1.0201 K) and dilated
+// by 0.5 px -- the conservative region whose bounding box is the culling box
+// -- so no dropped tile holds a pixel that can reach alpha_cut. The x-extent
+// of an ellipse over a strip is attained at the strip point nearest the
+// ellipse's rightmost (leftmost) point: the boundary x(dy) is concave
+// (convex). Float arithmetic (D = 4 A Cc - B^2 is formed in double: it
+// cancels for elongated ellipses) with explicit slack for the rounding: +1e-5
+// relative on the half-height, +4e-6 * 4AK under the square roots (the
+// argument's rounding error is a few ulp of 4AK: dy is a correctly rounded
+// difference and every factor carries a few ulp), +0.02 px on each side. Otherwise (degenerate / ill-conditioned ellipse) the full row.
+template <typename T> inline void row_geom(PG<T>& g) {
+  // D = 4 A Cc - B^2 cancels for elongated ellipses: formed in double, then rounded once
+  const double Nad = g.na, Nbd = g.nb, Ncd = g.nc;
+  const float D = (float)(4.0 * Nad * Ncd - Nbd * Nbd);
+  const float A = -g.na, B = -g.nb, Cc = -g.nc;  // q = A dx^2 + B dx dy + Cc dy^2 = -p2
+  const float K = g.cut2 * -1.0201f;
+  const float AK4 = 4.0f * A * K;
+  g.rg_hy = std::sqrt(AK4 / D) * 1.00001f;
+  const float hx = std::sqrt(4.0f * Cc * K / D);
+  g.rg_dyr = -B * hx / (2.0f * Cc);  // dy of the rightmost point; the leftmost is at -dyr
+  g.rg_ak4 = AK4;
+  g.rg_d = D;
+  g.rg_i2a = 1.0f / (2.0f * A);
+  g.rg_bi = -B * g.rg_i2a;  // x(dy) = bi dy +- sqrt(4AK - D dy^2) / (2A)
+  g.rg_del = AK4 * 4e-6f;
+}
+
+template <typename T> inline bool row_span(const PG<T>& g, int ty, int* tx0, int* tx1) {
+  if (!g.ell) {
+    *tx0 = g.cx0 / TILE;
+    *tx1 = (g.cx1 - 1) / TILE;
+    return true;
+  }
+  const float mx = (float)g.mx, my = (float)g.my;
+  const int ys = std::max(ty * TILE, g.cy0), ye = std::min(ty * TILE + TILE, g.cy1);
+  const float lo = std::fmax((float)ys - my, -g.rg_hy), hi = std::fmin((float)ye - my, g.rg_hy);
+  if (!(lo <= hi)) return false;
+  const float ur = std::fmin(std::fmax(g.rg_dyr, lo), hi), ul = std::fmin(std::fmax(-g.rg_dyr, lo), hi);
+  const float sr = std::sqrt(std::fmax(g.rg_ak4 - g.rg_d * ur * ur, 0.0f) + g.rg_del);
+  const float sl = std::sqrt(std::fmax(g.rg_ak4 - g.rg_d * ul * ul, 0.0f) + g.rg_del);
+  const float right = mx + (g.rg_bi * ur + sr * g.rg_i2a) + 0.52f;
+  const float left = mx + (g.rg_bi * ul - sl * g.rg_i2a) - 0.52f;
+  const int px0 = (int)std::fmax(std::floor(left - 0.5f), (float)g.cx0);
+  const int px1 = (int)std::fmin(std::floor(right - 0.5f) + 1.0f, (float)g.cx1);
+  if (px1 <= px0) return false;
+  *tx0 = px0 / TILE;
+  *tx1 = (px1 - 1) / TILE;
+  return true;
 }
 
 template <typename T>
@@ -328,6 +387,7 @@ PG<T> project_one(const Scene<T>& s, int64_t i, const Cam<T>& cam, const Opts<T>
   g.cx0 = g.x0; g.cx1 = g.x1; g.cy0 = g.y0; g.cy1 = g.y1;
   g.cut2 = -INFINITY;
   g.bin = g.valid;
+  g.ell = 0;
   if (sizeof(T) == 4 && g.valid) cull_box(g, (float)o.alpha_cut);
   return g;
 }
@@ -430,9 +490,10 @@ int64_t bin_tiles(const std::vector<PG<T>>& pg, const uint8_t* active, int W, in
     const PG<T>& g = pg[i];
     if (!g.bin || (active && !active[i])) continue;
     const uint64_t dk = depth_key((float)g.depth);
+    int a, b;
     for (int ty = g.cy0 / TILE; ty <= (g.cy1 - 1) / TILE; ++ty)
-      for (int tx = g.cx0 / TILE; tx <= (g.cx1 - 1) / TILE; ++tx)
-        pairs.emplace_back(((uint64_t)(ty * TW + tx) << 32) | dk, (uint32_t)i);
+      if (row_span(g, ty, &a, &b))
+        for (int tx = a; tx <= b; ++tx) pairs.emplace_back(((uint64_t)(ty * TW + tx) << 32) | dk, (uint32_t)i);
   }
   std::stable_sort(pairs.begin(), pairs.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
   keys->resize(pairs.size());
@@ -514,8 +575,10 @@ void render(const Scene<T>& s, const T* camp, const T* optp, const uint8_t* acti
       for (const int64_t g : order) {
         const PG<T>& q = pg[(size_t)g];
         const int ty0 = std::max(q.cy0 / TILE, r0), ty1 = std::min((q.cy1 - 1) / TILE, r1 - 1);
+        int a, b;
         for (int ty = ty0; ty <= ty1; ++ty)
-          for (int tx = q.cx0 / TILE; tx <= (q.cx1 - 1) / TILE; ++tx) lists[(size_t)ty * TW + tx].push_back(g);
+          if (row_span(q, ty, &a, &b))
+            for (int tx = a; tx <= b; ++tx) lists[(size_t)ty * TW + tx].push_back(g);
       }
     });
     std::atomic<int> next(0);
@@ -572,6 +635,7 @@ struct ProjOut {
   float *na, *nb, *nc, *cut2;
   int32_t *cx0, *cx1, *cy0, *cy1;
   uint8_t* bin;
+  uint8_t* ell;
 };
 
 template <typename T>
@@ -588,6 +652,7 @@ void export_proj(const std::vector<PG<T>>& pg, ProjOut* po) {
     po->x0[i] = g.x0; po->x1[i] = g.x1; po->y0[i] = g.y0; po->y1[i] = g.y1;
     po->na[i] = g.na; po->nb[i] = g.nb; po->nc[i] = g.nc; po->cut2[i] = g.cut2;
     po->cx0[i] = g.cx0; po->cx1[i] = g.cx1; po->cy0[i] = g.cy0; po->cy1[i] = g.cy1; po->bin[i] = g.bin;
+    po->ell[i] = g.ell;
   }
 }
 

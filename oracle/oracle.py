@@ -30,7 +30,7 @@ def build(force: bool = False) -> Path:
 class ProjOut(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in (
         "valid", "mx", "my", "a", "b", "c", "ia", "ib", "ic", "radius", "depth", "color",
-        "opacity", "x0", "x1", "y0", "y1", "na", "nb", "nc", "cut2", "cx0", "cx1", "cy0", "cy1", "bin")]
+        "opacity", "x0", "x1", "y0", "y1", "na", "nb", "nc", "cut2", "cx0", "cx1", "cy0", "cy1", "bin", "ell")]
 
 
 _lib = None
@@ -109,7 +109,8 @@ def project(scene, cam, opts=None, dtype=np.float32) -> dict:
                y0=np.zeros(n, np.int32), y1=np.zeros(n, np.int32), color=np.zeros((n, 3), dtype),
                na=np.zeros(n, np.float32), nb=np.zeros(n, np.float32), nc=np.zeros(n, np.float32),
                cut2=np.zeros(n, np.float32), cx0=np.zeros(n, np.int32), cx1=np.zeros(n, np.int32),
-               cy0=np.zeros(n, np.int32), cy1=np.zeros(n, np.int32), bin=np.zeros(n, np.uint8))
+               cy0=np.zeros(n, np.int32), cy1=np.zeros(n, np.int32), bin=np.zeros(n, np.uint8),
+               ell=np.zeros(n, np.uint8))
     for k in ("mx", "my", "a", "b", "c", "ia", "ib", "ic", "radius", "depth", "opacity"):
         out[k] = np.zeros(n, dtype)
     po = ProjOut()
@@ -119,6 +120,7 @@ def project(scene, cam, opts=None, dtype=np.float32) -> dict:
                                                    _p(pack_options(opts, dtype)), C.byref(po))
     out["valid"] = out["valid"].astype(bool)
     out["bin"] = out["bin"].astype(bool)
+    out["ell"] = out["ell"].astype(bool)
     return out
 
 

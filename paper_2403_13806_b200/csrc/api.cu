@@ -26,7 +26,7 @@ size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 struct Layout {
   // per-frame zeroed region [0, frame_bytes)
   size_t ctr, hist, emit_lb, ranges, frame_bytes;
-  size_t sticky, cam, recs, keysA, keysB, valsA, valsB, offsets, owners, ptileA, ptileB, pitemA, pitemB, lbA, lbB, total;
+  size_t sticky, cam, recs, tcount, keysA, keysB, valsA, valsB, offsets, owners, ptileA, ptileB, pitemA, pitemB, lbA, lbB, total;
 };
 
 int tiles_x(int w) { return (w + kTile - 1) / kTile; }
@@ -44,6 +44,7 @@ Layout make_layout(int64_t n_cap, int64_t pair_cap, int W, int H) {
   L.sticky = take(sizeof(Sticky));
   L.cam = take(sizeof(rs_camera));
   L.recs = take((size_t)n_cap * sizeof(Rec));
+  L.tcount = take((size_t)n_cap * 4);
   L.keysA = take((size_t)n_cap * 4);
   L.keysB = take((size_t)n_cap * 4);
   L.valsA = take((size_t)n_cap * 4);
@@ -248,11 +249,13 @@ static int32_t project_impl(rs_workspace* ws, const rs_scene* scene, const int32
     if (full)
       project_kernel<true, true><<<grid, 128, 0, st>>>(
           scene->planes, scene->sh, scene->plane_stride, scene->sh_degree, active_idx, (uint32_t)items, ws->at<rs_camera>(ws->L.cam), *opts,
-          ws->at<Rec>(ws->L.recs), ws->at<uint32_t>(ws->L.keysA), ws->ctr(), full, reinterpret_cast<int4*>(full_bbox));
+          ws->at<Rec>(ws->L.recs), ws->at<uint32_t>(ws->L.keysA), ws->at<uint32_t>(ws->L.tcount), ws->ctr(), full,
+          reinterpret_cast<int4*>(full_bbox));
     else
       (color ? project_kernel<false, true> : project_kernel<false, false>)<<<grid, 128, 0, st>>>(
           scene->planes, scene->sh, scene->plane_stride, scene->sh_degree, active_idx, (uint32_t)items, ws->at<rs_camera>(ws->L.cam), *opts,
-          ws->at<Rec>(ws->L.recs), ws->at<uint32_t>(ws->L.keysA), ws->ctr(), nullptr, nullptr);
+          ws->at<Rec>(ws->L.recs), ws->at<uint32_t>(ws->L.keysA), ws->at<uint32_t>(ws->L.tcount), ws->ctr(),
+          nullptr, nullptr);
   }
   return cuda_status();
 }
@@ -282,7 +285,7 @@ int32_t rs_bin(rs_workspace* ws, void* stream) {
                                     ws->at<uint32_t>(ws->L.keysB), nullptr, ws->at<uint32_t>(ws->L.valsA),
                                     ws->at<uint32_t>(ws->L.valsB), nullptr, n, n, 32, 0, 0, false, st, &keys_res,
                                     &items_sorted);
-    count_kernel<<<(n + kCountThreads - 1) / kCountThreads, kCountThreads, 0, st>>>(items_sorted, ws->at<Rec>(ws->L.recs), ws->ctr(), ws->TW,
+    count_kernel<<<(n + kCountThreads - 1) / kCountThreads, kCountThreads, 0, st>>>(items_sorted, ws->at<uint32_t>(ws->L.tcount), ws->ctr(),
                                                   (uint32_t)ws->pair_cap, ws->at<uint32_t>(ws->L.offsets),
                                                   ws->at<uint32_t>(ws->L.owners),
                                                   ws->at<unsigned long long>(ws->L.emit_lb),

@@ -15,12 +15,15 @@
 //                 look-back (logical block ids from an atomic ticket) ->
 //                 exclusive pair offset per rank; total P.
 //   emit_kernel   one CTA per 2048 consecutive pairs: the owning ranks of the
-//                 CTA's pair range are found by one binary search, their
-//                 offsets and rectangles staged in shared memory, and each
-//                 thread writes (tile, item) for its pairs -- coalesced stores.
+//                 CTA's pair range come from the count kernel's chunk owners;
+//                 a warp per owner computes its tile-row spans and marks the
+//                 row segments inside the window; a block max-scan maps every
+//                 pair slot to its segment and each thread writes (tile, item)
+//                 for its 8 pairs -- coalesced stores.
 //                 The CTA also accumulates both 8-bit digit histograms of the
 //                 tile ids for the tile sort (no separate histogram pass).
 #pragma once
+#include "rows.cuh"
 #include "rs_common.cuh"
 
 namespace rs {
@@ -56,7 +59,7 @@ __device__ __forceinline__ unsigned long long warp_lookback(volatile unsigned lo
 }
 
 __global__ void __launch_bounds__(kCountThreads) count_kernel(const uint32_t* __restrict__ items_sorted,
-                                                    const Rec* __restrict__ recs, Counters* __restrict__ ctr, int TW,
+                                                    const uint32_t* __restrict__ tcount, Counters* __restrict__ ctr,
                                                     uint32_t pair_cap, uint32_t* __restrict__ offsets,
                                                     uint32_t* __restrict__ chunk_owner,
                                                     unsigned long long* __restrict__ status,
@@ -71,12 +74,7 @@ __global__ void __launch_bounds__(kCountThreads) count_kernel(const uint32_t* __
   const uint32_t nvis = ctr->n_visible;
   if (b * kCountThreads >= nvis && b > 0) return;  // no ranks here, and no later block needs this status
   const uint32_t r = b * kCountThreads + tid;
-  uint32_t nt = 0;
-  if (r < nvis) {
-    const int4 d = cullbox_of(recs[items_sorted[r]].d);
-    const int tx0 = d.x / kTile, tx1 = (d.y - 1) / kTile, ty0 = d.z / kTile, ty1 = (d.w - 1) / kTile;
-    nt = (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
-  }
+  const uint32_t nt = r < nvis ? tcount[items_sorted[r]] : 0u;  // row-span pair count (project_kernel)
   uint32_t x = nt;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -121,6 +119,8 @@ __global__ void __launch_bounds__(kCountThreads) count_kernel(const uint32_t* __
   }
 }
 
+constexpr int kEmitOwners = 256;  // owners staged per batch (one per thread)
+
 __global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ items_sorted,
                                                    const Rec* __restrict__ recs, const uint32_t* __restrict__ offsets,
                                                    const uint32_t* __restrict__ chunk_owner,
@@ -128,18 +128,26 @@ __global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ 
                                                    uint16_t* __restrict__ pair_tiles, uint32_t* __restrict__ pair_items,
                                                    uint32_t* __restrict__ tile_hist /* 2 x 256 */,
                                                    uint32_t* __restrict__ lookback0, uint32_t sort_chunk) {
-  __shared__ uint32_t s_off[kEmitPairs + 1];
-  __shared__ uint16_t s_tx0[kEmitPairs], s_ty0[kEmitPairs], s_tw[kEmitPairs];
-  __shared__ uint32_t s_item[kEmitPairs];
+  // A "segment" is one tile row of one Gaussian: consecutive pairs with consecutive tile ids.
+  // Segment data is keyed by the CTA-local slot of its first pair inside this window.
+  __shared__ __align__(16) uint16_t s_seg_tile[kEmitPairs];
+  __shared__ uint32_t s_seg_item[kEmitPairs];
   __shared__ __align__(16) uint16_t s_tile_out[kEmitPairs];
-  // s_start (owner start marks) and s_item_out share storage (a barrier separates the
+  // s_start (segment start marks) and s_item_out share storage (a barrier separates the
   // last mark read from the first item write)
   __shared__ __align__(16) int s_start_item[kEmitPairs];
   int* const s_start = s_start_item;
   uint32_t* const s_item_out = reinterpret_cast<uint32_t*>(s_start_item);
   __shared__ uint32_t s_hist[2][256];
   __shared__ int s_wmax[8];
-  const int tid = threadIdx.x;
+  // owner batch: row geometry, record boxes, item and the exclusive prefix of their row counts
+  __shared__ RowGeom s_g[kEmitOwners];
+  __shared__ int4 s_cb[kEmitOwners];
+  __shared__ uint32_t s_oitem[kEmitOwners];
+  __shared__ int s_rpre[kEmitOwners + 1];
+  __shared__ uint32_t s_wsum[8];
+  __shared__ uint32_t s_o0;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t P = ctr->n_pairs, nvis = ctr->n_visible;
   // zero the tile sort's first-pass look-back words
   const uint32_t lb_words = (P + sort_chunk - 1) / sort_chunk * 256u;
@@ -149,29 +157,123 @@ __global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ 
   const uint32_t k1 = min(P, k0 + kEmitPairs);
   for (int i = tid; i < 512; i += 256) (&s_hist[0][0])[i] = 0;
   for (int i = tid; i < kEmitPairs; i += 256) s_start[i] = -1;
+  // owners of [k0, k1): ranks r0 .. owner(k1 - 1) <= chunk_owner[next chunk] (ranks without
+  // pairs may lie in between), staged 256 at a time. Their tile rows are flattened across the
+  // CTA (8 consecutive rows per thread); a block scan of the rows' span widths gives every
+  // row segment's pair position -- consecutive ranks own consecutive pair ranges, so the
+  // position is the batch's first offset plus the prefix -- and each segment overlapping the
+  // window leaves a start mark.
   const uint32_t r0 = chunk_owner[blockIdx.x];
-  // owners of [k0, k1): ranks r0 .. owner(k1 - 1) <= chunk_owner[next chunk]; at most k1 - k0 of them
   const uint32_t rlast = k1 < P ? chunk_owner[blockIdx.x + 1] : nvis - 1;
-  const uint32_t nown = min((uint32_t)kEmitPairs, rlast - r0 + 1);
-  for (uint32_t i = tid; i < nown; i += 256) {
-    const uint32_t o = offsets[r0 + i];
-    s_off[i] = o;
-    if (o < k1) {
-      const uint32_t it = items_sorted[r0 + i];
-      const int4 d = cullbox_of(recs[it].d);
-      const int tx0 = d.x / kTile, tx1 = (d.y - 1) / kTile;
-      s_tx0[i] = (uint16_t)tx0; s_ty0[i] = (uint16_t)(d.z / kTile); s_tw[i] = (uint16_t)(tx1 - tx0 + 1);
-      s_item[i] = it;
+  for (uint32_t rb = r0; rb <= rlast; rb += kEmitOwners) {
+    __syncthreads();  // previous batch's staging fully consumed
+    const uint32_t r = rb + tid;
+    int nrows = 0;
+    if (r <= rlast) {
+      const uint32_t o = offsets[r];
+      if (o < k1) {
+        const uint32_t it = items_sorted[r];
+        const Rec* R = recs + it;
+        const int4 d = __ldg(&R->d);
+        const int4 cb = cullbox_of(d);
+        if (cullbox_ell(d)) s_g[tid] = row_geom(__ldg(&R->a), __ldg(&R->b));  // else: full rows
+        s_cb[tid] = d;
+        s_oitem[tid] = it;
+        nrows = (cb.w - 1) / kTile - cb.z / kTile + 1;
+      }
+      if (tid == 0) s_o0 = o;
+    }
+    // exclusive prefix of the row counts (owners past the window count 0 rows)
+    int x = nrows;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_wsum[warp] = (uint32_t)x;
+    __syncthreads();
+    int wbase = 0, total_rows = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      wbase += w < warp ? (int)s_wsum[w] : 0;
+      total_rows += (int)s_wsum[w];
+    }
+    s_rpre[tid] = wbase + x - nrows;
+    if (tid == 0) s_rpre[kEmitOwners] = total_rows;
+    const uint32_t o0 = s_o0;
+    __syncthreads();
+    if (o0 >= k1) break;  // uniform: this batch starts past the window
+    uint32_t carry = 0;   // pairs of the rows of earlier chunks
+    for (int c0 = 0; c0 < total_rows && o0 + carry < k1; c0 += 8 * 256) {
+      const int j0 = c0 + 8 * tid;
+      int own = 0;
+      uint32_t w[8];
+      int t0[8], ty[8];
+      if (j0 < total_rows) {  // owner of row j0: last owner whose first row is <= j0
+        int lo = 0, hi = kEmitOwners - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (s_rpre[mid] <= j0) lo = mid; else hi = mid - 1;
+        }
+        own = lo;
+      }
+      uint32_t sum = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int j = j0 + q;
+        w[q] = 0;
+        t0[q] = 0;
+        ty[q] = 0;
+        if (j < total_rows) {
+          while (s_rpre[own + 1] <= j) ++own;  // skips owners with no rows
+          const int4 d = s_cb[own];
+          const int4 cb = cullbox_of(d);
+          ty[q] = cb.z / kTile + (j - s_rpre[own]);
+          int a, b;
+          if (row_span(s_g[own], cb, cullbox_ell(d), ty[q], a, b)) {
+            w[q] = (uint32_t)(b - a + 1);
+            t0[q] = a;
+          }
+          t0[q] |= own << 16;
+        }
+        sum += w[q];
+      }
+      // block exclusive scan of the per-thread sums
+      uint32_t xs = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, xs, o);
+        if (lane >= o) xs += y;
+      }
+      __syncthreads();  // s_wsum reuse
+      if (lane == 31) s_wsum[warp] = xs;
+      __syncthreads();
+      uint32_t base = 0, ctot = 0;
+#pragma unroll
+      for (int w8 = 0; w8 < 8; ++w8) {
+        base += w8 < warp ? s_wsum[w8] : 0u;
+        ctot += s_wsum[w8];
+      }
+      uint32_t pos = o0 + carry + base + xs - sum;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint32_t s0 = pos, s1 = pos + w[q];
+        if (w[q] && s1 > k0 && s0 < k1) {
+          const uint32_t first = max(s0, k0);
+          const int ls = (int)(first - k0);
+          const int ow = t0[q] >> 16;
+          s_seg_tile[ls] = (uint16_t)(ty[q] * TW + (t0[q] & 0xffff) + (int)(first - s0));
+          s_seg_item[ls] = s_oitem[ow];
+          s_start[ls] = ls;
+        }
+        pos = s1;
+      }
+      carry += ctot;
     }
   }
   __syncthreads();
-  // owner of every pair slot without a search: mark where each owner's pairs start in this
-  // CTA's window, then a block-wide running max carries the owner index forward
-  for (uint32_t i = tid; i < nown; i += 256) {
-    const uint32_t o = s_off[i];
-    if (o < k1) s_start[o > k0 ? o - k0 : 0] = (int)i;
-  }
-  __syncthreads();
+  // segment of every pair slot without a search: a block-wide running max carries the
+  // last start mark forward (slot 0 always holds one: the segment containing pair k0)
   const uint32_t q0 = 8 * tid;  // this thread's 8 consecutive pair slots
   int own[8];
   {  // two 128-bit shared loads per thread (no bank conflicts at an 8-word stride)
@@ -186,8 +288,7 @@ __global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ 
     run = max(run, own[q]);
     own[q] = run;
   }
-  // exclusive max-scan of the per-thread last owner across the block
-  const int lane = tid & 31, warp = tid >> 5;
+  // exclusive max-scan of the per-thread last mark across the block
   int x = run;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) x = max(x, __shfl_up_sync(0xffffffffu, x, o));
@@ -196,8 +297,6 @@ __global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ 
   int carry = __shfl_up_sync(0xffffffffu, x, 1);
   if (lane == 0) carry = -1;
   for (int w = 0; w < warp; ++w) carry = max(carry, s_wmax[w]);
-  uint32_t row = 0, col = 0, tw = 1;
-  int cur = -2;
   uint32_t tl[8], itm[8];
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
@@ -206,21 +305,11 @@ __global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ 
     itm[q] = 0;
     if (k < k1) {
       const int j = max(own[q], carry);
-      if (j != cur) {  // new owner: one division, then walk the rectangle row-major
-        cur = j;
-        tw = s_tw[j];
-        const uint32_t local = k - s_off[j];
-        row = local / tw;
-        col = local - row * tw;
-      } else if (++col == tw) {
-        col = 0;
-        ++row;
-      }
-      tl[q] = (s_ty0[j] + row) * TW + s_tx0[j] + col;
-      itm[q] = s_item[j];
+      tl[q] = (uint32_t)s_seg_tile[j] + (q0 + q - (uint32_t)j);
+      itm[q] = s_seg_item[j];
     }
   }
-  __syncthreads();  // all owner marks read before the aliased item slots are written
+  __syncthreads();  // all marks read before the aliased item slots are written
   reinterpret_cast<uint4*>(s_tile_out)[tid] =
       make_uint4(tl[0] | (tl[1] << 16), tl[2] | (tl[3] << 16), tl[4] | (tl[5] << 16), tl[6] | (tl[7] << 16));
   reinterpret_cast<uint4*>(s_item_out)[2 * tid] = make_uint4(itm[0], itm[1], itm[2], itm[3]);

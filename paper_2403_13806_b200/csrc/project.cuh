@@ -12,6 +12,7 @@
 // n_visible is counted with one atomic per warp.
 #pragma once
 #include "rs_common.cuh"
+#include "rows.cuh"
 #include "rs_math.cuh"
 
 namespace rs {
@@ -45,7 +46,8 @@ __global__ void __launch_bounds__(128) project_kernel(const float* __restrict__ 
                                                       const int32_t* __restrict__ active_idx, uint32_t n_items,
                                                       const rs_camera* __restrict__ camp, rs_options o,
                                                       Rec* __restrict__ recs,
-                                                      uint32_t* __restrict__ keys, Counters* __restrict__ ctr,
+                                                      uint32_t* __restrict__ keys, uint32_t* __restrict__ tcount,
+                                                      Counters* __restrict__ ctr,
                                                       float* __restrict__ full, int4* __restrict__ full_bbox) {
   const uint32_t item = blockIdx.x * blockDim.x + threadIdx.x;
   if (item == 0) ctr->n_items = n_items;
@@ -208,6 +210,7 @@ __global__ void __launch_bounds__(128) project_kernel(const float* __restrict__ 
       // binning uses this box; double precision, IEEE ops only (reproducible on the CPU).
       int cx0 = x0, cx1 = x1, cy0 = y0, cy1 = y1;
       bool tight = false;  // box derived from the ellipse: outside it p2 < cut2 is guaranteed
+      bool ell = false;    // the ellipse bounds the box: tile rows are binned by row_span (rows.cuh)
       if (valid) {
         const double Na = rec.a.z, Nb = rec.a.w, Nc = rec.b.x;
         const double C2 = cut2;
@@ -230,6 +233,7 @@ __global__ void __launch_bounds__(128) project_kernel(const float* __restrict__ 
           cx1 = min(x1, ex1);
           cy0 = max(y0, ey0);
           cy1 = min(y1, ey1);
+          ell = true;
           // the ellipse box is the binding bound on every side (or that side is the image edge):
           // then no pixel outside the culling box can composite, bbox gate included
           tight = (ex0 >= x0 || x0 == 0) && (ex1 <= x1 || x1 == cam.width) && (ey0 >= y0 || y0 == 0) &&
@@ -240,8 +244,11 @@ __global__ void __launch_bounds__(128) project_kernel(const float* __restrict__ 
       }
       binned = valid && cx1 > cx0 && cy1 > cy0;
       rec.d = make_int4(x0 | (x1 << 16), y0 | (y1 << 16), cx0 | (cx1 << 16) | (tight ? (int)0x80000000 : 0),
-                        cy0 | (cy1 << 16));
-      if (binned) recs[item] = rec;
+                        cy0 | (cy1 << 16) | (ell ? (int)0x80000000 : 0));
+      if (binned) {
+        recs[item] = rec;
+        tcount[item] = record_tiles(rec.a, rec.b, rec.d);  // pairs this item emits
+      }
       if (FULL) {
         float4* f = reinterpret_cast<float4*>(full + 16 * (size_t)item);
         f[0] = make_float4(mx, my, a, b);

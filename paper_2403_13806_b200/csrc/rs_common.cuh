@@ -20,7 +20,9 @@ constexpr int kPlanes = 59;
 //   d = {x0 | x1<<16, y0 | y1<<16, cx0 | cx1<<16 | tight<<31, cy0 | cy1<<16}
 //       [x0,x1)x[y0,y1): the half-open 3-sigma pixel bbox of render.py:133-137;
 //       [cx0,cx1)x[cy0,cy1): a sub-box outside which no pixel can reach
-//       alpha >= alpha_cut (culling only -- never changes a result, §4 DESIGN.md)
+//       alpha >= alpha_cut (culling only -- never changes a result, §4 DESIGN.md);
+//       bit 31 of d.w ("ell"): the box came from the ellipse, so the tile binning
+//       lists per tile row only the columns the ellipse reaches (rows.cuh)
 struct __align__(16) Rec {
   float4 a, b, c;
   int4 d;
@@ -33,8 +35,9 @@ __device__ __forceinline__ int4 bbox_of(const int4 d) { return make_int4(lo16(d.
 // culling box; bit 31 of d.z flags a box derived from the ellipse (then every pixel
 // outside it has p2 < cut2, so a per-pixel box test is redundant)
 __device__ __forceinline__ int4 cullbox_of(const int4 d) {
-  return make_int4(lo16(d.z), hi16(d.z) & 0x7fff, lo16(d.w), hi16(d.w));
+  return make_int4(lo16(d.z), hi16(d.z) & 0x7fff, lo16(d.w), hi16(d.w) & 0x7fff);
 }
+__device__ __forceinline__ bool cullbox_ell(const int4 d) { return d.w < 0; }
 __device__ __forceinline__ bool cullbox_tight(const int4 d) { return d.z < 0; }
 
 // Device-side counters, mirrors rs_stats (first four words) + sort bookkeeping.

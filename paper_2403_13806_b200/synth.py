@@ -140,8 +140,11 @@ BOX_HI = np.array([10.0, 10.0, 4.0])
 def config3(seed: int = 0, n: int = 6_000_000, n_cams: int = 512, n_frames: int = 300,
             width: int = 1920, height: int = 1080):
     """House scale: half uniform in the 20x20x4 box, half in 256 clusters
-    (sigma 0.3); log-scales N(-3.8,0.5). 512 random-walk cameras (8 walks x 64
-    steps) and a 300-frame circular test trajectory at z=2."""
+    (sigma 0.3); log-scales N(-3.8,0.5). 512 training cameras on 8 random walks
+    of 64 steps inside the box; the 300-frame test trajectory runs along the
+    same walks, one frame halfway between consecutive training poses (held-out
+    in-between views, as test views are taken from a capture path), evenly
+    subsampled from the 8 x 63 midpoints in walk order."""
     rng = np.random.default_rng(seed)
     n_uni = n // 2
     uni = rng.uniform(BOX_LO, BOX_HI, size=(n_uni, 3))
@@ -150,23 +153,27 @@ def config3(seed: int = 0, n: int = 6_000_000, n_cams: int = 512, n_frames: int 
     clu = np.clip(centers[labels] + rng.normal(0.0, 0.3, size=(n - n_uni, 3)), BOX_LO, BOX_HI)
     scene = _attributes(rng, np.concatenate([uni, clu]), n, -3.8, 0.5)
     walk_rng = np.random.default_rng(seed + 1)
-    cams = []
+    cams, mids = [], []
     walks, steps = 8, n_cams // 8
+
+    def cam_at(pos, head):
+        tgt = pos + np.array([np.cos(head), np.sin(head), -0.1])
+        return look_at_camera(pos, tgt, width=width, height=height, fov_deg=55.0)
+
     for _ in range(walks):
         pos = walk_rng.uniform([-8, -8, 1.0], [8, 8, 3.0])
         head = walk_rng.uniform(0, 2 * np.pi)
+        prev = None
         for _ in range(steps):
             head += walk_rng.normal(0.0, 0.3)
             pos = np.clip(pos + 0.4 * np.array([np.cos(head), np.sin(head), 0.0])
                           + walk_rng.normal(0, 0.05, 3), [-9.5, -9.5, 0.5], [9.5, 9.5, 3.5])
-            tgt = pos + np.array([np.cos(head), np.sin(head), -0.1])
-            cams.append(look_at_camera(pos, tgt, width=width, height=height, fov_deg=55.0))
-    traj = []
-    for k in range(n_frames):
-        th = 2 * np.pi * k / n_frames
-        eye = np.array([6 * np.cos(th), 6 * np.sin(th), 2.0])
-        tgt = eye + np.array([-np.sin(th), np.cos(th), -0.1])
-        traj.append(look_at_camera(eye, tgt, width=width, height=height, fov_deg=55.0))
+            cams.append(cam_at(pos, head))
+            if prev is not None:
+                mids.append(cam_at(0.5 * (prev[0] + pos), 0.5 * (prev[1] + head)))
+            prev = (pos.copy(), head)
+    pick = np.round(np.linspace(0, len(mids) - 1, n_frames)).astype(int) if mids else []
+    traj = [mids[k] for k in pick]
     return scene, cams, traj
 
 

@@ -211,3 +211,33 @@ def test_frame_graph_replay_matches_direct_render():
         assert not st.overflow
         for k in ("rgb", "alpha", "depth", "count"):
             assert torch.equal(got[k], ref[k]), k
+
+
+@pytest.mark.parametrize("case", [(60_000, 960, 540, 1), (120_000, 1920, 1080, 7)], ids=lambda c: f"{c[0]}-{c[1]}x{c[2]}")
+def test_binning_anisotropic_bit_exact(case):
+    """configs[4] distributions (heavy-tailed anisotropic scales): the tile-row spans of the
+    ellipse binning, pair lists, ranges, image and scores equal the oracle bit for bit."""
+    from oracle import oracle as O
+    from paper_2403_13806_b200.device import renderer
+    from paper_2403_13806_b200.render import RasterizeOptions, render_device
+    from paper_2403_13806_b200.synth import config4
+    from paper_2403_13806_b200.core import look_at_camera
+    n, W, H, view = case
+    scene, cams = config4(view, n=n, n_views=16)
+    cam = look_at_camera(cams[view].rotation.T @ -cams[view].translation, (0.0, 0.0, 0.0), width=W, height=H,
+                         fov_deg=55.0)
+    opts = RasterizeOptions(near_limit=0.2)
+    sc = torch.zeros(n, dtype=torch.float32, device="cuda")
+    out, st = render_device(scene, cam, opts, scores=sc)
+    fa = renderer().frame_arrays()
+    ob = O.bin_tiles(scene, cam, opts, np.float32)
+    pr = O.project(scene, cam, opts, np.float32)
+    bn = pr["bin"]
+    T = lambda a0, a1, b0, b1: ((a1 - 1) // 16 - a0 // 16 + 1) * ((b1 - 1) // 16 - b0 // 16 + 1)  # noqa: E731
+    assert ob["P"] < 0.8 * int(T(pr["cx0"][bn], pr["cx1"][bn], pr["cy0"][bn], pr["cy1"][bn]).sum())
+    assert st.n_pairs == ob["P"]
+    assert np.array_equal(fa["ranges"], ob["ranges"])
+    assert np.array_equal(fa["pair_items"], ob["vals"])
+    ref = O.views(scene, [cam], opts, np.float32, scores=True, images=True)
+    assert np.array_equal(out["rgb"].cpu().numpy(), ref["img_last"])
+    assert np.array_equal(sc.cpu().numpy(), ref["contrib"])
