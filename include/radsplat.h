@@ -141,6 +141,7 @@ typedef struct rs_buffers {
 typedef struct rs_workspace rs_workspace;
 
 #define RS_FLAG_COUNT_EVALS 1u /* count E and C (slower; for roofline accounting) */
+#define RS_FLAG_BLEND_1PX 2u   /* one pixel per thread blend variant (A/B measurement) */
 
 RS_API int32_t rs_abi_version(void);
 RS_API const char* rs_status_string(int32_t status);

@@ -16,6 +16,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libradsplat_b200.so"
 
 RS_OK, RS_EINVAL, RS_ENONFINITE, RS_ENOMEM_WORKSPACE, RS_ECUDA, RS_EOVERFLOW = range(6)
 RS_FLAG_COUNT_EVALS = 1
+RS_FLAG_BLEND_1PX = 2
 
 
 class NativeUnavailable(RuntimeError):

@@ -327,17 +327,22 @@ int32_t rs_blend_ex(rs_workspace* ws, const rs_options* opts, const rs_outputs* 
   if (color && !ws->has_color) return RS_EINVAL;  // projected by a score-only rs_render
   if (!color && !scores) return RS_EINVAL;
   const bool stats = (flags & RS_FLAG_COUNT_EVALS) != 0;
+  const bool one_px = (flags & RS_FLAG_BLEND_1PX) != 0;
   cudaStream_t st = S(stream);
   const int T = ws->TW * ws->TH;
   const uint2* ranges = ws->at<uint2>(ws->L.ranges);
   const uint32_t* items = final_pair_items(ws);
   const Rec* recs = ws->at<Rec>(ws->L.recs);
   Counters* ctr = ws->ctr();
-#define RS_BLEND(C, I, K, F)                                                                        \
-  blend_kernel<C, I, K, F><<<T, kBlendThreads, 0, st>>>(ranges, items, recs, ctr, ws->W, ws->H, ws->TW, *opts, \
-                                                        out, scores)
+#define RS_BLEND(C, I, K, F)                                                                              \
+  if (one_px)                                                                                             \
+    blend_kernel<C, I, K, F><<<T, kBlendThreads, 0, st>>>(ranges, items, recs, ctr, ws->W, ws->H, ws->TW, \
+                                                          *opts, out, scores);                            \
+  else                                                                                                    \
+    blend2_kernel<C, I, K, F><<<T, kBlend2Threads, 0, st>>>(ranges, items, recs, ctr, ws->W, ws->H,       \
+                                                            ws->TW, *opts, out, scores)
 #define RS_BLEND_F(C, I, K) \
-  if (fast) RS_BLEND(C, I, K, true); else RS_BLEND(C, I, K, false)
+  if (fast) { RS_BLEND(C, I, K, true); } else { RS_BLEND(C, I, K, false); }
   // exact-range exp2 is only needed for degenerate options (see blend.cuh FAST)
   const bool fast = opts->alpha_cut >= 1e-30f;
   if (color && scores) {

@@ -198,4 +198,245 @@ __global__ void __launch_bounds__(kBlendThreads) blend_kernel(
   }
 }
 
+// ---------------------------------------------------------------------------
+// Two pixels per thread: 128-thread CTA per 16x16 tile, warp w owns the 8x8
+// sub-rectangle (w%2, w/2), lane l the pixels (l%8, l/8) and (l%8, l/8 + 4) of
+// it. Each entry of a warp's list is read from shared memory once and
+// evaluated for both pixels (two independent dependency chains per thread),
+// halving the per-entry overhead (list walk, record loads, vote, loop).
+// Per-pixel arithmetic and decisions are exactly those of blend_kernel.
+// ---------------------------------------------------------------------------
+constexpr int kBlend2Threads = 128;
+
+template <bool COLOR, bool STATS, bool FAST>
+__device__ __forceinline__ float blend_px(const float4 ga, const float4 gb, const float4 gc, float xs, float ys,
+                                          const rs_options& o, float& tau, float& cr, float& cg, float& cb,
+                                          float& cd, int& cnt, bool& done, unsigned long long& evals) {
+  if (STATS) ++evals;
+  const float dx = __fsub_rn(xs, ga.x), dy = __fsub_rn(ys, ga.y);
+  const float p2 =
+      __fmaf_rn(__fmul_rn(ga.z, dx), dx, __fmaf_rn(__fmul_rn(ga.w, dy), dx, __fmul_rn(__fmul_rn(gb.x, dy), dy)));
+  float w = 0.0f;
+  if (p2 >= gb.z) {
+    const float pc = fminf(p2, 127.0f);
+    const float e = FAST ? exp2_core(pc) : exp2_contract(pc);
+    const float alpha = fminf(__fmul_rn(gb.y, e), o.alpha_max);
+    if (alpha >= o.alpha_cut) {
+      w = __fmul_rn(alpha, tau);
+      if (COLOR) {
+        cr = __fmaf_rn(gc.x, w, cr);
+        cg = __fmaf_rn(gc.y, w, cg);
+        cb = __fmaf_rn(gc.z, w, cb);
+        cd = __fmaf_rn(gb.w, w, cd);
+      }
+      ++cnt;
+      tau = __fmul_rn(tau, __fsub_rn(1.0f, alpha));
+      done = tau < o.tau_stop;
+    }
+  }
+  return w;
+}
+
+template <bool COLOR, bool CONTRIB, bool STATS, bool FAST>
+__global__ void __launch_bounds__(kBlend2Threads) blend2_kernel(
+    const uint2* __restrict__ ranges, const uint32_t* __restrict__ pair_items, const Rec* __restrict__ recs,
+    Counters* __restrict__ ctr, int W, int H, int TW, rs_options o, const rs_outputs out,
+    uint32_t* __restrict__ scores) {
+  constexpr int kBatch = 256;  // entries staged per batch (two per thread)
+  __shared__ Rec s_rec[kBatch];
+  __shared__ uint32_t s_w[CONTRIB ? kBatch : 1];
+  __shared__ uint8_t s_mask[kBatch];       // which warps' 8x8 sub-rectangles the entry touches
+  __shared__ uint8_t s_list[4][kBatch];    // per-warp compacted entry lists
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tile = blockIdx.x;
+  const int tx = tile % TW, ty = tile / TW;
+  const int ox = tx * kTile, oy = ty * kTile;
+  const int px = ox + (warp & 1) * 8 + (lane & 7);
+  const int py0 = oy + (warp >> 1) * 8 + (lane >> 3), py1 = py0 + 4;
+  const bool in0 = px < W && py0 < H, in1 = px < W && py1 < H;
+  const float xs = __fadd_rn((float)px, 0.5f);
+  const float ys0 = __fadd_rn((float)py0, 0.5f), ys1 = __fadd_rn((float)py1, 0.5f);
+  if (ctr->overflow) return;  // pair list incomplete: the host re-runs with a larger capacity
+  const uint2 rg = ranges[tile];
+  const uint32_t npairs = ctr->n_pairs;
+  const uint32_t end = rg.y < npairs ? rg.y : npairs;  // memory safety on overflow
+  const uint32_t lt = (1u << lane) - 1u;
+
+  float tau0 = 1.0f, r0 = 0.0f, g0 = 0.0f, b0 = 0.0f, d0 = 0.0f;
+  float tau1 = 1.0f, r1 = 0.0f, g1 = 0.0f, b1 = 0.0f, d1 = 0.0f;
+  int cnt0 = 0, cnt1 = 0;
+  unsigned long long evals = 0;
+  const bool start = 1.0f >= o.tau_stop;
+  bool done0 = !in0 || !start, done1 = !in1 || !start;
+
+  for (uint32_t base = rg.x; base < end; base += kBatch) {
+    if (__syncthreads_and(done0 && done1)) break;
+    uint32_t gid[2] = {0u, 0u};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int slot = tid + h * kBlend2Threads;
+      const uint32_t idx = base + slot;
+      if (idx < end) {
+        const Rec* R = recs + __ldg(pair_items + idx);
+        s_rec[slot].a = __ldg(&R->a);
+        s_rec[slot].b = __ldg(&R->b);
+        const float4 c = __ldg(&R->c);
+        if (COLOR || CONTRIB) s_rec[slot].c = c;
+        gid[h] = (uint32_t)__float_as_int(c.w);
+        const int4 d = cullbox_of(__ldg(&R->d));
+        s_rec[slot].d = d;
+        // box x sub-rectangle overlap: 2 column halves x 2 row halves -> bit w = (w%2, w/2)
+        const unsigned col = (d.x < ox + 8 && d.y > ox ? 1u : 0u) | (d.x < ox + 16 && d.y > ox + 8 ? 2u : 0u);
+        unsigned m = 0;
+        if (d.z < oy + 8 && d.w > oy) m |= col;
+        if (d.z < oy + 16 && d.w > oy + 8) m |= col << 2;
+        s_mask[slot] = (uint8_t)m;
+      }
+      if (CONTRIB) s_w[slot] = 0u;
+    }
+    __syncthreads();
+    const int n = (int)min((uint32_t)kBatch, end - base);
+    if (!__all_sync(0xffffffffu, done0 && done1)) {
+      int cntw = 0;
+      for (int c0 = 0; c0 < n; c0 += 32) {
+        const int e = c0 + lane;
+        const bool has = e < n && ((s_mask[e] >> warp) & 1u);
+        const unsigned bal = __ballot_sync(0xffffffffu, has);
+        if (has) s_list[warp][cntw + __popc(bal & lt)] = (uint8_t)e;
+        cntw += __popc(bal);
+      }
+      __syncwarp();
+      for (int q = 0; q < cntw; ++q) {
+        const Rec& E = s_rec[s_list[warp][q]];
+        const int4 bb = E.d;
+        const bool inx = px >= bb.x && px < bb.y;
+        const bool e0 = !done0 && inx && py0 >= bb.z && py0 < bb.w;
+        const bool e1 = !done1 && inx && py1 >= bb.z && py1 < bb.w;
+        float w0 = 0.0f, w1 = 0.0f;
+        if (e0 || e1) {
+          // both pixels in one basic block (selects, no per-pixel branches): two independent
+          // dependency chains per thread. Values computed for a pixel that is not evaluated
+          // (or below cut2) are discarded by the selects, so decisions and results are exactly
+          // those of blend_px.
+          const float4 ga = E.a, gb = E.b;
+          if (STATS) evals += (unsigned)e0 + (unsigned)e1;
+          const float dx = __fsub_rn(xs, ga.x);
+          const float ax = __fmul_rn(ga.z, dx);
+          const float dy0 = __fsub_rn(ys0, ga.y), dy1 = __fsub_rn(ys1, ga.y);
+          const float p20 = __fmaf_rn(ax, dx, __fmaf_rn(__fmul_rn(ga.w, dy0), dx, __fmul_rn(__fmul_rn(gb.x, dy0), dy0)));
+          const float p21 = __fmaf_rn(ax, dx, __fmaf_rn(__fmul_rn(ga.w, dy1), dx, __fmul_rn(__fmul_rn(gb.x, dy1), dy1)));
+          // the FAST exp2 is exact on [-126, 127]; lanes below cut2 (>= -126) are discarded
+          const float x0 = fmaxf(fminf(p20, 127.0f), -126.0f), x1 = fmaxf(fminf(p21, 127.0f), -126.0f);
+          const float ex0 = FAST ? exp2_core(x0) : exp2_contract(fminf(p20, 127.0f));
+          const float ex1 = FAST ? exp2_core(x1) : exp2_contract(fminf(p21, 127.0f));
+          const float al0 = fminf(__fmul_rn(gb.y, ex0), o.alpha_max), al1 = fminf(__fmul_rn(gb.y, ex1), o.alpha_max);
+          const bool c0 = e0 && p20 >= gb.z && al0 >= o.alpha_cut;
+          const bool c1 = e1 && p21 >= gb.z && al1 >= o.alpha_cut;
+          w0 = c0 ? __fmul_rn(al0, tau0) : 0.0f;
+          w1 = c1 ? __fmul_rn(al1, tau1) : 0.0f;
+          if (COLOR) {
+            const float4 gc = E.c;
+            if (c0) {
+              r0 = __fmaf_rn(gc.x, w0, r0); g0 = __fmaf_rn(gc.y, w0, g0); b0 = __fmaf_rn(gc.z, w0, b0);
+              d0 = __fmaf_rn(gb.w, w0, d0);
+            }
+            if (c1) {
+              r1 = __fmaf_rn(gc.x, w1, r1); g1 = __fmaf_rn(gc.y, w1, g1); b1 = __fmaf_rn(gc.z, w1, b1);
+              d1 = __fmaf_rn(gb.w, w1, d1);
+            }
+          }
+          cnt0 += c0 ? 1 : 0;
+          cnt1 += c1 ? 1 : 0;
+          tau0 = c0 ? __fmul_rn(tau0, __fsub_rn(1.0f, al0)) : tau0;
+          tau1 = c1 ? __fmul_rn(tau1, __fsub_rn(1.0f, al1)) : tau1;
+          done0 = done0 || tau0 < o.tau_stop;
+          done1 = done1 || tau1 < o.tau_stop;
+        }
+        if (CONTRIB) {
+          const uint32_t wm = __reduce_max_sync(0xffffffffu, __float_as_uint(fmaxf(w0, w1)));
+          if (lane == 0 && wm) atomicMax(&s_w[s_list[warp][q]], wm);
+        }
+        if (__all_sync(0xffffffffu, done0 && done1)) break;  // all 64 pixels of the warp terminated
+      }
+    }
+    __syncthreads();
+    if (CONTRIB) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int slot = tid + h * kBlend2Threads;
+        if (base + slot < end) {
+          const uint32_t v = s_w[slot];
+          if (v) atomicMax(scores + gid[h], v);
+        }
+      }
+    }
+  }
+
+  if (COLOR) {
+    if (out.rgb) {
+      if (in0) {
+        const size_t p = (size_t)py0 * W + px;
+        out.rgb[3 * p] = r0; out.rgb[3 * p + 1] = g0; out.rgb[3 * p + 2] = b0;
+        out.alpha[p] = __fsub_rn(1.0f, tau0);
+        out.count[p] = cnt0;
+      }
+      if (in1) {
+        const size_t p = (size_t)py1 * W + px;
+        out.rgb[3 * p] = r1; out.rgb[3 * p + 1] = g1; out.rgb[3 * p + 2] = b1;
+        out.alpha[p] = __fsub_rn(1.0f, tau1);
+        out.count[p] = cnt1;
+      }
+    }
+    if (out.depth) {
+      if (in0) out.depth[(size_t)py0 * W + px] = d0;
+      if (in1) out.depth[(size_t)py1 * W + px] = d1;
+    }
+    if (out.rgb64) {
+      // reference-typed images written straight to (mapped host) memory in whole tile rows,
+      // staged through the free record slots (see blend_kernel)
+      __syncthreads();
+      double* s_o = reinterpret_cast<double*>(s_rec);  // [0,768) rgb, [768,1024) alpha, [1024,1280) count
+      const int lx = (warp & 1) * 8 + (lane & 7);
+      const int l0 = ((warp >> 1) * 8 + (lane >> 3)) * kTile + lx, l1 = l0 + 4 * kTile;
+      s_o[3 * l0] = (double)r0; s_o[3 * l0 + 1] = (double)g0; s_o[3 * l0 + 2] = (double)b0;
+      s_o[3 * l1] = (double)r1; s_o[3 * l1 + 1] = (double)g1; s_o[3 * l1 + 2] = (double)b1;
+      s_o[768 + l0] = (double)__fsub_rn(1.0f, tau0);
+      s_o[768 + l1] = (double)__fsub_rn(1.0f, tau1);
+      reinterpret_cast<long long*>(s_o)[1024 + l0] = (long long)cnt0;
+      reinterpret_cast<long long*>(s_o)[1024 + l1] = (long long)cnt1;
+      __syncthreads();
+      const int cols = min(kTile, W - ox);
+#pragma unroll
+      for (int k = 0; k < 6; ++k) {
+        const int i = tid + k * kBlend2Threads;  // 16 rows x 48 values
+        const int row = i / (3 * kTile), c = i - row * (3 * kTile);
+        if (oy + row < H && c < 3 * cols) out.rgb64[((size_t)(oy + row) * W + ox) * 3 + c] = s_o[i];
+      }
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int i = tid + k * kBlend2Threads;
+        const int row = i / kTile, c = i % kTile;
+        if (oy + row < H && c < cols) {
+          const size_t p = (size_t)(oy + row) * W + ox + c;
+          out.alpha64[p] = s_o[768 + i];
+          out.count64[p] = reinterpret_cast<const long long*>(s_o)[1024 + i];
+        }
+      }
+    }
+  }
+  if (STATS) {
+    unsigned long long c = (unsigned long long)(cnt0 + cnt1);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      evals += __shfl_down_sync(0xffffffffu, evals, off);
+      c += __shfl_down_sync(0xffffffffu, c, off);
+    }
+    if (lane == 0) {
+      atomicAdd(&ctr->evals, evals);
+      atomicAdd(&ctr->composites, c);
+    }
+  }
+}
+
 }  // namespace rs
