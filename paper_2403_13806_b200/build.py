@@ -54,7 +54,8 @@ def needs_build() -> bool:
 def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not needs_build():
         return LIB
-    cmd = [nvcc(), *NVCC_FLAGS, *(["-Xptxas", "-v"] if verbose else []),
+    extra = os.environ.get("RS_NVCC_EXTRA", "").split()  # experiments only (e.g. -DRS_EXP_...)
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, *(["-Xptxas", "-v"] if verbose else []),
            str(CSRC / "api.cu"), "-o", str(LIB) + ".tmp"]
     subprocess.check_call(cmd)
     os.replace(str(LIB) + ".tmp", LIB)

@@ -26,7 +26,7 @@ size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 struct Layout {
   // per-frame zeroed region [0, frame_bytes)
   size_t ctr, hist, emit_lb, ranges, frame_bytes;
-  size_t sticky, cam, recs, tcount, keysA, keysB, valsA, valsB, offsets, owners, ptileA, ptileB, pitemA, pitemB, lbA, lbB, total;
+  size_t sticky, cam, recs, tcount, rowtab, keysA, keysB, valsA, valsB, offsets, owners, ptileA, ptileB, pitemA, pitemB, lbA, lbB, total;
 };
 
 int tiles_x(int w) { return (w + kTile - 1) / kTile; }
@@ -45,6 +45,7 @@ Layout make_layout(int64_t n_cap, int64_t pair_cap, int W, int H) {
   L.cam = take(sizeof(rs_camera));
   L.recs = take((size_t)n_cap * sizeof(Rec));
   L.tcount = take((size_t)n_cap * 4);
+  L.rowtab = take((size_t)n_cap * 4 * kRowTab);
   L.keysA = take((size_t)n_cap * 4);
   L.keysB = take((size_t)n_cap * 4);
   L.valsA = take((size_t)n_cap * 4);
@@ -249,13 +250,13 @@ static int32_t project_impl(rs_workspace* ws, const rs_scene* scene, const int32
     if (full)
       project_kernel<true, true><<<grid, 128, 0, st>>>(
           scene->planes, scene->sh, scene->plane_stride, scene->sh_degree, active_idx, (uint32_t)items, ws->at<rs_camera>(ws->L.cam), *opts,
-          ws->at<Rec>(ws->L.recs), ws->at<uint32_t>(ws->L.keysA), ws->at<uint32_t>(ws->L.tcount), ws->ctr(), full,
+          ws->at<Rec>(ws->L.recs), ws->at<uint32_t>(ws->L.keysA), ws->at<uint32_t>(ws->L.tcount), ws->at<uint4>(ws->L.rowtab), ws->ctr(), full,
           reinterpret_cast<int4*>(full_bbox));
     else
       (color ? project_kernel<false, true> : project_kernel<false, false>)<<<grid, 128, 0, st>>>(
           scene->planes, scene->sh, scene->plane_stride, scene->sh_degree, active_idx, (uint32_t)items, ws->at<rs_camera>(ws->L.cam), *opts,
-          ws->at<Rec>(ws->L.recs), ws->at<uint32_t>(ws->L.keysA), ws->at<uint32_t>(ws->L.tcount), ws->ctr(),
-          nullptr, nullptr);
+          ws->at<Rec>(ws->L.recs), ws->at<uint32_t>(ws->L.keysA), ws->at<uint32_t>(ws->L.tcount), ws->at<uint4>(ws->L.rowtab),
+          ws->ctr(), nullptr, nullptr);
   }
   return cuda_status();
 }
@@ -290,12 +291,20 @@ int32_t rs_bin(rs_workspace* ws, void* stream) {
                                                   ws->at<uint32_t>(ws->L.owners),
                                                   ws->at<unsigned long long>(ws->L.emit_lb),
                                                   ws->at<Sticky>(ws->L.sticky));
+    // both emitters; the device picks one per frame (bin.cuh emit_pair_balanced)
     const unsigned egrid = (unsigned)std::max<int64_t>(1, (ws->pair_cap + kEmitPairs - 1) / kEmitPairs);
-    emit_kernel<<<egrid, 256, 0, st>>>(items_sorted, ws->at<Rec>(ws->L.recs), ws->at<uint32_t>(ws->L.offsets),
+    emit_kernel<<<egrid, 256, 0, st>>>(items_sorted, ws->at<Rec>(ws->L.recs), ws->at<uint4>(ws->L.rowtab),
+                                       ws->at<uint32_t>(ws->L.offsets),
                                        ws->at<uint32_t>(ws->L.owners), ws->ctr(), ws->TW,
                                        ws->at<uint16_t>(ws->L.ptileA), ws->at<uint32_t>(ws->L.pitemA),
                                        ws->at<uint32_t>(ws->L.hist) + 4 * 256, ws->at<uint32_t>(ws->L.lbA),
                                        kSortThreads * kTileItems);
+    emitw_kernel<<<std::max(1, std::min((int)((n + 32 * kEmitWarps - 1) / (32 * kEmitWarps)), ws->sms * 5)),
+                   32 * kEmitWarps, 0, st>>>(
+        items_sorted, ws->at<Rec>(ws->L.recs), ws->at<uint4>(ws->L.rowtab), ws->at<uint32_t>(ws->L.offsets),
+        ws->at<uint32_t>(ws->L.tcount), ws->ctr(), ws->TW, ws->at<uint16_t>(ws->L.ptileA),
+        ws->at<uint32_t>(ws->L.pitemA), ws->at<uint32_t>(ws->L.hist) + 4 * 256, ws->at<uint32_t>(ws->L.lbA),
+        kSortThreads * kTileItems);
     const uint16_t* tiles_res;
     const uint32_t* pitems;
     run_sort<uint16_t, kTileItems>(ws, ws->at<uint16_t>(ws->L.ptileA), ws->at<uint16_t>(ws->L.ptileA),

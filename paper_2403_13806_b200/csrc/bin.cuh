@@ -121,8 +121,18 @@ __global__ void __launch_bounds__(kCountThreads) count_kernel(const uint32_t* __
 
 constexpr int kEmitOwners = 256;  // owners staged per batch (one per thread)
 
+// Two emitters, chosen on the device per frame (both are launched; one returns at once):
+// the pair-balanced emit_kernel wins when Gaussians cover many tiles (configs[1]: 33 pairs
+// per visible Gaussian, configs[4]: ~300), the rank-balanced emitw_kernel when they are
+// small (configs[2]: 17) -- measured on B200.
+constexpr uint32_t kEmitPairBalancedMean = 24;
+__device__ __forceinline__ bool emit_pair_balanced(uint32_t P, uint32_t nvis) {
+  return (unsigned long long)P >= (unsigned long long)kEmitPairBalancedMean * nvis;
+}
+
 __global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ items_sorted,
-                                                   const Rec* __restrict__ recs, const uint32_t* __restrict__ offsets,
+                                                   const Rec* __restrict__ recs, const uint4* __restrict__ rowtab,
+                                                   const uint32_t* __restrict__ offsets,
                                                    const uint32_t* __restrict__ chunk_owner,
                                                    const Counters* __restrict__ ctr, int TW,
                                                    uint16_t* __restrict__ pair_tiles, uint32_t* __restrict__ pair_items,
@@ -132,16 +142,20 @@ __global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ 
   // Segment data is keyed by the CTA-local slot of its first pair inside this window.
   __shared__ __align__(16) uint16_t s_seg_tile[kEmitPairs];
   __shared__ uint32_t s_seg_item[kEmitPairs];
-  __shared__ __align__(16) uint16_t s_tile_out[kEmitPairs];
-  // s_start (segment start marks) and s_item_out share storage (a barrier separates the
-  // last mark read from the first item write)
+  // s_tile_out reuses s_seg_tile and s_item_out reuses s_start (segment start marks): a
+  // barrier separates the last segment/mark read from the first output write
+  uint16_t* const s_tile_out = s_seg_tile;
   __shared__ __align__(16) int s_start_item[kEmitPairs];
   int* const s_start = s_start_item;
   uint32_t* const s_item_out = reinterpret_cast<uint32_t*>(s_start_item);
   __shared__ uint32_t s_hist[2][256];
   __shared__ int s_wmax[8];
   // owner batch: row geometry, record boxes, item and the exclusive prefix of their row counts
-  __shared__ RowGeom s_g[kEmitOwners];
+  union __align__(16) OwnerRows {  // row table (<= kRowTab rows) or the geometry to evaluate rows from
+    RowGeom g;
+    uint32_t tab[kRowTab];
+  };
+  __shared__ OwnerRows s_g[kEmitOwners];
   __shared__ int4 s_cb[kEmitOwners];
   __shared__ uint32_t s_oitem[kEmitOwners];
   __shared__ int s_rpre[kEmitOwners + 1];
@@ -149,6 +163,7 @@ __global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ 
   __shared__ uint32_t s_o0;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t P = ctr->n_pairs, nvis = ctr->n_visible;
+  if (!emit_pair_balanced(P, nvis)) return;  // emitw_kernel emits this frame
   // zero the tile sort's first-pass look-back words
   const uint32_t lb_words = (P + sort_chunk - 1) / sort_chunk * 256u;
   for (uint32_t k = blockIdx.x * blockDim.x + tid; k < lb_words; k += gridDim.x * blockDim.x) lookback0[k] = 0;
@@ -169,17 +184,25 @@ __global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ 
     __syncthreads();  // previous batch's staging fully consumed
     const uint32_t r = rb + tid;
     int nrows = 0;
-    if (r <= rlast) {
+    if (tid < kEmitOwners && r <= rlast) {
       const uint32_t o = offsets[r];
       if (o < k1) {
         const uint32_t it = items_sorted[r];
         const Rec* R = recs + it;
         const int4 d = __ldg(&R->d);
         const int4 cb = cullbox_of(d);
-        if (cullbox_ell(d)) s_g[tid] = row_geom(__ldg(&R->a), __ldg(&R->b));  // else: full rows
+        nrows = (cb.w - 1) / kTile - cb.z / kTile + 1;
+        if (cullbox_ell(d)) {  // else: full rows
+          if (nrows <= kRowTab) {
+            uint4* t = reinterpret_cast<uint4*>(s_g[tid].tab);
+#pragma unroll
+            for (int v = 0; v < kRowTab / 4; ++v) t[v] = __ldg(rowtab + (kRowTab / 4) * (size_t)it + v);
+          } else {
+            s_g[tid].g = row_geom(__ldg(&R->a), __ldg(&R->b));
+          }
+        }
         s_cb[tid] = d;
         s_oitem[tid] = it;
-        nrows = (cb.w - 1) / kTile - cb.z / kTile + 1;
       }
       if (tid == 0) s_o0 = o;
     }
@@ -198,7 +221,7 @@ __global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ 
       wbase += w < warp ? (int)s_wsum[w] : 0;
       total_rows += (int)s_wsum[w];
     }
-    s_rpre[tid] = wbase + x - nrows;
+    if (tid < kEmitOwners) s_rpre[tid] = wbase + x - nrows;
     if (tid == 0) s_rpre[kEmitOwners] = total_rows;
     const uint32_t o0 = s_o0;
     __syncthreads();
@@ -228,9 +251,21 @@ __global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ 
           while (s_rpre[own + 1] <= j) ++own;  // skips owners with no rows
           const int4 d = s_cb[own];
           const int4 cb = cullbox_of(d);
-          ty[q] = cb.z / kTile + (j - s_rpre[own]);
-          int a, b;
-          if (row_span(s_g[own], cb, cullbox_ell(d), ty[q], a, b)) {
+          const int k = j - s_rpre[own];
+          ty[q] = cb.z / kTile + k;
+          int a = cb.x / kTile, b = (cb.y - 1) / kTile;  // rectangle row
+          bool ok = true;
+          if (cullbox_ell(d)) {
+            if ((cb.w - 1) / kTile - cb.z / kTile < kRowTab) {  // tabulated by the projection
+              const uint32_t e = s_g[own].tab[k];
+              a = (int)(e & 0xffffu);
+              b = a + (int)(e >> 16) - 1;
+              ok = e != 0u;
+            } else {
+              ok = row_span(s_g[own].g, cb, ty[q], a, b);
+            }
+          }
+          if (ok) {
             w[q] = (uint32_t)(b - a + 1);
             t0[q] = a;
           }
@@ -338,6 +373,185 @@ __global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ 
   }
   __syncthreads();
   for (int i = tid; i < 512; i += 256) {
+    const uint32_t v = (&s_hist[0][0])[i];
+    if (v) atomicAdd(&tile_hist[i], v);
+  }
+}
+
+// Rank-balanced emitter: one warp per 32 consecutive depth ranks. The warp walks the
+// contiguous pair range of its ranks 32 pairs at a time (coalesced stores): each lane finds
+// its pair's rank (binary search over the ranks' offsets, shuffles) and tile row (binary
+// search over the rank's row-table prefix in shared memory; rectangle rows by division).
+// Ranks with more than kRowTab ellipse rows are emitted afterwards, one at a time by the
+// whole warp: rows evaluated 32 at a time (row_span), a warp scan, then their pairs. Warps are
+// independent (no block barriers in the main loop), so the imbalance between near (large)
+// and far (small) Gaussians is absorbed by the other warps of the SM.
+constexpr int kEmitWarps = 8;
+
+__global__ void __launch_bounds__(32 * kEmitWarps) emitw_kernel(
+    const uint32_t* __restrict__ items_sorted, const Rec* __restrict__ recs, const uint4* __restrict__ rowtab,
+    const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ tcount, Counters* __restrict__ ctr,
+    int TW, uint16_t* __restrict__ pair_tiles, uint32_t* __restrict__ pair_items,
+    uint32_t* __restrict__ tile_hist /* 2 x 256 */, uint32_t* __restrict__ lookback0, uint32_t sort_chunk) {
+  __shared__ uint32_t s_hist[2][256];
+  __shared__ uint16_t s_tx[kEmitWarps][32][kRowTab];   // first tile column of each tabulated row
+  __shared__ uint16_t s_pre[kEmitWarps][32][kRowTab];  // exclusive prefix of the row widths
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t P = ctr->n_pairs, nvis = ctr->n_visible;
+  if (emit_pair_balanced(P, nvis)) return;  // emit_kernel emits this frame
+  const uint32_t lb_words = (P + sort_chunk - 1) / sort_chunk * 256u;
+  for (uint32_t k = blockIdx.x * blockDim.x + tid; k < lb_words; k += gridDim.x * blockDim.x) lookback0[k] = 0;
+  for (int i = tid; i < 512; i += 32 * kEmitWarps) (&s_hist[0][0])[i] = 0;
+  __syncthreads();
+  // persistent warps: chunks of 32 ranks from a work counter, so the SM slots of a finished
+  // warp are refilled at once (no block barrier waits on the slowest warp until the end)
+  for (;;) {
+    uint32_t chunk = 0;
+    if (lane == 0) chunk = atomicAdd(&ctr->emit_work, 1u);
+    const uint32_t r0 = __shfl_sync(0xffffffffu, chunk, 0) * 32u;
+    if (r0 >= nvis) break;
+    const uint32_t r = r0 + lane;
+    const bool has = r < nvis;
+    uint32_t o = 0, cnt = 0, it = 0;
+    int kind = 0, ty0 = 0, tx0 = 0, tw = 1, nrows = 0;  // kind 0 rectangle, 1 table, 2 evaluated rows
+    int4 cb = make_int4(0, 0, 0, 0);
+    if (has) {
+      o = offsets[r];
+      it = items_sorted[r];
+      cnt = tcount[it];
+      const int4 d = __ldg(&recs[it].d);
+      cb = cullbox_of(d);
+      ty0 = cb.z / kTile;
+      nrows = (cb.w - 1) / kTile - ty0 + 1;
+      tx0 = cb.x / kTile;
+      tw = (cb.y - 1) / kTile - tx0 + 1;
+      if (cullbox_ell(d)) {
+        if (nrows <= kRowTab) {
+          kind = 1;
+          uint32_t acc = 0;
+#pragma unroll
+          for (int v = 0; v < kRowTab / 4; ++v) {
+            const uint4 q = __ldg(rowtab + (kRowTab / 4) * (size_t)it + v);
+            const uint32_t t[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int k = 4 * v + u;
+              s_tx[warp][lane][k] = (uint16_t)(t[u] & 0xffffu);
+              s_pre[warp][lane][k] = (uint16_t)acc;
+              acc += k < nrows ? t[u] >> 16 : 0u;
+            }
+          }
+        } else {
+          kind = 2;
+        }
+      }
+    }
+    __syncwarp();
+    const uint32_t o_first = __shfl_sync(0xffffffffu, o, 0);
+    const uint32_t rel = o - o_first;
+    const int last = min(31, (int)(nvis - 1 - r0));
+    const uint32_t T = __shfl_sync(0xffffffffu, rel + cnt, last);  // pairs of the warp's ranks
+    for (uint32_t p0 = 0; p0 < T; p0 += 32) {
+      const uint32_t p = p0 + lane;
+      // owner lane: the last one whose first pair is <= p (ranks without pairs share the
+      // next rank's offset, so the last such lane owns pairs)
+      int lo = 0;
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1) {
+        const uint32_t v = __shfl_sync(0xffffffffu, rel, lo + step);
+        if (lo + step <= last && v <= p) lo += step;
+      }
+      const int okind = __shfl_sync(0xffffffffu, kind, lo);
+      const uint32_t L = p - __shfl_sync(0xffffffffu, rel, lo);
+      const uint32_t oitem = __shfl_sync(0xffffffffu, it, lo);
+      const int oty0 = __shfl_sync(0xffffffffu, ty0, lo);
+      const int otx0 = __shfl_sync(0xffffffffu, tx0, lo);
+      const int otw = __shfl_sync(0xffffffffu, tw, lo);
+      const uint32_t k = o_first + p;
+      const bool ok = p < T && okind != 2 && k < P;
+      uint32_t tile = 0;
+      if (ok) {
+        if (okind == 1) {
+          int rk = 0;
+#pragma unroll
+          for (int step = kRowTab / 2; step > 0; step >>= 1)
+            if (s_pre[warp][lo][rk + step] <= L) rk += step;
+          tile = (uint32_t)((oty0 + rk) * TW + s_tx[warp][lo][rk]) + (L - s_pre[warp][lo][rk]);
+        } else {
+          const uint32_t row = L / (uint32_t)otw;
+          tile = (uint32_t)((oty0 + (int)row) * TW + otx0) + (L - row * (uint32_t)otw);
+        }
+        pair_tiles[k] = (uint16_t)tile;
+        pair_items[k] = oitem;
+        atomicAdd(&s_hist[0][tile & 255u], 1u);
+      }
+      // high digit: consecutive pairs mostly share it -> one shared atomic per run
+      const uint32_t hi8 = ok ? tile >> 8 : 0xffffffffu;
+      const uint32_t prev = __shfl_up_sync(0xffffffffu, hi8, 1);
+      const uint32_t next = __shfl_down_sync(0xffffffffu, hi8, 1);
+      const unsigned starts = __ballot_sync(0xffffffffu, lane == 0 || prev != hi8);
+      if (ok && (lane == 31 || next != hi8)) {
+        const int run_start = 31 - __clz(starts & ((2u << lane) - 1u));
+        atomicAdd(&s_hist[1][hi8], (uint32_t)(lane - run_start + 1));
+      }
+    }
+    // ranks whose ellipse rows were not tabulated: one at a time, the whole warp
+    unsigned big = __ballot_sync(0xffffffffu, kind == 2);
+    while (big) {
+      const int b = __ffs(big) - 1;
+      big &= big - 1;
+      const uint32_t bitem = __shfl_sync(0xffffffffu, it, b);
+      const int4 bcb = make_int4(__shfl_sync(0xffffffffu, cb.x, b), __shfl_sync(0xffffffffu, cb.y, b),
+                                 __shfl_sync(0xffffffffu, cb.z, b), __shfl_sync(0xffffffffu, cb.w, b));
+      const int bty0 = __shfl_sync(0xffffffffu, ty0, b), bn = __shfl_sync(0xffffffffu, nrows, b);
+      uint32_t pos = __shfl_sync(0xffffffffu, o, b);
+      const RowGeom g = row_geom(__ldg(&recs[bitem].a), __ldg(&recs[bitem].b));
+      for (int rc = 0; rc < bn; rc += 32) {
+        const int rowk = rc + lane;
+        int a0 = 0, a1 = -1;
+        const uint32_t w = rowk < bn && row_span(g, bcb, bty0 + rowk, a0, a1) ? (uint32_t)(a1 - a0 + 1) : 0u;
+        uint32_t incl = w;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
+          if (lane >= off) incl += y;
+        }
+        const uint32_t excl = incl - w;
+        const uint32_t ct = __shfl_sync(0xffffffffu, incl, 31);
+        for (uint32_t q0 = 0; q0 < ct; q0 += 32) {
+          const uint32_t q = q0 + lane;
+          int lo = 0;
+#pragma unroll
+          for (int step = 16; step > 0; step >>= 1) {
+            const uint32_t v = __shfl_sync(0xffffffffu, excl, lo + step);
+            if (v <= q) lo += step;
+          }
+          const uint32_t rx = q - __shfl_sync(0xffffffffu, excl, lo);
+          const int ra0 = __shfl_sync(0xffffffffu, a0, lo);
+          const uint32_t k = pos + q;
+          const bool ok = q < ct && k < P;
+          uint32_t tile = 0;
+          if (ok) {
+            tile = (uint32_t)((bty0 + rc + lo) * TW + ra0) + rx;
+            pair_tiles[k] = (uint16_t)tile;
+            pair_items[k] = bitem;
+            atomicAdd(&s_hist[0][tile & 255u], 1u);
+          }
+          const uint32_t hi8 = ok ? tile >> 8 : 0xffffffffu;
+          const uint32_t prev = __shfl_up_sync(0xffffffffu, hi8, 1);
+          const uint32_t next = __shfl_down_sync(0xffffffffu, hi8, 1);
+          const unsigned starts = __ballot_sync(0xffffffffu, lane == 0 || prev != hi8);
+          if (ok && (lane == 31 || next != hi8)) {
+            const int run_start = 31 - __clz(starts & ((2u << lane) - 1u));
+            atomicAdd(&s_hist[1][hi8], (uint32_t)(lane - run_start + 1));
+          }
+        }
+        pos += ct;
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < 512; i += 32 * kEmitWarps) {
     const uint32_t v = (&s_hist[0][0])[i];
     if (v) atomicAdd(&tile_hist[i], v);
   }

@@ -47,14 +47,17 @@ __global__ void __launch_bounds__(128) project_kernel(const float* __restrict__ 
                                                       const rs_camera* __restrict__ camp, rs_options o,
                                                       Rec* __restrict__ recs,
                                                       uint32_t* __restrict__ keys, uint32_t* __restrict__ tcount,
-                                                      Counters* __restrict__ ctr,
+                                                      uint4* __restrict__ rowtab, Counters* __restrict__ ctr,
                                                       float* __restrict__ full, int4* __restrict__ full_bbox) {
   const uint32_t item = blockIdx.x * blockDim.x + threadIdx.x;
   if (item == 0) ctr->n_items = n_items;
   // the camera lives in device memory (uploaded by a stream-ordered copy), so a captured
   // CUDA graph of the frame replays with a new camera without re-instantiation
   const rs_camera cam = *camp;
+  __shared__ RowCountSmem s_rows;
   bool valid = false, binned = false;
+  float4 ga = make_float4(0.f, 0.f, 0.f, 0.f), gb = ga;  // the binned record's geometry (tile-row count)
+  int4 gd = make_int4(0, 0, 0, 0);
   if (item < n_items) {
     const int64_t i = active_idx ? (int64_t)__ldg(active_idx + item) : (int64_t)item;
     const float* P = planes + i;
@@ -247,7 +250,9 @@ __global__ void __launch_bounds__(128) project_kernel(const float* __restrict__ 
                         cy0 | (cy1 << 16) | (ell ? (int)0x80000000 : 0));
       if (binned) {
         recs[item] = rec;
-        tcount[item] = record_tiles(rec.a, rec.b, rec.d);  // pairs this item emits
+        ga = rec.a;
+        gb = rec.b;
+        gd = rec.d;
       }
       if (FULL) {
         float4* f = reinterpret_cast<float4*>(full + 16 * (size_t)item);
@@ -260,6 +265,8 @@ __global__ void __launch_bounds__(128) project_kernel(const float* __restrict__ 
     }
     keys[item] = binned ? depth_key(depth) : kInvalidKey;
   }
+  // pairs per binned record (+ row tables), warp-cooperatively
+  warp_count_rows(s_rows, binned, ga, gb, gd, item, tcount, rowtab);
   const unsigned vb = __ballot_sync(0xffffffffu, binned);
   if ((threadIdx.x & 31) == 0 && vb) atomicAdd(&ctr->n_visible, (uint32_t)__popc(vb));
 }

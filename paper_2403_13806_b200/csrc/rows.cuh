@@ -21,8 +21,17 @@
 namespace rs {
 
 struct RowGeom {
-  float mx, my, hy, dyr, ak4, d, bi, i2a, del;
+  float mx, my, hy, dyr, ak4, d, bi, i2a, del, sd;  // sd = edge_s at dyr
 };
+
+// sqrt(max(4AK - D u^2, 0) + del): the boundary term at dy = u (even in u, so one value
+// serves the rightmost point dyr and the leftmost point -dyr)
+__device__ __forceinline__ float row_s(const RowGeom& g, float u) {
+  return __fsqrt_rn(__fadd_rn(fmaxf(__fsub_rn(g.ak4, __fmul_rn(__fmul_rn(g.d, u), u)), 0.0f), g.del));
+}
+// the term at a row edge u = ys - my, clamped to the ellipse's [-hy, hy]: adjacent rows share
+// their common edge, and for a non-empty row this is exactly row_s at its clamped lo / hi
+__device__ __forceinline__ float edge_s(const RowGeom& g, float u) { return row_s(g, fminf(fmaxf(u, -g.hy), g.hy)); }
 
 __device__ __forceinline__ RowGeom row_geom(const float4 a, const float4 b) {
   // D = 4 A Cc - B^2 cancels for elongated ellipses: formed in double, then rounded once
@@ -42,22 +51,25 @@ __device__ __forceinline__ RowGeom row_geom(const float4 a, const float4 b) {
   g.i2a = __fdiv_rn(1.0f, __fmul_rn(2.0f, A));
   g.bi = __fmul_rn(-B, g.i2a);  // x(dy) = bi dy +- sqrt(4AK - D dy^2) / (2A)
   g.del = __fmul_rn(AK4, 4e-6f);
+  g.sd = row_s(g, g.dyr);
   return g;
 }
 
-// cb = culling box (cx0, cx1, cy0, cy1); false = the row lists no tile.
-__device__ __forceinline__ bool row_span(const RowGeom& g, const int4 cb, bool ell, int ty, int& tx0, int& tx1) {
-  if (!ell) {
-    tx0 = cb.x / kTile;
-    tx1 = (cb.y - 1) / kTile;
-    return true;
-  }
-  const int ys = max(ty * kTile, cb.z), ye = min(ty * kTile + kTile, cb.w);
-  const float lo = fmaxf(__fsub_rn((float)ys, g.my), -g.hy), hi = fminf(__fsub_rn((float)ye, g.my), g.hy);
+// Edge offsets of tile row ty: [ys, ye) = the row's pixel rows inside the culling box,
+// ulo = ys - my, uhi = ye - my (floats; adjacent rows share an edge value).
+__device__ __forceinline__ float row_edge(const RowGeom& g, int y) { return __fsub_rn((float)y, g.my); }
+
+// Span of an ellipse row from its edge offsets and edge terms (slo = edge_s(ulo),
+// shi = edge_s(uhi)); identical to oracle row_span: the clamped dyr / -dyr is one of
+// lo, hi, +-dyr and the boundary term there is slo, shi or sd.
+__device__ __forceinline__ bool row_span_e(const RowGeom& g, const int4 cb, float ulo, float uhi, float slo, float shi,
+                                           int& tx0, int& tx1) {
+  const float lo = fmaxf(ulo, -g.hy), hi = fminf(uhi, g.hy);
   if (!(lo <= hi)) return false;
-  const float ur = fminf(fmaxf(g.dyr, lo), hi), ul = fminf(fmaxf(-g.dyr, lo), hi);
-  const float sr = __fsqrt_rn(__fadd_rn(fmaxf(__fsub_rn(g.ak4, __fmul_rn(__fmul_rn(g.d, ur), ur)), 0.0f), g.del));
-  const float sl = __fsqrt_rn(__fadd_rn(fmaxf(__fsub_rn(g.ak4, __fmul_rn(__fmul_rn(g.d, ul), ul)), 0.0f), g.del));
+  float ur, sr, ul, sl;
+  if (g.dyr < lo) { ur = lo; sr = slo; } else if (g.dyr > hi) { ur = hi; sr = shi; } else { ur = g.dyr; sr = g.sd; }
+  const float nd = -g.dyr;
+  if (nd < lo) { ul = lo; sl = slo; } else if (nd > hi) { ul = hi; sl = shi; } else { ul = nd; sl = g.sd; }
   const float right = __fadd_rn(__fadd_rn(g.mx, __fadd_rn(__fmul_rn(g.bi, ur), __fmul_rn(sr, g.i2a))), 0.52f);
   const float left = __fsub_rn(__fadd_rn(g.mx, __fsub_rn(__fmul_rn(g.bi, ul), __fmul_rn(sl, g.i2a))), 0.52f);
   const int px0 = (int)fmaxf(floorf(__fsub_rn(left, 0.5f)), (float)cb.x);
@@ -68,18 +80,78 @@ __device__ __forceinline__ bool row_span(const RowGeom& g, const int4 cb, bool e
   return true;
 }
 
-// Pairs a binned record emits: the sum of its rows' spans.
-__device__ __forceinline__ uint32_t record_tiles(const float4 a, const float4 b, const int4 d) {
+// Span of ellipse row ty (both edge terms evaluated here).
+__device__ __forceinline__ bool row_span(const RowGeom& g, const int4 cb, int ty, int& tx0, int& tx1) {
+  const float ulo = row_edge(g, max(ty * kTile, cb.z)), uhi = row_edge(g, min(ty * kTile + kTile, cb.w));
+  return row_span_e(g, cb, ulo, uhi, edge_s(g, ulo), edge_s(g, uhi), tx0, tx1);
+}
+
+// Row table: the spans of the tile rows of an ellipse record with <= kRowTab rows, one word
+// per row (tx0 | width << 16, 0 = empty row), written by the projection's count for the
+// emitter (kRowTab / 4 uint4 per item).
+constexpr int kRowTab = 16;
+
+// Per-thread staging of the warp-cooperative row count (project_kernel).
+struct RowCountSmem {
+  RowGeom g[128];
+  int4 d[128];
+  uint32_t cnt[128];
+  __align__(16) uint32_t tab[128][kRowTab];
+  int pre[4][33];
+};
+
+// Pairs each binned record of the warp emits (rectangle rows: closed form; ellipse rows:
+// flattened over the warp's lanes so every lane evaluates one row per round, whatever the
+// per-record row counts), plus the row table of ellipse records with <= kRowTab rows.
+__device__ __forceinline__ void warp_count_rows(RowCountSmem& S, bool binned, const float4 a, const float4 b,
+                                                const int4 d, uint32_t item, uint32_t* __restrict__ tcount,
+                                                uint4* __restrict__ rowtab) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int4 cb = cullbox_of(d);
-  const bool ell = cullbox_ell(d);
-  if (!ell) return (uint32_t)(((cb.y - 1) / kTile - cb.x / kTile + 1) * ((cb.w - 1) / kTile - cb.z / kTile + 1));
-  const RowGeom g = row_geom(a, b);
-  uint32_t n = 0;
-  for (int ty = cb.z / kTile; ty <= (cb.w - 1) / kTile; ++ty) {
-    int t0, t1;
-    if (row_span(g, cb, true, ty, t0, t1)) n += (uint32_t)(t1 - t0 + 1);
+  const bool ell = binned && cullbox_ell(d);
+  const int nrows = binned ? (cb.w - 1) / kTile - cb.z / kTile + 1 : 0;
+  const int nr = ell ? nrows : 0;
+  if (ell) {
+    S.g[tid] = row_geom(a, b);
+    S.d[tid] = d;
   }
-  return n;
+  S.cnt[tid] = 0;
+  int x = nr;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  S.pre[warp][lane] = x - nr;
+  if (lane == 31) S.pre[warp][32] = x;
+  __syncwarp();
+  const int total = S.pre[warp][32];
+  for (int base = 0; base < total; base += 32) {
+    const int j = base + lane;
+    if (j < total) {
+      int lo = 0, hi = 31;  // owner lane: the last one whose first row is <= j
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (S.pre[warp][mid] <= j) lo = mid; else hi = mid - 1;
+      }
+      const int ow = warp * 32 + lo, k = j - S.pre[warp][lo];
+      const int4 ocb = cullbox_of(S.d[ow]);
+      int t0, t1;
+      uint32_t w = 0;
+      if (row_span(S.g[ow], ocb, ocb.z / kTile + k, t0, t1)) w = (uint32_t)(t1 - t0 + 1);
+      if (w) atomicAdd(&S.cnt[ow], w);
+      if (k < kRowTab) S.tab[ow][k] = w ? (uint32_t)t0 | (w << 16) : 0u;
+    }
+  }
+  __syncwarp();
+  if (binned) {
+    tcount[item] = ell ? S.cnt[tid] : (uint32_t)(((cb.y - 1) / kTile - cb.x / kTile + 1) * nrows);
+    if (ell && nrows <= kRowTab) {
+      const uint4* t = reinterpret_cast<const uint4*>(S.tab[tid]);
+#pragma unroll
+      for (int v = 0; v < kRowTab / 4; ++v) rowtab[(kRowTab / 4) * (size_t)item + v] = t[v];
+    }
+  }
 }
 
 }  // namespace rs

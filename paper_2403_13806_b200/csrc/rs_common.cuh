@@ -46,8 +46,9 @@ struct Counters {
   unsigned long long evals, composites;
   unsigned long long pairs_needed;                 // true P (sizing hint after overflow)
   uint32_t tickets[16];  // onesweep chunk tickets, one per pass
-  uint32_t emit_ctr;     // decoupled look-back ticket of the pair emitter
-  uint32_t pad[5];
+  uint32_t emit_ctr;     // decoupled look-back ticket of the pair counter
+  uint32_t emit_work;    // rank-chunk work counter of the pair emitter
+  uint32_t pad[4];
 };
 static_assert(sizeof(Counters) == 128, "Counters is 128 B");
 

@@ -20,6 +20,8 @@ def main():
     opts = RasterizeOptions(near_limit=0.2)
     if kind == "render":
         scene, cams = synth.config1(0)
+    elif kind == "batch":
+        scene, cams = synth.config4(0, n_views=16)
     else:
         scene, cams = synth.config2(0)
     ds = device_scene(scene)
@@ -27,7 +29,7 @@ def main():
     scores = torch.zeros(len(scene), dtype=torch.int32, device=ds.device)
     out = r.alloc_outputs(cams[0])
     for f in range(frames):
-        if kind == "render":
+        if kind in ("render", "batch"):
             _, st = r.render(ds, cams[f], opts, out=out)
         else:
             _, st = r.render(ds, cams[f], opts, color=False, scores=scores)
