@@ -334,15 +334,17 @@ def main():
             "wall_fps": world * args.steps / wall,
             "workload_stats": {"visible_mean": NV / args.steps, "pairs_mean": P_ / args.steps,
                                "evals_per_px": E / args.steps / hw, "composites_per_px": C_ / args.steps / hw},
-            "roofline": {"kernel": "blend_kernel<COLOR>", "bound": "fp32", "achieved": achieved,
+            "roofline": {"kernel": "blend2_kernel<COLOR>", "bound": "fp32", "achieved": achieved,
                          "peak": fp32_peak, "unit": "TFLOP/s", "frac": achieved / fp32_peak,
-                         "traffic": None, "algorithmic": "16*E + 11*C flops per frame (SURVEY §8d)",
+                         "traffic": profiled_traffic("blend2_kernel<1, 0, 0, 1>"),
+                         "traffic_source": TRAFFIC_FILE + " (ncu --set full, dram read+write bytes per launch)",
+                         "algorithmic": "16*E + 11*C flops per frame (SURVEY §8d)",
                          "peak_source": "computed: SMs x 128 FP32 lanes x 2 x sm_max_mhz"},
             "frame_roofline": {"bytes_alg_per_frame": frame_bytes,
                                "achieved_gbs": frame_bytes / (t_max / args.steps / 1e3) / 1e9,
                                "peak_gbs": pk.get("hbm_gbs"),
                                "frac": frame_bytes / (t_max / args.steps / 1e3) / 1e9 / pk.get("hbm_gbs", 6548.8)},
-            "gpu_launches": args.steps * (1 + 5 + 1 + 1 + r_tile_passes(W_, H_) + 1 + 1),
+            "gpu_launches": args.steps * frame_launches(W_, H_),
             "clocks": clk.summary(),
         })
         # e2e: the reference-facing call (rasterize -> RenderOutput with host numpy
@@ -422,6 +424,15 @@ def main():
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         assert int((tab.values >= 0.01).sum()) == kept
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            threads = os.cpu_count() or 1
+            sel = cams[:2]
+            dt, _ = cpu_views(scene, sel, False, threads=threads)
+            result_cpu = {"value": len(sel) / dt, "unit": "views/s", "cores": threads, "kind": "port",
+                          "sample": f"{len(sel)} of the 200 views, each on {threads} threads "
+                                    f"(oracle/cpu_ref.cpp fp32 scoring, tile-parallel), CPU {cpu_model()}"}
+        else:
+            result_cpu = None
         e2e = {"value": n / float(te.item()), "unit": "views/s",
                "h2d_bytes_per_step": (hi - lo) * (C.sizeof(N.RsCamera) + C.sizeof(N.RsOptions)),
                "d2h_bytes_per_step": 4 * len(scene),
@@ -436,7 +447,8 @@ def main():
                        "parallelism": f"views sharded over {world} GPU(s) + NCCL all_reduce(MAX)"},
             "kept_at_0.01": kept, "wall_views_per_s": args.steps * n / wall,
             "e2e": e2e,
-            "gpu_launches": args.steps * len(mine) * (1 + 5 + 1 + 1 + r_tile_passes(W_, H_) + 1 + 1),
+            **({"cpu_baseline": result_cpu} if result_cpu else {}),
+            "gpu_launches": args.steps * len(mine) * frame_launches(W_, H_),
             "clocks": clk.summary(),
         })
     if rank == 0:
@@ -566,7 +578,7 @@ def run_trajectory(args, rank, world, local, dev, opts, r, opt_s, stream, flush,
                    "frames_per_gpu_per_step": per_step, "l2": "flushed (256 MB memset) between timed frames",
                    "parallelism": f"frames split across {world} GPU(s), no communication"},
         "arms": res_arms, "clocks": main_arm["clocks"],
-        "gpu_launches": sum(a["frames"] // world for a in res_arms.values()) * (1 + 5 + 1 + 1 + r_tile_passes(W_, H_) + 1 + 1),
+        "gpu_launches": sum(a["frames"] // world for a in res_arms.values()) * frame_launches(W_, H_),
         "frame_roofline": {"bytes_alg_per_frame": main_arm["bytes_alg_per_frame"],
                            "achieved_gbs": main_arm["bytes_alg_per_frame"] / (main_arm["ms_per_frame"] / 1e3) / 1e9,
                            "peak_gbs": pk.get("hbm_gbs"),
@@ -584,7 +596,8 @@ def run_trajectory(args, rank, world, local, dev, opts, r, opt_s, stream, flush,
             filt, _ = r.render(ds, cam, opts, active_idx=lists[clus(cam)])
             mse = float(((filt["rgb"] - full) ** 2).mean().item())
             ps.append(99.0 if mse == 0 else 10.0 * np.log10(1.0 / mse))
-        extra["psnr_filtered_vs_full_db"] = {"mean": float(np.mean(ps)), "min": float(np.min(ps)), "frames": len(ps)}
+        result["psnr_filtered_vs_full_db"] = {"mean": float(np.mean(ps)), "min": float(np.min(ps)),
+                                              "frames": len(ps)}
     # e2e through the public API (host results every frame)
     from paper_2403_13806_b200.render import rasterize
     from paper_2403_13806_b200.visibility import render_from_viewpoint
@@ -608,6 +621,23 @@ def run_trajectory(args, rank, world, local, dev, opts, r, opt_s, stream, flush,
         print(json.dumps(result), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+TRAFFIC_FILE = "profiles/round1_ncu_full_configs1_traffic.json"
+
+
+def profiled_traffic(kernel: str):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full capture (or None)."""
+    try:
+        return json.loads((ROOT / TRAFFIC_FILE).read_text()).get(kernel)
+    except (OSError, ValueError):
+        return None
+
+
+def frame_launches(W, H):
+    """Kernels per frame: project, depth histogram, 4 depth passes, count, both emitters
+    (one returns at once), the tile passes, ranges, blend."""
+    return 1 + 1 + 4 + 1 + 2 + r_tile_passes(W, H) + 1 + 1
 
 
 def r_tile_passes(W, H):
