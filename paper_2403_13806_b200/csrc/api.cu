@@ -25,7 +25,7 @@ size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
 struct Layout {
   // per-frame zeroed region [0, frame_bytes)
-  size_t ctr, hist, emit_lb, ranges, frame_bytes;
+  size_t ctr, hist, emit_lb, proj_lb, ranges, frame_bytes;
   size_t sticky, cam, recs, tcount, rowtab, keysA, keysB, valsA, valsB, offsets, owners, ptileA, ptileB, pitemA, pitemB, lbA, lbB, total;
 };
 
@@ -39,6 +39,7 @@ Layout make_layout(int64_t n_cap, int64_t pair_cap, int W, int H) {
   L.ctr = take(sizeof(Counters));
   L.hist = take(8 * 256 * sizeof(uint32_t));  // depth passes 0-3, tile passes 4-5
   L.emit_lb = take(((size_t)n_cap / kCountThreads + 2) * sizeof(unsigned long long));
+  L.proj_lb = take(((size_t)n_cap / kCompactKeys + 2) * sizeof(unsigned long long));
   L.ranges = take(TW * TH * sizeof(uint2));
   L.frame_bytes = o;
   L.sticky = take(sizeof(Sticky));
@@ -246,16 +247,16 @@ static int32_t project_impl(rs_workspace* ws, const rs_scene* scene, const int32
   ws->binned = false;
   ws->has_color = color || full;
   if (items > 0) {
-    const unsigned grid = (unsigned)((items + 127) / 128);
+    const unsigned grid = (unsigned)((items + kProjThreads - 1) / kProjThreads);
     if (full)
-      project_kernel<true, true><<<grid, 128, 0, st>>>(
+      project_kernel<true, true><<<grid, kProjThreads, 0, st>>>(
           scene->planes, scene->sh, scene->plane_stride, scene->sh_degree, active_idx, (uint32_t)items, ws->at<rs_camera>(ws->L.cam), *opts,
-          ws->at<Rec>(ws->L.recs), ws->at<uint32_t>(ws->L.keysA), ws->at<uint32_t>(ws->L.tcount), ws->at<uint4>(ws->L.rowtab), ws->ctr(), full,
+          ws->at<Rec>(ws->L.recs), ws->at<uint32_t>(ws->L.keysB), ws->at<uint32_t>(ws->L.tcount), ws->at<uint4>(ws->L.rowtab), ws->ctr(), full,
           reinterpret_cast<int4*>(full_bbox));
     else
-      (color ? project_kernel<false, true> : project_kernel<false, false>)<<<grid, 128, 0, st>>>(
+      (color ? project_kernel<false, true> : project_kernel<false, false>)<<<grid, kProjThreads, 0, st>>>(
           scene->planes, scene->sh, scene->plane_stride, scene->sh_degree, active_idx, (uint32_t)items, ws->at<rs_camera>(ws->L.cam), *opts,
-          ws->at<Rec>(ws->L.recs), ws->at<uint32_t>(ws->L.keysA), ws->at<uint32_t>(ws->L.tcount), ws->at<uint4>(ws->L.rowtab),
+          ws->at<Rec>(ws->L.recs), ws->at<uint32_t>(ws->L.keysB), ws->at<uint32_t>(ws->L.tcount), ws->at<uint4>(ws->L.rowtab),
           ws->ctr(), nullptr, nullptr);
   }
   return cuda_status();
@@ -278,14 +279,17 @@ int32_t rs_bin(rs_workspace* ws, void* stream) {
   cudaStream_t st = S(stream);
   const uint32_t n = ws->n_items;
   if (n > 0) {
-    radix_hist_kernel<<<std::max(1, std::min((int)((n + 255) / 256), ws->sms * 2)), 256, 0, st>>>(
-        ws->at<uint32_t>(ws->L.keysA), n, 4, kSortThreads * kDepthItems, ws->at<uint32_t>(ws->L.hist),
-        ws->at<uint32_t>(ws->L.lbA));
+    // depth sort of the n_visible binned items (compacted in item order by the projection)
+    const uint32_t* nvis = &ws->ctr()->n_visible;
+    compact_hist_kernel<<<(n + kCompactKeys - 1) / kCompactKeys, 256, 0, st>>>(
+        ws->at<uint32_t>(ws->L.keysB), n, ws->at<uint32_t>(ws->L.keysA), ws->at<uint32_t>(ws->L.valsA),
+        ws->at<unsigned long long>(ws->L.proj_lb), ws->ctr(), kSortThreads * kDepthItems,
+        ws->at<uint32_t>(ws->L.hist), ws->at<uint32_t>(ws->L.lbA));
     const uint32_t *keys_res, *items_sorted;
     run_sort<uint32_t, kDepthItems>(ws, ws->at<uint32_t>(ws->L.keysA), ws->at<uint32_t>(ws->L.keysA),
-                                    ws->at<uint32_t>(ws->L.keysB), nullptr, ws->at<uint32_t>(ws->L.valsA),
-                                    ws->at<uint32_t>(ws->L.valsB), nullptr, n, n, 32, 0, 0, false, st, &keys_res,
-                                    &items_sorted);
+                                    ws->at<uint32_t>(ws->L.keysB), ws->at<uint32_t>(ws->L.valsA),
+                                    ws->at<uint32_t>(ws->L.valsA), ws->at<uint32_t>(ws->L.valsB), nvis, 0, n, 32,
+                                    0, 0, false, st, &keys_res, &items_sorted);
     count_kernel<<<(n + kCountThreads - 1) / kCountThreads, kCountThreads, 0, st>>>(items_sorted, ws->at<uint32_t>(ws->L.tcount), ws->ctr(),
                                                   (uint32_t)ws->pair_cap, ws->at<uint32_t>(ws->L.offsets),
                                                   ws->at<uint32_t>(ws->L.owners),

@@ -28,35 +28,8 @@
 
 namespace rs {
 
-enum : unsigned long long { kLbAgg = 1ull << 62, kLbInc = 2ull << 62, kLbMask = (1ull << 62) - 1 };
 constexpr int kEmitPairs = 2048;  // pairs per emit CTA
 constexpr int kCountThreads = 1024;  // ranks per count CTA (few CTAs: short look-back chains)
-
-// Decoupled look-back over 64-bit status words (flag in the top 2 bits);
-// one warp reads 32 predecessors per step.
-__device__ __forceinline__ unsigned long long warp_lookback(volatile unsigned long long* st, uint32_t b, int lane) {
-  unsigned long long excl = 0;
-  int j = (int)b - 1;
-  while (j >= 0) {
-    const int k = j - lane;  // lane 0 = nearest predecessor
-    const unsigned long long s = k >= 0 ? st[k] : (unsigned long long)kLbInc;  // before block 0: inclusive zero
-    const unsigned ready = __ballot_sync(0xffffffffu, (s & ~(unsigned long long)kLbMask) != 0);
-    const unsigned inc = __ballot_sync(0xffffffffu, (s & (unsigned long long)kLbInc) != 0) & ready;
-    const unsigned notready = ~ready;
-    // use the window up to (and including) the nearest inclusive entry, or up to the first
-    // unpublished entry, whichever comes first
-    const int first_inc = inc ? __ffs(inc) - 1 : 32;
-    const int first_nr = notready ? __ffs(notready) - 1 : 32;
-    const int take = first_inc < first_nr ? first_inc + 1 : first_nr;  // lanes [0, take)
-    unsigned long long v = (lane < take && k >= 0) ? (s & (unsigned long long)kLbMask) : 0ull;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    excl += v;
-    if (first_inc < first_nr) break;
-    j -= take;
-  }
-  return excl;
-}
 
 __global__ void __launch_bounds__(kCountThreads) count_kernel(const uint32_t* __restrict__ items_sorted,
                                                     const uint32_t* __restrict__ tcount, Counters* __restrict__ ctr,

@@ -6,10 +6,11 @@
 // the Tier-A fp32 contract of oracle/cpu_ref.cpp:project_one() in the same
 // operation order (compiled with -fmad=false; explicit __fmaf_rn only where
 // the contract fuses), and writes
-//   * a 64-byte Rec for valid items (invalid items write nothing else), and
-//   * the 32-bit depth key (kInvalidKey for culled items) that the depth sort
-//     consumes; culled items sort last.
-// n_visible is counted with one atomic per warp.
+//   * a 64-byte Rec for binned items (culled items write nothing else),
+//   * the binned items' pair counts and tile-row tables (rows.cuh), and
+//   * the binned items' (32-bit depth key, item) compacted in item order
+//     (decoupled look-back over ticket-ordered blocks) for the depth sort,
+//     whose length n_visible the last block publishes.
 #pragma once
 #include "rs_common.cuh"
 #include "rows.cuh"
@@ -263,12 +264,10 @@ __global__ void __launch_bounds__(128) project_kernel(const float* __restrict__ 
         full_bbox[item] = make_int4(x0, x1, y0, y1);
       }
     }
-    keys[item] = binned ? depth_key(depth) : kInvalidKey;
   }
   // pairs per binned record (+ row tables), warp-cooperatively
   warp_count_rows(s_rows, binned, ga, gb, gd, item, tcount, rowtab);
-  const unsigned vb = __ballot_sync(0xffffffffu, binned);
-  if ((threadIdx.x & 31) == 0 && vb) atomicAdd(&ctr->n_visible, (uint32_t)__popc(vb));
+  if (item < n_items) keys[item] = binned ? depth_key(gb.w) : kInvalidKey;
 }
 
 }  // namespace rs

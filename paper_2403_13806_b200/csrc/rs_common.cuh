@@ -9,6 +9,7 @@ namespace rs {
 
 constexpr int kTile = 16;          // 16x16 pixel tiles, one CTA of 256 threads each
 constexpr int kBlendThreads = 256;
+constexpr int kProjThreads = 128;  // projection CTA (rows.cuh RowCountSmem is sized for it)
 constexpr uint32_t kInvalidKey = 0xffffffffu;
 constexpr int kPlanes = 59;
 
@@ -48,9 +49,38 @@ struct Counters {
   uint32_t tickets[16];  // onesweep chunk tickets, one per pass
   uint32_t emit_ctr;     // decoupled look-back ticket of the pair counter
   uint32_t emit_work;    // rank-chunk work counter of the pair emitter
-  uint32_t pad[4];
+  uint32_t proj_ticket;  // logical block ticket of the projection's compaction
+  uint32_t pad[3];
 };
 static_assert(sizeof(Counters) == 128, "Counters is 128 B");
+
+enum : unsigned long long { kLbAgg = 1ull << 62, kLbInc = 2ull << 62, kLbMask = (1ull << 62) - 1 };
+
+// Decoupled look-back over 64-bit status words (flag in the top 2 bits);
+// one warp reads 32 predecessors per step.
+__device__ __forceinline__ unsigned long long warp_lookback(volatile unsigned long long* st, uint32_t b, int lane) {
+  unsigned long long excl = 0;
+  int j = (int)b - 1;
+  while (j >= 0) {
+    const int k = j - lane;  // lane 0 = nearest predecessor
+    const unsigned long long s = k >= 0 ? st[k] : (unsigned long long)kLbInc;  // before block 0: inclusive zero
+    const unsigned ready = __ballot_sync(0xffffffffu, (s & ~(unsigned long long)kLbMask) != 0);
+    const unsigned inc = __ballot_sync(0xffffffffu, (s & (unsigned long long)kLbInc) != 0) & ready;
+    const unsigned notready = ~ready;
+    // use the window up to (and including) the nearest inclusive entry, or up to the first
+    // unpublished entry, whichever comes first
+    const int first_inc = inc ? __ffs(inc) - 1 : 32;
+    const int first_nr = notready ? __ffs(notready) - 1 : 32;
+    const int take = first_inc < first_nr ? first_inc + 1 : first_nr;  // lanes [0, take)
+    unsigned long long v = (lane < take && k >= 0) ? (s & (unsigned long long)kLbMask) : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    excl += v;
+    if (first_inc < first_nr) break;
+    j -= take;
+  }
+  return excl;
+}
 
 // Overflow record that outlives the per-frame counter reset: a batch of frames
 // (e.g. a scoring pass) is launched without host syncs and checked once.

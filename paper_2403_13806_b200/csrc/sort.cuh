@@ -1,15 +1,15 @@
 // sort.cuh -- hand-written stable LSD radix sort (onesweep, 8-bit digits).
 //
 // Replaces np.lexsort (render.py:218-222) twice per frame:
-//   * depth sort: 32-bit depth keys of all n items (culled = 0xffffffff, last),
-//     values = item index (implicit on the first pass), 4 passes;
+//   * depth sort: 32-bit depth keys of the n_visible binned items, values =
+//     item index (compacted in item order by compact_hist_kernel), 4 passes;
 //   * tile sort:  16-bit tile ids of the P Gaussian-tile pairs emitted in
 //     (depth, index) order, values = item id, ceil(tile_bits/8) passes.
 // Stability makes the per-tile order exactly the reference's (depth, index)
 // order restricted to the tile.
 //
-// Digit histograms of every pass come from the key producer (radix_hist_kernel
-// for depth keys, emit_kernel for tile ids), so each pass is ONE kernel: CTAs
+// Digit histograms of every pass come from the key producer (compact_hist_kernel
+// for depth keys, the emitters for tile ids), so each pass is ONE kernel: CTAs
 // take chunks of 256*ITEMS keys in launch order from an atomic ticket, rank
 // keys inside the chunk with a warp multisplit (match_any for narrow digits,
 // per-bit ballots for 7-8 bit digits, whichever measured faster), publish
@@ -34,30 +34,81 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   return m;
 }
 
-// Digit histograms of all passes of a 32-bit key sort (per-warp shared
-// sub-histograms), plus zeroing of the first pass's look-back words.
-// hist must be zero on entry.
-__global__ void __launch_bounds__(256) radix_hist_kernel(const uint32_t* __restrict__ keys, uint32_t n, int passes,
-                                                         uint32_t chunk, uint32_t* __restrict__ hist,
-                                                         uint32_t* __restrict__ lookback0) {
-  __shared__ uint32_t sh[8][4][256];
-  const int warp = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < 8 * 4 * 256; i += blockDim.x) (&sh[0][0][0])[i] = 0;
+// Order-preserving compaction of the binned items' depth keys (culled items carry
+// kInvalidKey) into (key, item) arrays for the depth sort, plus the digit histograms of
+// all 4 passes over the compacted keys and zeroing of the first pass's look-back words.
+// CTAs take chunks of kCompactKeys items from a ticket and find their output offset by
+// decoupled look-back; the last chunk publishes n_visible. hist must be zero on entry.
+constexpr int kCompactKeys = 256 * 16;
+
+__global__ void __launch_bounds__(256) compact_hist_kernel(const uint32_t* __restrict__ keys_all, uint32_t n,
+                                                           uint32_t* __restrict__ keys_out,
+                                                           uint32_t* __restrict__ vals_out,
+                                                           unsigned long long* __restrict__ status,
+                                                           Counters* __restrict__ ctr, uint32_t chunk,
+                                                           uint32_t* __restrict__ hist,
+                                                           uint32_t* __restrict__ lookback0) {
+  constexpr int IT = kCompactKeys / 256;
+  __shared__ uint32_t sh[4][4][256];  // 4 warp pairs x 4 digits
+  __shared__ uint32_t s_wcnt[8], s_blk;
+  __shared__ unsigned long long s_base;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_blk = atomicAdd(&ctr->proj_ticket, 1u);
+  for (int i = tid; i < 4 * 4 * 256; i += 256) (&sh[0][0][0])[i] = 0;
   __syncthreads();
-  const uint32_t stride = gridDim.x * blockDim.x;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const uint32_t k = keys[i];
-    for (int p = 0; p < passes; ++p) atomicAdd(&sh[warp][p][(k >> (8 * p)) & 0xffu], 1u);
+  const uint32_t b = s_blk, nb = (n + kCompactKeys - 1) / kCompactKeys;
+  const uint32_t base = b * kCompactKeys + warp * 32 * IT;  // warp-contiguous items, lane-minor
+  uint32_t k[IT];
+  uint32_t cnt = 0;
+#pragma unroll
+  for (int it = 0; it < IT; ++it) {
+    const uint32_t i = base + it * 32 + lane;
+    k[it] = i < n ? keys_all[i] : kInvalidKey;
+    cnt += k[it] != kInvalidKey;
+  }
+  // warp count (in item order within the warp: item-major, lane-minor)
+  uint32_t wc = cnt;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) wc += __shfl_xor_sync(0xffffffffu, wc, o);
+  if (lane == 0) s_wcnt[warp] = wc;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t total = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) total += s_wcnt[w];
+    volatile unsigned long long* st = status;
+    if (lane == 0) st[b] = (b == 0 ? kLbInc : kLbAgg) | total;
+    const unsigned long long excl = b == 0 ? 0ull : warp_lookback(st, b, lane);
+    if (lane == 0) {
+      if (b) st[b] = kLbInc | (excl + total);
+      s_base = excl;
+      if (b == nb - 1) ctr->n_visible = (uint32_t)(excl + total);
+    }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < passes * 256; i += blockDim.x) {
-    uint32_t v = 0;
+  uint32_t pos = (uint32_t)s_base;
+  for (int w = 0; w < warp; ++w) pos += s_wcnt[w];
 #pragma unroll
-    for (int w = 0; w < 8; ++w) v += (&sh[w][0][0])[i];
+  for (int it = 0; it < IT; ++it) {
+    const bool v = k[it] != kInvalidKey;
+    const unsigned bal = __ballot_sync(0xffffffffu, v);
+    if (v) {
+      const uint32_t at = pos + (uint32_t)__popc(bal & ((1u << lane) - 1u));
+      keys_out[at] = k[it];
+      vals_out[at] = base + it * 32 + lane;
+#pragma unroll
+      for (int p = 0; p < 4; ++p) atomicAdd(&sh[warp >> 1][p][(k[it] >> (8 * p)) & 0xffu], 1u);
+    }
+    pos += (uint32_t)__popc(bal);
+  }
+  __syncthreads();
+  for (int i = tid; i < 4 * 256; i += 256) {
+    const uint32_t v = sh[0][0][i] + sh[1][0][i] + sh[2][0][i] + sh[3][0][i];
     if (v) atomicAdd(&hist[i], v);
   }
+  // the first depth pass's look-back words: sized for every item (n_visible is not known yet)
   const uint32_t words = (n + chunk - 1) / chunk * 256u;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < words; i += stride) lookback0[i] = 0;
+  for (uint32_t i = b * 256 + tid; i < words; i += nb * 256) lookback0[i] = 0;
 }
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, uint32_t src_bytes) {
