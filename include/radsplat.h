@@ -19,6 +19,11 @@
  *                           io.py:198-243 LSB-first RVIS bitsets
  *   rs_check_finite      <- core.py:522-525 GaussianScene.is_finite
  *   rs_max_merge         <- render.py:84-85 ContributionAccumulator.update
+ *   rs_rspl_unpack /
+ *   rs_rspl_pack         <- io.py:128-191 load_scene / save_scene payload
+ *                           (RSPL file bytes straight to / from HBM)
+ *   rs_pack_bits         <- io.py:198-215 np.packbits(bitorder="little") of
+ *                           save_visibility
  *
  * Conventions
  *   - All data pointers are DEVICE pointers (rs_outputs' 64-bit images may be
@@ -216,6 +221,18 @@ RS_API int32_t rs_compact_bits(const uint8_t* bits, int64_t n, int32_t* out_idx,
 
 /* *out_bad (device) = number of non-finite scene values (planes and SH rows; 0 = finite). */
 RS_API int32_t rs_check_finite(const rs_scene* scene, uint32_t* out_bad, void* stream);
+
+/* RSPL payload (device, 16-B aligned: positions (n,3), log-scales (n,3),
+ * quaternions w-x-y-z (n,4), opacity logits (n), SH (n,48), fp32) -> device
+ * scene planes (see rs_scene) + SH rows; quaternions normalized in fp64 like
+ * the reference's GaussianScene (core.py:111-117), *out_bad (device) = number
+ * of zero quaternions. rs_rspl_pack is the inverse. */
+RS_API int32_t rs_rspl_unpack(const float* payload, int64_t n, float* planes, int64_t plane_stride, float* sh,
+                              uint32_t* out_bad, void* stream);
+RS_API int32_t rs_rspl_pack(const float* planes, int64_t plane_stride, const float* sh, int64_t n, float* payload,
+                            void* stream);
+/* n flags (bytes, nonzero = set) -> ceil(n/8) bytes of LSB-first bits (RVIS indicator). */
+RS_API int32_t rs_pack_bits(const uint8_t* flags, int64_t n, uint8_t* bits, void* stream);
 
 /* dst[i] = max(dst[i], src[i]) over n non-negative floats. */
 RS_API int32_t rs_max_merge(float* dst, const float* src, int64_t n, void* stream);

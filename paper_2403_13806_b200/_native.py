@@ -90,6 +90,9 @@ SIGNATURES = {
     "rs_compact_bits": (_i32, [_vp, _i64, _vp, _vp, _vp, _sz, _vp]),
     "rs_check_finite": (_i32, [C.POINTER(RsScene), _vp, _vp]),
     "rs_max_merge": (_i32, [_vp, _vp, _i64, _vp]),
+    "rs_rspl_unpack": (_i32, [_vp, _i64, _vp, _i64, _vp, _vp, _vp]),
+    "rs_rspl_pack": (_i32, [_vp, _i64, _vp, _i64, _vp, _vp]),
+    "rs_pack_bits": (_i32, [_vp, _i64, _vp, _vp]),
 }
 
 _lib = None

@@ -42,6 +42,10 @@ class StaleTableError(RuntimeError):
     """A per-Gaussian table was computed against a different scene revision."""
 
 
+class FileFormatError(IOError):
+    """A persisted file has the wrong magic or an unsupported version (core.py:35-36)."""
+
+
 SH_C0 = 0.28209479177387814
 SH_BANDS_FOR_DEGREE = (1, 4, 9, 16)
 SH_COLOR_OFFSET = 0.5

@@ -14,6 +14,7 @@
 #include "bin.cuh"
 #include "blend.cuh"
 #include "compact.cuh"
+#include "io.cuh"
 #include "project.cuh"
 #include "sort.cuh"
 
@@ -475,6 +476,34 @@ int32_t rs_check_finite(const rs_scene* scene, uint32_t* out_bad, void* stream) 
   cudaStream_t st = S(stream);
   cudaMemsetAsync(out_bad, 0, 4, st);
   if (scene->n > 0) finite_kernel<<<1184, 256, 0, st>>>(scene->planes, scene->sh, scene->n, scene->plane_stride, out_bad);
+  return cuda_status();
+}
+
+int32_t rs_rspl_unpack(const float* payload, int64_t n, float* planes, int64_t plane_stride, float* sh,
+                       uint32_t* out_bad, void* stream) {
+  if (n < 0 || plane_stride < n || !out_bad || (n > 0 && (!payload || !planes || !sh)) ||
+      (reinterpret_cast<uintptr_t>(payload) & 15) || (reinterpret_cast<uintptr_t>(sh) & 15))
+    return RS_EINVAL;
+  cudaStream_t st = S(stream);
+  cudaMemsetAsync(out_bad, 0, 4, st);
+  if (n > 0)
+    rspl_unpack_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(payload, n, planes, plane_stride, sh, out_bad);
+  return cuda_status();
+}
+
+int32_t rs_rspl_pack(const float* planes, int64_t plane_stride, const float* sh, int64_t n, float* payload,
+                     void* stream) {
+  if (n < 0 || plane_stride < n || (n > 0 && (!payload || !planes || !sh)) ||
+      (reinterpret_cast<uintptr_t>(payload) & 15) || (reinterpret_cast<uintptr_t>(sh) & 15))
+    return RS_EINVAL;
+  if (n > 0)
+    rspl_pack_kernel<<<(unsigned)((n + 255) / 256), 256, 0, S(stream)>>>(planes, plane_stride, sh, n, payload);
+  return cuda_status();
+}
+
+int32_t rs_pack_bits(const uint8_t* flags, int64_t n, uint8_t* bits, void* stream) {
+  if (n < 0 || (n > 0 && (!flags || !bits))) return RS_EINVAL;
+  if (n > 0) pack_bits_kernel<<<(unsigned)((n + 255) / 256), 256, 0, S(stream)>>>(flags, n, bits);
   return cuda_status();
 }
 

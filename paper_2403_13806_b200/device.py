@@ -73,6 +73,30 @@ class DeviceScene:
                 if int(bad.item()) != 0:
                     raise InvalidSceneError("scene contains non-finite parameters")
 
+    @classmethod
+    def from_tensors(cls, planes: torch.Tensor, sh: torch.Tensor, sh_degree: int, n: int | None = None,
+                     generation=None, check_finite: bool = True) -> "DeviceScene":
+        """Wrap device tensors already in the scene layout ((11, N) planes, (N, 48) SH rows),
+        e.g. an RSPL payload unpacked on the device (io.load_scene_device)."""
+        self = cls.__new__(cls)
+        lib = N.load()
+        self.device = planes.device
+        self.n = int(planes.shape[1]) if n is None else int(n)
+        self.sh_degree = int(sh_degree)
+        if not 0 <= self.sh_degree <= 3:
+            raise InvalidParameterError("active SH degree must be in 0..3")
+        self.generation = generation
+        self.planes, self.sh = planes, sh
+        self.struct = N.RsScene(planes.data_ptr(), sh.data_ptr(), self.n, max(self.n, 1), self.sh_degree, 0)
+        if check_finite and self.n:
+            with torch.cuda.device(self.device):
+                bad = torch.zeros(1, dtype=torch.int32, device=self.device)
+                N.check(lib.rs_check_finite(C.byref(self.struct), bad.data_ptr(),
+                                            torch.cuda.current_stream(self.device).cuda_stream), "check_finite")
+                if int(bad.item()) != 0:
+                    raise InvalidSceneError("scene contains non-finite parameters")
+        return self
+
     def __len__(self):
         return self.n
 

@@ -234,8 +234,43 @@ def main():
     for i, c in enumerate(cases["cases"]):
         assert c["active_count"] == d[f"pose{i}_active"] and c["cluster_index"] == d[f"pose{i}_cluster"]
     np.savez_compressed(HERE / "viewer_parity.npz", **d)
+
+    make_io(fs, conftest)
     print("golden fixtures written to", HERE)
 
 
+def make_io(fs, conftest):
+    """I: wire formats (io.py:128-243): reference-written RSPL / RVIS bytes."""
+    import tempfile
+    d = {}
+    with tempfile.TemporaryDirectory() as tmp:
+        rng = np.random.default_rng(1234)
+        for name, scene in (("s17", conftest.random_scene(rng, 17, sh_degree=2)),
+                            ("s1", conftest.random_scene(rng, 1, sh_degree=0)),
+                            ("room", fs.synthetic.make_two_room_scene(
+                                fs.synthetic.SyntheticSpec(kind="two_room", image_size=24, n_per_room=48),
+                                np.random.default_rng(0)))):
+            scene.metadata["prune_removed"] = 7
+            path = Path(tmp) / f"{name}.rspl"
+            fs.io.save_scene(scene, path, sidecar={"stage": "golden"})
+            d[name + "_rspl"] = np.frombuffer(path.read_bytes(), np.uint8)
+            d[name + "_json"] = np.frombuffer((Path(str(path) + ".json")).read_bytes(), np.uint8)
+            back = fs.io.load_scene(path)
+            pack_scene(d, name + "_", back)
+        vis = fs.visibility.ClusterVisibility(centers=rng.uniform(-5, 5, size=(3, 3)),
+                                              indicators=rng.uniform(size=(3, 45)) > 0.5,
+                                              t_cluster=0.001, scene_generation=42)
+        path = Path(tmp) / "v.rvis"
+        fs.io.save_visibility(vis, path)
+        d["vis_rvis"] = np.frombuffer(path.read_bytes(), np.uint8)
+        d["vis_indicators"] = vis.indicators
+        d["vis_centers"] = vis.centers
+    np.savez_compressed(HERE / "io.npz", **d)
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["io"]:  # only the wire-format fixtures
+        fs_, conftest_, _ = import_reference()
+        make_io(fs_, conftest_)
+    else:
+        main()
