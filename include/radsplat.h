@@ -19,6 +19,8 @@
  *                           io.py:198-243 LSB-first RVIS bitsets
  *   rs_check_finite      <- core.py:522-525 GaussianScene.is_finite
  *   rs_max_merge         <- render.py:84-85 ContributionAccumulator.update
+ *   rs_backward          <- render.py:328-487 rasterize_backward +
+ *                           _chain_to_parameters (after a training forward)
  *   rs_rspl_unpack /
  *   rs_rspl_pack         <- io.py:128-191 load_scene / save_scene payload
  *                           (RSPL file bytes straight to / from HBM)
@@ -116,6 +118,11 @@ typedef struct rs_outputs {
   double* rgb64;
   double* alpha64;
   int64_t* count64;
+  /* training forward (rasterize_cached, render.py:318-321): per pixel the
+   * final transmittance and the pair index of its last composited entry
+   * (-1: none), which rs_backward walks back from. */
+  float* tau;
+  int32_t* last;
 } rs_outputs;
 
 /* Per-frame counters (device side; copied out by rs_read_stats). */
@@ -200,6 +207,19 @@ RS_API int32_t rs_blend(rs_workspace* ws, const rs_options* opts, float* out_rgb
                  int32_t* out_count, uint32_t* scores, uint32_t flags, void* stream);
 RS_API int32_t rs_blend_ex(rs_workspace* ws, const rs_options* opts, const rs_outputs* out, uint32_t* scores,
                            uint32_t flags, void* stream);
+
+/* Gradients of a scalar loss through the image of the frame the last
+ * rs_render_ex on this workspace produced with rs_outputs tau / last (the
+ * training forward, render.py:318-321): grad_image = dL/dcolor (H*W*3, device),
+ * outputs per scene Gaussian (device, zeroed here): positions (n,3), sh (n,48),
+ * log-scales (n,3), quaternions (n,4), opacity logits (n), |dL/dmean2d| (n),
+ * touched (n bytes). Same scene / active list as that forward. fp32; the
+ * per-Gaussian sums are atomics, so results match the reference to a
+ * tolerance, not bit for bit. */
+RS_API int32_t rs_backward(rs_workspace* ws, const rs_scene* scene, const int32_t* active_idx, int64_t m,
+                           const rs_options* opts, const float* grad_image, const float* tau, const int32_t* last,
+                           float* g_pos, float* g_sh, float* g_ls, float* g_quat, float* g_logit, float* g_mean2d,
+                           uint8_t* touched, void* stream);
 
 /* Copy the device counters to host memory (synchronizes `stream`). */
 RS_API int32_t rs_read_stats(rs_workspace* ws, rs_stats* out, void* stream);

@@ -48,7 +48,8 @@ class RsOptions(C.Structure):
 
 
 class RsOutputs(C.Structure):
-    _fields_ = [(n, C.c_void_p) for n in ("rgb", "alpha", "depth", "count", "rgb64", "alpha64", "count64")]
+    _fields_ = [(n, C.c_void_p) for n in ("rgb", "alpha", "depth", "count", "rgb64", "alpha64", "count64", "tau",
+                                          "last")]
 
 
 class RsStats(C.Structure):
@@ -90,6 +91,8 @@ SIGNATURES = {
     "rs_compact_bits": (_i32, [_vp, _i64, _vp, _vp, _vp, _sz, _vp]),
     "rs_check_finite": (_i32, [C.POINTER(RsScene), _vp, _vp]),
     "rs_max_merge": (_i32, [_vp, _vp, _i64, _vp]),
+    "rs_backward": (_i32, [_vp, C.POINTER(RsScene), _vp, _i64, C.POINTER(RsOptions), _vp, _vp, _vp, _vp, _vp, _vp,
+                           _vp, _vp, _vp, _vp, _vp]),
     "rs_rspl_unpack": (_i32, [_vp, _i64, _vp, _i64, _vp, _vp, _vp]),
     "rs_rspl_pack": (_i32, [_vp, _i64, _vp, _i64, _vp, _vp]),
     "rs_pack_bits": (_i32, [_vp, _i64, _vp, _vp]),

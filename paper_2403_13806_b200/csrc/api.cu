@@ -15,6 +15,7 @@
 #include "blend.cuh"
 #include "compact.cuh"
 #include "io.cuh"
+#include "backward.cuh"
 #include "project.cuh"
 #include "sort.cuh"
 
@@ -27,7 +28,7 @@ size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 struct Layout {
   // per-frame zeroed region [0, frame_bytes)
   size_t ctr, hist, emit_lb, proj_lb, ranges, frame_bytes;
-  size_t sticky, cam, recs, tcount, rowtab, keysA, keysB, valsA, valsB, offsets, owners, ptileA, ptileB, pitemA, pitemB, lbA, lbB, total;
+  size_t sticky, cam, recs, tcount, rowtab, sgrad, titem, keysA, keysB, valsA, valsB, offsets, owners, ptileA, ptileB, pitemA, pitemB, lbA, lbB, total;
 };
 
 int tiles_x(int w) { return (w + kTile - 1) / kTile; }
@@ -48,6 +49,8 @@ Layout make_layout(int64_t n_cap, int64_t pair_cap, int W, int H) {
   L.recs = take((size_t)n_cap * sizeof(Rec));
   L.tcount = take((size_t)n_cap * 4);
   L.rowtab = take((size_t)n_cap * 4 * kRowTab);
+  L.sgrad = take((size_t)n_cap * 4 * kSGrad);  // rs_backward: screen-space gradient sums per item
+  L.titem = take((size_t)n_cap);
   L.keysA = take((size_t)n_cap * 4);
   L.keysB = take((size_t)n_cap * 4);
   L.valsA = take((size_t)n_cap * 4);
@@ -337,11 +340,12 @@ int32_t rs_blend_ex(rs_workspace* ws, const rs_options* opts, const rs_outputs* 
   if ((out.rgb != nullptr) != (out.alpha != nullptr) || (out.rgb != nullptr) != (out.count != nullptr) ||
       (out.rgb64 != nullptr) != (out.alpha64 != nullptr) || (out.rgb64 != nullptr) != (out.count64 != nullptr))
     return RS_EINVAL;
-  const bool color = out.rgb || out.rgb64 || out.depth;
+  const bool color = out.rgb || out.rgb64 || out.depth || out.tau;
+  if ((out.tau != nullptr) != (out.last != nullptr)) return RS_EINVAL;
   if (color && !ws->has_color) return RS_EINVAL;  // projected by a score-only rs_render
   if (!color && !scores) return RS_EINVAL;
   const bool stats = (flags & RS_FLAG_COUNT_EVALS) != 0;
-  const bool one_px = (flags & RS_FLAG_BLEND_1PX) != 0;
+  const bool one_px = (flags & RS_FLAG_BLEND_1PX) != 0 && !out.tau;  // the training outputs: 2-px kernel
   cudaStream_t st = S(stream);
   const int T = ws->TW * ws->TH;
   const uint2* ranges = ws->at<uint2>(ws->L.ranges);
@@ -359,7 +363,19 @@ int32_t rs_blend_ex(rs_workspace* ws, const rs_options* opts, const rs_outputs* 
   if (fast) { RS_BLEND(C, I, K, true); } else { RS_BLEND(C, I, K, false); }
   // exact-range exp2 is only needed for degenerate options (see blend.cuh FAST)
   const bool fast = opts->alpha_cut >= 1e-30f;
-  if (color && scores) {
+  if (out.tau) {  // training forward (rasterize_cached): records tau and the last composite per pixel
+    if (scores) {
+      if (fast) blend2_kernel<true, true, false, true, true><<<T, kBlend2Threads, 0, st>>>(
+          ranges, items, recs, ctr, ws->W, ws->H, ws->TW, *opts, out, scores);
+      else blend2_kernel<true, true, false, false, true><<<T, kBlend2Threads, 0, st>>>(
+          ranges, items, recs, ctr, ws->W, ws->H, ws->TW, *opts, out, scores);
+    } else {
+      if (fast) blend2_kernel<true, false, false, true, true><<<T, kBlend2Threads, 0, st>>>(
+          ranges, items, recs, ctr, ws->W, ws->H, ws->TW, *opts, out, scores);
+      else blend2_kernel<true, false, false, false, true><<<T, kBlend2Threads, 0, st>>>(
+          ranges, items, recs, ctr, ws->W, ws->H, ws->TW, *opts, out, scores);
+    }
+  } else if (color && scores) {
     if (stats) { RS_BLEND_F(true, true, true); } else { RS_BLEND_F(true, true, false); }
   } else if (color) {
     if (stats) { RS_BLEND_F(true, false, true); } else { RS_BLEND_F(true, false, false); }
@@ -374,7 +390,7 @@ int32_t rs_blend_ex(rs_workspace* ws, const rs_options* opts, const rs_outputs* 
 int32_t rs_blend(rs_workspace* ws, const rs_options* opts, float* out_rgb, float* out_alpha, float* out_depth,
                  int32_t* out_count, uint32_t* scores, uint32_t flags, void* stream) {
   if (out_rgb && (!out_alpha || !out_depth || !out_count)) return RS_EINVAL;
-  const rs_outputs out{out_rgb, out_alpha, out_depth, out_count, nullptr, nullptr, nullptr};
+  const rs_outputs out{out_rgb, out_alpha, out_depth, out_count, nullptr, nullptr, nullptr, nullptr, nullptr};
   return rs_blend_ex(ws, opts, &out, scores, flags, stream);
 }
 
@@ -382,7 +398,7 @@ int32_t rs_render_ex(rs_workspace* ws, const rs_scene* scene, const int32_t* act
                      const rs_camera* cam, const rs_options* opts, const rs_outputs* out, uint32_t* scores,
                      uint32_t flags, void* stream) {
   // a score-only frame (no image outputs) projects without the SH colour
-  const bool color = out && (out->rgb || out->rgb64 || out->depth);
+  const bool color = out && (out->rgb || out->rgb64 || out->depth || out->tau);
   int32_t s = project_impl(ws, scene, active_idx, m, cam, opts, nullptr, nullptr, color, stream);
   if (s != RS_OK) return s;
   if ((s = rs_bin(ws, stream)) != RS_OK) return s;
@@ -393,8 +409,39 @@ int32_t rs_render(rs_workspace* ws, const rs_scene* scene, const int32_t* active
                   const rs_camera* cam, const rs_options* opts, float* out_rgb, float* out_alpha, float* out_depth,
                   int32_t* out_count, uint32_t* scores, uint32_t flags, void* stream) {
   if (out_rgb && (!out_alpha || !out_depth || !out_count)) return RS_EINVAL;
-  const rs_outputs out{out_rgb, out_alpha, out_depth, out_count, nullptr, nullptr, nullptr};
+  const rs_outputs out{out_rgb, out_alpha, out_depth, out_count, nullptr, nullptr, nullptr, nullptr, nullptr};
   return rs_render_ex(ws, scene, active_idx, m, cam, opts, &out, scores, flags, stream);
+}
+
+int32_t rs_backward(rs_workspace* ws, const rs_scene* scene, const int32_t* active_idx, int64_t m,
+                    const rs_options* opts, const float* grad_image, const float* tau, const int32_t* last,
+                    float* g_pos, float* g_sh, float* g_ls, float* g_quat, float* g_logit, float* g_mean2d,
+                    uint8_t* touched, void* stream) {
+  if (!ws || !scene || !opts || !grad_image || !tau || !last || !g_pos || !g_sh || !g_ls || !g_quat || !g_logit ||
+      !g_mean2d || !touched || !ws->binned || !ws->has_color)
+    return RS_EINVAL;
+  const int64_t items = active_idx ? m : scene->n;
+  if (items != (int64_t)ws->n_items) return RS_EINVAL;  // not the frame rs_render_ex just produced
+  cudaStream_t st = S(stream);
+  const int64_t n = scene->n;
+  cudaMemsetAsync(g_pos, 0, (size_t)n * 12, st);
+  cudaMemsetAsync(g_sh, 0, (size_t)n * 192, st);
+  cudaMemsetAsync(g_ls, 0, (size_t)n * 12, st);
+  cudaMemsetAsync(g_quat, 0, (size_t)n * 16, st);
+  cudaMemsetAsync(g_logit, 0, (size_t)n * 4, st);
+  cudaMemsetAsync(g_mean2d, 0, (size_t)n * 4, st);
+  cudaMemsetAsync(touched, 0, (size_t)n, st);
+  if (items == 0) return cuda_status();
+  cudaMemsetAsync(ws->at<float>(ws->L.sgrad), 0, (size_t)items * 4 * kSGrad, st);
+  cudaMemsetAsync(ws->at<uint8_t>(ws->L.titem), 0, (size_t)items, st);
+  backward_blend_kernel<<<ws->TW * ws->TH, kBlendThreads, 0, st>>>(
+      ws->at<uint2>(ws->L.ranges), final_pair_items(ws), ws->at<Rec>(ws->L.recs), ws->ctr(), ws->W, ws->H, ws->TW,
+      *opts, grad_image, tau, last, ws->at<float>(ws->L.sgrad), ws->at<uint8_t>(ws->L.titem));
+  chain_kernel<<<(unsigned)((items + 127) / 128), 128, 0, st>>>(
+      scene->planes, scene->sh, scene->plane_stride, scene->sh_degree, active_idx, (uint32_t)items,
+      ws->at<rs_camera>(ws->L.cam), *opts, ws->at<float>(ws->L.sgrad), ws->at<uint8_t>(ws->L.titem), g_pos, g_sh,
+      g_ls, g_quat, g_logit, g_mean2d, touched);
+  return cuda_status();
 }
 
 int32_t rs_read_stats(rs_workspace* ws, rs_stats* out, void* stream) {

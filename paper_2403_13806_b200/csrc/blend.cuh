@@ -237,7 +237,9 @@ __device__ __forceinline__ float blend_px(const float4 ga, const float4 gb, cons
   return w;
 }
 
-template <bool COLOR, bool CONTRIB, bool STATS, bool FAST>
+// TRAIN: also record each pixel's final transmittance and last composited pair index
+// (rs_outputs tau / last) for rs_backward.
+template <bool COLOR, bool CONTRIB, bool STATS, bool FAST, bool TRAIN = false>
 __global__ void __launch_bounds__(kBlend2Threads) blend2_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ pair_items, const Rec* __restrict__ recs,
     Counters* __restrict__ ctr, int W, int H, int TW, rs_options o, const rs_outputs out,
@@ -266,6 +268,7 @@ __global__ void __launch_bounds__(kBlend2Threads) blend2_kernel(
   float tau0 = 1.0f, r0 = 0.0f, g0 = 0.0f, b0 = 0.0f, d0 = 0.0f;
   float tau1 = 1.0f, r1 = 0.0f, g1 = 0.0f, b1 = 0.0f, d1 = 0.0f;
   int cnt0 = 0, cnt1 = 0;
+  int last0 = -1, last1 = -1;  // pair index of each pixel's last composite (training outputs)
   unsigned long long evals = 0;
   const bool start = 1.0f >= o.tau_stop;
   bool done0 = !in0 || !start, done1 = !in1 || !start;
@@ -348,6 +351,11 @@ __global__ void __launch_bounds__(kBlend2Threads) blend2_kernel(
           }
           cnt0 += c0 ? 1 : 0;
           cnt1 += c1 ? 1 : 0;
+          if (TRAIN) {
+            const int k = (int)base + s_list[warp][q];
+            last0 = c0 ? k : last0;
+            last1 = c1 ? k : last1;
+          }
           tau0 = c0 ? __fmul_rn(tau0, __fsub_rn(1.0f, al0)) : tau0;
           tau1 = c1 ? __fmul_rn(tau1, __fsub_rn(1.0f, al1)) : tau1;
           done0 = done0 || tau0 < o.tau_stop;
@@ -391,6 +399,10 @@ __global__ void __launch_bounds__(kBlend2Threads) blend2_kernel(
     if (out.depth) {
       if (in0) out.depth[(size_t)py0 * W + px] = d0;
       if (in1) out.depth[(size_t)py1 * W + px] = d1;
+    }
+    if (TRAIN) {
+      if (in0) { out.tau[(size_t)py0 * W + px] = tau0; out.last[(size_t)py0 * W + px] = last0; }
+      if (in1) { out.tau[(size_t)py1 * W + px] = tau1; out.last[(size_t)py1 * W + px] = last1; }
     }
     if (out.rgb64) {
       // reference-typed images written straight to (mapped host) memory in whole tile rows,

@@ -152,6 +152,7 @@ class Renderer:
         self.buf = None
         self.handle = C.c_void_p()
         self.caps = (0, 0, 0, 0)
+        self.frame_id = 0  # frames launched on this workspace (rs_backward needs the latest one)
 
     # -- workspace ---------------------------------------------------------
     def ensure(self, n: int, pairs: int, width: int, height: int) -> None:
@@ -240,12 +241,13 @@ class Renderer:
         rgb/alpha/depth/count and/or reference-typed rgb64/alpha64/count64, which may
         live in pinned host memory)."""
         return N.RsOutputs(*(out[k].data_ptr() if k in out else None for k in
-                             ("rgb", "alpha", "depth", "count", "rgb64", "alpha64", "count64")))
+                             ("rgb", "alpha", "depth", "count", "rgb64", "alpha64", "count64", "tau", "last")))
 
     def launch(self, ds: DeviceScene, cam_s: N.RsCamera, opt_s: N.RsOptions, out: dict,
                scores: torch.Tensor | None = None, active_idx: torch.Tensor | None = None,
                m: int = 0, flags: int = 0) -> None:
         """Enqueue one frame (no host synchronization)."""
+        self.frame_id += 1
         N.check(self.lib.rs_render_ex(
             self.handle, C.byref(ds.struct), active_idx.data_ptr() if active_idx is not None else None,
             int(m), C.byref(cam_s), C.byref(opt_s), C.byref(self.outputs_struct(out)),
@@ -367,6 +369,7 @@ class FrameGraph:
             raise RuntimeError("the workspace was re-allocated after capture; capture again")
         if cam is not None:
             self.set_camera(cam)
+        self.r.frame_id += 1
         self.graph.replay()
 
 

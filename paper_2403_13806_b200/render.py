@@ -10,6 +10,8 @@ changing the import:
 * ``project_gaussian`` / ``project_scene`` (:161-211)
 * ``rasterize`` (:290-293), ``rasterize_with_contributions`` (:296-308),
   ``rasterize_filtered`` (:311-315)
+* ``rasterize_cached`` (:318-321) and ``rasterize_backward`` (:328-487), the
+  training pair
 
 The compute runs on the GPU in fp32 (the reference is fp64); results equal
 the Tier-A fp32 oracle bit for bit and the fp64 reference within the
@@ -25,7 +27,10 @@ import numpy as np
 import torch
 
 from .core import GaussianScene, ImageBuffer, InvalidParameterError
-from .device import DeviceScene, device_scene, renderer
+import ctypes as C
+
+from . import _native as N
+from .device import DeviceScene, device_scene, options_struct, renderer
 
 
 @dataclass(frozen=True)
@@ -152,6 +157,69 @@ def rasterize_filtered(scene, camera, active, options: RasterizeOptions = Raster
     """Render only the active Gaussians; only those are projected."""
     idx = active_indices(scene, active)
     return _render_host(scene, camera, options, active_idx=idx)
+
+
+# ---------------------------------------------------------------------------
+# training: forward with cache + backward (render.py:318-487; SURVEY §8f next #1)
+# ---------------------------------------------------------------------------
+def _training_forward(ds: DeviceScene, camera, options, active_idx=None):
+    r = renderer(ds.device)
+    out = r.alloc_outputs(camera)
+    H, W = int(camera.height), int(camera.width)
+    out["tau"] = torch.empty((H, W), dtype=torch.float32, device=ds.device)
+    out["last"] = torch.empty((H, W), dtype=torch.int32, device=ds.device)
+    r.render(ds, camera, options, out=out, active_idx=active_idx)
+    return out, r.frame_id
+
+
+def rasterize_cached(scene, camera, options: RasterizeOptions = RasterizeOptions()):
+    """Forward render keeping what the backward pass needs (render.py:318-321):
+    returns (RenderOutput, cache). The cache holds, on the device, the per-pixel
+    final transmittance and last composite; the binning stays in the workspace."""
+    ds = _check_scene(scene)
+    out, frame = _training_forward(ds, camera, options)
+    H, W = int(camera.height), int(camera.width)
+    res = RenderOutput(color=ImageBuffer.trusted(out["rgb"].double().cpu().numpy().reshape(H, W, 3)),
+                       alpha=out["alpha"].double().cpu().numpy(), count=out["count"].long().cpu().numpy(),
+                       depth=out["depth"])
+    return res, dict(options=options, device_out=out, frame=frame, camera=camera)
+
+
+def rasterize_backward(scene, camera, cache: dict, grad_image) -> dict:
+    """Analytic gradients of a scalar loss through the rendered image
+    (render.py:328-394 + _chain_to_parameters :397-487). ``grad_image`` =
+    dL/d(colour image), (H, W, 3). Returns float64 gradients w.r.t. positions,
+    sh, log_scales, quaternions, opacity_logits, plus ``mean2d_grad_norm`` and
+    ``touched`` -- the reference's dict, computed by rs_backward in fp32."""
+    ds = _check_scene(scene)
+    r = renderer(ds.device)
+    options = cache["options"]
+    out = cache["device_out"]
+    if r.frame_id != cache["frame"]:  # the workspace rendered something else since: redo the forward
+        out, cache["frame"] = _training_forward(ds, camera, options)
+        cache["device_out"] = out
+    H, W = int(camera.height), int(camera.width)
+    g = np.asarray(grad_image, dtype=np.float32)
+    if g.shape != (H, W, 3):
+        raise InvalidParameterError(f"grad_image must be ({H}, {W}, 3)")
+    dev = ds.device
+    grad = torch.from_numpy(np.ascontiguousarray(g)).to(dev)
+    n = max(ds.n, 1)
+    o = dict(positions=torch.empty((n, 3), device=dev), sh=torch.empty((n, 48), device=dev),
+             log_scales=torch.empty((n, 3), device=dev), quaternions=torch.empty((n, 4), device=dev),
+             opacity_logits=torch.empty(n, device=dev), mean2d_grad_norm=torch.empty(n, device=dev),
+             touched=torch.empty(n, dtype=torch.uint8, device=dev))
+    N.check(r.lib.rs_backward(r.handle, C.byref(ds.struct), None, 0, C.byref(options_struct(options)),
+                              grad.data_ptr(), out["tau"].data_ptr(), out["last"].data_ptr(),
+                              *(o[k].data_ptr() for k in ("positions", "sh", "log_scales", "quaternions",
+                                                         "opacity_logits", "mean2d_grad_norm", "touched")),
+                              r.stream), "backward")
+    res = {k: v[:ds.n].cpu().numpy() for k, v in o.items()}
+    grads = {k: res[k].astype(np.float64) for k in ("positions", "log_scales", "quaternions", "opacity_logits",
+                                                  "mean2d_grad_norm")}
+    grads["sh"] = res["sh"].astype(np.float64).reshape(ds.n, 3, 16)
+    grads["touched"] = res["touched"].astype(bool)
+    return grads
 
 
 def _project_all(scene, camera, options):

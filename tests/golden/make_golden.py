@@ -236,6 +236,7 @@ def main():
     np.savez_compressed(HERE / "viewer_parity.npz", **d)
 
     make_io(fs, conftest)
+    make_grad(fs, conftest)
     print("golden fixtures written to", HERE)
 
 
@@ -268,9 +269,50 @@ def make_io(fs, conftest):
     np.savez_compressed(HERE / "io.npz", **d)
 
 
+def make_grad(fs, conftest):
+    """J: backward pass (render.py:318-487): reference gradients through the image."""
+    R = fs.render
+    d = {}
+    rng = np.random.default_rng(99)
+    cases = []
+    cases.append(("deg0", conftest.random_scene(rng, 4, sh_degree=0, opacity_range=(0.3, 0.8),
+                                                scale_range=(0.15, 0.4)), conftest.facing_camera(8, 8, distance=4.0)))
+    cases.append(("deg2", conftest.random_scene(rng, 3, sh_degree=2, opacity_range=(0.3, 0.8),
+                                                scale_range=(0.15, 0.4)), conftest.facing_camera(8, 8, distance=4.0)))
+    cases.append(("deg3", conftest.random_scene(rng, 40, sh_degree=3, scale_range=(0.05, 0.3)),
+                  conftest.facing_camera(32, 24, distance=4.0)))
+    near = conftest.random_scene(rng, 3, scale_range=(0.2, 0.4))
+    far = fs.GaussianScene(positions=np.array([[100.0, 0.0, 0.0]]), opacity_logits=np.zeros(1),
+                           sh=np.zeros((1, 3, 16)), log_scales=np.full((1, 3), np.log(0.2)),
+                           quaternions=np.array([[1.0, 0.0, 0.0, 0.0]]))
+    both = fs.GaussianScene.from_primitives([near.primitive(i) for i in range(3)] + [far.primitive(0)])
+    cases.append(("touched", both, conftest.facing_camera(8, 8, distance=4.0)))
+    s0 = fs.synthetic  # noqa: F841
+    sc = conftest.random_scene(rng, 300, sh_degree=3, spread=1.2, scale_range=(0.02, 0.2))
+    cases.append(("many", sc, conftest.facing_camera(64, 48, distance=4.0)))
+    for name, scene, cam in cases:
+        p = name + "_"
+        pack_scene(d, p, scene)
+        pack_cam(d, p, cam)
+        opts = R.RasterizeOptions()
+        pack_opts(d, p, opts)
+        w = rng.normal(size=(cam.height, cam.width, 3)) if name != "touched" else np.ones((cam.height, cam.width, 3))
+        d[p + "w"] = w
+        out, cache = R.rasterize_cached(scene, cam)
+        g = R.rasterize_backward(scene, cam, cache, w)
+        d[p + "img"] = out.color.data
+        for k in ("positions", "sh", "log_scales", "quaternions", "opacity_logits", "mean2d_grad_norm", "touched"):
+            d[p + "g_" + k] = np.asarray(g[k])
+    d["cases"] = np.array([c[0] for c in cases])
+    np.savez_compressed(HERE / "grad.npz", **d)
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["io"]:  # only the wire-format fixtures
         fs_, conftest_, _ = import_reference()
         make_io(fs_, conftest_)
+    elif sys.argv[1:] == ["grad"]:  # only the backward-pass fixtures
+        fs_, conftest_, _ = import_reference()
+        make_grad(fs_, conftest_)
     else:
         main()
