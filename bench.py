@@ -42,9 +42,12 @@ METRIC_RENDER = "render FPS at 1256x828, 500k Gaussians (configs[1] orbit), 1 fr
 METRIC_SCORE = "importance-score views/s, 3M Gaussians x 200 views at 1256x828 (configs[2])"
 METRIC_HOUSE = "house-scale render FPS with visibility filtering, 6M Gaussians, 1920x1080 (configs[3])"
 METRIC_BATCH = "batched multi-view render frames/s, 1M heavy-tailed Gaussians, 1920x1080 (configs[4])"
-METRICS = {"render": METRIC_RENDER, "score": METRIC_SCORE, "house": METRIC_HOUSE, "batch": METRIC_BATCH}
+METRIC_TRAIN = "training step (forward with cache + backward) views/s, 500k Gaussians at 1256x828 (configs[1])"
+METRICS = {"render": METRIC_RENDER, "score": METRIC_SCORE, "house": METRIC_HOUSE, "batch": METRIC_BATCH,
+           "train": METRIC_TRAIN}
 WORKLOADS = {"render": "configs[1] orbit render", "score": "configs[2] importance scoring",
-             "house": "configs[3] house trajectory", "batch": "configs[4] batched views"}
+             "house": "configs[3] house trajectory", "batch": "configs[4] batched views",
+             "train": "configs[1] orbit, forward + backward"}
 
 
 def parse():
@@ -53,13 +56,13 @@ def parse():
     ap.add_argument("--steps", type=int, default=None,
                     help="default: render 200 frames, score 5 passes, house 300 frames, batch 3 x 64 frames")
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", choices=("render", "score", "house", "batch"), default="render")
+    ap.add_argument("--workload", choices=("render", "score", "house", "batch", "train"), default="render")
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--n-gaussians", type=int, default=None, help="override N (debug only)")
     a = ap.parse_args()
     if a.steps is None:
-        a.steps = {"render": 200, "score": 5, "house": 300, "batch": 3}[a.workload]
+        a.steps = {"render": 200, "score": 5, "house": 300, "batch": 3, "train": 100}[a.workload]
     return a
 
 
@@ -168,7 +171,7 @@ def make_workload(kind: str, n_override=None):
         return scene, traj
     if kind == "batch":
         return synth.config4(0, n=n_override or 1_000_000)
-    if kind == "render":
+    if kind in ("render", "train"):
         scene, cams = synth.config1(0, n=n_override or 500_000)
         return scene, cams
     scene, cams = synth.config2(0, n=n_override or 3_000_000)
@@ -249,6 +252,8 @@ def main():
 
     if args.workload in ("house", "batch"):
         return run_trajectory(args, rank, world, local, dev, opts, r, opt_s, stream, flush, pk, barrier)
+    if args.workload == "train":
+        return run_train(args, rank, world, local, dev, opts, r, opt_s, stream, flush, pk, barrier)
     scene, cams = make_workload(args.workload, args.n_gaussians)
     ds = device_scene(scene, dev)
     W_, H_ = cams[0].width, cams[0].height
@@ -617,6 +622,77 @@ def run_trajectory(args, rank, world, local, dev, opts, r, opt_s, stream, flush,
                      "d2h_bytes_per_step": per_step * hw * (24 + 8 + 8),
                      "api": "paper_2403_13806_b200." + ("visibility.render_from_viewpoint" if house
                                                         else "render.rasterize") + f" ({len(sel)} frames)"}
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_train(args, rank, world, local, dev, opts, r, opt_s, stream, flush, pk, barrier):
+    """Training step of the backward path: per view the training
+    forward (rs_render_ex recording tau / last) and rs_backward for a dense random
+    dL/dimage, gradients for every Gaussian parameter; views split across ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2403_13806_b200 import _native as N
+    from paper_2403_13806_b200.device import camera_struct, device_scene
+
+    scene, cams = make_workload("train", args.n_gaussians)
+    ds = device_scene(scene, dev)
+    W_, H_ = cams[0].width, cams[0].height
+    frames = lambda s: cams[(s * world + rank) % len(cams)]  # noqa: E731
+    out = r.alloc_outputs(cams[0])
+    out["tau"] = torch.empty((H_, W_), dtype=torch.float32, device=dev)
+    out["last"] = torch.empty((H_, W_), dtype=torch.int32, device=dev)
+    for s in range(min(args.steps, 50)):  # size the pair capacity (checked renders)
+        r.render(ds, frames(s), opts, out=out)
+    outs = r.outputs_struct(out)
+    n = ds.n
+    gimg = torch.randn((H_, W_, 3), dtype=torch.float32, device=dev, generator=torch.Generator(dev).manual_seed(0))
+    g = [torch.empty(k, dtype=torch.float32, device=dev) for k in (3 * n, 48 * n, 3 * n, 4 * n, n, n)]
+    touched = torch.empty(n, dtype=torch.uint8, device=dev)
+    lib, sptr = r.lib, stream.cuda_stream
+
+    def step(cs, ev):
+        ev[0].record(stream)
+        N.check(lib.rs_render_ex(r.handle, C.byref(ds.struct), None, 0, C.byref(cs), C.byref(opt_s),
+                                 C.byref(outs), None, 0, sptr))
+        ev[1].record(stream)
+        N.check(lib.rs_backward(r.handle, C.byref(ds.struct), None, 0, C.byref(opt_s), gimg.data_ptr(),
+                                out["tau"].data_ptr(), out["last"].data_ptr(), *(t.data_ptr() for t in g),
+                                touched.data_ptr(), sptr))
+        ev[2].record(stream)
+
+    plan = [camera_struct(frames(s)) for s in range(args.steps)]
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in plan]
+    for s in range(args.warmup):
+        step(plan[s % len(plan)], ev[0])
+    barrier()
+    with ClockSampler(local) as clk:
+        barrier()
+        for cs, e in zip(plan, ev):
+            flush.zero_()
+            step(cs, e)
+        barrier()
+    assert not r.stats().overflow
+    fwd = np.array([a.elapsed_time(b) for a, b, _ in ev])
+    bwd = np.array([b.elapsed_time(c) for _, b, c in ev])
+    t_local = torch.tensor([float(fwd.sum() + bwd.sum())], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+    t_max = float(t_local.item())
+    result = {
+        "metric": METRICS["train"], "value": world * args.steps / (t_max / 1e3), "unit": "views/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded configs[1], random dL/dimage; no dataset offline)",
+        "config": {"workload": WORKLOADS["train"], "n_gaussians": n, "width": W_, "height": H_,
+                   "l2": "flushed (256 MB memset) between timed steps",
+                   "parallelism": f"views split across {world} GPU(s), no communication"},
+        "stages_ms": {"forward_with_cache": float(fwd.mean()), "backward": float(bwd.mean())},
+        "gpu_launches": args.steps * (frame_launches(W_, H_) + 2), "clocks": clk.summary(),
+    }
     if rank == 0:
         print(json.dumps(result), flush=True)
     if world > 1:
