@@ -143,15 +143,33 @@ __global__ void __launch_bounds__(kBlendThreads) backward_blend_kernel(
         }
       }
       if (__any_sync(0xffffffffu, comp)) {
+        // reduce-scatter of v[0..7] across the warp (each butterfly step keeps half of the
+        // values: 4 + 2 + 1 + 1 + 1 shuffles instead of 8 x 5), then lane 4j + 0..3 holds
+        // the warp sum of value j; v[8] by a plain butterfly
+        const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+        float w4[4];
 #pragma unroll
-        for (int j = 0; j < kSGrad; ++j)
+        for (int k = 0; k < 4; ++k) {
+          const float r = __shfl_xor_sync(0xffffffffu, b4 ? v[k] : v[4 + k], 16);
+          w4[k] = (b4 ? v[4 + k] : v[k]) + r;
+        }
+        float w2[2];
 #pragma unroll
-          for (int off = 16; off > 0; off >>= 1) v[j] += __shfl_xor_sync(0xffffffffu, v[j], off);
+        for (int k = 0; k < 2; ++k) {
+          const float r = __shfl_xor_sync(0xffffffffu, b3 ? w4[k] : w4[2 + k], 8);
+          w2[k] = (b3 ? w4[2 + k] : w4[k]) + r;
+        }
+        float w1 = (b2 ? w2[1] : w2[0]) + __shfl_xor_sync(0xffffffffu, b2 ? w2[0] : w2[1], 4);
+        w1 += __shfl_xor_sync(0xffffffffu, w1, 2);
+        w1 += __shfl_xor_sync(0xffffffffu, w1, 1);
+        float v8 = v[8];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v8 += __shfl_xor_sync(0xffffffffu, v8, off);
+        const uint32_t it = s_item[e];
+        float* g = sgrad + (size_t)kSGrad * it;
+        if ((lane & 3) == 0) atomicAdd(g + (b4 ? 4 : 0) + (b3 ? 2 : 0) + (b2 ? 1 : 0), w1);
         if (lane == 0) {
-          const uint32_t it = s_item[e];
-          float* g = sgrad + (size_t)kSGrad * it;
-#pragma unroll
-          for (int j = 0; j < kSGrad; ++j) atomicAdd(g + j, v[j]);
+          atomicAdd(g + 8, v8);
           touched[it] = 1;
         }
       }
