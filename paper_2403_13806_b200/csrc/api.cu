@@ -11,7 +11,7 @@
 #include <cstring>
 #include <new>
 
-#include "bin.cuh"
+#include "segbin.cuh"
 #include "blend.cuh"
 #include "compact.cuh"
 #include "io.cuh"
@@ -27,28 +27,37 @@ size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
 struct Layout {
   // per-frame zeroed region [0, frame_bytes)
-  size_t ctr, hist, emit_lb, proj_lb, ranges, frame_bytes;
-  size_t sticky, cam, recs, tcount, rowtab, sgrad, titem, keysA, keysB, valsA, valsB, offsets, owners, ptileA, ptileB, pitemA, pitemB, lbA, lbB, total;
+  size_t ctr, hist, emit_lb, proj_lb, ranges, rowcnt, frame_bytes;
+  size_t sticky, cam, recs, nrows, sgrad, titem, keysA, keysB, valsA, valsB, offsets, segkeyA, segkeyB, segvalA,
+      segvalB, segitem, segspan, rowstart, chunkstart, chunkcnt, tilecnt, pitem, lbA, lbB, total;
 };
 
 int tiles_x(int w) { return (w + kTile - 1) / kTile; }
 
+int64_t seg_capacity(int64_t n_cap, int64_t pair_cap) {
+  // row segments <= pairs + 2 per Gaussian (only a culling box's first and last tile rows can
+  // miss the ellipse); more are reported as an overflow
+  return std::min<int64_t>(pair_cap + 2 * n_cap, 0xffffffffLL);
+}
+
 Layout make_layout(int64_t n_cap, int64_t pair_cap, int W, int H) {
   Layout L{};
   const size_t TW = tiles_x(W), TH = tiles_x(H);
+  const size_t seg_cap = (size_t)seg_capacity(n_cap, pair_cap);
   size_t o = 0;
   auto take = [&](size_t bytes) { const size_t at = o; o = align_up(o + bytes); return at; };
+  // per-frame zeroed region
   L.ctr = take(sizeof(Counters));
-  L.hist = take(8 * 256 * sizeof(uint32_t));  // depth passes 0-3, tile passes 4-5
-  L.emit_lb = take(((size_t)n_cap / kCountThreads + 2) * sizeof(unsigned long long));
+  L.hist = take(8 * 256 * sizeof(uint32_t));  // depth passes 0-3, segment row passes 4-5
+  L.emit_lb = take(((size_t)n_cap / kSegCountThreads + 2) * sizeof(unsigned long long));
   L.proj_lb = take(((size_t)n_cap / kCompactKeys + 2) * sizeof(unsigned long long));
   L.ranges = take(TW * TH * sizeof(uint2));
+  L.rowcnt = take((TH + 1) * sizeof(uint32_t));
   L.frame_bytes = o;
   L.sticky = take(sizeof(Sticky));
   L.cam = take(sizeof(rs_camera));
   L.recs = take((size_t)n_cap * sizeof(Rec));
-  L.tcount = take((size_t)n_cap * 4);
-  L.rowtab = take((size_t)n_cap * 4 * kRowTab);
+  L.nrows = take((size_t)n_cap * 4);
   L.sgrad = take((size_t)n_cap * 4 * kSGrad);  // rs_backward: screen-space gradient sums per item
   L.titem = take((size_t)n_cap);
   L.keysA = take((size_t)n_cap * 4);
@@ -56,12 +65,18 @@ Layout make_layout(int64_t n_cap, int64_t pair_cap, int W, int H) {
   L.valsA = take((size_t)n_cap * 4);
   L.valsB = take((size_t)n_cap * 4);
   L.offsets = take((size_t)n_cap * 4);
-  L.owners = take(((size_t)pair_cap / kEmitPairs + 2) * 4);
-  L.ptileA = take((size_t)pair_cap * 2);
-  L.ptileB = take((size_t)pair_cap * 2);
-  L.pitemA = take((size_t)pair_cap * 4);
-  L.pitemB = take((size_t)pair_cap * 4);
-  const size_t chunks = (size_t)(std::max(n_cap, pair_cap) + kMinChunk - 1) / kMinChunk + 1;
+  L.segkeyA = take(seg_cap * 2);
+  L.segkeyB = take(seg_cap * 2);
+  L.segvalA = take(seg_cap * 4);
+  L.segvalB = take(seg_cap * 4);
+  L.segitem = take(seg_cap * 4);
+  L.segspan = take(seg_cap * 4);
+  L.rowstart = take((TH + 1) * 4);
+  L.chunkstart = take((TH + 1) * 4);
+  L.chunkcnt = take((seg_cap / kExpandChunk + TH + 1) * TW * 4);
+  L.tilecnt = take(TW * TH * 4);
+  L.pitem = take((size_t)pair_cap * 4);
+  const size_t chunks = (std::max<size_t>((size_t)n_cap, seg_cap) + kMinChunk - 1) / kMinChunk + 1;
   L.lbA = take(chunks * 256 * 4);
   L.lbB = take(chunks * 256 * 4);
   L.total = o;
@@ -80,7 +95,7 @@ struct rs_workspace {
   // current frame (set by rs_project)
   uint32_t n_items;
   int W, H, TW, TH;
-  int tile_bits, tile_passes;
+  int row_bits;  // bits of a tile-row index (segment sort key)
   bool binned, have_cam, has_color;
 
   template <typename T> T* at(size_t off) const { return reinterpret_cast<T*>(base + off); }
@@ -219,9 +234,8 @@ int32_t rs_set_camera(rs_workspace* ws, const rs_camera* cam, void* stream) {
   ws->H = cam->height;
   ws->TW = TW;
   ws->TH = TH;
-  ws->tile_bits = 1;
-  while ((1 << ws->tile_bits) < TW * TH) ++ws->tile_bits;
-  ws->tile_passes = (ws->tile_bits + 7) / 8;
+  ws->row_bits = 1;
+  while ((1 << ws->row_bits) < TH) ++ws->row_bits;
   ws->have_cam = true;
   // stream-ordered upload; from pageable memory the driver stages it at once, so the
   // caller may reuse `cam` immediately (a captured frame graph then replays it)
@@ -255,13 +269,12 @@ static int32_t project_impl(rs_workspace* ws, const rs_scene* scene, const int32
     if (full)
       project_kernel<true, true><<<grid, kProjThreads, 0, st>>>(
           scene->planes, scene->sh, scene->plane_stride, scene->sh_degree, active_idx, (uint32_t)items, ws->at<rs_camera>(ws->L.cam), *opts,
-          ws->at<Rec>(ws->L.recs), ws->at<uint32_t>(ws->L.keysB), ws->at<uint32_t>(ws->L.tcount), ws->at<uint4>(ws->L.rowtab), ws->ctr(), full,
+          ws->at<Rec>(ws->L.recs), ws->at<uint32_t>(ws->L.keysB), ws->at<uint32_t>(ws->L.nrows), ws->ctr(), full,
           reinterpret_cast<int4*>(full_bbox));
     else
       (color ? project_kernel<false, true> : project_kernel<false, false>)<<<grid, kProjThreads, 0, st>>>(
           scene->planes, scene->sh, scene->plane_stride, scene->sh_degree, active_idx, (uint32_t)items, ws->at<rs_camera>(ws->L.cam), *opts,
-          ws->at<Rec>(ws->L.recs), ws->at<uint32_t>(ws->L.keysB), ws->at<uint32_t>(ws->L.tcount), ws->at<uint4>(ws->L.rowtab),
-          ws->ctr(), nullptr, nullptr);
+          ws->at<Rec>(ws->L.recs), ws->at<uint32_t>(ws->L.keysB), ws->at<uint32_t>(ws->L.nrows), ws->ctr(), nullptr, nullptr);
   }
   return cuda_status();
 }
@@ -294,43 +307,48 @@ int32_t rs_bin(rs_workspace* ws, void* stream) {
                                     ws->at<uint32_t>(ws->L.keysB), ws->at<uint32_t>(ws->L.valsA),
                                     ws->at<uint32_t>(ws->L.valsA), ws->at<uint32_t>(ws->L.valsB), nvis, 0, n, 32,
                                     0, 0, false, st, &keys_res, &items_sorted);
-    count_kernel<<<(n + kCountThreads - 1) / kCountThreads, kCountThreads, 0, st>>>(items_sorted, ws->at<uint32_t>(ws->L.tcount), ws->ctr(),
-                                                  (uint32_t)ws->pair_cap, ws->at<uint32_t>(ws->L.offsets),
-                                                  ws->at<uint32_t>(ws->L.owners),
-                                                  ws->at<unsigned long long>(ws->L.emit_lb),
-                                                  ws->at<Sticky>(ws->L.sticky));
-    // both emitters; the device picks one per frame (bin.cuh emit_pair_balanced)
-    const unsigned egrid = (unsigned)std::max<int64_t>(1, (ws->pair_cap + kEmitPairs - 1) / kEmitPairs);
-    emit_kernel<<<egrid, 256, 0, st>>>(items_sorted, ws->at<Rec>(ws->L.recs), ws->at<uint4>(ws->L.rowtab),
-                                       ws->at<uint32_t>(ws->L.offsets),
-                                       ws->at<uint32_t>(ws->L.owners), ws->ctr(), ws->TW,
-                                       ws->at<uint16_t>(ws->L.ptileA), ws->at<uint32_t>(ws->L.pitemA),
-                                       ws->at<uint32_t>(ws->L.hist) + 4 * 256, ws->at<uint32_t>(ws->L.lbA),
-                                       kSortThreads * kTileItems);
-    emitw_kernel<<<std::max(1, std::min((int)((n + 32 * kEmitWarps - 1) / (32 * kEmitWarps)), ws->sms * 5)),
-                   32 * kEmitWarps, 0, st>>>(
-        items_sorted, ws->at<Rec>(ws->L.recs), ws->at<uint4>(ws->L.rowtab), ws->at<uint32_t>(ws->L.offsets),
-        ws->at<uint32_t>(ws->L.tcount), ws->ctr(), ws->TW, ws->at<uint16_t>(ws->L.ptileA),
-        ws->at<uint32_t>(ws->L.pitemA), ws->at<uint32_t>(ws->L.hist) + 4 * 256, ws->at<uint32_t>(ws->L.lbA),
+    // row segments: count + offsets, emission in depth order, stable sort by tile row,
+    // per-tile ranges, expansion into the per-tile lists (segbin.cuh)
+    Counters* ctr = ws->ctr();
+    const uint32_t seg_cap = (uint32_t)seg_capacity(ws->n_cap, ws->pair_cap);
+    segcount_kernel<<<(n + kSegCountThreads - 1) / kSegCountThreads, kSegCountThreads, 0, st>>>(
+        items_sorted, ws->at<uint32_t>(ws->L.nrows), ctr, seg_cap, ws->at<uint32_t>(ws->L.offsets),
+        ws->at<unsigned long long>(ws->L.emit_lb), ws->at<Sticky>(ws->L.sticky));
+    segemit_kernel<<<std::max(1, std::min((int)((n + 255) / 256), ws->sms * 4)), 256, 0, st>>>(
+        items_sorted, ws->at<Rec>(ws->L.recs), ws->at<uint32_t>(ws->L.offsets), ctr, ws->TW,
+        ws->at<uint16_t>(ws->L.segkeyA), ws->at<uint32_t>(ws->L.segitem), ws->at<uint32_t>(ws->L.segspan), ws->TH,
+        ws->at<uint32_t>(ws->L.rowcnt), ws->at<uint32_t>(ws->L.hist) + 4 * 256, ws->at<uint32_t>(ws->L.lbA),
         kSortThreads * kTileItems);
-    const uint16_t* tiles_res;
-    const uint32_t* pitems;
-    run_sort<uint16_t, kTileItems>(ws, ws->at<uint16_t>(ws->L.ptileA), ws->at<uint16_t>(ws->L.ptileA),
-                                   ws->at<uint16_t>(ws->L.ptileB), ws->at<uint32_t>(ws->L.pitemA),
-                                   ws->at<uint32_t>(ws->L.pitemA), ws->at<uint32_t>(ws->L.pitemB),
-                                   &ws->ctr()->n_pairs, 0, (uint32_t)ws->pair_cap, ws->tile_bits, 4, 4, true, st,
-                                   &tiles_res, &pitems);
-    const unsigned rgrid = (unsigned)std::max<int64_t>(1, (ws->pair_cap + 2047) / 2048);
-    ranges_kernel<<<rgrid, 256, 0, st>>>(tiles_res, ws->ctr(), ws->at<uint2>(ws->L.ranges));
+    const uint16_t* rows_res;
+    const uint32_t* sorted_seg;
+    run_sort<uint16_t, kTileItems>(ws, ws->at<uint16_t>(ws->L.segkeyA), ws->at<uint16_t>(ws->L.segkeyA),
+                                   ws->at<uint16_t>(ws->L.segkeyB), nullptr, ws->at<uint32_t>(ws->L.segvalA),
+                                   ws->at<uint32_t>(ws->L.segvalB), &ctr->n_segs, 0, seg_cap, ws->row_bits, 4, 4,
+                                   false, st, &rows_res, &sorted_seg);
+    row_scan_kernel<<<1, 32, 0, st>>>(ws->at<uint32_t>(ws->L.rowcnt), ws->TH, ws->at<uint32_t>(ws->L.rowstart),
+                                      ws->at<uint32_t>(ws->L.chunkstart));
+    const unsigned gx = (unsigned)std::min<int64_t>(seg_cap / kExpandChunk + ws->TH + 1, (int64_t)ws->sms * 16);
+    const dim3 eg(gx, (ws->TW + kExpandCols - 1) / kExpandCols);  // chunks grid-strided
+    chunk_count_kernel<<<gx, 256, 0, st>>>(sorted_seg, ws->at<uint32_t>(ws->L.segspan),
+                                           ws->at<uint32_t>(ws->L.rowstart), ws->at<uint32_t>(ws->L.chunkstart),
+                                           ws->TH, ws->TW, ws->at<uint32_t>(ws->L.chunkcnt));
+    const int T = ws->TW * ws->TH;
+    tile_chunks_kernel<<<(T + 7) / 8, 256, 0, st>>>(ws->at<uint32_t>(ws->L.chunkstart), ws->TH, ws->TW,
+                                                        ws->at<uint32_t>(ws->L.chunkcnt),
+                                                        ws->at<uint32_t>(ws->L.tilecnt));
+    tile_scan_kernel<<<1, 1024, 0, st>>>(ws->at<uint32_t>(ws->L.tilecnt), T, ctr, (uint32_t)ws->pair_cap,
+                                         ws->at<uint2>(ws->L.ranges), ws->at<Sticky>(ws->L.sticky));
+    expand_kernel<true><<<eg, 256, 0, st>>>(sorted_seg, ws->at<uint32_t>(ws->L.segitem),
+                                            ws->at<uint32_t>(ws->L.segspan), ws->at<uint32_t>(ws->L.rowstart),
+                                            ws->at<uint32_t>(ws->L.chunkstart), ws->TH, ws->TW,
+                                            ws->at<uint32_t>(ws->L.chunkcnt), ws->at<uint2>(ws->L.ranges), ctr,
+                                            ws->at<uint32_t>(ws->L.pitem));
   }
   ws->binned = true;
   return cuda_status();
 }
 
-static const uint32_t* final_pair_items(const rs_workspace* ws) {
-  // tile sort ping-pong: 1 pass -> B, 2 passes -> A
-  return ws->tile_passes == 1 ? ws->at<uint32_t>(ws->L.pitemB) : ws->at<uint32_t>(ws->L.pitemA);
-}
+static const uint32_t* final_pair_items(const rs_workspace* ws) { return ws->at<uint32_t>(ws->L.pitem); }
 
 int32_t rs_blend_ex(rs_workspace* ws, const rs_options* opts, const rs_outputs* out_p, uint32_t* scores,
                     uint32_t flags, void* stream) {

@@ -7,13 +7,12 @@
 // operation order (compiled with -fmad=false; explicit __fmaf_rn only where
 // the contract fuses), and writes
 //   * a 64-byte Rec for binned items (culled items write nothing else),
-//   * the binned items' pair counts and tile-row tables (rows.cuh), and
+//   * the binned items' tile-row counts (their row segments, segbin.cuh), and
 //   * the binned items' (32-bit depth key, item) compacted in item order
 //     (decoupled look-back over ticket-ordered blocks) for the depth sort,
 //     whose length n_visible the last block publishes.
 #pragma once
 #include "rs_common.cuh"
-#include "rows.cuh"
 #include "rs_math.cuh"
 
 namespace rs {
@@ -47,18 +46,16 @@ __global__ void __launch_bounds__(128) project_kernel(const float* __restrict__ 
                                                       const int32_t* __restrict__ active_idx, uint32_t n_items,
                                                       const rs_camera* __restrict__ camp, rs_options o,
                                                       Rec* __restrict__ recs,
-                                                      uint32_t* __restrict__ keys, uint32_t* __restrict__ tcount,
-                                                      uint4* __restrict__ rowtab, Counters* __restrict__ ctr,
+                                                      uint32_t* __restrict__ keys, uint32_t* __restrict__ nrows,
+                                                      Counters* __restrict__ ctr,
                                                       float* __restrict__ full, int4* __restrict__ full_bbox) {
   const uint32_t item = blockIdx.x * blockDim.x + threadIdx.x;
   if (item == 0) ctr->n_items = n_items;
   // the camera lives in device memory (uploaded by a stream-ordered copy), so a captured
   // CUDA graph of the frame replays with a new camera without re-instantiation
   const rs_camera cam = *camp;
-  __shared__ RowCountSmem s_rows;
   bool valid = false, binned = false;
-  float4 ga = make_float4(0.f, 0.f, 0.f, 0.f), gb = ga;  // the binned record's geometry (tile-row count)
-  int4 gd = make_int4(0, 0, 0, 0);
+  float depth_b = 0.0f;  // depth of a binned record (its sort key)
   if (item < n_items) {
     const int64_t i = active_idx ? (int64_t)__ldg(active_idx + item) : (int64_t)item;
     const float* P = planes + i;
@@ -251,9 +248,8 @@ __global__ void __launch_bounds__(128) project_kernel(const float* __restrict__ 
                         cy0 | (cy1 << 16) | (ell ? (int)0x80000000 : 0));
       if (binned) {
         recs[item] = rec;
-        ga = rec.a;
-        gb = rec.b;
-        gd = rec.d;
+        nrows[item] = (uint32_t)((cy1 - 1) / kTile - cy0 / kTile + 1);  // its row segments (segbin.cuh)
+        depth_b = depth;
       }
       if (FULL) {
         float4* f = reinterpret_cast<float4*>(full + 16 * (size_t)item);
@@ -265,9 +261,7 @@ __global__ void __launch_bounds__(128) project_kernel(const float* __restrict__ 
       }
     }
   }
-  // pairs per binned record (+ row tables), warp-cooperatively
-  warp_count_rows(s_rows, binned, ga, gb, gd, item, tcount, rowtab);
-  if (item < n_items) keys[item] = binned ? depth_key(gb.w) : kInvalidKey;
+  if (item < n_items) keys[item] = binned ? depth_key(depth_b) : kInvalidKey;
 }
 
 }  // namespace rs

@@ -14,7 +14,7 @@
 // ellipses) with explicit slack for the rounding (oracle/cpu_ref.cpp:row_geom);
 // IEEE operations in the oracle's fixed order, so the binning is bit-exact.
 // On configs[1] this lists 19% fewer (tile, Gaussian) pairs than the
-// rectangles, 44% fewer on the anisotropic configs[4].
+// rectangles, 44% fewer on the anisotropic configs[4]. Used by segemit_kernel.
 #pragma once
 #include "rs_common.cuh"
 
@@ -84,74 +84,6 @@ __device__ __forceinline__ bool row_span_e(const RowGeom& g, const int4 cb, floa
 __device__ __forceinline__ bool row_span(const RowGeom& g, const int4 cb, int ty, int& tx0, int& tx1) {
   const float ulo = row_edge(g, max(ty * kTile, cb.z)), uhi = row_edge(g, min(ty * kTile + kTile, cb.w));
   return row_span_e(g, cb, ulo, uhi, edge_s(g, ulo), edge_s(g, uhi), tx0, tx1);
-}
-
-// Row table: the spans of the tile rows of an ellipse record with <= kRowTab rows, one word
-// per row (tx0 | width << 16, 0 = empty row), written by the projection's count for the
-// emitter (kRowTab / 4 uint4 per item).
-constexpr int kRowTab = 16;
-
-// Per-thread staging of the warp-cooperative row count (project_kernel).
-struct RowCountSmem {
-  RowGeom g[128];
-  int4 d[128];
-  uint32_t cnt[128];
-  __align__(16) uint32_t tab[128][kRowTab];
-  int pre[4][33];
-};
-
-// Pairs each binned record of the warp emits (rectangle rows: closed form; ellipse rows:
-// flattened over the warp's lanes so every lane evaluates one row per round, whatever the
-// per-record row counts), plus the row table of ellipse records with <= kRowTab rows.
-__device__ __forceinline__ void warp_count_rows(RowCountSmem& S, bool binned, const float4 a, const float4 b,
-                                                const int4 d, uint32_t item, uint32_t* __restrict__ tcount,
-                                                uint4* __restrict__ rowtab) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int4 cb = cullbox_of(d);
-  const bool ell = binned && cullbox_ell(d);
-  const int nrows = binned ? (cb.w - 1) / kTile - cb.z / kTile + 1 : 0;
-  const int nr = ell ? nrows : 0;
-  if (ell) {
-    S.g[tid] = row_geom(a, b);
-    S.d[tid] = d;
-  }
-  S.cnt[tid] = 0;
-  int x = nr;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  S.pre[warp][lane] = x - nr;
-  if (lane == 31) S.pre[warp][32] = x;
-  __syncwarp();
-  const int total = S.pre[warp][32];
-  for (int base = 0; base < total; base += 32) {
-    const int j = base + lane;
-    if (j < total) {
-      int lo = 0, hi = 31;  // owner lane: the last one whose first row is <= j
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (S.pre[warp][mid] <= j) lo = mid; else hi = mid - 1;
-      }
-      const int ow = warp * 32 + lo, k = j - S.pre[warp][lo];
-      const int4 ocb = cullbox_of(S.d[ow]);
-      int t0, t1;
-      uint32_t w = 0;
-      if (row_span(S.g[ow], ocb, ocb.z / kTile + k, t0, t1)) w = (uint32_t)(t1 - t0 + 1);
-      if (w) atomicAdd(&S.cnt[ow], w);
-      if (k < kRowTab) S.tab[ow][k] = w ? (uint32_t)t0 | (w << 16) : 0u;
-    }
-  }
-  __syncwarp();
-  if (binned) {
-    tcount[item] = ell ? S.cnt[tid] : (uint32_t)(((cb.y - 1) / kTile - cb.x / kTile + 1) * nrows);
-    if (ell && nrows <= kRowTab) {
-      const uint4* t = reinterpret_cast<const uint4*>(S.tab[tid]);
-#pragma unroll
-      for (int v = 0; v < kRowTab / 4; ++v) rowtab[(kRowTab / 4) * (size_t)item + v] = t[v];
-    }
-  }
 }
 
 }  // namespace rs

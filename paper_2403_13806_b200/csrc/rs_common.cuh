@@ -9,7 +9,7 @@ namespace rs {
 
 constexpr int kTile = 16;          // 16x16 pixel tiles, one CTA of 256 threads each
 constexpr int kBlendThreads = 256;
-constexpr int kProjThreads = 128;  // projection CTA (rows.cuh RowCountSmem is sized for it)
+constexpr int kProjThreads = 128;  // projection CTA
 constexpr uint32_t kInvalidKey = 0xffffffffu;
 constexpr int kPlanes = 59;
 
@@ -50,7 +50,8 @@ struct Counters {
   uint32_t emit_ctr;     // decoupled look-back ticket of the pair counter
   uint32_t emit_work;    // rank-chunk work counter of the pair emitter
   uint32_t proj_ticket;  // logical block ticket of the projection's compaction
-  uint32_t pad[3];
+  uint32_t n_segs;       // row segments of the binned items (segbin.cuh)
+  uint32_t pad[2];
 };
 static_assert(sizeof(Counters) == 128, "Counters is 128 B");
 
