@@ -341,7 +341,7 @@ def main():
                                "evals_per_px": E / args.steps / hw, "composites_per_px": C_ / args.steps / hw},
             "roofline": {"kernel": "blend2_kernel<COLOR>", "bound": "fp32", "achieved": achieved,
                          "peak": fp32_peak, "unit": "TFLOP/s", "frac": achieved / fp32_peak,
-                         "traffic": profiled_traffic("blend2_kernel<1, 0, 0, 1>"),
+                         "traffic": profiled_traffic("blend2_kernel<1, 0, 0, 1, 0>"),
                          "traffic_source": TRAFFIC_FILE + " (ncu --set full, dram read+write bytes per launch)",
                          "algorithmic": "16*E + 11*C flops per frame (SURVEY §8d)",
                          "peak_source": "computed: SMs x 128 FP32 lanes x 2 x sm_max_mhz"},
@@ -711,14 +711,14 @@ def profiled_traffic(kernel: str):
 
 
 def frame_launches(W, H):
-    """Kernels per frame: project, depth histogram, 4 depth passes, count, both emitters
-    (one returns at once), the tile passes, ranges, blend."""
-    return 1 + 1 + 4 + 1 + 2 + r_tile_passes(W, H) + 1 + 1
+    """Kernels per frame: project, depth compaction+histogram, 4 depth passes, segment
+    count, segment emission, the segment row passes, row scan, chunk count, tile chunks,
+    tile scan, expansion, blend."""
+    return 1 + 1 + 4 + 1 + 1 + row_passes(H) + 1 + 1 + 1 + 1 + 1 + 1
 
 
-def r_tile_passes(W, H):
-    T = ((W + 15) // 16) * ((H + 15) // 16)
-    return 1 if T <= 256 else 2
+def row_passes(H):
+    return 1 if (H + 15) // 16 <= 256 else 2
 
 
 if __name__ == "__main__":
