@@ -310,60 +310,76 @@ __global__ void __launch_bounds__(kBlend2Threads) blend2_kernel(
         cntw += __popc(bal);
       }
       __syncwarp();
-      for (int q = 0; q < cntw; ++q) {
-        const Rec& E = s_rec[s_list[warp][q]];
-        const int4 bb = E.d;
-        const bool inx = px >= bb.x && px < bb.y;
-        const bool e0 = !done0 && inx && py0 >= bb.z && py0 < bb.w;
-        const bool e1 = !done1 && inx && py1 >= bb.z && py1 < bb.w;
-        float w0 = 0.0f, w1 = 0.0f;
-        if (e0 || e1) {
-          // both pixels in one basic block (selects, no per-pixel branches): two independent
-          // dependency chains per thread. Values computed for a pixel that is not evaluated
-          // (or below cut2) are discarded by the selects, so decisions and results are exactly
-          // those of blend_px.
+      // two entries per iteration: both entries' coverage and alpha math (independent of the
+      // transmittance) first, then the two composites in list order -- four independent
+      // dependency chains per thread and one termination vote per pair of entries. Values
+      // computed for a pixel that is not composited are discarded by the selects, so the
+      // decisions and results are exactly those of blend_px (the FAST exp2 is exact on
+      // [-126, 127] and only p2 >= cut2 >= -126 is ever used).
+      for (int q = 0; q < cntw; q += 2) {
+        const int ea = s_list[warp][q];
+        const bool hasb = q + 1 < cntw;
+        const int eb = hasb ? s_list[warp][q + 1] : ea;
+        float al[2][2];
+        bool ok[2][2], box[2][2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const Rec& E = s_rec[u ? eb : ea];
+          const int4 bb = E.d;
           const float4 ga = E.a, gb = E.b;
-          if (STATS) evals += (unsigned)e0 + (unsigned)e1;
+          const bool inx = px >= bb.x && px < bb.y && (u == 0 || hasb);
+          box[u][0] = inx && py0 >= bb.z && py0 < bb.w;
+          box[u][1] = inx && py1 >= bb.z && py1 < bb.w;
           const float dx = __fsub_rn(xs, ga.x);
           const float ax = __fmul_rn(ga.z, dx);
           const float dy0 = __fsub_rn(ys0, ga.y), dy1 = __fsub_rn(ys1, ga.y);
           const float p20 = __fmaf_rn(ax, dx, __fmaf_rn(__fmul_rn(ga.w, dy0), dx, __fmul_rn(__fmul_rn(gb.x, dy0), dy0)));
           const float p21 = __fmaf_rn(ax, dx, __fmaf_rn(__fmul_rn(ga.w, dy1), dx, __fmul_rn(__fmul_rn(gb.x, dy1), dy1)));
-          // the FAST exp2 is exact on [-126, 127]; lanes below cut2 (>= -126) are discarded
-          const float x0 = fmaxf(fminf(p20, 127.0f), -126.0f), x1 = fmaxf(fminf(p21, 127.0f), -126.0f);
-          const float ex0 = FAST ? exp2_core(x0) : exp2_contract(fminf(p20, 127.0f));
-          const float ex1 = FAST ? exp2_core(x1) : exp2_contract(fminf(p21, 127.0f));
-          const float al0 = fminf(__fmul_rn(gb.y, ex0), o.alpha_max), al1 = fminf(__fmul_rn(gb.y, ex1), o.alpha_max);
-          const bool c0 = e0 && p20 >= gb.z && al0 >= o.alpha_cut;
-          const bool c1 = e1 && p21 >= gb.z && al1 >= o.alpha_cut;
-          w0 = c0 ? __fmul_rn(al0, tau0) : 0.0f;
-          w1 = c1 ? __fmul_rn(al1, tau1) : 0.0f;
+          const float ex0 = FAST ? exp2_core(fminf(p20, 127.0f)) : exp2_contract(fminf(p20, 127.0f));
+          const float ex1 = FAST ? exp2_core(fminf(p21, 127.0f)) : exp2_contract(fminf(p21, 127.0f));
+          al[u][0] = fminf(__fmul_rn(gb.y, ex0), o.alpha_max);
+          al[u][1] = fminf(__fmul_rn(gb.y, ex1), o.alpha_max);
+          ok[u][0] = box[u][0] && p20 >= gb.z && al[u][0] >= o.alpha_cut;
+          ok[u][1] = box[u][1] && p21 >= gb.z && al[u][1] >= o.alpha_cut;
+        }
+        float wmax[2] = {0.0f, 0.0f};
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const Rec& E = s_rec[u ? eb : ea];
+          if (STATS) evals += (unsigned)(box[u][0] && !done0) + (unsigned)(box[u][1] && !done1);
+          const bool c0 = ok[u][0] && !done0, c1 = ok[u][1] && !done1;
+          const float w0 = c0 ? __fmul_rn(al[u][0], tau0) : 0.0f;
+          const float w1 = c1 ? __fmul_rn(al[u][1], tau1) : 0.0f;
           if (COLOR) {
             const float4 gc = E.c;
+            const float z = E.b.w;
             if (c0) {
               r0 = __fmaf_rn(gc.x, w0, r0); g0 = __fmaf_rn(gc.y, w0, g0); b0 = __fmaf_rn(gc.z, w0, b0);
-              d0 = __fmaf_rn(gb.w, w0, d0);
+              d0 = __fmaf_rn(z, w0, d0);
             }
             if (c1) {
               r1 = __fmaf_rn(gc.x, w1, r1); g1 = __fmaf_rn(gc.y, w1, g1); b1 = __fmaf_rn(gc.z, w1, b1);
-              d1 = __fmaf_rn(gb.w, w1, d1);
+              d1 = __fmaf_rn(z, w1, d1);
             }
           }
           cnt0 += c0 ? 1 : 0;
           cnt1 += c1 ? 1 : 0;
           if (TRAIN) {
-            const int k = (int)base + s_list[warp][q];
+            const int k = (int)base + (u ? eb : ea);
             last0 = c0 ? k : last0;
             last1 = c1 ? k : last1;
           }
-          tau0 = c0 ? __fmul_rn(tau0, __fsub_rn(1.0f, al0)) : tau0;
-          tau1 = c1 ? __fmul_rn(tau1, __fsub_rn(1.0f, al1)) : tau1;
+          tau0 = c0 ? __fmul_rn(tau0, __fsub_rn(1.0f, al[u][0])) : tau0;
+          tau1 = c1 ? __fmul_rn(tau1, __fsub_rn(1.0f, al[u][1])) : tau1;
           done0 = done0 || tau0 < o.tau_stop;
           done1 = done1 || tau1 < o.tau_stop;
+          wmax[u] = fmaxf(w0, w1);
         }
         if (CONTRIB) {
-          const uint32_t wm = __reduce_max_sync(0xffffffffu, __float_as_uint(fmaxf(w0, w1)));
-          if (lane == 0 && wm) atomicMax(&s_w[s_list[warp][q]], wm);
+          const uint32_t wa = __reduce_max_sync(0xffffffffu, __float_as_uint(wmax[0]));
+          const uint32_t wb = __reduce_max_sync(0xffffffffu, __float_as_uint(wmax[1]));
+          if (lane == 0 && wa) atomicMax(&s_w[ea], wa);
+          if (lane == 0 && wb && hasb) atomicMax(&s_w[eb], wb);
         }
         if (__all_sync(0xffffffffu, done0 && done1)) break;  // all 64 pixels of the warp terminated
       }
