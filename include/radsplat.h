@@ -26,6 +26,8 @@
  *                           (RSPL file bytes straight to / from HBM)
  *   rs_pack_bits         <- io.py:198-215 np.packbits(bitorder="little") of
  *                           save_visibility
+ *   rs_sq_diff_sum       <- metrics.py:34-45 mse / psnr
+ *   rs_ssim              <- metrics.py:59-117 ssim / ssim_with_grad
  *
  * Conventions
  *   - All data pointers are DEVICE pointers (rs_outputs' 64-bit images may be
@@ -253,6 +255,18 @@ RS_API int32_t rs_rspl_pack(const float* planes, int64_t plane_stride, const flo
                             void* stream);
 /* n flags (bytes, nonzero = set) -> ceil(n/8) bytes of LSB-first bits (RVIS indicator). */
 RS_API int32_t rs_pack_bits(const uint8_t* flags, int64_t n, uint8_t* bits, void* stream);
+
+/* sum of (a - b)^2 over n float64 values (device) -> *out_sum (device). */
+RS_API int32_t rs_sq_diff_sum(const double* a, const double* b, int64_t n, double* out_sum, void* stream);
+/* SSIM of (H, W, C) float64 images x, y (device, channels last): *out_sum = the
+ * sum of the per-window SSIM over all 'valid' windows and channels (divide by
+ * (H-win+1)(W-win+1)C for the reference's mean); `kernel` = the win x win
+ * Gaussian window (device, float64, metrics.py:48-52). With `grad` (H*W*C,
+ * device) also dSSIM/dx; that needs a scratch of rs_ssim_workspace_size bytes. */
+RS_API size_t rs_ssim_workspace_size(int32_t height, int32_t width, int32_t channels, int32_t win);
+RS_API int32_t rs_ssim(const double* x, const double* y, int32_t height, int32_t width, int32_t channels,
+                       int32_t win, const double* kernel, double* out_sum, double* grad, void* scratch,
+                       size_t scratch_bytes, void* stream);
 
 /* dst[i] = max(dst[i], src[i]) over n non-negative floats. */
 RS_API int32_t rs_max_merge(float* dst, const float* src, int64_t n, void* stream);

@@ -15,6 +15,7 @@
 #include "blend.cuh"
 #include "compact.cuh"
 #include "io.cuh"
+#include "metrics.cuh"
 #include "backward.cuh"
 #include "project.cuh"
 #include "sort.cuh"
@@ -569,6 +570,41 @@ int32_t rs_rspl_pack(const float* planes, int64_t plane_stride, const float* sh,
 int32_t rs_pack_bits(const uint8_t* flags, int64_t n, uint8_t* bits, void* stream) {
   if (n < 0 || (n > 0 && (!flags || !bits))) return RS_EINVAL;
   if (n > 0) pack_bits_kernel<<<(unsigned)((n + 255) / 256), 256, 0, S(stream)>>>(flags, n, bits);
+  return cuda_status();
+}
+
+int32_t rs_sq_diff_sum(const double* a, const double* b, int64_t n, double* out_sum, void* stream) {
+  if (n < 0 || !out_sum || (n > 0 && (!a || !b))) return RS_EINVAL;
+  cudaStream_t st = S(stream);
+  cudaMemsetAsync(out_sum, 0, sizeof(double), st);
+  if (n > 0) sq_diff_sum_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 1184), 256, 0, st>>>(a, b, n, out_sum);
+  return cuda_status();
+}
+
+size_t rs_ssim_workspace_size(int32_t height, int32_t width, int32_t channels, int32_t win) {
+  if (height < win || width < win || channels <= 0 || win <= 0) return 0;
+  return (size_t)3 * (height - win + 1) * (width - win + 1) * channels * sizeof(double);
+}
+
+int32_t rs_ssim(const double* x, const double* y, int32_t height, int32_t width, int32_t channels, int32_t win,
+                const double* kernel, double* out_sum, double* grad, void* scratch, size_t scratch_bytes,
+                void* stream) {
+  if (!x || !y || !kernel || !out_sum || win <= 0 || win > kMaxSsimWin || height < win || width < win ||
+      channels <= 0)
+    return RS_EINVAL;
+  if (grad && (!scratch || scratch_bytes < rs_ssim_workspace_size(height, width, channels, win)))
+    return RS_ENOMEM_WORKSPACE;
+  cudaStream_t st = S(stream);
+  cudaMemsetAsync(out_sum, 0, sizeof(double), st);
+  const int64_t nwin = (int64_t)(height - win + 1) * (width - win + 1) * channels;
+  double* maps = grad ? static_cast<double*>(scratch) : nullptr;
+  ssim_window_kernel<<<(unsigned)((nwin + 255) / 256), 256, 0, st>>>(x, y, height, width, channels, win, kernel,
+                                                                    out_sum, maps);
+  if (grad) {
+    const int64_t npx = (int64_t)height * width * channels;
+    ssim_grad_kernel<<<(unsigned)((npx + 255) / 256), 256, 0, st>>>(x, y, height, width, channels, win, kernel,
+                                                                     maps, 1.0 / (double)nwin, grad);
+  }
   return cuda_status();
 }
 

@@ -237,6 +237,7 @@ def main():
 
     make_io(fs, conftest)
     make_grad(fs, conftest)
+    make_metrics(fs, conftest)
     print("golden fixtures written to", HERE)
 
 
@@ -307,6 +308,28 @@ def make_grad(fs, conftest):
     np.savez_compressed(HERE / "grad.npz", **d)
 
 
+def make_metrics(fs, conftest):
+    """K: image metrics (metrics.py:34-117) on rendered and random images."""
+    M = fs.metrics
+    d = {}
+    rng = np.random.default_rng(7)
+    scene = conftest.random_scene(rng, 30, sh_degree=1)
+    cam = conftest.facing_camera(40, 32, distance=4.0)
+    a = fs.render.rasterize(scene, cam).color.data
+    b = np.clip(a + rng.normal(scale=0.05, size=a.shape), 0.0, 1.0)
+    cases = {"render": (a, b), "rand": (rng.uniform(size=(24, 27, 3)), rng.uniform(size=(24, 27, 3))),
+             "gray": (rng.uniform(size=(16, 20)), rng.uniform(size=(16, 20)))}
+    for name, (x, y) in cases.items():
+        d[name + "_a"], d[name + "_b"] = x, y
+        d[name + "_mse"] = np.float64(M.mse(x, y))
+        d[name + "_psnr"] = np.float64(M.psnr(x, y))
+        d[name + "_ssim"] = np.float64(M.ssim(x, y))
+        v, g = M.ssim_with_grad(x, y)
+        d[name + "_ssim_g"] = g
+        d[name + "_ssim7"] = np.float64(M.ssim(x, y, win_size=7, sigma=1.0))
+    np.savez_compressed(HERE / "metrics.npz", **d)
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["io"]:  # only the wire-format fixtures
         fs_, conftest_, _ = import_reference()
@@ -314,5 +337,8 @@ if __name__ == "__main__":
     elif sys.argv[1:] == ["grad"]:  # only the backward-pass fixtures
         fs_, conftest_, _ = import_reference()
         make_grad(fs_, conftest_)
+    elif sys.argv[1:] == ["metrics"]:  # only the image-metric fixtures
+        fs_, conftest_, _ = import_reference()
+        make_metrics(fs_, conftest_)
     else:
         main()
