@@ -26,6 +26,8 @@
  *                           (RSPL file bytes straight to / from HBM)
  *   rs_pack_bits         <- io.py:198-215 np.packbits(bitorder="little") of
  *                           save_visibility
+ *   rs_nearest_cluster   <- visibility.py:80-83 ClusterVisibility.nearest_cluster,
+ *                           batched over a trajectory
  *   rs_sq_diff_sum       <- metrics.py:34-45 mse / psnr
  *   rs_ssim              <- metrics.py:59-117 ssim / ssim_with_grad
  *
@@ -255,6 +257,11 @@ RS_API int32_t rs_rspl_pack(const float* planes, int64_t plane_stride, const flo
                             void* stream);
 /* n flags (bytes, nonzero = set) -> ceil(n/8) bytes of LSB-first bits (RVIS indicator). */
 RS_API int32_t rs_pack_bits(const uint8_t* flags, int64_t n, uint8_t* bits, void* stream);
+
+/* out[i] = index of the centre (k x 3, float64) nearest to position i (m x 3,
+ * float64): Euclidean distance as np.linalg.norm, lowest index on ties. */
+RS_API int32_t rs_nearest_cluster(const double* centers, int32_t k, const double* positions, int64_t m, int32_t* out,
+                                  void* stream);
 
 /* sum of (a - b)^2 over n float64 values (device) -> *out_sum (device). */
 RS_API int32_t rs_sq_diff_sum(const double* a, const double* b, int64_t n, double* out_sum, void* stream);

@@ -96,6 +96,7 @@ SIGNATURES = {
     "rs_rspl_unpack": (_i32, [_vp, _i64, _vp, _i64, _vp, _vp, _vp]),
     "rs_rspl_pack": (_i32, [_vp, _i64, _vp, _i64, _vp, _vp]),
     "rs_pack_bits": (_i32, [_vp, _i64, _vp, _vp]),
+    "rs_nearest_cluster": (_i32, [_vp, _i32, _vp, _i64, _vp, _vp]),
     "rs_sq_diff_sum": (_i32, [_vp, _vp, _i64, _vp, _vp]),
     "rs_ssim_workspace_size": (_sz, [_i32, _i32, _i32, _i32]),
     "rs_ssim": (_i32, [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _vp]),

@@ -608,6 +608,14 @@ int32_t rs_ssim(const double* x, const double* y, int32_t height, int32_t width,
   return cuda_status();
 }
 
+int32_t rs_nearest_cluster(const double* centers, int32_t k, const double* positions, int64_t m, int32_t* out,
+                           void* stream) {
+  if (k <= 0 || m < 0 || !centers || (m > 0 && (!positions || !out))) return RS_EINVAL;
+  if (m > 0)
+    nearest_cluster_kernel<<<(unsigned)((m + 255) / 256), 256, 0, S(stream)>>>(centers, k, positions, m, out);
+  return cuda_status();
+}
+
 int32_t rs_max_merge(float* dst, const float* src, int64_t n, void* stream) {
   if (n < 0 || (n > 0 && (!dst || !src))) return RS_EINVAL;
   if (n > 0)

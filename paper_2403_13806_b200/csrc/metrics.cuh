@@ -103,4 +103,27 @@ __global__ void __launch_bounds__(256) ssim_grad_kernel(const double* __restrict
   grad[idx] = (cm + 2.0 * x[idx] * cv + y[idx] * cxy) * inv_n;
 }
 
+// Nearest cluster centre of each camera position (visibility.py:80-83):
+// Euclidean distance as np.linalg.norm computes it (sqrt(((dx^2 + dy^2) + dz^2)),
+// float64), argmin with the lowest index on ties; one thread per position.
+__global__ void __launch_bounds__(256) nearest_cluster_kernel(const double* __restrict__ centers, int k,
+                                                              const double* __restrict__ pos, int64_t m,
+                                                              int32_t* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const double px = pos[3 * i], py = pos[3 * i + 1], pz = pos[3 * i + 2];
+  double best = 0.0;
+  int arg = 0;
+  for (int j = 0; j < k; ++j) {
+    const double dx = __dsub_rn(centers[3 * j], px), dy = __dsub_rn(centers[3 * j + 1], py),
+                 dz = __dsub_rn(centers[3 * j + 2], pz);
+    const double d = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+    if (j == 0 || d < best) {  // strict: the first minimum wins (np.argmin)
+      best = d;
+      arg = j;
+    }
+  }
+  out[i] = arg;
+}
+
 }  // namespace rs

@@ -241,3 +241,23 @@ def test_binning_anisotropic_bit_exact(case):
     ref = O.views(scene, [cam], opts, np.float32, scores=True, images=True)
     assert np.array_equal(out["rgb"].cpu().numpy(), ref["img_last"])
     assert np.array_equal(sc.cpu().numpy(), ref["contrib"])
+
+
+def test_nearest_clusters_device_batch_matches_reference_rule():
+    """Batched device lookup == the reference's argmin of np.linalg.norm (lowest index on ties),
+    including exact ties and a trajectory's worth of cameras."""
+    from paper_2403_13806_b200.core import look_at_camera
+    from paper_2403_13806_b200.visibility import ClusterVisibility, nearest_clusters
+    rng = np.random.default_rng(3)
+    centers = rng.uniform(-5, 5, size=(17, 3))
+    centers[5] = centers[2]  # duplicate centre: ties must go to index 2
+    vis = ClusterVisibility(centers=centers, indicators=np.zeros((17, 4), bool), t_cluster=0.0, scene_generation=0)
+    eyes = np.concatenate([rng.uniform(-6, 6, size=(300, 3)), centers[[2, 5, 7]],
+                           (centers[[0]] + centers[[1]]) / 2.0])  # on a centre / equidistant
+    cams = [look_at_camera(e, e + np.array([1.0, 0.2, 0.1]), width=8, height=8) for e in eyes]
+    got = nearest_clusters(vis, cams)
+    ref = np.array([int(np.argmin(np.linalg.norm(centers - (-c.rotation.T @ c.translation)[None, :], axis=1)))
+                    for c in cams])
+    assert np.array_equal(got, ref)
+    assert np.array_equal(got, [vis.nearest_cluster(-c.rotation.T @ c.translation) for c in cams])
+    assert got[300] == 2 and got[301] == 2
