@@ -50,7 +50,7 @@ Layout make_layout(int64_t n_cap, int64_t pair_cap, int W, int H) {
   // per-frame zeroed region
   L.ctr = take(sizeof(Counters));
   L.hist = take(8 * 256 * sizeof(uint32_t));  // depth passes 0-3, segment row passes 4-5
-  L.emit_lb = take(((size_t)n_cap / kSegCountThreads + 2) * sizeof(unsigned long long));
+  L.emit_lb = take(((size_t)n_cap / (kSegCountThreads * kSegCountItems) + 2) * sizeof(unsigned long long));
   L.proj_lb = take(((size_t)n_cap / kCompactKeys + 2) * sizeof(unsigned long long));
   L.ranges = take(TW * TH * sizeof(uint2));
   L.rowcnt = take((TH + 1) * sizeof(uint32_t));
@@ -312,7 +312,8 @@ int32_t rs_bin(rs_workspace* ws, void* stream) {
     // per-tile ranges, expansion into the per-tile lists (segbin.cuh)
     Counters* ctr = ws->ctr();
     const uint32_t seg_cap = (uint32_t)seg_capacity(ws->n_cap, ws->pair_cap);
-    segcount_kernel<<<(n + kSegCountThreads - 1) / kSegCountThreads, kSegCountThreads, 0, st>>>(
+    segcount_kernel<<<(n + kSegCountThreads * kSegCountItems - 1) / (kSegCountThreads * kSegCountItems),
+                      kSegCountThreads, 0, st>>>(
         items_sorted, ws->at<uint32_t>(ws->L.nrows), ctr, seg_cap, ws->at<uint32_t>(ws->L.offsets),
         ws->at<unsigned long long>(ws->L.emit_lb), ws->at<Sticky>(ws->L.sticky));
     segemit_kernel<<<std::max(1, std::min((int)((n + 255) / 256), ws->sms * 4)), 256, 0, st>>>(

@@ -38,12 +38,15 @@ constexpr int kExpandCols = 32;                // tile columns per expand CTA (8
 constexpr int kMaxTileRows = 2048;             // image height <= 32767 px
 constexpr int kMaxTileCols = 2048;             // image width <= 32767 px
 
+constexpr int kSegCountItems = 4;  // ranks per thread (fewer, longer CTAs: a short look-back chain)
+
 __global__ void __launch_bounds__(kSegCountThreads) segcount_kernel(const uint32_t* __restrict__ items_sorted,
                                                                     const uint32_t* __restrict__ nrows,
                                                                     Counters* __restrict__ ctr, uint32_t seg_cap,
                                                                     uint32_t* __restrict__ offsets,
                                                                     unsigned long long* __restrict__ status,
                                                                     Sticky* __restrict__ sticky) {
+  constexpr uint32_t kPer = kSegCountThreads * kSegCountItems;
   __shared__ uint32_t s_block;
   __shared__ uint32_t s_wsum[kSegCountThreads / 32];
   __shared__ unsigned long long s_base;
@@ -52,10 +55,16 @@ __global__ void __launch_bounds__(kSegCountThreads) segcount_kernel(const uint32
   __syncthreads();
   const uint32_t b = s_block;
   const uint32_t nvis = ctr->n_visible;
-  if (b * kSegCountThreads >= nvis && b > 0) return;
-  const uint32_t r = b * kSegCountThreads + tid;
-  const uint32_t nt = r < nvis ? nrows[items_sorted[r]] : 0u;
-  uint32_t x = nt;
+  if (b * kPer >= nvis && b > 0) return;
+  // this thread's kSegCountItems consecutive ranks
+  const uint32_t r0 = b * kPer + tid * kSegCountItems;
+  uint32_t nt[kSegCountItems], tsum = 0;
+#pragma unroll
+  for (int q = 0; q < kSegCountItems; ++q) {
+    nt[q] = r0 + q < nvis ? nrows[items_sorted[r0 + q]] : 0u;
+    tsum += nt[q];
+  }
+  uint32_t x = tsum;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
@@ -76,7 +85,7 @@ __global__ void __launch_bounds__(kSegCountThreads) segcount_kernel(const uint32
     if (lane == 0) {
       if (b) st[b] = kLbInc | (excl + total);
       s_base = excl;
-      if (nvis > 0 && b == (nvis - 1) / kSegCountThreads) {
+      if (nvis > 0 && b == (nvis - 1) / kPer) {
         const unsigned long long end = excl + total;
         ctr->n_segs = (uint32_t)(end < seg_cap ? end : seg_cap);
         if (end > seg_cap) {  // too many segments: the frame is re-run with a larger workspace
@@ -91,7 +100,12 @@ __global__ void __launch_bounds__(kSegCountThreads) segcount_kernel(const uint32
     }
   }
   __syncthreads();
-  if (r < nvis) offsets[r] = (uint32_t)(s_base + off + x - nt);
+  uint32_t o = (uint32_t)s_base + off + x - tsum;
+#pragma unroll
+  for (int q = 0; q < kSegCountItems; ++q) {
+    if (r0 + q < nvis) offsets[r0 + q] = o;
+    o += nt[q];
+  }
 }
 
 // One warp per 32 consecutive ranks (persistent warps take rank chunks from a counter).
