@@ -256,6 +256,7 @@ __global__ void __launch_bounds__(256) expand_kernel(const uint32_t* __restrict_
                                                      const Counters* __restrict__ ctr,
                                                      uint32_t* __restrict__ pair_items) {
   __shared__ uint32_t s_item[256], s_span[256];
+  __shared__ int s_wk[8];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (WRITE && ctr->overflow) return;
   const int c0 = blockIdx.y * kExpandCols + warp * 4;  // this warp's 4 tile columns
@@ -271,15 +272,36 @@ __global__ void __launch_bounds__(256) expand_kernel(const uint32_t* __restrict_
       pos[q] = 0;
       if (WRITE && c0 + q < TW) pos[q] = ranges[ty * TW + c0 + q].x + chunk_count[(size_t)gc * TW + c0 + q];
     }
+    const int g0 = blockIdx.y * kExpandCols, g1 = g0 + kExpandCols - 1;  // this CTA's columns
     for (uint32_t base = s0; base < s1; base += 256) {
-      const uint32_t n = min(256u, s1 - base);
+      const uint32_t nb = min(256u, s1 - base);
       __syncthreads();
-      if (tid < n) {
+      // stage only the segments that reach this CTA's 32 columns, in order (block compaction):
+      // the warps then walk ~45% of the chunk instead of all of it
+      uint32_t sp = kEmptySpan, sit = 0;
+      if (tid < nb) {
         const uint32_t sid = sorted_seg[base + tid];
-        if (WRITE) s_item[tid] = seg_item[sid];
-        s_span[tid] = seg_span[sid];
+        sp = seg_span[sid];
+        if (WRITE) sit = seg_item[sid];
+      }
+      const int a0 = (int)(sp & 0xffffu), a1 = (int)(sp >> 16);
+      const bool keep = a0 <= a1 && a0 <= g1 && a1 >= g0;
+      const unsigned kb = __ballot_sync(0xffffffffu, keep);
+      if (lane == 0) s_wk[warp] = __popc(kb);
+      __syncthreads();
+      int koff = 0, n2 = 0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) {
+        koff += w < warp ? s_wk[w] : 0;
+        n2 += s_wk[w];
+      }
+      if (keep) {
+        const int at = koff + __popc(kb & lt);
+        s_span[at] = sp;
+        if (WRITE) s_item[at] = sit;
       }
       __syncthreads();
+      const uint32_t n = (uint32_t)n2;
       if (c0 >= TW) continue;
       for (uint32_t sub = 0; sub < n; sub += 32) {
         const uint32_t e = sub + lane;
