@@ -30,7 +30,7 @@ struct Layout {
   // per-frame zeroed region [0, frame_bytes)
   size_t ctr, hist, emit_lb, proj_lb, ranges, rowcnt, frame_bytes;
   size_t sticky, cam, recs, nrows, sgrad, titem, keysA, keysB, valsA, valsB, offsets, segkeyA, segkeyB, segvalA,
-      segvalB, segitem, segspan, rowstart, chunkstart, chunkcnt, tilecnt, pitem, lbA, lbB, total;
+      segvalB, segitem, segspan, rowstart, chunkstart, chunkcnt, chunkinfo, densel, tilecnt, pitem, lbA, lbB, total;
 };
 
 int tiles_x(int w) { return (w + kTile - 1) / kTile; }
@@ -75,6 +75,8 @@ Layout make_layout(int64_t n_cap, int64_t pair_cap, int W, int H) {
   L.rowstart = take((TH + 1) * 4);
   L.chunkstart = take((TH + 1) * 4);
   L.chunkcnt = take((seg_cap / kExpandChunk + TH + 1) * TW * 4);
+  L.chunkinfo = take((seg_cap / kExpandChunk + TH + 1) * 8);
+  L.densel = take((seg_cap / kExpandChunk + TH + 1) * 4);
   L.tilecnt = take(TW * TH * 4);
   L.pitem = take((size_t)pair_cap * 4);
   const size_t chunks = (std::max<size_t>((size_t)n_cap, seg_cap) + kMinChunk - 1) / kMinChunk + 1;
@@ -85,6 +87,22 @@ Layout make_layout(int64_t n_cap, int64_t pair_cap, int W, int H) {
 }
 
 }  // namespace
+
+int expand_major_thresh() {  // expand's column-major switch (x8): RS_EXPAND_MAJOR overrides (tuning)
+  static const int t = [] {
+    const char* e = std::getenv("RS_EXPAND_MAJOR");
+    return e ? std::atoi(e) : 8;
+  }();
+  return t;
+}
+
+int expand_dense_span() {  // chunks averaging >= this many tiles per segment take the ballot walk
+  static const int t = [] {
+    const char* e = std::getenv("RS_EXPAND_DENSE");
+    return e ? std::atoi(e) : 6;
+  }();
+  return t;
+}
 
 struct rs_workspace {
   unsigned char* base;
@@ -98,7 +116,14 @@ struct rs_workspace {
   int W, H, TW, TH;
   int row_bits;  // bits of a tile-row index (segment sort key)
   bool binned, have_cam, has_color;
+  cudaStream_t aux = nullptr;  // second stream (dense expansion next to the sparse one)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 
+  ~rs_workspace() {
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (aux) cudaStreamDestroy(aux);
+  }
   template <typename T> T* at(size_t off) const { return reinterpret_cast<T*>(base + off); }
   Counters* ctr() const { return at<Counters>(L.ctr); }
 };
@@ -217,7 +242,10 @@ int32_t rs_workspace_create(void* device_mem, size_t bytes, int64_t n_cap, int64
   cudaGetDevice(&dev);
   if (cudaDeviceGetAttribute(&ws->sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) ws->sms = 148;
   configure_kernels();
-  if (cudaMemset(ws->at<Sticky>(L.sticky), 0, sizeof(Sticky)) != cudaSuccess) {
+  if (cudaMemset(ws->at<Sticky>(L.sticky), 0, sizeof(Sticky)) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&ws->aux, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ws->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ws->ev_join, cudaEventDisableTiming) != cudaSuccess) {
     delete ws;
     return RS_ECUDA;
   }
@@ -330,21 +358,34 @@ int32_t rs_bin(rs_workspace* ws, void* stream) {
     row_scan_kernel<<<1, 32, 0, st>>>(ws->at<uint32_t>(ws->L.rowcnt), ws->TH, ws->at<uint32_t>(ws->L.rowstart),
                                       ws->at<uint32_t>(ws->L.chunkstart));
     const unsigned gx = (unsigned)std::min<int64_t>(seg_cap / kExpandChunk + ws->TH + 1, (int64_t)ws->sms * 16);
-    const dim3 eg(gx, (ws->TW + kExpandCols - 1) / kExpandCols);  // chunks grid-strided
+    // expansion: the sparse chunks grid-strided (column groups x chunk slots), the dense ones on
+    // persistent ticketed CTAs on the workspace's second stream, concurrently
+    const dim3 eg((ws->TW + kExpandCols - 1) / kExpandCols, gx), dg(ws->sms * 6);
     chunk_count_kernel<<<gx, 256, 0, st>>>(sorted_seg, ws->at<uint32_t>(ws->L.segspan),
                                            ws->at<uint32_t>(ws->L.rowstart), ws->at<uint32_t>(ws->L.chunkstart),
-                                           ws->TH, ws->TW, ws->at<uint32_t>(ws->L.chunkcnt));
+                                           ws->TH, ws->TW, ws->at<uint32_t>(ws->L.chunkcnt),
+                                           ws->at<uint2>(ws->L.chunkinfo), expand_dense_span(), ctr,
+                                           ws->at<uint32_t>(ws->L.densel));
     const int T = ws->TW * ws->TH;
     tile_chunks_kernel<<<(T + 7) / 8, 256, 0, st>>>(ws->at<uint32_t>(ws->L.chunkstart), ws->TH, ws->TW,
                                                         ws->at<uint32_t>(ws->L.chunkcnt),
                                                         ws->at<uint32_t>(ws->L.tilecnt));
     tile_scan_kernel<<<1, 1024, 0, st>>>(ws->at<uint32_t>(ws->L.tilecnt), T, ctr, (uint32_t)ws->pair_cap,
                                          ws->at<uint2>(ws->L.ranges), ws->at<Sticky>(ws->L.sticky));
-    expand_kernel<true><<<eg, 256, 0, st>>>(sorted_seg, ws->at<uint32_t>(ws->L.segitem),
-                                            ws->at<uint32_t>(ws->L.segspan), ws->at<uint32_t>(ws->L.rowstart),
-                                            ws->at<uint32_t>(ws->L.chunkstart), ws->TH, ws->TW,
+    cudaEventRecord(ws->ev_fork, st);
+    cudaStreamWaitEvent(ws->aux, ws->ev_fork, 0);
+    expand_dense_kernel<<<dg, 256, 0, ws->aux>>>(sorted_seg, ws->at<uint32_t>(ws->L.segitem),
+                                            ws->at<uint32_t>(ws->L.segspan), ws->at<uint2>(ws->L.chunkinfo),
+                                            ws->at<uint32_t>(ws->L.densel), ws->TW,
                                             ws->at<uint32_t>(ws->L.chunkcnt), ws->at<uint2>(ws->L.ranges), ctr,
                                             ws->at<uint32_t>(ws->L.pitem));
+    cudaEventRecord(ws->ev_join, ws->aux);
+    expand_kernel<<<eg, 256, 0, st>>>(sorted_seg, ws->at<uint32_t>(ws->L.segitem),
+                                      ws->at<uint32_t>(ws->L.segspan), ws->at<uint2>(ws->L.chunkinfo),
+                                      ws->at<uint32_t>(ws->L.chunkstart), ws->TH, ws->TW,
+                                      ws->at<uint32_t>(ws->L.chunkcnt), ws->at<uint2>(ws->L.ranges), ctr,
+                                      ws->at<uint32_t>(ws->L.pitem), expand_major_thresh());
+    cudaStreamWaitEvent(st, ws->ev_join, 0);
   }
   ws->binned = true;
   return cuda_status();

@@ -242,89 +242,203 @@ __device__ __forceinline__ bool chunk_of(const uint32_t* __restrict__ chunk_star
 }
 
 // Pass 2: the chunk's covering segments appended to each column's tile list after all
-// earlier chunks of the row (ranges + chunk prefix): warp w owns 4 columns, 32 segments per
-// ballot (their order = depth order), segments staged 256 at a time. (WRITE = false: the
-// same walk only counting -- kept for reference; chunk_count_kernel is the pass 1 used.)
-template <bool WRITE>
+// earlier chunks of the row (ranges + chunk prefix). A CTA owns 32 tile columns and takes the
+// chunk 256 segments at a time, warp w the w-th 32 of them: each lane turns its segment's span
+// into a 32-bit mask over the CTA's columns, a 32x32 bit transpose (5 shuffle stages) gives
+// lane c the mask of the warp's segments covering column c, and lane c appends those items in
+// segment (= depth) order after the earlier warps' counts (one shared-memory exchange).
+__device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
+  constexpr uint32_t kM[5] = {0x0000ffffu, 0x00ff00ffu, 0x0f0f0f0fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+  for (int s = 0; s < 5; ++s) {
+    const int j = 16 >> s;
+    const uint32_t m = kM[s];
+    const uint32_t y = __shfl_xor_sync(0xffffffffu, x, j);
+    x = (lane & j) ? ((x & ~m) | ((y >> j) & m)) : ((x & m) | ((y & m) << j));
+  }
+  return x;
+}
+
+// Dense chunks (long spans: most of the CTA's columns covered by most segments): warp w owns
+// 4 columns and walks all the chunk's segments that reach the CTA's columns (staged 256 at a
+// time, block-compacted in order), one ballot per column per 32 segments -- every store
+// instruction writes one column's run contiguously.
+__device__ __forceinline__ void expand_dense_chunk(const uint32_t* __restrict__ sorted_seg,
+                                                   const uint32_t* __restrict__ seg_item,
+                                                   const uint32_t* __restrict__ seg_span, uint32_t s0, uint32_t cnt,
+                                                   int ty, uint32_t gc, int g0, int TW,
+                                                   const uint32_t* __restrict__ chunk_count,
+                                                   const uint2* __restrict__ ranges,
+                                                   uint32_t* __restrict__ pair_items, uint32_t* s_item,
+                                                   uint32_t* s_span, int* s_wk) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t lt = (1u << lane) - 1u;
+  const int c0 = g0 + warp * 4;  // this warp's 4 tile columns
+  const int g1 = g0 + kExpandCols - 1;
+  uint32_t pos[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) pos[q] = c0 + q < TW ? ranges[ty * TW + c0 + q].x + chunk_count[(size_t)gc * TW + c0 + q] : 0u;
+  for (uint32_t base = 0; base < cnt; base += 256) {
+    const uint32_t nb = min(256u, cnt - base);
+    uint32_t sp = kEmptySpan, sit = 0;
+    if (tid < nb) {
+      const uint32_t sid = sorted_seg[s0 + base + tid];
+      sp = seg_span[sid];
+      sit = seg_item[sid];
+    }
+    const int a0 = (int)(sp & 0xffffu), a1 = (int)(sp >> 16);
+    const bool keep = a0 <= a1 && a0 <= g1 && a1 >= g0;
+    const unsigned kb = __ballot_sync(0xffffffffu, keep);
+    __syncthreads();  // the previous batch's readers are done
+    if (lane == 0) s_wk[warp] = __popc(kb);
+    __syncthreads();
+    int koff = 0, n = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      koff += w < warp ? s_wk[w] : 0;
+      n += s_wk[w];
+    }
+    if (keep) {
+      const int at = koff + __popc(kb & lt);
+      s_span[at] = sp;
+      s_item[at] = sit;
+    }
+    __syncthreads();
+    if (c0 >= TW) continue;
+    for (int sub = 0; sub < n; sub += 32) {
+      const int e = sub + lane;
+      const uint32_t sq = e < n ? s_span[e] : kEmptySpan;
+      const int t0 = (int)(sq & 0xffffu), t1 = (int)(sq >> 16);
+      const bool near = t0 <= t1 && t0 <= c0 + 3 && t1 >= c0;
+      if (!__any_sync(0xffffffffu, near)) continue;
+      const uint32_t item = near ? s_item[e] : 0u;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int c = c0 + q;
+        const bool cov = near && t0 <= c && c <= t1;
+        const unsigned bal = __ballot_sync(0xffffffffu, cov);
+        if (cov) pair_items[pos[q] + __popc(bal & lt)] = item;
+        pos[q] += __popc(bal);
+      }
+    }
+  }
+}
+
+constexpr int kExpandSub = kExpandChunk / 256;  // 32-segment sub-steps per warp per chunk
+
 __global__ void __launch_bounds__(256) expand_kernel(const uint32_t* __restrict__ sorted_seg,
                                                      const uint32_t* __restrict__ seg_item,
                                                      const uint32_t* __restrict__ seg_span,
-                                                     const uint32_t* __restrict__ row_start,
+                                                     const uint2* __restrict__ chunk_info,
                                                      const uint32_t* __restrict__ chunk_start, int TH, int TW,
-                                                     uint32_t* __restrict__ chunk_count /* [chunk][TW] */,
+                                                     const uint32_t* __restrict__ chunk_count /* [chunk][TW] */,
                                                      const uint2* __restrict__ ranges,
                                                      const Counters* __restrict__ ctr,
-                                                     uint32_t* __restrict__ pair_items) {
-  __shared__ uint32_t s_item[256], s_span[256];
-  __shared__ int s_wk[8];
+                                                     uint32_t* __restrict__ pair_items, int major_thresh) {
+  __shared__ uint32_t s_cnt[2][8][32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (WRITE && ctr->overflow) return;
-  const int c0 = blockIdx.y * kExpandCols + warp * 4;  // this warp's 4 tile columns
+  if (ctr->overflow) return;
   const uint32_t lt = (1u << lane) - 1u;
-  for (uint32_t gc = blockIdx.x;; gc += gridDim.x) {  // chunks of all rows, grid-strided
-    int ty;
-    uint32_t lc;
-    if (!chunk_of(chunk_start, TH, gc, ty, lc)) break;
-    const uint32_t s0 = row_start[ty] + lc * kExpandChunk, s1 = min(row_start[ty + 1], s0 + kExpandChunk);
-    uint32_t pos[4];
+  // column group fastest in the grid: a chunk's CTAs run together and share its segments in L2
+  const int g0 = blockIdx.x * kExpandCols;  // this CTA's first tile column
+  const int c = g0 + lane;                  // lane's column (every warp)
+  const uint32_t n_chunks = chunk_start[TH];
+  int flip = 0;
+  for (uint32_t gc = blockIdx.y; gc < n_chunks; gc += gridDim.y) {  // chunks of all rows, grid-strided
+    const uint2 info = chunk_info[gc];  // {first segment, row | count << 16 | dense << 31}
+    if (info.y >> 31) continue;         // dense: expand_dense_kernel (concurrently, on a second stream)
+    const int ty = (int)(info.y & 0xffffu);
+    const uint32_t cnt = (info.y >> 16) & 0x7fffu;
+    const uint32_t pos = c < TW ? ranges[ty * TW + c].x + chunk_count[(size_t)gc * TW + c] : 0u;
+    // warp w: the chunk's segments [128 w, 128 w + 128), 32 per sub-step, all loads issued up front
+    uint32_t sid[kExpandSub], m[kExpandSub], item[kExpandSub], cm[kExpandSub];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      pos[q] = 0;
-      if (WRITE && c0 + q < TW) pos[q] = ranges[ty * TW + c0 + q].x + chunk_count[(size_t)gc * TW + c0 + q];
+    for (int k = 0; k < kExpandSub; ++k) {
+      const uint32_t e = (uint32_t)(warp * 32 * kExpandSub + k * 32 + lane);
+      sid[k] = e < cnt ? sorted_seg[info.x + e] : 0xffffffffu;
     }
-    const int g0 = blockIdx.y * kExpandCols, g1 = g0 + kExpandCols - 1;  // this CTA's columns
-    for (uint32_t base = s0; base < s1; base += 256) {
-      const uint32_t nb = min(256u, s1 - base);
-      __syncthreads();
-      // stage only the segments that reach this CTA's 32 columns, in order (block compaction):
-      // the warps then walk ~45% of the chunk instead of all of it
-      uint32_t sp = kEmptySpan, sit = 0;
-      if (tid < nb) {
-        const uint32_t sid = sorted_seg[base + tid];
-        sp = seg_span[sid];
-        if (WRITE) sit = seg_item[sid];
-      }
-      const int a0 = (int)(sp & 0xffffu), a1 = (int)(sp >> 16);
-      const bool keep = a0 <= a1 && a0 <= g1 && a1 >= g0;
-      const unsigned kb = __ballot_sync(0xffffffffu, keep);
-      if (lane == 0) s_wk[warp] = __popc(kb);
-      __syncthreads();
-      int koff = 0, n2 = 0;
+    uint32_t sp[kExpandSub];
 #pragma unroll
-      for (int w = 0; w < 8; ++w) {
-        koff += w < warp ? s_wk[w] : 0;
-        n2 += s_wk[w];
-      }
-      if (keep) {
-        const int at = koff + __popc(kb & lt);
-        s_span[at] = sp;
-        if (WRITE) s_item[at] = sit;
-      }
-      __syncthreads();
-      const uint32_t n = (uint32_t)n2;
-      if (c0 >= TW) continue;
-      for (uint32_t sub = 0; sub < n; sub += 32) {
-        const uint32_t e = sub + lane;
-        const uint32_t sp = e < n ? s_span[e] : kEmptySpan;
-        const int t0 = (int)(sp & 0xffffu), t1 = (int)(sp >> 16);
-        const bool near = t0 <= t1 && t0 <= c0 + 3 && t1 >= c0;
-        if (!__any_sync(0xffffffffu, near)) continue;
-        const uint32_t item = (WRITE && near) ? s_item[e] : 0u;
+    for (int k = 0; k < kExpandSub; ++k) sp[k] = seg_span[sid[k] != 0xffffffffu ? sid[k] : 0u];  // all in flight
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int c = c0 + q;
-          const bool cov = near && t0 <= c && c <= t1;
-          const unsigned bal = __ballot_sync(0xffffffffu, cov);
-          if (WRITE && cov) pair_items[pos[q] + __popc(bal & lt)] = item;
-          pos[q] += __popc(bal);
+    for (int k = 0; k < kExpandSub; ++k) {
+      const int a = max((int)(sp[k] & 0xffffu) - g0, 0), b = min((int)(sp[k] >> 16) - g0, kExpandCols - 1);
+      m[k] = sid[k] != 0xffffffffu && a <= b ? (0xffffffffu >> (31 - b)) & (0xffffffffu << a) : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < kExpandSub; ++k) item[k] = m[k] ? seg_item[sid[k]] : 0u;
+    uint32_t mine = 0;
+#pragma unroll
+    for (int k = 0; k < kExpandSub; ++k) {
+      cm[k] = __any_sync(0xffffffffu, m[k] != 0u) ? transpose32(m[k], lane) : 0u;
+      mine += __popc(cm[k]);
+    }
+    s_cnt[flip][warp][lane] = mine;
+    __syncthreads();
+    uint32_t p = pos;  // after the earlier warps' segments
+#pragma unroll
+    for (int w = 0; w < 8; ++w) p += w < warp ? s_cnt[flip][w][lane] : 0u;
+    flip ^= 1;  // double-buffered counts: one barrier per chunk
+#pragma unroll
+    for (int k = 0; k < kExpandSub; ++k) {
+      uint32_t x = cm[k];
+      const uint32_t cols = __ballot_sync(0xffffffffu, x != 0u);
+      if (!cols) continue;
+      const int deep = __reduce_max_sync(0xffffffffu, (unsigned)__popc(x));
+      if (__popc(cols) * major_thresh <= deep * 8) {
+        // few, deep columns: one column at a time, the covering lanes store contiguously
+        for (uint32_t cs = cols; cs; cs &= cs - 1u) {
+          const int col = __ffs(cs) - 1;
+          const uint32_t xc = __shfl_sync(0xffffffffu, x, col);
+          const uint32_t pc = __shfl_sync(0xffffffffu, p, col);
+          if ((xc >> lane) & 1u) pair_items[pc + __popc(xc & lt)] = item[k];
+        }
+        p += __popc(x);
+      } else {
+        // many shallow columns: lane = column, appending its covering segments in order
+        while (__any_sync(0xffffffffu, x != 0u)) {
+          const int src = x ? __ffs(x) - 1 : 0;
+          const uint32_t it = __shfl_sync(0xffffffffu, item[k], src);
+          if (x) {
+            pair_items[p++] = it;
+            x &= x - 1u;
+          }
         }
       }
     }
-    if (!WRITE && lane == 0) {
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (c0 + q < TW) chunk_count[(size_t)gc * TW + c0 + q] = pos[q];
-    }
+  }
+}
+
+// The dense chunks (listed by chunk_count_kernel, any order: chunks are independent).
+__global__ void __launch_bounds__(256) expand_dense_kernel(const uint32_t* __restrict__ sorted_seg,
+                                                           const uint32_t* __restrict__ seg_item,
+                                                           const uint32_t* __restrict__ seg_span,
+                                                           const uint2* __restrict__ chunk_info,
+                                                           const uint32_t* __restrict__ dense_list, int TW,
+                                                           const uint32_t* __restrict__ chunk_count,
+                                                           const uint2* __restrict__ ranges,
+                                                           Counters* __restrict__ ctr,
+                                                           uint32_t* __restrict__ pair_items) {
+  __shared__ uint32_t s_item[256], s_span[256];
+  __shared__ int s_wk[8];
+  __shared__ uint32_t s_tk[2];
+  if (ctr->overflow) return;
+  const uint32_t groups = (uint32_t)(TW + kExpandCols - 1) / kExpandCols;
+  const uint32_t total = ctr->n_dense * groups;
+  if (threadIdx.x == 0) s_tk[0] = atomicAdd(&ctr->dense_work, 1u);
+  __syncthreads();
+  int flip = 0;
+  // persistent CTAs take (dense chunk, column group) tickets, the next one fetched while this one
+  // runs (every chunk walk has a barrier); a chunk's column groups are consecutive tickets
+  for (;;) {
+    const uint32_t t = s_tk[flip];
+    if (t >= total) break;
+    if (threadIdx.x == 0) s_tk[flip ^ 1] = atomicAdd(&ctr->dense_work, 1u);
+    const uint32_t gc = dense_list[t / groups];
+    const uint2 info = chunk_info[gc];
+    expand_dense_chunk(sorted_seg, seg_item, seg_span, info.x, (info.y >> 16) & 0x7fffu, (int)(info.y & 0xffffu), gc,
+                       (int)(t % groups) * kExpandCols, TW, chunk_count, ranges, pair_items, s_item, s_span, s_wk);
+    flip ^= 1;
   }
 }
 
@@ -334,8 +448,12 @@ __global__ void __launch_bounds__(256) chunk_count_kernel(const uint32_t* __rest
                                                           const uint32_t* __restrict__ seg_span,
                                                           const uint32_t* __restrict__ row_start,
                                                           const uint32_t* __restrict__ chunk_start, int TH, int TW,
-                                                          uint32_t* __restrict__ chunk_count) {
+                                                          uint32_t* __restrict__ chunk_count,
+                                                          uint2* __restrict__ chunk_info, int dense_span,
+                                                          Counters* __restrict__ ctr,
+                                                          uint32_t* __restrict__ dense_list) {
   __shared__ uint32_t s_cnt[kMaxTileCols];
+  __shared__ uint32_t s_tiles;
   const int tid = threadIdx.x;
   for (uint32_t gc = blockIdx.x;; gc += gridDim.x) {
     int ty;
@@ -343,14 +461,25 @@ __global__ void __launch_bounds__(256) chunk_count_kernel(const uint32_t* __rest
     if (!chunk_of(chunk_start, TH, gc, ty, lc)) break;
     __syncthreads();
     for (int c = tid; c < TW; c += 256) s_cnt[c] = 0;
+    if (tid == 0) s_tiles = 0;
     __syncthreads();
     const uint32_t s0 = row_start[ty] + lc * kExpandChunk, s1 = min(row_start[ty + 1], s0 + kExpandChunk);
+    int tiles = 0;
     for (uint32_t sidx = s0 + tid; sidx < s1; sidx += 256) {
       const uint32_t sp = seg_span[sorted_seg[sidx]];
       const int t0 = (int)(sp & 0xffffu), t1 = (int)(sp >> 16);
       for (int c = t0; c <= t1; ++c) atomicAdd(&s_cnt[c], 1u);
+      tiles += max(t1 - t0 + 1, 0);
     }
+    tiles = __reduce_add_sync(0xffffffffu, tiles);
+    if ((tid & 31) == 0) atomicAdd(&s_tiles, (uint32_t)tiles);
     __syncthreads();
+    // dense: the segments average >= dense_span tiles (expand_kernel's ballot walk)
+    if (tid == 0) {
+      const bool dense = s_tiles >= (uint32_t)dense_span * (s1 - s0);
+      chunk_info[gc] = make_uint2(s0, (uint32_t)ty | ((s1 - s0) << 16) | (dense ? 0x80000000u : 0u));
+      if (dense) dense_list[atomicAdd(&ctr->n_dense, 1u)] = gc;
+    }
     for (int c = tid; c < TW; c += 256) chunk_count[(size_t)gc * TW + c] = s_cnt[c];
   }
 }
