@@ -18,12 +18,17 @@
 //                    depth order (stable).
 //   row_scan_kernel  per-row segment starts; rows cut into chunks of 1024.
 //   chunk_count_kernel  one CTA per chunk: per tile column the number of the
-//                    chunk's segments covering it (shared-memory counters).
+//                    chunk's segments covering it (shared-memory counters);
+//                    the chunk's {first segment, row, count, dense} record and
+//                    the list of dense chunks (>= 8 tiles per segment).
 //   tile_chunks_kernel / tile_scan_kernel  per tile: prefix over its row's
 //                    chunks and its total; exclusive scan over the tiles ->
 //                    ranges [start, end), P, overflow.
-//   expand_kernel<true>  the same walk again, appending each covering
-//                    segment's item to the column's tile list at its rank.
+//   expand_kernel    sparse chunks x 32-column groups: per warp 32 segments'
+//                    column masks, transposed (lane = column), each column's
+//                    covering items appended at its rank.
+//   expand_dense_kernel  dense chunks (second stream, concurrently): warp =
+//                    4 columns, one ballot per column per 32 segments.
 // The pair lists and ranges are the same as a stable sort of all pairs by
 // tile would produce (the parity tests compare them with the oracle).
 #pragma once
