@@ -723,9 +723,9 @@ def profiled_traffic(kernel: str):
 
 def frame_launches(W, H):
     """Kernels per frame: project, depth compaction+histogram, 4 depth passes, segment
-    count, segment emission, the segment row passes, row scan, chunk count, tile chunks,
-    tile scan, expansion (sparse and dense chunks), blend."""
-    return 1 + 1 + 4 + 1 + 1 + row_passes(H) + 1 + 1 + 1 + 1 + 2 + 1
+    count, segment emission, the segment row passes, chunk count (with the row scan), tile
+    chunks, tile scan, expansion (sparse and dense chunks), blend."""
+    return 1 + 1 + 4 + 1 + 1 + row_passes(H) + 1 + 1 + 1 + 2 + 1
 
 
 def row_passes(H):

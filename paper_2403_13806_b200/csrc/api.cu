@@ -348,15 +348,13 @@ int32_t rs_bin(rs_workspace* ws, void* stream) {
         items_sorted, ws->at<Rec>(ws->L.recs), ws->at<uint32_t>(ws->L.offsets), ctr, ws->TW,
         ws->at<uint16_t>(ws->L.segkeyA), ws->at<uint32_t>(ws->L.segitem), ws->at<uint32_t>(ws->L.segspan), ws->TH,
         ws->at<uint32_t>(ws->L.rowcnt), ws->at<uint32_t>(ws->L.hist) + 4 * 256, ws->at<uint32_t>(ws->L.lbA),
-        kSortThreads * kTileItems);
+        kSortThreads * kTileItems, ws->at<uint32_t>(ws->L.rowstart), ws->at<uint32_t>(ws->L.chunkstart));
     const uint16_t* rows_res;
     const uint32_t* sorted_seg;
     run_sort<uint16_t, kTileItems>(ws, ws->at<uint16_t>(ws->L.segkeyA), ws->at<uint16_t>(ws->L.segkeyA),
                                    ws->at<uint16_t>(ws->L.segkeyB), nullptr, ws->at<uint32_t>(ws->L.segvalA),
                                    ws->at<uint32_t>(ws->L.segvalB), &ctr->n_segs, 0, seg_cap, ws->row_bits, 4, 4,
                                    false, st, &rows_res, &sorted_seg);
-    row_scan_kernel<<<1, 32, 0, st>>>(ws->at<uint32_t>(ws->L.rowcnt), ws->TH, ws->at<uint32_t>(ws->L.rowstart),
-                                      ws->at<uint32_t>(ws->L.chunkstart));
     const unsigned gx = (unsigned)std::min<int64_t>(seg_cap / kExpandChunk + ws->TH + 1, (int64_t)ws->sms * 16);
     // expansion: the sparse chunks grid-strided (column groups x chunk slots), the dense ones on
     // persistent ticketed CTAs on the workspace's second stream, concurrently

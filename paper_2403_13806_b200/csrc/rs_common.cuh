@@ -53,7 +53,8 @@ struct Counters {
   uint32_t n_segs;       // row segments of the binned items (segbin.cuh)
   uint32_t n_dense;      // dense expansion chunks listed by chunk_count_kernel
   uint32_t dense_work;   // (dense chunk, column group) tickets of expand_dense_kernel
-  uint32_t pad[4];
+  uint32_t emit_done;    // finished segemit CTAs (the last one scans the row counts)
+  uint32_t pad[3];
 };
 static_assert(sizeof(Counters) == 128, "Counters is 128 B");
 

@@ -13,10 +13,11 @@
 //   segemit_kernel   one warp per 32 ranks, rows flattened over the lanes:
 //                    each segment's span (row_span), written in depth-rank
 //                    order as (row key, item, span); per-row segment counts
-//                    (= the sort's digit histogram).
+//                    (= the sort's digit histogram). The last CTA scans the
+//                    counts: per-row segment starts, rows cut into chunks of
+//                    1024.
 //   onesweep (1 pass over the row key, sort.cuh) -> every row's segments in
 //                    depth order (stable).
-//   row_scan_kernel  per-row segment starts; rows cut into chunks of 1024.
 //   chunk_count_kernel  one CTA per chunk: per tile column the number of the
 //                    chunk's segments covering it (shared-memory counters);
 //                    the chunk's {first segment, row, count, dense} record and
@@ -113,6 +114,60 @@ __global__ void __launch_bounds__(kSegCountThreads) segcount_kernel(const uint32
   }
 }
 
+constexpr int kExpandChunk = 1024;  // segments per expansion chunk (rows cut into chunks)
+
+// Per-row segment starts and chunk starts (chunks of kExpandChunk segments) of TH <= 2048 rows:
+// a 256-thread block scan, 8 rows per thread (row counts read from L2).
+__device__ __forceinline__ void row_scan_block(const uint32_t* row_count, int TH, uint32_t* s_rs, uint32_t* s_cs,
+                                               uint32_t* s_w /* 16, shared */) {
+  constexpr int kPer = (kMaxTileRows + 255) / 256;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint32_t rc[kPer], rs = 0, cs = 0;
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {
+    const int ty = tid * kPer + q;
+    rc[q] = ty < TH ? __ldcg(row_count + ty) : 0u;
+    rs += rc[q];
+    cs += (rc[q] + kExpandChunk - 1) / kExpandChunk;
+  }
+  uint32_t xr = rs, xc = cs;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t yr = __shfl_up_sync(0xffffffffu, xr, o), yc = __shfl_up_sync(0xffffffffu, xc, o);
+    if (lane >= o) {
+      xr += yr;
+      xc += yc;
+    }
+  }
+  if (lane == 31) {
+    s_w[warp] = xr;
+    s_w[8 + warp] = xc;
+  }
+  __syncthreads();
+  uint32_t r = xr - rs, ch = xc - cs;
+#pragma unroll
+  for (int w = 0; w < 8; ++w)
+    if (w < warp) {
+      r += s_w[w];
+      ch += s_w[8 + w];
+    }
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {
+    const int ty = tid * kPer + q;
+    if (ty <= TH) {
+      s_rs[ty] = r;
+      s_cs[ty] = ch;
+    }
+    r += rc[q];
+    ch += (rc[q] + kExpandChunk - 1) / kExpandChunk;
+  }
+  if (tid == 255) {  // the totals (TH = 2048 has no thread for index TH above)
+    s_rs[TH] = r;
+    s_cs[TH] = ch;
+  }
+  __syncthreads();
+}
+
 // One warp per 32 consecutive ranks (persistent warps take rank chunks from a counter).
 __global__ void __launch_bounds__(256) segemit_kernel(const uint32_t* __restrict__ items_sorted,
                                                       const Rec* __restrict__ recs,
@@ -122,7 +177,9 @@ __global__ void __launch_bounds__(256) segemit_kernel(const uint32_t* __restrict
                                                       uint32_t* __restrict__ seg_span,
                                                       int TH, uint32_t* __restrict__ row_count,
                                                       uint32_t* __restrict__ key_hist /* 2 x 256 */,
-                                                      uint32_t* __restrict__ lookback0, uint32_t sort_chunk) {
+                                                      uint32_t* __restrict__ lookback0, uint32_t sort_chunk,
+                                                      uint32_t* __restrict__ row_start,
+                                                      uint32_t* __restrict__ chunk_start) {
   __shared__ RowGeom s_g[8][32];
   __shared__ int4 s_cb[8][32];
   __shared__ int s_pre[8][33];
@@ -213,28 +270,20 @@ __global__ void __launch_bounds__(256) segemit_kernel(const uint32_t* __restrict
       if (TH > 256) atomicAdd(&key_hist[256 + (i >> 8)], v);
     }
   }
-}
-
-// One CTA: per-row segment starts and chunk starts (chunks of kExpandChunk segments).
-constexpr int kExpandChunk = 1024;
-__global__ void __launch_bounds__(256) row_scan_kernel(const uint32_t* __restrict__ row_count, int TH,
-                                                       uint32_t* __restrict__ row_start,
-                                                       uint32_t* __restrict__ chunk_start) {
-  if (threadIdx.x != 0) return;
-  uint32_t acc = 0, ch = 0;
-  for (int ty = 0; ty < TH; ++ty) {
-    row_start[ty] = acc;
-    chunk_start[ty] = ch;
-    acc += row_count[ty];
-    ch += (row_count[ty] + kExpandChunk - 1) / kExpandChunk;
+  // the last CTA to finish: row segment starts and chunk starts for the expansion passes
+  __shared__ uint32_t s_last, s_w[16];
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = atomicAdd(&ctr->emit_done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    row_scan_block(row_count, TH, row_start, chunk_start, s_w);
   }
-  row_start[TH] = acc;
-  chunk_start[TH] = ch;
 }
 
 // (chunk, 32 columns) of a row: which row / which of its chunks (binary search over chunk starts)
-__device__ __forceinline__ bool chunk_of(const uint32_t* __restrict__ chunk_start, int TH, uint32_t gc, int& ty,
-                                         uint32_t& lc) {
+__device__ __forceinline__ bool chunk_of(const uint32_t* chunk_start, int TH, uint32_t gc, int& ty, uint32_t& lc) {
   if (gc >= chunk_start[TH]) return false;
   int lo = 0, hi = TH - 1;
   while (lo < hi) {
@@ -516,46 +565,52 @@ __global__ void __launch_bounds__(256) tile_chunks_kernel(const uint32_t* __rest
 }
 
 // One CTA: exclusive scan of the tile counts (row-major tile ids) -> ranges (empty tiles
-// [0, 0)), P and the overflow verdict.
+// [0, 0)), P and the overflow verdict. Thread t owns ceil(T / 1024) consecutive tiles.
 __global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restrict__ tile_count, int T,
                                                          Counters* __restrict__ ctr, uint32_t pair_cap,
                                                          uint2* __restrict__ ranges, Sticky* __restrict__ sticky) {
-  __shared__ unsigned long long s_wsum[32];
-  __shared__ unsigned long long s_carry;
+  __shared__ unsigned long long s_w[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) s_carry = 0;
+  const int per = (T + 1023) / 1024;
+  const int t0 = min(tid * per, T), t1 = min(t0 + per, T);
+  unsigned long long sum = 0;
+  for (int t = t0; t < t1; ++t) sum += tile_count[t];
+  unsigned long long x = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_w[warp] = x;
   __syncthreads();
-  for (int t0 = 0; t0 < T; t0 += 1024) {
-    const int t = t0 + tid;
-    const unsigned long long v = t < T ? (unsigned long long)tile_count[t] : 0ull;
-    unsigned long long x = v;
+  if (warp == 0) {
+    const unsigned long long v = s_w[lane];
+    unsigned long long z = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, z, o);
+      if (lane >= o) z += y;
     }
-    if (lane == 31) s_wsum[warp] = x;
-    __syncthreads();
-    unsigned long long off = s_carry;
-    for (int w = 0; w < warp; ++w) off += s_wsum[w];
-    const unsigned long long st = off + x - v;
-    if (t < T)
-      ranges[t] = v ? make_uint2((uint32_t)min(st, (unsigned long long)pair_cap),
-                                 (uint32_t)min(st + v, (unsigned long long)pair_cap))
-                    : make_uint2(0u, 0u);
-    __syncthreads();
-    if (tid == 1023) s_carry = off + x;
-    __syncthreads();
+    s_w[lane] = z - v;  // exclusive warp offsets
+    if (lane == 31) {   // P and the overflow verdict
+      const unsigned long long P = z;
+      ctr->n_pairs = (uint32_t)(P < pair_cap ? P : pair_cap);
+      if (P > ctr->pairs_needed) ctr->pairs_needed = P;
+      if (P > pair_cap) {
+        ctr->overflow = 1u;
+        atomicOr(&sticky->overflowed, 1u);
+        atomicMax(&sticky->pairs_needed_max, P);
+      }
+    }
   }
-  if (tid == 0) {
-    const unsigned long long P = s_carry;
-    ctr->n_pairs = (uint32_t)(P < pair_cap ? P : pair_cap);
-    if (P > ctr->pairs_needed) ctr->pairs_needed = P;
-    if (P > pair_cap) {
-      ctr->overflow = 1u;
-      atomicOr(&sticky->overflowed, 1u);
-      atomicMax(&sticky->pairs_needed_max, P);
-    }
+  __syncthreads();
+  unsigned long long st = s_w[warp] + x - sum;
+  for (int t = t0; t < t1; ++t) {
+    const unsigned long long v = tile_count[t];
+    ranges[t] = v ? make_uint2((uint32_t)min(st, (unsigned long long)pair_cap),
+                               (uint32_t)min(st + v, (unsigned long long)pair_cap))
+                  : make_uint2(0u, 0u);
+    st += v;
   }
 }
 

@@ -7,6 +7,6 @@ for cfg in "$@"; do
  IFS=, read d t w <<< "$cfg"
  for k in render score batch; do
   RS_EXPAND_DENSE=$d RS_EXPAND_MAJOR=$t RS_EXPAND_WAVES=$w ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/l_$k.csv python tools/profile_frame.py $k 2 > /dev/null 2>&1
-  echo "d=$d t=$t w=$w $k $(python tools/launches.py gpurun_out/l_$k.csv 16 | grep -E 'chunk_count|expand|total' | awk '{print $1}' | tr '\n' ' ')"
+  echo "d=$d t=$t w=$w $k $(python tools/launches.py gpurun_out/l_$k.csv 15 | grep -E 'chunk_count|expand|total' | awk '{print $1}' | tr '\n' ' ')"
  done
 done
