@@ -30,7 +30,7 @@ struct Layout {
   // per-frame zeroed region [0, frame_bytes)
   size_t ctr, hist, emit_lb, proj_lb, ranges, rowcnt, frame_bytes;
   size_t sticky, cam, recs, nrows, sgrad, titem, keysA, keysB, valsA, valsB, offsets, segkeyA, segkeyB, segvalA,
-      segvalB, segitem, segspan, rowstart, chunkstart, chunkcnt, chunkinfo, densel, tilecnt, pitem, lbA, lbB, total;
+      segvalB, segitem, segspan, geom, rowstart, chunkstart, chunkcnt, chunkinfo, densel, tilecnt, pitem, lbA, lbB, total;
 };
 
 int tiles_x(int w) { return (w + kTile - 1) / kTile; }
@@ -72,6 +72,7 @@ Layout make_layout(int64_t n_cap, int64_t pair_cap, int W, int H) {
   L.segvalB = take(seg_cap * 4);
   L.segitem = take(seg_cap * 4);
   L.segspan = take(seg_cap * 4);
+  L.geom = take((size_t)n_cap * 32);
   L.rowstart = take((TH + 1) * 4);
   L.chunkstart = take((TH + 1) * 4);
   L.chunkcnt = take((seg_cap / kExpandChunk + TH + 1) * TW * 4);
@@ -346,7 +347,8 @@ int32_t rs_bin(rs_workspace* ws, void* stream) {
         ws->at<unsigned long long>(ws->L.emit_lb), ws->at<Sticky>(ws->L.sticky));
     segemit_kernel<<<std::max(1, std::min((int)((n + 255) / 256), ws->sms * 4)), 256, 0, st>>>(
         items_sorted, ws->at<Rec>(ws->L.recs), ws->at<uint32_t>(ws->L.offsets), ctr, ws->TW,
-        ws->at<uint16_t>(ws->L.segkeyA), ws->at<uint32_t>(ws->L.segitem), ws->at<uint32_t>(ws->L.segspan), ws->TH,
+        ws->at<uint16_t>(ws->L.segkeyA), ws->at<uint32_t>(ws->L.segitem), ws->at<uint32_t>(ws->L.segspan),
+        ws->at<float4>(ws->L.geom), ws->TH,
         ws->at<uint32_t>(ws->L.rowcnt), ws->at<uint32_t>(ws->L.hist) + 4 * 256, ws->at<uint32_t>(ws->L.lbA),
         kSortThreads * kTileItems, ws->at<uint32_t>(ws->L.rowstart), ws->at<uint32_t>(ws->L.chunkstart));
     const uint16_t* rows_res;
@@ -410,13 +412,14 @@ int32_t rs_blend_ex(rs_workspace* ws, const rs_options* opts, const rs_outputs* 
   const uint2* ranges = ws->at<uint2>(ws->L.ranges);
   const uint32_t* items = final_pair_items(ws);
   const Rec* recs = ws->at<Rec>(ws->L.recs);
+  const float4* geom = ws->at<float4>(ws->L.geom);  // ellipse row geometry (warp quarter masks)
   Counters* ctr = ws->ctr();
 #define RS_BLEND(C, I, K, F)                                                                              \
   if (one_px)                                                                                             \
     blend_kernel<C, I, K, F><<<T, kBlendThreads, 0, st>>>(ranges, items, recs, ctr, ws->W, ws->H, ws->TW, \
                                                           *opts, out, scores);                            \
   else                                                                                                    \
-    blend2_kernel<C, I, K, F><<<T, kBlend2Threads, 0, st>>>(ranges, items, recs, ctr, ws->W, ws->H,       \
+    blend2_kernel<C, I, K, F><<<T, kBlend2Threads, 0, st>>>(ranges, items, recs, geom, ctr, ws->W, ws->H, \
                                                             ws->TW, *opts, out, scores)
 #define RS_BLEND_F(C, I, K) \
   if (fast) { RS_BLEND(C, I, K, true); } else { RS_BLEND(C, I, K, false); }
@@ -425,14 +428,14 @@ int32_t rs_blend_ex(rs_workspace* ws, const rs_options* opts, const rs_outputs* 
   if (out.tau) {  // training forward (rasterize_cached): records tau and the last composite per pixel
     if (scores) {
       if (fast) blend2_kernel<true, true, false, true, true><<<T, kBlend2Threads, 0, st>>>(
-          ranges, items, recs, ctr, ws->W, ws->H, ws->TW, *opts, out, scores);
+          ranges, items, recs, geom, ctr, ws->W, ws->H, ws->TW, *opts, out, scores);
       else blend2_kernel<true, true, false, false, true><<<T, kBlend2Threads, 0, st>>>(
-          ranges, items, recs, ctr, ws->W, ws->H, ws->TW, *opts, out, scores);
+          ranges, items, recs, geom, ctr, ws->W, ws->H, ws->TW, *opts, out, scores);
     } else {
       if (fast) blend2_kernel<true, false, false, true, true><<<T, kBlend2Threads, 0, st>>>(
-          ranges, items, recs, ctr, ws->W, ws->H, ws->TW, *opts, out, scores);
+          ranges, items, recs, geom, ctr, ws->W, ws->H, ws->TW, *opts, out, scores);
       else blend2_kernel<true, false, false, false, true><<<T, kBlend2Threads, 0, st>>>(
-          ranges, items, recs, ctr, ws->W, ws->H, ws->TW, *opts, out, scores);
+          ranges, items, recs, geom, ctr, ws->W, ws->H, ws->TW, *opts, out, scores);
     }
   } else if (color && scores) {
     if (stats) { RS_BLEND_F(true, true, true); } else { RS_BLEND_F(true, true, false); }

@@ -26,6 +26,7 @@
 // with one atomicMax per (tile, Gaussian) -- max-merge is order independent
 // (render.py:71-76), so the result is deterministic.
 #pragma once
+#include "rows.cuh"
 #include "rs_common.cuh"
 #include "rs_math.cuh"
 
@@ -246,8 +247,8 @@ __device__ __forceinline__ float blend_px(const float4 ga, const float4 gb, cons
 template <bool COLOR, bool CONTRIB, bool STATS, bool FAST, bool TRAIN = false>
 __global__ void __launch_bounds__(kBlend2Threads) blend2_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ pair_items, const Rec* __restrict__ recs,
-    Counters* __restrict__ ctr, int W, int H, int TW, rs_options o, const rs_outputs out,
-    uint32_t* __restrict__ scores) {
+    const float4* __restrict__ geom, Counters* __restrict__ ctr, int W, int H, int TW, rs_options o,
+    const rs_outputs out, uint32_t* __restrict__ scores) {
   constexpr int kBatch = 256;  // entries staged per batch (two per thread)
   __shared__ Rec s_rec[kBatch];
   __shared__ uint32_t s_w[CONTRIB ? kBatch : 1];
@@ -285,19 +286,30 @@ __global__ void __launch_bounds__(kBlend2Threads) blend2_kernel(
       const int slot = tid + h * kBlend2Threads;
       const uint32_t idx = base + slot;
       if (idx < end) {
-        const Rec* R = recs + __ldg(pair_items + idx);
-        s_rec[slot].a = __ldg(&R->a);
+        const uint32_t it = __ldg(pair_items + idx);
+        const Rec* R = recs + it;
+        const float4 a = __ldg(&R->a);
+        s_rec[slot].a = a;
         s_rec[slot].b = __ldg(&R->b);
         const float4 c = __ldg(&R->c);
         if (COLOR || CONTRIB) s_rec[slot].c = c;
         gid[h] = (uint32_t)__float_as_int(c.w);
-        const int4 d = cullbox_of(__ldg(&R->d));
+        const int4 dr = __ldg(&R->d);
+        const int4 d = cullbox_of(dr);
         s_rec[slot].d = d;
-        // box x sub-rectangle overlap: 2 column halves x 2 row halves -> bit w = (w%2, w/2)
-        const unsigned col = (d.x < ox + 8 && d.y > ox ? 1u : 0u) | (d.x < ox + 16 && d.y > ox + 8 ? 2u : 0u);
-        unsigned m = 0;
-        if (d.z < oy + 8 && d.w > oy) m |= col;
-        if (d.z < oy + 16 && d.w > oy + 8) m |= col << 2;
+        unsigned m;
+        if (!STATS && cullbox_ell(dr)) {
+          // the 8x8 quarters the ellipse strips of the tile's two half-rows reach: a warp whose
+          // quarter no pixel of the entry can composite in never walks it (STATS keeps the box
+          // quarters: every in-box pixel is evaluated, the oracle's E count)
+          m = quarter_mask(load_row_geom(geom + 2 * (size_t)it, a.x, a.y), d, ox, oy);
+        } else {
+          // box x sub-rectangle overlap: 2 column halves x 2 row halves -> bit w = (w%2, w/2)
+          const unsigned col = (d.x < ox + 8 && d.y > ox ? 1u : 0u) | (d.x < ox + 16 && d.y > ox + 8 ? 2u : 0u);
+          m = 0;
+          if (d.z < oy + 8 && d.w > oy) m |= col;
+          if (d.z < oy + 16 && d.w > oy + 8) m |= col << 2;
+        }
         s_mask[slot] = (uint8_t)m;
       }
       if (CONTRIB) s_w[slot] = 0u;

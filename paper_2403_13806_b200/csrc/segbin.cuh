@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(256) segemit_kernel(const uint32_t* __restrict
                                                       const uint32_t* __restrict__ offsets,
                                                       Counters* __restrict__ ctr, int TW,
                                                       uint16_t* __restrict__ seg_key, uint32_t* __restrict__ seg_item,
-                                                      uint32_t* __restrict__ seg_span,
+                                                      uint32_t* __restrict__ seg_span, float4* __restrict__ geom,
                                                       int TH, uint32_t* __restrict__ row_count,
                                                       uint32_t* __restrict__ key_hist /* 2 x 256 */,
                                                       uint32_t* __restrict__ lookback0, uint32_t sort_chunk,
@@ -209,7 +209,10 @@ __global__ void __launch_bounds__(256) segemit_kernel(const uint32_t* __restrict
         const int4 cb = cullbox_of(d);
         nr = (cb.w - 1) / kTile - cb.z / kTile + 1;
         s_cb[warp][lane] = make_int4(cb.x, cb.y, cb.z, cb.w | (cullbox_ell(d) ? (int)0x80000000 : 0));
-        if (cullbox_ell(d)) s_g[warp][lane] = row_geom(__ldg(&R->a), __ldg(&R->b));
+        if (cullbox_ell(d)) {
+          s_g[warp][lane] = row_geom(__ldg(&R->a), __ldg(&R->b));
+          store_row_geom(geom + 2 * (size_t)it, s_g[warp][lane]);  // blend2_kernel's quarter masks
+        }
         atomicAdd(&s_rows[cb.z / kTile], 1);  // one segment in each of its rows
         atomicAdd(&s_rows[cb.z / kTile + nr], -1);
       }
