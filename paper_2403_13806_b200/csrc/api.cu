@@ -28,12 +28,14 @@ size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
 struct Layout {
   // per-frame zeroed region [0, frame_bytes)
-  size_t ctr, hist, emit_lb, proj_lb, ranges, rowcnt, frame_bytes;
-  size_t sticky, cam, recs, nrows, sgrad, titem, keysA, keysB, valsA, valsB, offsets, segkeyA, segkeyB, segvalA,
-      segvalB, segitem, segspan, geom, rowstart, chunkstart, chunkcnt, chunkinfo, densel, tilecnt, pitem, lbA, lbB, total;
+  size_t ctr, hist, proj_lb, ranges, frame_bytes;
+  size_t sticky, cam, recs, nrows, sgrad, titem, keysA, keysB, valsA, valsB, rowtab, rowcnt, segitem, segspan, geom,
+      rowstart, chunkstart, chunkcnt, chunkinfo, densel, tilecnt, pitem, lbA, lbB, total;
 };
 
 int tiles_x(int w) { return (w + kTile - 1) / kTile; }
+
+size_t rowtab_stride(int64_t n_cap) { return (size_t)n_cap / kRankChunk + 1; }
 
 int64_t seg_capacity(int64_t n_cap, int64_t pair_cap) {
   // row segments <= pairs + 2 per Gaussian (only a culling box's first and last tile rows can
@@ -49,11 +51,9 @@ Layout make_layout(int64_t n_cap, int64_t pair_cap, int W, int H) {
   auto take = [&](size_t bytes) { const size_t at = o; o = align_up(o + bytes); return at; };
   // per-frame zeroed region
   L.ctr = take(sizeof(Counters));
-  L.hist = take(8 * 256 * sizeof(uint32_t));  // depth passes 0-3, segment row passes 4-5
-  L.emit_lb = take(((size_t)n_cap / (kSegCountThreads * kSegCountItems) + 2) * sizeof(unsigned long long));
+  L.hist = take(4 * 256 * sizeof(uint32_t));  // depth passes 0-3
   L.proj_lb = take(((size_t)n_cap / kCompactKeys + 2) * sizeof(unsigned long long));
   L.ranges = take(TW * TH * sizeof(uint2));
-  L.rowcnt = take((TH + 1) * sizeof(uint32_t));
   L.frame_bytes = o;
   L.sticky = take(sizeof(Sticky));
   L.cam = take(sizeof(rs_camera));
@@ -65,11 +65,8 @@ Layout make_layout(int64_t n_cap, int64_t pair_cap, int W, int H) {
   L.keysB = take((size_t)n_cap * 4);
   L.valsA = take((size_t)n_cap * 4);
   L.valsB = take((size_t)n_cap * 4);
-  L.offsets = take((size_t)n_cap * 4);
-  L.segkeyA = take(seg_cap * 2);
-  L.segkeyB = take(seg_cap * 2);
-  L.segvalA = take(seg_cap * 4);
-  L.segvalB = take(seg_cap * 4);
+  L.rowtab = take(rowtab_stride(n_cap) * TH * 4);  // per tile row: Gaussians per rank chunk
+  L.rowcnt = take((TH + 1) * sizeof(uint32_t));
   L.segitem = take(seg_cap * 4);
   L.segspan = take(seg_cap * 4);
   L.geom = take((size_t)n_cap * 32);
@@ -80,7 +77,7 @@ Layout make_layout(int64_t n_cap, int64_t pair_cap, int W, int H) {
   L.densel = take((seg_cap / kExpandChunk + TH + 1) * 4);
   L.tilecnt = take(TW * TH * 4);
   L.pitem = take((size_t)pair_cap * 4);
-  const size_t chunks = (std::max<size_t>((size_t)n_cap, seg_cap) + kMinChunk - 1) / kMinChunk + 1;
+  const size_t chunks = ((size_t)n_cap + kMinChunk - 1) / kMinChunk + 1;  // depth sort look-back
   L.lbA = take(chunks * 256 * 4);
   L.lbB = take(chunks * 256 * 4);
   L.total = o;
@@ -115,7 +112,6 @@ struct rs_workspace {
   // current frame (set by rs_project)
   uint32_t n_items;
   int W, H, TW, TH;
-  int row_bits;  // bits of a tile-row index (segment sort key)
   bool binned, have_cam, has_color;
   cudaStream_t aux = nullptr;  // second stream (dense expansion next to the sparse one)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -136,7 +132,6 @@ cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 int32_t cuda_status() { return cudaGetLastError() == cudaSuccess ? RS_OK : RS_ECUDA; }
 
 constexpr int kDepthItems = 8;   // 2048-key chunks: more CTAs for the small depth sort
-constexpr int kTileItems = 16;   // 4096-pair chunks for the tile sort
 
 // LSD passes of one sort over `bits` key bits; the digit histograms
 // (hist_slot) and the first pass's zeroed look-back words were produced by
@@ -195,7 +190,7 @@ void set_smem_all() {
 }
 void configure_kernels() {  // per device; idempotent
   set_smem_all<uint32_t, kDepthItems>();
-  set_smem_all<uint16_t, kTileItems>();
+  cudaFuncSetAttribute(segplace_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * kMaxTileRows);
 }
 
 }  // namespace
@@ -264,8 +259,6 @@ int32_t rs_set_camera(rs_workspace* ws, const rs_camera* cam, void* stream) {
   ws->H = cam->height;
   ws->TW = TW;
   ws->TH = TH;
-  ws->row_bits = 1;
-  while ((1 << ws->row_bits) < TH) ++ws->row_bits;
   ws->have_cam = true;
   // stream-ordered upload; from pageable memory the driver stages it at once, so the
   // caller may reuse `cam` immediately (a captured frame graph then replays it)
@@ -283,7 +276,7 @@ static int32_t project_impl(rs_workspace* ws, const rs_scene* scene, const int32
   if (items < 0) return RS_EINVAL;
   if (items > ws->n_cap) return RS_ENOMEM_WORKSPACE;
   cudaStream_t st = S(stream);
-  // zero counters, histograms, ranges and emit look-back in one memset
+  // zero counters, histograms, ranges and the compaction look-back in one memset
   cudaMemsetAsync(ws->base, 0, ws->L.frame_bytes, st);
   if (cam) {
     const int32_t s = rs_set_camera(ws, cam, stream);
@@ -337,31 +330,27 @@ int32_t rs_bin(rs_workspace* ws, void* stream) {
                                     ws->at<uint32_t>(ws->L.keysB), ws->at<uint32_t>(ws->L.valsA),
                                     ws->at<uint32_t>(ws->L.valsA), ws->at<uint32_t>(ws->L.valsB), nvis, 0, n, 32,
                                     0, 0, false, st, &keys_res, &items_sorted);
-    // row segments: count + offsets, emission in depth order, stable sort by tile row,
-    // per-tile ranges, expansion into the per-tile lists (segbin.cuh)
+    // row segments: per rank chunk and row counts, their per-row prefix, each segment placed
+    // in row-major depth-stable order; per-tile ranges, expansion into the per-tile lists
+    // (segbin.cuh)
     Counters* ctr = ws->ctr();
     const uint32_t seg_cap = (uint32_t)seg_capacity(ws->n_cap, ws->pair_cap);
-    segcount_kernel<<<(n + kSegCountThreads * kSegCountItems - 1) / (kSegCountThreads * kSegCountItems),
-                      kSegCountThreads, 0, st>>>(
-        items_sorted, ws->at<uint32_t>(ws->L.nrows), ctr, seg_cap, ws->at<uint32_t>(ws->L.offsets),
-        ws->at<unsigned long long>(ws->L.emit_lb), ws->at<Sticky>(ws->L.sticky));
-    segemit_kernel<<<std::max(1, std::min((int)((n + 255) / 256), ws->sms * 4)), 256, 0, st>>>(
-        items_sorted, ws->at<Rec>(ws->L.recs), ws->at<uint32_t>(ws->L.offsets), ctr, ws->TW,
-        ws->at<uint16_t>(ws->L.segkeyA), ws->at<uint32_t>(ws->L.segitem), ws->at<uint32_t>(ws->L.segspan),
-        ws->at<float4>(ws->L.geom), ws->TH,
-        ws->at<uint32_t>(ws->L.rowcnt), ws->at<uint32_t>(ws->L.hist) + 4 * 256, ws->at<uint32_t>(ws->L.lbA),
-        kSortThreads * kTileItems, ws->at<uint32_t>(ws->L.rowstart), ws->at<uint32_t>(ws->L.chunkstart));
-    const uint16_t* rows_res;
-    const uint32_t* sorted_seg;
-    run_sort<uint16_t, kTileItems>(ws, ws->at<uint16_t>(ws->L.segkeyA), ws->at<uint16_t>(ws->L.segkeyA),
-                                   ws->at<uint16_t>(ws->L.segkeyB), nullptr, ws->at<uint32_t>(ws->L.segvalA),
-                                   ws->at<uint32_t>(ws->L.segvalB), &ctr->n_segs, 0, seg_cap, ws->row_bits, 4, 4,
-                                   false, st, &rows_res, &sorted_seg);
+    const uint32_t tab_stride = (uint32_t)rowtab_stride(ws->n_cap);
+    const unsigned rc = (n + kRankChunk - 1) / kRankChunk;
+    segrows_kernel<<<rc, 256, 0, st>>>(items_sorted, ws->at<Rec>(ws->L.recs), ctr, ws->TH, tab_stride,
+                                       ws->at<uint32_t>(ws->L.rowtab));
+    segscan_kernel<<<ws->TH, 256, 0, st>>>(ws->at<uint32_t>(ws->L.rowtab), tab_stride, ctr, ws->TH, seg_cap,
+                                           ws->at<uint32_t>(ws->L.rowcnt), ws->at<uint32_t>(ws->L.rowstart),
+                                           ws->at<uint32_t>(ws->L.chunkstart), ws->at<Sticky>(ws->L.sticky));
+    segplace_kernel<<<rc, 256, 64 * ws->TH, st>>>(items_sorted, ws->at<Rec>(ws->L.recs), ctr, ws->TH,
+                                                  ws->at<uint32_t>(ws->L.rowtab), tab_stride,
+                                                  ws->at<uint32_t>(ws->L.rowstart), ws->at<uint32_t>(ws->L.segitem),
+                                                  ws->at<uint32_t>(ws->L.segspan), ws->at<float4>(ws->L.geom));
     const unsigned gx = (unsigned)std::min<int64_t>(seg_cap / kExpandChunk + ws->TH + 1, (int64_t)ws->sms * 16);
     // expansion: the sparse chunks grid-strided (column groups x chunk slots), the dense ones on
     // persistent ticketed CTAs on the workspace's second stream, concurrently
     const dim3 eg((ws->TW + kExpandCols - 1) / kExpandCols, gx), dg(ws->sms * 6);
-    chunk_count_kernel<<<gx, 256, 0, st>>>(sorted_seg, ws->at<uint32_t>(ws->L.segspan),
+    chunk_count_kernel<<<gx, 256, 0, st>>>(ws->at<uint32_t>(ws->L.segspan),
                                            ws->at<uint32_t>(ws->L.rowstart), ws->at<uint32_t>(ws->L.chunkstart),
                                            ws->TH, ws->TW, ws->at<uint32_t>(ws->L.chunkcnt),
                                            ws->at<uint2>(ws->L.chunkinfo), expand_dense_span(), ctr,
@@ -374,13 +363,13 @@ int32_t rs_bin(rs_workspace* ws, void* stream) {
                                          ws->at<uint2>(ws->L.ranges), ws->at<Sticky>(ws->L.sticky));
     cudaEventRecord(ws->ev_fork, st);
     cudaStreamWaitEvent(ws->aux, ws->ev_fork, 0);
-    expand_dense_kernel<<<dg, 256, 0, ws->aux>>>(sorted_seg, ws->at<uint32_t>(ws->L.segitem),
+    expand_dense_kernel<<<dg, 256, 0, ws->aux>>>(ws->at<uint32_t>(ws->L.segitem),
                                             ws->at<uint32_t>(ws->L.segspan), ws->at<uint2>(ws->L.chunkinfo),
                                             ws->at<uint32_t>(ws->L.densel), ws->TW,
                                             ws->at<uint32_t>(ws->L.chunkcnt), ws->at<uint2>(ws->L.ranges), ctr,
                                             ws->at<uint32_t>(ws->L.pitem));
     cudaEventRecord(ws->ev_join, ws->aux);
-    expand_kernel<<<eg, 256, 0, st>>>(sorted_seg, ws->at<uint32_t>(ws->L.segitem),
+    expand_kernel<<<eg, 256, 0, st>>>(ws->at<uint32_t>(ws->L.segitem),
                                       ws->at<uint32_t>(ws->L.segspan), ws->at<uint2>(ws->L.chunkinfo),
                                       ws->at<uint32_t>(ws->L.chunkstart), ws->TH, ws->TW,
                                       ws->at<uint32_t>(ws->L.chunkcnt), ws->at<uint2>(ws->L.ranges), ctr,

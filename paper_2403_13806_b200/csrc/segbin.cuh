@@ -7,17 +7,15 @@
 // sorting all pairs by tile, the binning works on ROW SEGMENTS -- one per
 // (Gaussian, tile row), ~5x fewer than pairs:
 //
-//   segcount_kernel  per depth rank: its segment count (tile rows of its
-//                    culling box), block scan + decoupled look-back ->
-//                    exclusive segment offset per rank; S.
-//   segemit_kernel   one warp per 32 ranks, rows flattened over the lanes:
-//                    each segment's span (row_span), written in depth-rank
-//                    order as (row key, item, span); per-row segment counts
-//                    (= the sort's digit histogram). The last CTA scans the
-//                    counts: per-row segment starts, rows cut into chunks of
-//                    1024.
-//   onesweep (1 pass over the row key, sort.cuh) -> every row's segments in
-//                    depth order (stable).
+//   segrows_kernel   per chunk of 256 depth ranks: its Gaussians per tile row
+//                    (a difference array over the rows of their culling boxes).
+//   segscan_kernel   per row: exclusive prefix over the chunks and the row's
+//                    total; the last CTA: per-row segment starts, rows cut into
+//                    expansion chunks of 1024, S.
+//   segplace_kernel  per rank chunk: each segment's span (row_span) written
+//                    straight to its row-major, depth-stable place (row start +
+//                    earlier chunks + earlier warps + a per-row ballot), rows
+//                    flattened over the lanes. No sort of the segments.
 //   chunk_count_kernel  one CTA per chunk: per tile column the number of the
 //                    chunk's segments covering it (shared-memory counters);
 //                    the chunk's {first segment, row, count, dense} record and
@@ -38,83 +36,68 @@
 
 namespace rs {
 
-constexpr int kSegCountThreads = 1024;
 constexpr uint32_t kEmptySpan = 0x00000001u;  // t0 = 1 > t1 = 0: the row lists no tile
 constexpr int kExpandCols = 32;                // tile columns per expand CTA (8 warps x 4)
 constexpr int kMaxTileRows = 2048;             // image height <= 32767 px
 constexpr int kMaxTileCols = 2048;             // image width <= 32767 px
+constexpr int kRankChunk = 256;                // depth ranks per placement chunk (one CTA)
+constexpr int kExpandChunk = 1024;             // segments per expansion chunk (rows cut into chunks)
 
-constexpr int kSegCountItems = 4;  // ranks per thread (fewer, longer CTAs: a short look-back chain)
-
-__global__ void __launch_bounds__(kSegCountThreads) segcount_kernel(const uint32_t* __restrict__ items_sorted,
-                                                                    const uint32_t* __restrict__ nrows,
-                                                                    Counters* __restrict__ ctr, uint32_t seg_cap,
-                                                                    uint32_t* __restrict__ offsets,
-                                                                    unsigned long long* __restrict__ status,
-                                                                    Sticky* __restrict__ sticky) {
-  constexpr uint32_t kPer = kSegCountThreads * kSegCountItems;
-  __shared__ uint32_t s_block;
-  __shared__ uint32_t s_wsum[kSegCountThreads / 32];
-  __shared__ unsigned long long s_base;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) s_block = atomicAdd(&ctr->emit_ctr, 1u);
-  __syncthreads();
-  const uint32_t b = s_block;
-  const uint32_t nvis = ctr->n_visible;
-  if (b * kPer >= nvis && b > 0) return;
-  // this thread's kSegCountItems consecutive ranks
-  const uint32_t r0 = b * kPer + tid * kSegCountItems;
-  uint32_t nt[kSegCountItems], tsum = 0;
-#pragma unroll
-  for (int q = 0; q < kSegCountItems; ++q) {
-    nt[q] = r0 + q < nvis ? nrows[items_sorted[r0 + q]] : 0u;
-    tsum += nt[q];
-  }
-  uint32_t x = tsum;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) s_wsum[warp] = x;
-  __syncthreads();
-  uint32_t off = 0, total = 0;
-#pragma unroll
-  for (int w = 0; w < kSegCountThreads / 32; ++w) {
-    off += w < warp ? s_wsum[w] : 0u;
-    total += s_wsum[w];
-  }
-  if (warp == 0) {
-    volatile unsigned long long* st = status;
-    if (lane == 0) st[b] = (b == 0 ? kLbInc : kLbAgg) | total;
-    const unsigned long long excl = b == 0 ? 0ull : warp_lookback(st, b, lane);
-    if (lane == 0) {
-      if (b) st[b] = kLbInc | (excl + total);
-      s_base = excl;
-      if (nvis > 0 && b == (nvis - 1) / kPer) {
-        const unsigned long long end = excl + total;
-        ctr->n_segs = (uint32_t)(end < seg_cap ? end : seg_cap);
-        if (end > seg_cap) {  // too many segments: the frame is re-run with a larger workspace
-          ctr->overflow = 1u;
-          atomicOr(&sticky->overflowed, 1u);
-          // pair capacity that certainly holds this frame's segments (segments <= pairs + 2 n)
-          const unsigned long long need = end;
-          if (need > ctr->pairs_needed) ctr->pairs_needed = need;
-          atomicMax(&sticky->pairs_needed_max, need);
-        }
-      }
-    }
-  }
-  __syncthreads();
-  uint32_t o = (uint32_t)s_base + off + x - tsum;
-#pragma unroll
-  for (int q = 0; q < kSegCountItems; ++q) {
-    if (r0 + q < nvis) offsets[r0 + q] = o;
-    o += nt[q];
-  }
+// Tile rows [r0, r1] of a binned record's culling box.
+__device__ __forceinline__ void box_rows(const int4 cb, int& r0, int& r1) {
+  r0 = cb.z / kTile;
+  r1 = (cb.w - 1) / kTile;
 }
 
-constexpr int kExpandChunk = 1024;  // segments per expansion chunk (rows cut into chunks)
+// Pass 1: per rank chunk (256 consecutive depth ranks) the number of its Gaussians in each tile
+// row (a per-CTA difference array over the rows), stored row-major: row_tab[ty][chunk].
+__global__ void __launch_bounds__(256) segrows_kernel(const uint32_t* __restrict__ items_sorted,
+                                                      const Rec* __restrict__ recs,
+                                                      const Counters* __restrict__ ctr, int TH, uint32_t tab_stride,
+                                                      uint32_t* __restrict__ row_tab) {
+  __shared__ int s_d[kMaxTileRows + 1];
+  __shared__ uint32_t s_w[8];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t nvis = ctr->n_visible;
+  const uint32_t c = blockIdx.x;
+  if (c * kRankChunk >= nvis) return;
+  for (int i = tid; i <= TH; i += 256) s_d[i] = 0;
+  __syncthreads();
+  const uint32_t r = c * kRankChunk + tid;
+  if (r < nvis) {
+    int r0, r1;
+    box_rows(cullbox_of(__ldg(&recs[__ldg(items_sorted + r)].d)), r0, r1);
+    atomicAdd(&s_d[r0], 1);
+    atomicAdd(&s_d[r1 + 1], -1);
+  }
+  __syncthreads();
+  // prefix over the rows (8 per thread) -> the chunk's Gaussians per row
+  constexpr int kPer = (kMaxTileRows + 255) / 256;
+  int v[kPer], sum = 0;
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {
+    const int ty = tid * kPer + q;
+    v[q] = ty < TH ? s_d[ty] : 0;
+    sum += v[q];
+  }
+  int x = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_w[warp] = (uint32_t)x;
+  __syncthreads();
+  int run = x - sum;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) run += w < warp ? (int)s_w[w] : 0;
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {
+    const int ty = tid * kPer + q;
+    run += v[q];
+    if (ty < TH) row_tab[(size_t)ty * tab_stride + c] = (uint32_t)run;
+  }
+}
 
 // Per-row segment starts and chunk starts (chunks of kExpandChunk segments) of TH <= 2048 rows:
 // a 256-thread block scan, 8 rows per thread (row counts read from L2).
@@ -168,120 +151,170 @@ __device__ __forceinline__ void row_scan_block(const uint32_t* row_count, int TH
   __syncthreads();
 }
 
-// One warp per 32 consecutive ranks (persistent warps take rank chunks from a counter).
-__global__ void __launch_bounds__(256) segemit_kernel(const uint32_t* __restrict__ items_sorted,
-                                                      const Rec* __restrict__ recs,
-                                                      const uint32_t* __restrict__ offsets,
-                                                      Counters* __restrict__ ctr, int TW,
-                                                      uint16_t* __restrict__ seg_key, uint32_t* __restrict__ seg_item,
-                                                      uint32_t* __restrict__ seg_span, float4* __restrict__ geom,
-                                                      int TH, uint32_t* __restrict__ row_count,
-                                                      uint32_t* __restrict__ key_hist /* 2 x 256 */,
-                                                      uint32_t* __restrict__ lookback0, uint32_t sort_chunk,
+// Pass 2, one CTA per tile row: exclusive prefix of the row's chunk counts (in place) and the
+// row's total. The last CTA: per-row segment starts, expansion chunk starts, S and the
+// segment-capacity verdict.
+__global__ void __launch_bounds__(256) segscan_kernel(uint32_t* __restrict__ row_tab, uint32_t tab_stride,
+                                                      Counters* __restrict__ ctr, int TH, uint32_t seg_cap,
+                                                      uint32_t* __restrict__ row_total,
                                                       uint32_t* __restrict__ row_start,
-                                                      uint32_t* __restrict__ chunk_start) {
-  __shared__ RowGeom s_g[8][32];
-  __shared__ int4 s_cb[8][32];
-  __shared__ int s_pre[8][33];
-  __shared__ int s_rows[kMaxTileRows + 1];  // per-row difference array of this CTA's segments
+                                                      uint32_t* __restrict__ chunk_start,
+                                                      Sticky* __restrict__ sticky) {
+  __shared__ uint32_t s_w[16], s_last;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t nvis = ctr->n_visible;
-  const uint32_t S = ctr->n_segs;
-  const bool over = ctr->overflow != 0u;
-  const uint32_t lb_words = (S + sort_chunk - 1) / sort_chunk * 256u;
-  for (uint32_t k = blockIdx.x * blockDim.x + tid; k < lb_words; k += gridDim.x * blockDim.x) lookback0[k] = 0;
-  for (int i = tid; i <= TH; i += 256) s_rows[i] = 0;
-  __syncthreads();
-  if (!over) {
-    for (;;) {
-      uint32_t chunk = 0;
-      if (lane == 0) chunk = atomicAdd(&ctr->emit_work, 1u);
-      const uint32_t r0 = __shfl_sync(0xffffffffu, chunk, 0) * 32u;
-      if (r0 >= nvis) break;
-      const uint32_t r = r0 + lane;
-      int nr = 0;
-      uint32_t o = 0, it = 0;
-      if (r < nvis) {
-        o = offsets[r];
-        it = items_sorted[r];
-        const Rec* R = recs + it;
-        const int4 d = __ldg(&R->d);
-        const int4 cb = cullbox_of(d);
-        nr = (cb.w - 1) / kTile - cb.z / kTile + 1;
-        s_cb[warp][lane] = make_int4(cb.x, cb.y, cb.z, cb.w | (cullbox_ell(d) ? (int)0x80000000 : 0));
-        if (cullbox_ell(d)) {
-          s_g[warp][lane] = row_geom(__ldg(&R->a), __ldg(&R->b));
-          store_row_geom(geom + 2 * (size_t)it, s_g[warp][lane]);  // blend2_kernel's quarter masks
-        }
-        atomicAdd(&s_rows[cb.z / kTile], 1);  // one segment in each of its rows
-        atomicAdd(&s_rows[cb.z / kTile + nr], -1);
-      }
-      int x = nr;
+  const uint32_t nc = (ctr->n_visible + kRankChunk - 1) / kRankChunk;
+  uint32_t* tab = row_tab + (size_t)blockIdx.x * tab_stride;
+  uint32_t carry = 0;
+  constexpr int kPer = 4;
+  for (uint32_t base = 0; base < nc; base += 256 * kPer) {
+    uint32_t v[kPer], sum = 0;
 #pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, x, off);
-        if (lane >= off) x += y;
-      }
-      s_pre[warp][lane] = x - nr;
-      if (lane == 31) s_pre[warp][32] = x;
-      __syncwarp();
-      const int total = s_pre[warp][32];
-      for (int base = 0; base < total; base += 32) {
-        const int j = base + lane;
-        int lo = 0;
-        if (j < total) {
-          int hi = 31;
-          while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (s_pre[warp][mid] <= j) lo = mid; else hi = mid - 1;
-          }
-        }
-        const uint32_t so = __shfl_sync(0xffffffffu, o, lo);
-        const uint32_t sitem = __shfl_sync(0xffffffffu, it, lo);
-        if (j < total) {
-          const int k = j - s_pre[warp][lo];
-          const int4 c4 = s_cb[warp][lo];
-          const bool ell = c4.w < 0;
-          const int4 cb = make_int4(c4.x, c4.y, c4.z, c4.w & 0x7fffffff);
-          const int ty = cb.z / kTile + k;
-          int t0 = cb.x / kTile, t1 = (cb.y - 1) / kTile;
-          const bool ok = ell ? row_span(s_g[warp][lo], cb, ty, t0, t1) : true;
-          const uint32_t s = so + (uint32_t)k;
-          seg_key[s] = (uint16_t)ty;
-          seg_item[s] = sitem;
-          seg_span[s] = ok ? ((uint32_t)t0 | ((uint32_t)t1 << 16)) : kEmptySpan;
-
-        }
-      }
-      __syncwarp();
+    for (int q = 0; q < kPer; ++q) {
+      const uint32_t i = base + tid * kPer + q;
+      v[q] = i < nc ? tab[i] : 0u;
+      sum += v[q];
     }
-  }
-  __syncthreads();
-  if (tid == 0) {  // difference array -> per-row segment counts (TH <= 2048, one pass)
-    int run = 0;
-    for (int i = 0; i < TH; ++i) {
-      run += s_rows[i];
-      s_rows[i] = run;
+    uint32_t x = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
     }
-  }
-  __syncthreads();
-  for (int i = tid; i < TH; i += 256) {
-    const uint32_t v = (uint32_t)s_rows[i];
-    if (v) {
-      atomicAdd(&row_count[i], v);
-      atomicAdd(&key_hist[i & 255], v);
-      if (TH > 256) atomicAdd(&key_hist[256 + (i >> 8)], v);
+    __syncthreads();  // s_w reuse
+    if (lane == 31) s_w[warp] = x;
+    __syncthreads();
+    uint32_t run = carry + x - sum, tot = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      run += w < warp ? s_w[w] : 0u;
+      tot += s_w[w];
     }
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      const uint32_t i = base + tid * kPer + q;
+      if (i < nc) tab[i] = run;
+      run += v[q];
+    }
+    carry += tot;
   }
-  // the last CTA to finish: row segment starts and chunk starts for the expansion passes
-  __shared__ uint32_t s_last, s_w[16];
+  if (tid == 0) row_total[blockIdx.x] = carry;
   __threadfence();
   __syncthreads();
   if (tid == 0) s_last = atomicAdd(&ctr->emit_done, 1u) == gridDim.x - 1;
   __syncthreads();
-  if (s_last) {
-    __threadfence();
-    row_scan_block(row_count, TH, row_start, chunk_start, s_w);
+  if (!s_last) return;
+  __threadfence();
+  row_scan_block(row_total, TH, row_start, chunk_start, s_w);
+  const uint32_t S = __ldcg(row_start + TH);
+  if (S > seg_cap)  // nothing is placed: no chunks for the later passes either
+    for (int ty = tid; ty <= TH; ty += 256) {
+      row_start[ty] = 0;
+      chunk_start[ty] = 0;
+    }
+  if (tid == 0) {
+    ctr->n_segs = S < seg_cap ? S : seg_cap;
+    if (S > seg_cap) {  // too many segments: the frame is re-run with a larger workspace
+      ctr->overflow = 1u;
+      atomicOr(&sticky->overflowed, 1u);
+      // pair capacity that certainly holds this frame's segments (segments <= pairs + 2 n)
+      if (S > ctr->pairs_needed) ctr->pairs_needed = S;
+      atomicMax(&sticky->pairs_needed_max, (unsigned long long)S);
+    }
+  }
+}
+
+// Pass 3, one CTA per rank chunk: every segment written straight to its place in row-major,
+// depth-stable order -- row start + the earlier chunks' Gaussians in the row (pass 2) + the
+// earlier warps' (a per-row ballot per warp) + the earlier lanes'. The rows of the warp's
+// Gaussians are flattened over the lanes for the span computation (row_span, rows.cuh).
+// Dynamic shared memory: per warp and row the ballot and the offset (2 x 8 x TH words).
+__global__ void __launch_bounds__(256) segplace_kernel(const uint32_t* __restrict__ items_sorted,
+                                                       const Rec* __restrict__ recs, const Counters* __restrict__ ctr,
+                                                       int TH, const uint32_t* __restrict__ row_tab,
+                                                       uint32_t tab_stride, const uint32_t* __restrict__ row_start,
+                                                       uint32_t* __restrict__ seg_item,
+                                                       uint32_t* __restrict__ seg_span, float4* __restrict__ geom) {
+  extern __shared__ uint32_t s_dyn[];
+  uint32_t* s_bal = s_dyn;           // [8][TH]
+  uint32_t* s_off = s_dyn + 8 * TH;  // [8][TH]
+  __shared__ RowGeom s_g[8][32];
+  __shared__ int4 s_cb[8][32];
+  __shared__ int s_pre[8][33];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t nvis = ctr->n_visible;
+  const uint32_t c = blockIdx.x;
+  if (c * kRankChunk >= nvis || ctr->overflow) return;
+  const uint32_t r = c * kRankChunk + tid;
+  int r0 = 0x7fffffff, r1 = -1, nr = 0;
+  uint32_t it = 0;
+  if (r < nvis) {
+    it = __ldg(items_sorted + r);
+    const Rec* R = recs + it;
+    const int4 d = __ldg(&R->d);
+    const int4 cb = cullbox_of(d);
+    box_rows(cb, r0, r1);
+    nr = r1 - r0 + 1;
+    s_cb[warp][lane] = make_int4(cb.x, cb.y, cb.z, cb.w | (cullbox_ell(d) ? (int)0x80000000 : 0));
+    if (cullbox_ell(d)) {
+      s_g[warp][lane] = row_geom(__ldg(&R->a), __ldg(&R->b));
+      store_row_geom(geom + 2 * (size_t)it, s_g[warp][lane]);  // blend2_kernel's quarter masks
+    }
+  }
+  for (int i = lane; i < TH; i += 32) s_off[warp * TH + i] = 0u;
+  __syncwarp();
+  const int lo = __reduce_min_sync(0xffffffffu, r0), hi = __reduce_max_sync(0xffffffffu, r1);
+  for (int ty = lo; ty <= hi; ++ty) {  // per row: which of the warp's Gaussians lie in it
+    const uint32_t bal = __ballot_sync(0xffffffffu, r0 <= ty && ty <= r1);
+    if (lane == 0) {
+      s_bal[warp * TH + ty] = bal;
+      s_off[warp * TH + ty] = (uint32_t)__popc(bal);
+    }
+  }
+  __syncthreads();
+  for (int ty = tid; ty < TH; ty += 256) {  // per row: start of each warp's run
+    uint32_t run = __ldg(row_start + ty) + __ldg(row_tab + (size_t)ty * tab_stride + c);
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      const uint32_t v = s_off[w * TH + ty];
+      s_off[w * TH + ty] = run;
+      run += v;
+    }
+  }
+  __syncthreads();
+  // the warp's segments flattened over the lanes
+  int x = nr;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, off);
+    if (lane >= off) x += y;
+  }
+  s_pre[warp][lane] = x - nr;
+  if (lane == 31) s_pre[warp][32] = x;
+  __syncwarp();
+  const int total = s_pre[warp][32];
+  for (int base = 0; base < total; base += 32) {
+    const int j = base + lane;
+    int own = 0;
+    if (j < total) {
+      int hi2 = 31;
+      while (own < hi2) {
+        const int mid = (own + hi2 + 1) >> 1;
+        if (s_pre[warp][mid] <= j) own = mid; else hi2 = mid - 1;
+      }
+    }
+    const uint32_t sitem = __shfl_sync(0xffffffffu, it, own);
+    if (j < total) {
+      const int k = j - s_pre[warp][own];
+      const int4 c4 = s_cb[warp][own];
+      const bool ell = c4.w < 0;
+      const int4 cb = make_int4(c4.x, c4.y, c4.z, c4.w & 0x7fffffff);
+      const int ty = cb.z / kTile + k;
+      int t0 = cb.x / kTile, t1 = (cb.y - 1) / kTile;
+      const bool ok = ell ? row_span(s_g[warp][own], cb, ty, t0, t1) : true;
+      const uint32_t pos = s_off[warp * TH + ty] + (uint32_t)__popc(s_bal[warp * TH + ty] & ((1u << own) - 1u));
+      seg_item[pos] = sitem;
+      seg_span[pos] = ok ? ((uint32_t)t0 | ((uint32_t)t1 << 16)) : kEmptySpan;
+    }
   }
 }
 
@@ -320,8 +353,7 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
 // 4 columns and walks all the chunk's segments that reach the CTA's columns (staged 256 at a
 // time, block-compacted in order), one ballot per column per 32 segments -- every store
 // instruction writes one column's run contiguously.
-__device__ __forceinline__ void expand_dense_chunk(const uint32_t* __restrict__ sorted_seg,
-                                                   const uint32_t* __restrict__ seg_item,
+__device__ __forceinline__ void expand_dense_chunk(const uint32_t* __restrict__ seg_item,
                                                    const uint32_t* __restrict__ seg_span, uint32_t s0, uint32_t cnt,
                                                    int ty, uint32_t gc, int g0, int TW,
                                                    const uint32_t* __restrict__ chunk_count,
@@ -339,9 +371,8 @@ __device__ __forceinline__ void expand_dense_chunk(const uint32_t* __restrict__ 
     const uint32_t nb = min(256u, cnt - base);
     uint32_t sp = kEmptySpan, sit = 0;
     if (tid < nb) {
-      const uint32_t sid = sorted_seg[s0 + base + tid];
-      sp = seg_span[sid];
-      sit = seg_item[sid];
+      sp = seg_span[s0 + base + tid];
+      sit = seg_item[s0 + base + tid];
     }
     const int a0 = (int)(sp & 0xffffu), a1 = (int)(sp >> 16);
     const bool keep = a0 <= a1 && a0 <= g1 && a1 >= g0;
@@ -383,8 +414,7 @@ __device__ __forceinline__ void expand_dense_chunk(const uint32_t* __restrict__ 
 
 constexpr int kExpandSub = kExpandChunk / 256;  // 32-segment sub-steps per warp per chunk
 
-__global__ void __launch_bounds__(256) expand_kernel(const uint32_t* __restrict__ sorted_seg,
-                                                     const uint32_t* __restrict__ seg_item,
+__global__ void __launch_bounds__(256) expand_kernel(const uint32_t* __restrict__ seg_item,
                                                      const uint32_t* __restrict__ seg_span,
                                                      const uint2* __restrict__ chunk_info,
                                                      const uint32_t* __restrict__ chunk_start, int TH, int TW,
@@ -412,7 +442,7 @@ __global__ void __launch_bounds__(256) expand_kernel(const uint32_t* __restrict_
 #pragma unroll
     for (int k = 0; k < kExpandSub; ++k) {
       const uint32_t e = (uint32_t)(warp * 32 * kExpandSub + k * 32 + lane);
-      sid[k] = e < cnt ? sorted_seg[info.x + e] : 0xffffffffu;
+      sid[k] = e < cnt ? info.x + e : 0xffffffffu;
     }
     uint32_t sp[kExpandSub];
 #pragma unroll
@@ -467,8 +497,7 @@ __global__ void __launch_bounds__(256) expand_kernel(const uint32_t* __restrict_
 }
 
 // The dense chunks (listed by chunk_count_kernel, any order: chunks are independent).
-__global__ void __launch_bounds__(256) expand_dense_kernel(const uint32_t* __restrict__ sorted_seg,
-                                                           const uint32_t* __restrict__ seg_item,
+__global__ void __launch_bounds__(256) expand_dense_kernel(const uint32_t* __restrict__ seg_item,
                                                            const uint32_t* __restrict__ seg_span,
                                                            const uint2* __restrict__ chunk_info,
                                                            const uint32_t* __restrict__ dense_list, int TW,
@@ -493,7 +522,7 @@ __global__ void __launch_bounds__(256) expand_dense_kernel(const uint32_t* __res
     if (threadIdx.x == 0) s_tk[flip ^ 1] = atomicAdd(&ctr->dense_work, 1u);
     const uint32_t gc = dense_list[t / groups];
     const uint2 info = chunk_info[gc];
-    expand_dense_chunk(sorted_seg, seg_item, seg_span, info.x, (info.y >> 16) & 0x7fffu, (int)(info.y & 0xffffu), gc,
+    expand_dense_chunk(seg_item, seg_span, info.x, (info.y >> 16) & 0x7fffu, (int)(info.y & 0xffffu), gc,
                        (int)(t % groups) * kExpandCols, TW, chunk_count, ranges, pair_items, s_item, s_span, s_wk);
     flip ^= 1;
   }
@@ -501,8 +530,7 @@ __global__ void __launch_bounds__(256) expand_dense_kernel(const uint32_t* __res
 
 // Pass 1 (order-free): per (chunk, tile column) the number of the chunk's segments covering
 // the column -- shared-memory counters over all the row's columns, one CTA per chunk.
-__global__ void __launch_bounds__(256) chunk_count_kernel(const uint32_t* __restrict__ sorted_seg,
-                                                          const uint32_t* __restrict__ seg_span,
+__global__ void __launch_bounds__(256) chunk_count_kernel(const uint32_t* __restrict__ seg_span,
                                                           const uint32_t* __restrict__ row_start,
                                                           const uint32_t* __restrict__ chunk_start, int TH, int TW,
                                                           uint32_t* __restrict__ chunk_count,
@@ -523,7 +551,7 @@ __global__ void __launch_bounds__(256) chunk_count_kernel(const uint32_t* __rest
     const uint32_t s0 = row_start[ty] + lc * kExpandChunk, s1 = min(row_start[ty + 1], s0 + kExpandChunk);
     int tiles = 0;
     for (uint32_t sidx = s0 + tid; sidx < s1; sidx += 256) {
-      const uint32_t sp = seg_span[sorted_seg[sidx]];
+      const uint32_t sp = seg_span[sidx];
       const int t0 = (int)(sp & 0xffffu), t1 = (int)(sp >> 16);
       for (int c = t0; c <= t1; ++c) atomicAdd(&s_cnt[c], 1u);
       tiles += max(t1 - t0 + 1, 0);
