@@ -263,11 +263,17 @@ __global__ void __launch_bounds__(256) segplace_kernel(const uint32_t* __restric
   for (int i = lane; i < TH; i += 32) s_off[warp * TH + i] = 0u;
   __syncwarp();
   const int lo = __reduce_min_sync(0xffffffffu, r0), hi = __reduce_max_sync(0xffffffffu, r1);
-  for (int ty = lo; ty <= hi; ++ty) {  // per row: which of the warp's Gaussians lie in it
-    const uint32_t bal = __ballot_sync(0xffffffffu, r0 <= ty && ty <= r1);
-    if (lane == 0) {
-      s_bal[warp * TH + ty] = bal;
-      s_off[warp * TH + ty] = (uint32_t)__popc(bal);
+  const uint32_t span = (uint32_t)(r1 - r0);
+  for (int t0 = lo; t0 <= hi; t0 += 32) {  // per row: which of the warp's Gaussians lie in it
+    uint32_t mine = 0;                      // row t0 + lane's ballot
+    const int m = min(32, hi - t0 + 1);
+    for (int q = 0; q < m; ++q) {
+      const uint32_t bal = __ballot_sync(0xffffffffu, (uint32_t)(t0 + q - r0) <= span);
+      mine = lane == q ? bal : mine;
+    }
+    if (lane < m) {
+      s_bal[warp * TH + t0 + lane] = mine;
+      s_off[warp * TH + t0 + lane] = (uint32_t)__popc(mine);
     }
   }
   __syncthreads();
@@ -292,16 +298,14 @@ __global__ void __launch_bounds__(256) segplace_kernel(const uint32_t* __restric
   if (lane == 31) s_pre[warp][32] = x;
   __syncwarp();
   const int total = s_pre[warp][32];
+  const int pre = x - nr;
+  int carry = 0;  // owners started before the window (the valid lanes are 0..m-1, nr >= 1)
   for (int base = 0; base < total; base += 32) {
     const int j = base + lane;
-    int own = 0;
-    if (j < total) {
-      int hi2 = 31;
-      while (own < hi2) {
-        const int mid = (own + hi2 + 1) >> 1;
-        if (s_pre[warp][mid] <= j) own = mid; else hi2 = mid - 1;
-      }
-    }
+    const int rel = pre - base;
+    const uint32_t starts = __reduce_or_sync(0xffffffffu, nr > 0 && rel >= 0 && rel < 32 ? 1u << rel : 0u);
+    const int own = j < total ? carry + __popc(starts & ((2u << lane) - 1u)) - 1 : 0;
+    carry += __popc(starts);
     const uint32_t sitem = __shfl_sync(0xffffffffu, it, own);
     if (j < total) {
       const int k = j - s_pre[warp][own];
