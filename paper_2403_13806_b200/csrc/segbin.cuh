@@ -427,6 +427,7 @@ __global__ void __launch_bounds__(256) expand_kernel(const uint32_t* __restrict_
                                                      const Counters* __restrict__ ctr,
                                                      uint32_t* __restrict__ pair_items, int major_thresh) {
   __shared__ uint32_t s_cnt[2][8][32];
+  __shared__ uint32_t s_cm[8][kExpandSub * 32], s_ci[8][kExpandSub * 32];  // per-warp compaction
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (ctr->overflow) return;
   const uint32_t lt = (1u << lane) - 1u;
@@ -458,10 +459,30 @@ __global__ void __launch_bounds__(256) expand_kernel(const uint32_t* __restrict_
     }
 #pragma unroll
     for (int k = 0; k < kExpandSub; ++k) item[k] = m[k] ? seg_item[sid[k]] : 0u;
+    // the warp's segments that reach the CTA's columns, compacted in order (fewer transposes)
+    uint32_t nrel = 0;
+#pragma unroll
+    for (int k = 0; k < kExpandSub; ++k) {
+      const uint32_t bal = __ballot_sync(0xffffffffu, m[k] != 0u);
+      if (m[k]) {
+        const uint32_t at = nrel + __popc(bal & lt);
+        s_cm[warp][at] = m[k];
+        s_ci[warp][at] = item[k];
+      }
+      nrel += __popc(bal);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < kExpandSub; ++k) {
+      const uint32_t e = k * 32 + lane;
+      m[k] = e < nrel ? s_cm[warp][e] : 0u;
+      item[k] = e < nrel ? s_ci[warp][e] : 0u;
+    }
+    __syncwarp();
     uint32_t mine = 0;
 #pragma unroll
     for (int k = 0; k < kExpandSub; ++k) {
-      cm[k] = __any_sync(0xffffffffu, m[k] != 0u) ? transpose32(m[k], lane) : 0u;
+      cm[k] = k * 32 < (int)nrel ? transpose32(m[k], lane) : 0u;
       mine += __popc(cm[k]);
     }
     s_cnt[flip][warp][lane] = mine;
