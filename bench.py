@@ -547,7 +547,24 @@ def run_trajectory(args, rank, world, local, dev, opts, r, opt_s, stream, flush,
                 idx = list_for(arm, cam) if filt else None
                 plan.append((camera_struct(cam), idx))
 
+        # house: one CUDA graph per index list (64 cluster lists per filtered arm, one unfiltered),
+        # captured after the capacity pre-pass; a frame = camera upload + one graph launch (the
+        # small filtered frames are otherwise bound by the host launching ~15 kernels)
+        graphs = {}
+        if house:
+            from paper_2403_13806_b200.device import FrameGraph
+            torch.cuda.synchronize(dev)
+            for _, idx in plan:
+                key = None if idx is None else idx.data_ptr()
+                if key not in graphs:
+                    graphs[key] = FrameGraph(r, ds, traj[0], opts, out, None, idx,
+                                             int(idx.numel()) if idx is not None else 0)
+
         def launch(cs, idx):
+            if graphs:
+                N.check(lib.rs_set_camera(r.handle, C.byref(cs), sptr))
+                graphs[None if idx is None else idx.data_ptr()].graph.replay()
+                return
             N.check(lib.rs_render_ex(r.handle, C.byref(ds.struct), idx.data_ptr() if idx is not None else None,
                                      int(idx.numel()) if idx is not None else 0, C.byref(cs), C.byref(opt_s),
                                      C.byref(outs), None, 0, sptr))
