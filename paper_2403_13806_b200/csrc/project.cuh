@@ -59,7 +59,12 @@ __global__ void __launch_bounds__(128) project_kernel(const float* __restrict__ 
   if (item < n_items) {
     const int64_t i = active_idx ? (int64_t)__ldg(active_idx + item) : (int64_t)item;
     const float* P = planes + i;
+    // all eleven plane loads issued together (one memory round trip per thread)
     const float px = __ldg(P), py = __ldg(P + stride), pz = __ldg(P + 2 * stride);
+    const float lg = __ldg(P + 3 * stride);
+    const float ls0 = __ldg(P + 4 * stride), ls1 = __ldg(P + 5 * stride), ls2 = __ldg(P + 6 * stride);
+    float qw = __ldg(P + 7 * stride), qx = __ldg(P + 8 * stride), qy = __ldg(P + 9 * stride),
+          qz = __ldg(P + 10 * stride);
     // t = R p + T (render.py:100)
     float t[3];
 #pragma unroll
@@ -73,8 +78,6 @@ __global__ void __launch_bounds__(128) project_kernel(const float* __restrict__ 
     const float my = __fadd_rn(__fdiv_rn(__fmul_rn(cam.fy, t[1]), tz), cam.cy);
     const float depth = __fadd_rn(t[2], 0.0f);
     // quaternion -> rotation (core.py:111-139)
-    float qw = __ldg(P + 7 * stride), qx = __ldg(P + 8 * stride), qy = __ldg(P + 9 * stride),
-          qz = __ldg(P + 10 * stride);
     const float qn = __fsqrt_rn(
         __fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(qw, qw), __fmul_rn(qx, qx)), __fmul_rn(qy, qy)), __fmul_rn(qz, qz)));
     qw = __fdiv_rn(qw, qn); qx = __fdiv_rn(qx, qn); qy = __fdiv_rn(qy, qn); qz = __fdiv_rn(qz, qn);
@@ -91,7 +94,7 @@ __global__ void __launch_bounds__(128) project_kernel(const float* __restrict__ 
     // Sigma = L L^T, L = Rq diag(exp(log_s)) (render.py:108-111)
     float sc[3];
 #pragma unroll
-    for (int j = 0; j < 3; ++j) sc[j] = exp_contract(__ldg(P + (4 + j) * stride));
+    for (int j = 0; j < 3; ++j) sc[j] = exp_contract(j == 0 ? ls0 : j == 1 ? ls1 : ls2);
     float L[9];
 #pragma unroll
     for (int r = 0; r < 3; ++r)
@@ -188,7 +191,6 @@ __global__ void __launch_bounds__(128) project_kernel(const float* __restrict__ 
       }
       }  // COLOR
       // opacity = sigmoid(logit) (core.py:419-421)
-      const float lg = __ldg(P + 3 * stride);
       float op;
       if (lg >= 0.0f) {
         op = __fdiv_rn(1.0f, __fadd_rn(1.0f, exp_contract(-lg)));
