@@ -1,16 +1,15 @@
 // project.cuh -- per-Gaussian projection (replaces render.py:95-158).
 //
 // One thread per item. Reads the 11 geometry planes with coalesced 4-byte loads
-// and, for visible Gaussians of colour frames, the 192-byte SH row with twelve
-// 128-bit loads issued together; evaluates
-// the Tier-A fp32 contract of oracle/cpu_ref.cpp:project_one() in the same
-// operation order (compiled with -fmad=false; explicit __fmaf_rn only where
-// the contract fuses), and writes
+// (all issued before any arithmetic: one memory round trip) and, for visible
+// Gaussians of colour frames, the 192-byte SH row with twelve 128-bit loads
+// issued together; evaluates the Tier-A fp32 contract of
+// oracle/cpu_ref.cpp:project_one() in the same operation order (compiled with
+// -fmad=false; explicit __fmaf_rn only where the contract fuses), and writes
 //   * a 64-byte Rec for binned items (culled items write nothing else),
-//   * the binned items' tile-row counts (their row segments, segbin.cuh), and
-//   * the binned items' (32-bit depth key, item) compacted in item order
-//     (decoupled look-back over ticket-ordered blocks) for the depth sort,
-//     whose length n_visible the last block publishes.
+//   * the binned items' tile-row counts, and
+//   * every item's 32-bit depth key (kInvalidKey when not binned), which
+//     compact_hist_kernel (sort.cuh) compacts for the depth sort.
 #pragma once
 #include "rs_common.cuh"
 #include "rs_math.cuh"
