@@ -29,7 +29,7 @@ size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 struct Layout {
   // per-frame zeroed region [0, frame_bytes)
   size_t ctr, hist, proj_lb, ranges, frame_bytes;
-  size_t sticky, cam, recs, nrows, sgrad, titem, keysA, keysB, valsA, valsB, rowtab, rowcnt, segitem, segspan, geom,
+  size_t sticky, cam, recs, sgrad, titem, keysA, keysB, valsA, valsB, rowtab, rowcnt, segitem, segspan, geom,
       rowstart, chunkstart, chunkcnt, chunkinfo, densel, tilecnt, pitem, lbA, lbB, total;
 };
 
@@ -58,7 +58,6 @@ Layout make_layout(int64_t n_cap, int64_t pair_cap, int W, int H) {
   L.sticky = take(sizeof(Sticky));
   L.cam = take(sizeof(rs_camera));
   L.recs = take((size_t)n_cap * sizeof(Rec));
-  L.nrows = take((size_t)n_cap * 4);
   L.sgrad = take((size_t)n_cap * 4 * kSGrad);  // rs_backward: screen-space gradient sums per item
   L.titem = take((size_t)n_cap);
   L.keysA = take((size_t)n_cap * 4);
@@ -292,12 +291,12 @@ static int32_t project_impl(rs_workspace* ws, const rs_scene* scene, const int32
     if (full)
       project_kernel<true, true><<<grid, kProjThreads, 0, st>>>(
           scene->planes, scene->sh, scene->plane_stride, scene->sh_degree, active_idx, (uint32_t)items, ws->at<rs_camera>(ws->L.cam), *opts,
-          ws->at<Rec>(ws->L.recs), ws->at<uint32_t>(ws->L.keysB), ws->at<uint32_t>(ws->L.nrows), ws->ctr(), full,
+          ws->at<Rec>(ws->L.recs), ws->at<uint32_t>(ws->L.keysB), ws->ctr(), full,
           reinterpret_cast<int4*>(full_bbox));
     else
       (color ? project_kernel<false, true> : project_kernel<false, false>)<<<grid, kProjThreads, 0, st>>>(
           scene->planes, scene->sh, scene->plane_stride, scene->sh_degree, active_idx, (uint32_t)items, ws->at<rs_camera>(ws->L.cam), *opts,
-          ws->at<Rec>(ws->L.recs), ws->at<uint32_t>(ws->L.keysB), ws->at<uint32_t>(ws->L.nrows), ws->ctr(), nullptr, nullptr);
+          ws->at<Rec>(ws->L.recs), ws->at<uint32_t>(ws->L.keysB), ws->ctr(), nullptr, nullptr);
   }
   return cuda_status();
 }

@@ -6,8 +6,7 @@
 // issued together; evaluates the Tier-A fp32 contract of
 // oracle/cpu_ref.cpp:project_one() in the same operation order (compiled with
 // -fmad=false; explicit __fmaf_rn only where the contract fuses), and writes
-//   * a 64-byte Rec for binned items (culled items write nothing else),
-//   * the binned items' tile-row counts, and
+//   * a 64-byte Rec for binned items (culled items write nothing else), and
 //   * every item's 32-bit depth key (kInvalidKey when not binned), which
 //     compact_hist_kernel (sort.cuh) compacts for the depth sort.
 #pragma once
@@ -45,7 +44,7 @@ __global__ void __launch_bounds__(128) project_kernel(const float* __restrict__ 
                                                       const int32_t* __restrict__ active_idx, uint32_t n_items,
                                                       const rs_camera* __restrict__ camp, rs_options o,
                                                       Rec* __restrict__ recs,
-                                                      uint32_t* __restrict__ keys, uint32_t* __restrict__ nrows,
+                                                      uint32_t* __restrict__ keys,
                                                       Counters* __restrict__ ctr,
                                                       float* __restrict__ full, int4* __restrict__ full_bbox) {
   const uint32_t item = blockIdx.x * blockDim.x + threadIdx.x;
@@ -249,7 +248,6 @@ __global__ void __launch_bounds__(128) project_kernel(const float* __restrict__ 
                         cy0 | (cy1 << 16) | (ell ? (int)0x80000000 : 0));
       if (binned) {
         recs[item] = rec;
-        nrows[item] = (uint32_t)((cy1 - 1) / kTile - cy0 / kTile + 1);  // its row segments (segbin.cuh)
         depth_b = depth;
       }
       if (FULL) {
