@@ -26,6 +26,7 @@
 // with one atomicMax per (tile, Gaussian) -- max-merge is order independent
 // (render.py:71-76), so the result is deterministic.
 #pragma once
+#include "f32x2.cuh"
 #include "rows.cuh"
 #include "rs_common.cuh"
 #include "rs_math.cuh"
@@ -245,7 +246,10 @@ __device__ __forceinline__ float blend_px(const float4 ga, const float4 gb, cons
 // TRAIN: also record each pixel's final transmittance and last composited pair index
 // (rs_outputs tau / last) for rs_backward.
 template <bool COLOR, bool CONTRIB, bool STATS, bool FAST, bool TRAIN = false>
-__global__ void __launch_bounds__(kBlend2Threads) blend2_kernel(
+#ifndef RS_BLEND_MINB
+#define RS_BLEND_MINB 1
+#endif
+__global__ void __launch_bounds__(kBlend2Threads, RS_BLEND_MINB) blend2_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ pair_items, const Rec* __restrict__ recs,
     const float4* __restrict__ geom, Counters* __restrict__ ctr, int W, int H, int TW, rs_options o,
     const rs_outputs out, uint32_t* __restrict__ scores) {
@@ -263,15 +267,15 @@ __global__ void __launch_bounds__(kBlend2Threads) blend2_kernel(
   const int py0 = oy + (warp >> 1) * 8 + (lane >> 3), py1 = py0 + 4;
   const bool in0 = px < W && py0 < H, in1 = px < W && py1 < H;
   const float xs = __fadd_rn((float)px, 0.5f);
-  const float ys0 = __fadd_rn((float)py0, 0.5f), ys1 = __fadd_rn((float)py1, 0.5f);
   if (ctr->overflow) return;  // pair list incomplete: the host re-runs with a larger capacity
   const uint2 rg = ranges[tile];
   const uint32_t npairs = ctr->n_pairs;
   const uint32_t end = rg.y < npairs ? rg.y : npairs;  // memory safety on overflow
   const uint32_t lt = (1u << lane) - 1u;
 
-  float tau0 = 1.0f, r0 = 0.0f, g0 = 0.0f, b0 = 0.0f, d0 = 0.0f;
-  float tau1 = 1.0f, r1 = 0.0f, g1 = 0.0f, b1 = 0.0f, d1 = 0.0f;
+  // per-pixel state of the thread's two pixels as packed pairs {py0, py1}
+  f2 tau = f2_splat(1.0f), rgb[3] = {f2_splat(0.0f), f2_splat(0.0f), f2_splat(0.0f)}, dep = f2_splat(0.0f);
+  const f2 ys2 = f2_pack(__fadd_rn((float)py0, 0.5f), __fadd_rn((float)py1, 0.5f));
   int cnt0 = 0, cnt1 = 0;
   int last0 = -1, last1 = -1;  // pair index of each pixel's last composite (training outputs)
   unsigned long long evals = 0;
@@ -337,7 +341,9 @@ __global__ void __launch_bounds__(kBlend2Threads) blend2_kernel(
         int ent[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) ent[u] = s_list[warp][min(q + u, cntw - 1)];
-        float al[U][2];
+        // the two pixels (rows py0, py1) in packed fp32 pairs: every FADD2/FMUL2/FFMA2 below is
+        // the scalar contract's operation on both pixels at once (f32x2.cuh)
+        f2 al[U];
         bool ok[U][2], box[U][2];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -349,15 +355,34 @@ __global__ void __launch_bounds__(kBlend2Threads) blend2_kernel(
           box[u][1] = inx && py1 >= bb.z && py1 < bb.w;
           const float dx = __fsub_rn(xs, ga.x);
           const float ax = __fmul_rn(ga.z, dx);
-          const float dy0 = __fsub_rn(ys0, ga.y), dy1 = __fsub_rn(ys1, ga.y);
-          const float p20 = __fmaf_rn(ax, dx, __fmaf_rn(__fmul_rn(ga.w, dy0), dx, __fmul_rn(__fmul_rn(gb.x, dy0), dy0)));
-          const float p21 = __fmaf_rn(ax, dx, __fmaf_rn(__fmul_rn(ga.w, dy1), dx, __fmul_rn(__fmul_rn(gb.x, dy1), dy1)));
-          const float ex0 = FAST ? exp2_core(fminf(p20, 127.0f)) : exp2_contract(fminf(p20, 127.0f));
-          const float ex1 = FAST ? exp2_core(fminf(p21, 127.0f)) : exp2_contract(fminf(p21, 127.0f));
-          al[u][0] = fminf(__fmul_rn(gb.y, ex0), o.alpha_max);
-          al[u][1] = fminf(__fmul_rn(gb.y, ex1), o.alpha_max);
-          ok[u][0] = box[u][0] && p20 >= gb.z && al[u][0] >= o.alpha_cut;
-          ok[u][1] = box[u][1] && p21 >= gb.z && al[u][1] >= o.alpha_cut;
+          const f2 dy = f2_sub(ys2, f2_splat(ga.y));
+          // p2 = fma(ax, dx, fma(nb*dy, dx, (nc*dy)*dy))
+          const f2 t3 = f2_mul(f2_mul(f2_splat(gb.x), dy), dy);
+          const f2 p2 = f2_fma(f2_splat(ax), f2_splat(dx), f2_fma(f2_mul(f2_splat(ga.w), dy), f2_splat(dx), t3));
+          const float p20 = f2_lo(p2), p21 = f2_hi(p2);
+          // exp2_core(min(p2, 127)) (rs_math.cuh) on the pair
+          f2 ex;
+          if (FAST) {
+            const f2 x = f2_pack(fminf(p20, 127.0f), fminf(p21, 127.0f));
+            const f2 t = f2_add(x, f2_splat(kMagic));
+            const f2 r = f2_sub(x, f2_sub(t, f2_splat(kMagic)));
+            const f2 sc = f2_pack(__int_as_float((__float_as_int(f2_lo(t)) << 23) + 0x3f800000),
+                                  __int_as_float((__float_as_int(f2_hi(t)) << 23) + 0x3f800000));
+            f2 pp = f2_fma(f2_splat(fbits(0x3920e999u)), r, f2_splat(fbits(0x3aafa2b5u)));
+            pp = f2_fma(pp, r, f2_splat(fbits(0x3c1d96deu)));
+            pp = f2_fma(pp, r, f2_splat(fbits(0x3d63576au)));
+            pp = f2_fma(pp, r, f2_splat(fbits(0x3e75fdedu)));
+            pp = f2_fma(pp, r, f2_splat(fbits(0x3f317218u)));
+            pp = f2_fma(pp, r, f2_splat(1.0f));
+            ex = f2_mul(pp, sc);
+          } else {
+            ex = f2_pack(exp2_contract(fminf(p20, 127.0f)), exp2_contract(fminf(p21, 127.0f)));
+          }
+          const f2 av = f2_mul(f2_splat(gb.y), ex);
+          const float a0 = fminf(f2_lo(av), o.alpha_max), a1 = fminf(f2_hi(av), o.alpha_max);
+          al[u] = f2_pack(a0, a1);
+          ok[u][0] = box[u][0] && p20 >= gb.z && a0 >= o.alpha_cut;
+          ok[u][1] = box[u][1] && p21 >= gb.z && a1 >= o.alpha_cut;
         }
         float wmax[U];
 #pragma unroll
@@ -365,19 +390,16 @@ __global__ void __launch_bounds__(kBlend2Threads) blend2_kernel(
           const Rec& E = s_rec[ent[u]];
           if (STATS) evals += (unsigned)(box[u][0] && !done0) + (unsigned)(box[u][1] && !done1);
           const bool c0 = ok[u][0] && !done0, c1 = ok[u][1] && !done1;
-          const float w0 = c0 ? __fmul_rn(al[u][0], tau0) : 0.0f;
-          const float w1 = c1 ? __fmul_rn(al[u][1], tau1) : 0.0f;
+          const f2 wt = f2_mul(al[u], tau);
+          const float w0 = c0 ? f2_lo(wt) : 0.0f, w1 = c1 ? f2_hi(wt) : 0.0f;
           if (COLOR) {
+            // fma(c, +0, acc) = acc for the pixel that does not composite (c, z finite, acc >= +0)
             const float4 gc = E.c;
-            const float z = E.b.w;
-            if (c0) {
-              r0 = __fmaf_rn(gc.x, w0, r0); g0 = __fmaf_rn(gc.y, w0, g0); b0 = __fmaf_rn(gc.z, w0, b0);
-              d0 = __fmaf_rn(z, w0, d0);
-            }
-            if (c1) {
-              r1 = __fmaf_rn(gc.x, w1, r1); g1 = __fmaf_rn(gc.y, w1, g1); b1 = __fmaf_rn(gc.z, w1, b1);
-              d1 = __fmaf_rn(z, w1, d1);
-            }
+            const f2 w = f2_pack(w0, w1);
+            rgb[0] = f2_fma(f2_splat(gc.x), w, rgb[0]);
+            rgb[1] = f2_fma(f2_splat(gc.y), w, rgb[1]);
+            rgb[2] = f2_fma(f2_splat(gc.z), w, rgb[2]);
+            dep = f2_fma(f2_splat(E.b.w), w, dep);
           }
           cnt0 += c0 ? 1 : 0;
           cnt1 += c1 ? 1 : 0;
@@ -386,8 +408,9 @@ __global__ void __launch_bounds__(kBlend2Threads) blend2_kernel(
             last0 = c0 ? k : last0;
             last1 = c1 ? k : last1;
           }
-          tau0 = c0 ? __fmul_rn(tau0, __fsub_rn(1.0f, al[u][0])) : tau0;
-          tau1 = c1 ? __fmul_rn(tau1, __fsub_rn(1.0f, al[u][1])) : tau1;
+          const f2 tn = f2_mul(tau, f2_sub(f2_splat(1.0f), al[u]));
+          const float tau0 = c0 ? f2_lo(tn) : f2_lo(tau), tau1 = c1 ? f2_hi(tn) : f2_hi(tau);
+          tau = f2_pack(tau0, tau1);
           done0 = done0 || tau0 < o.tau_stop;
           done1 = done1 || tau1 < o.tau_stop;
           wmax[u] = fmaxf(w0, w1);
@@ -415,6 +438,9 @@ __global__ void __launch_bounds__(kBlend2Threads) blend2_kernel(
     }
   }
 
+  const float tau0 = f2_lo(tau), tau1 = f2_hi(tau);
+  const float r0 = f2_lo(rgb[0]), g0 = f2_lo(rgb[1]), b0 = f2_lo(rgb[2]), d0 = f2_lo(dep);
+  const float r1 = f2_hi(rgb[0]), g1 = f2_hi(rgb[1]), b1 = f2_hi(rgb[2]), d1 = f2_hi(dep);
   if (COLOR) {
     if (out.rgb) {
       if (in0) {

@@ -55,3 +55,14 @@ for _ in range(50):
              count64=torch.empty((H, W), dtype=torch.int64, pin_memory=True))
     del o
 print(f"pinned alloc (cached): {1e3 * (time.perf_counter() - t0) / 50:.3f} ms")
+# the zero-copy host-output frame without the API's allocations
+oh = dict(rgb64=torch.empty((H, W, 3), dtype=torch.float64, pin_memory=True),
+          alpha64=torch.empty((H, W), dtype=torch.float64, pin_memory=True),
+          count64=torch.empty((H, W), dtype=torch.int64, pin_memory=True),
+          depth=torch.empty((H, W), dtype=torch.float32, device="cuda"))
+for c in cams[:5]:
+    r.render(ds, c, opts, out=oh)
+t0 = time.perf_counter()
+for c in cams[:50]:
+    r.render(ds, c, opts, out=oh)
+print(f"render() host outputs, reused buffers: {1e3 * (time.perf_counter() - t0) / 50:.3f} ms/frame")
