@@ -30,6 +30,8 @@ namespace rs {
 
 constexpr int kSGrad = 9;  // screen-space gradient words per item
 
+// FAST: alpha_cut >= 1e-30 (the host's check), so the exact-range exp2_core serves (blend.cuh).
+template <bool FAST>
 __global__ void __launch_bounds__(kBlendThreads) backward_blend_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ pair_items, const Rec* __restrict__ recs,
     const Counters* __restrict__ ctr, int W, int H, int TW, rs_options o, const float* __restrict__ grad_image,
@@ -118,18 +120,19 @@ __global__ void __launch_bounds__(kBlendThreads) backward_blend_kernel(
         const float p2 = __fmaf_rn(__fmul_rn(ga.z, dx), dx,
                                    __fmaf_rn(__fmul_rn(ga.w, dy), dx, __fmul_rn(__fmul_rn(gb4.x, dy), dy)));
         if (p2 >= gb4.z) {
-          const float raw = __fmul_rn(gb4.y, exp2_contract(fminf(p2, 127.0f)));
+          const float raw = __fmul_rn(gb4.y, FAST ? exp2_core(fminf(p2, 127.0f)) : exp2_contract(fminf(p2, 127.0f)));
           const float alpha = fminf(raw, o.alpha_max);
           if (alpha >= o.alpha_cut) {  // composited in the forward pass (k <= last: tau_before >= tau_stop)
             comp = true;
             const float om = __fsub_rn(1.0f, alpha);
-            const float tb = __fdiv_rn(tau, om);
+            const float rom = __frcp_rn(om);  // one reciprocal for both quotients (tolerance path)
+            const float tb = __fmul_rn(tau, rom);
             const float w = __fmul_rn(alpha, tb);
             const float cdot = __fadd_rn(__fadd_rn(__fmul_rn(gc.x, gr), __fmul_rn(gc.y, gg)), __fmul_rn(gc.z, gb));
             v[0] = __fmul_rn(w, gr);
             v[1] = __fmul_rn(w, gg);
             v[2] = __fmul_rn(w, gb);
-            const float da = raw > o.alpha_max ? 0.0f : __fsub_rn(__fmul_rn(tb, cdot), __fdiv_rn(suffix, om));
+            const float da = raw > o.alpha_max ? 0.0f : __fsub_rn(__fmul_rn(tb, cdot), __fmul_rn(suffix, rom));
             v[3] = __fmul_rn(da, alpha);                      // -> dL/do = sum / o
             const float dq = __fmul_rn(__fmul_rn(-0.5f, alpha), da);
             v[4] = __fmul_rn(dq, dx);
