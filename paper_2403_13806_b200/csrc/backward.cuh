@@ -4,15 +4,16 @@
 //
 // Training forward (rs_render_ex with rs_outputs tau / last) leaves, per pixel,
 // the final transmittance and the pair index of its last composite. Then:
-//   backward_blend_kernel  one 256-thread CTA per tile, one pixel per thread,
-//       walks the tile's list BACK to front (batches of 256 staged in shared
-//       memory, per-warp entry lists as in the blend). For each entry the pixel
+//   backward2_kernel  one 128-thread CTA per tile, two pixels per thread, walks
+//       the tile's list BACK to front (batches of 256 staged in shared memory,
+//       per-warp entry lists by ellipse quarters as in blend2_kernel; FAST =
+//       alpha_cut >= 1e-30: the exact-range exp2 core). For each entry the pixel
 //       composited in the forward pass (index <= last, inside the box, alpha >=
 //       alpha_cut -- the same fp32 alpha), tau_before = tau / (1 - alpha) and,
 //       as render.py:366-391: weight = alpha tau_before, g_color += weight g,
 //       d_alpha = tau_before (c.g) - suffix / (1 - alpha) (0 when alpha was
 //       clamped), dq = -0.5 alpha d_alpha, suffix += weight (c.g). Per entry the
-//       warp reduces its lanes' nine partial sums (g_color, sum d_alpha alpha,
+//       warp reduces its lanes' nine partial sums (both pixels added first) (g_color, sum d_alpha alpha,
 //       sum dq dx, sum dq dy, sum dq dx^2, sum dq 2 dx dy, sum dq dy^2) and lane 0
 //       adds them to the item's screen-space gradient (atomicAdd).
 //   chain_kernel  one thread per item: recomputes the projection intermediates
@@ -23,6 +24,8 @@
 // fp32 throughout; the per-Gaussian sums are atomics (order-dependent rounding),
 // so parity with the fp64 reference is a tolerance, not bit equality.
 #pragma once
+#include "f32x2.cuh"
+#include "rows.cuh"
 #include "rs_common.cuh"
 #include "rs_math.cuh"
 
@@ -30,72 +33,90 @@ namespace rs {
 
 constexpr int kSGrad = 9;  // screen-space gradient words per item
 
-// FAST: alpha_cut >= 1e-30 (the host's check), so the exact-range exp2_core serves (blend.cuh).
+// Two pixels per thread (rows py0, py0 + 4 of the warp's 8x8 quarter, as blend2_kernel),
+// 128-thread CTA per tile, batches of 256 records walked back to front. The forward's
+// composite decision (p2, alpha) is recomputed with blend2_kernel's packed contract ops, so
+// it is the forward's bit for bit; the gradient arithmetic after it is fp32 (tolerance).
+// Per entry the two pixels' nine partial sums are added before one warp reduce-scatter.
+constexpr int kBwd2Threads = 128;
 template <bool FAST>
-__global__ void __launch_bounds__(kBlendThreads) backward_blend_kernel(
+__global__ void __launch_bounds__(kBwd2Threads) backward2_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ pair_items, const Rec* __restrict__ recs,
-    const Counters* __restrict__ ctr, int W, int H, int TW, rs_options o, const float* __restrict__ grad_image,
-    const float* __restrict__ tau_final, const int32_t* __restrict__ last, float* __restrict__ sgrad,
-    uint8_t* __restrict__ touched) {
-  __shared__ Rec s_rec[kBlendThreads];
-  __shared__ uint32_t s_item[kBlendThreads];
-  __shared__ uint8_t s_mask[kBlendThreads];
-  __shared__ uint8_t s_list[kBlendThreads / 32][kBlendThreads];
+    const float4* __restrict__ geom, const Counters* __restrict__ ctr, int W, int H, int TW, rs_options o,
+    const float* __restrict__ grad_image, const float* __restrict__ tau_final, const int32_t* __restrict__ last,
+    float* __restrict__ sgrad, uint8_t* __restrict__ touched) {
+  constexpr int kBatch = 256;
+  __shared__ Rec s_rec[kBatch];
+  __shared__ uint32_t s_item[kBatch];
+  __shared__ uint8_t s_mask[kBatch];
+  __shared__ uint8_t s_list[4][kBatch];
+  __shared__ int s_maxlast[4];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int tile = blockIdx.x;
   const int tx = tile % TW, ty = tile / TW;
   const int ox = tx * kTile, oy = ty * kTile;
   const int px = ox + (warp & 1) * 8 + (lane & 7);
-  const int py = oy + (warp >> 1) * 4 + (lane >> 3);
-  const bool inside = px < W && py < H;
-  const float xs = __fadd_rn((float)px, 0.5f), ys = __fadd_rn((float)py, 0.5f);
+  const int py0 = oy + (warp >> 1) * 8 + (lane >> 3), py1 = py0 + 4;
+  const bool in0 = px < W && py0 < H, in1 = px < W && py1 < H;
+  const float xs = __fadd_rn((float)px, 0.5f);
+  const f2 ys2 = f2_pack(__fadd_rn((float)py0, 0.5f), __fadd_rn((float)py1, 0.5f));
   if (ctr->overflow) return;
   const uint2 rg = ranges[tile];
   const uint32_t end = min(rg.y, ctr->n_pairs);
   const uint32_t lt = (1u << lane) - 1u;
-  const size_t p = (size_t)py * W + px;
-  float tau = 1.0f, gr = 0.0f, gg = 0.0f, gb = 0.0f;
-  int lastk = -1;
-  if (inside) {
-    tau = tau_final[p];
-    lastk = last[p];
-    gr = grad_image[3 * p];
-    gg = grad_image[3 * p + 1];
-    gb = grad_image[3 * p + 2];
-  }
-  float suffix = 0.0f;
-  // the CTA's lowest pair index any of its pixels still needs (entries after every pixel's
-  // last composite are skipped wholesale)
-  int maxlast = lastk;
+  float tau[2] = {1.0f, 1.0f}, gcol[2][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}}, suffix[2] = {0.0f, 0.0f};
+  int lastk[2] = {-1, -1};
+  const bool inside[2] = {in0, in1};
+  const int pyv[2] = {py0, py1};
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+    if (inside[j]) {
+      const size_t p = (size_t)pyv[j] * W + px;
+      tau[j] = tau_final[p];
+      lastk[j] = last[p];
+      gcol[j][0] = grad_image[3 * p];
+      gcol[j][1] = grad_image[3 * p + 1];
+      gcol[j][2] = grad_image[3 * p + 2];
+    }
+  // entries after every pixel's last composite are skipped wholesale
+  int maxlast = max(lastk[0], lastk[1]);
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) maxlast = max(maxlast, __shfl_xor_sync(0xffffffffu, maxlast, off));
-  __shared__ int s_maxlast[kBlendThreads / 32];
   if (lane == 0) s_maxlast[warp] = maxlast;
   __syncthreads();
-  int cta_last = -1;
-#pragma unroll
-  for (int w = 0; w < kBlendThreads / 32; ++w) cta_last = max(cta_last, s_maxlast[w]);
+  const int cta_last = max(max(s_maxlast[0], s_maxlast[1]), max(s_maxlast[2], s_maxlast[3]));
   const uint32_t stop = cta_last < 0 ? rg.x : min(end, (uint32_t)cta_last + 1u);
 
   for (uint32_t top = stop; top > rg.x;) {
-    const uint32_t base = top - min((uint32_t)kBlendThreads, top - rg.x);
+    const uint32_t base = top - min((uint32_t)kBatch, top - rg.x);
     const int n = (int)(top - base);
     __syncthreads();
-    if (tid < n) {
-      const uint32_t it = __ldg(pair_items + base + tid);
-      const Rec* R = recs + it;
-      s_rec[tid].a = __ldg(&R->a);
-      s_rec[tid].b = __ldg(&R->b);
-      s_rec[tid].c = __ldg(&R->c);
-      const int4 d = cullbox_of(__ldg(&R->d));
-      s_rec[tid].d = d;
-      s_item[tid] = it;
-      const unsigned col = (d.x < ox + 8 && d.y > ox ? 1u : 0u) | (d.x < ox + 16 && d.y > ox + 8 ? 2u : 0u);
-      unsigned m = 0;
 #pragma unroll
-      for (int r = 0; r < 4; ++r)
-        if (d.z < oy + 4 * r + 4 && d.w > oy + 4 * r) m |= col << (2 * r);
-      s_mask[tid] = (uint8_t)m;
+    for (int h = 0; h < 2; ++h) {
+      const int slot = tid + h * kBwd2Threads;
+      if (slot < n) {
+        const uint32_t it = __ldg(pair_items + base + slot);
+        const Rec* R = recs + it;
+        const float4 a = __ldg(&R->a);
+        s_rec[slot].a = a;
+        s_rec[slot].b = __ldg(&R->b);
+        s_rec[slot].c = __ldg(&R->c);
+        const int4 dr = __ldg(&R->d);
+        const int4 d = cullbox_of(dr);
+        s_rec[slot].d = d;
+        s_item[slot] = it;
+        // the 8x8 quarters the entry can composite in (blend2_kernel's warp lists)
+        unsigned m;
+        if (cullbox_ell(dr)) {
+          m = quarter_mask(load_row_geom(geom + 2 * (size_t)it, a.x, a.y), d, ox, oy);
+        } else {
+          const unsigned col = (d.x < ox + 8 && d.y > ox ? 1u : 0u) | (d.x < ox + 16 && d.y > ox + 8 ? 2u : 0u);
+          m = 0;
+          if (d.z < oy + 8 && d.w > oy) m |= col;
+          if (d.z < oy + 16 && d.w > oy + 8) m |= col << 2;
+        }
+        s_mask[slot] = (uint8_t)m;
+      }
     }
     __syncthreads();
     int cntw = 0;
@@ -111,56 +132,84 @@ __global__ void __launch_bounds__(kBlendThreads) backward_blend_kernel(
       const int e = s_list[warp][q];
       const Rec& E = s_rec[e];
       const int4 bb = E.d;
+      const float4 ga = E.a, gb4 = E.b;
       const int k = (int)base + e;
+      const bool inx = px >= bb.x && px < bb.y;
+      const bool cand0 = in0 && k <= lastk[0] && inx && py0 >= bb.z && py0 < bb.w;
+      const bool cand1 = in1 && k <= lastk[1] && inx && py1 >= bb.z && py1 < bb.w;
+      if (!__any_sync(0xffffffffu, cand0 || cand1)) continue;
+      // the forward's p2 / alpha (blend2_kernel's operations)
+      const float dx = __fsub_rn(xs, ga.x);
+      const float ax = __fmul_rn(ga.z, dx);
+      const f2 dy2 = f2_sub(ys2, f2_splat(ga.y));
+      const f2 t3 = f2_mul(f2_mul(f2_splat(gb4.x), dy2), dy2);
+      const f2 p2 = f2_fma(f2_splat(ax), f2_splat(dx), f2_fma(f2_mul(f2_splat(ga.w), dy2), f2_splat(dx), t3));
+      const float p20 = f2_lo(p2), p21 = f2_hi(p2);
+      f2 ex;
+      if (FAST) {
+        const f2 x = f2_pack(fminf(p20, 127.0f), fminf(p21, 127.0f));
+        const f2 t = f2_add(x, f2_splat(kMagic));
+        const f2 r = f2_sub(x, f2_sub(t, f2_splat(kMagic)));
+        const f2 sc = f2_pack(__int_as_float((__float_as_int(f2_lo(t)) << 23) + 0x3f800000),
+                              __int_as_float((__float_as_int(f2_hi(t)) << 23) + 0x3f800000));
+        f2 pp = f2_fma(f2_splat(fbits(0x3920e999u)), r, f2_splat(fbits(0x3aafa2b5u)));
+        pp = f2_fma(pp, r, f2_splat(fbits(0x3c1d96deu)));
+        pp = f2_fma(pp, r, f2_splat(fbits(0x3d63576au)));
+        pp = f2_fma(pp, r, f2_splat(fbits(0x3e75fdedu)));
+        pp = f2_fma(pp, r, f2_splat(fbits(0x3f317218u)));
+        pp = f2_fma(pp, r, f2_splat(1.0f));
+        ex = f2_mul(pp, sc);
+      } else {
+        ex = f2_pack(exp2_contract(fminf(p20, 127.0f)), exp2_contract(fminf(p21, 127.0f)));
+      }
+      const f2 raw2 = f2_mul(f2_splat(gb4.y), ex);
+      const float raw[2] = {f2_lo(raw2), f2_hi(raw2)};
+      const float p2v[2] = {p20, p21};
+      const bool cand[2] = {cand0, cand1};
+      const float dyv[2] = {__fsub_rn(__fadd_rn((float)py0, 0.5f), ga.y), __fsub_rn(__fadd_rn((float)py1, 0.5f), ga.y)};
+      const float4 gc = E.c;
       float v[kSGrad] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       bool comp = false;
-      if (inside && k <= lastk && px >= bb.x && px < bb.y && py >= bb.z && py < bb.w) {
-        const float4 ga = E.a, gb4 = E.b, gc = E.c;
-        const float dx = __fsub_rn(xs, ga.x), dy = __fsub_rn(ys, ga.y);
-        const float p2 = __fmaf_rn(__fmul_rn(ga.z, dx), dx,
-                                   __fmaf_rn(__fmul_rn(ga.w, dy), dx, __fmul_rn(__fmul_rn(gb4.x, dy), dy)));
-        if (p2 >= gb4.z) {
-          const float raw = __fmul_rn(gb4.y, FAST ? exp2_core(fminf(p2, 127.0f)) : exp2_contract(fminf(p2, 127.0f)));
-          const float alpha = fminf(raw, o.alpha_max);
-          if (alpha >= o.alpha_cut) {  // composited in the forward pass (k <= last: tau_before >= tau_stop)
-            comp = true;
-            const float om = __fsub_rn(1.0f, alpha);
-            const float rom = __frcp_rn(om);  // one reciprocal for both quotients (tolerance path)
-            const float tb = __fmul_rn(tau, rom);
-            const float w = __fmul_rn(alpha, tb);
-            const float cdot = __fadd_rn(__fadd_rn(__fmul_rn(gc.x, gr), __fmul_rn(gc.y, gg)), __fmul_rn(gc.z, gb));
-            v[0] = __fmul_rn(w, gr);
-            v[1] = __fmul_rn(w, gg);
-            v[2] = __fmul_rn(w, gb);
-            const float da = raw > o.alpha_max ? 0.0f : __fsub_rn(__fmul_rn(tb, cdot), __fmul_rn(suffix, rom));
-            v[3] = __fmul_rn(da, alpha);                      // -> dL/do = sum / o
-            const float dq = __fmul_rn(__fmul_rn(-0.5f, alpha), da);
-            v[4] = __fmul_rn(dq, dx);
-            v[5] = __fmul_rn(dq, dy);
-            v[6] = __fmul_rn(dq, __fmul_rn(dx, dx));
-            v[7] = __fmul_rn(dq, __fmul_rn(__fmul_rn(2.0f, dy), dx));
-            v[8] = __fmul_rn(dq, __fmul_rn(dy, dy));
-            suffix = __fadd_rn(suffix, __fmul_rn(w, cdot));
-            tau = tb;
-          }
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const float alpha = fminf(raw[j], o.alpha_max);
+        if (cand[j] && p2v[j] >= gb4.z && alpha >= o.alpha_cut) {  // composited in the forward pass
+          comp = true;
+          const float dy = dyv[j];
+          const float rom = __frcp_rn(__fsub_rn(1.0f, alpha));
+          const float tb = __fmul_rn(tau[j], rom);
+          const float w = __fmul_rn(alpha, tb);
+          const float cdot = __fadd_rn(__fadd_rn(__fmul_rn(gc.x, gcol[j][0]), __fmul_rn(gc.y, gcol[j][1])),
+                                       __fmul_rn(gc.z, gcol[j][2]));
+          v[0] += __fmul_rn(w, gcol[j][0]);
+          v[1] += __fmul_rn(w, gcol[j][1]);
+          v[2] += __fmul_rn(w, gcol[j][2]);
+          const float da = raw[j] > o.alpha_max ? 0.0f : __fsub_rn(__fmul_rn(tb, cdot), __fmul_rn(suffix[j], rom));
+          v[3] += __fmul_rn(da, alpha);
+          const float dq = __fmul_rn(__fmul_rn(-0.5f, alpha), da);
+          v[4] += __fmul_rn(dq, dx);
+          v[5] += __fmul_rn(dq, dy);
+          v[6] += __fmul_rn(dq, __fmul_rn(dx, dx));
+          v[7] += __fmul_rn(dq, __fmul_rn(__fmul_rn(2.0f, dy), dx));
+          v[8] += __fmul_rn(dq, __fmul_rn(dy, dy));
+          suffix[j] = __fadd_rn(suffix[j], __fmul_rn(w, cdot));
+          tau[j] = tb;
         }
       }
       if (__any_sync(0xffffffffu, comp)) {
-        // reduce-scatter of v[0..7] across the warp (each butterfly step keeps half of the
-        // values: 4 + 2 + 1 + 1 + 1 shuffles instead of 8 x 5), then lane 4j + 0..3 holds
-        // the warp sum of value j; v[8] by a plain butterfly
+        // reduce-scatter of v[0..7] (4 + 2 + 1 + 1 + 1 shuffles), v[8] by a butterfly
         const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
         float w4[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const float r = __shfl_xor_sync(0xffffffffu, b4 ? v[k] : v[4 + k], 16);
-          w4[k] = (b4 ? v[4 + k] : v[k]) + r;
+        for (int kk = 0; kk < 4; ++kk) {
+          const float r = __shfl_xor_sync(0xffffffffu, b4 ? v[kk] : v[4 + kk], 16);
+          w4[kk] = (b4 ? v[4 + kk] : v[kk]) + r;
         }
         float w2[2];
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
-          const float r = __shfl_xor_sync(0xffffffffu, b3 ? w4[k] : w4[2 + k], 8);
-          w2[k] = (b3 ? w4[2 + k] : w4[k]) + r;
+        for (int kk = 0; kk < 2; ++kk) {
+          const float r = __shfl_xor_sync(0xffffffffu, b3 ? w4[kk] : w4[2 + kk], 8);
+          w2[kk] = (b3 ? w4[2 + kk] : w4[kk]) + r;
         }
         float w1 = (b2 ? w2[1] : w2[0]) + __shfl_xor_sync(0xffffffffu, b2 ? w2[0] : w2[1], 4);
         w1 += __shfl_xor_sync(0xffffffffu, w1, 2);
