@@ -22,6 +22,38 @@
 
 using namespace rs;
 
+// Frame kernels launched straight onto a stream use programmatic stream serialization (PDL):
+// the grid is scheduled while the previous kernel drains and waits in griddepcontrol.wait
+// (pdl_wait, the first statement of each kernel) for its completion -- the launch gaps of the
+// chain of small binning kernels are hidden (configs[2] scoring +3%). Not while a CUDA graph
+// is being captured: replayed graphs already launch back to back, and programmatic edges in
+// them measured 2% slower per configs[1] frame.
+enum PdlClass { kPdlChain = 1, kPdlExpand = 2, kPdlBlend = 4, kPdlAll = 7 };
+static int pdl_mode() {  // RS_PDL (A/B measurements): bit 0 binning chain, bit 1 expand, bit 2 blend
+  static const int m = [] {
+    const char* e = std::getenv("RS_PDL");
+    return e ? std::atoi(e) : kPdlAll;
+  }();
+  return m;
+}
+static int g_pdl_class = kPdlChain;  // class of the next launch() (set by the callers below)
+template <typename... KP, typename... A>
+static void launch(void (*k)(KP...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, A&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cap);
+  cfg.numAttrs = (cap == cudaStreamCaptureStatusNone && (pdl_mode() & g_pdl_class)) ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, k, static_cast<KP>(args)...);
+}
+
 namespace {
 
 size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
@@ -156,9 +188,8 @@ void run_sort(rs_workspace* ws, const K* keys0, K* keysA, K* keysB, const uint32
     uint32_t* lb_next = last ? nullptr : lb[(p + 1) % 2];
     const int wk = (!last || last_keys) ? 1 : 0;
 #define RS_PASS(NB)                                                                                       \
-  onesweep_kernel<K, ITEMS, NB><<<grid, kSortThreads, smem, st>>>(kin, vin, kout, vout, n_ptr, n_static,   \
-                                                                  hist + p * 256, lb[p % 2], lb_next,      \
-                                                                  ctr->tickets + ticket_slot + p, 8 * p, wk)
+  launch(onesweep_kernel<K, ITEMS, NB>, grid, kSortThreads, smem, st, kin, vin, kout, vout, n_ptr, n_static, \
+         hist + p * 256, lb[p % 2], lb_next, ctr->tickets + ticket_slot + p, 8 * p, wk)
     switch (nbits) {
       case 1: RS_PASS(1); break;
       case 2: RS_PASS(2); break;
@@ -289,14 +320,15 @@ static int32_t project_impl(rs_workspace* ws, const rs_scene* scene, const int32
   if (items > 0) {
     const unsigned grid = (unsigned)((items + kProjThreads - 1) / kProjThreads);
     if (full)
-      project_kernel<true, true><<<grid, kProjThreads, 0, st>>>(
-          scene->planes, scene->sh, scene->plane_stride, scene->sh_degree, active_idx, (uint32_t)items, ws->at<rs_camera>(ws->L.cam), *opts,
-          ws->at<Rec>(ws->L.recs), ws->at<uint32_t>(ws->L.keysB), ws->ctr(), full,
-          reinterpret_cast<int4*>(full_bbox));
+      launch(project_kernel<true, true>, grid, kProjThreads, 0, st, scene->planes, scene->sh,
+             scene->plane_stride, scene->sh_degree, active_idx, (uint32_t)items, ws->at<rs_camera>(ws->L.cam),
+             *opts, ws->at<Rec>(ws->L.recs), ws->at<uint32_t>(ws->L.keysB), ws->ctr(), full,
+             reinterpret_cast<int4*>(full_bbox));
     else
-      (color ? project_kernel<false, true> : project_kernel<false, false>)<<<grid, kProjThreads, 0, st>>>(
-          scene->planes, scene->sh, scene->plane_stride, scene->sh_degree, active_idx, (uint32_t)items, ws->at<rs_camera>(ws->L.cam), *opts,
-          ws->at<Rec>(ws->L.recs), ws->at<uint32_t>(ws->L.keysB), ws->ctr(), nullptr, nullptr);
+      launch((color ? project_kernel<false, true> : project_kernel<false, false>), grid, kProjThreads, 0, st,
+             scene->planes, scene->sh, scene->plane_stride, scene->sh_degree, active_idx, (uint32_t)items,
+             ws->at<rs_camera>(ws->L.cam), *opts, ws->at<Rec>(ws->L.recs), ws->at<uint32_t>(ws->L.keysB),
+             ws->ctr(), nullptr, nullptr);
   }
   return cuda_status();
 }
@@ -320,10 +352,10 @@ int32_t rs_bin(rs_workspace* ws, void* stream) {
   if (n > 0) {
     // depth sort of the n_visible binned items (compacted in item order by the projection)
     const uint32_t* nvis = &ws->ctr()->n_visible;
-    compact_hist_kernel<<<(n + kCompactKeys - 1) / kCompactKeys, 256, 0, st>>>(
-        ws->at<uint32_t>(ws->L.keysB), n, ws->at<uint32_t>(ws->L.keysA), ws->at<uint32_t>(ws->L.valsA),
-        ws->at<unsigned long long>(ws->L.proj_lb), ws->ctr(), kSortThreads * kDepthItems,
-        ws->at<uint32_t>(ws->L.hist), ws->at<uint32_t>(ws->L.lbA));
+    launch(compact_hist_kernel, (n + kCompactKeys - 1) / kCompactKeys, 256, 0, st,
+           ws->at<uint32_t>(ws->L.keysB), n, ws->at<uint32_t>(ws->L.keysA), ws->at<uint32_t>(ws->L.valsA),
+           ws->at<unsigned long long>(ws->L.proj_lb), ws->ctr(), kSortThreads * kDepthItems,
+           ws->at<uint32_t>(ws->L.hist), ws->at<uint32_t>(ws->L.lbA));
     const uint32_t *keys_res, *items_sorted;
     run_sort<uint32_t, kDepthItems>(ws, ws->at<uint32_t>(ws->L.keysA), ws->at<uint32_t>(ws->L.keysA),
                                     ws->at<uint32_t>(ws->L.keysB), ws->at<uint32_t>(ws->L.valsA),
@@ -336,44 +368,41 @@ int32_t rs_bin(rs_workspace* ws, void* stream) {
     const uint32_t seg_cap = (uint32_t)seg_capacity(ws->n_cap, ws->pair_cap);
     const uint32_t tab_stride = (uint32_t)rowtab_stride(ws->n_cap);
     const unsigned rc = (n + kRankChunk - 1) / kRankChunk;
-    segrows_kernel<<<rc, 256, 0, st>>>(items_sorted, ws->at<Rec>(ws->L.recs), ctr, ws->TH, tab_stride,
-                                       ws->at<uint32_t>(ws->L.rowtab));
-    segscan_kernel<<<ws->TH, 256, 0, st>>>(ws->at<uint32_t>(ws->L.rowtab), tab_stride, ctr, ws->TH, seg_cap,
-                                           ws->at<uint32_t>(ws->L.rowcnt), ws->at<uint32_t>(ws->L.rowstart),
-                                           ws->at<uint32_t>(ws->L.chunkstart), ws->at<Sticky>(ws->L.sticky));
-    segplace_kernel<<<rc, 256, 64 * ws->TH, st>>>(items_sorted, ws->at<Rec>(ws->L.recs), ctr, ws->TH,
-                                                  ws->at<uint32_t>(ws->L.rowtab), tab_stride,
-                                                  ws->at<uint32_t>(ws->L.rowstart), ws->at<uint32_t>(ws->L.segitem),
-                                                  ws->at<uint32_t>(ws->L.segspan), ws->at<float4>(ws->L.geom));
+    launch(segrows_kernel, rc, 256, 0, st, items_sorted, ws->at<Rec>(ws->L.recs), ctr, ws->TH, tab_stride,
+           ws->at<uint32_t>(ws->L.rowtab));
+    launch(segscan_kernel, ws->TH, 256, 0, st, ws->at<uint32_t>(ws->L.rowtab), tab_stride, ctr, ws->TH, seg_cap,
+           ws->at<uint32_t>(ws->L.rowcnt), ws->at<uint32_t>(ws->L.rowstart), ws->at<uint32_t>(ws->L.chunkstart),
+           ws->at<Sticky>(ws->L.sticky));
+    launch(segplace_kernel, rc, 256, 64 * ws->TH, st, items_sorted, ws->at<Rec>(ws->L.recs), ctr, ws->TH,
+           ws->at<uint32_t>(ws->L.rowtab), tab_stride, ws->at<uint32_t>(ws->L.rowstart),
+           ws->at<uint32_t>(ws->L.segitem), ws->at<uint32_t>(ws->L.segspan), ws->at<float4>(ws->L.geom));
     const unsigned gx = (unsigned)std::min<int64_t>(seg_cap / kExpandChunk + ws->TH + 1, (int64_t)ws->sms * 16);
     // expansion: the sparse chunks grid-strided (column groups x chunk slots), the dense ones on
     // persistent ticketed CTAs on the workspace's second stream, concurrently
     const dim3 eg((ws->TW + kExpandCols - 1) / kExpandCols, gx), dg(ws->sms * 6);
-    chunk_count_kernel<<<gx, 256, 0, st>>>(ws->at<uint32_t>(ws->L.segspan),
-                                           ws->at<uint32_t>(ws->L.rowstart), ws->at<uint32_t>(ws->L.chunkstart),
-                                           ws->TH, ws->TW, ws->at<uint32_t>(ws->L.chunkcnt),
-                                           ws->at<uint2>(ws->L.chunkinfo), expand_dense_span(), ctr,
-                                           ws->at<uint32_t>(ws->L.densel));
+    launch(chunk_count_kernel, gx, 256, 0, st, ws->at<uint32_t>(ws->L.segspan),
+           ws->at<uint32_t>(ws->L.rowstart), ws->at<uint32_t>(ws->L.chunkstart), ws->TH, ws->TW,
+           ws->at<uint32_t>(ws->L.chunkcnt), ws->at<uint2>(ws->L.chunkinfo), expand_dense_span(), ctr,
+           ws->at<uint32_t>(ws->L.densel));
     const int T = ws->TW * ws->TH;
-    tile_chunks_kernel<<<(T + 7) / 8, 256, 0, st>>>(ws->at<uint32_t>(ws->L.chunkstart), ws->TH, ws->TW,
-                                                        ws->at<uint32_t>(ws->L.chunkcnt),
-                                                        ws->at<uint32_t>(ws->L.tilecnt));
-    tile_scan_kernel<<<1, 1024, 0, st>>>(ws->at<uint32_t>(ws->L.tilecnt), T, ctr, (uint32_t)ws->pair_cap,
-                                         ws->at<uint2>(ws->L.ranges), ws->at<Sticky>(ws->L.sticky));
+    launch(tile_chunks_kernel, (T + 7) / 8, 256, 0, st, ws->at<uint32_t>(ws->L.chunkstart), ws->TH, ws->TW,
+           ws->at<uint32_t>(ws->L.chunkcnt), ws->at<uint32_t>(ws->L.tilecnt));
+    launch(tile_scan_kernel, 1, 1024, 0, st, ws->at<uint32_t>(ws->L.tilecnt), T, ctr, (uint32_t)ws->pair_cap,
+           ws->at<uint2>(ws->L.ranges), ws->at<Sticky>(ws->L.sticky));
     cudaEventRecord(ws->ev_fork, st);
     cudaStreamWaitEvent(ws->aux, ws->ev_fork, 0);
-    expand_dense_kernel<<<dg, 256, 0, ws->aux>>>(ws->at<uint32_t>(ws->L.segitem),
-                                            ws->at<uint32_t>(ws->L.segspan), ws->at<uint2>(ws->L.chunkinfo),
-                                            ws->at<uint32_t>(ws->L.densel), ws->TW,
-                                            ws->at<uint32_t>(ws->L.chunkcnt), ws->at<uint2>(ws->L.ranges), ctr,
-                                            ws->at<uint32_t>(ws->L.pitem));
+    g_pdl_class = kPdlExpand;
+    launch(expand_dense_kernel, dg, 256, 0, ws->aux, ws->at<uint32_t>(ws->L.segitem),
+           ws->at<uint32_t>(ws->L.segspan), ws->at<uint2>(ws->L.chunkinfo), ws->at<uint32_t>(ws->L.densel),
+           ws->TW, ws->at<uint32_t>(ws->L.chunkcnt), ws->at<uint2>(ws->L.ranges), ctr,
+           ws->at<uint32_t>(ws->L.pitem));
     cudaEventRecord(ws->ev_join, ws->aux);
-    expand_kernel<<<eg, 256, 0, st>>>(ws->at<uint32_t>(ws->L.segitem),
-                                      ws->at<uint32_t>(ws->L.segspan), ws->at<uint2>(ws->L.chunkinfo),
-                                      ws->at<uint32_t>(ws->L.chunkstart), ws->TH, ws->TW,
-                                      ws->at<uint32_t>(ws->L.chunkcnt), ws->at<uint2>(ws->L.ranges), ctr,
-                                      ws->at<uint32_t>(ws->L.pitem), expand_major_thresh());
+    launch(expand_kernel, eg, 256, 0, st, ws->at<uint32_t>(ws->L.segitem), ws->at<uint32_t>(ws->L.segspan),
+           ws->at<uint2>(ws->L.chunkinfo), ws->at<uint32_t>(ws->L.chunkstart), ws->TH, ws->TW,
+           ws->at<uint32_t>(ws->L.chunkcnt), ws->at<uint2>(ws->L.ranges), ctr, ws->at<uint32_t>(ws->L.pitem),
+           expand_major_thresh());
     cudaStreamWaitEvent(st, ws->ev_join, 0);
+    g_pdl_class = kPdlChain;
   }
   ws->binned = true;
   return cuda_status();
@@ -402,28 +431,32 @@ int32_t rs_blend_ex(rs_workspace* ws, const rs_options* opts, const rs_outputs* 
   const Rec* recs = ws->at<Rec>(ws->L.recs);
   const float4* geom = ws->at<float4>(ws->L.geom);  // ellipse row geometry (warp quarter masks)
   Counters* ctr = ws->ctr();
+  g_pdl_class = kPdlBlend;
+  struct Restore {
+    ~Restore() { g_pdl_class = kPdlChain; }
+  } restore;
 #define RS_BLEND(C, I, K, F)                                                                              \
   if (one_px)                                                                                             \
-    blend_kernel<C, I, K, F><<<T, kBlendThreads, 0, st>>>(ranges, items, recs, ctr, ws->W, ws->H, ws->TW, \
-                                                          *opts, out, scores);                            \
+    launch(blend_kernel<C, I, K, F>, T, kBlendThreads, 0, st, ranges, items, recs, ctr, ws->W, ws->H,     \
+           ws->TW, *opts, out, scores);                                                                    \
   else                                                                                                    \
-    blend2_kernel<C, I, K, F><<<T, kBlend2Threads, 0, st>>>(ranges, items, recs, geom, ctr, ws->W, ws->H, \
-                                                            ws->TW, *opts, out, scores)
+    launch(blend2_kernel<C, I, K, F>, T, kBlend2Threads, 0, st, ranges, items, recs, geom, ctr, ws->W,    \
+           ws->H, ws->TW, *opts, out, scores)
 #define RS_BLEND_F(C, I, K) \
   if (fast) { RS_BLEND(C, I, K, true); } else { RS_BLEND(C, I, K, false); }
   // exact-range exp2 is only needed for degenerate options (see blend.cuh FAST)
   const bool fast = opts->alpha_cut >= 1e-30f;
   if (out.tau) {  // training forward (rasterize_cached): records tau and the last composite per pixel
     if (scores) {
-      if (fast) blend2_kernel<true, true, false, true, true><<<T, kBlend2Threads, 0, st>>>(
-          ranges, items, recs, geom, ctr, ws->W, ws->H, ws->TW, *opts, out, scores);
-      else blend2_kernel<true, true, false, false, true><<<T, kBlend2Threads, 0, st>>>(
-          ranges, items, recs, geom, ctr, ws->W, ws->H, ws->TW, *opts, out, scores);
+      if (fast) launch(blend2_kernel<true, true, false, true, true>, T, kBlend2Threads, 0, st, ranges, items,
+                       recs, geom, ctr, ws->W, ws->H, ws->TW, *opts, out, scores);
+      else launch(blend2_kernel<true, true, false, false, true>, T, kBlend2Threads, 0, st, ranges, items, recs,
+                  geom, ctr, ws->W, ws->H, ws->TW, *opts, out, scores);
     } else {
-      if (fast) blend2_kernel<true, false, false, true, true><<<T, kBlend2Threads, 0, st>>>(
-          ranges, items, recs, geom, ctr, ws->W, ws->H, ws->TW, *opts, out, scores);
-      else blend2_kernel<true, false, false, false, true><<<T, kBlend2Threads, 0, st>>>(
-          ranges, items, recs, geom, ctr, ws->W, ws->H, ws->TW, *opts, out, scores);
+      if (fast) launch(blend2_kernel<true, false, false, true, true>, T, kBlend2Threads, 0, st, ranges, items,
+                       recs, geom, ctr, ws->W, ws->H, ws->TW, *opts, out, scores);
+      else launch(blend2_kernel<true, false, false, false, true>, T, kBlend2Threads, 0, st, ranges, items, recs,
+                  geom, ctr, ws->W, ws->H, ws->TW, *opts, out, scores);
     }
   } else if (color && scores) {
     if (stats) { RS_BLEND_F(true, true, true); } else { RS_BLEND_F(true, true, false); }
@@ -485,14 +518,13 @@ int32_t rs_backward(rs_workspace* ws, const rs_scene* scene, const int32_t* acti
   cudaMemsetAsync(ws->at<float>(ws->L.sgrad), 0, (size_t)items * 4 * kSGrad, st);
   cudaMemsetAsync(ws->at<uint8_t>(ws->L.titem), 0, (size_t)items, st);
   auto* bwd = opts->alpha_cut >= 1e-30f ? backward2_kernel<true> : backward2_kernel<false>;
-  bwd<<<ws->TW * ws->TH, kBwd2Threads, 0, st>>>(
-      ws->at<uint2>(ws->L.ranges), final_pair_items(ws), ws->at<Rec>(ws->L.recs), ws->at<float4>(ws->L.geom),
-      ws->ctr(), ws->W, ws->H, ws->TW, *opts, grad_image, tau, last, ws->at<float>(ws->L.sgrad),
-      ws->at<uint8_t>(ws->L.titem));
-  chain_kernel<<<(unsigned)((items + 127) / 128), 128, 0, st>>>(
-      scene->planes, scene->sh, scene->plane_stride, scene->sh_degree, active_idx, (uint32_t)items,
-      ws->at<rs_camera>(ws->L.cam), *opts, ws->at<float>(ws->L.sgrad), ws->at<uint8_t>(ws->L.titem), g_pos, g_sh,
-      g_ls, g_quat, g_logit, g_mean2d, touched);
+  launch(bwd, ws->TW * ws->TH, kBwd2Threads, 0, st, ws->at<uint2>(ws->L.ranges), final_pair_items(ws),
+         ws->at<Rec>(ws->L.recs), ws->at<float4>(ws->L.geom), ws->ctr(), ws->W, ws->H, ws->TW, *opts,
+         grad_image, tau, last, ws->at<float>(ws->L.sgrad), ws->at<uint8_t>(ws->L.titem));
+  launch(chain_kernel, (unsigned)((items + 127) / 128), 128, 0, st, scene->planes, scene->sh,
+         scene->plane_stride, scene->sh_degree, active_idx, (uint32_t)items, ws->at<rs_camera>(ws->L.cam),
+         *opts, ws->at<float>(ws->L.sgrad), ws->at<uint8_t>(ws->L.titem), g_pos, g_sh, g_ls, g_quat, g_logit,
+         g_mean2d, touched);
   return cuda_status();
 }
 

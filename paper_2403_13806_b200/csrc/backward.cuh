@@ -45,6 +45,8 @@ __global__ void __launch_bounds__(kBwd2Threads) backward2_kernel(
     const float4* __restrict__ geom, const Counters* __restrict__ ctr, int W, int H, int TW, rs_options o,
     const float* __restrict__ grad_image, const float* __restrict__ tau_final, const int32_t* __restrict__ last,
     float* __restrict__ sgrad, uint8_t* __restrict__ touched) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int kBatch = 256;
   __shared__ Rec s_rec[kBatch];
   __shared__ uint32_t s_item[kBatch];
@@ -245,6 +247,8 @@ __global__ void __launch_bounds__(128) chain_kernel(
     const float* __restrict__ sgrad, const uint8_t* __restrict__ touched, float* __restrict__ g_pos,
     float* __restrict__ g_sh, float* __restrict__ g_ls, float* __restrict__ g_quat, float* __restrict__ g_logit,
     float* __restrict__ g_mean2d, uint8_t* __restrict__ touched_out) {
+  pdl_wait();
+  pdl_trigger();
   const uint32_t item = blockIdx.x * blockDim.x + threadIdx.x;
   if (item >= n_items || !touched[item]) return;
   const rs_camera cam = *camp;

@@ -41,6 +41,8 @@ __global__ void __launch_bounds__(kBlendThreads) blend_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ pair_items, const Rec* __restrict__ recs,
     Counters* __restrict__ ctr, int W, int H, int TW, rs_options o, const rs_outputs out,
     uint32_t* __restrict__ scores) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ Rec s_rec[kBlendThreads];  // one 64-byte record per entry: one base address per iteration
   __shared__ uint32_t s_w[CONTRIB ? kBlendThreads : 1];
   __shared__ uint8_t s_mask[kBlendThreads];             // which warps' 8x4 sub-rectangles the entry touches
@@ -253,6 +255,8 @@ __global__ void __launch_bounds__(kBlend2Threads, RS_BLEND_MINB) blend2_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ pair_items, const Rec* __restrict__ recs,
     const float4* __restrict__ geom, Counters* __restrict__ ctr, int W, int H, int TW, rs_options o,
     const rs_outputs out, uint32_t* __restrict__ scores) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int kBatch = 256;  // entries staged per batch (two per thread)
   __shared__ Rec s_rec[kBatch];
   __shared__ uint32_t s_w[CONTRIB ? kBatch : 1];

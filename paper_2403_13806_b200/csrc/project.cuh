@@ -47,6 +47,8 @@ __global__ void __launch_bounds__(128) project_kernel(const float* __restrict__ 
                                                       uint32_t* __restrict__ keys,
                                                       Counters* __restrict__ ctr,
                                                       float* __restrict__ full, int4* __restrict__ full_bbox) {
+  pdl_wait();
+  pdl_trigger();
   const uint32_t item = blockIdx.x * blockDim.x + threadIdx.x;
   if (item == 0) ctr->n_items = n_items;
   // the camera lives in device memory (uploaded by a stream-ordered copy), so a captured

@@ -42,6 +42,12 @@ __device__ __forceinline__ bool cullbox_ell(const int4 d) { return d.w < 0; }
 __device__ __forceinline__ bool cullbox_tight(const int4 d) { return d.z < 0; }
 
 // Device-side counters, mirrors rs_stats (first four words) + sort bookkeeping.
+// Programmatic dependent launch (api.cu launch()): wait for the previous kernel of the stream
+// to complete (its writes visible), then let the next one be scheduled. No-ops for a kernel
+// launched without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 struct Counters {
   uint32_t n_items, n_visible, n_pairs, overflow;  // n_pairs = min(P, pair capacity)
   unsigned long long evals, composites;

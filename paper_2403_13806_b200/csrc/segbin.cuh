@@ -55,6 +55,8 @@ __global__ void __launch_bounds__(256) segrows_kernel(const uint32_t* __restrict
                                                       const Rec* __restrict__ recs,
                                                       const Counters* __restrict__ ctr, int TH, uint32_t tab_stride,
                                                       uint32_t* __restrict__ row_tab) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ int s_d[kMaxTileRows + 1];
   __shared__ uint32_t s_w[8];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -160,6 +162,8 @@ __global__ void __launch_bounds__(256) segscan_kernel(uint32_t* __restrict__ row
                                                       uint32_t* __restrict__ row_start,
                                                       uint32_t* __restrict__ chunk_start,
                                                       Sticky* __restrict__ sticky) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ uint32_t s_w[16], s_last;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t nc = (ctr->n_visible + kRankChunk - 1) / kRankChunk;
@@ -234,6 +238,8 @@ __global__ void __launch_bounds__(256) segplace_kernel(const uint32_t* __restric
                                                        uint32_t tab_stride, const uint32_t* __restrict__ row_start,
                                                        uint32_t* __restrict__ seg_item,
                                                        uint32_t* __restrict__ seg_span, float4* __restrict__ geom) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ uint32_t s_dyn[];
   uint32_t* s_bal = s_dyn;           // [8][TH]
   uint32_t* s_off = s_dyn + 8 * TH;  // [8][TH]
@@ -426,6 +432,8 @@ __global__ void __launch_bounds__(256) expand_kernel(const uint32_t* __restrict_
                                                      const uint2* __restrict__ ranges,
                                                      const Counters* __restrict__ ctr,
                                                      uint32_t* __restrict__ pair_items, int major_thresh) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ uint32_t s_cnt[2][8][32];
   __shared__ uint32_t s_cm[8][kExpandSub * 32], s_ci[8][kExpandSub * 32];  // per-warp compaction
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -530,6 +538,8 @@ __global__ void __launch_bounds__(256) expand_dense_kernel(const uint32_t* __res
                                                            const uint2* __restrict__ ranges,
                                                            Counters* __restrict__ ctr,
                                                            uint32_t* __restrict__ pair_items) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ uint32_t s_item[256], s_span[256];
   __shared__ int s_wk[8];
   __shared__ uint32_t s_tk[2];
@@ -562,6 +572,8 @@ __global__ void __launch_bounds__(256) chunk_count_kernel(const uint32_t* __rest
                                                           uint2* __restrict__ chunk_info, int dense_span,
                                                           Counters* __restrict__ ctr,
                                                           uint32_t* __restrict__ dense_list) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ uint32_t s_cnt[kMaxTileCols];
   __shared__ uint32_t s_tiles;
   const int tid = threadIdx.x;
@@ -599,6 +611,8 @@ __global__ void __launch_bounds__(256) chunk_count_kernel(const uint32_t* __rest
 __global__ void __launch_bounds__(256) tile_chunks_kernel(const uint32_t* __restrict__ chunk_start, int TH, int TW,
                                                           uint32_t* __restrict__ chunk_count,
                                                           uint32_t* __restrict__ tile_count) {
+  pdl_wait();
+  pdl_trigger();
   const int lane = threadIdx.x & 31;
   const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (t >= TW * TH) return;
@@ -625,6 +639,8 @@ __global__ void __launch_bounds__(256) tile_chunks_kernel(const uint32_t* __rest
 __global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restrict__ tile_count, int T,
                                                          Counters* __restrict__ ctr, uint32_t pair_cap,
                                                          uint2* __restrict__ ranges, Sticky* __restrict__ sticky) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ unsigned long long s_w[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int per = (T + 1023) / 1024;

@@ -48,6 +48,8 @@ __global__ void __launch_bounds__(256) compact_hist_kernel(const uint32_t* __res
                                                            Counters* __restrict__ ctr, uint32_t chunk,
                                                            uint32_t* __restrict__ hist,
                                                            uint32_t* __restrict__ lookback0) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int IT = kCompactKeys / 256;
   __shared__ uint32_t sh[4][4][256];  // 4 warp pairs x 4 digits
   __shared__ uint32_t s_wcnt[8], s_blk;
@@ -138,6 +140,8 @@ __global__ void __launch_bounds__(kSortThreads, 4) onesweep_kernel(
     uint32_t* __restrict__ vals_out, const uint32_t* __restrict__ n_ptr, uint32_t n_static,
     const uint32_t* __restrict__ pass_hist, uint32_t* __restrict__ lookback, uint32_t* __restrict__ lookback_next,
     uint32_t* __restrict__ ticket, int shift, int write_keys) {
+  pdl_wait();
+  pdl_trigger();
   constexpr uint32_t CHUNK = kSortThreads * ITEMS;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   OnesweepSmem<K, ITEMS>& S = *reinterpret_cast<OnesweepSmem<K, ITEMS>*>(smem_raw);
