@@ -36,7 +36,7 @@ static int pdl_mode() {  // RS_PDL (A/B measurements): bit 0 binning chain, bit 
   }();
   return m;
 }
-static int g_pdl_class = kPdlChain;  // class of the next launch() (set by the callers below)
+static thread_local int g_pdl_class = kPdlChain;  // class of the next launch() (set by the callers below)
 template <typename... KP, typename... A>
 static void launch(void (*k)(KP...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, A&&... args) {
   cudaLaunchConfig_t cfg{};
