@@ -62,7 +62,7 @@ struct Layout {
   // per-frame zeroed region [0, frame_bytes)
   size_t ctr, hist, proj_lb, ranges, frame_bytes;
   size_t sticky, cam, recs, sgrad, titem, keysA, keysB, valsA, valsB, rowtab, rowcnt, segitem, segspan, geom,
-      rowstart, chunkstart, chunkcnt, chunkinfo, densel, tilecnt, pitem, lbA, lbB, total;
+      rowstart, chunkstart, chunkcnt, chunkinfo, densel, tilecnt, tileord, pitem, lbA, lbB, total;
 };
 
 int tiles_x(int w) { return (w + kTile - 1) / kTile; }
@@ -107,6 +107,7 @@ Layout make_layout(int64_t n_cap, int64_t pair_cap, int W, int H) {
   L.chunkinfo = take((seg_cap / kExpandChunk + TH + 1) * 8);
   L.densel = take((seg_cap / kExpandChunk + TH + 1) * 4);
   L.tilecnt = take(TW * TH * 4);
+  L.tileord = take(TW * TH * 4);  // blend CTA -> tile, longest lists first
   L.pitem = take((size_t)pair_cap * 4);
   const size_t chunks = ((size_t)n_cap + kMinChunk - 1) / kMinChunk + 1;  // depth sort look-back
   L.lbA = take(chunks * 256 * 4);
@@ -388,7 +389,7 @@ int32_t rs_bin(rs_workspace* ws, void* stream) {
     launch(tile_chunks_kernel, (T + 7) / 8, 256, 0, st, ws->at<uint32_t>(ws->L.chunkstart), ws->TH, ws->TW,
            ws->at<uint32_t>(ws->L.chunkcnt), ws->at<uint32_t>(ws->L.tilecnt));
     launch(tile_scan_kernel, 1, 1024, 0, st, ws->at<uint32_t>(ws->L.tilecnt), T, ctr, (uint32_t)ws->pair_cap,
-           ws->at<uint2>(ws->L.ranges), ws->at<Sticky>(ws->L.sticky));
+           ws->at<uint2>(ws->L.ranges), ws->at<Sticky>(ws->L.sticky), ws->at<uint32_t>(ws->L.tileord));
     cudaEventRecord(ws->ev_fork, st);
     cudaStreamWaitEvent(ws->aux, ws->ev_fork, 0);
     g_pdl_class = kPdlExpand;
@@ -430,6 +431,7 @@ int32_t rs_blend_ex(rs_workspace* ws, const rs_options* opts, const rs_outputs* 
   const uint32_t* items = final_pair_items(ws);
   const Rec* recs = ws->at<Rec>(ws->L.recs);
   const float4* geom = ws->at<float4>(ws->L.geom);  // ellipse row geometry (warp quarter masks)
+  const uint32_t* order = ws->at<uint32_t>(ws->L.tileord);  // CTA -> tile (tile_scan_kernel)
   Counters* ctr = ws->ctr();
   g_pdl_class = kPdlBlend;
   struct Restore {
@@ -440,8 +442,8 @@ int32_t rs_blend_ex(rs_workspace* ws, const rs_options* opts, const rs_outputs* 
     launch(blend_kernel<C, I, K, F>, T, kBlendThreads, 0, st, ranges, items, recs, ctr, ws->W, ws->H,     \
            ws->TW, *opts, out, scores);                                                                    \
   else                                                                                                    \
-    launch(blend2_kernel<C, I, K, F>, T, kBlend2Threads, 0, st, ranges, items, recs, geom, ctr, ws->W,    \
-           ws->H, ws->TW, *opts, out, scores)
+    launch(blend2_kernel<C, I, K, F>, T, kBlend2Threads, 0, st, ranges, items, recs, geom, order, ctr,    \
+           ws->W, ws->H, ws->TW, *opts, out, scores)
 #define RS_BLEND_F(C, I, K) \
   if (fast) { RS_BLEND(C, I, K, true); } else { RS_BLEND(C, I, K, false); }
   // exact-range exp2 is only needed for degenerate options (see blend.cuh FAST)
@@ -449,14 +451,14 @@ int32_t rs_blend_ex(rs_workspace* ws, const rs_options* opts, const rs_outputs* 
   if (out.tau) {  // training forward (rasterize_cached): records tau and the last composite per pixel
     if (scores) {
       if (fast) launch(blend2_kernel<true, true, false, true, true>, T, kBlend2Threads, 0, st, ranges, items,
-                       recs, geom, ctr, ws->W, ws->H, ws->TW, *opts, out, scores);
+                       recs, geom, order, ctr, ws->W, ws->H, ws->TW, *opts, out, scores);
       else launch(blend2_kernel<true, true, false, false, true>, T, kBlend2Threads, 0, st, ranges, items, recs,
-                  geom, ctr, ws->W, ws->H, ws->TW, *opts, out, scores);
+                  geom, order, ctr, ws->W, ws->H, ws->TW, *opts, out, scores);
     } else {
       if (fast) launch(blend2_kernel<true, false, false, true, true>, T, kBlend2Threads, 0, st, ranges, items,
-                       recs, geom, ctr, ws->W, ws->H, ws->TW, *opts, out, scores);
+                       recs, geom, order, ctr, ws->W, ws->H, ws->TW, *opts, out, scores);
       else launch(blend2_kernel<true, false, false, false, true>, T, kBlend2Threads, 0, st, ranges, items, recs,
-                  geom, ctr, ws->W, ws->H, ws->TW, *opts, out, scores);
+                  geom, order, ctr, ws->W, ws->H, ws->TW, *opts, out, scores);
     }
   } else if (color && scores) {
     if (stats) { RS_BLEND_F(true, true, true); } else { RS_BLEND_F(true, true, false); }

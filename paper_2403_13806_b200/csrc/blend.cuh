@@ -253,8 +253,8 @@ template <bool COLOR, bool CONTRIB, bool STATS, bool FAST, bool TRAIN = false>
 #endif
 __global__ void __launch_bounds__(kBlend2Threads, RS_BLEND_MINB) blend2_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ pair_items, const Rec* __restrict__ recs,
-    const float4* __restrict__ geom, Counters* __restrict__ ctr, int W, int H, int TW, rs_options o,
-    const rs_outputs out, uint32_t* __restrict__ scores) {
+    const float4* __restrict__ geom, const uint32_t* __restrict__ tile_order, Counters* __restrict__ ctr, int W,
+    int H, int TW, rs_options o, const rs_outputs out, uint32_t* __restrict__ scores) {
   pdl_wait();
   pdl_trigger();
   constexpr int kBatch = 256;  // entries staged per batch (two per thread)
@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(kBlend2Threads, RS_BLEND_MINB) blend2_kernel(
   __shared__ uint8_t s_list[4][kBatch];    // per-warp compacted entry lists
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int tile = blockIdx.x;
+  const int tile = (int)__ldg(tile_order + blockIdx.x);  // longest tile lists first
   const int tx = tile % TW, ty = tile / TW;
   const int ox = tx * kTile, oy = ty * kTile;
   const int px = ox + (warp & 1) * 8 + (lane & 7);
