@@ -521,8 +521,8 @@ int32_t rs_backward(rs_workspace* ws, const rs_scene* scene, const int32_t* acti
   cudaMemsetAsync(ws->at<uint8_t>(ws->L.titem), 0, (size_t)items, st);
   auto* bwd = opts->alpha_cut >= 1e-30f ? backward2_kernel<true> : backward2_kernel<false>;
   launch(bwd, ws->TW * ws->TH, kBwd2Threads, 0, st, ws->at<uint2>(ws->L.ranges), final_pair_items(ws),
-         ws->at<Rec>(ws->L.recs), ws->at<float4>(ws->L.geom), ws->ctr(), ws->W, ws->H, ws->TW, *opts,
-         grad_image, tau, last, ws->at<float>(ws->L.sgrad), ws->at<uint8_t>(ws->L.titem));
+         ws->at<Rec>(ws->L.recs), ws->at<float4>(ws->L.geom), ws->at<uint32_t>(ws->L.tileord), ws->ctr(), ws->W,
+         ws->H, ws->TW, *opts, grad_image, tau, last, ws->at<float>(ws->L.sgrad), ws->at<uint8_t>(ws->L.titem));
   launch(chain_kernel, (unsigned)((items + 127) / 128), 128, 0, st, scene->planes, scene->sh,
          scene->plane_stride, scene->sh_degree, active_idx, (uint32_t)items, ws->at<rs_camera>(ws->L.cam),
          *opts, ws->at<float>(ws->L.sgrad), ws->at<uint8_t>(ws->L.titem), g_pos, g_sh, g_ls, g_quat, g_logit,

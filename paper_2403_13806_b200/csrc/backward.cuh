@@ -42,8 +42,8 @@ constexpr int kBwd2Threads = 128;
 template <bool FAST>
 __global__ void __launch_bounds__(kBwd2Threads) backward2_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ pair_items, const Rec* __restrict__ recs,
-    const float4* __restrict__ geom, const Counters* __restrict__ ctr, int W, int H, int TW, rs_options o,
-    const float* __restrict__ grad_image, const float* __restrict__ tau_final, const int32_t* __restrict__ last,
+    const float4* __restrict__ geom, const uint32_t* __restrict__ tile_order, const Counters* __restrict__ ctr,
+    int W, int H, int TW, rs_options o, const float* __restrict__ grad_image, const float* __restrict__ tau_final, const int32_t* __restrict__ last,
     float* __restrict__ sgrad, uint8_t* __restrict__ touched) {
   pdl_wait();
   pdl_trigger();
@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(kBwd2Threads) backward2_kernel(
   __shared__ uint8_t s_list[4][kBatch];
   __shared__ int s_maxlast[4];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int tile = blockIdx.x;
+  const int tile = (int)__ldg(tile_order + blockIdx.x);  // longest tile lists first
   const int tx = tile % TW, ty = tile / TW;
   const int ox = tx * kTile, oy = ty * kTile;
   const int px = ox + (warp & 1) * 8 + (lane & 7);
