@@ -634,6 +634,13 @@ __global__ void __launch_bounds__(256) tile_chunks_kernel(const uint32_t* __rest
   if (lane == 0) tile_count[t] = carry;
 }
 
+// Class of a tile's list length for the blend order: floor(log2 v) and the next two bits.
+__device__ __forceinline__ int len_class(uint32_t v) {
+  if (v < 4) return (int)v;
+  const int e = 31 - __clz(v);
+  return 4 * (e - 1) + (int)((v >> (e - 2)) & 3u);
+}
+
 // One CTA: exclusive scan of the tile counts (row-major tile ids) -> ranges (empty tiles
 // [0, 0)), P and the overflow verdict. Thread t owns ceil(T / 1024) consecutive tiles.
 __global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restrict__ tile_count, int T,
@@ -643,7 +650,8 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restr
   pdl_wait();
   pdl_trigger();
   __shared__ unsigned long long s_w[32];
-  __shared__ uint32_t s_bucket[33], s_cursor[33];
+  constexpr int kClasses = 33 * 4;  // log2 of the list length, quartered
+  __shared__ uint32_t s_bucket[kClasses], s_cursor[kClasses];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int per = (T + 1023) / 1024;
   const int t0 = min(tid * per, T), t1 = min(t0 + per, T);
@@ -679,7 +687,7 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restr
   }
   __syncthreads();
   unsigned long long st = s_w[warp] + x - sum;
-  if (tid < 33) s_bucket[tid] = 0;
+  if (tid < kClasses) s_bucket[tid] = 0;
   __syncthreads();
   for (int t = t0; t < t1; ++t) {
     const unsigned long long v = tile_count[t];
@@ -687,18 +695,18 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restr
                                (uint32_t)min(st + v, (unsigned long long)pair_cap))
                   : make_uint2(0u, 0u);
     st += v;
-    atomicAdd(&s_bucket[32 - __clz((uint32_t)v)], 1u);  // log2 class of the tile's list length
+    atomicAdd(&s_bucket[len_class((uint32_t)v)], 1u);
   }
   __syncthreads();
   if (tid == 0) {  // blend order: longest lists first (the last wave of CTAs holds the short ones)
     uint32_t run = 0;
-    for (int b = 32; b >= 0; --b) {
+    for (int b = kClasses - 1; b >= 0; --b) {
       s_cursor[b] = run;
       run += s_bucket[b];
     }
   }
   __syncthreads();
-  for (int t = t0; t < t1; ++t) tile_order[atomicAdd(&s_cursor[32 - __clz(tile_count[t])], 1u)] = (uint32_t)t;
+  for (int t = t0; t < t1; ++t) tile_order[atomicAdd(&s_cursor[len_class(tile_count[t])], 1u)] = (uint32_t)t;
 }
 
 }  // namespace rs
