@@ -14,7 +14,7 @@
 // ellipses) with explicit slack for the rounding (oracle/cpu_ref.cpp:row_geom);
 // IEEE operations in the oracle's fixed order, so the binning is bit-exact.
 // On configs[1] this lists 19% fewer (tile, Gaussian) pairs than the
-// rectangles, 44% fewer on the anisotropic configs[4]. Used by segemit_kernel.
+// rectangles, 44% fewer on the anisotropic configs[4]. Used by segplace_kernel.
 #pragma once
 #include "rs_common.cuh"
 
@@ -62,7 +62,7 @@ __device__ __forceinline__ float row_edge(const RowGeom& g, int y) { return __fs
 // Pixel columns [px0, px1) of an ellipse strip from its edge offsets and edge terms
 // (slo = edge_s(ulo), shi = edge_s(uhi)); identical to oracle row_span: the clamped dyr /
 // -dyr is one of lo, hi, +-dyr and the boundary term there is slo, shi or sd. Holds for any
-// strip of pixel rows (segemit also takes the two 8-row halves of a tile row).
+// strip of pixel rows (the blend also takes the two 8-row halves of a tile row).
 __device__ __forceinline__ bool row_px_e(const RowGeom& g, const int4 cb, float ulo, float uhi, float slo, float shi,
                                          int& px0, int& px1) {
   const float lo = fmaxf(ulo, -g.hy), hi = fminf(uhi, g.hy);
@@ -94,7 +94,7 @@ __device__ __forceinline__ bool row_span(const RowGeom& g, const int4 cb, int ty
   return row_span_e(g, cb, ulo, uhi, edge_s(g, ulo), edge_s(g, uhi), tx0, tx1);
 }
 
-// RowGeom without the mean, as two float4 per Gaussian (segemit_kernel -> blend2_kernel).
+// RowGeom without the mean, as two float4 per Gaussian (segplace_kernel -> blend2_kernel, backward2_kernel).
 __device__ __forceinline__ void store_row_geom(float4* dst, const RowGeom& g) {
   dst[0] = make_float4(g.hy, g.dyr, g.ak4, g.d);
   dst[1] = make_float4(g.bi, g.i2a, g.del, g.sd);

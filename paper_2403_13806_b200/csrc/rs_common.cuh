@@ -53,13 +53,12 @@ struct Counters {
   unsigned long long evals, composites;
   unsigned long long pairs_needed;                 // true P (sizing hint after overflow)
   uint32_t tickets[12];  // onesweep chunk tickets, one per pass
-  uint32_t emit_ctr;     // decoupled look-back ticket of the pair counter
-  uint32_t emit_work;    // rank-chunk work counter of the pair emitter
-  uint32_t proj_ticket;  // logical block ticket of the projection's compaction
+  uint32_t spare0, spare1;
+  uint32_t proj_ticket;  // logical block ticket of the depth-key compaction
   uint32_t n_segs;       // row segments of the binned items (segbin.cuh)
   uint32_t n_dense;      // dense expansion chunks listed by chunk_count_kernel
   uint32_t dense_work;   // (dense chunk, column group) tickets of expand_dense_kernel
-  uint32_t emit_done;    // finished segemit CTAs (the last one scans the row counts)
+  uint32_t emit_done;    // finished segscan CTAs (the last one scans the row totals)
   uint32_t pad[3];
 };
 static_assert(sizeof(Counters) == 128, "Counters is 128 B");
