@@ -739,14 +739,10 @@ def profiled_traffic(kernel: str):
 
 
 def frame_launches(W, H):
-    """Kernels per frame: project, depth compaction+histogram, 4 depth passes, segment
-    count, segment emission, the segment row passes, chunk count (with the row scan), tile
-    chunks, tile scan, expansion (sparse and dense chunks), blend."""
-    return 1 + 1 + 4 + 1 + 1 + row_passes(H) + 1 + 1 + 1 + 2 + 1
-
-
-def row_passes(H):
-    return 1 if (H + 15) // 16 <= 256 else 2
+    """Kernels per frame (image size independent): project, depth-key compaction + histograms,
+    4 depth passes, segment rows / scan / placement, chunk count, tile chunks, tile scan (ranges
+    + blend order), expansion (sparse and dense chunks), blend."""
+    return 1 + 1 + 4 + 3 + 1 + 1 + 1 + 2 + 1
 
 
 if __name__ == "__main__":
