@@ -258,10 +258,12 @@ __global__ void __launch_bounds__(kBlend2Threads, RS_BLEND_MINB) blend2_kernel(
   pdl_wait();
   pdl_trigger();
   constexpr int kBatch = 256;  // entries staged per batch (two per thread)
-  __shared__ Rec s_rec[kBatch];
-  __shared__ uint32_t s_w[CONTRIB ? kBatch : 1];
-  __shared__ uint8_t s_mask[kBatch];       // which warps' 8x8 sub-rectangles the entry touches
-  __shared__ uint8_t s_list[4][kBatch];    // per-warp compacted entry lists
+  constexpr int U = kBlendUnroll;
+  // slot kBatch: an empty-box sentinel that pads every warp list to a multiple of U entries
+  __shared__ Rec s_rec[kBatch + 1];
+  __shared__ uint32_t s_w[CONTRIB ? kBatch + 1 : 1];
+  __shared__ uint8_t s_mask[kBatch];             // which warps' 8x8 sub-rectangles the entry touches
+  __shared__ uint16_t s_list[4][kBatch + U];     // per-warp compacted entry lists (+ sentinel pad)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int tile = (int)__ldg(tile_order + blockIdx.x);  // longest tile lists first
@@ -283,6 +285,13 @@ __global__ void __launch_bounds__(kBlend2Threads, RS_BLEND_MINB) blend2_kernel(
   int cnt0 = 0, cnt1 = 0;
   int last0 = -1, last1 = -1;  // pair index of each pixel's last composite (training outputs)
   unsigned long long evals = 0;
+  if (tid == 0) {
+    s_rec[kBatch].a = make_float4(0.f, 0.f, 0.f, 0.f);
+    s_rec[kBatch].b = make_float4(0.f, 0.f, 0.f, 0.f);
+    s_rec[kBatch].c = make_float4(0.f, 0.f, 0.f, 0.f);
+    s_rec[kBatch].d = make_int4(0, 0, 0, 0);  // empty box: never evaluated
+    if (CONTRIB) s_w[kBatch] = 0u;
+  }
   const bool start = 1.0f >= o.tau_stop;
   bool done0 = !in0 || !start, done1 = !in1 || !start;
 
@@ -330,9 +339,10 @@ __global__ void __launch_bounds__(kBlend2Threads, RS_BLEND_MINB) blend2_kernel(
         const int e = c0 + lane;
         const bool has = e < n && ((s_mask[e] >> warp) & 1u);
         const unsigned bal = __ballot_sync(0xffffffffu, has);
-        if (has) s_list[warp][cntw + __popc(bal & lt)] = (uint8_t)e;
+        if (has) s_list[warp][cntw + __popc(bal & lt)] = (uint16_t)e;
         cntw += __popc(bal);
       }
+      if (lane < U) s_list[warp][cntw + lane] = (uint16_t)kBatch;
       __syncwarp();
       // kBlendUnroll entries per iteration: all their coverage and alpha math (independent of
       // the transmittance) first, then the composites in list order -- independent dependency
@@ -340,11 +350,10 @@ __global__ void __launch_bounds__(kBlend2Threads, RS_BLEND_MINB) blend2_kernel(
       // computed for a pixel that is not composited are discarded by the selects, so the
       // decisions and results are exactly those of blend_px (the FAST exp2 is exact on
       // [-126, 127] and only p2 >= cut2 >= -126 is ever used).
-      constexpr int U = kBlendUnroll;
       for (int q = 0; q < cntw; q += U) {
         int ent[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) ent[u] = s_list[warp][min(q + u, cntw - 1)];
+        for (int u = 0; u < U; ++u) ent[u] = s_list[warp][q + u];
         // the two pixels (rows py0, py1) in packed fp32 pairs: every FADD2/FMUL2/FFMA2 below is
         // the scalar contract's operation on both pixels at once (f32x2.cuh)
         f2 al[U];
@@ -354,7 +363,7 @@ __global__ void __launch_bounds__(kBlend2Threads, RS_BLEND_MINB) blend2_kernel(
           const Rec& E = s_rec[ent[u]];
           const int4 bb = E.d;
           const float4 ga = E.a, gb = E.b;
-          const bool inx = px >= bb.x && px < bb.y && q + u < cntw;
+          const bool inx = px >= bb.x && px < bb.y;
           box[u][0] = inx && py0 >= bb.z && py0 < bb.w;
           box[u][1] = inx && py1 >= bb.z && py1 < bb.w;
           const float dx = __fsub_rn(xs, ga.x);
@@ -423,7 +432,7 @@ __global__ void __launch_bounds__(kBlend2Threads, RS_BLEND_MINB) blend2_kernel(
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             const uint32_t wm = __reduce_max_sync(0xffffffffu, __float_as_uint(wmax[u]));
-            if (lane == 0 && wm && q + u < cntw) atomicMax(&s_w[ent[u]], wm);
+            if (lane == 0 && wm) atomicMax(&s_w[ent[u]], wm);
           }
         }
         if (__all_sync(0xffffffffu, done0 && done1)) break;  // all 64 pixels of the warp terminated
