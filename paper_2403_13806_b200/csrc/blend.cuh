@@ -401,19 +401,34 @@ __global__ void __launch_bounds__(kBlend2Threads, RS_BLEND_MINB) blend2_kernel(
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const Rec& E = s_rec[ent[u]];
-          if (STATS) evals += (unsigned)(box[u][0] && !done0) + (unsigned)(box[u][1] && !done1);
-          const bool c0 = ok[u][0] && !done0, c1 = ok[u][1] && !done1;
-          const f2 wt = f2_mul(al[u], tau);
-          const float w0 = c0 ? f2_lo(wt) : 0.0f, w1 = c1 ? f2_hi(wt) : 0.0f;
+          // a pixel composites iff tau_before >= tau_stop (render.py:261); out-of-image pixels
+          // never pass the box test. Colour frames take a non-compositing pixel's alpha as 0
+          // (w = 0 * tau = +0, tau * (1 - 0) = tau: exactly the skipped composite, fewer
+          // selects); score-only frames select the products instead (a shorter dependency
+          // chain through tau, which their lighter loop cannot hide)
+          const bool live0 = COLOR ? f2_lo(tau) >= o.tau_stop : !done0;
+          const bool live1 = COLOR ? f2_hi(tau) >= o.tau_stop : !done1;
+          if (STATS) evals += (unsigned)(box[u][0] && live0 && in0) + (unsigned)(box[u][1] && live1 && in1);
+          const bool c0 = ok[u][0] && live0, c1 = ok[u][1] && live1;
+          f2 wt;
           if (COLOR) {
-            // fma(c, +0, acc) = acc for the pixel that does not composite (c, z finite, acc >= +0)
+            const f2 ae = f2_pack(c0 ? f2_lo(al[u]) : 0.0f, c1 ? f2_hi(al[u]) : 0.0f);
+            wt = f2_mul(ae, tau);
             const float4 gc = E.c;
-            const f2 w = f2_pack(w0, w1);
-            rgb[0] = f2_fma(f2_splat(gc.x), w, rgb[0]);
-            rgb[1] = f2_fma(f2_splat(gc.y), w, rgb[1]);
-            rgb[2] = f2_fma(f2_splat(gc.z), w, rgb[2]);
-            dep = f2_fma(f2_splat(E.b.w), w, dep);
+            rgb[0] = f2_fma(f2_splat(gc.x), wt, rgb[0]);
+            rgb[1] = f2_fma(f2_splat(gc.y), wt, rgb[1]);
+            rgb[2] = f2_fma(f2_splat(gc.z), wt, rgb[2]);
+            dep = f2_fma(f2_splat(E.b.w), wt, dep);
+            tau = f2_mul(tau, f2_sub(f2_splat(1.0f), ae));
+          } else {
+            const f2 wp = f2_mul(al[u], tau);
+            wt = f2_pack(c0 ? f2_lo(wp) : 0.0f, c1 ? f2_hi(wp) : 0.0f);
+            const f2 tn = f2_mul(tau, f2_sub(f2_splat(1.0f), al[u]));
+            tau = f2_pack(c0 ? f2_lo(tn) : f2_lo(tau), c1 ? f2_hi(tn) : f2_hi(tau));
+            done0 = done0 || f2_lo(tau) < o.tau_stop;
+            done1 = done1 || f2_hi(tau) < o.tau_stop;
           }
+          const float w0 = f2_lo(wt), w1 = f2_hi(wt);
           cnt0 += c0 ? 1 : 0;
           cnt1 += c1 ? 1 : 0;
           if (TRAIN) {
@@ -421,11 +436,6 @@ __global__ void __launch_bounds__(kBlend2Threads, RS_BLEND_MINB) blend2_kernel(
             last0 = c0 ? k : last0;
             last1 = c1 ? k : last1;
           }
-          const f2 tn = f2_mul(tau, f2_sub(f2_splat(1.0f), al[u]));
-          const float tau0 = c0 ? f2_lo(tn) : f2_lo(tau), tau1 = c1 ? f2_hi(tn) : f2_hi(tau);
-          tau = f2_pack(tau0, tau1);
-          done0 = done0 || tau0 < o.tau_stop;
-          done1 = done1 || tau1 < o.tau_stop;
           wmax[u] = fmaxf(w0, w1);
         }
         if (CONTRIB) {
@@ -434,6 +444,10 @@ __global__ void __launch_bounds__(kBlend2Threads, RS_BLEND_MINB) blend2_kernel(
             const uint32_t wm = __reduce_max_sync(0xffffffffu, __float_as_uint(wmax[u]));
             if (lane == 0 && wm) atomicMax(&s_w[ent[u]], wm);
           }
+        }
+        if (COLOR) {
+          done0 = !in0 || f2_lo(tau) < o.tau_stop;
+          done1 = !in1 || f2_hi(tau) < o.tau_stop;
         }
         if (__all_sync(0xffffffffu, done0 && done1)) break;  // all 64 pixels of the warp terminated
       }
