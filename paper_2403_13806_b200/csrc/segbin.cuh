@@ -698,11 +698,27 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restr
     atomicAdd(&s_bucket[len_class((uint32_t)v)], 1u);
   }
   __syncthreads();
-  if (tid == 0) {  // blend order: longest lists first (the last wave of CTAs holds the short ones)
-    uint32_t run = 0;
-    for (int b = kClasses - 1; b >= 0; --b) {
-      s_cursor[b] = run;
-      run += s_bucket[b];
+  if (warp == 0) {  // blend order: longest lists first (the last wave of CTAs holds the short ones)
+    constexpr int kPer = (kClasses + 31) / 32;  // classes per lane, descending
+    uint32_t v[kPer], sum = 0;
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      const int b = kClasses - 1 - (lane * kPer + q);
+      v[q] = b >= 0 ? s_bucket[b] : 0u;
+      sum += v[q];
+    }
+    uint32_t x = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    uint32_t run = x - sum;
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      const int b = kClasses - 1 - (lane * kPer + q);
+      if (b >= 0) s_cursor[b] = run;
+      run += v[q];
     }
   }
   __syncthreads();
