@@ -439,11 +439,17 @@ __global__ void __launch_bounds__(kBlend2Threads, RS_BLEND_MINB) blend2_kernel(
           wmax[u] = fmaxf(w0, w1);
         }
         if (CONTRIB) {
+          // the group's U warp maxima, lane u folding entry u's into the batch slot: one
+          // shared atomic instruction per group instead of U
+          uint32_t mine = 0;
+          int slot = 0;
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             const uint32_t wm = __reduce_max_sync(0xffffffffu, __float_as_uint(wmax[u]));
-            if (lane == 0 && wm) atomicMax(&s_w[ent[u]], wm);
+            mine = lane == u ? wm : mine;
+            slot = lane == u ? ent[u] : slot;
           }
+          if (mine) atomicMax(&s_w[slot], mine);
         }
         if (COLOR) {
           done0 = !in0 || f2_lo(tau) < o.tau_stop;
