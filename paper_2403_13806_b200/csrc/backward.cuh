@@ -178,7 +178,8 @@ __global__ void __launch_bounds__(kBwd2Threads) backward2_kernel(
         if (cand[j] && p2v[j] >= gb4.z && alpha >= o.alpha_cut) {  // composited in the forward pass
           comp = true;
           const float dy = dyv[j];
-          const float rom = __frcp_rn(__fsub_rn(1.0f, alpha));
+          float rom;  // 1 / (1 - alpha), alpha <= alpha_max < 1: the hardware reciprocal (tolerance path)
+          asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rom) : "f"(__fsub_rn(1.0f, alpha)));
           const float tb = __fmul_rn(tau[j], rom);
           const float w = __fmul_rn(alpha, tb);
           const float cdot = __fadd_rn(__fadd_rn(__fmul_rn(gc.x, gcol[j][0]), __fmul_rn(gc.y, gcol[j][1])),
