@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(kBwd2Threads) backward2_kernel(
   const uint2 rg = ranges[tile];
   const uint32_t end = min(rg.y, ctr->n_pairs);
   const uint32_t lt = (1u << lane) - 1u;
-  float tau[2] = {1.0f, 1.0f}, gcol[2][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}}, suffix[2] = {0.0f, 0.0f};
+  float tau[2] = {1.0f, 1.0f}, gcol[2][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
   int lastk[2] = {-1, -1};
   const bool inside[2] = {in0, in1};
   const int pyv[2] = {py0, py1};
@@ -80,6 +80,10 @@ __global__ void __launch_bounds__(kBwd2Threads) backward2_kernel(
       gcol[j][1] = grad_image[3 * p + 1];
       gcol[j][2] = grad_image[3 * p + 2];
     }
+  // the two pixels' state as packed pairs {py0, py1}
+  f2 tau2 = f2_pack(tau[0], tau[1]), suffix2 = f2_splat(0.0f);
+  const f2 gcol2[3] = {f2_pack(gcol[0][0], gcol[1][0]), f2_pack(gcol[0][1], gcol[1][1]),
+                       f2_pack(gcol[0][2], gcol[1][2])};
   // entries after every pixel's last composite are skipped wholesale
   int maxlast = max(lastk[0], lastk[1]);
 #pragma unroll
@@ -165,41 +169,46 @@ __global__ void __launch_bounds__(kBwd2Threads) backward2_kernel(
         ex = f2_pack(exp2_contract(fminf(p20, 127.0f)), exp2_contract(fminf(p21, 127.0f)));
       }
       const f2 raw2 = f2_mul(f2_splat(gb4.y), ex);
-      const float raw[2] = {f2_lo(raw2), f2_hi(raw2)};
-      const float p2v[2] = {p20, p21};
-      const bool cand[2] = {cand0, cand1};
-      const float dyv[2] = {__fsub_rn(__fadd_rn((float)py0, 0.5f), ga.y), __fsub_rn(__fadd_rn((float)py1, 0.5f), ga.y)};
-      const float4 gc = E.c;
-      float v[kSGrad] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-      bool comp = false;
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const float alpha = fminf(raw[j], o.alpha_max);
-        if (cand[j] && p2v[j] >= gb4.z && alpha >= o.alpha_cut) {  // composited in the forward pass
-          comp = true;
-          const float dy = dyv[j];
-          float rom;  // 1 / (1 - alpha), alpha <= alpha_max < 1: the hardware reciprocal (tolerance path)
-          asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rom) : "f"(__fsub_rn(1.0f, alpha)));
-          const float tb = __fmul_rn(tau[j], rom);
-          const float w = __fmul_rn(alpha, tb);
-          const float cdot = __fadd_rn(__fadd_rn(__fmul_rn(gc.x, gcol[j][0]), __fmul_rn(gc.y, gcol[j][1])),
-                                       __fmul_rn(gc.z, gcol[j][2]));
-          v[0] += __fmul_rn(w, gcol[j][0]);
-          v[1] += __fmul_rn(w, gcol[j][1]);
-          v[2] += __fmul_rn(w, gcol[j][2]);
-          const float da = raw[j] > o.alpha_max ? 0.0f : __fsub_rn(__fmul_rn(tb, cdot), __fmul_rn(suffix[j], rom));
-          v[3] += __fmul_rn(da, alpha);
-          const float dq = __fmul_rn(__fmul_rn(-0.5f, alpha), da);
-          v[4] += __fmul_rn(dq, dx);
-          v[5] += __fmul_rn(dq, dy);
-          v[6] += __fmul_rn(dq, __fmul_rn(dx, dx));
-          v[7] += __fmul_rn(dq, __fmul_rn(__fmul_rn(2.0f, dy), dx));
-          v[8] += __fmul_rn(dq, __fmul_rn(dy, dy));
-          suffix[j] = __fadd_rn(suffix[j], __fmul_rn(w, cdot));
-          tau[j] = tb;
-        }
-      }
+      const float a0 = fminf(f2_lo(raw2), o.alpha_max), a1 = fminf(f2_hi(raw2), o.alpha_max);
+      // composited in the forward pass (same decisions as blend2_kernel)
+      const bool c0 = cand0 && p20 >= gb4.z && a0 >= o.alpha_cut;
+      const bool c1 = cand1 && p21 >= gb4.z && a1 >= o.alpha_cut;
+      const bool comp = c0 || c1;
+      float v[kSGrad];
       if (__any_sync(0xffffffffu, comp)) {
+        // both pixels' gradient terms as packed pairs (tolerance path: fp32, any association)
+        // a pixel that did not composite gets alpha 0 (its p2 may lie outside the exp2 core's
+        // exact range: garbage there must not reach the sums)
+        const f2 al = f2_pack(c0 ? a0 : 0.0f, c1 ? a1 : 0.0f);
+        const f2 om = f2_sub(f2_splat(1.0f), al);
+        float r0, r1;  // 1 / (1 - alpha), alpha <= alpha_max < 1: the hardware reciprocal
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r0) : "f"(f2_lo(om)));
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r1) : "f"(f2_hi(om)));
+        const f2 rom = f2_pack(r0, r1);
+        const f2 tb = f2_mul(tau2, rom);
+        const f2 w = f2_mul(al, tb);
+        const float4 gc = E.c;
+        const f2 cdot = f2_fma(f2_splat(gc.z), gcol2[2], f2_fma(f2_splat(gc.y), gcol2[1], f2_mul(f2_splat(gc.x), gcol2[0])));
+        const f2 wg0 = f2_mul(w, gcol2[0]), wg1 = f2_mul(w, gcol2[1]), wg2 = f2_mul(w, gcol2[2]);
+        v[0] = f2_lo(wg0) + f2_hi(wg0);
+        v[1] = f2_lo(wg1) + f2_hi(wg1);
+        v[2] = f2_lo(wg2) + f2_hi(wg2);
+        const f2 dar = f2_sub(f2_mul(tb, cdot), f2_mul(suffix2, rom));
+        // d_alpha (0 where alpha was clamped at alpha_max, or no composite)
+        const f2 da = f2_pack(c0 && f2_lo(raw2) <= o.alpha_max ? f2_lo(dar) : 0.0f,
+                              c1 && f2_hi(raw2) <= o.alpha_max ? f2_hi(dar) : 0.0f);
+        const f2 daa = f2_mul(da, al);
+        v[3] = f2_lo(daa) + f2_hi(daa);
+        const f2 dq = f2_mul(f2_mul(f2_splat(-0.5f), al), da);
+        const f2 dqy = f2_mul(dq, dy2), dqyy = f2_mul(dqy, dy2);
+        const float sdq = f2_lo(dq) + f2_hi(dq), sdqy = f2_lo(dqy) + f2_hi(dqy);
+        v[4] = sdq * dx;
+        v[5] = sdqy;
+        v[6] = sdq * (dx * dx);
+        v[7] = 2.0f * dx * sdqy;
+        v[8] = f2_lo(dqyy) + f2_hi(dqyy);
+        suffix2 = f2_fma(w, cdot, suffix2);
+        tau2 = f2_pack(c0 ? f2_lo(tb) : f2_lo(tau2), c1 ? f2_hi(tb) : f2_hi(tau2));
         // reduce-scatter of v[0..7] (4 + 2 + 1 + 1 + 1 shuffles), v[8] by a butterfly
         const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
         float w4[4];
