@@ -509,13 +509,15 @@ int32_t rs_backward(rs_workspace* ws, const rs_scene* scene, const int32_t* acti
   if (items != (int64_t)ws->n_items) return RS_EINVAL;  // not the frame rs_render_ex just produced
   cudaStream_t st = S(stream);
   const int64_t n = scene->n;
-  cudaMemsetAsync(g_pos, 0, (size_t)n * 12, st);
-  cudaMemsetAsync(g_sh, 0, (size_t)n * 192, st);
-  cudaMemsetAsync(g_ls, 0, (size_t)n * 12, st);
-  cudaMemsetAsync(g_quat, 0, (size_t)n * 16, st);
-  cudaMemsetAsync(g_logit, 0, (size_t)n * 4, st);
-  cudaMemsetAsync(g_mean2d, 0, (size_t)n * 4, st);
-  cudaMemsetAsync(touched, 0, (size_t)n, st);
+  if (active_idx || items == 0) {  // Gaussians outside the list keep zero gradients; else
+    cudaMemsetAsync(g_pos, 0, (size_t)n * 12, st);  // chain_kernel writes every item's
+    cudaMemsetAsync(g_sh, 0, (size_t)n * 192, st);
+    cudaMemsetAsync(g_ls, 0, (size_t)n * 12, st);
+    cudaMemsetAsync(g_quat, 0, (size_t)n * 16, st);
+    cudaMemsetAsync(g_logit, 0, (size_t)n * 4, st);
+    cudaMemsetAsync(g_mean2d, 0, (size_t)n * 4, st);
+    cudaMemsetAsync(touched, 0, (size_t)n, st);
+  }
   if (items == 0) return cuda_status();
   cudaMemsetAsync(ws->at<float>(ws->L.sgrad), 0, (size_t)items * 4 * kSGrad, st);
   cudaMemsetAsync(ws->at<uint8_t>(ws->L.titem), 0, (size_t)items, st);

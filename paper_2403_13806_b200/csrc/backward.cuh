@@ -260,9 +260,26 @@ __global__ void __launch_bounds__(128) chain_kernel(
   pdl_wait();
   pdl_trigger();
   const uint32_t item = blockIdx.x * blockDim.x + threadIdx.x;
-  if (item >= n_items || !touched[item]) return;
-  const rs_camera cam = *camp;
+  if (item >= n_items) return;
   const int64_t i = active_idx ? (int64_t)active_idx[item] : (int64_t)item;
+  if (!touched[item]) {
+    if (!active_idx) {  // every item covered here: its zero gradients too (no memset pass)
+      for (int k = 0; k < 3; ++k) g_pos[3 * i + k] = 0.0f;
+      if ((reinterpret_cast<uintptr_t>(g_sh) & 15) == 0) {
+        float4* gs = reinterpret_cast<float4*>(g_sh + 48 * i);
+        for (int k = 0; k < 12; ++k) gs[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+      } else {
+        for (int k = 0; k < 48; ++k) g_sh[48 * i + k] = 0.0f;
+      }
+      for (int k = 0; k < 3; ++k) g_ls[3 * i + k] = 0.0f;
+      for (int k = 0; k < 4; ++k) g_quat[4 * i + k] = 0.0f;
+      g_logit[i] = 0.0f;
+      g_mean2d[i] = 0.0f;
+      touched_out[i] = 0;
+    }
+    return;
+  }
+  const rs_camera cam = *camp;
   const float* P = planes + i;
   const float* S = sgrad + (size_t)kSGrad * item;
   const float p[3] = {P[0], P[stride], P[2 * stride]};
