@@ -689,13 +689,20 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restr
   unsigned long long st = s_w[warp] + x - sum;
   if (tid < kClasses) s_bucket[tid] = 0;
   __syncthreads();
-  for (int t = t0; t < t1; ++t) {
-    const unsigned long long v = tile_count[t];
-    ranges[t] = v ? make_uint2((uint32_t)min(st, (unsigned long long)pair_cap),
-                               (uint32_t)min(st + v, (unsigned long long)pair_cap))
-                  : make_uint2(0u, 0u);
-    st += v;
-    atomicAdd(&s_bucket[len_class((uint32_t)v)], 1u);
+  for (int k = 0; k < per; ++k) {  // every lane iterates: the class counts are warp-aggregated
+    const int t = t0 + k;
+    const unsigned long long v = t < t1 ? tile_count[t] : 0ull;
+    if (t < t1) {
+      ranges[t] = v ? make_uint2((uint32_t)min(st, (unsigned long long)pair_cap),
+                                 (uint32_t)min(st + v, (unsigned long long)pair_cap))
+                    : make_uint2(0u, 0u);
+      st += v;
+    }
+    // empty tiles (most of a sparse frame: one class, per-tile atomics would serialise) are
+    // counted per warp
+    const uint32_t empties = __ballot_sync(0xffffffffu, t < t1 && v == 0);
+    if (lane == 0 && empties) atomicAdd(&s_bucket[0], (uint32_t)__popc(empties));
+    if (t < t1 && v) atomicAdd(&s_bucket[len_class((uint32_t)v)], 1u);
   }
   __syncthreads();
   if (warp == 0) {  // blend order: longest lists first (the last wave of CTAs holds the short ones)
@@ -722,7 +729,17 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restr
     }
   }
   __syncthreads();
-  for (int t = t0; t < t1; ++t) tile_order[atomicAdd(&s_cursor[len_class(tile_count[t])], 1u)] = (uint32_t)t;
+  const uint32_t lt = (1u << lane) - 1u;
+  for (int k = 0; k < per; ++k) {
+    const int t = t0 + k;
+    const uint32_t v = t < t1 ? tile_count[t] : 0u;
+    const uint32_t empties = __ballot_sync(0xffffffffu, t < t1 && v == 0);
+    uint32_t base = 0;
+    if (lane == 0 && empties) base = atomicAdd(&s_cursor[0], (uint32_t)__popc(empties));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (t < t1)
+      tile_order[v ? atomicAdd(&s_cursor[len_class(v)], 1u) : base + __popc(empties & lt)] = (uint32_t)t;
+  }
 }
 
 }  // namespace rs

@@ -1,5 +1,5 @@
 """ncu driver: configs[3]-sized filtered frames (1920x1080, a 1.7k-Gaussian index list of the
-6M house scene: the Gaussians nearest the trajectory's first camera centre) and unfiltered ones.
+6M house scene: a random 1.7k subset) and unfiltered ones.
 
     python tools/profile_house.py [filtered|unfiltered] [frames]
 """
@@ -14,7 +14,6 @@ import torch  # noqa: E402
 from paper_2403_13806_b200 import synth  # noqa: E402
 from paper_2403_13806_b200.device import device_scene, renderer  # noqa: E402
 from paper_2403_13806_b200.render import RasterizeOptions  # noqa: E402
-from paper_2403_13806_b200.visibility import _center  # noqa: E402
 
 
 def main():
@@ -25,10 +24,9 @@ def main():
     ds = device_scene(scene)
     r = renderer(ds.device)
     idx = None
-    if kind == "filtered":
-        pos = np.asarray(scene.positions)
-        d2 = ((pos - _center(traj[0])[None, :]) ** 2).sum(1)
-        idx = torch.from_numpy(np.sort(np.argpartition(d2, 1700)[:1700]).astype(np.int32)).to(ds.device)
+    if kind == "filtered":  # 1.7k random Gaussians (the config rule's list size)
+        pick = np.random.default_rng(0).choice(len(scene), 1700, replace=False)
+        idx = torch.from_numpy(np.sort(pick).astype(np.int32)).to(ds.device)
     out = r.alloc_outputs(traj[0])
     for f in range(frames):
         _, st = r.render(ds, traj[f], opts, out=out, active_idx=idx)
