@@ -163,7 +163,10 @@ cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 int32_t cuda_status() { return cudaGetLastError() == cudaSuccess ? RS_OK : RS_ECUDA; }
 
-constexpr int kDepthItems = 8;   // 2048-key chunks: more CTAs for the small depth sort
+#ifndef RS_DEPTH_ITEMS
+#define RS_DEPTH_ITEMS 8
+#endif
+constexpr int kDepthItems = RS_DEPTH_ITEMS;  // 2048-key chunks (16: no change in the benches)
 
 // LSD passes of one sort over `bits` key bits; the digit histograms
 // (hist_slot) and the first pass's zeroed look-back words were produced by
