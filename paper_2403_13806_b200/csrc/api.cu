@@ -61,7 +61,7 @@ size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 struct Layout {
   // per-frame zeroed region [0, frame_bytes)
   size_t ctr, hist, proj_lb, ranges, frame_bytes;
-  size_t sticky, cam, recs, sgrad, titem, keysA, keysB, valsA, valsB, rowtab, rowcnt, segitem, segspan, geom,
+  size_t sticky, cam, recs, rows, sgrad, titem, keysA, keysB, valsA, valsB, rowtab, rowcnt, segitem, segspan, geom,
       rowstart, chunkstart, chunkcnt, chunkinfo, densel, tilecnt, tileord, pitem, lbA, lbB, total;
 };
 
@@ -90,6 +90,7 @@ Layout make_layout(int64_t n_cap, int64_t pair_cap, int W, int H) {
   L.sticky = take(sizeof(Sticky));
   L.cam = take(sizeof(rs_camera));
   L.recs = take((size_t)n_cap * sizeof(Rec));
+  L.rows = take((size_t)n_cap * 4);  // per binned item its tile-row range
   L.sgrad = take((size_t)n_cap * 4 * kSGrad);  // rs_backward: screen-space gradient sums per item
   L.titem = take((size_t)n_cap);
   L.keysA = take((size_t)n_cap * 4);
@@ -326,13 +327,13 @@ static int32_t project_impl(rs_workspace* ws, const rs_scene* scene, const int32
     if (full)
       launch(project_kernel<true, true>, grid, kProjThreads, 0, st, scene->planes, scene->sh,
              scene->plane_stride, scene->sh_degree, active_idx, (uint32_t)items, ws->at<rs_camera>(ws->L.cam),
-             *opts, ws->at<Rec>(ws->L.recs), ws->at<uint32_t>(ws->L.keysB), ws->ctr(), full,
-             reinterpret_cast<int4*>(full_bbox));
+             *opts, ws->at<Rec>(ws->L.recs), ws->at<uint32_t>(ws->L.keysB), ws->at<uint32_t>(ws->L.rows),
+             ws->ctr(), full, reinterpret_cast<int4*>(full_bbox));
     else
       launch((color ? project_kernel<false, true> : project_kernel<false, false>), grid, kProjThreads, 0, st,
              scene->planes, scene->sh, scene->plane_stride, scene->sh_degree, active_idx, (uint32_t)items,
              ws->at<rs_camera>(ws->L.cam), *opts, ws->at<Rec>(ws->L.recs), ws->at<uint32_t>(ws->L.keysB),
-             ws->ctr(), nullptr, nullptr);
+             ws->at<uint32_t>(ws->L.rows), ws->ctr(), nullptr, nullptr);
   }
   return cuda_status();
 }
@@ -372,7 +373,7 @@ int32_t rs_bin(rs_workspace* ws, void* stream) {
     const uint32_t seg_cap = (uint32_t)seg_capacity(ws->n_cap, ws->pair_cap);
     const uint32_t tab_stride = (uint32_t)rowtab_stride(ws->n_cap);
     const unsigned rc = (n + kRankChunk - 1) / kRankChunk;
-    launch(segrows_kernel, rc, 256, 0, st, items_sorted, ws->at<Rec>(ws->L.recs), ctr, ws->TH, tab_stride,
+    launch(segrows_kernel, rc, 256, 0, st, items_sorted, ws->at<uint32_t>(ws->L.rows), ctr, ws->TH, tab_stride,
            ws->at<uint32_t>(ws->L.rowtab));
     launch(segscan_kernel, ws->TH, 256, 0, st, ws->at<uint32_t>(ws->L.rowtab), tab_stride, ctr, ws->TH, seg_cap,
            ws->at<uint32_t>(ws->L.rowcnt), ws->at<uint32_t>(ws->L.rowstart), ws->at<uint32_t>(ws->L.chunkstart),

@@ -6,7 +6,8 @@
 // issued together; evaluates the Tier-A fp32 contract of
 // oracle/cpu_ref.cpp:project_one() in the same operation order (compiled with
 // -fmad=false; explicit __fmaf_rn only where the contract fuses), and writes
-//   * a 64-byte Rec for binned items (culled items write nothing else), and
+//   * a 64-byte Rec and its tile-row range (u32 r0 | r1 << 16) for binned items (culled
+//     items write nothing else), and
 //   * every item's 32-bit depth key (kInvalidKey when not binned), which
 //     compact_hist_kernel (sort.cuh) compacts for the depth sort.
 #pragma once
@@ -44,7 +45,7 @@ __global__ void __launch_bounds__(128) project_kernel(const float* __restrict__ 
                                                       const int32_t* __restrict__ active_idx, uint32_t n_items,
                                                       const rs_camera* __restrict__ camp, rs_options o,
                                                       Rec* __restrict__ recs,
-                                                      uint32_t* __restrict__ keys,
+                                                      uint32_t* __restrict__ keys, uint32_t* __restrict__ rows,
                                                       Counters* __restrict__ ctr,
                                                       float* __restrict__ full, int4* __restrict__ full_bbox) {
   pdl_wait();
@@ -250,6 +251,7 @@ __global__ void __launch_bounds__(128) project_kernel(const float* __restrict__ 
                         cy0 | (cy1 << 16) | (ell ? (int)0x80000000 : 0));
       if (binned) {
         recs[item] = rec;
+        rows[item] = (uint32_t)(cy0 / kTile) | ((uint32_t)((cy1 - 1) / kTile) << 16);  // segrows_kernel
         depth_b = depth;
       }
       if (FULL) {

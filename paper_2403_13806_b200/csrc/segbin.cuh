@@ -52,7 +52,7 @@ __device__ __forceinline__ void box_rows(const int4 cb, int& r0, int& r1) {
 // Pass 1: per rank chunk (256 consecutive depth ranks) the number of its Gaussians in each tile
 // row (a per-CTA difference array over the rows), stored row-major: row_tab[ty][chunk].
 __global__ void __launch_bounds__(256) segrows_kernel(const uint32_t* __restrict__ items_sorted,
-                                                      const Rec* __restrict__ recs,
+                                                      const uint32_t* __restrict__ item_rows,
                                                       const Counters* __restrict__ ctr, int TH, uint32_t tab_stride,
                                                       uint32_t* __restrict__ row_tab) {
   pdl_wait();
@@ -68,7 +68,9 @@ __global__ void __launch_bounds__(256) segrows_kernel(const uint32_t* __restrict
   const uint32_t r = c * kRankChunk + tid;
   if (r < nvis) {
     int r0, r1;
-    box_rows(cullbox_of(__ldg(&recs[__ldg(items_sorted + r)].d)), r0, r1);
+    const uint32_t rr = __ldg(item_rows + __ldg(items_sorted + r));  // the projection's r0 | r1 << 16
+    r0 = (int)(rr & 0xffffu);
+    r1 = (int)(rr >> 16);
     atomicAdd(&s_d[r0], 1);
     atomicAdd(&s_d[r1 + 1], -1);
   }
