@@ -314,18 +314,16 @@ __global__ void __launch_bounds__(kBlend2Threads, RS_BLEND_MINB) blend2_kernel(
         const int4 dr = __ldg(&R->d);
         const int4 d = cullbox_of(dr);
         s_rec[slot].d = d;
-        unsigned m;
-        if (!STATS && cullbox_ell(dr)) {
-          // the 8x8 quarters the ellipse strips of the tile's two half-rows reach: a warp whose
-          // quarter no pixel of the entry can composite in never walks it (STATS keeps the box
-          // quarters: every in-box pixel is evaluated, the oracle's E count)
+        // box x sub-rectangle overlap: 2 column halves x 2 row halves -> bit w = (w%2, w/2)
+        const unsigned col = (d.x < ox + 8 && d.y > ox ? 1u : 0u) | (d.x < ox + 16 && d.y > ox + 8 ? 2u : 0u);
+        unsigned m = 0;
+        if (d.z < oy + 8 && d.w > oy) m |= col;
+        if (d.z < oy + 16 && d.w > oy + 8) m |= col << 2;
+        if (!STATS && cullbox_ell(dr) && (m & (m - 1u))) {
+          // a box over several quarters: the ones the ellipse strips of the tile's two half-rows
+          // reach -- a warp whose quarter no pixel of the entry can composite in never walks it
+          // (STATS keeps the box quarters: every in-box pixel is evaluated, the oracle's E count)
           m = quarter_mask(load_row_geom(geom + 2 * (size_t)it, a.x, a.y), d, ox, oy);
-        } else {
-          // box x sub-rectangle overlap: 2 column halves x 2 row halves -> bit w = (w%2, w/2)
-          const unsigned col = (d.x < ox + 8 && d.y > ox ? 1u : 0u) | (d.x < ox + 16 && d.y > ox + 8 ? 2u : 0u);
-          m = 0;
-          if (d.z < oy + 8 && d.w > oy) m |= col;
-          if (d.z < oy + 16 && d.w > oy + 8) m |= col << 2;
         }
         s_mask[slot] = (uint8_t)m;
       }
