@@ -257,10 +257,14 @@ __global__ void __launch_bounds__(kBlend2Threads, RS_BLEND_MINB) blend2_kernel(
     int H, int TW, rs_options o, const rs_outputs out, uint32_t* __restrict__ scores) {
   pdl_wait();
   pdl_trigger();
-  constexpr int kBatch = 256;  // entries staged per batch (two per thread)
+#ifndef RS_BLEND_BATCH
+#define RS_BLEND_BATCH 256
+#endif
+  constexpr int kBatch = RS_BLEND_BATCH;  // entries staged per batch
+  constexpr int kPerThread = kBatch / kBlend2Threads;
   constexpr int U = kBlendUnroll;
   // slot kBatch: an empty-box sentinel that pads every warp list to a multiple of U entries
-  __shared__ Rec s_rec[kBatch + 1];
+  __shared__ Rec s_rec[kBatch + 1 > 160 ? kBatch + 1 : 160];  // >= 10 KB: the float64 epilogue's staging
   __shared__ uint32_t s_w[CONTRIB ? kBatch + 1 : 1];
   __shared__ uint8_t s_mask[kBatch];             // which warps' 8x8 sub-rectangles the entry touches
   __shared__ uint16_t s_list[4][kBatch + U];     // per-warp compacted entry lists (+ sentinel pad)
@@ -297,9 +301,10 @@ __global__ void __launch_bounds__(kBlend2Threads, RS_BLEND_MINB) blend2_kernel(
 
   for (uint32_t base = rg.x; base < end; base += kBatch) {
     if (__syncthreads_and(done0 && done1)) break;
-    uint32_t gid[2] = {0u, 0u};
+    uint32_t gid[kPerThread];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < kPerThread; ++h) {
+      gid[h] = 0u;
       const int slot = tid + h * kBlend2Threads;
       const uint32_t idx = base + slot;
       if (idx < end) {
@@ -459,7 +464,7 @@ __global__ void __launch_bounds__(kBlend2Threads, RS_BLEND_MINB) blend2_kernel(
     __syncthreads();
     if (CONTRIB) {
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < kPerThread; ++h) {
         const int slot = tid + h * kBlend2Threads;
         if (base + slot < end) {
           const uint32_t v = s_w[slot];
