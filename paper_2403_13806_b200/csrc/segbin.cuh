@@ -22,7 +22,7 @@
 //                    the list of dense chunks (>= 8 tiles per segment).
 //   tile_chunks_kernel / tile_scan_kernel  per tile: prefix over its row's
 //                    chunks and its total; exclusive scan over the tiles ->
-//                    ranges [start, end), P, overflow.
+//                    ranges [start, end), P, overflow, the blend order.
 //   expand_kernel    sparse chunks x 32-column groups: per warp 32 segments'
 //                    column masks, transposed (lane = column), each column's
 //                    covering items appended at its rank.
@@ -343,12 +343,13 @@ __device__ __forceinline__ bool chunk_of(const uint32_t* chunk_start, int TH, ui
   return true;
 }
 
-// Pass 2: the chunk's covering segments appended to each column's tile list after all
-// earlier chunks of the row (ranges + chunk prefix). A CTA owns 32 tile columns and takes the
-// chunk 256 segments at a time, warp w the w-th 32 of them: each lane turns its segment's span
-// into a 32-bit mask over the CTA's columns, a 32x32 bit transpose (5 shuffle stages) gives
-// lane c the mask of the warp's segments covering column c, and lane c appends those items in
-// segment (= depth) order after the earlier warps' counts (one shared-memory exchange).
+// Expansion: a chunk's covering segments appended to each column's tile list after all earlier
+// chunks of the row (ranges + chunk prefix). A sparse-chunk CTA owns 32 tile columns; warp w
+// takes 128 of the chunk's segments (all loads issued up front), compacts the ones reaching
+// the CTA's columns, turns each span into a 32-bit column mask, and a 32x32 bit transpose (5
+// shuffle stages) gives lane c the mask of the warp's segments covering column c; lane c then
+// appends those items in segment (= depth) order after the earlier warps' counts (one
+// shared-memory exchange per chunk).
 __device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
   constexpr uint32_t kM[5] = {0x0000ffffu, 0x00ff00ffu, 0x0f0f0f0fu, 0x33333333u, 0x55555555u};
 #pragma unroll
@@ -565,8 +566,8 @@ __global__ void __launch_bounds__(256) expand_dense_kernel(const uint32_t* __res
   }
 }
 
-// Pass 1 (order-free): per (chunk, tile column) the number of the chunk's segments covering
-// the column -- shared-memory counters over all the row's columns, one CTA per chunk.
+// Expansion counts (order-free): per (chunk, tile column) the number of the chunk's segments
+// covering the column -- shared-memory counters over all the row's columns, one CTA per chunk.
 __global__ void __launch_bounds__(256) chunk_count_kernel(const uint32_t* __restrict__ seg_span,
                                                           const uint32_t* __restrict__ row_start,
                                                           const uint32_t* __restrict__ chunk_start, int TH, int TW,
@@ -644,7 +645,8 @@ __device__ __forceinline__ int len_class(uint32_t v) {
 }
 
 // One CTA: exclusive scan of the tile counts (row-major tile ids) -> ranges (empty tiles
-// [0, 0)), P and the overflow verdict. Thread t owns ceil(T / 1024) consecutive tiles.
+// [0, 0)), P and the overflow verdict, plus the blend order (tiles by list-length class,
+// longest first). Thread t owns ceil(T / 1024) consecutive tiles.
 __global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restrict__ tile_count, int T,
                                                          Counters* __restrict__ ctr, uint32_t pair_cap,
                                                          uint2* __restrict__ ranges, Sticky* __restrict__ sticky,
