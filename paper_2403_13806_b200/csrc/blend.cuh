@@ -267,6 +267,9 @@ __global__ void __launch_bounds__(kBlend2Threads, RS_BLEND_MINB) blend2_kernel(
   __shared__ Rec s_rec[kBatch + 1 > 160 ? kBatch + 1 : 160];  // >= 10 KB: the float64 epilogue's staging
   __shared__ uint32_t s_w[CONTRIB ? kBatch + 1 : 1];
   __shared__ uint8_t s_mask[kBatch];             // which warps' 8x8 sub-rectangles the entry touches
+  // per entry and quarter: which of the quarter's 8 columns (bits 0-7) and 8 rows (8-15) lie in
+  // the box -- a lane's box test is one AND against its own column and row bits
+  __shared__ uint16_t s_boxm[kBatch + 1][4];
   __shared__ uint16_t s_list[4][kBatch + U];     // per-warp compacted entry lists (+ sentinel pad)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -286,6 +289,9 @@ __global__ void __launch_bounds__(kBlend2Threads, RS_BLEND_MINB) blend2_kernel(
   // per-pixel state of the thread's two pixels as packed pairs {py0, py1}
   f2 tau = f2_splat(1.0f), rgb[3] = {f2_splat(0.0f), f2_splat(0.0f), f2_splat(0.0f)}, dep = f2_splat(0.0f);
   const f2 ys2 = f2_pack(__fadd_rn((float)py0, 0.5f), __fadd_rn((float)py1, 0.5f));
+  // this lane's column bit and row bits in s_boxm (pixel rows lane / 8 and lane / 8 + 4)
+  const uint32_t sel0 = (1u << (lane & 7)) | (1u << (8 + (lane >> 3)));
+  const uint32_t sel1 = (1u << (lane & 7)) | (1u << (12 + (lane >> 3)));
   int cnt0 = 0, cnt1 = 0;
   int last0 = -1, last1 = -1;  // pair index of each pixel's last composite (training outputs)
   unsigned long long evals = 0;
@@ -294,6 +300,8 @@ __global__ void __launch_bounds__(kBlend2Threads, RS_BLEND_MINB) blend2_kernel(
     s_rec[kBatch].b = make_float4(0.f, 0.f, 0.f, 0.f);
     s_rec[kBatch].c = make_float4(0.f, 0.f, 0.f, 0.f);
     s_rec[kBatch].d = make_int4(0, 0, 0, 0);  // empty box: never evaluated
+#pragma unroll
+    for (int w = 0; w < 4; ++w) s_boxm[kBatch][w] = 0;
     if (CONTRIB) s_w[kBatch] = 0u;
   }
   const bool start = 1.0f >= o.tau_stop;
@@ -317,8 +325,16 @@ __global__ void __launch_bounds__(kBlend2Threads, RS_BLEND_MINB) blend2_kernel(
         if (COLOR || CONTRIB) s_rec[slot].c = c;
         gid[h] = (uint32_t)__float_as_int(c.w);
         const int4 dr = __ldg(&R->d);
-        const int4 d = cullbox_of(dr);
-        s_rec[slot].d = d;
+        const int4 d = cullbox_of(dr);  // only as the s_boxm bits below (the walk never reads E.d)
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          const int qx = ox + (w & 1) * 8, qy = oy + (w >> 1) * 8;
+          const int c0 = min(max(d.x - qx, 0), 8), c1 = min(max(d.y - qx, 0), 8);
+          const int r0 = min(max(d.z - qy, 0), 8), r1 = min(max(d.w - qy, 0), 8);
+          const uint32_t cm = ((1u << c1) - 1u) & ~((1u << c0) - 1u);
+          const uint32_t rm = ((1u << r1) - 1u) & ~((1u << r0) - 1u);
+          s_boxm[slot][w] = (uint16_t)(cm | (rm << 8));
+        }
         // box x sub-rectangle overlap: 2 column halves x 2 row halves -> bit w = (w%2, w/2)
         const unsigned col = (d.x < ox + 8 && d.y > ox ? 1u : 0u) | (d.x < ox + 16 && d.y > ox + 8 ? 2u : 0u);
         unsigned m = 0;
@@ -364,11 +380,10 @@ __global__ void __launch_bounds__(kBlend2Threads, RS_BLEND_MINB) blend2_kernel(
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const Rec& E = s_rec[ent[u]];
-          const int4 bb = E.d;
           const float4 ga = E.a, gb = E.b;
-          const bool inx = px >= bb.x && px < bb.y;
-          box[u][0] = inx && py0 >= bb.z && py0 < bb.w;
-          box[u][1] = inx && py1 >= bb.z && py1 < bb.w;
+          const uint32_t bm = s_boxm[ent[u]][warp];
+          box[u][0] = (bm & sel0) == sel0;
+          box[u][1] = (bm & sel1) == sel1;
           const float dx = __fsub_rn(xs, ga.x);
           const float ax = __fmul_rn(ga.z, dx);
           const f2 dy = f2_sub(ys2, f2_splat(ga.y));
