@@ -51,6 +51,7 @@ __global__ void __launch_bounds__(kBwd2Threads) backward2_kernel(
   __shared__ Rec s_rec[kBatch];
   __shared__ uint32_t s_item[kBatch];
   __shared__ uint8_t s_mask[kBatch];
+  __shared__ uint16_t s_boxm[kBatch][4];  // per quarter: box columns (bits 0-7) and rows (8-15)
   __shared__ uint8_t s_list[4][kBatch];
   __shared__ int s_maxlast[4];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -62,6 +63,8 @@ __global__ void __launch_bounds__(kBwd2Threads) backward2_kernel(
   const bool in0 = px < W && py0 < H, in1 = px < W && py1 < H;
   const float xs = __fadd_rn((float)px, 0.5f);
   const f2 ys2 = f2_pack(__fadd_rn((float)py0, 0.5f), __fadd_rn((float)py1, 0.5f));
+  const uint32_t sel0 = (1u << (lane & 7)) | (1u << (8 + (lane >> 3)));
+  const uint32_t sel1 = (1u << (lane & 7)) | (1u << (12 + (lane >> 3)));
   if (ctr->overflow) return;
   const uint2 rg = ranges[tile];
   const uint32_t end = min(rg.y, ctr->n_pairs);
@@ -109,7 +112,15 @@ __global__ void __launch_bounds__(kBwd2Threads) backward2_kernel(
         s_rec[slot].c = __ldg(&R->c);
         const int4 dr = __ldg(&R->d);
         const int4 d = cullbox_of(dr);
-        s_rec[slot].d = d;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          const int qx = ox + (w & 1) * 8, qy = oy + (w >> 1) * 8;
+          const int c0 = min(max(d.x - qx, 0), 8), c1 = min(max(d.y - qx, 0), 8);
+          const int r0 = min(max(d.z - qy, 0), 8), r1 = min(max(d.w - qy, 0), 8);
+          const uint32_t cm = ((1u << c1) - 1u) & ~((1u << c0) - 1u);
+          const uint32_t rm = ((1u << r1) - 1u) & ~((1u << r0) - 1u);
+          s_boxm[slot][w] = (uint16_t)(cm | (rm << 8));
+        }
         s_item[slot] = it;
         // the 8x8 quarters the entry can composite in (blend2_kernel's warp lists)
         unsigned m;
@@ -137,12 +148,11 @@ __global__ void __launch_bounds__(kBwd2Threads) backward2_kernel(
     for (int q = cntw - 1; q >= 0; --q) {
       const int e = s_list[warp][q];
       const Rec& E = s_rec[e];
-      const int4 bb = E.d;
       const float4 ga = E.a, gb4 = E.b;
       const int k = (int)base + e;
-      const bool inx = px >= bb.x && px < bb.y;
-      const bool cand0 = in0 && k <= lastk[0] && inx && py0 >= bb.z && py0 < bb.w;
-      const bool cand1 = in1 && k <= lastk[1] && inx && py1 >= bb.z && py1 < bb.w;
+      const uint32_t bm = s_boxm[e][warp];
+      const bool cand0 = k <= lastk[0] && (bm & sel0) == sel0;  // (out-of-image pixels: lastk -1)
+      const bool cand1 = k <= lastk[1] && (bm & sel1) == sel1;
       if (!__any_sync(0xffffffffu, cand0 || cand1)) continue;
       // the forward's p2 / alpha (blend2_kernel's operations)
       const float dx = __fsub_rn(xs, ga.x);
