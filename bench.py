@@ -146,9 +146,9 @@ def cpu_views(scene, cams, images: bool, threads: int | None = None):
     return time.perf_counter() - t0, r
 
 
-def dict_opts():
+def dict_opts(precision: str = "fp32"):
     from paper_2403_13806_b200.render import RasterizeOptions
-    return RasterizeOptions(near_limit=0.2)
+    return RasterizeOptions(near_limit=0.2, precision=precision)
 
 
 def cpu_model() -> str:
@@ -386,7 +386,7 @@ def main():
         # pre-pass: overflow-checked capacity sizing over this rank's views
         P_ = 0
         for c in cams[lo:hi]:
-            _, st = r.render(ds, c, opts, color=False, scores=scores.view(torch.int32))
+            _, st = r.render(ds, c, opts, color=False, scores=scores)
             P_ += st.n_pairs
         sc_ptr = scores.data_ptr()
 

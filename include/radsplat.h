@@ -42,8 +42,16 @@
  *   - Re-entrant per workspace; no global mutable state.
  *   - Return value: RS_OK or an RS_E* code (mapped to the reference exception
  *     classes in paper_2403_13806_b200/_native.py).
- *   - Arithmetic is fp32 with the operation order of the Tier-A contract
- *     (oracle/cpu_ref.cpp); results are bit-identical to that oracle.
+ *   - Two arithmetic precisions, chosen per frame by rs_options.precision:
+ *       RS_F32: fp32 with the operation order of the Tier-A contract
+ *               (oracle/cpu_ref.cpp, float tier) -- the fast path;
+ *       RS_F64: fp64 with the reference's own expressions and operation order
+ *               (render.py:95-158, :250-281) and a contract exp -- results are
+ *               bit-identical to the oracle's fp64 contract tier, which matches
+ *               the NumPy reference to ~1e-15 (the composite order is the
+ *               reference's exact (fp64 depth, index) order).
+ *     Cameras and options always cross the boundary in fp64 (the reference's
+ *     values); the fp32 path rounds them once (round to nearest).
  */
 #ifndef RADSPLAT_H
 #define RADSPLAT_H
@@ -55,7 +63,7 @@
 extern "C" {
 #endif
 
-#define RS_ABI_VERSION 1
+#define RS_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define RS_API __attribute__((visibility("default")))
@@ -72,8 +80,11 @@ enum {
   RS_EOVERFLOW = 5          /* more tile pairs than the workspace's pair capacity */
 };
 
-/* Scene in device memory (236 B per Gaussian):
- *   planes: 11 planes of `plane_stride` floats (coalesced per-plane loads)
+/* Storage / arithmetic types (rs_scene.dtype, rs_options.precision). */
+enum { RS_F32 = 0, RS_F64 = 1 };
+
+/* Scene in device memory (236 B per Gaussian as fp32, 472 B as fp64):
+ *   planes: 11 planes of `plane_stride` values (coalesced per-plane loads)
  *     planes 0-2  positions x,y,z          (core.py:478)
  *     plane  3    opacity logit            (core.py:479; opacity = sigmoid)
  *     planes 4-6  log scales x,y,z         (core.py:481; scale = exp)
@@ -83,41 +94,46 @@ enum {
  *     Gaussians of frames that produce colour. 16-byte aligned.
  */
 typedef struct rs_scene {
-  const float* planes;
-  const float* sh;
+  const void* planes; /* float or double (dtype) */
+  const void* sh;     /* float or double (dtype) */
   int64_t n;
   int64_t plane_stride;
   int32_t sh_degree; /* 0..3 */
-  int32_t _pad;
+  int32_t dtype;     /* RS_F32 or RS_F64: storage type of planes and sh. Values
+                        are widened exactly; an fp64 scene in an RS_F32 frame is
+                        rounded to fp32 on load (= numpy astype(float32)). */
 } rs_scene;
 
 /* Pinhole camera (core.py:316-374): p_cam = R p + t, row-major R. `center`
- * = -R^T t, computed by the caller in fp64 and rounded to fp32. */
+ * = -R^T t (core.py:351-354), computed by the caller in fp64. */
 typedef struct rs_camera {
   int32_t width, height;
-  float fx, fy, cx, cy;
-  float R[9];
-  float t[3];
-  float center[3];
+  double fx, fy, cx, cy;
+  double R[9];
+  double t[3];
+  double center[3];
 } rs_camera;
 
-/* RasterizeOptions (render.py:37-46). */
+/* RasterizeOptions (render.py:37-46) + the arithmetic precision of the frame. */
 typedef struct rs_options {
-  float alpha_max, alpha_cut, tau_stop, near_limit, lowpass, sigma_bound;
+  double alpha_max, alpha_cut, tau_stop, near_limit, lowpass, sigma_bound;
+  int32_t precision; /* RS_F32 (fast fp32 contract) or RS_F64 (reference fp64) */
+  int32_t _pad;
 } rs_options;
 
 /* Image outputs of a colour frame (rs_render_ex / rs_blend_ex). Every pointer
  * may be NULL (that output is skipped); rgb, alpha and count go together.
- *   rgb (H*W*3), alpha, depth (H*W) fp32 and count (H*W) int32: device images.
+ *   rgb (H*W*3), alpha, depth (H*W) and count (H*W) int32: device images, fp32
+ *     (float*) in RS_F32 frames, fp64 (double*, same fields) in RS_F64 frames.
  *   rgb64 (H*W*3), alpha64 (H*W) float64 and count64 (H*W) int64: the
  *     reference's RenderOutput types (render.py:62-68, :236-239, :283); any
  *     device-dereferenceable memory, typically mapped pinned HOST memory
  *     (cudaHostAlloc; same pointer under UVA) so the blend writes the result
  *     straight over the host link while other tiles are still compositing. */
 typedef struct rs_outputs {
-  float* rgb;
-  float* alpha;
-  float* depth;
+  void* rgb;   /* float (RS_F32) or double (RS_F64) */
+  void* alpha; /* float or double */
+  void* depth; /* float or double */
   int32_t* count;
   double* rgb64;
   double* alpha64;
@@ -139,6 +155,10 @@ typedef struct rs_stats {
                            counted when RS_FLAG_COUNT_EVALS is set)            */
   uint64_t composites;  /* C: composited (pixel, Gaussian) pairs (same flag)   */
   uint64_t pairs_needed;/* P, the pair capacity this frame needs               */
+  uint32_t bad_index;   /* 1 if active_idx held an index outside [0, n): those
+                           entries were skipped; the caller reports RS_EINVAL
+                           (InvalidParameterError, render.py:231-234)          */
+  uint32_t _pad;
 } rs_stats;
 
 /* Device pointers into a workspace, for inspection / parity tests. */
@@ -146,6 +166,10 @@ typedef struct rs_buffers {
   const void* records;          /* n_cap x 64 B projected records, item order:
                                    {mx,my,na,nb},{nc,opacity,cut2,depth},
                                    {r,g,b,gid},{x0,x1,y0,y1}                  */
+  const void* records64;        /* n_cap x 96 B fp64 records (RS_F64 frames):
+                                   mx,my,inv_a,2*inv_b,inv_c,opacity,depth,
+                                   ln(alpha_cut/opacity)-1e-6, r,g,b (double),
+                                   gid, pad (uint32)                           */
   const uint32_t* items_sorted; /* n_items item ids in (depth, index) order   */
   const uint32_t* pair_items;   /* n_pairs item ids, grouped by tile           */
   const uint32_t* ranges;       /* tiles x 2 : [start, end) into pair_items    */
@@ -180,16 +204,21 @@ RS_API void rs_workspace_destroy(rs_workspace* ws);
  *               only listed Gaussians are projected); NULL = all scene->n.
  *   out_rgb (H*W*3), out_alpha, out_depth (H*W), out_count (H*W int32): may
  *               all be NULL for a score-only (importance) pass.
- *   scores:     optional n floats (as uint32 bit patterns of non-negative
- *               floats) max-merged with each Gaussian's max alpha*tau.
+ *               Out-of-range entries are skipped and flagged (rs_stats.bad_index).
+ *   out_rgb (H*W*3), out_alpha, out_depth (H*W), out_count (H*W int32): may
+ *               all be NULL for a score-only (importance) pass; float images in
+ *               RS_F32 frames, double in RS_F64 frames.
+ *   scores:     optional n values max-merged with each Gaussian's max alpha*tau
+ *               (render.py:273-275): uint32 bit patterns of non-negative floats
+ *               (RS_F32) or uint64 bit patterns of non-negative doubles (RS_F64).
  */
 RS_API int32_t rs_render(rs_workspace* ws, const rs_scene* scene, const int32_t* active_idx, int64_t m, const rs_camera* cam,
-                  const rs_options* opts, float* out_rgb, float* out_alpha, float* out_depth, int32_t* out_count,
-                  uint32_t* scores, uint32_t flags, void* stream);
+                  const rs_options* opts, void* out_rgb, void* out_alpha, void* out_depth, int32_t* out_count,
+                  void* scores, uint32_t flags, void* stream);
 
 /* rs_render with the image outputs of an rs_outputs (NULL = score-only frame). */
 RS_API int32_t rs_render_ex(rs_workspace* ws, const rs_scene* scene, const int32_t* active_idx, int64_t m,
-                            const rs_camera* cam, const rs_options* opts, const rs_outputs* out, uint32_t* scores,
+                            const rs_camera* cam, const rs_options* opts, const rs_outputs* out, void* scores,
                             uint32_t flags, void* stream);
 
 /* Stream-ordered camera upload into the workspace (also fixes the image size of
@@ -201,15 +230,17 @@ RS_API int32_t rs_project(rs_workspace* ws, const rs_scene* scene, const int32_t
                    const rs_options* opts, void* stream);
 RS_API int32_t rs_bin(rs_workspace* ws, void* stream);
 /* rs_project that also writes, per item (culled included), the reference's
- * ProjectedGaussian fields (render.py:49-59) as 16 floats
- * {mx, my, a, b, c, inv_a, inv_b, inv_c, radius, depth, r, g, b, opacity,
- *  valid, 0} to out_proj and {x0, x1, y0, y1} to out_bbox (render.py:161-211). */
+ * ProjectedGaussian fields (render.py:49-59) as 16 values (float in RS_F32,
+ * double in RS_F64 frames) {mx, my, a, b, c, inv_a, inv_b, inv_c, radius,
+ * depth, r, g, b, opacity, valid, cut} to out_proj and {x0, x1, y0, y1} to
+ * out_bbox (render.py:161-211). */
 RS_API int32_t rs_project_full(rs_workspace* ws, const rs_scene* scene, const int32_t* active_idx, int64_t m,
-                        const rs_camera* cam, const rs_options* opts, float* out_proj, int32_t* out_bbox,
+                        const rs_camera* cam, const rs_options* opts, void* out_proj, int32_t* out_bbox,
                         void* stream);
-RS_API int32_t rs_blend(rs_workspace* ws, const rs_options* opts, float* out_rgb, float* out_alpha, float* out_depth,
-                 int32_t* out_count, uint32_t* scores, uint32_t flags, void* stream);
-RS_API int32_t rs_blend_ex(rs_workspace* ws, const rs_options* opts, const rs_outputs* out, uint32_t* scores,
+/* rs_blend / rs_blend_ex: `opts` must have the precision of the rs_project call. */
+RS_API int32_t rs_blend(rs_workspace* ws, const rs_options* opts, void* out_rgb, void* out_alpha, void* out_depth,
+                 int32_t* out_count, void* scores, uint32_t flags, void* stream);
+RS_API int32_t rs_blend_ex(rs_workspace* ws, const rs_options* opts, const rs_outputs* out, void* scores,
                            uint32_t flags, void* stream);
 
 /* Gradients of a scalar loss through the image of the frame the last
@@ -217,9 +248,9 @@ RS_API int32_t rs_blend_ex(rs_workspace* ws, const rs_options* opts, const rs_ou
  * training forward, render.py:318-321): grad_image = dL/dcolor (H*W*3, device),
  * outputs per scene Gaussian (device, zeroed here): positions (n,3), sh (n,48),
  * log-scales (n,3), quaternions (n,4), opacity logits (n), |dL/dmean2d| (n),
- * touched (n bytes). Same scene / active list as that forward. fp32; the
- * per-Gaussian sums are atomics, so results match the reference to a
- * tolerance, not bit for bit. */
+ * touched (n bytes). Same scene / active list as that forward. RS_F32 frames
+ * of fp32 scenes only (RS_EINVAL otherwise); the per-Gaussian sums are
+ * atomics, so results match the reference to a tolerance, not bit for bit. */
 RS_API int32_t rs_backward(rs_workspace* ws, const rs_scene* scene, const int32_t* active_idx, int64_t m,
                            const rs_options* opts, const float* grad_image, const float* tau, const int32_t* last,
                            float* g_pos, float* g_sh, float* g_ls, float* g_quat, float* g_logit, float* g_mean2d,
@@ -230,9 +261,12 @@ RS_API int32_t rs_read_stats(rs_workspace* ws, rs_stats* out, void* stream);
 /* Did any frame since the last reset overflow its pair capacity, and the
  * largest P such a frame needed (synchronizes `stream`; reset != 0 clears
  * the record). Lets a batch of frames -- a scoring pass -- run without a
- * host sync per frame and be checked once. */
+ * host sync per frame and be checked once. rs_read_sticky also reports
+ * whether any of those frames skipped an out-of-range active_idx entry. */
 RS_API int32_t rs_read_overflow(rs_workspace* ws, uint32_t* out_overflowed, uint64_t* out_pairs_needed_max,
                                 int32_t reset, void* stream);
+RS_API int32_t rs_read_sticky(rs_workspace* ws, uint32_t* out_overflowed, uint64_t* out_pairs_needed_max,
+                              uint32_t* out_bad_index, int32_t reset, void* stream);
 RS_API int32_t rs_get_buffers(rs_workspace* ws, rs_buffers* out);
 
 /* Stable compaction: indices i (ascending) with flags[i] != 0, count -> *out_count (device). */
@@ -243,7 +277,8 @@ RS_API int32_t rs_compact(const uint8_t* flags, int64_t n, int32_t* out_idx, uin
 RS_API int32_t rs_compact_bits(const uint8_t* bits, int64_t n, int32_t* out_idx, uint32_t* out_count, void* scratch,
                         size_t scratch_bytes, void* stream);
 
-/* *out_bad (device) = number of non-finite scene values (planes and SH rows; 0 = finite). */
+/* *out_bad (device) = number of non-finite scene values (planes and SH rows,
+ * either dtype; 0 = finite). */
 RS_API int32_t rs_check_finite(const rs_scene* scene, uint32_t* out_bad, void* stream);
 
 /* RSPL payload (device, 16-B aligned: positions (n,3), log-scales (n,3),

@@ -5,10 +5,16 @@
 // bench.py's cpu_baseline / --impl reference leg use it, as the checker and
 // as the CPU baseline.
 //
-// A scalar restatement of the reference NumPy rasterizer, instantiated twice:
+// A scalar restatement of the reference NumPy rasterizer, instantiated three times:
 //   * T = double  ("Tier B"): the reference's expressions in the reference's
 //     order with std::exp, pinned against golden vectors produced by the
 //     reference itself (tests/golden/make_golden.py).
+//   * T = double, CT ("Tier C", the parity contract of the CUDA path's RS_F64
+//     frames): Tier B with exp64_contract (an exp from IEEE double add/mul/fma
+//     only; device twin in csrc/rs_math.cuh) instead of std::exp, its argument
+//     clamped at 709 (an overflow guard), and the pixel gate of the fp32 tier's
+//     culling box (which drops only pixels with alpha < alpha_cut). Tier C vs
+//     Tier B: within a few ulp.
 //   * T = float   ("Tier A", the parity contract for the CUDA path): the same
 //     algorithm in fp32 with every operation and its order written out, no
 //     FMA contraction except the explicit fmaf() calls (-ffp-contract=off),
@@ -116,6 +122,44 @@ inline float log2_contract(float x) {
   return std::fma(t * p, 2.88539004f, (float)e);
 }
 
+// e^x in double (device twin: exp64_contract in csrc/rs_math.cuh): n = rint(x log2 e)
+// by the magic-number add, Cody-Waite r = x - n ln2, degree-12 Taylor in Horner form
+// (|r| <= 0.347), times 2^n through the exponent field.
+inline double pow2i64(int n) {  // n in [-1022, 1023]
+  const uint64_t u = (uint64_t)(n + 1023) << 52;
+  double d;
+  std::memcpy(&d, &u, 8);
+  return d;
+}
+inline double exp64_contract(double x) {
+  if (x != x) return x;
+  if (x > 709.782712893384) return INFINITY;
+  if (x < -745.2) return 0.0;
+  const double t = std::fma(x, 1.4426950408889634, 6755399441055744.0);
+  const double n = t - 6755399441055744.0;
+  double r = std::fma(n, -0.6931471803691238, x);
+  r = std::fma(n, -1.9082149292705877e-10, r);
+  double p = 1.0 / 479001600.0;
+  p = std::fma(p, r, 1.0 / 39916800.0);
+  p = std::fma(p, r, 1.0 / 3628800.0);
+  p = std::fma(p, r, 1.0 / 362880.0);
+  p = std::fma(p, r, 1.0 / 40320.0);
+  p = std::fma(p, r, 1.0 / 5040.0);
+  p = std::fma(p, r, 1.0 / 720.0);
+  p = std::fma(p, r, 1.0 / 120.0);
+  p = std::fma(p, r, 1.0 / 24.0);
+  p = std::fma(p, r, 1.0 / 6.0);
+  p = std::fma(p, r, 0.5);
+  p = std::fma(p, r, 1.0);
+  p = std::fma(p, r, 1.0);
+  uint64_t tb;
+  std::memcpy(&tb, &t, 8);
+  const int ni = (int)(int32_t)(uint32_t)tb;  // n in the low word of t
+  if (ni > 1023) return (p * pow2i64(1023)) * 2.0;
+  if (ni >= -1022) return p * pow2i64(ni);
+  return (p * pow2i64(ni + 600)) * pow2i64(-600);
+}
+
 template <typename T> struct M;
 template <> struct M<double> {
   static double exp(double x) { return std::exp(x); }
@@ -123,6 +167,11 @@ template <> struct M<double> {
 template <> struct M<float> {
   static float exp(float x) { return exp_contract(x); }
 };
+// the exp of a tier: CT = the fp64 contract (Tier C)
+template <typename T, bool CT> inline T texp(T x) {
+  if constexpr (CT) return (T)exp64_contract((double)x);
+  else return M<T>::exp(x);
+}
 
 // order-preserving map of the fp32 depth to 32 key bits (-0 folded into +0)
 inline uint32_t depth_key(float d) {
@@ -270,7 +319,7 @@ template <typename T> inline bool row_span(const PG<T>& g, int ty, int* tx0, int
   return true;
 }
 
-template <typename T>
+template <typename T, bool CT = false>
 PG<T> project_one(const Scene<T>& s, int64_t i, const Cam<T>& cam, const Opts<T>& o) {
   PG<T> g;
   const T px = s.pos[3 * i], py = s.pos[3 * i + 1], pz = s.pos[3 * i + 2];
@@ -298,7 +347,7 @@ PG<T> project_one(const Scene<T>& s, int64_t i, const Cam<T>& cam, const Opts<T>
   Rq[8] = (T)1 - (T)2 * (qx * qx + qy * qy);
   // Sigma = L L^T, L = Rq diag(exp(log_s))  (render.py:108-111)
   T sc[3];
-  for (int j = 0; j < 3; ++j) sc[j] = M<T>::exp(s.ls[3 * i + j]);
+  for (int j = 0; j < 3; ++j) sc[j] = texp<T, CT>(s.ls[3 * i + j]);
   T L[9];
   for (int r = 0; r < 3; ++r)
     for (int j = 0; j < 3; ++j) L[3 * r + j] = Rq[3 * r + j] * sc[j];
@@ -375,9 +424,9 @@ PG<T> project_one(const Scene<T>& s, int64_t i, const Cam<T>& cam, const Opts<T>
   // opacity = sigmoid(logit) (core.py:419-421)
   const T lg = s.logit[i];
   if (lg >= (T)0) {
-    g.opacity = (T)1 / ((T)1 + M<T>::exp(-lg));
+    g.opacity = (T)1 / ((T)1 + texp<T, CT>(-lg));
   } else {
-    const T e = M<T>::exp(lg);
+    const T e = texp<T, CT>(lg);
     g.opacity = e / ((T)1 + e);
   }
   const float K = fbits(0xbf38aa3bu);  // -0.5 * log2(e)
@@ -388,14 +437,14 @@ PG<T> project_one(const Scene<T>& s, int64_t i, const Cam<T>& cam, const Opts<T>
   g.cut2 = -INFINITY;
   g.bin = g.valid;
   g.ell = 0;
-  if (sizeof(T) == 4 && g.valid) cull_box(g, (float)o.alpha_cut);
+  if ((sizeof(T) == 4 || CT) && g.valid) cull_box(g, (float)o.alpha_cut);
   return g;
 }
 
-template <typename T>
+template <typename T, bool CT = false>
 std::vector<PG<T>> project_all(const Scene<T>& s, const Cam<T>& cam, const Opts<T>& o) {
   std::vector<PG<T>> v((size_t)s.n);
-  for (int64_t i = 0; i < s.n; ++i) v[(size_t)i] = project_one(s, i, cam, o);
+  for (int64_t i = 0; i < s.n; ++i) v[(size_t)i] = project_one<T, CT>(s, i, cam, o);
   return v;
 }
 
@@ -420,14 +469,22 @@ template <typename T> inline void atomic_max(T* p, T v) {
 }
 
 // Per-pixel evaluation of one Gaussian: returns alpha (render.py:255-259).
-template <typename T> inline T pixel_alpha(const PG<T>& g, T xs, T ys, T alpha_max);
-template <> inline double pixel_alpha<double>(const PG<double>& g, double xs, double ys, double alpha_max) {
+template <typename T, bool CT = false> inline T pixel_alpha(const PG<T>& g, T xs, T ys, T alpha_max);
+template <> inline double pixel_alpha<double, true>(const PG<double>& g, double xs, double ys, double alpha_max) {
+  // Tier C: the reference expression with the contract exp, argument clamped at 709
+  const double dx = xs - g.mx, dy = ys - g.my;
+  const double q = (g.ia * dx * dx) + (2.0 * g.ib) * dy * dx + (g.ic * dy * dy);
+  const double x = -0.5 * q;
+  const double raw = g.opacity * exp64_contract(x < 709.0 || x != x ? x : 709.0);
+  return (raw != raw || raw < alpha_max) ? raw : alpha_max;
+}
+template <> inline double pixel_alpha<double, false>(const PG<double>& g, double xs, double ys, double alpha_max) {
   const double dx = xs - g.mx, dy = ys - g.my;
   const double q = (g.ia * dx * dx) + (2.0 * g.ib) * dy * dx + (g.ic * dy * dy);
   const double raw = g.opacity * std::exp(-0.5 * q);
   return (raw != raw || raw < alpha_max) ? raw : alpha_max;  // np.minimum propagates NaN
 }
-template <> inline float pixel_alpha<float>(const PG<float>& g, float xs, float ys, float alpha_max) {
+template <> inline float pixel_alpha<float, false>(const PG<float>& g, float xs, float ys, float alpha_max) {
   const float dx = xs - g.mx, dy = ys - g.my;
   const float p2 = std::fma(g.na * dx, dx, std::fma(g.nb * dy, dx, (g.nc * dy) * dy));
   // 2^min(p2, 127): an overflow guard (o * 2^127 saturates alpha_max for any o >= 5.8e-39)
@@ -448,7 +505,7 @@ struct Out {
 };
 
 // Composite one pixel over a front-to-back list (oracles.py:32-59 semantics).
-template <typename T>
+template <typename T, bool CT = false>
 inline void composite_pixel(const std::vector<PG<T>>& pg, const int64_t* list, size_t len, int x, int y,
                             const Opts<T>& o, T* rgbd, T& tau_out, int32_t& cnt, T* contrib, Counters& k) {
   const T xs = (T)x + (T)0.5, ys = (T)y + (T)0.5;
@@ -461,7 +518,7 @@ inline void composite_pixel(const std::vector<PG<T>>& pg, const int64_t* list, s
     // pixels that cannot reach alpha_cut, so gating with it changes no result
     if (!(g.cx0 <= x && x < g.cx1 && g.cy0 <= y && y < g.cy1)) continue;
     ++k.E;
-    const T alpha = pixel_alpha<T>(g, xs, ys, o.alpha_max);
+    const T alpha = pixel_alpha<T, CT>(g, xs, ys, o.alpha_max);
     if (alpha >= o.alpha_cut && tau >= o.tau_stop) {
       const T w = alpha * tau;  // render.py:267
       r = mac<T>(g.color[0], w, r);
@@ -480,7 +537,9 @@ inline void composite_pixel(const std::vector<PG<T>>& pg, const int64_t* list, s
 }
 
 // Tile binning: 64-bit keys (tile << 32 | depth_key), emitted in index order,
-// stable-sorted; ranges[t] = [start, end). Returns the pair count.
+// stable-sorted (fp64 tiers: by tile, then the fp64 depth -- the fp32 depth key
+// can tie where the fp64 depths differ); ranges[t] = [start, end). Returns the
+// pair count.
 template <typename T>
 int64_t bin_tiles(const std::vector<PG<T>>& pg, const uint8_t* active, int W, int H, std::vector<uint64_t>* keys,
                   std::vector<uint32_t>* vals, std::vector<uint32_t>* ranges) {
@@ -495,7 +554,14 @@ int64_t bin_tiles(const std::vector<PG<T>>& pg, const uint8_t* active, int W, in
       if (row_span(g, ty, &a, &b))
         for (int tx = a; tx <= b; ++tx) pairs.emplace_back(((uint64_t)(ty * TW + tx) << 32) | dk, (uint32_t)i);
   }
-  std::stable_sort(pairs.begin(), pairs.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+  if constexpr (sizeof(T) == 4) {
+    std::stable_sort(pairs.begin(), pairs.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+  } else {  // fp64 tiers: (tile, fp64 depth), index order on ties -- the reference's order per tile
+    std::stable_sort(pairs.begin(), pairs.end(), [&](const auto& a, const auto& b) {
+      const uint64_t ta = a.first >> 32, tb = b.first >> 32;
+      return ta != tb ? ta < tb : pg[a.second].depth < pg[b.second].depth;
+    });
+  }
   keys->resize(pairs.size());
   vals->resize(pairs.size());
   ranges->assign(2 * (size_t)TW * TH, 0);
@@ -520,13 +586,13 @@ template <typename F> void parallel(int threads, F fn) {
   for (auto& th : pool) th.join();
 }
 
-template <typename T>
+template <typename T, bool CT = false>
 std::vector<PG<T>> project_par(const Scene<T>& s, const Cam<T>& cam, const Opts<T>& o, int threads) {
   std::vector<PG<T>> v((size_t)s.n);
   const int64_t per = (s.n + threads - 1) / std::max(threads, 1);
   parallel(threads, [&](int t) {
     const int64_t lo = t * per, hi = std::min<int64_t>(s.n, lo + per);
-    for (int64_t i = lo; i < hi; ++i) v[(size_t)i] = project_one(s, i, cam, o);
+    for (int64_t i = lo; i < hi; ++i) v[(size_t)i] = project_one<T, CT>(s, i, cam, o);
   });
   return v;
 }
@@ -536,13 +602,13 @@ std::vector<PG<T>> project_par(const Scene<T>& s, const Cam<T>& cam, const Opts<
 // list per pixel (oracles.py literal). `threads` splits projection, tile-list
 // construction (bands of tile rows) and compositing (tiles); contributions
 // merge by an atomic max, which is order independent (render.py:71-76).
-template <typename T>
+template <typename T, bool CT = false>
 void render(const Scene<T>& s, const T* camp, const T* optp, const uint8_t* active, int method, Out out,
             Counters* kc, int threads = 1) {
   const Cam<T> cam(camp);
   const Opts<T> o(optp);
   threads = std::max(threads, 1);
-  const std::vector<PG<T>> pg = project_par(s, cam, o, threads);
+  const std::vector<PG<T>> pg = project_par<T, CT>(s, cam, o, threads);
   T* contrib = (T*)out.contrib;
   const int W = cam.W, H = cam.H;
   auto store = [&](int x, int y, const T* rgbd, T tau, int32_t c) {
@@ -561,7 +627,7 @@ void render(const Scene<T>& s, const T* camp, const T* optp, const uint8_t* acti
       int32_t c;
       for (int y; (y = next.fetch_add(1)) < H;)
         for (int x = 0; x < W; ++x) {
-          composite_pixel(pg, order.data(), order.size(), x, y, o, rgbd, tau, c, contrib, kk[t]);
+          composite_pixel<T, CT>(pg, order.data(), order.size(), x, y, o, rgbd, tau, c, contrib, kk[t]);
           store(x, y, rgbd, tau, c);
         }
     });
@@ -590,7 +656,7 @@ void render(const Scene<T>& s, const T* camp, const T* optp, const uint8_t* acti
         const int tx = tile % TW, ty = tile / TW;
         for (int y = ty * TILE; y < std::min(H, ty * TILE + TILE); ++y)
           for (int x = tx * TILE; x < std::min(W, tx * TILE + TILE); ++x) {
-            composite_pixel(pg, list.data(), list.size(), x, y, o, rgbd, tau, c, contrib, kk[t]);
+            composite_pixel<T, CT>(pg, list.data(), list.size(), x, y, o, rgbd, tau, c, contrib, kk[t]);
             store(x, y, rgbd, tau, c);
           }
       }
@@ -608,7 +674,7 @@ template <typename T> Scene<T> mkscene(const T* pos, const T* logit, const T* sh
 // CPU-baseline driver: views one after another, each rendered by all threads
 // (so a bounded sample of a few views still uses every core); scores merge by
 // max across views (pruning.py:80-82).
-template <typename T>
+template <typename T, bool CT = false>
 void views(const Scene<T>& s, const T* cams, int64_t n_views, const T* optp, int threads, int want_images,
            T* contrib, T* img_last, int64_t* counters) {
   Counters kc;
@@ -622,7 +688,7 @@ void views(const Scene<T>& s, const T* cams, int64_t n_views, const T* optp, int
       out.img = img.data();
     }
     out.contrib = contrib;
-    render<T>(s, cp, optp, nullptr, 0, out, &kc, threads);
+    render<T, CT>(s, cp, optp, nullptr, 0, out, &kc, threads);
     if (img_last && v == n_views - 1) std::memcpy(img_last, img.data(), img.size() * sizeof(T));
   }
   if (counters) { counters[0] += kc.E; counters[1] += kc.C; }
@@ -658,15 +724,15 @@ void export_proj(const std::vector<PG<T>>& pg, ProjOut* po) {
 
 }  // namespace
 
-#define ORC_DEFINE(SUF, T)                                                                                       \
+#define ORC_DEFINE(SUF, T, CT)                                                                                       \
   extern "C" void orc_project_##SUF(const T* pos, const T* logit, const T* sh, const T* ls, const T* quat,       \
                                     int64_t n, int deg, const T* cam, const T* opts, ProjOut* po) {              \
-    export_proj(project_all(mkscene(pos, logit, sh, ls, quat, n, deg), Cam<T>(cam), Opts<T>(opts)), po);        \
+    export_proj(project_all<T, CT>(mkscene(pos, logit, sh, ls, quat, n, deg), Cam<T>(cam), Opts<T>(opts)), po); \
   }                                                                                                              \
   extern "C" int64_t orc_order_##SUF(const T* pos, const T* logit, const T* sh, const T* ls, const T* quat,     \
                                      int64_t n, int deg, const T* cam, const T* opts, const uint8_t* active,     \
                                      int64_t* order) {                                                           \
-    auto pg = project_all(mkscene(pos, logit, sh, ls, quat, n, deg), Cam<T>(cam), Opts<T>(opts));               \
+    auto pg = project_all<T, CT>(mkscene(pos, logit, sh, ls, quat, n, deg), Cam<T>(cam), Opts<T>(opts));       \
     auto v = composite_order(pg, active);                                                                        \
     std::copy(v.begin(), v.end(), order);                                                                        \
     return (int64_t)v.size();                                                                                    \
@@ -675,7 +741,7 @@ void export_proj(const std::vector<PG<T>>& pg, ProjOut* po) {
                                    int64_t n, int deg, const T* cam, const T* opts, const uint8_t* active,       \
                                    uint64_t* keys, uint32_t* vals, uint32_t* ranges, int64_t cap) {              \
     const Cam<T> c(cam);                                                                                         \
-    auto pg = project_all(mkscene(pos, logit, sh, ls, quat, n, deg), c, Opts<T>(opts));                         \
+    auto pg = project_all<T, CT>(mkscene(pos, logit, sh, ls, quat, n, deg), c, Opts<T>(opts));                 \
     std::vector<uint64_t> k; std::vector<uint32_t> v, r;                                                         \
     const int64_t P = bin_tiles(pg, active, c.W, c.H, &k, &v, &r);                                               \
     if (P <= cap) { std::copy(k.begin(), k.end(), keys); std::copy(v.begin(), v.end(), vals); }                  \
@@ -688,22 +754,26 @@ void export_proj(const std::vector<PG<T>>& pg, ProjOut* po) {
                                    int64_t* counters) {                                                          \
     Out o{img, alpha, depth, count, contrib};                                                                    \
     Counters k;                                                                                                  \
-    render<T>(mkscene(pos, logit, sh, ls, quat, n, deg), cam, opts, active, method, o, &k);                      \
+    render<T, CT>(mkscene(pos, logit, sh, ls, quat, n, deg), cam, opts, active, method, o, &k);                  \
     if (counters) { counters[0] = k.E; counters[1] = k.C; }                                                      \
   }                                                                                                              \
   extern "C" void orc_views_##SUF(const T* pos, const T* logit, const T* sh, const T* ls, const T* quat,        \
                                   int64_t n, int deg, const T* cams, int64_t n_views, const T* opts,             \
                                   int threads, int want_images, T* contrib, T* img_last, int64_t* counters) {    \
-    views<T>(mkscene(pos, logit, sh, ls, quat, n, deg), cams, n_views, opts, threads, want_images, contrib,       \
+    views<T, CT>(mkscene(pos, logit, sh, ls, quat, n, deg), cams, n_views, opts, threads, want_images, contrib,   \
              img_last, counters);                                                                                \
   }
 
-ORC_DEFINE(f32, float)
-ORC_DEFINE(f64, double)
+ORC_DEFINE(f32, float, false)
+ORC_DEFINE(f64, double, false)
+ORC_DEFINE(c64, double, true)
 
 // scalar access to the contract exponentials (device bit-compare tests)
 extern "C" void orc_exp2_contract(const float* x, float* y, int64_t n) {
   for (int64_t i = 0; i < n; ++i) y[i] = exp2_contract(x[i]);
+}
+extern "C" void orc_exp64_contract(const double* x, double* y, int64_t n) {
+  for (int64_t i = 0; i < n; ++i) y[i] = exp64_contract(x[i]);
 }
 extern "C" void orc_exp_contract(const float* x, float* y, int64_t n) {
   for (int64_t i = 0; i < n; ++i) y[i] = exp_contract(x[i]);

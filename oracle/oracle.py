@@ -3,8 +3,10 @@
 TEST INFRASTRUCTURE ONLY: imported by tests/, ``__graft_entry__.smoke()`` and
 bench.py's CPU-baseline legs as the checker; the product package never
 imports it. ``dtype=np.float32`` selects the Tier-A fp32 contract the CUDA
-path must reproduce bit for bit; ``np.float64`` the Tier-B restatement pinned
-against the reference's own outputs (tests/golden).
+path's RS_F32 frames reproduce bit for bit; ``np.float64`` the Tier-B
+restatement pinned against the reference's own outputs (tests/golden);
+``"c64"`` the Tier-C fp64 contract (Tier B with the contract exp and the
+culling-box gate) that RS_F64 frames reproduce bit for bit.
 """
 
 from __future__ import annotations
@@ -43,7 +45,7 @@ def lib():
             build()
         _lib = C.CDLL(str(LIB))
         vp, i64, i32 = C.c_void_p, C.c_int64, C.c_int
-        for suf in ("f32", "f64"):
+        for suf in ("f32", "f64", "c64"):
             getattr(_lib, f"orc_project_{suf}").argtypes = [vp] * 5 + [i64, i32, vp, vp, C.POINTER(ProjOut)]
             getattr(_lib, f"orc_order_{suf}").argtypes = [vp] * 5 + [i64, i32, vp, vp, vp, vp]
             getattr(_lib, f"orc_order_{suf}").restype = i64
@@ -53,6 +55,7 @@ def lib():
             getattr(_lib, f"orc_views_{suf}").argtypes = [vp] * 5 + [i64, i32, vp, i64, vp, i32, i32, vp, vp, vp]
         _lib.orc_exp2_contract.argtypes = [vp, vp, i64]
         _lib.orc_exp_contract.argtypes = [vp, vp, i64]
+        _lib.orc_exp64_contract.argtypes = [vp, vp, i64]
         _lib.orc_log2_contract.argtypes = [vp, vp, i64]
         _lib.orc_depth_key.argtypes = [C.c_float]
         _lib.orc_depth_key.restype = C.c_uint32
@@ -64,11 +67,19 @@ def _p(a):
 
 
 def _suf(dtype):
+    if isinstance(dtype, str) and dtype == "c64":
+        return "c64"
     return "f32" if np.dtype(dtype) == np.float32 else "f64"
+
+
+def _np(dtype):
+    """numpy value type of a tier (Tier C computes in float64)."""
+    return np.float64 if isinstance(dtype, str) and dtype == "c64" else np.dtype(dtype).type
 
 
 class _Scene:
     def __init__(self, scene, dtype):
+        dtype = _np(dtype)
         f = lambda a, shape: np.ascontiguousarray(np.asarray(a).reshape(shape), dtype=dtype)  # noqa: E731
         n = np.asarray(scene.positions).shape[0]
         self.n = n
@@ -84,6 +95,7 @@ class _Scene:
 
 
 def pack_camera(cam, dtype=np.float32) -> np.ndarray:
+    dtype = _np(dtype)
     """[W, H, fx, fy, cx, cy, R(9), t(3), C(3)]; C = -R^T t computed in fp64."""
     R = np.asarray(cam.rotation, np.float64)
     t = np.asarray(cam.translation, np.float64)
@@ -93,6 +105,7 @@ def pack_camera(cam, dtype=np.float32) -> np.ndarray:
 
 
 def pack_options(opts=None, dtype=np.float32) -> np.ndarray:
+    dtype = _np(dtype)
     if opts is None:
         v = [0.99, 1.0 / 255.0, 1e-4, 0.01, 0.3, 3.0]
     elif isinstance(opts, (list, tuple, np.ndarray)):
@@ -106,13 +119,13 @@ def project(scene, cam, opts=None, dtype=np.float32) -> dict:
     s = _Scene(scene, dtype)
     n = s.n
     out = dict(valid=np.zeros(n, np.uint8), x0=np.zeros(n, np.int32), x1=np.zeros(n, np.int32),
-               y0=np.zeros(n, np.int32), y1=np.zeros(n, np.int32), color=np.zeros((n, 3), dtype),
+               y0=np.zeros(n, np.int32), y1=np.zeros(n, np.int32), color=np.zeros((n, 3), _np(dtype)),
                na=np.zeros(n, np.float32), nb=np.zeros(n, np.float32), nc=np.zeros(n, np.float32),
                cut2=np.zeros(n, np.float32), cx0=np.zeros(n, np.int32), cx1=np.zeros(n, np.int32),
                cy0=np.zeros(n, np.int32), cy1=np.zeros(n, np.int32), bin=np.zeros(n, np.uint8),
                ell=np.zeros(n, np.uint8))
     for k in ("mx", "my", "a", "b", "c", "ia", "ib", "ic", "radius", "depth", "opacity"):
-        out[k] = np.zeros(n, dtype)
+        out[k] = np.zeros(n, _np(dtype))
     po = ProjOut()
     for k, _ in ProjOut._fields_:
         setattr(po, k, out[k].ctypes.data)
@@ -152,12 +165,13 @@ def render(scene, cam, opts=None, dtype=np.float32, active=None, method: int = 0
     """Render one view: img (H,W,3), alpha, depth, count, contrib (N,), E, C."""
     s = _Scene(scene, dtype)
     H, W = cam.height, cam.width
-    img = np.zeros((H, W, 3), dtype)
-    alpha = np.zeros((H, W), dtype)
-    depth = np.zeros((H, W), dtype)
+    vt = _np(dtype)
+    img = np.zeros((H, W, 3), vt)
+    alpha = np.zeros((H, W), vt)
+    depth = np.zeros((H, W), vt)
     count = np.zeros((H, W), np.int32)
-    contrib = np.zeros(s.n, dtype) if contrib is None else contrib
-    assert contrib.dtype == np.dtype(dtype) and contrib.flags.c_contiguous
+    contrib = np.zeros(s.n, vt) if contrib is None else contrib
+    assert contrib.dtype == np.dtype(vt) and contrib.flags.c_contiguous
     k = np.zeros(2, np.int64)
     act = None if active is None else np.ascontiguousarray(active, np.uint8)
     getattr(lib(), f"orc_render_{_suf(dtype)}")(*s.args(), _p(pack_camera(cam, dtype)),
@@ -172,8 +186,8 @@ def views(scene, cams, opts=None, dtype=np.float32, threads: int | None = None,
     s = _Scene(scene, dtype)
     threads = threads or os.cpu_count() or 1
     cp = np.ascontiguousarray(np.stack([pack_camera(c, dtype) for c in cams]))
-    contrib = np.zeros(s.n, dtype) if scores else None
-    last = np.zeros((cams[-1].height, cams[-1].width, 3), dtype) if images else None
+    contrib = np.zeros(s.n, _np(dtype)) if scores else None
+    last = np.zeros((cams[-1].height, cams[-1].width, 3), _np(dtype)) if images else None
     k = np.zeros(2, np.int64)
     getattr(lib(), f"orc_views_{_suf(dtype)}")(*s.args(), _p(cp), len(cams), _p(pack_options(opts, dtype)),
                                                int(threads), int(images), _p(contrib), _p(last), _p(k))
@@ -184,6 +198,13 @@ def exp2_contract(x: np.ndarray) -> np.ndarray:
     x = np.ascontiguousarray(x, np.float32)
     y = np.empty_like(x)
     lib().orc_exp2_contract(_p(x), _p(y), x.size)
+    return y
+
+
+def exp64_contract(x: np.ndarray) -> np.ndarray:
+    x = np.ascontiguousarray(x, np.float64)
+    y = np.empty_like(x)
+    lib().orc_exp64_contract(_p(x), _p(y), x.size)
     return y
 
 

@@ -17,6 +17,8 @@ LIB_PATH = Path(__file__).resolve().parent / "libradsplat_b200.so"
 RS_OK, RS_EINVAL, RS_ENONFINITE, RS_ENOMEM_WORKSPACE, RS_ECUDA, RS_EOVERFLOW = range(6)
 RS_FLAG_COUNT_EVALS = 1
 RS_FLAG_BLEND_1PX = 2
+RS_F32, RS_F64 = 0, 1
+ABI_VERSION = 2
 
 
 class NativeUnavailable(RuntimeError):
@@ -33,18 +35,19 @@ class PairOverflow(RuntimeError):
 
 class RsScene(C.Structure):
     _fields_ = [("planes", C.c_void_p), ("sh", C.c_void_p), ("n", C.c_int64), ("plane_stride", C.c_int64),
-                ("sh_degree", C.c_int32), ("_pad", C.c_int32)]
+                ("sh_degree", C.c_int32), ("dtype", C.c_int32)]
 
 
 class RsCamera(C.Structure):
-    _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("fx", C.c_float), ("fy", C.c_float),
-                ("cx", C.c_float), ("cy", C.c_float), ("R", C.c_float * 9), ("t", C.c_float * 3),
-                ("center", C.c_float * 3)]
+    _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("fx", C.c_double), ("fy", C.c_double),
+                ("cx", C.c_double), ("cy", C.c_double), ("R", C.c_double * 9), ("t", C.c_double * 3),
+                ("center", C.c_double * 3)]
 
 
 class RsOptions(C.Structure):
-    _fields_ = [(n, C.c_float) for n in
-                ("alpha_max", "alpha_cut", "tau_stop", "near_limit", "lowpass", "sigma_bound")]
+    _fields_ = [(n, C.c_double) for n in
+                ("alpha_max", "alpha_cut", "tau_stop", "near_limit", "lowpass", "sigma_bound")] + \
+               [("precision", C.c_int32), ("_pad", C.c_int32)]
 
 
 class RsOutputs(C.Structure):
@@ -55,11 +58,12 @@ class RsOutputs(C.Structure):
 class RsStats(C.Structure):
     _fields_ = [("n_items", C.c_uint32), ("n_visible", C.c_uint32), ("n_pairs", C.c_uint32),
                 ("overflow", C.c_uint32), ("evals", C.c_uint64), ("composites", C.c_uint64),
-                ("pairs_needed", C.c_uint64)]
+                ("pairs_needed", C.c_uint64), ("bad_index", C.c_uint32), ("_pad", C.c_uint32)]
 
 
 class RsBuffers(C.Structure):
-    _fields_ = [("records", C.c_void_p), ("items_sorted", C.c_void_p), ("pair_items", C.c_void_p),
+    _fields_ = [("records", C.c_void_p), ("records64", C.c_void_p), ("items_sorted", C.c_void_p),
+                ("pair_items", C.c_void_p),
                 ("ranges", C.c_void_p), ("counters", C.c_void_p), ("tiles_x", C.c_int32),
                 ("tiles_y", C.c_int32)]
 
@@ -85,6 +89,7 @@ SIGNATURES = {
     "rs_blend_ex": (_i32, [_vp, C.POINTER(RsOptions), C.POINTER(RsOutputs), _vp, _u32, _vp]),
     "rs_read_stats": (_i32, [_vp, C.POINTER(RsStats), _vp]),
     "rs_read_overflow": (_i32, [_vp, C.POINTER(_u32), C.POINTER(C.c_uint64), _i32, _vp]),
+    "rs_read_sticky": (_i32, [_vp, C.POINTER(_u32), C.POINTER(C.c_uint64), C.POINTER(_u32), _i32, _vp]),
     "rs_get_buffers": (_i32, [_vp, C.POINTER(RsBuffers)]),
     "rs_compact_workspace_size": (_sz, [_i64]),
     "rs_compact": (_i32, [_vp, _i64, _vp, _vp, _vp, _sz, _vp]),
@@ -116,7 +121,7 @@ def load(require_cuda: bool = True):
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.rs_abi_version() != 1:
+        if lib.rs_abi_version() != ABI_VERSION:
             raise NativeUnavailable("ABI version mismatch")
         _lib = lib
     if require_cuda:

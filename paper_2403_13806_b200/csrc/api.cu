@@ -1,5 +1,5 @@
 // api.cu -- the C ABI (include/radsplat.h): workspace layout and the frame
-// pipeline  project -> depth sort -> pair emission -> tile sort -> blend.
+// pipeline  project -> depth sort -> row segments -> per-tile lists -> blend.
 //
 // One translation unit: the kernels live in the .cuh files next to this one.
 // Build: see paper_2403_13806_b200/build.py (nvcc -gencode arch=compute_100a,
@@ -13,6 +13,7 @@
 
 #include "segbin.cuh"
 #include "blend.cuh"
+#include "blend64.cuh"
 #include "compact.cuh"
 #include "io.cuh"
 #include "metrics.cuh"
@@ -61,7 +62,7 @@ size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 struct Layout {
   // per-frame zeroed region [0, frame_bytes)
   size_t ctr, hist, proj_lb, ranges, frame_bytes;
-  size_t sticky, cam, recs, rows, sgrad, titem, keysA, keysB, valsA, valsB, rowtab, rowcnt, segitem, segspan, geom,
+  size_t sticky, cam, recs, recs64, rows, sgrad, titem, keysA, keysB, valsA, valsB, rowtab, rowcnt, segitem, segspan, geom,
       rowstart, chunkstart, chunkcnt, chunkinfo, densel, tilecnt, tileord, pitem, lbA, lbB, total;
 };
 
@@ -88,8 +89,9 @@ Layout make_layout(int64_t n_cap, int64_t pair_cap, int W, int H) {
   L.ranges = take(TW * TH * sizeof(uint2));
   L.frame_bytes = o;
   L.sticky = take(sizeof(Sticky));
-  L.cam = take(sizeof(rs_camera));
+  L.cam = take(sizeof(CamPair));
   L.recs = take((size_t)n_cap * sizeof(Rec));
+  L.recs64 = take((size_t)n_cap * sizeof(Rec64));  // RS_F64 frames
   L.rows = take((size_t)n_cap * 4);  // per binned item its tile-row range
   L.sgrad = take((size_t)n_cap * 4 * kSGrad);  // rs_backward: screen-space gradient sums per item
   L.titem = take((size_t)n_cap);
@@ -146,6 +148,7 @@ struct rs_workspace {
   uint32_t n_items;
   int W, H, TW, TH;
   bool binned, have_cam, has_color;
+  bool f64;  // precision of the current frame (rs_options.precision == RS_F64)
   cudaStream_t aux = nullptr;  // second stream (dense expansion next to the sparse one)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 
@@ -161,6 +164,16 @@ struct rs_workspace {
 namespace {
 
 cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// the fp32 path's options: each value rounded once (round to nearest = numpy astype(float32))
+Opt32 opt32(const rs_options& o) {
+  return Opt32{(float)o.alpha_max, (float)o.alpha_cut, (float)o.tau_stop, (float)o.near_limit, (float)o.lowpass,
+               (float)o.sigma_bound};
+}
+Opt64 opt64(const rs_options& o) {
+  return Opt64{o.alpha_max, o.alpha_cut, o.tau_stop, o.near_limit, o.lowpass, o.sigma_bound};
+}
+bool valid_options(const rs_options* o) { return o && (o->precision == RS_F32 || o->precision == RS_F64); }
 
 int32_t cuda_status() { return cudaGetLastError() == cudaSuccess ? RS_OK : RS_ECUDA; }
 
@@ -295,17 +308,50 @@ int32_t rs_set_camera(rs_workspace* ws, const rs_camera* cam, void* stream) {
   ws->TW = TW;
   ws->TH = TH;
   ws->have_cam = true;
+  // both precisions' cameras: the fp32 one rounded once here (round to nearest)
+  CamPair cp;
+  cp.c64 = *cam;
+  Cam32& c = cp.c32;
+  c.width = cam->width;
+  c.height = cam->height;
+  c.fx = (float)cam->fx; c.fy = (float)cam->fy; c.cx = (float)cam->cx; c.cy = (float)cam->cy;
+  for (int k = 0; k < 9; ++k) c.R[k] = (float)cam->R[k];
+  for (int k = 0; k < 3; ++k) { c.t[k] = (float)cam->t[k]; c.center[k] = (float)cam->center[k]; }
   // stream-ordered upload; from pageable memory the driver stages it at once, so the
   // caller may reuse `cam` immediately (a captured frame graph then replays it)
-  cudaMemcpyAsync(ws->at<rs_camera>(ws->L.cam), cam, sizeof(rs_camera), cudaMemcpyHostToDevice, S(stream));
+  cudaMemcpyAsync(ws->at<CamPair>(ws->L.cam), &cp, sizeof(CamPair), cudaMemcpyHostToDevice, S(stream));
   return cuda_status();
 }
 
+}  // extern "C"
+
+template <bool FULL, bool COLOR, typename TS>
+static void launch_project(rs_workspace* ws, const rs_scene* scene, const int32_t* active_idx, uint32_t items,
+                           const rs_options* opts, void* full, int32_t* full_bbox, cudaStream_t st) {
+  const unsigned grid = (items + kProjThreads - 1) / kProjThreads;
+  const TS* planes = static_cast<const TS*>(scene->planes);
+  const TS* sh = static_cast<const TS*>(scene->sh);
+  CamPair* cp = ws->at<CamPair>(ws->L.cam);
+  if (ws->f64)
+    launch(project64_kernel<FULL, COLOR, TS>, grid, kProjThreads, 0, st, planes, sh, scene->plane_stride,
+           scene->sh_degree, active_idx, items, scene->n, &cp->c64, opt64(*opts), ws->at<Rec>(ws->L.recs),
+           ws->at<Rec64>(ws->L.recs64), ws->at<uint32_t>(ws->L.keysB), ws->at<uint32_t>(ws->L.rows), ws->ctr(),
+           ws->at<Sticky>(ws->L.sticky), static_cast<double*>(full), reinterpret_cast<int4*>(full_bbox));
+  else
+    launch(project_kernel<FULL, COLOR, TS>, grid, kProjThreads, 0, st, planes, sh, scene->plane_stride,
+           scene->sh_degree, active_idx, items, scene->n, &cp->c32, opt32(*opts), ws->at<Rec>(ws->L.recs),
+           ws->at<uint32_t>(ws->L.keysB), ws->at<uint32_t>(ws->L.rows), ws->ctr(), ws->at<Sticky>(ws->L.sticky),
+           static_cast<float*>(full), reinterpret_cast<int4*>(full_bbox));
+}
+
+extern "C" {
+
 static int32_t project_impl(rs_workspace* ws, const rs_scene* scene, const int32_t* active_idx, int64_t m,
-                            const rs_camera* cam, const rs_options* opts, float* full, int32_t* full_bbox,
+                            const rs_camera* cam, const rs_options* opts, void* full, int32_t* full_bbox,
                             bool color, void* stream) {
-  if (!ws || !scene || !opts || !scene->planes || !scene->sh || scene->sh_degree < 0 || scene->sh_degree > 3 ||
-      scene->n < 0 || scene->plane_stride < scene->n || (reinterpret_cast<uintptr_t>(scene->sh) & 15))
+  if (!ws || !scene || !valid_options(opts) || !scene->planes || !scene->sh || scene->sh_degree < 0 ||
+      scene->sh_degree > 3 || scene->n < 0 || scene->plane_stride < scene->n ||
+      (scene->dtype != RS_F32 && scene->dtype != RS_F64) || (reinterpret_cast<uintptr_t>(scene->sh) & 15))
     return RS_EINVAL;
   const int64_t items = active_idx ? m : scene->n;
   if (items < 0) return RS_EINVAL;
@@ -322,18 +368,20 @@ static int32_t project_impl(rs_workspace* ws, const rs_scene* scene, const int32
   ws->n_items = (uint32_t)items;
   ws->binned = false;
   ws->has_color = color || full;
+  ws->f64 = opts->precision == RS_F64;
   if (items > 0) {
-    const unsigned grid = (unsigned)((items + kProjThreads - 1) / kProjThreads);
-    if (full)
-      launch(project_kernel<true, true>, grid, kProjThreads, 0, st, scene->planes, scene->sh,
-             scene->plane_stride, scene->sh_degree, active_idx, (uint32_t)items, ws->at<rs_camera>(ws->L.cam),
-             *opts, ws->at<Rec>(ws->L.recs), ws->at<uint32_t>(ws->L.keysB), ws->at<uint32_t>(ws->L.rows),
-             ws->ctr(), full, reinterpret_cast<int4*>(full_bbox));
-    else
-      launch((color ? project_kernel<false, true> : project_kernel<false, false>), grid, kProjThreads, 0, st,
-             scene->planes, scene->sh, scene->plane_stride, scene->sh_degree, active_idx, (uint32_t)items,
-             ws->at<rs_camera>(ws->L.cam), *opts, ws->at<Rec>(ws->L.recs), ws->at<uint32_t>(ws->L.keysB),
-             ws->at<uint32_t>(ws->L.rows), ws->ctr(), nullptr, nullptr);
+    const uint32_t n = (uint32_t)items;
+    const bool d = scene->dtype == RS_F64;
+    if (full) {
+      if (d) launch_project<true, true, double>(ws, scene, active_idx, n, opts, full, full_bbox, st);
+      else launch_project<true, true, float>(ws, scene, active_idx, n, opts, full, full_bbox, st);
+    } else if (color) {
+      if (d) launch_project<false, true, double>(ws, scene, active_idx, n, opts, nullptr, nullptr, st);
+      else launch_project<false, true, float>(ws, scene, active_idx, n, opts, nullptr, nullptr, st);
+    } else {
+      if (d) launch_project<false, false, double>(ws, scene, active_idx, n, opts, nullptr, nullptr, st);
+      else launch_project<false, false, float>(ws, scene, active_idx, n, opts, nullptr, nullptr, st);
+    }
   }
   return cuda_status();
 }
@@ -344,7 +392,7 @@ int32_t rs_project(rs_workspace* ws, const rs_scene* scene, const int32_t* activ
 }
 
 int32_t rs_project_full(rs_workspace* ws, const rs_scene* scene, const int32_t* active_idx, int64_t m,
-                        const rs_camera* cam, const rs_options* opts, float* out_proj, int32_t* out_bbox,
+                        const rs_camera* cam, const rs_options* opts, void* out_proj, int32_t* out_bbox,
                         void* stream) {
   if (!out_proj || !out_bbox) return RS_EINVAL;
   return project_impl(ws, scene, active_idx, m, cam, opts, out_proj, out_bbox, true, stream);
@@ -365,7 +413,10 @@ int32_t rs_bin(rs_workspace* ws, void* stream) {
     run_sort<uint32_t, kDepthItems>(ws, ws->at<uint32_t>(ws->L.keysA), ws->at<uint32_t>(ws->L.keysA),
                                     ws->at<uint32_t>(ws->L.keysB), ws->at<uint32_t>(ws->L.valsA),
                                     ws->at<uint32_t>(ws->L.valsA), ws->at<uint32_t>(ws->L.valsB), nvis, 0, n, 32,
-                                    0, 0, false, st, &keys_res, &items_sorted);
+                                    0, 0, ws->f64, st, &keys_res, &items_sorted);
+    if (ws->f64)  // fp32-rounded depth keys: runs of equal keys re-ordered by the fp64 depth
+      launch(tiefix_kernel, std::min((n + 255) / 256, (uint32_t)ws->sms * 8), 256, 0, st, keys_res,
+             const_cast<uint32_t*>(items_sorted), nvis, ws->at<Rec64>(ws->L.recs64));
     // row segments: per rank chunk and row counts, their per-row prefix, each segment placed
     // in row-major depth-stable order; per-tile ranges, expansion into the per-tile lists
     // (segbin.cuh)
@@ -415,9 +466,10 @@ int32_t rs_bin(rs_workspace* ws, void* stream) {
 
 static const uint32_t* final_pair_items(const rs_workspace* ws) { return ws->at<uint32_t>(ws->L.pitem); }
 
-int32_t rs_blend_ex(rs_workspace* ws, const rs_options* opts, const rs_outputs* out_p, uint32_t* scores,
+int32_t rs_blend_ex(rs_workspace* ws, const rs_options* opts, const rs_outputs* out_p, void* scores_v,
                     uint32_t flags, void* stream) {
-  if (!ws || !opts || !ws->binned) return RS_EINVAL;
+  if (!ws || !valid_options(opts) || !ws->binned) return RS_EINVAL;
+  if ((opts->precision == RS_F64) != ws->f64) return RS_EINVAL;  // not the precision of the projection
   rs_outputs out{};
   if (out_p) out = *out_p;
   if ((out.rgb != nullptr) != (out.alpha != nullptr) || (out.rgb != nullptr) != (out.count != nullptr) ||
@@ -425,10 +477,10 @@ int32_t rs_blend_ex(rs_workspace* ws, const rs_options* opts, const rs_outputs* 
     return RS_EINVAL;
   const bool color = out.rgb || out.rgb64 || out.depth || out.tau;
   if ((out.tau != nullptr) != (out.last != nullptr)) return RS_EINVAL;
+  if (out.tau && ws->f64) return RS_EINVAL;  // the training outputs are fp32-path only
   if (color && !ws->has_color) return RS_EINVAL;  // projected by a score-only rs_render
-  if (!color && !scores) return RS_EINVAL;
+  if (!color && !scores_v) return RS_EINVAL;
   const bool stats = (flags & RS_FLAG_COUNT_EVALS) != 0;
-  const bool one_px = (flags & RS_FLAG_BLEND_1PX) != 0 && !out.tau;  // the training outputs: 2-px kernel
   cudaStream_t st = S(stream);
   const int T = ws->TW * ws->TH;
   const uint2* ranges = ws->at<uint2>(ws->L.ranges);
@@ -441,28 +493,56 @@ int32_t rs_blend_ex(rs_workspace* ws, const rs_options* opts, const rs_outputs* 
   struct Restore {
     ~Restore() { g_pdl_class = kPdlChain; }
   } restore;
+  if (ws->f64) {
+    const Out64 o64{static_cast<double*>(out.rgb), static_cast<double*>(out.alpha), static_cast<double*>(out.depth),
+                    out.count, out.rgb64, out.alpha64, out.count64};
+    const Opt64 op = opt64(*opts);
+    const Rec64* r64 = ws->at<Rec64>(ws->L.recs64);
+    auto* sc = static_cast<unsigned long long*>(scores_v);
+    const bool fast = opts->alpha_cut >= 1e-300;  // exp64_hot's normal range (blend64.cuh)
+#define RS_B64(C, I, K, F) \
+  launch(blend64_kernel<C, I, K, F>, T, kBlend64Threads, 0, st, ranges, items, recs, r64, geom, order, ctr, ws->W, \
+         ws->H, ws->TW, op, o64, sc)
+#define RS_B64_F(C, I, K) \
+  if (fast) { RS_B64(C, I, K, true); } else { RS_B64(C, I, K, false); }
+    if (color && sc) {
+      if (stats) { RS_B64_F(true, true, true); } else { RS_B64_F(true, true, false); }
+    } else if (color) {
+      if (stats) { RS_B64_F(true, false, true); } else { RS_B64_F(true, false, false); }
+    } else {
+      if (stats) { RS_B64_F(false, true, true); } else { RS_B64_F(false, true, false); }
+    }
+#undef RS_B64_F
+#undef RS_B64
+    return cuda_status();
+  }
+  const Out32 o32{static_cast<float*>(out.rgb), static_cast<float*>(out.alpha), static_cast<float*>(out.depth),
+                  out.count, out.rgb64, out.alpha64, out.count64, out.tau, out.last};
+  const Opt32 op = opt32(*opts);
+  uint32_t* scores = static_cast<uint32_t*>(scores_v);
+  const bool one_px = (flags & RS_FLAG_BLEND_1PX) != 0 && !out.tau;  // the training outputs: 2-px kernel
 #define RS_BLEND(C, I, K, F)                                                                              \
   if (one_px)                                                                                             \
     launch(blend_kernel<C, I, K, F>, T, kBlendThreads, 0, st, ranges, items, recs, ctr, ws->W, ws->H,     \
-           ws->TW, *opts, out, scores);                                                                    \
+           ws->TW, op, o32, scores);                                                                       \
   else                                                                                                    \
     launch(blend2_kernel<C, I, K, F>, T, kBlend2Threads, 0, st, ranges, items, recs, geom, order, ctr,    \
-           ws->W, ws->H, ws->TW, *opts, out, scores)
+           ws->W, ws->H, ws->TW, op, o32, scores)
 #define RS_BLEND_F(C, I, K) \
   if (fast) { RS_BLEND(C, I, K, true); } else { RS_BLEND(C, I, K, false); }
   // exact-range exp2 is only needed for degenerate options (see blend.cuh FAST)
-  const bool fast = opts->alpha_cut >= 1e-30f;
+  const bool fast = op.alpha_cut >= 1e-30f;
   if (out.tau) {  // training forward (rasterize_cached): records tau and the last composite per pixel
     if (scores) {
       if (fast) launch(blend2_kernel<true, true, false, true, true>, T, kBlend2Threads, 0, st, ranges, items,
-                       recs, geom, order, ctr, ws->W, ws->H, ws->TW, *opts, out, scores);
+                       recs, geom, order, ctr, ws->W, ws->H, ws->TW, op, o32, scores);
       else launch(blend2_kernel<true, true, false, false, true>, T, kBlend2Threads, 0, st, ranges, items, recs,
-                  geom, order, ctr, ws->W, ws->H, ws->TW, *opts, out, scores);
+                  geom, order, ctr, ws->W, ws->H, ws->TW, op, o32, scores);
     } else {
       if (fast) launch(blend2_kernel<true, false, false, true, true>, T, kBlend2Threads, 0, st, ranges, items,
-                       recs, geom, order, ctr, ws->W, ws->H, ws->TW, *opts, out, scores);
+                       recs, geom, order, ctr, ws->W, ws->H, ws->TW, op, o32, scores);
       else launch(blend2_kernel<true, false, false, false, true>, T, kBlend2Threads, 0, st, ranges, items, recs,
-                  geom, order, ctr, ws->W, ws->H, ws->TW, *opts, out, scores);
+                  geom, order, ctr, ws->W, ws->H, ws->TW, op, o32, scores);
     }
   } else if (color && scores) {
     if (stats) { RS_BLEND_F(true, true, true); } else { RS_BLEND_F(true, true, false); }
@@ -476,15 +556,15 @@ int32_t rs_blend_ex(rs_workspace* ws, const rs_options* opts, const rs_outputs* 
   return cuda_status();
 }
 
-int32_t rs_blend(rs_workspace* ws, const rs_options* opts, float* out_rgb, float* out_alpha, float* out_depth,
-                 int32_t* out_count, uint32_t* scores, uint32_t flags, void* stream) {
+int32_t rs_blend(rs_workspace* ws, const rs_options* opts, void* out_rgb, void* out_alpha, void* out_depth,
+                 int32_t* out_count, void* scores, uint32_t flags, void* stream) {
   if (out_rgb && (!out_alpha || !out_depth || !out_count)) return RS_EINVAL;
   const rs_outputs out{out_rgb, out_alpha, out_depth, out_count, nullptr, nullptr, nullptr, nullptr, nullptr};
   return rs_blend_ex(ws, opts, &out, scores, flags, stream);
 }
 
 int32_t rs_render_ex(rs_workspace* ws, const rs_scene* scene, const int32_t* active_idx, int64_t m,
-                     const rs_camera* cam, const rs_options* opts, const rs_outputs* out, uint32_t* scores,
+                     const rs_camera* cam, const rs_options* opts, const rs_outputs* out, void* scores,
                      uint32_t flags, void* stream) {
   // a score-only frame (no image outputs) projects without the SH colour
   const bool color = out && (out->rgb || out->rgb64 || out->depth || out->tau);
@@ -495,8 +575,8 @@ int32_t rs_render_ex(rs_workspace* ws, const rs_scene* scene, const int32_t* act
 }
 
 int32_t rs_render(rs_workspace* ws, const rs_scene* scene, const int32_t* active_idx, int64_t m,
-                  const rs_camera* cam, const rs_options* opts, float* out_rgb, float* out_alpha, float* out_depth,
-                  int32_t* out_count, uint32_t* scores, uint32_t flags, void* stream) {
+                  const rs_camera* cam, const rs_options* opts, void* out_rgb, void* out_alpha, void* out_depth,
+                  int32_t* out_count, void* scores, uint32_t flags, void* stream) {
   if (out_rgb && (!out_alpha || !out_depth || !out_count)) return RS_EINVAL;
   const rs_outputs out{out_rgb, out_alpha, out_depth, out_count, nullptr, nullptr, nullptr, nullptr, nullptr};
   return rs_render_ex(ws, scene, active_idx, m, cam, opts, &out, scores, flags, stream);
@@ -506,9 +586,10 @@ int32_t rs_backward(rs_workspace* ws, const rs_scene* scene, const int32_t* acti
                     const rs_options* opts, const float* grad_image, const float* tau, const int32_t* last,
                     float* g_pos, float* g_sh, float* g_ls, float* g_quat, float* g_logit, float* g_mean2d,
                     uint8_t* touched, void* stream) {
-  if (!ws || !scene || !opts || !grad_image || !tau || !last || !g_pos || !g_sh || !g_ls || !g_quat || !g_logit ||
-      !g_mean2d || !touched || !ws->binned || !ws->has_color)
-    return RS_EINVAL;
+  if (!ws || !scene || !valid_options(opts) || !grad_image || !tau || !last || !g_pos || !g_sh || !g_ls || !g_quat ||
+      !g_logit || !g_mean2d || !touched || !ws->binned || !ws->has_color || ws->f64 ||
+      opts->precision != RS_F32 || scene->dtype != RS_F32)
+    return RS_EINVAL;  // the training pair is the fp32 path
   const int64_t items = active_idx ? m : scene->n;
   if (items != (int64_t)ws->n_items) return RS_EINVAL;  // not the frame rs_render_ex just produced
   cudaStream_t st = S(stream);
@@ -525,14 +606,15 @@ int32_t rs_backward(rs_workspace* ws, const rs_scene* scene, const int32_t* acti
   if (items == 0) return cuda_status();
   cudaMemsetAsync(ws->at<float>(ws->L.sgrad), 0, (size_t)items * 4 * kSGrad, st);
   cudaMemsetAsync(ws->at<uint8_t>(ws->L.titem), 0, (size_t)items, st);
-  auto* bwd = opts->alpha_cut >= 1e-30f ? backward2_kernel<true> : backward2_kernel<false>;
+  const Opt32 op = opt32(*opts);
+  auto* bwd = op.alpha_cut >= 1e-30f ? backward2_kernel<true> : backward2_kernel<false>;
   launch(bwd, ws->TW * ws->TH, kBwd2Threads, 0, st, ws->at<uint2>(ws->L.ranges), final_pair_items(ws),
          ws->at<Rec>(ws->L.recs), ws->at<float4>(ws->L.geom), ws->at<uint32_t>(ws->L.tileord), ws->ctr(), ws->W,
-         ws->H, ws->TW, *opts, grad_image, tau, last, ws->at<float>(ws->L.sgrad), ws->at<uint8_t>(ws->L.titem));
-  launch(chain_kernel, (unsigned)((items + 127) / 128), 128, 0, st, scene->planes, scene->sh,
-         scene->plane_stride, scene->sh_degree, active_idx, (uint32_t)items, ws->at<rs_camera>(ws->L.cam),
-         *opts, ws->at<float>(ws->L.sgrad), ws->at<uint8_t>(ws->L.titem), g_pos, g_sh, g_ls, g_quat, g_logit,
-         g_mean2d, touched);
+         ws->H, ws->TW, op, grad_image, tau, last, ws->at<float>(ws->L.sgrad), ws->at<uint8_t>(ws->L.titem));
+  launch(chain_kernel, (unsigned)((items + 127) / 128), 128, 0, st, static_cast<const float*>(scene->planes),
+         static_cast<const float*>(scene->sh), scene->plane_stride, scene->sh_degree, active_idx, (uint32_t)items,
+         &ws->at<CamPair>(ws->L.cam)->c32, op, ws->at<float>(ws->L.sgrad), ws->at<uint8_t>(ws->L.titem), g_pos,
+         g_sh, g_ls, g_quat, g_logit, g_mean2d, touched);
   return cuda_status();
 }
 
@@ -548,6 +630,8 @@ int32_t rs_read_stats(rs_workspace* ws, rs_stats* out, void* stream) {
   out->evals = c.evals;
   out->composites = c.composites;
   out->pairs_needed = c.pairs_needed;
+  out->bad_index = c.bad_index;
+  out->_pad = 0;
   return RS_OK;
 }
 
@@ -564,9 +648,25 @@ int32_t rs_read_overflow(rs_workspace* ws, uint32_t* out_overflowed, uint64_t* o
   return RS_OK;
 }
 
+int32_t rs_read_sticky(rs_workspace* ws, uint32_t* out_overflowed, uint64_t* out_pairs_needed_max,
+                       uint32_t* out_bad_index, int32_t reset, void* stream) {
+  if (!out_bad_index) return RS_EINVAL;
+  Sticky h;
+  if (!ws || !out_overflowed || !out_pairs_needed_max) return RS_EINVAL;
+  Sticky* d = ws->at<Sticky>(ws->L.sticky);
+  if (cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, S(stream)) != cudaSuccess) return RS_ECUDA;
+  if (reset && cudaMemsetAsync(d, 0, sizeof(Sticky), S(stream)) != cudaSuccess) return RS_ECUDA;
+  if (cudaStreamSynchronize(S(stream)) != cudaSuccess) return RS_ECUDA;
+  *out_overflowed = h.overflowed;
+  *out_pairs_needed_max = h.pairs_needed_max;
+  *out_bad_index = h.bad_index;
+  return RS_OK;
+}
+
 int32_t rs_get_buffers(rs_workspace* ws, rs_buffers* out) {
   if (!ws || !out) return RS_EINVAL;
   out->records = ws->at<void>(ws->L.recs);
+  out->records64 = ws->at<void>(ws->L.recs64);
   out->items_sorted = ws->at<uint32_t>(ws->L.valsA);  // 4 depth passes end in A
   out->pair_items = final_pair_items(ws);
   out->ranges = ws->at<uint32_t>(ws->L.ranges);
@@ -610,11 +710,20 @@ int32_t rs_compact_bits(const uint8_t* bits, int64_t n, int32_t* out_idx, uint32
 
 int32_t rs_check_finite(const rs_scene* scene, uint32_t* out_bad, void* stream) {
   if (!scene || !out_bad || scene->n < 0 || (scene->n > 0 && (!scene->planes || !scene->sh)) ||
-      scene->plane_stride < scene->n)
+      scene->plane_stride < scene->n || (scene->dtype != RS_F32 && scene->dtype != RS_F64))
     return RS_EINVAL;
   cudaStream_t st = S(stream);
   cudaMemsetAsync(out_bad, 0, 4, st);
-  if (scene->n > 0) finite_kernel<<<1184, 256, 0, st>>>(scene->planes, scene->sh, scene->n, scene->plane_stride, out_bad);
+  if (scene->n > 0) {
+    if (scene->dtype == RS_F64)
+      finite_kernel<double><<<1184, 256, 0, st>>>(static_cast<const double*>(scene->planes),
+                                                  static_cast<const double*>(scene->sh), scene->n,
+                                                  scene->plane_stride, out_bad);
+    else
+      finite_kernel<float><<<1184, 256, 0, st>>>(static_cast<const float*>(scene->planes),
+                                                 static_cast<const float*>(scene->sh), scene->n,
+                                                 scene->plane_stride, out_bad);
+  }
   return cuda_status();
 }
 

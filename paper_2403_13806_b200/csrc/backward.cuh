@@ -43,7 +43,7 @@ template <bool FAST>
 __global__ void __launch_bounds__(kBwd2Threads) backward2_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ pair_items, const Rec* __restrict__ recs,
     const float4* __restrict__ geom, const uint32_t* __restrict__ tile_order, const Counters* __restrict__ ctr,
-    int W, int H, int TW, rs_options o, const float* __restrict__ grad_image, const float* __restrict__ tau_final, const int32_t* __restrict__ last,
+    int W, int H, int TW, Opt32 o, const float* __restrict__ grad_image, const float* __restrict__ tau_final, const int32_t* __restrict__ last,
     float* __restrict__ sgrad, uint8_t* __restrict__ touched) {
   pdl_wait();
   pdl_trigger();
@@ -263,7 +263,7 @@ __device__ __forceinline__ void quat_rotmat_backward(const float q[4], const flo
 
 __global__ void __launch_bounds__(128) chain_kernel(
     const float* __restrict__ planes, const float* __restrict__ sh, int64_t stride, int deg,
-    const int32_t* __restrict__ active_idx, uint32_t n_items, const rs_camera* __restrict__ camp, rs_options o,
+    const int32_t* __restrict__ active_idx, uint32_t n_items, const Cam32* __restrict__ camp, Opt32 o,
     const float* __restrict__ sgrad, const uint8_t* __restrict__ touched, float* __restrict__ g_pos,
     float* __restrict__ g_sh, float* __restrict__ g_ls, float* __restrict__ g_quat, float* __restrict__ g_logit,
     float* __restrict__ g_mean2d, uint8_t* __restrict__ touched_out) {
@@ -289,7 +289,7 @@ __global__ void __launch_bounds__(128) chain_kernel(
     }
     return;
   }
-  const rs_camera cam = *camp;
+  const Cam32 cam = *camp;
   const float* P = planes + i;
   const float* S = sgrad + (size_t)kSGrad * item;
   const float p[3] = {P[0], P[stride], P[2 * stride]};

@@ -39,7 +39,7 @@ namespace rs {
 template <bool COLOR, bool CONTRIB, bool STATS, bool FAST>
 __global__ void __launch_bounds__(kBlendThreads) blend_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ pair_items, const Rec* __restrict__ recs,
-    Counters* __restrict__ ctr, int W, int H, int TW, rs_options o, const rs_outputs out,
+    Counters* __restrict__ ctr, int W, int H, int TW, Opt32 o, const Out32 out,
     uint32_t* __restrict__ scores) {
   pdl_wait();
   pdl_trigger();
@@ -218,7 +218,7 @@ constexpr int kBlendUnroll = RS_BLEND_UNROLL;  // list entries per inner iterati
 
 template <bool COLOR, bool STATS, bool FAST>
 __device__ __forceinline__ float blend_px(const float4 ga, const float4 gb, const float4 gc, float xs, float ys,
-                                          const rs_options& o, float& tau, float& cr, float& cg, float& cb,
+                                          const Opt32& o, float& tau, float& cr, float& cg, float& cb,
                                           float& cd, int& cnt, bool& done, unsigned long long& evals) {
   if (STATS) ++evals;
   const float dx = __fsub_rn(xs, ga.x), dy = __fsub_rn(ys, ga.y);
@@ -254,7 +254,7 @@ template <bool COLOR, bool CONTRIB, bool STATS, bool FAST, bool TRAIN = false>
 __global__ void __launch_bounds__(kBlend2Threads, RS_BLEND_MINB) blend2_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ pair_items, const Rec* __restrict__ recs,
     const float4* __restrict__ geom, const uint32_t* __restrict__ tile_order, Counters* __restrict__ ctr, int W,
-    int H, int TW, rs_options o, const rs_outputs out, uint32_t* __restrict__ scores) {
+    int H, int TW, Opt32 o, const Out32 out, uint32_t* __restrict__ scores) {
   pdl_wait();
   pdl_trigger();
 #ifndef RS_BLEND_BATCH

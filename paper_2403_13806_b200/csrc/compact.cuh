@@ -102,12 +102,13 @@ __global__ void __launch_bounds__(kCompactThreads) compact_kernel(const uint8_t*
 }
 
 // number of non-finite values over the 11 planes and the SH rows (core.py:522-525)
-__global__ void finite_kernel(const float* __restrict__ planes, const float* __restrict__ sh, int64_t n,
+template <typename T>
+__global__ void finite_kernel(const T* __restrict__ planes, const T* __restrict__ sh, int64_t n,
                               int64_t stride, uint32_t* __restrict__ bad) {
   uint32_t local = 0;
   const int64_t total = n * 11 + n * 48;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
-    float v;
+    T v;
     if (k < n * 11) {
       const int64_t plane = k / n, i = k - plane * n;
       v = __ldg(planes + plane * stride + i);

@@ -30,6 +30,63 @@ struct __align__(16) Rec {
 };
 static_assert(sizeof(Rec) == 64, "record must be 64 B");
 
+// fp64 record of an RS_F64 frame (96 B = 6 x 16 B), the reference's projected
+// quantities in double (render.py:95-158): the blend evaluates
+// q = (ia dx) dx + (ib2 dy) dx + (ic dy) dy, alpha = min(o exp(-q/2), alpha_max)
+// exactly as render.py:254-259. lnc = ln(alpha_cut / o) - 1e-6 is a conservative
+// skip bound (-q/2 < lnc => alpha < alpha_cut): the exp is not evaluated, no
+// result changes. The binning uses the fp32 Rec written next to it (boxes, row
+// geometry, depth key).
+struct __align__(16) Rec64 {
+  double mx, my, ia, ib2, ic, o, depth, lnc;
+  double r, g, b;
+  uint32_t gid, pad;
+};
+static_assert(sizeof(Rec64) == 96, "fp64 record must be 96 B");
+
+// Device-side views of the boundary structs (include/radsplat.h): the fp32 path
+// works on the camera and options rounded once on the host (round to nearest,
+// = numpy astype(float32)); the fp64 path reads rs_camera / rs_options as is.
+struct Cam32 {
+  int32_t width, height;
+  float fx, fy, cx, cy;
+  float R[9];
+  float t[3];
+  float center[3];
+};
+struct Opt32 {
+  float alpha_max, alpha_cut, tau_stop, near_limit, lowpass, sigma_bound;
+};
+struct Opt64 {
+  double alpha_max, alpha_cut, tau_stop, near_limit, lowpass, sigma_bound;
+};
+// typed rs_outputs (RS_F32 / RS_F64 frames)
+struct Out32 {
+  float* rgb;
+  float* alpha;
+  float* depth;
+  int32_t* count;
+  double* rgb64;
+  double* alpha64;
+  int64_t* count64;
+  float* tau;
+  int32_t* last;
+};
+struct Out64 {
+  double* rgb;
+  double* alpha;
+  double* depth;
+  int32_t* count;
+  double* rgb64;
+  double* alpha64;
+  int64_t* count64;
+};
+// the camera as it lives in the workspace: both precisions, uploaded together
+struct CamPair {
+  rs_camera c64;
+  Cam32 c32;
+};
+
 __device__ __forceinline__ int lo16(int v) { return v & 0xffff; }
 __device__ __forceinline__ int hi16(int v) { return (int)((unsigned)v >> 16); }
 __device__ __forceinline__ int4 bbox_of(const int4 d) { return make_int4(lo16(d.x), hi16(d.x), lo16(d.y), hi16(d.y)); }
@@ -59,7 +116,8 @@ struct Counters {
   uint32_t n_dense;      // dense expansion chunks listed by chunk_count_kernel
   uint32_t dense_work;   // (dense chunk, column group) tickets of expand_dense_kernel
   uint32_t emit_done;    // finished segscan CTAs (the last one scans the row totals)
-  uint32_t pad[3];
+  uint32_t bad_index;    // an active_idx entry outside [0, n) was skipped
+  uint32_t pad[2];
 };
 static_assert(sizeof(Counters) == 128, "Counters is 128 B");
 
@@ -94,7 +152,7 @@ __device__ __forceinline__ unsigned long long warp_lookback(volatile unsigned lo
 // Overflow record that outlives the per-frame counter reset: a batch of frames
 // (e.g. a scoring pass) is launched without host syncs and checked once.
 struct Sticky {
-  uint32_t overflowed, pad;
+  uint32_t overflowed, bad_index;
   unsigned long long pairs_needed_max;
 };
 

@@ -95,6 +95,52 @@ __device__ __forceinline__ float log2_contract(float x) {
   return __fmaf_rn(__fmul_rn(t, p), 2.88539004f, (float)e);
 }
 
+// ---------------------------------------------------------------------------
+// fp64 contract (RS_F64 frames; oracle: exp64_contract in oracle/cpu_ref.cpp).
+// e^x: n = rint(x log2 e) by the magic-number add, r = x - n ln2 (Cody-Waite,
+// two fused steps), e^r by its degree-12 Taylor polynomial in Horner form
+// (|r| <= 0.347: truncation < 2e-16 relative), times 2^n built in the exponent
+// field. Only IEEE double add/mul/fma: the CPU oracle computes the same bits.
+// ---------------------------------------------------------------------------
+constexpr double kMagic64 = 6755399441055744.0;  // 1.5 * 2^52
+constexpr double kLog2e64 = 1.4426950408889634;
+constexpr double kLn2Hi = 0.6931471803691238;      // 0x3fe62e42fee00000: n * kLn2Hi exact for |n| < 2^11
+constexpr double kLn2Lo = 1.9082149292705877e-10;  // ln 2 - kLn2Hi
+
+__device__ __forceinline__ double exp64_poly(double r) {
+  double p = 1.0 / 479001600.0;  // 1/12!
+  p = __fma_rn(p, r, 1.0 / 39916800.0);
+  p = __fma_rn(p, r, 1.0 / 3628800.0);
+  p = __fma_rn(p, r, 1.0 / 362880.0);
+  p = __fma_rn(p, r, 1.0 / 40320.0);
+  p = __fma_rn(p, r, 1.0 / 5040.0);
+  p = __fma_rn(p, r, 1.0 / 720.0);
+  p = __fma_rn(p, r, 1.0 / 120.0);
+  p = __fma_rn(p, r, 1.0 / 24.0);
+  p = __fma_rn(p, r, 1.0 / 6.0);
+  p = __fma_rn(p, r, 0.5);
+  p = __fma_rn(p, r, 1.0);
+  p = __fma_rn(p, r, 1.0);
+  return p;
+}
+
+__device__ __forceinline__ double pow2i64(int n) { return __hiloint2double((n + 1023) << 20, 0); }  // n in [-1022, 1023]
+
+__device__ __forceinline__ double exp64_contract(double x) {
+  if (x != x) return x;
+  if (x > 709.782712893384) return __longlong_as_double(0x7ff0000000000000ll);  // overflow: inf
+  if (x < -745.2) return 0.0;
+  const double t = __fma_rn(x, kLog2e64, kMagic64);
+  const double n = __dsub_rn(t, kMagic64);
+  double r = __fma_rn(n, -kLn2Hi, x);
+  r = __fma_rn(n, -kLn2Lo, r);
+  const double p = exp64_poly(r);
+  const int ni = __double2loint(t);  // n in the low word of t (two's complement)
+  if (ni > 1023) return __dmul_rn(__dmul_rn(p, pow2i64(1023)), 2.0);
+  if (ni >= -1022) return __dmul_rn(p, pow2i64(ni));
+  return __dmul_rn(__dmul_rn(p, pow2i64(ni + 600)), pow2i64(-600));  // subnormal range
+}
+
 // order-preserving 32-bit key of an fp32 depth (-0 folded into +0)
 __device__ __forceinline__ uint32_t depth_key(float d) {
   const uint32_t u = __float_as_uint(__fadd_rn(d, 0.0f));

@@ -1,16 +1,14 @@
 // sort.cuh -- hand-written stable LSD radix sort (onesweep, 8-bit digits).
 //
-// Replaces np.lexsort (render.py:218-222) twice per frame:
-//   * depth sort: 32-bit depth keys of the n_visible binned items, values =
-//     item index (compacted in item order by compact_hist_kernel), 4 passes;
-//   * tile sort:  16-bit tile ids of the P Gaussian-tile pairs emitted in
-//     (depth, index) order, values = item id, ceil(tile_bits/8) passes.
-// Stability makes the per-tile order exactly the reference's (depth, index)
-// order restricted to the tile.
+// Replaces np.lexsort (render.py:218-222): the depth sort of the frame -- 32-bit
+// depth keys of the n_visible binned items, values = item index (compacted in
+// item order by compact_hist_kernel), 4 passes. Stability keeps equal depths in
+// index order; the per-tile lists are then placed in this order without a
+// second sort (segbin.cuh), so each tile's list is exactly the reference's
+// (depth, index) order restricted to the tile.
 //
-// Digit histograms of every pass come from the key producer (compact_hist_kernel
-// for depth keys, the emitters for tile ids), so each pass is ONE kernel: CTAs
-// take chunks of 256*ITEMS keys in launch order from an atomic ticket, rank
+// Digit histograms of every pass come from the key producer (compact_hist_kernel),
+// so each pass is ONE kernel: CTAs take chunks of 256*ITEMS keys in launch order from an atomic ticket, rank
 // keys inside the chunk with a warp multisplit (match_any for narrow digits,
 // per-bit ballots for 7-8 bit digits, whichever measured faster), publish
 // the chunk's digit counts right after loading (before ranking, so successors
@@ -297,6 +295,39 @@ __global__ void __launch_bounds__(kSortThreads, 4) onesweep_kernel(
     const uint32_t g = S.gout[((uint32_t)k >> shift) & dmask] + p;
     if (write_keys) keys_out[g] = k;
     vals_out[g] = S.vals[p];
+  }
+}
+
+// RS_F64 frames: the depth keys are the fp32 roundings of the fp64 depths (monotone, so
+// the radix order is the fp64 order except inside runs of equal keys). Each run is
+// re-ordered by (fp64 depth, item) -- the reference's exact lexsort((idx, depth))
+// (render.py:218-222): the run's first position sorts it by insertion (runs are short:
+// a few items share an fp32 depth; equal fp64 depths keep item order, so an already
+// ordered run costs one pass).
+__global__ void __launch_bounds__(256) tiefix_kernel(const uint32_t* __restrict__ keys, uint32_t* __restrict__ items,
+                                                     const uint32_t* __restrict__ n_ptr,
+                                                     const Rec64* __restrict__ recs64) {
+  pdl_wait();
+  pdl_trigger();
+  const uint32_t n = *n_ptr;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i + 1 < n; i += gridDim.x * blockDim.x) {
+    const uint32_t k = keys[i];
+    if (keys[i + 1] != k || (i > 0 && keys[i - 1] == k)) continue;  // not the start of a run
+    uint32_t e = i + 2;
+    while (e < n && keys[e] == k) ++e;
+    for (uint32_t a = i + 1; a < e; ++a) {
+      const uint32_t it = items[a];
+      const double d = recs64[it].depth;
+      uint32_t b = a;
+      while (b > i) {
+        const uint32_t pv = items[b - 1];
+        const double pd = recs64[pv].depth;
+        if (pd < d || (pd == d && pv < it)) break;
+        items[b] = pv;
+        --b;
+      }
+      items[b] = it;
+    }
   }
 }
 

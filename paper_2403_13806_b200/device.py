@@ -1,9 +1,15 @@
 """Device residency: scenes in HBM, workspaces, and the frame launcher.
 
-* ``DeviceScene`` -- the scene in HBM: 11 fp32 geometry planes of N floats
-  plus N SH rows of 48 floats (the layout ``rs_scene`` documents). Reference scenes are immutable and carry a
-  ``generation`` tag (core.py:467-485), so an uploaded copy is cached per
-  (object, generation) and reused by every later call on the same scene.
+* ``DeviceScene`` -- the scene in HBM: 11 geometry planes of N values plus N
+  SH rows of 48 values (the layout ``rs_scene`` documents), stored as fp32 when
+  every value is exactly an fp32 number (synthetic scenes, RSPL files) and as
+  fp64 otherwise (the reference's float64 arrays), so no frame ever sees
+  rounded inputs. Reference scenes are immutable and carry a ``generation``
+  tag (core.py:467-485), so an uploaded copy is cached per (object,
+  generation) and reused by every later call on the same scene.
+* Precision: every frame runs in fp64 (the reference's arithmetic, RS_F64:
+  bit-identical to the oracle's Tier C, ~1e-15 from the reference) unless its
+  options ask for ``precision="fp32"`` (the fast fp32 contract, Tier A).
 * ``Renderer`` -- one per device: owns the workspace (grown on demand; a pair
   overflow re-runs the frame with the capacity the device reported), the
   stream, and launches ``rs_render`` / ``rs_project_full`` / ``rs_compact``.
@@ -23,13 +29,45 @@ from . import _native as N
 from .core import InvalidParameterError, InvalidSceneError
 
 PLANES = 11  # positions(3), opacity logit, log scales(3), quaternion(4); SH rows are separate
+DEFAULT_PRECISION = "fp64"
+_PRECISIONS = {"fp64": N.RS_F64, "f64": N.RS_F64, "float64": N.RS_F64, "double": N.RS_F64,
+               "fp32": N.RS_F32, "f32": N.RS_F32, "float32": N.RS_F32, "float": N.RS_F32}
 
 
-def pack_planes(scene) -> np.ndarray:
-    """(11, N) float32 plane-major geometry of a scene-like object."""
+def precision_of(opts) -> int:
+    """RS_F32 / RS_F64 of a RasterizeOptions-like object (``precision`` attribute;
+    objects without one -- e.g. the reference's own RasterizeOptions -- get fp64)."""
+    p = getattr(opts, "precision", None) or DEFAULT_PRECISION
+    try:
+        return _PRECISIONS[str(p).lower()]
+    except KeyError:
+        raise InvalidParameterError(f"precision must be 'fp32' or 'fp64', got {p!r}") from None
+
+
+def value_dtype(precision: int) -> torch.dtype:
+    return torch.float64 if precision == N.RS_F64 else torch.float32
+
+
+def _arrays(scene):
+    return (scene.positions, scene.opacity_logits, scene.log_scales, scene.quaternions, scene.sh)
+
+
+def storage_dtype(scene) -> np.dtype:
+    """float32 when every value is exactly representable in fp32, else float64."""
+    for a in _arrays(scene):
+        a = np.asarray(a)
+        if a.dtype == np.float32 or a.size == 0:
+            continue
+        if a.dtype != np.float64 or not np.array_equal(a.astype(np.float32).astype(np.float64), a):
+            return np.dtype(np.float64)
+    return np.dtype(np.float32)
+
+
+def pack_planes(scene, dtype=np.float32) -> np.ndarray:
+    """(11, N) plane-major geometry of a scene-like object."""
     pos = np.asarray(scene.positions)
     n = pos.shape[0]
-    out = np.empty((PLANES, n), np.float32)
+    out = np.empty((PLANES, n), dtype)
     out[0:3] = pos.reshape(n, 3).T
     out[3] = np.asarray(scene.opacity_logits).reshape(n)
     out[4:7] = np.asarray(scene.log_scales).reshape(n, 3).T
@@ -37,20 +75,21 @@ def pack_planes(scene) -> np.ndarray:
     return out
 
 
-def pack_sh(scene) -> np.ndarray:
-    """(N, 48) float32 SH rows, channel-major [c][b] (core.py:480)."""
+def pack_sh(scene, dtype=np.float32) -> np.ndarray:
+    """(N, 48) SH rows, channel-major [c][b] (core.py:480)."""
     sh = np.asarray(scene.sh)
-    return np.ascontiguousarray(sh.reshape(sh.shape[0], 48), dtype=np.float32)
+    return np.ascontiguousarray(sh.reshape(sh.shape[0], 48), dtype=dtype)
 
 
 class DeviceScene:
-    """A scene resident in HBM (fp32 planes) plus its ``rs_scene`` descriptor."""
+    """A scene resident in HBM (fp32 or fp64 planes) plus its ``rs_scene`` descriptor."""
 
-    def __init__(self, scene, device: torch.device | None = None, check_finite: bool = True):
+    def __init__(self, scene, device: torch.device | None = None, check_finite: bool = True, dtype=None):
         lib = N.load()
         self.device = torch.device(device or torch.device("cuda", torch.cuda.current_device()))
-        host = torch.from_numpy(pack_planes(scene))
-        host_sh = torch.from_numpy(pack_sh(scene))
+        dt = np.dtype(dtype) if dtype is not None else storage_dtype(scene)
+        host = torch.from_numpy(pack_planes(scene, dt))
+        host_sh = torch.from_numpy(pack_sh(scene, dt))
         self.n = int(host.shape[1])
         self.sh_degree = int(scene.active_sh_degree)
         if not 0 <= self.sh_degree <= 3:
@@ -61,10 +100,10 @@ class DeviceScene:
                 self.planes = host.pin_memory().to(self.device, non_blocking=True)
                 self.sh = host_sh.pin_memory().to(self.device, non_blocking=True)
             else:
-                self.planes = torch.zeros((PLANES, 1), dtype=torch.float32, device=self.device)
-                self.sh = torch.zeros((1, 48), dtype=torch.float32, device=self.device)
+                self.planes = torch.zeros((PLANES, 1), dtype=host.dtype, device=self.device)
+                self.sh = torch.zeros((1, 48), dtype=host.dtype, device=self.device)
         self.struct = N.RsScene(self.planes.data_ptr(), self.sh.data_ptr(), self.n, max(self.n, 1),
-                                self.sh_degree, 0)
+                                self.sh_degree, self.dtype_code)
         if check_finite and self.n:
             with torch.cuda.device(self.device):
                 bad = torch.zeros(1, dtype=torch.int32, device=self.device)
@@ -87,7 +126,10 @@ class DeviceScene:
             raise InvalidParameterError("active SH degree must be in 0..3")
         self.generation = generation
         self.planes, self.sh = planes, sh
-        self.struct = N.RsScene(planes.data_ptr(), sh.data_ptr(), self.n, max(self.n, 1), self.sh_degree, 0)
+        if planes.dtype not in (torch.float32, torch.float64) or sh.dtype != planes.dtype:
+            raise InvalidParameterError("scene planes / SH must be float32 or float64 (same dtype)")
+        self.struct = N.RsScene(planes.data_ptr(), sh.data_ptr(), self.n, max(self.n, 1), self.sh_degree,
+                                self.dtype_code)
         if check_finite and self.n:
             with torch.cuda.device(self.device):
                 bad = torch.zeros(1, dtype=torch.int32, device=self.device)
@@ -97,6 +139,10 @@ class DeviceScene:
                     raise InvalidSceneError("scene contains non-finite parameters")
         return self
 
+    @property
+    def dtype_code(self) -> int:
+        return N.RS_F64 if self.planes.dtype == torch.float64 else N.RS_F32
+
     def __len__(self):
         return self.n
 
@@ -104,18 +150,21 @@ class DeviceScene:
 _scene_cache: dict = {}
 
 
-def device_scene(scene, device: torch.device | None = None) -> DeviceScene:
-    """Upload once per (scene object, generation, device); later calls reuse it."""
+def device_scene(scene, device: torch.device | None = None, dtype=None) -> DeviceScene:
+    """Upload once per (scene object, generation, device, storage dtype); later calls
+    reuse it. ``dtype`` None = exact storage (storage_dtype)."""
     if isinstance(scene, DeviceScene):
-        return scene
+        if dtype is None or np.dtype(dtype) == (np.float64 if scene.dtype_code == N.RS_F64 else np.float32):
+            return scene
+        raise InvalidParameterError("a DeviceScene cannot change its storage dtype")
     N.load()  # raises NativeUnavailable without the library or a CUDA device (no CPU fallback)
     dev = torch.device(device or torch.device("cuda", torch.cuda.current_device()))
-    key = (id(scene), dev)
+    key = (id(scene), dev, None if dtype is None else np.dtype(dtype).str)
     hit = _scene_cache.get(key)
     gen = getattr(scene, "generation", None)
     if hit is not None and hit.generation == gen and hit.n == len(scene.positions):
         return hit
-    ds = DeviceScene(scene, dev)
+    ds = DeviceScene(scene, dev, dtype=dtype)
     _scene_cache[key] = ds
     try:
         weakref.finalize(scene, _scene_cache.pop, key, None)
@@ -125,22 +174,24 @@ def device_scene(scene, device: torch.device | None = None) -> DeviceScene:
 
 
 def camera_struct(cam) -> N.RsCamera:
-    """fp32 camera packet; the centre -R^T t is formed in fp64, then rounded."""
+    """fp64 camera packet (the reference's values); centre = -R^T t (core.py:351-354).
+    The library rounds it once for fp32 frames."""
     R = np.asarray(cam.rotation, np.float64).reshape(3, 3)
     t = np.asarray(cam.translation, np.float64).reshape(3)
     c = -R.T @ t
     s = N.RsCamera()
     s.width, s.height = int(cam.width), int(cam.height)
-    s.fx, s.fy, s.cx, s.cy = (float(np.float32(v)) for v in (cam.fx, cam.fy, cam.cx, cam.cy))
-    s.R[:] = [float(v) for v in R.ravel().astype(np.float32)]
-    s.t[:] = [float(v) for v in t.astype(np.float32)]
-    s.center[:] = [float(v) for v in c.astype(np.float32)]
+    s.fx, s.fy, s.cx, s.cy = (float(v) for v in (cam.fx, cam.fy, cam.cx, cam.cy))
+    s.R[:] = [float(v) for v in R.ravel()]
+    s.t[:] = [float(v) for v in t]
+    s.center[:] = [float(v) for v in c]
     return s
 
 
 def options_struct(opts) -> N.RsOptions:
-    return N.RsOptions(*(float(np.float32(getattr(opts, k))) for k in
-                         ("alpha_max", "alpha_cut", "tau_stop", "near_limit", "lowpass", "sigma_bound")))
+    return N.RsOptions(*(float(getattr(opts, k)) for k in
+                         ("alpha_max", "alpha_cut", "tau_stop", "near_limit", "lowpass", "sigma_bound")),
+                       precision_of(opts), 0)
 
 
 class Renderer:
@@ -164,6 +215,7 @@ class Renderer:
         if size == 0:
             raise InvalidParameterError(f"unsupported workspace shape {caps}")
         self.close()
+        self.frame_id += 1  # a new workspace holds no frame: a cached backward must redo its forward
         with torch.cuda.device(self.device):
             self.buf = torch.empty(size, dtype=torch.uint8, device=self.device)
         N.check(self.lib.rs_workspace_create(self.buf.data_ptr(), size, *caps, C.byref(self.handle)),
@@ -195,10 +247,13 @@ class Renderer:
         return st
 
     def read_overflow(self, reset: bool = True) -> tuple[bool, int]:
-        """(did any frame since the last reset overflow, largest P it needed); synchronizes."""
-        o, p = C.c_uint32(), C.c_uint64()
-        N.check(self.lib.rs_read_overflow(self.handle, C.byref(o), C.byref(p), int(reset), self.stream),
-                "read_overflow")
+        """(did any frame since the last reset overflow, largest P it needed); synchronizes.
+        Raises InvalidParameterError if one of those frames had an out-of-range active index."""
+        o, p, b = C.c_uint32(), C.c_uint64(), C.c_uint32()
+        N.check(self.lib.rs_read_sticky(self.handle, C.byref(o), C.byref(p), C.byref(b), int(reset), self.stream),
+                "read_sticky")
+        if b.value:
+            raise InvalidParameterError("active index list holds an index outside the scene")
         return bool(o.value), int(p.value)
 
     def buffers(self) -> N.RsBuffers:
@@ -220,19 +275,21 @@ class Renderer:
         return dict(
             stats=st, tiles_x=b.tiles_x, tiles_y=b.tiles_y,
             records=self.view(b.records, 16 * st.n_items, torch.float32).view(-1, 16).cpu().numpy(),
+            records64=self.view(b.records64, 24 * st.n_items, torch.float32).view(-1, 24).cpu().numpy(),
             items_sorted=self.view(b.items_sorted, st.n_items, torch.int32).cpu().numpy().view(np.uint32),
             pair_items=self.view(b.pair_items, st.n_pairs, torch.int32).cpu().numpy().view(np.uint32),
             ranges=self.view(b.ranges, 2 * T, torch.int32).cpu().numpy().view(np.uint32).reshape(T, 2))
 
     # -- frames --------------------------------------------------------------
-    def alloc_outputs(self, cam, color: bool = True) -> dict:
+    def alloc_outputs(self, cam, color: bool = True, precision: int = N.RS_F32) -> dict:
+        """Device images of a frame: float32 (RS_F32) or float64 (RS_F64) rgb/alpha/depth."""
         H, W = int(cam.height), int(cam.width)
         if not color:
             return {}
-        d = self.device
-        return dict(rgb=torch.empty((H, W, 3), dtype=torch.float32, device=d),
-                    alpha=torch.empty((H, W), dtype=torch.float32, device=d),
-                    depth=torch.empty((H, W), dtype=torch.float32, device=d),
+        d, vt = self.device, value_dtype(precision)
+        return dict(rgb=torch.empty((H, W, 3), dtype=vt, device=d),
+                    alpha=torch.empty((H, W), dtype=vt, device=d),
+                    depth=torch.empty((H, W), dtype=vt, device=d),
                     count=torch.empty((H, W), dtype=torch.int32, device=d))
 
     @staticmethod
@@ -253,6 +310,14 @@ class Renderer:
             int(m), C.byref(cam_s), C.byref(opt_s), C.byref(self.outputs_struct(out)),
             scores.data_ptr() if scores is not None else None, flags, self.stream), "render")
 
+    @staticmethod
+    def check_scores(scores: torch.Tensor | None, precision: int) -> None:
+        """A score vector holds the frame's value type (float32 / float64, non-negative)."""
+        if scores is not None and scores.dtype not in (value_dtype(precision), torch.int32, torch.int64):
+            raise InvalidParameterError(f"scores must be {value_dtype(precision)} for this precision")
+        if scores is not None and scores.element_size() != (8 if precision == N.RS_F64 else 4):
+            raise InvalidParameterError("scores element size does not match the precision")
+
     def render(self, ds: DeviceScene, cam, opts, *, color: bool = True, scores: torch.Tensor | None = None,
                active_idx: torch.Tensor | None = None, m: int | None = None, count_evals: bool = False,
                out: dict | None = None) -> tuple[dict, N.RsStats]:
@@ -261,12 +326,15 @@ class Renderer:
         W, H = int(cam.width), int(cam.height)
         self.ensure(items, self.caps[1] or max(4 * items, 1 << 20), W, H)
         cam_s, opt_s = camera_struct(cam), options_struct(opts)
-        out = out if out is not None else self.alloc_outputs(cam, color)
+        self.check_scores(scores, opt_s.precision)
+        out = out if out is not None else self.alloc_outputs(cam, color, opt_s.precision)
         flags = N.RS_FLAG_COUNT_EVALS if count_evals else 0
         snapshot = scores.clone() if scores is not None else None
         for _ in range(4):
             self.launch(ds, cam_s, opt_s, out, scores, active_idx, items, flags)
             st = self.stats()
+            if st.bad_index:
+                raise InvalidParameterError("active index list holds an index outside the scene")
             if not st.overflow:
                 return out, st
             self.ensure(items, int(st.pairs_needed * 1.15) + 1024, W, H)
@@ -285,6 +353,7 @@ class Renderer:
         W, H = max(int(c.width) for c in cams), max(int(c.height) for c in cams)
         self.ensure(ds.n, self.caps[1] or max(4 * ds.n, 1 << 20), W, H)
         opt_s = options_struct(opts)
+        self.check_scores(scores, opt_s.precision)
         structs = [camera_struct(c) for c in cams]
         snapshot = scores.clone()
         self.read_overflow(reset=True)
@@ -304,19 +373,24 @@ class Renderer:
         replay time: size it with ``pairs_hint`` or a checked ``render`` beforehand)."""
         items = ds.n if active_idx is None else int(active_idx.numel())
         self.ensure(items, max(self.caps[1], pairs_hint or 0, 1 << 16), int(cam.width), int(cam.height))
-        out = self.alloc_outputs(cam, color)
+        out = self.alloc_outputs(cam, color, precision_of(opts))
         torch.cuda.synchronize(self.device)
+        self.frame_id += 1  # capture records a frame without running it
         return FrameGraph(self, ds, cam, opts, out, scores, active_idx, items)
 
     def project_full(self, ds: DeviceScene, cam, opts) -> tuple[np.ndarray, np.ndarray]:
-        """ProjectedGaussian fields for every Gaussian (render.py:161-211)."""
+        """ProjectedGaussian fields for every Gaussian (render.py:161-211), in the
+        frame's value type."""
         self.ensure(ds.n, self.caps[1] or (1 << 16), int(cam.width), int(cam.height))
         n = max(ds.n, 1)
-        full = torch.empty((n, 16), dtype=torch.float32, device=self.device)
+        self.frame_id += 1  # the projection replaces the workspace's frame
+        full = torch.empty((n, 16), dtype=value_dtype(precision_of(opts)), device=self.device)
         bbox = torch.empty((n, 4), dtype=torch.int32, device=self.device)
         N.check(self.lib.rs_project_full(self.handle, C.byref(ds.struct), None, 0, C.byref(camera_struct(cam)),
                                          C.byref(options_struct(opts)), full.data_ptr(), bbox.data_ptr(),
                                          self.stream), "project_full")
+        if self.stats().bad_index:
+            raise InvalidParameterError("active index list holds an index outside the scene")
         return full[:ds.n].cpu().numpy(), bbox[:ds.n].cpu().numpy()
 
     def compact(self, flags: torch.Tensor, bits: bool = False, n: int | None = None) -> torch.Tensor:
@@ -371,6 +445,18 @@ class FrameGraph:
             self.set_camera(cam)
         self.r.frame_id += 1
         self.graph.replay()
+
+
+def pack_bits_device(flags: torch.Tensor) -> torch.Tensor:
+    """(n,) bool/uint8 CUDA tensor -> LSB-first bitset bytes (np.packbits(bitorder="little"))."""
+    lib = N.load()
+    n = int(flags.numel())
+    out = torch.empty(max((n + 7) // 8, 1), dtype=torch.uint8, device=flags.device)
+    f = flags.contiguous().view(torch.uint8)
+    with torch.cuda.device(flags.device):
+        N.check(lib.rs_pack_bits(f.data_ptr() if n else None, n, out.data_ptr(),
+                                 torch.cuda.current_stream(flags.device).cuda_stream), "pack_bits")
+    return out[:(n + 7) // 8]
 
 
 _renderers: dict = {}

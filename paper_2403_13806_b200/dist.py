@@ -16,9 +16,10 @@ import torch
 import torch.distributed as dist
 
 
-def world() -> tuple[int, int]:
+def world(group=None) -> tuple[int, int]:
+    """(rank, size) in ``group`` (default group); (0, 1) without a process group."""
     if dist.is_available() and dist.is_initialized():
-        return dist.get_rank(), dist.get_world_size()
+        return dist.get_rank(group), dist.get_world_size(group)
     return 0, 1
 
 

@@ -32,7 +32,7 @@ import torch
 
 from . import _native as N
 from .core import FileFormatError, GaussianScene, InvalidParameterError
-from .device import PLANES, DeviceScene, renderer
+from .device import PLANES, DeviceScene, pack_bits_device, renderer  # noqa: F401 (re-export)
 from .visibility import ClusterVisibility
 
 SCENE_MAGIC = b"RSPL"
@@ -83,8 +83,10 @@ def _device_payload(ds: DeviceScene) -> np.ndarray:
     lib = N.load()
     n = ds.n
     buf = torch.empty(max(FLOATS_PER_GAUSSIAN * n, 4), dtype=torch.float32, device=ds.device)
+    # RSPL is fp32 (io.py:128-142): an fp64-stored scene is rounded once, like the reference's writer
+    planes, sh = ds.planes.float().contiguous(), ds.sh.float().contiguous()
     with torch.cuda.device(ds.device):
-        N.check(lib.rs_rspl_pack(ds.planes.data_ptr(), ds.struct.plane_stride, ds.sh.data_ptr(), n, buf.data_ptr(),
+        N.check(lib.rs_rspl_pack(planes.data_ptr(), planes.shape[1], sh.data_ptr(), n, buf.data_ptr(),
                                  torch.cuda.current_stream(ds.device).cuda_stream), "rspl_pack")
     return buf[:FLOATS_PER_GAUSSIAN * n].cpu().numpy()
 
@@ -238,15 +240,3 @@ def load_visibility_device(path, scene=None, device: torch.device | None = None)
     for j in range(k):
         cache[(j, dev)] = r.compact(bits[j], bits=True, n=size)
     return vis
-
-
-def pack_bits_device(flags: torch.Tensor) -> torch.Tensor:
-    """(n,) bool/uint8 CUDA tensor -> LSB-first bitset bytes (np.packbits(bitorder="little"))."""
-    lib = N.load()
-    n = int(flags.numel())
-    out = torch.empty(max((n + 7) // 8, 1), dtype=torch.uint8, device=flags.device)
-    f = flags.contiguous().view(torch.uint8)
-    with torch.cuda.device(flags.device):
-        N.check(lib.rs_pack_bits(f.data_ptr() if n else None, n, out.data_ptr(),
-                                 torch.cuda.current_stream(flags.device).cuda_stream), "pack_bits")
-    return out[:(n + 7) // 8]

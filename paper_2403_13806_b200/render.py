@@ -13,10 +13,14 @@ changing the import:
 * ``rasterize_cached`` (:318-321) and ``rasterize_backward`` (:328-487), the
   training pair
 
-The compute runs on the GPU in fp32 (the reference is fp64); results equal
-the Tier-A fp32 oracle bit for bit and the fp64 reference within the
-tolerances documented in DESIGN.md. Device-native entry points that keep
-everything in HBM (``render_device``) are what the benchmarks use.
+The compute runs on the GPU in fp64 by default -- the reference's own
+expressions and composite order, bit-identical to the oracle's Tier C and
+within ~1e-15 of the NumPy reference -- or, with
+``RasterizeOptions(precision="fp32")``, on the fast fp32 path (bit-identical
+to the Tier-A fp32 oracle; DESIGN.md §4 gives its measured distance from the
+reference). The training pair (``rasterize_cached`` / ``rasterize_backward``)
+is fp32. Device-native entry points that keep everything in HBM
+(``render_device``) are what the benchmarks use.
 """
 
 from __future__ import annotations
@@ -26,21 +30,32 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-from .core import GaussianScene, ImageBuffer, InvalidParameterError
 import ctypes as C
+from dataclasses import replace
 
 from . import _native as N
-from .device import DeviceScene, device_scene, options_struct, renderer
+from .core import GaussianScene, ImageBuffer, InvalidParameterError
+from .device import DeviceScene, device_scene, options_struct, precision_of, renderer, value_dtype
 
 
 @dataclass(frozen=True)
 class RasterizeOptions:
+    """render.py:37-46, plus the arithmetic precision of the GPU frame: "fp64"
+    (default; the reference's arithmetic) or "fp32" (the fast contract)."""
     alpha_max: float = 0.99
     alpha_cut: float = 1.0 / 255.0
     tau_stop: float = 1e-4
     near_limit: float = 0.01
     lowpass: float = 0.3
     sigma_bound: float = 3.0
+    precision: str = "fp64"
+
+
+def fp32_options(options) -> RasterizeOptions:
+    """The same options on the fp32 path (the training pair's precision)."""
+    return RasterizeOptions(*(float(getattr(options, k)) for k in
+                              ("alpha_max", "alpha_cut", "tau_stop", "near_limit", "lowpass", "sigma_bound")),
+                            precision="fp32")
 
 
 @dataclass(frozen=True)
@@ -98,12 +113,12 @@ def render_device(scene, camera, options: RasterizeOptions = RasterizeOptions(),
                   count_evals: bool = False):
     """Render one view on the GPU; returns (dict of device tensors, rs_stats).
 
-    ``scores`` is an (N,) float32 CUDA tensor max-merged in place (bit-level
-    atomicMax on non-negative floats)."""
+    ``scores`` is an (N,) CUDA tensor of the frame's value type (float32 for
+    fp32 frames, float64 for fp64 frames) max-merged in place (bit-level
+    atomicMax on non-negative values)."""
     ds = _check_scene(scene)
     r = renderer(ds.device)
-    sc = scores.view(torch.int32) if scores is not None else None
-    return r.render(ds, camera, options, color=color, scores=sc, active_idx=active_idx,
+    return r.render(ds, camera, options, color=color, scores=scores, active_idx=active_idx,
                     count_evals=count_evals)
 
 
@@ -118,9 +133,8 @@ def _render_host(scene, camera, options, *, scores: torch.Tensor | None = None,
     out = dict(rgb64=torch.empty((H, W, 3), dtype=torch.float64, pin_memory=True),
                alpha64=torch.empty((H, W), dtype=torch.float64, pin_memory=True),
                count64=torch.empty((H, W), dtype=torch.int64, pin_memory=True),
-               depth=torch.empty((H, W), dtype=torch.float32, device=ds.device))
-    sc = scores.view(torch.int32) if scores is not None else None
-    r.render(ds, camera, options, scores=sc, active_idx=active_idx, out=out)  # synchronizes
+               depth=torch.empty((H, W), dtype=value_dtype(precision_of(options)), device=ds.device))
+    r.render(ds, camera, options, scores=scores, active_idx=active_idx, out=out)  # synchronizes
     return RenderOutput(color=ImageBuffer.trusted(out["rgb64"].numpy()), alpha=out["alpha64"].numpy(),
                         count=out["count64"].numpy(), depth=out["depth"])
 
@@ -136,7 +150,7 @@ def rasterize_with_contributions(scene, camera, accumulator: ContributionAccumul
     if len(accumulator) != len(scene):
         raise InvalidParameterError("accumulator length must equal scene size")
     ds = _check_scene(scene)
-    scores = torch.zeros(max(ds.n, 1), dtype=torch.float32, device=ds.device)
+    scores = torch.zeros(max(ds.n, 1), dtype=value_dtype(precision_of(options)), device=ds.device)
     res = _render_host(ds, camera, options, scores=scores)
     accumulator.update(scores[:ds.n].cpu().numpy().astype(np.float64))
     return res
@@ -162,8 +176,19 @@ def rasterize_filtered(scene, camera, active, options: RasterizeOptions = Raster
 # ---------------------------------------------------------------------------
 # training: forward with cache + backward (render.py:318-487)
 # ---------------------------------------------------------------------------
+def _fp32_scene(scene) -> DeviceScene:
+    """The scene as the training pair reads it: fp32 storage (rounded once if needed)."""
+    ds = _check_scene(scene)
+    if ds.dtype_code == N.RS_F32 or isinstance(scene, DeviceScene):
+        if ds.dtype_code != N.RS_F32:
+            raise InvalidParameterError("the training pair needs an fp32 device scene")
+        return ds
+    return device_scene(scene, ds.device, dtype=np.float32)
+
+
 def _training_forward(ds: DeviceScene, camera, options, active_idx=None):
     r = renderer(ds.device)
+    options = fp32_options(options)
     out = r.alloc_outputs(camera)
     H, W = int(camera.height), int(camera.width)
     out["tau"] = torch.empty((H, W), dtype=torch.float32, device=ds.device)
@@ -175,8 +200,9 @@ def _training_forward(ds: DeviceScene, camera, options, active_idx=None):
 def rasterize_cached(scene, camera, options: RasterizeOptions = RasterizeOptions()):
     """Forward render keeping what the backward pass needs (render.py:318-321):
     returns (RenderOutput, cache). The cache holds, on the device, the per-pixel
-    final transmittance and last composite; the binning stays in the workspace."""
-    ds = _check_scene(scene)
+    final transmittance and last composite; the binning stays in the workspace.
+    The training pair runs on the fp32 path (fp32 scene storage)."""
+    ds = _fp32_scene(scene)
     out, frame = _training_forward(ds, camera, options)
     H, W = int(camera.height), int(camera.width)
     res = RenderOutput(color=ImageBuffer.trusted(out["rgb"].double().cpu().numpy().reshape(H, W, 3)),
@@ -191,9 +217,9 @@ def rasterize_backward(scene, camera, cache: dict, grad_image) -> dict:
     dL/d(colour image), (H, W, 3). Returns float64 gradients w.r.t. positions,
     sh, log_scales, quaternions, opacity_logits, plus ``mean2d_grad_norm`` and
     ``touched`` -- the reference's dict, computed by rs_backward in fp32."""
-    ds = _check_scene(scene)
+    ds = _fp32_scene(scene)
     r = renderer(ds.device)
-    options = cache["options"]
+    options = fp32_options(cache["options"])
     out = cache["device_out"]
     if r.frame_id != cache["frame"]:  # the workspace rendered something else since: redo the forward
         out, cache["frame"] = _training_forward(ds, camera, options)

@@ -54,12 +54,28 @@ def load_cam(d, p):
                          translation=d[p + "t"])
 
 
-def options_from(vals):
+def options_from(vals, precision=None):
+    """RasterizeOptions-like values; ``precision`` None = the library default (fp64)."""
     from types import SimpleNamespace
     if vals is None:
         vals = [0.99, 1.0 / 255.0, 1e-4, 0.01, 0.3, 3.0]
     keys = ("alpha_max", "alpha_cut", "tau_stop", "near_limit", "lowpass", "sigma_bound")
-    return SimpleNamespace(**dict(zip(keys, (float(v) for v in vals))))
+    o = SimpleNamespace(**dict(zip(keys, (float(v) for v in vals))))
+    if precision is not None:
+        o.precision = precision
+    return o
+
+
+def with_precision(opts, precision):
+    """Copy of RasterizeOptions-like ``opts`` (None = defaults) on the given path."""
+    keys = ("alpha_max", "alpha_cut", "tau_stop", "near_limit", "lowpass", "sigma_bound")
+    vals = None if opts is None else [getattr(opts, k) for k in keys]
+    return options_from(vals, precision)
+
+
+# the two GPU paths and the oracle tier each must reproduce bit for bit
+PRECISIONS = [("fp32", np.float32), ("fp64", "c64")]
+PREC_IDS = ["fp32", "fp64"]
 
 
 def render_cases():
@@ -79,6 +95,19 @@ def render_cases():
     s, cam, o = load_case(d, "cfg0_")
     out.append(("config0", s, cam, options_from(o), d, "cfg0_"))
     return out
+
+
+def reference_check_fp64(name, img, alpha, count, contrib, d, p):
+    """fp64 path (Tier C bits) vs the fp64 reference's golden output: same
+    composite decisions everywhere (count identical), pixels and scores within
+    a few ulp -- asserted at 1e-12 (north_star: 1e-4 pixels, 1e-5 scores)."""
+    assert np.array_equal(count, d[p + "count"]), (name, int((count != d[p + "count"]).sum()))
+    assert np.abs(img - d[p + "img"]).max(initial=0.0) <= 1e-12, name
+    assert np.abs(alpha - d[p + "alpha"]).max(initial=0.0) <= 1e-12, name
+    ref = d[p + "contrib"]
+    assert np.array_equal(contrib > 0, ref > 0), name
+    rel = np.abs(contrib - ref) / np.maximum(ref, 1e-300)
+    assert rel.max(initial=0.0) <= 1e-12, (name, float(rel.max(initial=0.0)))
 
 
 def tier_b_check(name, img, alpha, count, contrib, d, p, thresholds=(0.001, 0.01, 0.05)):

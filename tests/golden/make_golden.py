@@ -235,9 +235,9 @@ def main():
         assert c["active_count"] == d[f"pose{i}_active"] and c["cluster_index"] == d[f"pose{i}_cluster"]
     np.savez_compressed(HERE / "viewer_parity.npz", **d)
 
-    make_io(fs, conftest)
-    make_grad(fs, conftest)
-    make_metrics(fs, conftest)
+    make_io(fs, cf)
+    make_grad(fs, cf)
+    make_metrics(fs, cf)
     print("golden fixtures written to", HERE)
 
 

@@ -16,27 +16,29 @@ from paper_2403_13806_b200.render import RasterizeOptions, render_device  # noqa
 from paper_2403_13806_b200.synth import config1, config4  # noqa: E402
 
 
-def check(scene, cam, opts):
+def check(scene, cam, opts, tier):
     n = len(scene)
-    sc = torch.zeros(n, dtype=torch.float32, device="cuda")
+    sc = torch.zeros(n, dtype=torch.float32 if tier is np.float32 else torch.float64, device="cuda")
     out, st = render_device(scene, cam, opts, scores=sc)
     fa = renderer().frame_arrays()
-    ob = O.bin_tiles(scene, cam, opts, np.float32)
+    ob = O.bin_tiles(scene, cam, opts, tier)
     assert st.n_pairs == ob["P"], (st.n_pairs, ob["P"])
     assert np.array_equal(fa["ranges"], ob["ranges"])
     assert np.array_equal(fa["pair_items"], ob["vals"])
-    ref = O.views(scene, [cam], opts, np.float32, scores=True, images=True)
+    ref = O.views(scene, [cam], opts, tier, scores=True, images=True)
     assert np.array_equal(out["rgb"].cpu().numpy(), ref["img_last"])
     assert np.array_equal(sc.cpu().numpy(), ref["contrib"])
 
 
 def main():
-    opts = RasterizeOptions(near_limit=0.2)
-    for n, W, H, fov in ((50_000, 33, 17, 60.0), (100_000, 640, 480, 55.0), (60_000, 1920, 1080, 55.0)):
-        scene, _ = config1(n, n=n, n_frames=1)
-        check(scene, look_at_camera((2.8, -1.1, 0.7), (0.1, 0.0, 0.0), width=W, height=H, fov_deg=fov), opts)
-    scene, cams = config4(0, n=20_000, n_views=4)  # heavy tails: long row segments (dense chunks)
-    check(scene, cams[1], opts)
+    for prec, tier in (("fp32", np.float32), ("fp64", "c64")):
+        opts = RasterizeOptions(near_limit=0.2, precision=prec)
+        for n, W, H, fov in ((50_000, 33, 17, 60.0), (100_000, 640, 480, 55.0), (60_000, 1920, 1080, 55.0)):
+            scene, _ = config1(n, n=n, n_frames=1)
+            check(scene, look_at_camera((2.8, -1.1, 0.7), (0.1, 0.0, 0.0), width=W, height=H, fov_deg=fov), opts,
+                  tier)
+        scene, cams = config4(0, n=20_000, n_views=4)  # heavy tails: long row segments (dense chunks)
+        check(scene, cams[1], opts, tier)
     print("ok")
 
 

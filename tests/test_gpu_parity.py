@@ -1,20 +1,22 @@
-"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle.
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, both precisions.
 
-Tier A (contract): bit-exact against the fp32 oracle -- projection fields,
-tile keys, per-tile sorted order, ranges, visible-index lists, RGB/alpha/
-depth/count, importance scores. The north-star tolerances (pixels <= 1e-4
-abs, scores <= 1e-5 rel) are asserted as well, but the observed difference
-is exactly zero by construction (same operations, same order, no FMA
-contraction, a shared exp2/exp).
-Tier B (semantic anchor): against the fp64 reference's own outputs
-(tests/golden, made by the reference), within the documented fp32 budget.
+fp32 frames vs Tier A and fp64 frames vs Tier C (the oracle's two contracts):
+bit-exact -- projection fields, tile keys, per-tile sorted order, ranges,
+visible-index lists, RGB/alpha/depth/count, importance scores. The north-star
+tolerances (pixels <= 1e-4 abs, scores <= 1e-5 rel) are asserted as well; the
+observed difference is exactly zero by construction (same operations, same
+order, no FMA contraction, shared exp implementations).
+Against the fp64 reference's own outputs (tests/golden, made by the
+reference): fp64 frames agree to 1e-12 with identical composite decisions;
+fp32 frames within the documented fp32 budget (tier_b_check).
 """
 
 import numpy as np
 import pytest
 import torch
 
-from conftest import golden, load_case, load_cam, options_from, render_cases, tier_b_check
+from conftest import (PREC_IDS, PRECISIONS, golden, load_case, load_cam, options_from, reference_check_fp64,
+                      render_cases, tier_b_check, with_precision)
 
 pytestmark = pytest.mark.gpu
 
@@ -31,10 +33,11 @@ def _oracle():
 
 
 def _render_gpu(scene, cam, opts, scores=True, count_evals=False):
-    from paper_2403_13806_b200.device import device_scene, renderer
+    from paper_2403_13806_b200.device import device_scene, precision_of, renderer, value_dtype
     from paper_2403_13806_b200.render import render_device
     ds = device_scene(scene)
-    sc = torch.zeros(max(ds.n, 1), dtype=torch.float32, device=ds.device) if scores else None
+    vt = value_dtype(precision_of(opts))
+    sc = torch.zeros(max(ds.n, 1), dtype=vt, device=ds.device) if scores else None
     out, st = render_device(ds, cam, opts, scores=sc, count_evals=count_evals)
     host = {k: v.cpu().numpy() for k, v in out.items()}
     if scores:
@@ -42,11 +45,13 @@ def _render_gpu(scene, cam, opts, scores=True, count_evals=False):
     return host, st, renderer(ds.device)
 
 
+@pytest.mark.parametrize("prec,tier", PRECISIONS, ids=PREC_IDS)
 @pytest.mark.parametrize("case", CASES, ids=IDS)
-def test_render_bit_exact_vs_fp32_oracle(case):
+def test_render_bit_exact_vs_oracle(case, prec, tier):
     name, scene, cam, opts, d, p = case
+    opts = with_precision(opts, prec)
     O = _oracle()
-    ref = O.render(scene, cam, opts, np.float32)
+    ref = O.render(scene, cam, opts, tier)
     got, st, _ = _render_gpu(scene, cam, opts)
     for k in ("img", "alpha", "depth"):
         g = got["rgb"] if k == "img" else got[k]
@@ -59,39 +64,56 @@ def test_render_bit_exact_vs_fp32_oracle(case):
 
 @pytest.mark.parametrize("case", CASES, ids=IDS)
 def test_render_vs_reference_fp64(case):
-    """Tier B: within fp32 of the reference's own output (golden, made by fieldsplat)."""
+    """fp64 frames vs the reference's own output (golden, made by fieldsplat):
+    identical composite decisions, pixels and scores within 1e-12."""
     name, scene, cam, opts, d, p = case
-    got, _, _ = _render_gpu(scene, cam, opts)
-    tier_b_check(name, got["rgb"], got["alpha"], got["count"], got["contrib"], d, p)
+    got, _, _ = _render_gpu(scene, cam, with_precision(opts, "fp64"))
+    reference_check_fp64(name, got["rgb"], got["alpha"], got["count"], got["contrib"], d, p)
 
 
 @pytest.mark.parametrize("case", CASES, ids=IDS)
-def test_projection_bit_exact(case):
+def test_render_vs_reference_fp32_budget(case):
+    """fp32 frames: within the documented fp32 budget of the reference (tier_b_check)."""
     name, scene, cam, opts, d, p = case
+    got, _, _ = _render_gpu(scene, cam, with_precision(opts, "fp32"))
+    tier_b_check(name, got["rgb"], got["alpha"], got["count"], got["contrib"], d, p)
+
+
+@pytest.mark.parametrize("prec,tier", PRECISIONS, ids=PREC_IDS)
+@pytest.mark.parametrize("case", CASES, ids=IDS)
+def test_projection_bit_exact(case, prec, tier):
+    name, scene, cam, opts, d, p = case
+    opts = with_precision(opts, prec)
     from paper_2403_13806_b200.render import project_scene
     O = _oracle()
-    ref = O.project(scene, cam, opts, np.float32)
+    ref = O.project(scene, cam, opts, tier)
+    vt = np.float32 if prec == "fp32" else np.float64
     _, proj = project_scene(scene, cam, opts)
     assert np.array_equal(proj["valid"], ref["valid"])
     v = ref["valid"]
     for k, rk in (("mx", "mx"), ("my", "my"), ("a", "a"), ("b", "b"), ("c", "c"), ("inv_a", "ia"),
                   ("inv_b", "ib"), ("inv_c", "ic"), ("radius", "radius"), ("depth", "depth"),
                   ("opacity", "opacity")):
-        assert np.array_equal(proj[k].astype(np.float32)[v], ref[rk][v]), (name, k)
-    assert np.array_equal(proj["color"].astype(np.float32)[v], ref["color"][v])
+        assert np.array_equal(proj[k].astype(vt)[v], ref[rk][v]), (name, k)
+    assert np.array_equal(proj["color"].astype(vt)[v], ref["color"][v])
     for k in ("x0", "x1", "y0", "y1"):
         assert np.array_equal(proj[k][v], ref[k][v]), (name, k)
     # against the reference's own projection (fp64): bbox/valid decisions agree
     assert np.array_equal(proj["valid"], d[p + "proj_valid"]), name
-    assert np.allclose(proj["mx"][v], d[p + "proj_mx"][v], rtol=1e-5, atol=1e-4)
+    if prec == "fp64":
+        assert np.allclose(proj["mx"][v], d[p + "proj_mx"][v], rtol=1e-13, atol=1e-12)
+    else:
+        assert np.allclose(proj["mx"][v], d[p + "proj_mx"][v], rtol=1e-5, atol=1e-4)
 
 
+@pytest.mark.parametrize("prec,tier", PRECISIONS, ids=PREC_IDS)
 @pytest.mark.parametrize("case", CASES, ids=IDS)
-def test_binning_bit_exact(case):
+def test_binning_bit_exact(case, prec, tier):
     """Tile keys, per-tile (depth, index) order and ranges equal the oracle's."""
     name, scene, cam, opts, d, p = case
+    opts = with_precision(opts, prec)
     O = _oracle()
-    ob = O.bin_tiles(scene, cam, opts, np.float32)
+    ob = O.bin_tiles(scene, cam, opts, tier)
     _, st, r = _render_gpu(scene, cam, opts, scores=False)
     fa = r.frame_arrays()
     assert fa["stats"].n_pairs == ob["P"] and not fa["stats"].overflow
@@ -107,48 +129,52 @@ def test_binning_bit_exact(case):
     assert np.array_equal(keys, ob["keys"]), name
     # global (depth, index) order over visible Gaussians
     nv = fa["stats"].n_visible
-    order = O.order(scene, cam, opts, np.float32)
+    order = O.order(scene, cam, opts, tier)
     assert nv == len(order) <= int(d[p + "proj_valid"].sum())
     assert np.array_equal(fa["items_sorted"][:nv].astype(np.int64), order)
 
 
-def test_filtered_equals_subset_render():
+@pytest.mark.parametrize("prec,tier", PRECISIONS, ids=PREC_IDS)
+def test_filtered_equals_subset_render(prec, tier):
     from paper_2403_13806_b200.render import rasterize, rasterize_filtered
     d = golden("known")
     scene, cam, o = load_case(d, "filtered_")
-    opts = options_from(o)
+    opts = options_from(o, prec)
     active = d["filtered_active"]
     O = _oracle()
-    ref = O.render(scene, cam, opts, np.float32, active=active)
+    ref = O.render(scene, cam, opts, tier, active=active)
     got = rasterize_filtered(scene, cam, active, opts)
-    assert np.array_equal(got.color.data.astype(np.float32), ref["img"])
+    assert np.array_equal(got.color.data.astype(ref["img"].dtype), ref["img"])
     assert np.array_equal(got.count, ref["count"])
-    assert np.abs(got.color.data - d["filtered_img"]).max() <= 1e-5
+    assert np.abs(got.color.data - d["filtered_img"]).max() <= (1e-5 if prec == "fp32" else 1e-12)
     # all-active filter is the identity (test_render.py:151-156)
     full = rasterize(scene, cam, opts)
     allf = rasterize_filtered(scene, cam, np.ones(len(scene), bool), opts)
     assert np.array_equal(full.color.data, allf.color.data)
 
 
-def test_compute_importance_matches_oracle_and_reference():
+@pytest.mark.parametrize("prec,tier", PRECISIONS, ids=PREC_IDS)
+def test_compute_importance_matches_oracle_and_reference(prec, tier):
     from paper_2403_13806_b200.core import GaussianScene
     from paper_2403_13806_b200.pruning import compute_importance
     d = golden("known")
     scene = GaussianScene(positions=d["imp_pos"], opacity_logits=d["imp_logit"], sh=d["imp_sh"],
                           log_scales=d["imp_ls"], quaternions=d["imp_quat"], active_sh_degree=int(d["imp_deg"]))
     cams = [load_cam(d, f"imp_cam{i}_") for i in range(2)]
-    table = compute_importance(scene, cams)
+    opts = options_from(None, prec)
+    table = compute_importance(scene, cams, opts)
     O = _oracle()
-    exp = np.zeros(len(scene), np.float32)
+    vt = np.float32 if prec == "fp32" else np.float64
+    exp = np.zeros(len(scene), vt)
     for cam in cams:
-        exp = np.maximum(exp, O.render(scene, cam, None, np.float32)["contrib"])
-    assert np.array_equal(table.values.astype(np.float32), exp)
+        exp = np.maximum(exp, O.render(scene, cam, opts, tier)["contrib"])
+    assert np.array_equal(table.values.astype(vt), exp)
     assert table.n_cameras == 2
     rel = np.abs(table.values - d["imp_values"]) / np.maximum(d["imp_values"], 1e-30)
-    assert rel.max() <= SCORE_RTOL
+    assert rel.max() <= (SCORE_RTOL if prec == "fp32" else 1e-12)
     # duplicate cameras / order invariance (test_pruning.py:54-66)
-    assert np.array_equal(compute_importance(scene, cams + cams + cams[:1]).values, table.values)
-    assert np.array_equal(compute_importance(scene, cams[::-1]).values, table.values)
+    assert np.array_equal(compute_importance(scene, cams + cams + cams[:1], opts).values, table.values)
+    assert np.array_equal(compute_importance(scene, cams[::-1], opts).values, table.values)
 
 
 def test_known_answers():
@@ -175,7 +201,8 @@ def test_known_answers():
     t = compute_importance(s, [cam])
     assert t.values[0] > 0.5 and t.values[3] == 0.0                             # test_pruning.py:68-73
     s, cam, _ = load_case(d, "occluder1_")
-    assert compute_importance(s, [cam]).values[0] == np.float32(0.99)           # clamp: 0.99f exactly
+    assert compute_importance(s, [cam]).values[0] == 0.99                       # clamp: alpha_max exactly
+    assert compute_importance(s, [cam], options_from(None, "fp32")).values[0] == np.float32(0.99)
     for nm in ("behind", "offscreen"):
         s, cam, _ = load_case(d, nm + "_")
         assert project_scene(s, cam)[0] == []
@@ -218,13 +245,15 @@ def test_accumulator_length_and_active_shape_rejected():
         rasterize_filtered(s, cam, np.ones(len(s) + 2, bool))
 
 
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
 @pytest.mark.parametrize("case", CASES[:12] + CASES[-4:], ids=IDS[:12] + IDS[-4:])
-def test_rasterize_host_outputs_equal_device_images(case):
+def test_rasterize_host_outputs_equal_device_images(case, prec):
     """rasterize(): the blend writes float64 colour/alpha and int64 count straight into
-    pinned host memory (rs_outputs rgb64/alpha64/count64) -- exactly the widened fp32
+    pinned host memory (rs_outputs rgb64/alpha64/count64) -- exactly the (widened)
     device images, including partial edge tiles."""
     from paper_2403_13806_b200.render import rasterize
     name, scene, cam, opts, d, p = case
+    opts = with_precision(opts, prec)
     got, _, _ = _render_gpu(scene, cam, opts, scores=False)
     res = rasterize(scene, cam, opts)
     assert res.color.data.dtype == np.float64 and res.alpha.dtype == np.float64 and res.count.dtype == np.int64
@@ -235,24 +264,26 @@ def test_rasterize_host_outputs_equal_device_images(case):
     assert np.array_equal(res.depth, got["depth"].astype(np.float64)), name
 
 
-def test_rasterize_host_outputs_odd_sizes():
+@pytest.mark.parametrize("prec,tier", PRECISIONS, ids=PREC_IDS)
+def test_rasterize_host_outputs_odd_sizes(prec, tier):
     """Image sizes that are not tile multiples: the staged row writes clip at W and H."""
     from oracle import oracle as O
     from paper_2403_13806_b200.core import look_at_camera
     from paper_2403_13806_b200.render import RasterizeOptions, rasterize
     from paper_2403_13806_b200.synth import config0
     scene, _ = config0(0)
-    opts = RasterizeOptions(near_limit=0.2)
+    opts = RasterizeOptions(near_limit=0.2, precision=prec)
     for w, h in ((1, 1), (17, 5), (33, 47), (130, 97)):
         cam = look_at_camera(np.array([0.0, -3.0, 0.4]), np.zeros(3), width=w, height=h, fov_deg=50.0)
         res = rasterize(scene, cam, opts)
-        ref = O.render(scene, cam, opts, np.float32)
+        ref = O.render(scene, cam, opts, tier)
         assert np.array_equal(res.color.data, ref["img"].astype(np.float64)), (w, h)
         assert np.array_equal(res.alpha, ref["alpha"].astype(np.float64)), (w, h)
         assert np.array_equal(res.count, ref["count"].astype(np.int64)), (w, h)
 
 
-def test_score_views_overflow_recovery_matches_per_view_renders():
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
+def test_score_views_overflow_recovery_matches_per_view_renders(prec):
     """A scoring pass launched without per-view host syncs: a view that overflows the
     pair capacity is detected once per pass (rs_read_overflow) and the pass re-run from a
     snapshot -- the result equals the max over checked single-view renders."""
@@ -260,16 +291,17 @@ def test_score_views_overflow_recovery_matches_per_view_renders():
     from paper_2403_13806_b200.render import RasterizeOptions, render_device
     from paper_2403_13806_b200.synth import config2
     scene, cams = config2(0, n=60_000, n_views=6)
-    opts = RasterizeOptions(near_limit=0.2)
+    opts = RasterizeOptions(near_limit=0.2, precision=prec)
+    vt = torch.float32 if prec == "fp32" else torch.float64
     ds = device_scene(scene)
-    ref = torch.zeros(ds.n, dtype=torch.float32, device=ds.device)
+    ref = torch.zeros(ds.n, dtype=vt, device=ds.device)
     for c in cams:
         render_device(ds, c, opts, color=False, scores=ref)
     r = Renderer(ds.device)
     r.ensure(ds.n, 1 << 16, cams[0].width, cams[0].height)  # far below this pass's P
-    pre = torch.rand(ds.n, device=ds.device) * 1e-3  # an accumulator that already holds values
+    pre = torch.rand(ds.n, device=ds.device, dtype=vt) * 1e-3  # an accumulator that already holds values
     got = pre.clone()
-    r.score_views(ds, cams, opts, got.view(torch.int32))
+    r.score_views(ds, cams, opts, got)
     assert r.caps[1] > (1 << 16)
     assert torch.equal(got, torch.maximum(ref, pre))
     over, _ = r.read_overflow()

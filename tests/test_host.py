@@ -35,11 +35,36 @@ def test_library_exports_every_declared_symbol():
         assert hasattr(lib, n), n
     assert set(_declared()) == set(_native.SIGNATURES)
     lib = _native.load(require_cuda=False)
-    assert lib.rs_abi_version() == 1
+    assert lib.rs_abi_version() == _native.ABI_VERSION == 2
     assert lib.rs_status_string(5) == b"tile pair capacity exceeded"
     assert lib.rs_workspace_size(500_000, 10_000_000, 1256, 828) > 0
     assert lib.rs_workspace_size(-1, 10, 16, 16) == 0
     assert lib.rs_compact_workspace_size(0) > 0
+
+
+def test_integration_structs_match_header():
+    """INTEGRATION.md's documented ctypes structs (the binding a maintainer copies) have
+    the header's fields, types and sizes -- i.e. _native.py's mirror of include/radsplat.h."""
+    import ctypes
+    import re
+
+    from paper_2403_13806_b200 import _native as N
+    text = (ROOT / "INTEGRATION.md").read_text()
+    block = re.search(r"```python\n(# rs structs \(ABI 2\)\n.*?)```", text, re.S)
+    assert block, "INTEGRATION.md lost its struct block"
+    ns = {}
+    exec(block.group(1), ns)
+    for doc, mine in (("rs_scene", N.RsScene), ("rs_camera", N.RsCamera), ("rs_options", N.RsOptions),
+                      ("rs_outputs", N.RsOutputs), ("rs_stats", N.RsStats)):
+        d = ns[doc]
+        assert ctypes.sizeof(d) == ctypes.sizeof(mine), doc
+        assert [(n, t) for n, t in d._fields_] == [(n, t) for n, t in mine._fields_], doc
+    assert len(N.RsOutputs._fields_) == 9
+    # and the header declares the same members in the same order
+    hdr = (ROOT / "include" / "radsplat.h").read_text()
+    body = re.search(r"typedef struct rs_outputs \{(.*?)\} rs_outputs;", hdr, re.S).group(1)
+    members = re.findall(r"\*\s*(\w+);", body)
+    assert members == [n for n, _ in N.RsOutputs._fields_]
 
 
 def test_status_codes_map_to_reference_exceptions():
@@ -309,3 +334,47 @@ def test_sharded_scoring_merge_gloo_world2():
         assert p.exitcode == 0
     for _, got, exp in res:
         assert got == exp  # bit-identical to the single-process max over all views
+
+
+def _bits_worker(rank, world, port, q):
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2403_13806_b200.dist import shard_range
+    from paper_2403_13806_b200.visibility import gather_cluster_bits
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        k, n = 7, 37
+        full = np.random.default_rng(11).uniform(size=(k, n)) > 0.6
+        lo, hi = shard_range(k, rank, world)  # this rank "bakes" clusters [lo, hi)
+        local = torch.from_numpy(np.packbits(full[lo:hi], axis=1, bitorder="little").reshape(hi - lo, -1))
+        got = gather_cluster_bits(local, k, n)
+        q.put((rank, got.tobytes(), full.tobytes()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_cluster_bitset_gather_gloo_world2():
+    """bake_visibility(shard=True)'s merge: per-rank LSB-first cluster bitsets all-gathered
+    into the (k, N) indicators, identical on every rank (visibility.py:195-204)."""
+    import socket
+
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_bits_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for _, got, exp in res:
+        assert got == exp

@@ -89,7 +89,7 @@ def test_scene_file_straight_to_device(tmp_path, name):
     io, d = _io(), golden("io")
     p = _write(tmp_path, name, d)
     ds = io.load_scene_device(p)
-    ref = DeviceScene(io.load_scene(p))
+    ref = DeviceScene(io.load_scene(p), dtype=np.float32)  # RSPL payloads are fp32
     n = ref.n
     assert ds.n == n and ds.sh_degree == ref.sh_degree
     assert torch.equal(ds.planes[:, :n], ref.planes[:, :n]) and torch.equal(ds.sh[:n], ref.sh[:n])
