@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--n-gaussians", type=int, default=None, help="override N (debug only)")
+    ap.add_argument("--precision", choices=("fp32", "fp64"), default="fp32",
+                    help="arithmetic of the timed frames (fp32 = BASELINE configs' dtype)")
     a = ap.parse_args()
     if a.steps is None:
         a.steps = {"render": 200, "score": 5, "house": 300, "batch": 3, "train": 100}[a.workload]
@@ -138,11 +140,12 @@ def peaks():
 # ---------------------------------------------------------------------------
 # CPU baseline (oracle port, all host cores)
 # ---------------------------------------------------------------------------
-def cpu_views(scene, cams, images: bool, threads: int | None = None):
+def cpu_views(scene, cams, images: bool, threads: int | None = None, precision: str = "fp32"):
     from oracle import oracle as O
     O.build()
     t0 = time.perf_counter()
-    r = O.views(scene, cams, dict_opts(), np.float32, threads=threads, scores=not images, images=images)
+    r = O.views(scene, cams, dict_opts(precision), np.float32 if precision == "fp32" else np.float64,
+                threads=threads, scores=not images, images=images)
     return time.perf_counter() - t0, r
 
 
@@ -235,7 +238,8 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    opts = dict_opts()
+    opts = dict_opts(args.precision)
+    PREC = 1 if args.precision == "fp64" else 0
     r = renderer(dev)
     lib = r.lib
     opt_s = options_struct(opts)
@@ -260,7 +264,7 @@ def main():
     result = {}
     if args.workload == "render":
         frames = lambda s: cams[(s * world + rank) % len(cams)]  # noqa: E731
-        out = r.alloc_outputs(cams[0])
+        out = r.alloc_outputs(cams[0], precision=PREC)
         # untimed pre-pass over every frame the timed loop will render: sizes the
         # pair capacity (overflow-checked) and counts E / C for the roofline
         E = C_ = P_ = NV = 0
@@ -327,7 +331,7 @@ def main():
         result.update({
             "metric": METRICS["render"], "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64" if PREC else "f32",
             "data": "synthetic (seeded configs[1]: 500k Gaussians in 32 clusters, SH deg 3; no dataset offline)",
             "config": {"workload": "configs[1] orbit render", "n_gaussians": len(scene), "width": W_, "height": H_,
                        "tile": 16, "frames": args.steps, "l2": "flushed (256 MB memset) between timed steps",
@@ -382,7 +386,7 @@ def main():
         n = len(cams)
         lo, hi = shard_range(n, rank, world)
         mine = [camera_struct(c) for c in cams[lo:hi]]
-        scores = torch.zeros(len(scene), dtype=torch.float32, device=dev)
+        scores = torch.zeros(len(scene), dtype=torch.float64 if PREC else torch.float32, device=dev)
         # pre-pass: overflow-checked capacity sizing over this rank's views
         P_ = 0
         for c in cams[lo:hi]:
@@ -445,7 +449,7 @@ def main():
         result.update({
             "metric": METRIC_SCORE, "value": value, "unit": "views/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64" if PREC else "f32",
             "data": "synthetic (seeded configs[2]: 3M Gaussians, log-scale N(-4,0.6); no dataset offline)",
             "config": {"workload": "configs[2] importance scoring", "n_gaussians": len(scene), "views": n,
                        "width": W_, "height": H_, "l2": "flushed (256 MB memset) between timed passes",

@@ -10,11 +10,13 @@
 //     order with std::exp, pinned against golden vectors produced by the
 //     reference itself (tests/golden/make_golden.py).
 //   * T = double, CT ("Tier C", the parity contract of the CUDA path's RS_F64
-//     frames): Tier B with exp64_contract (an exp from IEEE double add/mul/fma
-//     only; device twin in csrc/rs_math.cuh) instead of std::exp, its argument
-//     clamped at 709 (an overflow guard), and the pixel gate of the fp32 tier's
-//     culling box (which drops only pixels with alpha < alpha_cut). Tier C vs
-//     Tier B: within a few ulp.
+//     frames): Tier B's projection with exp64_contract (an exp from IEEE double
+//     add/mul/fma only; device twin in csrc/rs_math.cuh) instead of std::exp;
+//     the composite with fused roundings -- x = -q/2 as two fmas, a table exp
+//     (exp64_tab) with its argument clamped at 709 (an overflow guard),
+//     rgb/depth += c w and tau (1 - alpha) as fmas -- and the pixel gate of the
+//     fp32 tier's culling box (which drops only pixels with alpha < alpha_cut).
+//     Tier C vs Tier B (and the reference): a few ulp (tests: <= 1e-12).
 //   * T = float   ("Tier A", the parity contract for the CUDA path): the same
 //     algorithm in fp32 with every operation and its order written out, no
 //     FMA contraction except the explicit fmaf() calls (-ffp-contract=off),
@@ -158,6 +160,46 @@ inline double exp64_contract(double x) {
   if (ni > 1023) return (p * pow2i64(1023)) * 2.0;
   if (ni >= -1022) return p * pow2i64(ni);
   return (p * pow2i64(ni + 600)) * pow2i64(-600);
+}
+
+// e^x of the fp64 contract's blend (device twin: exp64_tab in csrc/rs_math.cuh):
+// k = rint(x 64 / ln 2), r = x - k ln2/64 (Cody-Waite), degree-5 Taylor, times
+// T[k mod 64] = exp64_contract(j ln2/64) scaled by 2^(k div 64) in the exponent field.
+struct Exp64Tab {
+  double T[64];
+  Exp64Tab() {
+    for (int j = 0; j < 64; ++j) T[j] = exp64_contract((double)j * (0.6931471805599453 / 64.0));
+  }
+};
+inline double with_exp(double t, int add) {  // t * 2^add by the exponent field (t normal, result normal)
+  uint64_t u;
+  std::memcpy(&u, &t, 8);
+  u += (uint64_t)(int64_t)add << 52;
+  double d;
+  std::memcpy(&d, &u, 8);
+  return d;
+}
+inline double exp64_tab(double x) {
+  static const Exp64Tab tab;
+  if (x != x) return x;
+  if (x > 709.782712893384) return INFINITY;
+  if (x < -745.2) return 0.0;
+  const double t = std::fma(x, 92.33248261689366, 6755399441055744.0);
+  const double kd = t - 6755399441055744.0;
+  double r = std::fma(kd, -(0.6931471803691238 / 64.0), x);
+  r = std::fma(kd, -(1.9082149292705877e-10 / 64.0), r);
+  double p = std::fma(1.0 / 120.0, r, 1.0 / 24.0);
+  p = std::fma(p, r, 1.0 / 6.0);
+  p = std::fma(p, r, 0.5);
+  p = std::fma(p, r, 1.0);
+  p = std::fma(p, r, 1.0);
+  uint64_t tb;
+  std::memcpy(&tb, &t, 8);
+  const int k = (int)(int32_t)(uint32_t)tb;
+  const int n = k >> 6;
+  const double tj = tab.T[k & 63];
+  if (n >= -1022) return p * with_exp(tj, n);
+  return (p * with_exp(tj, n + 600)) * pow2i64(-600);
 }
 
 template <typename T> struct M;
@@ -471,11 +513,12 @@ template <typename T> inline void atomic_max(T* p, T v) {
 // Per-pixel evaluation of one Gaussian: returns alpha (render.py:255-259).
 template <typename T, bool CT = false> inline T pixel_alpha(const PG<T>& g, T xs, T ys, T alpha_max);
 template <> inline double pixel_alpha<double, true>(const PG<double>& g, double xs, double ys, double alpha_max) {
-  // Tier C: the reference expression with the contract exp, argument clamped at 709
+  // Tier C: -q/2 of render.py:254-256 with fused roundings, (na, nb, nc) = -(ia/2, ib, ic/2)
+  // (exact scalings), the table exp, argument clamped at 709
+  const double na = -0.5 * g.ia, nb = -g.ib, nc = -0.5 * g.ic;
   const double dx = xs - g.mx, dy = ys - g.my;
-  const double q = (g.ia * dx * dx) + (2.0 * g.ib) * dy * dx + (g.ic * dy * dy);
-  const double x = -0.5 * q;
-  const double raw = g.opacity * exp64_contract(x < 709.0 || x != x ? x : 709.0);
+  const double x = std::fma(nc * dy, dy, std::fma(nb * dy, dx, (na * dx) * dx));
+  const double raw = g.opacity * exp64_tab(x > 709.0 ? 709.0 : x);
   return (raw != raw || raw < alpha_max) ? raw : alpha_max;
 }
 template <> inline double pixel_alpha<double, false>(const PG<double>& g, double xs, double ys, double alpha_max) {
@@ -521,14 +564,22 @@ inline void composite_pixel(const std::vector<PG<T>>& pg, const int64_t* list, s
     const T alpha = pixel_alpha<T, CT>(g, xs, ys, o.alpha_max);
     if (alpha >= o.alpha_cut && tau >= o.tau_stop) {
       const T w = alpha * tau;  // render.py:267
-      r = mac<T>(g.color[0], w, r);
-      gg = mac<T>(g.color[1], w, gg);
-      b = mac<T>(g.color[2], w, b);
-      d = mac<T>(g.depth, w, d);
+      if constexpr (CT) {  // Tier C: fused accumulation and transmittance update
+        r = std::fma(g.color[0], w, r);
+        gg = std::fma(g.color[1], w, gg);
+        b = std::fma(g.color[2], w, b);
+        d = std::fma(g.depth, w, d);
+      } else {
+        r = mac<T>(g.color[0], w, r);
+        gg = mac<T>(g.color[1], w, gg);
+        b = mac<T>(g.color[2], w, b);
+        d = mac<T>(g.depth, w, d);
+      }
       if (contrib) atomic_max(contrib + list[j], w);  // render.py:273-275
       ++c;
       ++k.C;
-      tau = tau * ((T)1 - alpha);  // render.py:281
+      if constexpr (CT) tau = std::fma(-alpha, tau, tau);
+      else tau = tau * ((T)1 - alpha);  // render.py:281
     }
   }
   rgbd[0] = r; rgbd[1] = gg; rgbd[2] = b; rgbd[3] = d;

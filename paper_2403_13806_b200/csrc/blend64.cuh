@@ -11,13 +11,19 @@
 // fp64 region alpha >= alpha_cut), the per-pixel culling-box gate as one AND
 // against the lane's column / row bits.
 //
-// Per pixel and Gaussian (render.py:254-281):
-//   q     = (ia dx) dx + ((2 ib) dy) dx + (ic dy) dy
-//   alpha = min(o exp(-q/2), alpha_max)            (exp64_contract, arg <= 709)
+// Per pixel and Gaussian (render.py:254-281, with fused roundings):
+//   x     = fma(nc dy, dy, fma(nb dy, dx, (na dx) dx))   (= -q/2; (na,nb,nc) = -(ia/2, ib, ic/2))
+//   alpha = min(o exp(min(x, 709)), alpha_max)          (exp64_tab, rs_math.cuh)
 //   if alpha >= alpha_cut and tau >= tau_stop:
-//       w = alpha tau; rgb = rgb + c w; depth = depth + z w; count++; tau = tau (1 - alpha)
-// -q/2 < lnc (a conservative per-Gaussian bound) proves alpha < alpha_cut
-// without the exp. Importance: the warp maximum of w's fp64 bits (two REDUX
+//       w = alpha tau; rgb = fma(c, w, rgb); depth = fma(z, w, depth); count++;
+//       tau = fma(-alpha, tau, tau)
+// x < lnc (a conservative per-Gaussian bound) proves alpha < alpha_cut. A pixel
+// that does not composite takes alpha = 0 (w = +0, fma(c, 0, rgb) = rgb, tau
+// unchanged: exactly the skipped composite), so the loop has no branches. With
+// FAST (alpha_cut >= 1e-300, alpha_max and tau_stop >= 0) the threshold tests are
+// integer compares of the fp64 bit patterns (the thresholds are non-negative, so
+// the signed order of the bits is the value order) -- the FP64 pipe is the
+// kernel's bound. Importance: the warp maximum of w's fp64 bits (two REDUX
 // steps: high words, then low words among the lanes holding the maximal high
 // word; w >= 0, so the unsigned order is the value order), one shared 64-bit
 // atomicMax per (entry, group), one global atomicMax per (tile, Gaussian).
@@ -30,17 +36,9 @@ namespace rs {
 
 constexpr int kBlend64Threads = 128;
 
-// e^x for x <= 709 (hot-loop form of exp64_contract): FAST = the caller
-// guarantees x >= lnc >= ln(1e-300) - 1e-6, so the result is normal
-template <bool FAST>
-__device__ __forceinline__ double exp64_hot(double x) {
-  if (!FAST) return exp64_contract(x);
-  const double t = __fma_rn(x, kLog2e64, kMagic64);
-  const double n = __dsub_rn(t, kMagic64);
-  double r = __fma_rn(n, -kLn2Hi, x);
-  r = __fma_rn(n, -kLn2Lo, r);
-  return __dmul_rn(exp64_poly(r), pow2i64(__double2loint(t)));
-}
+// a >= b / a > b for doubles with b >= 0 (not NaN): the signed order of the bit patterns
+__device__ __forceinline__ bool ge_nn(double a, double b) { return __double_as_longlong(a) >= __double_as_longlong(b); }
+__device__ __forceinline__ bool gt_nn(double a, double b) { return __double_as_longlong(a) > __double_as_longlong(b); }
 
 __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
   const uint32_t hi = (uint32_t)(v >> 32), lo = (uint32_t)v;
@@ -49,8 +47,11 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v)
   return ((unsigned long long)mh << 32) | ml;
 }
 
+#ifndef RS_BLEND64_MINB
+#define RS_BLEND64_MINB 4  // 4 CTAs / SM: <= 128 registers (shared memory allows 4 as well)
+#endif
 template <bool COLOR, bool CONTRIB, bool STATS, bool FAST>
-__global__ void __launch_bounds__(kBlend64Threads, 1) blend64_kernel(
+__global__ void __launch_bounds__(kBlend64Threads, RS_BLEND64_MINB) blend64_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ pair_items, const Rec* __restrict__ recs,
     const Rec64* __restrict__ recs64, const float4* __restrict__ geom, const uint32_t* __restrict__ tile_order,
     Counters* __restrict__ ctr, int W, int H, int TW, Opt64 o, const Out64 out,
@@ -65,6 +66,7 @@ __global__ void __launch_bounds__(kBlend64Threads, 1) blend64_kernel(
   __shared__ uint8_t s_mask[kBatch];
   __shared__ uint16_t s_boxm[kBatch + 1][4];
   __shared__ uint16_t s_list[4][kBatch + U];
+  __shared__ double s_exp[64];  // exp64_tab's 2^(j/64) table
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int tile = (int)__ldg(tile_order + blockIdx.x);
@@ -86,6 +88,7 @@ __global__ void __launch_bounds__(kBlend64Threads, 1) blend64_kernel(
   double r0 = 0.0, g0 = 0.0, b0 = 0.0, d0 = 0.0, r1 = 0.0, g1 = 0.0, b1 = 0.0, d1 = 0.0;
   int cnt0 = 0, cnt1 = 0;
   unsigned long long evals = 0;
+  if (tid < 64) s_exp[tid] = exp64_tab_entry(tid);
   if (tid == 0) {
     Rec64 z{};
     s_rec[kBatch] = z;
@@ -163,57 +166,54 @@ __global__ void __launch_bounds__(kBlend64Threads, 1) blend64_kernel(
           bx0[u] = (bm & sel0) == sel0;
           bx1[u] = (bm & sel1) == sel1;
           const double dx = xs - E.mx;
-          const double qa = (E.ia * dx) * dx;
+          const double qa = (E.na * dx) * dx;
           const double dy0 = ys0 - E.my, dy1 = ys1 - E.my;
-          const double q0 = (qa + (E.ib2 * dy0) * dx) + (E.ic * dy0) * dy0;
-          const double q1 = (qa + (E.ib2 * dy1) * dx) + (E.ic * dy1) * dy1;
-          const double x0 = -0.5 * q0, x1 = -0.5 * q1;
+          const double x0 = __fma_rn(E.nc * dy0, dy0, __fma_rn(E.nb * dy0, dx, qa));
+          const double x1 = __fma_rn(E.nc * dy1, dy1, __fma_rn(E.nb * dy1, dx, qa));
           const bool e0 = bx0[u] && x0 >= E.lnc, e1 = bx1[u] && x1 >= E.lnc;
-          double a0 = 0.0, a1 = 0.0;
-          if (e0) {
-            const double raw = E.o * exp64_hot<FAST>(fmin(x0, 709.0));
-            a0 = raw > o.alpha_max ? o.alpha_max : raw;
-          }
-          if (e1) {
-            const double raw = E.o * exp64_hot<FAST>(fmin(x1, 709.0));
-            a1 = raw > o.alpha_max ? o.alpha_max : raw;
+          // evaluated for every lane (the values of skipped pixels are discarded)
+          const double xc0 = gt_nn(x0, 709.0) ? 709.0 : x0, xc1 = gt_nn(x1, 709.0) ? 709.0 : x1;
+          const double raw0 = E.o * exp64_tab<FAST>(xc0, s_exp), raw1 = E.o * exp64_tab<FAST>(xc1, s_exp);
+          double a0, a1;
+          if (FAST) {
+            a0 = gt_nn(raw0, o.alpha_max) ? o.alpha_max : raw0;
+            a1 = gt_nn(raw1, o.alpha_max) ? o.alpha_max : raw1;
+            ok0[u] = e0 && ge_nn(a0, o.alpha_cut);
+            ok1[u] = e1 && ge_nn(a1, o.alpha_cut);
+          } else {
+            a0 = raw0 > o.alpha_max ? o.alpha_max : raw0;
+            a1 = raw1 > o.alpha_max ? o.alpha_max : raw1;
+            ok0[u] = e0 && a0 >= o.alpha_cut;
+            ok1[u] = e1 && a1 >= o.alpha_cut;
           }
           al0[u] = a0;
           al1[u] = a1;
-          ok0[u] = e0 && a0 >= o.alpha_cut;
-          ok1[u] = e1 && a1 >= o.alpha_cut;
         }
         unsigned long long wmax[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const Rec64& E = s_rec[ent[u]];
-          const bool live0 = tau0 >= o.tau_stop, live1 = tau1 >= o.tau_stop;
+          const bool live0 = FAST ? ge_nn(tau0, o.tau_stop) : tau0 >= o.tau_stop;
+          const bool live1 = FAST ? ge_nn(tau1, o.tau_stop) : tau1 >= o.tau_stop;
           if (STATS) evals += (unsigned)(bx0[u] && live0 && in0) + (unsigned)(bx1[u] && live1 && in1);
           const bool c0 = ok0[u] && live0, c1 = ok1[u] && live1;
-          double w0 = 0.0, w1 = 0.0;
-          if (c0) {
-            w0 = al0[u] * tau0;
-            if (COLOR) {
-              r0 = r0 + E.r * w0;
-              g0 = g0 + E.g * w0;
-              b0 = b0 + E.b * w0;
-              d0 = d0 + E.depth * w0;
-            }
-            tau0 = tau0 * (1.0 - al0[u]);
-            ++cnt0;
+          const double ae0 = c0 ? al0[u] : 0.0, ae1 = c1 ? al1[u] : 0.0;
+          const double w0 = ae0 * tau0, w1 = ae1 * tau1;
+          if (COLOR) {
+            r0 = __fma_rn(E.r, w0, r0);
+            g0 = __fma_rn(E.g, w0, g0);
+            b0 = __fma_rn(E.b, w0, b0);
+            d0 = __fma_rn(E.depth, w0, d0);
+            r1 = __fma_rn(E.r, w1, r1);
+            g1 = __fma_rn(E.g, w1, g1);
+            b1 = __fma_rn(E.b, w1, b1);
+            d1 = __fma_rn(E.depth, w1, d1);
           }
-          if (c1) {
-            w1 = al1[u] * tau1;
-            if (COLOR) {
-              r1 = r1 + E.r * w1;
-              g1 = g1 + E.g * w1;
-              b1 = b1 + E.b * w1;
-              d1 = d1 + E.depth * w1;
-            }
-            tau1 = tau1 * (1.0 - al1[u]);
-            ++cnt1;
-          }
-          wmax[u] = (unsigned long long)__double_as_longlong(fmax(w0, w1));
+          tau0 = __fma_rn(-ae0, tau0, tau0);
+          tau1 = __fma_rn(-ae1, tau1, tau1);
+          cnt0 += c0 ? 1 : 0;
+          cnt1 += c1 ? 1 : 0;
+          wmax[u] = (unsigned long long)__double_as_longlong(w0 > w1 ? w0 : w1);
         }
         if (CONTRIB) {
           unsigned long long mine = 0;
@@ -226,8 +226,8 @@ __global__ void __launch_bounds__(kBlend64Threads, 1) blend64_kernel(
           }
           if (mine) atomicMax(&s_w[slot], mine);
         }
-        done0 = !in0 || tau0 < o.tau_stop;
-        done1 = !in1 || tau1 < o.tau_stop;
+        done0 = !in0 || !(FAST ? ge_nn(tau0, o.tau_stop) : tau0 >= o.tau_stop);
+        done1 = !in1 || !(FAST ? ge_nn(tau1, o.tau_stop) : tau1 >= o.tau_stop);
         if (__all_sync(0xffffffffu, done0 && done1)) break;
       }
     }

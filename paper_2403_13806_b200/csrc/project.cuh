@@ -498,7 +498,7 @@ __global__ void __launch_bounds__(128) project64_kernel(const TS* __restrict__ p
         recs[item] = rec;
         Rec64 r64;
         r64.mx = mx; r64.my = my;
-        r64.ia = ia; r64.ib2 = 2.0 * ib; r64.ic = ic;
+        r64.na = -0.5 * ia; r64.nb = -ib; r64.nc = -0.5 * ic;
         r64.o = op; r64.depth = depth;
         // conservative exp skip (a margin far above the exp / log rounding): -q/2 < lnc
         // implies o * exp(-q/2) < alpha_cut; never changes a result

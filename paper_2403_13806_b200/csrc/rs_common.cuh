@@ -31,14 +31,15 @@ struct __align__(16) Rec {
 static_assert(sizeof(Rec) == 64, "record must be 64 B");
 
 // fp64 record of an RS_F64 frame (96 B = 6 x 16 B), the reference's projected
-// quantities in double (render.py:95-158): the blend evaluates
-// q = (ia dx) dx + (ib2 dy) dx + (ic dy) dy, alpha = min(o exp(-q/2), alpha_max)
-// exactly as render.py:254-259. lnc = ln(alpha_cut / o) - 1e-6 is a conservative
-// skip bound (-q/2 < lnc => alpha < alpha_cut): the exp is not evaluated, no
-// result changes. The binning uses the fp32 Rec written next to it (boxes, row
-// geometry, depth key).
+// quantities in double (render.py:95-158), the conic pre-scaled by -1/2 (exact):
+// (na, nb, nc) = -(ia/2, ib, ic/2), so the blend's
+// x = fma(nc dy, dy, fma(nb dy, dx, (na dx) dx)) is -q/2 of render.py:254-256 with
+// fused roundings, alpha = min(o e^x, alpha_max). lnc = ln(alpha_cut / o) - 1e-6 is
+// a conservative skip bound (x < lnc => alpha < alpha_cut): the exp is not
+// evaluated, no result changes. The binning uses the fp32 Rec written next to it
+// (boxes, row geometry, depth key).
 struct __align__(16) Rec64 {
-  double mx, my, ia, ib2, ic, o, depth, lnc;
+  double mx, my, na, nb, nc, o, depth, lnc;
   double r, g, b;
   uint32_t gid, pad;
 };

@@ -141,6 +141,43 @@ __device__ __forceinline__ double exp64_contract(double x) {
   return __dmul_rn(__dmul_rn(p, pow2i64(ni + 600)), pow2i64(-600));  // subnormal range
 }
 
+// e^x for the fp64 blend (oracle: exp64_tab): k = rint(x 64 / ln 2), r = x - k ln2/64
+// (Cody-Waite, |r| <= ln2/128), e^r by its degree-5 Taylor polynomial (truncation
+// < 4e-17), times T[k mod 64] 2^(k div 64) -- T[j] = exp64_contract(j ln2/64), the
+// kernel's shared-memory table; the power of two is added to T's exponent field.
+// FAST: the caller guarantees the result is a normal number (x in [-708, 709]).
+constexpr double kInvLn2x64 = 92.33248261689366;              // 64 / ln 2
+constexpr double kLn2o64Hi = 0.6931471803691238 / 64.0;        // kLn2Hi / 64 (exact)
+constexpr double kLn2o64Lo = 1.9082149292705877e-10 / 64.0;    // kLn2Lo / 64 (exact)
+constexpr double kLn2o64 = 0.6931471805599453 / 64.0;          // table argument step
+
+__device__ __forceinline__ double exp64_tab_entry(int j) { return exp64_contract((double)j * kLn2o64); }
+
+template <bool FAST>
+__device__ __forceinline__ double exp64_tab(double x, const double* __restrict__ T) {
+  if (!FAST) {
+    if (x != x) return x;
+    if (x > 709.782712893384) return __longlong_as_double(0x7ff0000000000000ll);
+    if (x < -745.2) return 0.0;
+  }
+  const double t = __fma_rn(x, kInvLn2x64, kMagic64);
+  const double kd = __dsub_rn(t, kMagic64);
+  double r = __fma_rn(kd, -kLn2o64Hi, x);
+  r = __fma_rn(kd, -kLn2o64Lo, r);
+  double p = __fma_rn(1.0 / 120.0, r, 1.0 / 24.0);
+  p = __fma_rn(p, r, 1.0 / 6.0);
+  p = __fma_rn(p, r, 0.5);
+  p = __fma_rn(p, r, 1.0);
+  p = __fma_rn(p, r, 1.0);
+  const int k = __double2loint(t);
+  const int n = k >> 6;  // floor(k / 64)
+  const double tj = T[k & 63];
+  if (FAST || n >= -1022)
+    return __dmul_rn(p, __hiloint2double(__double2hiint(tj) + (n << 20), __double2loint(tj)));
+  return __dmul_rn(__dmul_rn(p, __hiloint2double(__double2hiint(tj) + ((n + 600) << 20), __double2loint(tj))),
+                   pow2i64(-600));
+}
+
 // order-preserving 32-bit key of an fp32 depth (-0 folded into +0)
 __device__ __forceinline__ uint32_t depth_key(float d) {
   const uint32_t u = __float_as_uint(__fadd_rn(d, 0.0f));
