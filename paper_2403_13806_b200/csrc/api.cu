@@ -12,6 +12,7 @@
 #include <new>
 
 #include "segbin.cuh"
+#include "dsort.cuh"
 #include "blend.cuh"
 #include "blend64.cuh"
 #include "compact.cuh"
@@ -38,6 +39,31 @@ static int pdl_mode() {  // RS_PDL (A/B measurements): bit 0 binning chain, bit 
   return m;
 }
 static thread_local int g_pdl_class = kPdlChain;  // class of the next launch() (set by the callers below)
+
+// A cooperative launch (all CTAs co-resident: grid barriers inside the kernel are safe).
+template <typename... KP, typename... A>
+static cudaError_t launch_coop(void (*k)(KP...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, A&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KP>(args)...);
+}
+
+constexpr uint32_t kDsortMaxItems = 1u << 20;
+static int dsort_mode() {  // RS_DSORT: 0 onesweep launches, 2 always the cooperative sort (A/B measurements)
+  static const int m = [] {
+    const char* e = std::getenv("RS_DSORT");
+    return e ? std::atoi(e) : 1;
+  }();
+  return m;
+}
 template <typename... KP, typename... A>
 static void launch(void (*k)(KP...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, A&&... args) {
   cudaLaunchConfig_t cfg{};
@@ -59,14 +85,26 @@ namespace {
 
 size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
+constexpr int kMaxDsortCtas = 160;  // cooperative depth sort: one CTA per SM (column_prefix: <= 32 x 5 rows)
+
 struct Layout {
   // per-frame zeroed region [0, frame_bytes)
   size_t ctr, hist, proj_lb, ranges, frame_bytes;
-  size_t sticky, cam, recs, recs64, rows, sgrad, titem, keysA, keysB, valsA, valsB, rowtab, rowcnt, segitem, segspan, geom,
-      rowstart, chunkstart, chunkcnt, chunkinfo, densel, tilecnt, tileord, pitem, lbA, lbB, total;
+  size_t sticky, cam, recs, recs64, dtab, rows, sgrad, titem, keysA, keysB, valsA, valsB, rowtab, rowcnt, segitem, segspan, geom,
+      rowstart, chunkstart, chunkcnt, keysC, chunkinfo, densel, tilecnt, tileord, pitem, lbA, lbB, total;
 };
 
 int tiles_x(int w) { return (w + kTile - 1) / kTile; }
+
+int device_sms() {  // SMs of the current device (148 on B200)
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+    cudaGetLastError();
+    sms = 148;
+  }
+  return sms;
+}
 
 size_t rowtab_stride(int64_t n_cap) { return (size_t)n_cap / kRankChunk + 1; }
 
@@ -76,7 +114,7 @@ int64_t seg_capacity(int64_t n_cap, int64_t pair_cap) {
   return std::min<int64_t>(pair_cap + 2 * n_cap, 0xffffffffLL);
 }
 
-Layout make_layout(int64_t n_cap, int64_t pair_cap, int W, int H) {
+Layout make_layout(int64_t n_cap, int64_t pair_cap, int W, int H, int sms) {
   Layout L{};
   const size_t TW = tiles_x(W), TH = tiles_x(H);
   const size_t seg_cap = (size_t)seg_capacity(n_cap, pair_cap);
@@ -87,16 +125,19 @@ Layout make_layout(int64_t n_cap, int64_t pair_cap, int W, int H) {
   L.hist = take(4 * 256 * sizeof(uint32_t));  // depth passes 0-3
   L.proj_lb = take(((size_t)n_cap / kCompactKeys + 2) * sizeof(unsigned long long));
   L.ranges = take(TW * TH * sizeof(uint2));
+  L.dtab = take((size_t)4 * std::min(sms, kMaxDsortCtas) * 256 * 4);  // dsort_kernel's per-pass digit tables
   L.frame_bytes = o;
   L.sticky = take(sizeof(Sticky));
   L.cam = take(sizeof(CamPair));
   L.recs = take((size_t)n_cap * sizeof(Rec));
   L.recs64 = take((size_t)n_cap * sizeof(Rec64));  // RS_F64 frames
+
   L.rows = take((size_t)n_cap * 4);  // per binned item its tile-row range
   L.sgrad = take((size_t)n_cap * 4 * kSGrad);  // rs_backward: screen-space gradient sums per item
   L.titem = take((size_t)n_cap);
   L.keysA = take((size_t)n_cap * 4);
-  L.keysB = take((size_t)n_cap * 4);
+  L.keysB = take((size_t)n_cap * 4);  // the projection's per-item depth keys
+  L.keysC = take((size_t)n_cap * 4);  // dsort_kernel's second key buffer (keysB holds its input)
   L.valsA = take((size_t)n_cap * 4);
   L.valsB = take((size_t)n_cap * 4);
   L.rowtab = take(rowtab_stride(n_cap) * TH * 4);  // per tile row: Gaussians per rank chunk
@@ -239,6 +280,8 @@ void set_smem_all() {
 void configure_kernels() {  // per device; idempotent
   set_smem_all<uint32_t, kDepthItems>();
   cudaFuncSetAttribute(segplace_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * kMaxTileRows);
+  cudaFuncSetAttribute(dsort_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DsortSmem));
+  cudaFuncSetAttribute(dsort_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DsortSmem));
 }
 
 }  // namespace
@@ -261,7 +304,7 @@ const char* rs_status_string(int32_t s) {
 
 size_t rs_workspace_size(int64_t n_cap, int64_t pair_cap, int32_t width, int32_t height) {
   if (n_cap < 0 || pair_cap < 0 || width <= 0 || height <= 0) return 0;
-  return make_layout(n_cap, pair_cap, width, height).total;
+  return make_layout(n_cap, pair_cap, width, height, device_sms()).total;
 }
 
 int32_t rs_workspace_create(void* device_mem, size_t bytes, int64_t n_cap, int64_t pair_cap, int32_t width,
@@ -271,7 +314,7 @@ int32_t rs_workspace_create(void* device_mem, size_t bytes, int64_t n_cap, int64
     return RS_EINVAL;
   const int TW = tiles_x(width), TH = tiles_x(height);
   if ((int64_t)TW * TH > 65536 || width > 32767 || height > 32767) return RS_EINVAL;  // 15-bit box fields
-  const Layout L = make_layout(n_cap, pair_cap, width, height);
+  const Layout L = make_layout(n_cap, pair_cap, width, height, device_sms());
   if (bytes < L.total) return RS_ENOMEM_WORKSPACE;
   rs_workspace* ws = new (std::nothrow) rs_workspace();
   if (!ws) return RS_ECUDA;
@@ -403,17 +446,41 @@ int32_t rs_bin(rs_workspace* ws, void* stream) {
   cudaStream_t st = S(stream);
   const uint32_t n = ws->n_items;
   if (n > 0) {
-    // depth sort of the n_visible binned items (compacted in item order by the projection)
+    // depth sort of the n_visible binned items (the projection wrote every item's key;
+    // culled items carry kInvalidKey)
     const uint32_t* nvis = &ws->ctr()->n_visible;
-    launch(compact_hist_kernel, (n + kCompactKeys - 1) / kCompactKeys, 256, 0, st,
-           ws->at<uint32_t>(ws->L.keysB), n, ws->at<uint32_t>(ws->L.keysA), ws->at<uint32_t>(ws->L.valsA),
-           ws->at<unsigned long long>(ws->L.proj_lb), ws->ctr(), kSortThreads * kDepthItems,
-           ws->at<uint32_t>(ws->L.hist), ws->at<uint32_t>(ws->L.lbA));
     const uint32_t *keys_res, *items_sorted;
-    run_sort<uint32_t, kDepthItems>(ws, ws->at<uint32_t>(ws->L.keysA), ws->at<uint32_t>(ws->L.keysA),
-                                    ws->at<uint32_t>(ws->L.keysB), ws->at<uint32_t>(ws->L.valsA),
-                                    ws->at<uint32_t>(ws->L.valsA), ws->at<uint32_t>(ws->L.valsB), nvis, 0, n, 32,
-                                    0, 0, ws->f64, st, &keys_res, &items_sorted);
+    bool sorted = false;
+    // one cooperative kernel (compaction fused into pass 0, 4 passes, grid barriers) for frames
+    // of up to ~1M items, where the launch chain's per-kernel latency dominates (configs[1]:
+    // 52 vs 65 us); larger frames keep the onesweep launches (configs[2]: 112 vs 153 us)
+    if (dsort_mode() == 2 || (dsort_mode() == 1 && n <= kDsortMaxItems)) {
+      const int G = std::min(ws->sms, kMaxDsortCtas);
+      const cudaError_t e = ws->f64
+          ? launch_coop(dsort_kernel<true>, G, kDsortThreads, sizeof(DsortSmem), st, ws->at<uint32_t>(ws->L.keysB), n,
+                        ws->at<uint32_t>(ws->L.keysA), ws->at<uint32_t>(ws->L.valsA), ws->at<uint32_t>(ws->L.keysC),
+                        ws->at<uint32_t>(ws->L.valsB), ws->at<uint32_t>(ws->L.dtab), ws->ctr())
+          : launch_coop(dsort_kernel<false>, G, kDsortThreads, sizeof(DsortSmem), st, ws->at<uint32_t>(ws->L.keysB), n,
+                        ws->at<uint32_t>(ws->L.keysA), ws->at<uint32_t>(ws->L.valsA), ws->at<uint32_t>(ws->L.keysC),
+                        ws->at<uint32_t>(ws->L.valsB), ws->at<uint32_t>(ws->L.dtab), ws->ctr());
+      if (e == cudaSuccess) {
+        keys_res = ws->at<uint32_t>(ws->L.keysA);
+        items_sorted = ws->at<uint32_t>(ws->L.valsA);
+        sorted = true;
+      } else {
+        cudaGetLastError();  // not launchable here (e.g. an SM partition): the launch chain below
+      }
+    }
+    if (!sorted) {
+      launch(compact_hist_kernel, (n + kCompactKeys - 1) / kCompactKeys, 256, 0, st,
+             ws->at<uint32_t>(ws->L.keysB), n, ws->at<uint32_t>(ws->L.keysA), ws->at<uint32_t>(ws->L.valsA),
+             ws->at<unsigned long long>(ws->L.proj_lb), ws->ctr(), kSortThreads * kDepthItems,
+             ws->at<uint32_t>(ws->L.hist), ws->at<uint32_t>(ws->L.lbA));
+      run_sort<uint32_t, kDepthItems>(ws, ws->at<uint32_t>(ws->L.keysA), ws->at<uint32_t>(ws->L.keysA),
+                                      ws->at<uint32_t>(ws->L.keysB), ws->at<uint32_t>(ws->L.valsA),
+                                      ws->at<uint32_t>(ws->L.valsA), ws->at<uint32_t>(ws->L.valsB), nvis, 0, n, 32,
+                                      0, 0, ws->f64, st, &keys_res, &items_sorted);
+    }
     if (ws->f64)  // fp32-rounded depth keys: runs of equal keys re-ordered by the fp64 depth
       launch(tiefix_kernel, std::min((n + 255) / 256, (uint32_t)ws->sms * 8), 256, 0, st, keys_res,
              const_cast<uint32_t*>(items_sorted), nvis, ws->at<Rec64>(ws->L.recs64));

@@ -1,0 +1,262 @@
+// dsort.cuh -- the frame's depth sort as ONE cooperative kernel (replaces the
+// compaction kernel + four onesweep launches of sort.cuh on the frame path).
+//
+// np.lexsort((idx, depth)) of render.py:218-222 over the binned items: a stable
+// LSD radix sort of their 32-bit depth keys (8-bit digits, 4 passes), values =
+// item index. One CTA per SM stays resident for the whole sort; passes are
+// separated by grid barriers instead of kernel boundaries, and a CTA's digit
+// offsets come from the published per-CTA histograms (every CTA reads the
+// G x 256 table after a barrier) instead of a decoupled look-back chain:
+//
+//   pass 0 reads the projection's per-item keys directly (culled items carry
+//   kInvalidKey and drop out: the compaction is fused into the first pass),
+//   CTA b taking items [b ci, (b+1) ci); passes 1-3 read the previous pass's
+//   output, CTA b taking sorted positions [b cs, (b+1) cs), cs = ceil(n_vis/G).
+//   Per pass: barrier; column prefix of the pass's [G][256] histogram table
+//   over the rows < b and the digit totals; the keys ranked stably within
+//   4096-key sub-chunks (warp multisplit, per-warp digit runs) and scattered to
+//   their global positions, each key also counted for the next pass in the row
+//   of the CTA that will own its new position (global atomics) -- so one grid
+//   barrier per pass. n_visible = the pass-0 total. Passes alternate B, A, B, A: the
+//   sorted keys / items end in kA / vA. Data written by other CTAs is read
+//   through L2 (ld.cg): an SM's L1 may hold the buffer from two passes earlier.
+//
+// Same result as the onesweep path bit for bit (the parity tests compare the
+// sorted order with the oracle's).
+#pragma once
+#include "rs_common.cuh"
+
+namespace rs {
+
+constexpr int kDsortThreads = 1024;                           // one CTA of 32 warps per SM
+constexpr int kDsortWarps = kDsortThreads / 32;
+constexpr int kDsortItems = 4;                                // keys per thread per sub-chunk
+constexpr int kDsortChunk = kDsortThreads * kDsortItems;      // 4096
+
+// Grid barrier over the co-resident CTAs of a cooperative launch: arrive on a counter,
+// the last arrival bumps the generation the others spin on. `bar` = {count, gen}, zeroed
+// before the launch (the frame's counter memset).
+__device__ __forceinline__ void grid_barrier(uint32_t* bar, uint32_t nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile uint32_t* gen = bar + 1;
+    const uint32_t g = *gen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == nblocks - 1) {
+      bar[0] = 0;
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*gen == g) __nanosleep(20);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+struct DsortSmem {
+  uint32_t hist[256];                // running global offset of each digit for this CTA's keys
+  uint32_t whist[kDsortWarps][256];  // per-warp digit counts of a sub-chunk, then per-warp starts
+  uint32_t part[2][kDsortWarps][256];  // column-prefix partial sums: [pre | tot][row slice][digit]
+  uint32_t wsum[8];
+};
+
+// Column prefix of a pass's [G][256] histogram table: pre = sum over rows < b, tot = sum over
+// all rows, for digit tid < 256. Thread (slice w, digit group g) sums rows [w R, (w+1) R) of
+// digits [8 g, 8 g + 8) with two 16-byte loads per row -- every load of the table in flight
+// at once (R <= 5 rows per slice for G <= 160).
+__device__ __forceinline__ void column_prefix(const uint32_t* __restrict__ table, uint32_t G, uint32_t b,
+                                              DsortSmem& S, uint32_t& pre, uint32_t& tot) {
+  const int tid = threadIdx.x, g = tid & 31, w = tid >> 5;
+  const uint32_t R = (G + kDsortWarps - 1) / kDsortWarps;  // <= kColRows (G <= 160)
+  const uint32_t r0 = min(w * R, G), r1 = min(r0 + R, G);
+  uint32_t sp[8] = {0, 0, 0, 0, 0, 0, 0, 0}, st[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  constexpr int kColRows = 5;
+  uint4 xs[kColRows], ys[kColRows];
+#pragma unroll
+  for (int k = 0; k < kColRows; ++k) {  // every load issued before any is used
+    const uint32_t r = r0 + k;
+    const uint4* row = reinterpret_cast<const uint4*>(table + (size_t)min(r, G - 1) * 256 + 8 * g);
+    xs[k] = r < r1 ? __ldcg(row) : make_uint4(0, 0, 0, 0);
+    ys[k] = r < r1 ? __ldcg(row + 1) : make_uint4(0, 0, 0, 0);
+  }
+#pragma unroll
+  for (int k = 0; k < kColRows; ++k) {
+    const uint32_t v[8] = {xs[k].x, xs[k].y, xs[k].z, xs[k].w, ys[k].x, ys[k].y, ys[k].z, ys[k].w};
+    const bool before = r0 + k < b;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      st[q] += v[q];
+      sp[q] += before ? v[q] : 0u;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    S.part[0][w][8 * g + k] = sp[k];
+    S.part[1][w][8 * g + k] = st[k];
+  }
+  __syncthreads();
+  pre = 0;
+  tot = 0;
+  if (tid < 256) {
+#pragma unroll 8
+    for (int q = 0; q < kDsortWarps; ++q) {
+      pre += S.part[0][q][tid];
+      tot += S.part[1][q][tid];
+    }
+  }
+}
+
+// tables: 4 x [G][256] digit histograms (one per pass), zero on entry (the frame memset).
+// Pass p's table is complete at the barrier that starts pass p: pass 0's from the CTAs'
+// own item ranges, pass p+1's accumulated by pass p's scatter (each key is counted, with a
+// global atomic, for the CTA that owns its new position in pass p+1) -- one grid barrier
+// per pass.
+template <bool LAST_KEYS>
+__global__ void __launch_bounds__(kDsortThreads, 1) dsort_kernel(
+    const uint32_t* __restrict__ keys_all, uint32_t n_items, uint32_t* __restrict__ kA, uint32_t* __restrict__ vA,
+    uint32_t* __restrict__ kB, uint32_t* __restrict__ vB, uint32_t* __restrict__ tables,
+    Counters* __restrict__ ctr) {
+  uint32_t* bar = ctr->gbar;
+  extern __shared__ __align__(16) unsigned char dsort_smem[];
+  DsortSmem& S = *reinterpret_cast<DsortSmem*>(dsort_smem);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t G = gridDim.x, b = blockIdx.x;
+  const uint32_t lt = (1u << lane) - 1u;
+  const uint32_t ci = (n_items + G - 1) / G;
+  uint32_t nvis = 0, cs = 1;
+  const uint32_t* kin = keys_all;
+  const uint32_t* vin = nullptr;  // pass 0: value = item index
+  uint32_t* kout = kB;
+  uint32_t* vout = vB;
+  uint32_t kk[kDsortItems];
+  bool one;
+  {  // pass 0's histogram: this CTA's item range (valid keys)
+    const uint32_t lo = min(b * ci, n_items), hi = min(lo + ci, n_items);
+    one = hi - lo <= (uint32_t)kDsortChunk;
+    if (tid < 256) S.hist[tid] = 0;
+    __syncthreads();
+    for (uint32_t base = lo; base < hi; base += kDsortChunk) {
+      const uint32_t wbase = base + warp * 32 * kDsortItems;
+#pragma unroll
+      for (int it = 0; it < kDsortItems; ++it) {
+        const uint32_t i = wbase + it * 32 + lane;
+        kk[it] = i < hi ? __ldcg(kin + i) : kInvalidKey;
+      }
+#pragma unroll
+      for (int it = 0; it < kDsortItems; ++it)
+        if (kk[it] != kInvalidKey) atomicAdd(&S.hist[kk[it] & 0xffu], 1u);
+    }
+    __syncthreads();
+    if (tid < 256) tables[(size_t)b * 256 + tid] = S.hist[tid];
+  }
+  for (int p = 0; p < 4; ++p) {
+    const int shift = 8 * p;
+    grid_barrier(bar, G);
+    uint32_t pre, tot;
+    column_prefix(tables + (size_t)p * G * 256, G, b, S, pre, tot);
+    uint32_t x = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31 && warp < 8) S.wsum[warp] = x;
+    __syncthreads();
+    uint32_t dstart = x - tot, all = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      dstart += w < warp ? S.wsum[w] : 0u;
+      all += S.wsum[w];
+    }
+    if (p == 0) {
+      nvis = all;
+      cs = max((nvis + G - 1) / G, 1u);
+    }
+    if (tid < 256) S.hist[tid] = dstart + pre;  // where this CTA's first key of digit tid goes
+    uint32_t lo, hi;
+    if (p == 0) {
+      lo = min(b * ci, n_items);
+      hi = min(lo + ci, n_items);
+    } else {
+      lo = min(b * cs, nvis);
+      hi = min(lo + cs, nvis);
+      one = hi - lo <= (uint32_t)kDsortChunk;
+    }
+    uint32_t* next = p < 3 ? tables + (size_t)(p + 1) * G * 256 : nullptr;
+    __syncthreads();
+    // stable rank + scatter, sub-chunk by sub-chunk (warp-contiguous, item-major, lane-minor)
+    for (uint32_t base = lo; base < hi; base += kDsortChunk) {
+      const uint32_t wbase = base + warp * 32 * kDsortItems;
+      uint32_t rk[kDsortItems], vv[kDsortItems];
+      bool ok[kDsortItems];
+#pragma unroll
+      for (int it = 0; it < kDsortItems; ++it) {
+        const uint32_t i = wbase + it * 32 + lane;
+        if (!one || p > 0) kk[it] = i < hi ? __ldcg(kin + i) : kInvalidKey;
+        vv[it] = vin ? (i < hi ? __ldcg(vin + i) : 0u) : i;  // values loaded with the keys
+        ok[it] = i < hi && (p > 0 || kk[it] != kInvalidKey);
+      }
+      for (int i = tid; i < kDsortWarps * 256; i += kDsortThreads) (&S.whist[0][0])[i] = 0;
+      __syncthreads();
+#pragma unroll
+      for (int it = 0; it < kDsortItems; ++it) {
+        const uint32_t d = (kk[it] >> shift) & 0xffu;
+        uint32_t peers = __ballot_sync(0xffffffffu, ok[it]);
+#pragma unroll
+        for (int bt = 0; bt < 8; ++bt) {
+          const uint32_t bal = __ballot_sync(0xffffffffu, (d >> bt) & 1u);
+          peers &= ((d >> bt) & 1u) ? bal : ~bal;
+        }
+        uint32_t r0 = 0;
+        if (ok[it]) r0 = S.whist[warp][d];
+        __syncwarp();
+        if (ok[it] && (31 - __clz(peers)) == lane) S.whist[warp][d] = r0 + __popc(peers);
+        __syncwarp();
+        rk[it] = r0 + __popc(peers & lt);
+      }
+      __syncthreads();
+      {  // per digit: start of each warp's run = running offset + earlier warps; 4 threads per
+         // digit (8 warps each), their totals combined through part[0]
+        const int d = tid & 255, qq = tid >> 8;
+        uint32_t c[8], sum = 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+          c[w] = S.whist[8 * qq + w][d];
+          sum += c[w];
+        }
+        S.part[0][qq][d] = sum;
+        __syncthreads();
+        uint32_t run = S.hist[d];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) run += q < qq ? S.part[0][q][d] : 0u;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+          S.whist[8 * qq + w][d] = run;
+          run += c[w];
+        }
+        __syncthreads();
+        if (qq == 3) S.hist[d] = run;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int it = 0; it < kDsortItems; ++it) {
+        if (!ok[it]) continue;
+        const uint32_t d = (kk[it] >> shift) & 0xffu;
+        const uint32_t pos = S.whist[warp][d] + rk[it];
+        if (p < 3 || LAST_KEYS) kout[pos] = kk[it];
+        vout[pos] = vv[it];
+        // next pass: this key belongs to the CTA that owns position pos
+        if (next) atomicAdd(next + (size_t)(pos / cs) * 256 + ((kk[it] >> (shift + 8)) & 0xffu), 1u);
+      }
+      __syncthreads();
+    }
+    kin = kout;
+    vin = vout;
+    kout = (kout == kB) ? kA : kB;
+    vout = (vout == vB) ? vA : vB;
+  }
+  if (b == 0 && tid == 0) ctr->n_visible = nvis;
+}
+
+}  // namespace rs

@@ -118,7 +118,7 @@ struct Counters {
   uint32_t dense_work;   // (dense chunk, column group) tickets of expand_dense_kernel
   uint32_t emit_done;    // finished segscan CTAs (the last one scans the row totals)
   uint32_t bad_index;    // an active_idx entry outside [0, n) was skipped
-  uint32_t pad[2];
+  uint32_t gbar[2];      // grid barrier {arrivals, generation} of the cooperative kernels
 };
 static_assert(sizeof(Counters) == 128, "Counters is 128 B");
 
