@@ -1,24 +1,28 @@
 #!/usr/bin/env python
-"""Benchmark: RadSplat render FPS at 1256x828 (BASELINE configs[1]) and
-importance-score views/s (configs[2]) on B200.
+"""Benchmark: RadSplat render FPS at 1256x828 vs #Gaussians (BASELINE configs[1])
+and importance-score views/s (configs[2]) on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload render|score]
-                    [--impl b200|reference] [--no-cpu-baseline]
+    python bench.py [--gpus N] [--steps K] [--warmup W]
+                    [--workload render|score|house|batch|train] [--precision fp32|fp64]
+                    [--impl b200|reference] [--no-cpu-baseline] [--quick]
 
-One JSON line on rank 0 (contract in the task brief):
+One JSON line on rank 0 (contract in the task brief). With --gpus N > 1 and no
+torchrun environment, the script re-launches itself under
+torch.distributed.run (N ranks, one per GPU, NCCL, 127.0.0.1).
+
 * render (default): a step = one 500k-Gaussian 1256x828 frame per rank along
-  the 1000-frame orbit (rank r renders frame (s*N + r) mod 1000): weak scaling,
-  value = frames/s over all ranks; each frame is one CUDA-graph launch
-  (rs_render captured once, camera uploaded per frame), timed with CUDA events
-  on the launching stream. Per-stage device times (preprocess / sort / blend)
-  come from a separate pass with events around the three C-ABI stages. L2 is
-  flushed (256 MB memset) between timed steps, outside the events.
-* score: a step = one full scoring pass of configs[2] (3M Gaussians, 200
-  Fibonacci views, 1256x828): views sharded contiguously across ranks, one
-  NCCL MAX all-reduce; strong scaling, value = views/s.
-* --impl reference: the CPU oracle port (oracle/cpu_ref.cpp, the restated
-  reference algorithm; the reference itself is pure NumPy and cannot travel)
-  on all host cores, same metric and config, rank 0 only.
+  the 1000-frame orbit (rank r renders frame (s*N + r) mod 1000): replicas,
+  weak scaling, value = frames/s over all ranks. Each frame is one CUDA-graph
+  replay of rs_render (camera uploaded per frame), device time from CUDA events
+  on the launching stream, max over ranks; L2 flushed (256 MB memset) between
+  timed frames, outside the events. The same line carries, measured in the
+  same run: `fp64` (the reference-arithmetic path), `score` (configs[2]
+  views/s: views sharded over the ranks + one NCCL MAX all-reduce, strong
+  scaling) and `fps_vs_n` (BASELINE's FPS-vs-#Gaussians sweep at 1256x828).
+* score / house / batch / train: one workload per line (see their functions).
+* --impl reference: the reference's algorithm on the host CPU (the oracle's
+  restatement, oracle/cpu_ref.cpp: the reference itself is NumPy and cannot
+  travel to the GPU box), all host threads, same metric/config, rank 0 only.
 """
 
 from __future__ import annotations
@@ -48,23 +52,26 @@ METRICS = {"render": METRIC_RENDER, "score": METRIC_SCORE, "house": METRIC_HOUSE
 WORKLOADS = {"render": "configs[1] orbit render", "score": "configs[2] importance scoring",
              "house": "configs[3] house trajectory", "batch": "configs[4] batched views",
              "train": "configs[1] orbit, forward + backward"}
+SWEEP_N = (125_000, 250_000, 500_000, 1_000_000, 2_000_000, 3_000_000)
+TRAFFIC_FILE = "profiles/round2_ncu_traffic.json"
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=None,
-                    help="default: render 200 frames, score 5 passes, house 300 frames, batch 3 x 64 frames")
+                    help="default: render 200 frames, score 3 passes, house 300 frames, batch 3 x 64 frames")
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--workload", choices=("render", "score", "house", "batch", "train"), default="render")
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--n-gaussians", type=int, default=None, help="override N (debug only)")
     ap.add_argument("--precision", choices=("fp32", "fp64"), default="fp32",
-                    help="arithmetic of the timed frames (fp32 = BASELINE configs' dtype)")
+                    help="arithmetic of the headline frames (fp32 = BASELINE configs' dtype)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--quick", action="store_true", help="render: skip the fp64 / score / fps_vs_n blocks")
+    ap.add_argument("--n-gaussians", type=int, default=None, help="override N (debug only)")
     a = ap.parse_args()
     if a.steps is None:
-        a.steps = {"render": 200, "score": 5, "house": 300, "batch": 3, "train": 100}[a.workload]
+        a.steps = {"render": 200, "score": 3, "house": 300, "batch": 3, "train": 100}[a.workload]
     return a
 
 
@@ -72,8 +79,23 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
+def maybe_spawn(args) -> int | None:
+    """--gpus N > 1 without a torchrun environment: re-run this command under
+    torch.distributed.run with N ranks (one per GPU) and return its exit code."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 # ---------------------------------------------------------------------------
-# clocks
+# clocks, peaks, host
 # ---------------------------------------------------------------------------
 class ClockSampler:
     """nvidia-smi -lms 200 during the timed region (clocks + throttle reasons)."""
@@ -85,6 +107,7 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.p = None
+        self.lines = []
 
     def __enter__(self):
         try:
@@ -96,7 +119,6 @@ class ClockSampler:
         return self
 
     def __exit__(self, *a):
-        self.lines = []
         if self.p:
             time.sleep(0.25)
             self.p.terminate()
@@ -110,7 +132,7 @@ class ClockSampler:
     def summary(self) -> dict:
         sm, mx, reasons, util_sm = [], None, set(), []
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for ln in getattr(self, "lines", []):
+        for ln in self.lines:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 9:
                 continue
@@ -132,26 +154,11 @@ class ClockSampler:
 
 def peaks():
     try:
-        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+        d = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+        d["_source"] = "MEASURED_PEAKS.json (driver-measured copy bandwidth)"
+        return d
     except Exception:
-        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "_fallback": True}
-
-
-# ---------------------------------------------------------------------------
-# CPU baseline (oracle port, all host cores)
-# ---------------------------------------------------------------------------
-def cpu_views(scene, cams, images: bool, threads: int | None = None, precision: str = "fp32"):
-    from oracle import oracle as O
-    O.build()
-    t0 = time.perf_counter()
-    r = O.views(scene, cams, dict_opts(precision), np.float32 if precision == "fp32" else np.float64,
-                threads=threads, scores=not images, images=images)
-    return time.perf_counter() - t0, r
-
-
-def dict_opts(precision: str = "fp32"):
-    from paper_2403_13806_b200.render import RasterizeOptions
-    return RasterizeOptions(near_limit=0.2, precision=precision)
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "_source": "fallback (B200_PROFILING.md)"}
 
 
 def cpu_model() -> str:
@@ -164,9 +171,65 @@ def cpu_model() -> str:
     return "unknown"
 
 
-# ---------------------------------------------------------------------------
-# workloads
-# ---------------------------------------------------------------------------
+def dict_opts(precision: str = "fp32"):
+    from paper_2403_13806_b200.render import RasterizeOptions
+    return RasterizeOptions(near_limit=0.2, precision=precision)
+
+
+def cpu_views(scene, cams, images: bool, threads: int, precision: str = "fp32"):
+    """The oracle (the reference's algorithm restated, tile-parallel) on host threads."""
+    from oracle import oracle as O
+    O.build()
+    t0 = time.perf_counter()
+    r = O.views(scene, cams, dict_opts(precision), np.float32 if precision == "fp32" else np.float64,
+                threads=threads, scores=not images, images=images)
+    return time.perf_counter() - t0, r
+
+
+def crop_camera(cam, frac: int):
+    """The central 1/frac x 1/frac window of a camera's image (same intrinsics, shifted
+    principal point): a bounded CPU sample of a frame."""
+    from paper_2403_13806_b200.core import PinholeCamera
+    w, h = cam.width // frac, cam.height // frac
+    return PinholeCamera(rotation=cam.rotation, translation=cam.translation, fx=cam.fx, fy=cam.fy,
+                         cx=cam.cx - (cam.width - w) / 2.0, cy=cam.cy - (cam.height - h) / 2.0, width=w, height=h)
+
+
+def bytes_alg_render(n_in, n_vis, P, HW):
+    """SURVEY §8d per-frame algorithmic bytes (attributes once, records and pairs written +
+    read once, pair values read by the blend, RGB + alpha + depth fp32 written)."""
+    return 236 * n_in + 2 * 48 * n_vis + 2 * 12 * P + 4 * P + 20 * HW
+
+
+def bytes_alg_score(n_in, n_vis, P):
+    """SURVEY §8d per-view algorithmic bytes of a scoring view (no SH, no image)."""
+    return 44 * n_in + 2 * 36 * n_vis + 2 * 12 * P + 4 * P + 4 * n_vis
+
+
+def frame_launches(n_items: int, f64: bool) -> int:
+    """Kernels per frame: project, depth sort (1 cooperative kernel up to 2^20 items, else
+    compaction + 4 onesweep passes), fp64 tie fix, segment rows / scan / placement, chunk
+    counts, tile chunks, tile scan, expansion (sparse + dense), blend."""
+    sort = 1 if n_items <= (1 << 20) else 5
+    return 1 + sort + (1 if f64 else 0) + 3 + 1 + 1 + 1 + 2 + 1
+
+
+def profiled_traffic(kernel: str):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full capture (or None)."""
+    try:
+        return json.loads((ROOT / TRAFFIC_FILE).read_text()).get(kernel)
+    except (OSError, ValueError):
+        return None
+
+
+def make_config(workload: str, scene_n: int, W: int, H: int, world: int) -> dict:
+    """The `config` dict of a line -- identical for the GPU arm and the reference arm."""
+    par = ("views sharded over {w} GPU(s) + NCCL all_reduce(MAX)" if workload == "score"
+           else "frames split across {w} GPU(s), no communication").format(w=world)
+    return {"workload": WORKLOADS[workload], "n_gaussians": scene_n, "width": W, "height": H, "tile": 16,
+            "l2": "flushed (256 MB memset) between timed steps", "parallelism": par}
+
+
 def make_workload(kind: str, n_override=None):
     from paper_2403_13806_b200 import synth
     if kind == "house":
@@ -175,312 +238,446 @@ def make_workload(kind: str, n_override=None):
     if kind == "batch":
         return synth.config4(0, n=n_override or 1_000_000)
     if kind in ("render", "train"):
-        scene, cams = synth.config1(0, n=n_override or 500_000)
-        return scene, cams
-    scene, cams = synth.config2(0, n=n_override or 3_000_000)
-    return scene, cams
+        return synth.config1(0, n=n_override or 500_000)
+    return synth.config2(0, n=n_override or 3_000_000)
 
 
+# ---------------------------------------------------------------------------
+# the reference arm
+# ---------------------------------------------------------------------------
 def run_reference(args):
+    """The reference's algorithm on the host's cores (the oracle port: the reference itself is
+    NumPy and cannot travel to the GPU box). A step = one bounded sample of the workload."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
     scene, cams = make_workload(args.workload, args.n_gaussians)
     threads = os.cpu_count() or 1
     images = args.workload != "score"
-    # a step = one frame (or view) rendered by all host threads (bounded sample);
-    # a wall-clock guard keeps the whole arm within a few minutes on small hosts
+    crop = 4 if args.workload == "batch" else 1  # configs[4] frames: the central 1/16 (see sample)
+    sample = [crop_camera(c, crop) if crop > 1 else c for c in cams]
     for s in range(args.warmup):
-        cpu_views(scene, cams[s:s + 1], images, threads=threads)
+        cpu_views(scene, sample[s:s + 1], images, threads)
     total_t, done, budget = 0.0, 0, float(os.environ.get("RADSPLAT_REF_BUDGET_S", 240))
     for s in range(args.steps):
-        dt, _ = cpu_views(scene, [cams[s % len(cams)]], images, threads=threads)
+        dt, _ = cpu_views(scene, [sample[s % len(sample)]], images, threads)
         total_t += dt
         done += 1
         if total_t > budget:
             break
-    value = done / total_t
+    value = done / total_t / (crop * crop)
     unit = "frames/s" if images else "views/s"
+    W, H = cams[0].width, cams[0].height
     line = {
         "metric": METRICS[args.workload], "impl": "reference", "value": value, "unit": unit,
         "n_gpus": world, "steps": args.steps, "steps_completed": done, "warmup": args.warmup,
         "ms_per_step": 1e3 * total_t / done,
-        "higher_is_better": True, "scaling": "weak" if images else "strong", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong" if args.workload == "score" else "weak", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic (seeded, BASELINE configs distributions)",
-        "config": {"workload": WORKLOADS[args.workload], "n_gaussians": len(scene), "width": cams[0].width,
-                   "height": cams[0].height},
+        "config": make_config(args.workload, len(scene), W, H, world),
         "cpu_baseline": {"value": value, "unit": unit, "cores": threads, "kind": "port",
-                         "sample": f"1 {'frame' if images else 'view'} per step on {threads} threads "
-                                   f"(oracle/cpu_ref.cpp fp32 restatement, tile-parallel); CPU {cpu_model()}"},
+                         "sample": (f"1 {'frame' if images else 'view'} per step" +
+                                    (f" (its central 1/{crop * crop}, rate scaled to whole frames)" if crop > 1
+                                     else "") +
+                                    f" on {threads} threads (oracle/cpu_ref.cpp fp32 restatement, tile-parallel); "
+                                    f"CPU {cpu_model()}")},
         "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def bytes_alg_render(n_in, n_vis, P, HW):
-    """SURVEY §8d per-frame algorithmic bytes."""
-    return 236 * n_in + 2 * 48 * n_vis + 2 * 12 * P + 4 * P + 20 * HW
+# ---------------------------------------------------------------------------
+# GPU context
+# ---------------------------------------------------------------------------
+class Ctx:
+    def __init__(self, args):
+        import torch
+        import torch.distributed as dist
+        from paper_2403_13806_b200.device import renderer
+        self.torch, self.dist = torch, dist
+        self.rank, self.world, self.local = dist_env()
+        if self.world != args.gpus and not (args.gpus == 1 and self.world == 1):
+            raise SystemExit(f"world size {self.world} != --gpus {args.gpus}")
+        torch.cuda.set_device(self.local)
+        self.dev = torch.device("cuda", self.local)
+        if self.world > 1:
+            dist.init_process_group("nccl", device_id=self.dev)
+        self.r = renderer(self.dev)
+        self.lib = self.r.lib
+        self.stream = torch.cuda.current_stream(self.dev)
+        self.sptr = self.stream.cuda_stream
+        self.flush = torch.empty(256 << 20, dtype=torch.uint8, device=self.dev)
+        self.pk = peaks()
+        self.sms = torch.cuda.get_device_properties(self.dev).multi_processor_count
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+        self.torch.cuda.synchronize(self.dev)
+
+    def max_over_ranks(self, v: float) -> float:
+        t = self.torch.tensor([float(v)], dtype=self.torch.float64, device=self.dev)
+        if self.world > 1:
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(self, v: float) -> float:
+        t = self.torch.tensor([float(v)], dtype=self.torch.float64, device=self.dev)
+        if self.world > 1:
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
+        return float(t.item())
+
+    def fp32_peak(self) -> float:
+        return self.sms * 128 * 2 * self.pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+
+    def hbm(self) -> float:
+        return float(self.pk.get("hbm_gbs", 6650.0))
+
+    def events(self, n):
+        E = self.torch.cuda.Event
+        return [(E(enable_timing=True), E(enable_timing=True)) for _ in range(n)]
+
+    def close(self):
+        if self.world > 1:
+            self.dist.destroy_process_group()
 
 
-def main():
-    args = parse()
-    if args.impl == "reference":
-        return run_reference(args)
-    import torch
-    import torch.distributed as dist
+def check_sticky(ctx):
+    """Overflow / bad-index record over every frame since the last reset (the whole timed
+    region): an overflowed frame would have been timed as an incomplete one."""
+    over, _ = ctx.r.read_overflow(reset=True)
+    if over:
+        raise RuntimeError("a timed frame overflowed its pair capacity")
 
+
+def staged_times(ctx, ds, cams, opts, out_ptrs, scores=None, flags=0):
+    """Per-stage device times (project / sort / blend, ms per frame) of `cams`, the three
+    C-ABI stages launched one by one with events between them."""
     from paper_2403_13806_b200 import _native as N
-    from paper_2403_13806_b200.device import camera_struct, device_scene, options_struct, renderer
-    from paper_2403_13806_b200.dist import all_reduce_max, shard_range
-
-    rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-    opts = dict_opts(args.precision)
-    PREC = 1 if args.precision == "fp64" else 0
-    r = renderer(dev)
-    lib = r.lib
+    from paper_2403_13806_b200.device import camera_struct, options_struct
+    torch = ctx.torch
     opt_s = options_struct(opts)
-    stream = torch.cuda.current_stream(dev)
-    sptr = stream.cuda_stream
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    pk = peaks()
-    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    sc = scores.data_ptr() if scores is not None else None
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in cams]
+    structs = [camera_struct(c) for c in cams]
+    for cs, e in zip(structs, ev):
+        ctx.flush.zero_()
+        e[0].record(ctx.stream)
+        N.check(ctx.lib.rs_project(ctx.r.handle, C.byref(ds.struct), None, 0, C.byref(cs), C.byref(opt_s),
+                                   ctx.sptr))
+        e[1].record(ctx.stream)
+        N.check(ctx.lib.rs_bin(ctx.r.handle, ctx.sptr))
+        e[2].record(ctx.stream)
+        N.check(ctx.lib.rs_blend(ctx.r.handle, C.byref(opt_s), *out_ptrs, sc, flags, ctx.sptr))
+        e[3].record(ctx.stream)
+    torch.cuda.synchronize(ctx.dev)
+    st = np.array([[e[i].elapsed_time(e[i + 1]) for i in range(3)] for e in ev])
+    check_sticky(ctx)
+    return st.mean(axis=0)
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize(dev)
 
-    if args.workload in ("house", "batch"):
-        return run_trajectory(args, rank, world, local, dev, opts, r, opt_s, stream, flush, pk, barrier)
-    if args.workload == "train":
-        return run_train(args, rank, world, local, dev, opts, r, opt_s, stream, flush, pk, barrier)
-    scene, cams = make_workload(args.workload, args.n_gaussians)
-    ds = device_scene(scene, dev)
-    W_, H_ = cams[0].width, cams[0].height
-    result = {}
-    if args.workload == "render":
-        frames = lambda s: cams[(s * world + rank) % len(cams)]  # noqa: E731
-        out = r.alloc_outputs(cams[0], precision=PREC)
-        # untimed pre-pass over every frame the timed loop will render: sizes the
-        # pair capacity (overflow-checked) and counts E / C for the roofline
-        E = C_ = P_ = NV = 0
-        for s in range(args.steps):
-            _, st = r.render(ds, frames(s), opts, out=out, count_evals=True)
+def measure_render(ctx, scene, frames, opts, steps, warmup, clocks=True):
+    """Timed configs[1]-style frames: checked pre-pass (capacity, E/C/P), per-stage pass, then
+    K CUDA-graph replays timed with events (L2 flushed between them, outside the events)."""
+    from paper_2403_13806_b200.device import device_scene, precision_of
+    torch = ctx.torch
+    prec = precision_of(opts)
+    ds = device_scene(scene, ctx.dev)
+    cam0 = frames(0)
+    hw = cam0.width * cam0.height
+    out = ctx.r.alloc_outputs(cam0, precision=prec)
+    E = C_ = P_ = NV = 0
+    for s in range(steps):
+        _, st = ctx.r.render(ds, frames(s), opts, out=out, count_evals=True)
+        E += st.evals
+        C_ += st.composites
+        P_ += st.n_pairs
+        NV += st.n_visible
+    ptrs = [out[k].data_ptr() for k in ("rgb", "alpha", "depth", "count")]
+    for s in range(warmup):
+        ctx.r.render(ds, frames(s), opts, out=out)
+    stages = staged_times(ctx, ds, [frames(s) for s in range(min(steps, 50))], opts, ptrs)
+    fg = ctx.r.capture(ds, cam0, opts)
+    for s in range(warmup):
+        fg.replay(frames(s))
+    ctx.barrier()
+    ctx.r.read_overflow(reset=True)
+    ev = ctx.events(steps)
+    clk = ClockSampler(ctx.local) if clocks else None
+    if clk:
+        clk.__enter__()
+    ctx.barrier()
+    t0 = time.perf_counter()
+    for s in range(steps):
+        ctx.flush.zero_()
+        ev[s][0].record(ctx.stream)
+        fg.replay(frames(s))
+        ev[s][1].record(ctx.stream)
+    ctx.barrier()
+    wall = time.perf_counter() - t0
+    if clk:
+        clk.__exit__(None, None, None)
+    check_sticky(ctx)
+    t_max = ctx.max_over_ranks(sum(a.elapsed_time(b) for a, b in ev))  # ms, K frames
+    n = steps
+    fp32_peak = ctx.fp32_peak()
+    flops = 16 * E + 11 * C_
+    res = {
+        "fps": ctx.world * n / (t_max / 1e3), "ms_per_frame": t_max / n, "wall_fps": ctx.world * n / wall,
+        "stages_ms": {"preprocess": float(stages[0]), "sort": float(stages[1]), "blend": float(stages[2])},
+        "visible_mean": NV / n, "pairs_mean": P_ / n, "evals_per_px": E / n / hw, "composites_per_px": C_ / n / hw,
+        "flops_alg_per_frame": flops / n, "bytes_alg_per_frame": bytes_alg_render(len(scene), NV / n, P_ / n, hw),
+        "n_gaussians": len(scene), "frames": n, "clocks": clk.summary() if clk else None,
+    }
+    res["blend_tflops"] = flops / n / (stages[2] / 1e3) / 1e12
+    res["blend_frac_fp32"] = res["blend_tflops"] / fp32_peak
+    res["hbm_frac"] = res["bytes_alg_per_frame"] / (res["ms_per_frame"] / 1e3) / 1e9 / ctx.hbm()
+    return res
+
+
+def e2e_render(ctx, scene, cams, opts, frames: int):
+    """The drop-in call: render.rasterize() -> RenderOutput with host float64/int64 arrays
+    (camera in, image out, every frame)."""
+    from paper_2403_13806_b200 import _native as N
+    from paper_2403_13806_b200.render import rasterize
+    for c in cams[:2]:
+        rasterize(scene, c, opts)
+    ctx.barrier()
+    t0 = time.perf_counter()
+    for c in cams[:frames]:
+        rasterize(scene, c, opts)
+    ctx.barrier()
+    te = ctx.max_over_ranks(time.perf_counter() - t0)
+    hw = cams[0].width * cams[0].height
+    return {"value": ctx.world * frames / te, "unit": "frames/s",
+            "h2d_bytes_per_step": C.sizeof(N.RsCamera) + C.sizeof(N.RsOptions),
+            "d2h_bytes_per_step": hw * (24 + 8 + 8),
+            "api": "paper_2403_13806_b200.render.rasterize (scene resident in HBM after the first call)"}
+
+
+def measure_score(ctx, scene, cams, opts, steps, warmup, staged_views=6):
+    """One scoring pass = every camera's score-only frame max-merged into one vector (views
+    split contiguously over the ranks), then one all_reduce(MAX) (NCCL). Device time of the
+    whole pass with events, max over ranks."""
+    from paper_2403_13806_b200 import _native as N
+    from paper_2403_13806_b200.device import (camera_struct, device_scene, options_struct, precision_of,
+                                              value_dtype)
+    from paper_2403_13806_b200.dist import all_reduce_max, shard_range
+    torch = ctx.torch
+    prec = precision_of(opts)
+    ds = device_scene(scene, ctx.dev)
+    n = len(cams)
+    lo, hi = shard_range(n, ctx.rank, ctx.world)
+    mine = cams[lo:hi]
+    scores = torch.zeros(len(scene), dtype=value_dtype(prec), device=ctx.dev)
+    E = C_ = P_ = NV = 0  # pre-pass over this rank's views: pair capacity and the roofline counts
+    sel = mine[::max(1, len(mine) // staged_views)][:staged_views]
+    sel_ids = {id(c) for c in sel}
+    for c in mine:
+        _, st = ctx.r.render(ds, c, opts, color=False, scores=scores, count_evals=id(c) in sel_ids)
+        P_ += st.n_pairs
+        NV += st.n_visible
+        if id(c) in sel_ids:
             E += st.evals
             C_ += st.composites
-            P_ += st.n_pairs
-            NV += st.n_visible
-        cam_structs = [camera_struct(frames(s)) for s in range(args.steps)]
-        ptr = {k: v.data_ptr() for k, v in out.items()}
+    opt_s = options_struct(opts)
+    structs = [camera_struct(c) for c in mine]
+    sc_ptr = scores.data_ptr()
 
-        def step(cs, evs):
-            evs[0].record(stream)
-            N.check(lib.rs_project(r.handle, C.byref(ds.struct), None, 0, C.byref(cs), C.byref(opt_s), sptr))
-            evs[1].record(stream)
-            N.check(lib.rs_bin(r.handle, sptr))
-            evs[2].record(stream)
-            N.check(lib.rs_blend(r.handle, C.byref(opt_s), ptr["rgb"], ptr["alpha"], ptr["depth"], ptr["count"],
-                                 None, 0, sptr))
-            evs[3].record(stream)
+    def one_pass():
+        scores.zero_()
+        for cs in structs:
+            N.check(ctx.lib.rs_render(ctx.r.handle, C.byref(ds.struct), None, 0, C.byref(cs), C.byref(opt_s),
+                                      None, None, None, None, sc_ptr, 0, ctx.sptr))
+        all_reduce_max(scores)
 
-        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
-        for s in range(args.warmup):
-            step(camera_struct(frames(s)), ev[0])
-        barrier()
-        # (1) per-stage device times: the three C-ABI stages launched one by one
-        for s in range(args.steps):
-            flush.zero_()
-            step(cam_structs[s], ev[s])
-        torch.cuda.synchronize(dev)
-        stage = np.array([[ev[s][i].elapsed_time(ev[s][i + 1]) for i in range(3)] for s in range(args.steps)])
-        # (2) the timed frames: each one CUDA-graph launch (camera upload + memset + 12 kernels)
-        fg = r.capture(ds, frames(0), opts)
-        gev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-        for s in range(args.warmup):
-            fg.replay(frames(s))
-        barrier()
-        with ClockSampler(local) as clk:
-            barrier()
-            t0 = time.perf_counter()
-            for s in range(args.steps):
-                flush.zero_()
-                gev[s][0].record(stream)
-                fg.replay(frames(s))
-                gev[s][1].record(stream)
-            barrier()
-            wall = time.perf_counter() - t0
-        st = r.stats()
-        assert not st.overflow
-        t_frames = float(sum(a.elapsed_time(b) for a, b in gev))  # ms, device time of the K frames
-        t_staged = float(stage.sum())
-        t_local = torch.tensor([t_frames], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
-        t_max = float(t_local.item())
-        value = world * args.steps / (t_max / 1e3)
-        blend_ms = float(stage[:, 2].sum())
-        fp32_peak = sms * 128 * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
-        flops = 16 * E + 11 * C_
-        achieved = flops / (blend_ms / 1e3) / 1e12
-        hw = W_ * H_
-        frame_bytes = bytes_alg_render(len(scene), NV / args.steps, P_ / args.steps, hw)
-        result.update({
-            "metric": METRICS["render"], "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64" if PREC else "f32",
-            "data": "synthetic (seeded configs[1]: 500k Gaussians in 32 clusters, SH deg 3; no dataset offline)",
-            "config": {"workload": "configs[1] orbit render", "n_gaussians": len(scene), "width": W_, "height": H_,
-                       "tile": 16, "frames": args.steps, "l2": "flushed (256 MB memset) between timed steps",
-                       "parallelism": f"frames split across {world} GPU(s), no communication"},
-            "stages_ms": {"preprocess": float(stage[:, 0].mean()), "sort": float(stage[:, 1].mean()),
-                          "blend": float(stage[:, 2].mean()),
-                          "note": "separate pass, three C-ABI stage launches per frame"},
-            "fps_without_graph": world * args.steps / (t_staged / 1e3) if world == 1 else None,
-            "wall_fps": world * args.steps / wall,
-            "workload_stats": {"visible_mean": NV / args.steps, "pairs_mean": P_ / args.steps,
-                               "evals_per_px": E / args.steps / hw, "composites_per_px": C_ / args.steps / hw},
-            "roofline": {"kernel": "blend2_kernel<COLOR>", "bound": "fp32", "achieved": achieved,
-                         "peak": fp32_peak, "unit": "TFLOP/s", "frac": achieved / fp32_peak,
-                         "traffic": profiled_traffic("blend2_kernel<1, 0, 0, 1, 0>"),
-                         "traffic_source": TRAFFIC_FILE + " (ncu --set full, dram read+write bytes per launch)",
-                         "algorithmic": "16*E + 11*C flops per frame (SURVEY §8d)",
-                         "peak_source": "computed: SMs x 128 FP32 lanes x 2 x sm_max_mhz"},
-            "frame_roofline": {"bytes_alg_per_frame": frame_bytes,
-                               "achieved_gbs": frame_bytes / (t_max / args.steps / 1e3) / 1e9,
-                               "peak_gbs": pk.get("hbm_gbs"),
-                               "frac": frame_bytes / (t_max / args.steps / 1e3) / 1e9 / pk.get("hbm_gbs", 6548.8)},
-            "gpu_launches": args.steps * frame_launches(W_, H_),
-            "clocks": clk.summary(),
-        })
-        # e2e: the reference-facing call (rasterize -> RenderOutput with host numpy
-        # fp64 arrays), camera in, image + alpha + count + depth out, every step
-        from paper_2403_13806_b200.render import rasterize
-        ke = min(args.steps, 30)
-        for s in range(2):
-            rasterize(scene, frames(s), opts)
-        barrier()
+    for _ in range(warmup):
+        one_pass()
+    ctx.barrier()
+    ctx.r.read_overflow(reset=True)
+    ev = ctx.events(steps)
+    with ClockSampler(ctx.local) as clk:
+        ctx.barrier()
         t0 = time.perf_counter()
-        for s in range(ke):
-            rasterize(scene, frames(s), opts)
-        barrier()
-        te = time.perf_counter() - t0
-        te_t = torch.tensor([te], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(te_t, op=dist.ReduceOp.MAX)
-        result["e2e"] = {"value": world * ke / float(te_t.item()), "unit": "frames/s",
-                         "h2d_bytes_per_step": C.sizeof(N.RsCamera) + C.sizeof(N.RsOptions),
-                         "d2h_bytes_per_step": hw * (24 + 8 + 8),
-                         "api": "paper_2403_13806_b200.render.rasterize (scene resident in HBM after first call)"}
-        if rank == 0 and world == 1 and not args.no_cpu_baseline:
-            threads = os.cpu_count() or 1
-            sel = [frames(s) for s in range(4)]
-            dt, _ = cpu_views(scene, sel, True, threads=threads)
-            result["cpu_baseline"] = {"value": len(sel) / dt, "unit": "frames/s", "cores": threads, "kind": "port",
-                                      "sample": f"{len(sel)} orbit frames, each on {threads} threads "
-                                                f"(oracle/cpu_ref.cpp fp32, tile-parallel), CPU {cpu_model()}"}
-    else:
-        n = len(cams)
-        lo, hi = shard_range(n, rank, world)
-        mine = [camera_struct(c) for c in cams[lo:hi]]
-        scores = torch.zeros(len(scene), dtype=torch.float64 if PREC else torch.float32, device=dev)
-        # pre-pass: overflow-checked capacity sizing over this rank's views
-        P_ = 0
-        for c in cams[lo:hi]:
-            _, st = r.render(ds, c, opts, color=False, scores=scores)
-            P_ += st.n_pairs
-        sc_ptr = scores.data_ptr()
-
-        def one_pass():
-            scores.zero_()
-            for cs in mine:
-                N.check(lib.rs_render(r.handle, C.byref(ds.struct), None, 0, C.byref(cs), C.byref(opt_s), None, None,
-                                      None, None, sc_ptr, 0, sptr))
-            all_reduce_max(scores)
-
-        for _ in range(args.warmup):
+        for s in range(steps):
+            ctx.flush.zero_()
+            ev[s][0].record(ctx.stream)
             one_pass()
-        barrier()
-        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-        with ClockSampler(local) as clk:
-            barrier()
-            t0 = time.perf_counter()
-            for s in range(args.steps):
-                flush.zero_()
-                evs[s][0].record(stream)
-                one_pass()
-                evs[s][1].record(stream)
-            barrier()
-            wall = time.perf_counter() - t0
-        assert not r.stats().overflow
-        t_local = torch.tensor([sum(a.elapsed_time(b) for a, b in evs)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
-        t_max = float(t_local.item())
-        value = args.steps * n / (t_max / 1e3)
-        kept = int((scores >= 0.01).sum().item())
-        # e2e: the reference-facing compute_importance (cameras in, fp64 host table out)
-        from paper_2403_13806_b200.pruning import compute_importance
-        compute_importance(scene, cams, opts)
-        barrier()
-        t0 = time.perf_counter()
-        tab = compute_importance(scene, cams, opts)
-        barrier()
-        te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        assert int((tab.values >= 0.01).sum()) == kept
-        if rank == 0 and world == 1 and not args.no_cpu_baseline:
-            threads = os.cpu_count() or 1
-            sel = cams[:2]
-            dt, _ = cpu_views(scene, sel, False, threads=threads)
-            result_cpu = {"value": len(sel) / dt, "unit": "views/s", "cores": threads, "kind": "port",
-                          "sample": f"{len(sel)} of the 200 views, each on {threads} threads "
-                                    f"(oracle/cpu_ref.cpp fp32 scoring, tile-parallel), CPU {cpu_model()}"}
-        else:
-            result_cpu = None
-        e2e = {"value": n / float(te.item()), "unit": "views/s",
-               "h2d_bytes_per_step": (hi - lo) * (C.sizeof(N.RsCamera) + C.sizeof(N.RsOptions)),
-               "d2h_bytes_per_step": 4 * len(scene),
-               "api": "paper_2403_13806_b200.pruning.compute_importance (one full pass of all views)"}
-        result.update({
-            "metric": METRIC_SCORE, "value": value, "unit": "views/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64" if PREC else "f32",
-            "data": "synthetic (seeded configs[2]: 3M Gaussians, log-scale N(-4,0.6); no dataset offline)",
-            "config": {"workload": "configs[2] importance scoring", "n_gaussians": len(scene), "views": n,
-                       "width": W_, "height": H_, "l2": "flushed (256 MB memset) between timed passes",
-                       "parallelism": f"views sharded over {world} GPU(s) + NCCL all_reduce(MAX)"},
-            "kept_at_0.01": kept, "wall_views_per_s": args.steps * n / wall,
-            "e2e": e2e,
-            **({"cpu_baseline": result_cpu} if result_cpu else {}),
-            "gpu_launches": args.steps * len(mine) * frame_launches(W_, H_),
-            "clocks": clk.summary(),
-        })
-    if rank == 0:
-        print(json.dumps(result), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+            ev[s][1].record(ctx.stream)
+        ctx.barrier()
+        wall = time.perf_counter() - t0
+    check_sticky(ctx)
+    t_max = ctx.max_over_ranks(sum(a.elapsed_time(b) for a, b in ev))
+    kept = int((scores[:len(scene)] >= 0.01).sum().item())
+    stages = staged_times(ctx, ds, sel, opts, [None, None, None, None], scores=scores)
+    flops = (16 * E + 5 * C_) / max(len(sel), 1)
+    peak = ctx.fp32_peak()
+    nv = max(len(mine), 1)
+    hw = cams[0].width * cams[0].height
+    view_ms = t_max / steps / max(hi - lo, 1)
+    res = {
+        "views_per_s": steps * n / (t_max / 1e3), "ms_per_pass": t_max / steps, "wall_views_per_s": steps * n / wall,
+        "kept_at_0.01": kept, "clocks": clk.summary(), "views": n, "views_this_rank": hi - lo,
+        "stages_ms_per_view": {"preprocess": float(stages[0]), "sort": float(stages[1]), "blend": float(stages[2])},
+        "visible_mean": NV / nv, "pairs_mean": P_ / nv, "evals_per_px": E / max(len(sel), 1) / hw,
+        "composites_per_px": C_ / max(len(sel), 1) / hw,
+    }
+    blend_t = flops / (stages[2] / 1e3) / 1e12
+    byt = bytes_alg_score(len(scene), NV / nv, P_ / nv)
+    res["roofline"] = {
+        "kernel": "blend64_kernel<0,1,0,1> (score)" if prec == N.RS_F64 else "blend2_kernel<0,1,0,1,0> (score)",
+        "bound": "fp64" if prec == N.RS_F64 else "fp32", "achieved": blend_t, "peak": peak, "unit": "TFLOP/s",
+        "frac": blend_t / peak, "traffic": profiled_traffic("blend2_kernel<0, 1, 0, 1, 0>"),
+        "algorithmic": "16*E + 5*C flops per view (SURVEY §8d), E/C counted on the staged views",
+        "peak_source": "computed: SMs x 128 FP32 lanes x 2 x sm_max_mhz"}
+    res["view_roofline"] = {"bytes_alg_per_view": byt, "achieved_gbs": byt / (view_ms / 1e3) / 1e9,
+                            "peak_gbs": ctx.hbm(), "frac": byt / (view_ms / 1e3) / 1e9 / ctx.hbm()}
+    return res
 
 
-def run_trajectory(args, rank, world, local, dev, opts, r, opt_s, stream, flush, pk, barrier):
-    """configs[3] (house: 300-frame trajectory, FPS with vs without visibility
-    filtering) and configs[4] (batched multi-view render: 64 frames per GPU per
-    step). Frames are split across ranks with no communication (replicas); each
-    frame is one rs_render_ex launch sequence timed with CUDA events on the
-    launching stream, L2 flushed between frames (outside the events)."""
-    import torch
-    import torch.distributed as dist
+def e2e_score(ctx, scene, cams, opts):
+    """The drop-in compute_importance (cameras in, float64 host table out), one full pass,
+    sharded over the ranks (shard=True: the collective path) when N > 1."""
+    from paper_2403_13806_b200 import _native as N
+    from paper_2403_13806_b200.dist import shard_range
+    from paper_2403_13806_b200.pruning import compute_importance
+    compute_importance(scene, cams, opts, shard=ctx.world > 1)
+    ctx.barrier()
+    t0 = time.perf_counter()
+    tab = compute_importance(scene, cams, opts, shard=ctx.world > 1)
+    ctx.barrier()
+    te = ctx.max_over_ranks(time.perf_counter() - t0)
+    lo, hi = shard_range(len(cams), ctx.rank, ctx.world)
+    vsz = 8 if getattr(opts, "precision", "fp64") == "fp64" else 4
+    return tab, {"value": len(cams) / te, "unit": "views/s",
+                 "h2d_bytes_per_step": (hi - lo) * (C.sizeof(N.RsCamera) + C.sizeof(N.RsOptions)),
+                 "d2h_bytes_per_step": vsz * len(scene),
+                 "api": "paper_2403_13806_b200.pruning.compute_importance (one full pass of all views)"}
 
+
+def roofline_render(ctx, m, prec_fp64: bool) -> dict:
+    kern = "blend64_kernel<1, 0, 0, 1>" if prec_fp64 else "blend2_kernel<1, 0, 0, 1, 0>"
+    return {"kernel": kern, "bound": "fp64" if prec_fp64 else "fp32", "achieved": m["blend_tflops"],
+            "peak": ctx.fp32_peak(), "unit": "TFLOP/s", "frac": m["blend_frac_fp32"],
+            "traffic": profiled_traffic(kern),
+            "traffic_source": TRAFFIC_FILE + " (ncu --set full: dram read+write bytes per launch)",
+            "algorithmic": "16*E + 11*C flops per frame (SURVEY §8d), E/C counted by the device",
+            "peak_source": "computed: SMs x 128 FP32 lanes x 2 x sm_max_mhz (MEASURED_PEAKS.json has no FP32 "
+                           "figure)"}
+
+
+# ---------------------------------------------------------------------------
+# workloads
+# ---------------------------------------------------------------------------
+def run_render(args, ctx):
+    from paper_2403_13806_b200 import synth
+    scene, cams = make_workload("render", args.n_gaussians)
+    frames = lambda s: cams[(s * ctx.world + ctx.rank) % len(cams)]  # noqa: E731
+    opts = dict_opts(args.precision)
+    m = measure_render(ctx, scene, frames, opts, args.steps, args.warmup)
+    W_, H_ = cams[0].width, cams[0].height
+    f64 = args.precision == "fp64"
+    my_frames = [frames(s) for s in range(min(args.steps, 30))]
+    result = {
+        "metric": METRIC_RENDER, "value": m["fps"], "unit": "frames/s", "n_gpus": ctx.world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": m["ms_per_frame"], "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64" if f64 else "f32",
+        "data": "synthetic (seeded configs[1]: 500k Gaussians in 32 clusters, SH deg 3; no dataset offline)",
+        "config": make_config("render", len(scene), W_, H_, ctx.world),
+        "stages_ms": {**m["stages_ms"], "note": "separate pass, three C-ABI stage launches per frame"},
+        "wall_fps": m["wall_fps"],
+        "workload_stats": {k: m[k] for k in ("visible_mean", "pairs_mean", "evals_per_px", "composites_per_px")},
+        "roofline": roofline_render(ctx, m, f64),
+        "frame_roofline": {"bytes_alg_per_frame": m["bytes_alg_per_frame"],
+                           "achieved_gbs": m["hbm_frac"] * ctx.hbm(), "peak_gbs": ctx.hbm(),
+                           "peak_source": ctx.pk["_source"], "frac": m["hbm_frac"]},
+        "gpu_launches": args.steps * frame_launches(len(scene), f64),
+        "clocks": m["clocks"],
+        "e2e": e2e_render(ctx, scene, my_frames, opts, len(my_frames)),
+    }
+    if ctx.rank == 0 and ctx.world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        sel = [frames(s) for s in range(4)]
+        dt, _ = cpu_views(scene, sel, True, threads)
+        result["cpu_baseline"] = {"value": len(sel) / dt, "unit": "frames/s", "cores": threads, "kind": "port",
+                                  "sample": f"{len(sel)} orbit frames, each on {threads} threads "
+                                            f"(oracle/cpu_ref.cpp fp32, tile-parallel), CPU {cpu_model()}"}
+    if not args.quick:
+        # the reference-arithmetic path on the same frames
+        o64 = dict_opts("fp32" if f64 else "fp64")
+        m64 = measure_render(ctx, scene, frames, o64, min(args.steps, 100), args.warmup, clocks=False)
+        result["fp64" if not f64 else "fp32"] = {
+            "fps": m64["fps"], "ms_per_frame": m64["ms_per_frame"], "stages_ms": m64["stages_ms"],
+            "e2e_fps": e2e_render(ctx, scene, my_frames, o64, len(my_frames))["value"],
+            "roofline": roofline_render(ctx, m64, not f64),
+            "note": ("fp64 = the reference's arithmetic (bit-identical to the oracle's Tier C, within ~1e-15 of "
+                     "the NumPy reference); the same graph-replay timing") if not f64 else "fp32 contract path"}
+        # configs[2] importance scoring (views sharded over the ranks, NCCL MAX all-reduce)
+        s2, c2 = synth.config2(0)
+        so = dict_opts("fp32")
+        sm = measure_score(ctx, s2, c2, so, steps=2, warmup=1)
+        _, se2e = e2e_score(ctx, s2, c2, so)
+        result["score"] = {"metric": METRIC_SCORE, "value": sm["views_per_s"], "unit": "views/s",
+                           "scaling": "strong", "n_gpus": ctx.world, **{k: v for k, v in sm.items()
+                                                                         if k != "views_per_s"},
+                           "e2e": se2e}
+        # FPS vs #Gaussians at 1256x828 (BASELINE metric), configs[1] distributions
+        sweep = []
+        for n in SWEEP_N:
+            sc, cc = synth.config1(0, n=n, n_frames=1000)
+            fr = lambda s, cc=cc: cc[(s * ctx.world + ctx.rank) % len(cc)]  # noqa: E731
+            ms = measure_render(ctx, sc, fr, opts, 40, 3, clocks=False)
+            sweep.append({"n_gaussians": n, "fps": ms["fps"], "ms_per_frame": ms["ms_per_frame"],
+                          "stages_ms": ms["stages_ms"], "visible_mean": ms["visible_mean"],
+                          "pairs_mean": ms["pairs_mean"], "blend_frac_fp32": ms["blend_frac_fp32"],
+                          "hbm_frac": ms["hbm_frac"]})
+            del sc
+        result["fps_vs_n"] = sweep
+    return result
+
+
+def run_score(args, ctx):
+    scene, cams = make_workload("score", args.n_gaussians)
+    opts = dict_opts(args.precision)
+    sm = measure_score(ctx, scene, cams, opts, args.steps, args.warmup)
+    tab, e2e = e2e_score(ctx, scene, cams, opts)
+    assert int((tab.values >= 0.01).sum()) == sm["kept_at_0.01"]
+    W_, H_ = cams[0].width, cams[0].height
+    result = {
+        "metric": METRIC_SCORE, "value": sm["views_per_s"], "unit": "views/s", "n_gpus": ctx.world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sm["ms_per_pass"], "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64" if args.precision == "fp64" else "f32",
+        "data": "synthetic (seeded configs[2]: 3M Gaussians, log-scale N(-4,0.6); no dataset offline)",
+        "config": make_config("score", len(scene), W_, H_, ctx.world),
+        **{k: v for k, v in sm.items() if k not in ("views_per_s", "ms_per_pass")},
+        "e2e": e2e,
+        "gpu_launches": args.steps * (sm["views_this_rank"] * frame_launches(len(scene), args.precision == "fp64")),
+    }
+    if ctx.rank == 0 and ctx.world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        sel = cams[:2]
+        dt, _ = cpu_views(scene, sel, False, threads)
+        result["cpu_baseline"] = {"value": len(sel) / dt, "unit": "views/s", "cores": threads, "kind": "port",
+                                  "sample": f"{len(sel)} of the 200 views, each on {threads} threads "
+                                            f"(oracle/cpu_ref.cpp fp32 scoring, tile-parallel), CPU {cpu_model()}"}
+    return result
+
+
+def run_trajectory(args, ctx):
+    """configs[3] (house: 300-frame trajectory, FPS with vs without visibility filtering,
+    bakes at the config's rule, the reference's defaults and a quality-matched threshold) and
+    configs[4] (batched multi-view render: 64 frames per GPU per step). Frames split across
+    ranks (replicas); each frame timed with CUDA events on the launching stream, L2 flushed
+    between frames (outside the events)."""
     from paper_2403_13806_b200 import _native as N
     from paper_2403_13806_b200 import synth
-    from paper_2403_13806_b200.device import camera_struct, device_scene
+    from paper_2403_13806_b200.device import FrameGraph, camera_struct, device_scene, options_struct
     from paper_2403_13806_b200.visibility import _center, bake_visibility, cluster_cameras
-
+    torch = ctx.torch
+    opts = dict_opts(args.precision)
+    opt_s = options_struct(opts)
     house = args.workload == "house"
+    rank, world = ctx.rank, ctx.world
     if house:
         scene, train_cams, traj = synth.config3(0, n=args.n_gaussians or 6_000_000)
         per_step = 1
@@ -490,52 +687,49 @@ def run_trajectory(args, rank, world, local, dev, opts, r, opt_s, stream, flush,
         per_step = 64
         frame_cams = lambda s: [traj[((s * world + rank) * per_step + i) % len(traj)]  # noqa: E731
                                 for i in range(per_step)]
-    ds = device_scene(scene, dev)
+    ds = device_scene(scene, ctx.dev)
     W_, H_ = traj[0].width, traj[0].height
     hw = W_ * H_
     T = ((W_ + 15) // 16) * ((H_ + 15) // 16)
-    lib = r.lib
-    sptr = stream.cuda_stream
+    r, lib, sptr = ctx.r, ctx.lib, ctx.sptr
     extra = {}
+    tables = {}
+    # house bake settings: the config's rule (h >= 0.01 read as the reference's strict
+    # h > 0.01, member cameras only), the reference's bake defaults (h > 0.001, 3 jittered
+    # auxiliary cameras per member, visibility.py:175-177), and quality-matched thresholds
+    # (h > 1e-4 and h > 0: every Gaussian a member camera composites -- the reference's >= 45 dB
+    # acceptance bar on the baking views, test_acceptance.py:303-329)
+    bakes = (("filtered", 0.01, 0), ("filtered_ref_defaults", 0.001, 3), ("filtered_1e-4", 1e-4, 0),
+             ("filtered_0", 0.0, 0)) if house else ()
     if house:
-        # bake: k-means (k=64) over the 512 training-camera centres, then one importance
-        # pass per cluster over its member cameras; list = {h > 0.01} (reference strict >,
-        # visibility.py:204; aux cameras 0 = "from that cluster's cameras")
         clustering = cluster_cameras(np.array([_center(c) for c in train_cams]), 64, seed=0)
-        barrier()
-        tables = {}
-        # "filtered": the configs[3] rule (h >= 0.01 read as the reference's strict h > 0.01, member
-        # cameras only); "filtered_ref_defaults": the reference's bake defaults (h > 0.001 and 3
-        # jittered auxiliary cameras per member, visibility.py:175-177)
-        for arm, t_c, aux in (("filtered", 0.01, 0), ("filtered_ref_defaults", 0.001, 3)):
+        ctx.barrier()
+        for arm, t_c, aux in bakes:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
+            e0.record(ctx.stream)
             vt = bake_visibility(scene, clustering, train_cams, t_cluster=t_c, aux_per_camera=aux, seed=0,
-                                 options=opts)
-            e1.record(stream)
-            barrier()
+                                 options=opts, shard=world > 1)
+            e1.record(ctx.stream)
+            ctx.barrier()
             counts = vt.active_counts()
             extra.setdefault("bake", {})[arm] = {
                 "clusters": 64, "cameras": len(train_cams), "aux_per_camera": aux, "t_cluster": t_c,
                 "ms": e0.elapsed_time(e1), "active_mean": float(counts.mean()), "active_min": int(counts.min()),
                 "active_max": int(counts.max())}
-            tables[arm] = (vt, {j: vt.visible_indices(j, dev) for j in range(vt.k)})
-        vis = tables["filtered"][0]
+            tables[arm] = (vt, {j: vt.visible_indices(j, ctx.dev) for j in range(vt.k)})
 
-        def list_for(arm, cam):
-            vt, ls = tables[arm]
-            return ls[vt.nearest_cluster(_center(cam))]
+    def list_for(arm, cam):
+        vt, ls = tables[arm]
+        return ls[vt.nearest_cluster(_center(cam))]
+
     out = r.alloc_outputs(traj[0])
     outs = r.outputs_struct(out)
-
-    arms = ([("filtered", True), ("filtered_ref_defaults", True), ("unfiltered", False)] if house
-            else [("all", False)])
+    arms = [(a, True) for a, _, _ in bakes] + [("unfiltered", False)] if house else [("all", False)]
     res_arms = {}
     for arm, filt in arms:
-        # untimed checked pre-pass over every timed frame: pair capacity + E/C/P statistics
         E = C_ = P_ = NV = NI = 0
         nfr = 0
-        for s in range(args.steps):
+        for s in range(args.steps):  # checked pre-pass: pair capacity + E/C/P statistics
             for cam in frame_cams(s):
                 idx = list_for(arm, cam) if filt else None
                 _, st = r.render(ds, cam, opts, out=out, active_idx=idx, count_evals=True)
@@ -545,19 +739,13 @@ def run_trajectory(args, rank, world, local, dev, opts, r, opt_s, stream, flush,
                 NV += st.n_visible
                 NI += st.n_items
                 nfr += 1
-        plan = []
-        for s in range(args.steps):
-            for cam in frame_cams(s):
-                idx = list_for(arm, cam) if filt else None
-                plan.append((camera_struct(cam), idx))
-
-        # house: one CUDA graph per index list (64 cluster lists per filtered arm, one unfiltered),
-        # captured after the capacity pre-pass; a frame = camera upload + one graph launch (the
-        # small filtered frames are otherwise bound by the host launching ~15 kernels)
+        plan = [(camera_struct(cam), list_for(arm, cam) if filt else None)
+                for s in range(args.steps) for cam in frame_cams(s)]
+        # house: one CUDA graph per index list (a filtered frame is otherwise bound by the host
+        # launching ~12 kernels); camera uploaded per frame, then one graph launch
         graphs = {}
         if house:
-            from paper_2403_13806_b200.device import FrameGraph
-            torch.cuda.synchronize(dev)
+            torch.cuda.synchronize(ctx.dev)
             for _, idx in plan:
                 key = None if idx is None else idx.data_ptr()
                 if key not in graphs:
@@ -575,105 +763,136 @@ def run_trajectory(args, rank, world, local, dev, opts, r, opt_s, stream, flush,
 
         for cs, idx in plan[:max(args.warmup, 1)]:
             launch(cs, idx)
-        barrier()
-        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in plan]
-        with ClockSampler(local) as clk:
-            barrier()
+        ctx.barrier()
+        r.read_overflow(reset=True)
+        evs = ctx.events(len(plan))
+        with ClockSampler(ctx.local) as clk:
+            ctx.barrier()
             for (cs, idx), (a, b) in zip(plan, evs):
-                flush.zero_()
-                a.record(stream)
+                ctx.flush.zero_()
+                a.record(ctx.stream)
                 launch(cs, idx)
-                b.record(stream)
-            barrier()
-        assert not r.stats().overflow
-        t_local = torch.tensor([sum(a.elapsed_time(b) for a, b in evs)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
-        t_max = float(t_local.item())
+                b.record(ctx.stream)
+            ctx.barrier()
+        check_sticky(ctx)
+        t_max = ctx.max_over_ranks(sum(a.elapsed_time(b) for a, b in evs))
+        sel = [c for s in range(args.steps) for c in frame_cams(s)][:6]
+        stages = staged_times(ctx, ds, sel, opts, [out[k].data_ptr() for k in ("rgb", "alpha", "depth", "count")]) \
+            if not filt else None
         res_arms[arm] = {
             "fps": world * nfr / (t_max / 1e3), "ms_per_frame": t_max / nfr, "clocks": clk.summary(),
             "projected_mean": NI / nfr, "visible_mean": NV / nfr, "pairs_mean": P_ / nfr,
             "pairs_per_tile_mean": P_ / nfr / T, "evals_per_px": E / nfr / hw, "composites_per_px": C_ / nfr / hw,
+            "flops_alg_per_frame": (16 * E + 11 * C_) / nfr,
             "bytes_alg_per_frame": bytes_alg_render(NI / nfr, NV / nfr, P_ / nfr, hw),
             "frames": nfr * world}
+        if stages is not None:
+            res_arms[arm]["stages_ms"] = {"preprocess": float(stages[0]), "sort": float(stages[1]),
+                                          "blend": float(stages[2])}
     main_arm = res_arms["filtered" if house else "all"]
-    t_max = main_arm["ms_per_frame"] * (main_arm["frames"] // world)
-    metric = METRICS[args.workload]
+    ref_arm = res_arms["unfiltered" if house else "all"]
     if house:
+        # quality of each bake vs the full render (the reference's acceptance metric, PSNR,
+        # test_acceptance.py:303-329) on baking (training) views and on trajectory frames
+        for arm, _, _ in bakes:
+            for where, cams_q in (("baking_views", train_cams[::32]), ("trajectory", traj[::19])):
+                ps = []
+                for cam in cams_q:
+                    full, _ = r.render(ds, cam, opts)
+                    full = full["rgb"].clone()
+                    filt_img, _ = r.render(ds, cam, opts, active_idx=list_for(arm, cam))
+                    mse = float(((filt_img["rgb"].double() - full.double()) ** 2).mean().item())
+                    ps.append(float("inf") if mse == 0 else 10.0 * np.log10(1.0 / mse))
+                res_arms[arm][f"psnr_vs_full_db_{where}"] = {
+                    "mean": float(np.mean([p for p in ps if np.isfinite(p)])) if any(np.isfinite(ps)) else "inf",
+                    "min": float(np.min(ps)) if np.isfinite(np.min(ps)) else "inf", "frames": len(ps)}
         extra["fps_unfiltered"] = res_arms["unfiltered"]["fps"]
-        extra["fps_ref_defaults"] = res_arms["filtered_ref_defaults"]["fps"]
         extra["filtering_speedup"] = res_arms["filtered"]["fps"] / res_arms["unfiltered"]["fps"]
-    value = main_arm["fps"]
+        ok = [a for a, _, _ in bakes
+              if res_arms[a]["psnr_vs_full_db_baking_views"]["min"] == "inf"
+              or res_arms[a]["psnr_vs_full_db_baking_views"]["min"] >= 45.0]
+        best = max(ok, key=lambda a: res_arms[a]["fps"]) if ok else None
+        extra["quality_matched"] = {"arm": best, "fps": res_arms[best]["fps"] if best else None,
+                                    "speedup_vs_unfiltered": res_arms[best]["fps"] / res_arms["unfiltered"]["fps"]
+                                    if best else None,
+                                    "bar": ">= 45 dB vs the full render on every sampled baking view "
+                                           "(test_acceptance.py:303-329)"}
+    # roofline of the dominant kernel (the blend of the unfiltered / batch frames)
+    fl, bl = ref_arm["flops_alg_per_frame"], ref_arm["stages_ms"]["blend"]
+    ach = fl / (bl / 1e3) / 1e12
+    peak = ctx.fp32_peak()
+    t_frame = main_arm["ms_per_frame"]
     result = {
-        "metric": metric, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32",
+        "metric": METRICS[args.workload], "value": main_arm["fps"], "unit": "frames/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_frame * per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64" if args.precision == "fp64" else "f32",
         "data": f"synthetic (seeded configs[{3 if house else 4}]; no dataset offline)",
-        "config": {"workload": WORKLOADS[args.workload],
-                   "n_gaussians": len(scene), "width": W_, "height": H_, "tile": 16,
-                   "frames_per_gpu_per_step": per_step, "l2": "flushed (256 MB memset) between timed frames",
-                   "parallelism": f"frames split across {world} GPU(s), no communication"},
+        "config": make_config(args.workload, len(scene), W_, H_, world),
+        "frames_per_gpu_per_step": per_step,
         "arms": res_arms, "clocks": main_arm["clocks"],
-        "gpu_launches": sum(a["frames"] // world for a in res_arms.values()) * frame_launches(W_, H_),
+        "gpu_launches": sum(a["frames"] // world for a in res_arms.values())
+        * frame_launches(len(scene), args.precision == "fp64"),
+        "roofline": {"kernel": "blend2_kernel<1, 0, 0, 1, 0>" + (" (unfiltered frames)" if house else ""),
+                     "bound": "fp32", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                     "traffic": None, "algorithmic": "16*E + 11*C flops per frame (SURVEY §8d)",
+                     "peak_source": "computed: SMs x 128 FP32 lanes x 2 x sm_max_mhz"},
         "frame_roofline": {"bytes_alg_per_frame": main_arm["bytes_alg_per_frame"],
-                           "achieved_gbs": main_arm["bytes_alg_per_frame"] / (main_arm["ms_per_frame"] / 1e3) / 1e9,
-                           "peak_gbs": pk.get("hbm_gbs"),
-                           "frac": main_arm["bytes_alg_per_frame"] / (main_arm["ms_per_frame"] / 1e3) / 1e9
-                           / pk.get("hbm_gbs", 6548.8)},
+                           "achieved_gbs": main_arm["bytes_alg_per_frame"] / (t_frame / 1e3) / 1e9,
+                           "peak_gbs": ctx.hbm(),
+                           "frac": main_arm["bytes_alg_per_frame"] / (t_frame / 1e3) / 1e9 / ctx.hbm()},
         **extra,
     }
-    if house:
-        # quality of the filtered frames vs the full render (reference acceptance: PSNR,
-        # test_acceptance.py:303-329), on a sample of the timed frames
-        for arm in ("filtered", "filtered_ref_defaults"):
-            ps = []
-            for cam in [c for s in range(args.steps) for c in frame_cams(s)][:16]:
-                full, _ = r.render(ds, cam, opts)
-                full = full["rgb"].clone()
-                filt, _ = r.render(ds, cam, opts, active_idx=list_for(arm, cam))
-                mse = float(((filt["rgb"] - full) ** 2).mean().item())
-                ps.append(99.0 if mse == 0 else 10.0 * np.log10(1.0 / mse))
-            res_arms[arm]["psnr_vs_full_db"] = {"mean": float(np.mean(ps)), "min": float(np.min(ps)),
-                                                "frames": len(ps)}
     # e2e through the public API (host results every frame)
     from paper_2403_13806_b200.render import rasterize
     from paper_2403_13806_b200.visibility import render_from_viewpoint
     sel = [c for s in range(args.steps) for c in frame_cams(s)][:8]
+    vis = tables["filtered"][0] if house else None
     call = (lambda c: render_from_viewpoint(scene, vis, c, opts)) if house else (lambda c: rasterize(scene, c, opts))
     call(sel[0])
-    barrier()
+    ctx.barrier()
     t0 = time.perf_counter()
     for c in sel:
         call(c)
-    barrier()
-    te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    result["e2e"] = {"value": world * len(sel) / float(te.item()), "unit": "frames/s",
+    ctx.barrier()
+    te = ctx.max_over_ranks(time.perf_counter() - t0)
+    result["e2e"] = {"value": world * len(sel) / te, "unit": "frames/s",
                      "h2d_bytes_per_step": per_step * (C.sizeof(N.RsCamera) + C.sizeof(N.RsOptions)),
                      "d2h_bytes_per_step": per_step * hw * (24 + 8 + 8),
                      "api": "paper_2403_13806_b200." + ("visibility.render_from_viewpoint" if house
                                                         else "render.rasterize") + f" ({len(sel)} frames)"}
-    if rank == 0:
-        print(json.dumps(result), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        if house:
+            cam = frame_cams(0)[0]
+            dt, _ = cpu_views(scene, [cam], True, threads)
+            result["cpu_baseline"] = {"value": 1.0 / dt, "unit": "frames/s", "cores": threads, "kind": "port",
+                                      "sample": f"1 unfiltered trajectory frame on {threads} threads "
+                                                f"(oracle/cpu_ref.cpp fp32, tile-parallel), CPU {cpu_model()}"}
+        else:
+            crop = crop_camera(frame_cams(0)[0], 4)
+            dt, _ = cpu_views(scene, [crop], True, threads)
+            result["cpu_baseline"] = {"value": 1.0 / (16 * dt), "unit": "frames/s", "cores": threads, "kind": "port",
+                                      "sample": f"the central 480x270 window (1/16) of one 1920x1080 view on "
+                                                f"{threads} threads, rate scaled to whole frames (oracle/cpu_ref.cpp "
+                                                f"fp32, tile-parallel), CPU {cpu_model()}"}
+    return result
 
 
-def run_train(args, rank, world, local, dev, opts, r, opt_s, stream, flush, pk, barrier):
+def run_train(args, ctx):
     """Training step of the backward path: per view the training
     forward (rs_render_ex recording tau / last) and rs_backward for a dense random
     dL/dimage, gradients for every Gaussian parameter; views split across ranks."""
-    import torch
-    import torch.distributed as dist
-
     from paper_2403_13806_b200 import _native as N
-    from paper_2403_13806_b200.device import camera_struct, device_scene
-
+    from paper_2403_13806_b200.device import camera_struct, device_scene, options_struct
+    torch = ctx.torch
+    opts = dict_opts("fp32")
+    opt_s = options_struct(opts)
     scene, cams = make_workload("train", args.n_gaussians)
-    ds = device_scene(scene, dev)
+    ds = device_scene(scene, ctx.dev)
+    r, dev = ctx.r, ctx.dev
     W_, H_ = cams[0].width, cams[0].height
-    frames = lambda s: cams[(s * world + rank) % len(cams)]  # noqa: E731
+    frames = lambda s: cams[(s * ctx.world + ctx.rank) % len(cams)]  # noqa: E731
     out = r.alloc_outputs(cams[0])
     out["tau"] = torch.empty((H_, W_), dtype=torch.float32, device=dev)
     out["last"] = torch.empty((H_, W_), dtype=torch.int32, device=dev)
@@ -684,69 +903,59 @@ def run_train(args, rank, world, local, dev, opts, r, opt_s, stream, flush, pk, 
     gimg = torch.randn((H_, W_, 3), dtype=torch.float32, device=dev, generator=torch.Generator(dev).manual_seed(0))
     g = [torch.empty(k, dtype=torch.float32, device=dev) for k in (3 * n, 48 * n, 3 * n, 4 * n, n, n)]
     touched = torch.empty(n, dtype=torch.uint8, device=dev)
-    lib, sptr = r.lib, stream.cuda_stream
+    lib, sptr = r.lib, ctx.sptr
 
     def step(cs, ev):
-        ev[0].record(stream)
+        ev[0].record(ctx.stream)
         N.check(lib.rs_render_ex(r.handle, C.byref(ds.struct), None, 0, C.byref(cs), C.byref(opt_s),
                                  C.byref(outs), None, 0, sptr))
-        ev[1].record(stream)
+        ev[1].record(ctx.stream)
         N.check(lib.rs_backward(r.handle, C.byref(ds.struct), None, 0, C.byref(opt_s), gimg.data_ptr(),
                                 out["tau"].data_ptr(), out["last"].data_ptr(), *(t.data_ptr() for t in g),
                                 touched.data_ptr(), sptr))
-        ev[2].record(stream)
+        ev[2].record(ctx.stream)
 
     plan = [camera_struct(frames(s)) for s in range(args.steps)]
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in plan]
     for s in range(args.warmup):
         step(plan[s % len(plan)], ev[0])
-    barrier()
-    with ClockSampler(local) as clk:
-        barrier()
+    ctx.barrier()
+    r.read_overflow(reset=True)
+    with ClockSampler(ctx.local) as clk:
+        ctx.barrier()
         for cs, e in zip(plan, ev):
-            flush.zero_()
+            ctx.flush.zero_()
             step(cs, e)
-        barrier()
-    assert not r.stats().overflow
+        ctx.barrier()
+    check_sticky(ctx)
     fwd = np.array([a.elapsed_time(b) for a, b, _ in ev])
     bwd = np.array([b.elapsed_time(c) for _, b, c in ev])
-    t_local = torch.tensor([float(fwd.sum() + bwd.sum())], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
-    t_max = float(t_local.item())
-    result = {
-        "metric": METRICS["train"], "value": world * args.steps / (t_max / 1e3), "unit": "views/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+    t_max = ctx.max_over_ranks(float(fwd.sum() + bwd.sum()))
+    return {
+        "metric": METRIC_TRAIN, "value": ctx.world * args.steps / (t_max / 1e3), "unit": "views/s",
+        "n_gpus": ctx.world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded configs[1], random dL/dimage; no dataset offline)",
-        "config": {"workload": WORKLOADS["train"], "n_gaussians": n, "width": W_, "height": H_,
-                   "l2": "flushed (256 MB memset) between timed steps",
-                   "parallelism": f"views split across {world} GPU(s), no communication"},
+        "config": make_config("train", n, W_, H_, ctx.world),
         "stages_ms": {"forward_with_cache": float(fwd.mean()), "backward": float(bwd.mean())},
-        "gpu_launches": args.steps * (frame_launches(W_, H_) + 2), "clocks": clk.summary(),
+        "gpu_launches": args.steps * (frame_launches(n, False) + 2), "clocks": clk.summary(),
     }
-    if rank == 0:
+
+
+def main():
+    args = parse()
+    rc = maybe_spawn(args)
+    if rc is not None:
+        sys.exit(rc)
+    if args.impl == "reference":
+        return run_reference(args)
+    ctx = Ctx(args)
+    fn = {"render": run_render, "score": run_score, "house": run_trajectory, "batch": run_trajectory,
+          "train": run_train}[args.workload]
+    result = fn(args, ctx)
+    if ctx.rank == 0:
         print(json.dumps(result), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
-
-
-TRAFFIC_FILE = "profiles/round1_ncu_full_configs1_traffic.json"
-
-
-def profiled_traffic(kernel: str):
-    """DRAM bytes per launch of `kernel` from the committed ncu --set full capture (or None)."""
-    try:
-        return json.loads((ROOT / TRAFFIC_FILE).read_text()).get(kernel)
-    except (OSError, ValueError):
-        return None
-
-
-def frame_launches(W, H):
-    """Kernels per frame (image size independent): project, depth-key compaction + histograms,
-    4 depth passes, segment rows / scan / placement, chunk count, tile chunks, tile scan (ranges
-    + blend order), expansion (sparse and dense chunks), blend."""
-    return 1 + 1 + 4 + 3 + 1 + 1 + 1 + 2 + 1
+    ctx.close()
 
 
 if __name__ == "__main__":
