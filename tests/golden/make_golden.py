@@ -238,6 +238,7 @@ def main():
     make_io(fs, cf)
     make_grad(fs, cf)
     make_metrics(fs, cf)
+    make_scale(fs)
     print("golden fixtures written to", HERE)
 
 
@@ -330,8 +331,77 @@ def make_metrics(fs, conftest):
     np.savez_compressed(HERE / "metrics.npz", **d)
 
 
+# ---------------------------------------------------------------------------
+# L: BASELINE-scale frames rendered by the reference itself (SURVEY §8d scenes from
+# paper_2403_13806_b200.synth, upcast to fp64 exactly like the reference reads RSPL).
+# Stored compactly: the full per-pixel composite count (uint16), colour/alpha on a
+# seeded sample of pixels, and every non-zero importance score (index + value).
+# ---------------------------------------------------------------------------
+SCALE_CASES = {
+    # name: (config, scene kwargs, camera source, width, height)
+    "c1": ("config1", {"n": 500_000}, ("orbit", 137), 628, 414),      # configs[1] frame 137, half res
+    "c4": ("config4", {"n": 1_000_000}, ("views", 0), 240, 135),      # configs[4] view 0, 1/8 res
+    "c3": ("config3", {"n": 300_000}, ("traj", 0), 480, 270),         # configs[3] scaled to 300k, inside
+    "c2": ("config2", {"n": 3_000_000}, ("views", 0), 314, 207),      # configs[2] view 0, 1/4 res
+}
+SCALE_SAMPLE = 20_000
+
+
+def scale_case(name):
+    """(SceneArrays, camera) of a scale case -- shared by make_golden and the tests."""
+    from paper_2403_13806_b200 import synth
+    from paper_2403_13806_b200.core import look_at_camera
+    cfg, kw, (src, k), w, h = SCALE_CASES[name]
+    out = getattr(synth, cfg)(0, **kw)
+    scene = out[0]
+    cams = out[2] if src == "traj" else out[1]
+    c = cams[k]
+    R, t = np.asarray(c.rotation, np.float64), np.asarray(c.translation, np.float64)
+    eye = -R.T @ t
+    fwd = R[2]  # camera z axis in world coordinates (look direction)
+    import math
+    fov = math.degrees(2.0 * math.atan(c.width / (2.0 * c.fx)))
+    cam = look_at_camera(eye, eye + fwd, width=w, height=h, fov_deg=fov)
+    return scene, cam
+
+
+def make_scale(fs, names=None):
+    d = {}
+    R = fs.render
+    opts = R.RasterizeOptions(near_limit=0.2)
+    for name in names or SCALE_CASES:
+        sa, cam = scale_case(name)
+        scene = fs.GaussianScene(positions=sa.positions.astype(np.float64),
+                                 opacity_logits=sa.opacity_logits.astype(np.float64),
+                                 sh=sa.sh.astype(np.float64), log_scales=sa.log_scales.astype(np.float64),
+                                 quaternions=sa.quaternions.astype(np.float64),
+                                 active_sh_degree=sa.active_sh_degree)
+        rcam = fs.PinholeCamera(rotation=cam.rotation, translation=cam.translation, fx=cam.fx, fy=cam.fy,
+                                cx=cam.cx, cy=cam.cy, width=cam.width, height=cam.height)
+        acc = R.ContributionAccumulator(len(scene))
+        out = R.rasterize_with_contributions(scene, rcam, acc, opts)
+        p = name + "_"
+        pack_cam(d, p, cam)
+        pack_opts(d, p, opts)
+        d[p + "count"] = np.asarray(out.count, np.uint16)
+        npx = cam.width * cam.height
+        pix = np.sort(np.random.default_rng(7).choice(npx, size=min(SCALE_SAMPLE, npx), replace=False))
+        d[p + "pix"] = pix.astype(np.int64)
+        d[p + "img_s"] = np.asarray(out.color.data, np.float64).reshape(-1, 3)[pix]
+        d[p + "alpha_s"] = np.asarray(out.alpha, np.float64).reshape(-1)[pix]
+        nz = np.nonzero(acc.values)[0]
+        d[p + "score_idx"] = nz.astype(np.int64)
+        d[p + "score_val"] = acc.values[nz].astype(np.float64)
+        d[p + "n"] = np.int64(len(scene))
+        print(name, "visible composites", int(out.count.sum()), "non-zero scores", len(nz), flush=True)
+    np.savez_compressed(HERE / "scale.npz", **d)
+
+
 if __name__ == "__main__":
-    if sys.argv[1:] == ["io"]:  # only the wire-format fixtures
+    if sys.argv[1:2] == ["scale"]:  # only the BASELINE-scale frames (a few minutes)
+        fs_, _, _ = import_reference()
+        make_scale(fs_, sys.argv[2:] or None)
+    elif sys.argv[1:] == ["io"]:  # only the wire-format fixtures
         fs_, conftest_, _ = import_reference()
         make_io(fs_, conftest_)
     elif sys.argv[1:] == ["grad"]:  # only the backward-pass fixtures
