@@ -53,7 +53,9 @@ WORKLOADS = {"render": "configs[1] orbit render", "score": "configs[2] importanc
              "house": "configs[3] house trajectory", "batch": "configs[4] batched views",
              "train": "configs[1] orbit, forward + backward"}
 SWEEP_N = (125_000, 250_000, 500_000, 1_000_000, 2_000_000, 3_000_000)
-TRAFFIC_FILE = "profiles/round2_ncu_traffic.json"
+TRAFFIC = {"render_fp32": "profiles/round2_full_configs1_fp32_traffic.json",
+           "render_fp64": "profiles/round2_full_configs1_fp64_traffic.json",
+           "score_fp32": "profiles/round2_full_configs2_fp32_traffic.json"}
 
 
 def parse():
@@ -214,11 +216,12 @@ def frame_launches(n_items: int, f64: bool) -> int:
     return 1 + sort + (1 if f64 else 0) + 3 + 1 + 1 + 1 + 2 + 1
 
 
-def profiled_traffic(kernel: str):
-    """DRAM bytes per launch of `kernel` from the committed ncu --set full capture (or None)."""
+def profiled_traffic(which: str, kernel: str):
+    """DRAM bytes per launch of `kernel` (the warm-workspace frame's launch) from the committed
+    ncu --set full capture of that workload (profiles/round2_full_*.csv), or None."""
     try:
-        return json.loads((ROOT / TRAFFIC_FILE).read_text()).get(kernel)
-    except (OSError, ValueError):
+        return json.loads((ROOT / TRAFFIC[which]).read_text()).get(kernel)
+    except (KeyError, OSError, ValueError):
         return None
 
 
@@ -527,7 +530,9 @@ def measure_score(ctx, scene, cams, opts, steps, warmup, staged_views=6):
     res["roofline"] = {
         "kernel": "blend64_kernel<0,1,0,1> (score)" if prec == N.RS_F64 else "blend2_kernel<0,1,0,1,0> (score)",
         "bound": "fp64" if prec == N.RS_F64 else "fp32", "achieved": blend_t, "peak": peak, "unit": "TFLOP/s",
-        "frac": blend_t / peak, "traffic": profiled_traffic("blend2_kernel<0, 1, 0, 1, 0>"),
+        "frac": blend_t / peak,
+        "traffic": profiled_traffic("score_fp64" if prec == N.RS_F64 else "score_fp32", "blend2_kernel<0, 1, 0, 1, 0>"),
+        "traffic_source": TRAFFIC["score_fp32"] + " (ncu --set full, dram read+write bytes per launch)",
         "algorithmic": "16*E + 5*C flops per view (SURVEY §8d), E/C counted on the staged views",
         "peak_source": "computed: SMs x 128 FP32 lanes x 2 x sm_max_mhz"}
     res["view_roofline"] = {"bytes_alg_per_view": byt, "achieved_gbs": byt / (view_ms / 1e3) / 1e9,
@@ -559,8 +564,9 @@ def roofline_render(ctx, m, prec_fp64: bool) -> dict:
     kern = "blend64_kernel<1, 0, 0, 1>" if prec_fp64 else "blend2_kernel<1, 0, 0, 1, 0>"
     return {"kernel": kern, "bound": "fp64" if prec_fp64 else "fp32", "achieved": m["blend_tflops"],
             "peak": ctx.fp32_peak(), "unit": "TFLOP/s", "frac": m["blend_frac_fp32"],
-            "traffic": profiled_traffic(kern),
-            "traffic_source": TRAFFIC_FILE + " (ncu --set full: dram read+write bytes per launch)",
+            "traffic": profiled_traffic("render_fp64" if prec_fp64 else "render_fp32", kern),
+            "traffic_source": TRAFFIC["render_fp64" if prec_fp64 else "render_fp32"]
+            + " (ncu --set full: dram read+write bytes per launch)",
             "algorithmic": "16*E + 11*C flops per frame (SURVEY §8d), E/C counted by the device",
             "peak_source": "computed: SMs x 128 FP32 lanes x 2 x sm_max_mhz (MEASURED_PEAKS.json has no FP32 "
                            "figure)"}
