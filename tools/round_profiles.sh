@@ -26,7 +26,7 @@ ncu --set full --import-source on --clock-control none -c 40 \
 for f in $O/${R}_full_*.ncu-rep; do
   b=${f%.ncu-rep}
   python tools/ncu_summary.py $f $b > $b.txt 2>&1
-  python tools/ncu_src.py $f "blend" 0 40 > ${b}_blend_src.txt 2>&1
+  python tools/ncu_src.py $f "blend" 1 40 > ${b}_blend_src.txt 2>&1  # skip the first (overflowed) frame's blend
 done
 python tools/ncu_src.py $O/${R}_full_configs1_fp32.ncu-rep "dsort" 0 30 > $O/${R}_full_configs1_fp32_dsort_src.txt 2>&1
 rm -f $O/*.ncu-rep
