@@ -13,7 +13,8 @@
 //     frames): Tier B's projection with exp64_contract (an exp from IEEE double
 //     add/mul/fma only; device twin in csrc/rs_math.cuh) instead of std::exp;
 //     the composite with fused roundings -- x = -q/2 as two fmas, a table exp
-//     (exp64_tab) with its argument clamped at 709 (an overflow guard),
+//     (exp64_tab: 1024-entry table + degree-3 polynomial) with its argument
+//     clamped at 709 (an overflow guard),
 //     rgb/depth += c w and tau (1 - alpha) as fmas -- and the pixel gate of the
 //     fp32 tier's culling box (which drops only pixels with alpha < alpha_cut).
 //     Tier C vs Tier B (and the reference): a few ulp (tests: <= 1e-12).
@@ -163,12 +164,12 @@ inline double exp64_contract(double x) {
 }
 
 // e^x of the fp64 contract's blend (device twin: exp64_tab in csrc/rs_math.cuh):
-// k = rint(x 64 / ln 2), r = x - k ln2/64 (Cody-Waite), degree-5 Taylor, times
-// T[k mod 64] = exp64_contract(j ln2/64) scaled by 2^(k div 64) in the exponent field.
+// k = rint(x 1024 / ln 2), r = x - k ln2/1024 (Cody-Waite), degree-3 Taylor, times
+// T[k mod 1024] = exp64_contract(j ln2/1024) scaled by 2^(k div 1024) in the exponent field.
 struct Exp64Tab {
-  double T[64];
+  double T[1024];
   Exp64Tab() {
-    for (int j = 0; j < 64; ++j) T[j] = exp64_contract((double)j * (0.6931471805599453 / 64.0));
+    for (int j = 0; j < 1024; ++j) T[j] = exp64_contract((double)j * (0.6931471805599453 / 1024.0));
   }
 };
 inline double with_exp(double t, int add) {  // t * 2^add by the exponent field (t normal, result normal)
@@ -184,20 +185,18 @@ inline double exp64_tab(double x) {
   if (x != x) return x;
   if (x > 709.782712893384) return INFINITY;
   if (x < -745.2) return 0.0;
-  const double t = std::fma(x, 92.33248261689366, 6755399441055744.0);
+  const double t = std::fma(x, 1477.3197218702985, 6755399441055744.0);
   const double kd = t - 6755399441055744.0;
-  double r = std::fma(kd, -(0.6931471803691238 / 64.0), x);
-  r = std::fma(kd, -(1.9082149292705877e-10 / 64.0), r);
-  double p = std::fma(1.0 / 120.0, r, 1.0 / 24.0);
-  p = std::fma(p, r, 1.0 / 6.0);
-  p = std::fma(p, r, 0.5);
+  double r = std::fma(kd, -(0.6931471803691238 / 1024.0), x);
+  r = std::fma(kd, -(1.9082149292705877e-10 / 1024.0), r);
+  double p = std::fma(1.0 / 6.0, r, 0.5);
   p = std::fma(p, r, 1.0);
   p = std::fma(p, r, 1.0);
   uint64_t tb;
   std::memcpy(&tb, &t, 8);
   const int k = (int)(int32_t)(uint32_t)tb;
-  const int n = k >> 6;
-  const double tj = tab.T[k & 63];
+  const int n = k >> 10;
+  const double tj = tab.T[k & 1023];
   if (n >= -1022) return p * with_exp(tj, n);
   return (p * with_exp(tj, n + 600)) * pow2i64(-600);
 }

@@ -90,7 +90,7 @@ constexpr int kMaxDsortCtas = 160;  // cooperative depth sort: one CTA per SM (c
 struct Layout {
   // per-frame zeroed region [0, frame_bytes)
   size_t ctr, hist, proj_lb, ranges, frame_bytes;
-  size_t sticky, cam, recs, recs64, dtab, rows, sgrad, titem, keysA, keysB, valsA, valsB, rowtab, rowcnt, segitem, segspan, geom,
+  size_t sticky, cam, recs, recs64, exptab, dtab, rows, sgrad, titem, keysA, keysB, valsA, valsB, rowtab, rowcnt, segitem, segspan, geom,
       rowstart, chunkstart, chunkcnt, keysC, chunkinfo, densel, tilecnt, tileord, pitem, lbA, lbB, total;
 };
 
@@ -131,6 +131,7 @@ Layout make_layout(int64_t n_cap, int64_t pair_cap, int W, int H, int sms) {
   L.cam = take(sizeof(CamPair));
   L.recs = take((size_t)n_cap * sizeof(Rec));
   L.recs64 = take((size_t)n_cap * sizeof(Rec64));  // RS_F64 frames
+  L.exptab = take((size_t)kExpTab * sizeof(double));  // blend64's exp table (built at create)
 
   L.rows = take((size_t)n_cap * 4);  // per binned item its tile-row range
   L.sgrad = take((size_t)n_cap * 4 * kSGrad);  // rs_backward: screen-space gradient sums per item
@@ -329,6 +330,7 @@ int32_t rs_workspace_create(void* device_mem, size_t bytes, int64_t n_cap, int64
   cudaGetDevice(&dev);
   if (cudaDeviceGetAttribute(&ws->sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) ws->sms = 148;
   configure_kernels();
+  exp_table_kernel<<<(kExpTab + 255) / 256, 256>>>(ws->at<double>(L.exptab));
   if (cudaMemset(ws->at<Sticky>(L.sticky), 0, sizeof(Sticky)) != cudaSuccess ||
       cudaStreamCreateWithFlags(&ws->aux, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&ws->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
@@ -571,7 +573,7 @@ int32_t rs_blend_ex(rs_workspace* ws, const rs_options* opts, const rs_outputs* 
                       opts->tau_stop >= 0.0;
 #define RS_B64(C, I, K, F) \
   launch(blend64_kernel<C, I, K, F>, T, kBlend64Threads, 0, st, ranges, items, recs, r64, geom, order, ctr, ws->W, \
-         ws->H, ws->TW, op, o64, sc)
+         ws->H, ws->TW, op, o64, sc, ws->at<double>(ws->L.exptab))
 #define RS_B64_F(C, I, K) \
   if (fast) { RS_B64(C, I, K, true); } else { RS_B64(C, I, K, false); }
     if (color && sc) {

@@ -13,7 +13,7 @@
 //
 // Per pixel and Gaussian (render.py:254-281, with fused roundings):
 //   x     = fma(nc dy, dy, fma(nb dy, dx, (na dx) dx))   (= -q/2; (na,nb,nc) = -(ia/2, ib, ic/2))
-//   alpha = min(o exp(min(x, 709)), alpha_max)          (exp64_tab, rs_math.cuh)
+//   alpha = min(o exp(min(x, 709)), alpha_max)          (exp64_tab, rs_math.cuh: 1024-entry table)
 //   if alpha >= alpha_cut and tau >= tau_stop:
 //       w = alpha tau; rgb = fma(c, w, rgb); depth = fma(z, w, depth); count++;
 //       tau = fma(-alpha, tau, tau)
@@ -55,18 +55,24 @@ __global__ void __launch_bounds__(kBlend64Threads, RS_BLEND64_MINB) blend64_kern
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ pair_items, const Rec* __restrict__ recs,
     const Rec64* __restrict__ recs64, const float4* __restrict__ geom, const uint32_t* __restrict__ tile_order,
     Counters* __restrict__ ctr, int W, int H, int TW, Opt64 o, const Out64 out,
-    unsigned long long* __restrict__ scores) {
+    unsigned long long* __restrict__ scores, const double* __restrict__ exp_table) {
   pdl_wait();
   pdl_trigger();
   constexpr int kBatch = 256;
   constexpr int kPerThread = kBatch / kBlend64Threads;
-  constexpr int U = 4;  // list entries per inner iteration
+#ifndef RS_BLEND64_UNROLL_C
+#define RS_BLEND64_UNROLL_C 2  // colour frames (measured 2: 303 us < 4: 332 < 6: 340 at configs[1])
+#endif
+#ifndef RS_BLEND64_UNROLL_S
+#define RS_BLEND64_UNROLL_S 8  // score-only frames (measured 8: 426 us < 6: 435 < 4: 451 < 2: 495)
+#endif
+  constexpr int U = COLOR ? RS_BLEND64_UNROLL_C : RS_BLEND64_UNROLL_S;  // list entries per inner iteration
   __shared__ Rec64 s_rec[kBatch + 1];  // slot kBatch: empty-box sentinel padding the warp lists
   __shared__ unsigned long long s_w[CONTRIB ? kBatch + 1 : 1];
   __shared__ uint8_t s_mask[kBatch];
   __shared__ uint16_t s_boxm[kBatch + 1][4];
   __shared__ uint16_t s_list[4][kBatch + U];
-  __shared__ double s_exp[64];  // exp64_tab's 2^(j/64) table
+  __shared__ double s_exp[kExpTab];  // exp64_tab's 2^(j/1024) table
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int tile = (int)__ldg(tile_order + blockIdx.x);
@@ -88,7 +94,7 @@ __global__ void __launch_bounds__(kBlend64Threads, RS_BLEND64_MINB) blend64_kern
   double r0 = 0.0, g0 = 0.0, b0 = 0.0, d0 = 0.0, r1 = 0.0, g1 = 0.0, b1 = 0.0, d1 = 0.0;
   int cnt0 = 0, cnt1 = 0;
   unsigned long long evals = 0;
-  if (tid < 64) s_exp[tid] = exp64_tab_entry(tid);
+  for (int j = tid; j < kExpTab; j += kBlend64Threads) s_exp[j] = __ldg(exp_table + j);
   if (tid == 0) {
     Rec64 z{};
     s_rec[kBatch] = z;
@@ -308,6 +314,12 @@ __global__ void __launch_bounds__(kBlend64Threads, RS_BLEND64_MINB) blend64_kern
       atomicAdd(&ctr->composites, c);
     }
   }
+}
+
+// exp64_tab's table, built once per workspace (rs_workspace_create)
+__global__ void exp_table_kernel(double* __restrict__ t) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < kExpTab) t[j] = exp64_tab_entry(j);
 }
 
 }  // namespace rs

@@ -141,17 +141,19 @@ __device__ __forceinline__ double exp64_contract(double x) {
   return __dmul_rn(__dmul_rn(p, pow2i64(ni + 600)), pow2i64(-600));  // subnormal range
 }
 
-// e^x for the fp64 blend (oracle: exp64_tab): k = rint(x 64 / ln 2), r = x - k ln2/64
-// (Cody-Waite, |r| <= ln2/128), e^r by its degree-5 Taylor polynomial (truncation
-// < 4e-17), times T[k mod 64] 2^(k div 64) -- T[j] = exp64_contract(j ln2/64), the
-// kernel's shared-memory table; the power of two is added to T's exponent field.
-// FAST: the caller guarantees the result is a normal number (x in [-708, 709]).
-constexpr double kInvLn2x64 = 92.33248261689366;              // 64 / ln 2
-constexpr double kLn2o64Hi = 0.6931471803691238 / 64.0;        // kLn2Hi / 64 (exact)
-constexpr double kLn2o64Lo = 1.9082149292705877e-10 / 64.0;    // kLn2Lo / 64 (exact)
-constexpr double kLn2o64 = 0.6931471805599453 / 64.0;          // table argument step
+// e^x for the fp64 blend (oracle: exp64_tab): k = rint(x 1024 / ln 2), r = x - k ln2/1024
+// (Cody-Waite, |r| <= ln2/2048), e^r by its degree-3 Taylor polynomial (truncation
+// < 6e-16), times T[k mod 1024] 2^(k div 1024) -- T[j] = exp64_contract(j ln2/1024), a
+// table built once per workspace and staged in shared memory; the power of two is
+// added to T's exponent field. FAST: the caller guarantees a normal result (x in [-708, 709]).
+constexpr int kExpTabBits = 10;
+constexpr int kExpTab = 1 << kExpTabBits;
+constexpr double kInvLn2xT = 1477.3197218702985;              // 1024 / ln 2
+constexpr double kLn2oTHi = 0.6931471803691238 / 1024.0;       // kLn2Hi / 1024 (exact)
+constexpr double kLn2oTLo = 1.9082149292705877e-10 / 1024.0;   // kLn2Lo / 1024 (exact)
+constexpr double kLn2oT = 0.6931471805599453 / 1024.0;         // table argument step
 
-__device__ __forceinline__ double exp64_tab_entry(int j) { return exp64_contract((double)j * kLn2o64); }
+__device__ __forceinline__ double exp64_tab_entry(int j) { return exp64_contract((double)j * kLn2oT); }
 
 template <bool FAST>
 __device__ __forceinline__ double exp64_tab(double x, const double* __restrict__ T) {
@@ -160,18 +162,16 @@ __device__ __forceinline__ double exp64_tab(double x, const double* __restrict__
     if (x > 709.782712893384) return __longlong_as_double(0x7ff0000000000000ll);
     if (x < -745.2) return 0.0;
   }
-  const double t = __fma_rn(x, kInvLn2x64, kMagic64);
+  const double t = __fma_rn(x, kInvLn2xT, kMagic64);
   const double kd = __dsub_rn(t, kMagic64);
-  double r = __fma_rn(kd, -kLn2o64Hi, x);
-  r = __fma_rn(kd, -kLn2o64Lo, r);
-  double p = __fma_rn(1.0 / 120.0, r, 1.0 / 24.0);
-  p = __fma_rn(p, r, 1.0 / 6.0);
-  p = __fma_rn(p, r, 0.5);
+  double r = __fma_rn(kd, -kLn2oTHi, x);
+  r = __fma_rn(kd, -kLn2oTLo, r);
+  double p = __fma_rn(1.0 / 6.0, r, 0.5);
   p = __fma_rn(p, r, 1.0);
   p = __fma_rn(p, r, 1.0);
   const int k = __double2loint(t);
-  const int n = k >> 6;  // floor(k / 64)
-  const double tj = T[k & 63];
+  const int n = k >> kExpTabBits;  // floor(k / 1024)
+  const double tj = T[k & (kExpTab - 1)];
   if (FAST || n >= -1022)
     return __dmul_rn(p, __hiloint2double(__double2hiint(tj) + (n << 20), __double2loint(tj)));
   return __dmul_rn(__dmul_rn(p, __hiloint2double(__double2hiint(tj) + ((n + 600) << 20), __double2loint(tj))),

@@ -1,6 +1,6 @@
 """A/B of blend variants on configs[1] frames: project+bin once, then time rs_blend per flag.
 
-    python tools/blend_ab.py [frames]
+    python tools/blend_ab.py [frames] [render|score] [fp32|fp64]
 """
 import ctypes as C
 import sys
@@ -15,18 +15,19 @@ from paper_2403_13806_b200.render import RasterizeOptions  # noqa: E402
 
 frames = int(sys.argv[1]) if len(sys.argv) > 1 else 20
 kind = sys.argv[2] if len(sys.argv) > 2 else "render"
-opts = RasterizeOptions(near_limit=0.2)
+prec = sys.argv[3] if len(sys.argv) > 3 else "fp32"
+opts = RasterizeOptions(near_limit=0.2, precision=prec)
 scene, cams = synth.config1(0) if kind == "render" else synth.config2(0)
 ds = device_scene(scene)
 r = renderer(ds.device)
-out = r.alloc_outputs(cams[0])
-sc = torch.zeros(len(scene), dtype=torch.int32, device=ds.device)
+out = r.alloc_outputs(cams[0], precision=0 if prec == "fp32" else 1)
+sc = torch.zeros(len(scene), dtype=torch.float32 if prec == "fp32" else torch.float64, device=ds.device)
 for f in range(frames):
     r.render(ds, cams[f], opts, out=out, color=kind == "render", scores=None if kind == "render" else sc)
 os_ = options_struct(opts)
 st = torch.cuda.current_stream().cuda_stream
 outs = r.outputs_struct(out) if kind == "render" else N.RsOutputs()
-res = {0: [], N.RS_FLAG_BLEND_1PX: []}
+res = {0: [], N.RS_FLAG_BLEND_1PX: []} if prec == "fp32" else {0: []}
 ref = {}
 for f in range(frames):
     N.check(r.lib.rs_project(r.handle, C.byref(ds.struct), None, 0, C.byref(camera_struct(cams[f])), C.byref(os_), st))
@@ -47,6 +48,7 @@ for f in range(frames):
             else:
                 ref.setdefault((f, flag), sc.clone())
 for f in range(frames):
-    assert torch.equal(ref[(f, 0)], ref[(f, N.RS_FLAG_BLEND_1PX)]), f
+    if prec == "fp32":
+        assert torch.equal(ref[(f, 0)], ref[(f, N.RS_FLAG_BLEND_1PX)]), f
 for flag, v in res.items():
-    print(kind, "2px" if flag == 0 else "1px", f"{1e3 * sum(v) / len(v):.1f} us")
+    print(kind, prec, "2px" if flag == 0 else "1px", f"{1e3 * sum(v) / len(v):.1f} us")
