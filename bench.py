@@ -937,6 +937,41 @@ def run_train(args, ctx):
     fwd = np.array([a.elapsed_time(b) for a, b, _ in ev])
     bwd = np.array([b.elapsed_time(c) for _, b, c in ev])
     t_max = ctx.max_over_ranks(float(fwd.sum() + bwd.sum()))
+    # e2e: a device-resident optimizer step through the public training pair --
+    # rasterize_cached(device_outputs) -> L2 loss on the device -> rasterize_backward(device)
+    # -> in-place SGD on the parameter planes; per step the camera goes up, the loss comes down
+    from paper_2403_13806_b200.device import DeviceScene
+    from paper_2403_13806_b200.render import rasterize_backward, rasterize_cached
+    pl, shp = ds.planes.clone(), ds.sh.clone()
+    dsp = DeviceScene.from_tensors(pl, shp, ds.sh_degree, check_finite=False)
+    target = torch.zeros((H_, W_, 3), dtype=torch.float32, device=dev)
+
+    def opt_step(cam):
+        img, cache = rasterize_cached(dsp, cam, opts, device_outputs=True)
+        diff = img["rgb"] - target
+        loss = (diff * diff).mean()
+        gr = rasterize_backward(dsp, cam, cache, diff * (2.0 / diff.numel()), device=True)
+        with torch.no_grad():
+            pl[0:3] -= 1e-4 * gr["positions"].T
+            pl[3] -= 1e-4 * gr["opacity_logits"]
+            pl[4:7] -= 1e-4 * gr["log_scales"].T
+            pl[7:11] -= 1e-4 * gr["quaternions"].T
+            shp.sub_(1e-4 * gr["sh"].reshape(-1, 48))
+        return float(loss.item())
+
+    ke = min(args.steps, 30)
+    for s in range(2):
+        opt_step(frames(s))
+    ctx.barrier()
+    t0 = time.perf_counter()
+    for s in range(ke):
+        opt_step(frames(s))
+    ctx.barrier()
+    te = ctx.max_over_ranks(time.perf_counter() - t0)
+    e2e = {"value": ctx.world * ke / te, "unit": "views/s",
+           "h2d_bytes_per_step": C.sizeof(N.RsCamera) + C.sizeof(N.RsOptions), "d2h_bytes_per_step": 4,
+           "api": "render.rasterize_cached(device_outputs=True) + rasterize_backward(device=True) + in-place "
+                  "SGD on DeviceScene.from_tensors parameters (one optimizer step per view)"}
     return {
         "metric": METRIC_TRAIN, "value": ctx.world * args.steps / (t_max / 1e3), "unit": "views/s",
         "n_gpus": ctx.world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps,
@@ -945,6 +980,7 @@ def run_train(args, ctx):
         "config": make_config("train", n, W_, H_, ctx.world),
         "stages_ms": {"forward_with_cache": float(fwd.mean()), "backward": float(bwd.mean())},
         "gpu_launches": args.steps * (frame_launches(n, False) + 2), "clocks": clk.summary(),
+        "e2e": e2e,
     }
 
 

@@ -256,6 +256,11 @@ class Renderer:
             raise InvalidParameterError("active index list holds an index outside the scene")
         return bool(o.value), int(p.value)
 
+    def clear_sticky(self) -> None:
+        o, p, b = C.c_uint32(), C.c_uint64(), C.c_uint32()
+        N.check(self.lib.rs_read_sticky(self.handle, C.byref(o), C.byref(p), C.byref(b), 1, self.stream),
+                "read_sticky")
+
     def buffers(self) -> N.RsBuffers:
         b = N.RsBuffers()
         N.check(self.lib.rs_get_buffers(self.handle, C.byref(b)), "get_buffers")
@@ -334,6 +339,7 @@ class Renderer:
             self.launch(ds, cam_s, opt_s, out, scores, active_idx, items, flags)
             st = self.stats()
             if st.bad_index:
+                self.clear_sticky()  # reported here: later passes must not re-raise it
                 raise InvalidParameterError("active index list holds an index outside the scene")
             if not st.overflow:
                 return out, st
@@ -390,6 +396,7 @@ class Renderer:
                                          C.byref(options_struct(opts)), full.data_ptr(), bbox.data_ptr(),
                                          self.stream), "project_full")
         if self.stats().bad_index:
+            self.clear_sticky()
             raise InvalidParameterError("active index list holds an index outside the scene")
         return full[:ds.n].cpu().numpy(), bbox[:ds.n].cpu().numpy()
 

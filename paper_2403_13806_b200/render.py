@@ -197,13 +197,22 @@ def _training_forward(ds: DeviceScene, camera, options, active_idx=None):
     return out, r.frame_id
 
 
-def rasterize_cached(scene, camera, options: RasterizeOptions = RasterizeOptions()):
+def rasterize_cached(scene, camera, options: RasterizeOptions = RasterizeOptions(), *,
+                     device_outputs: bool = False):
     """Forward render keeping what the backward pass needs (render.py:318-321):
     returns (RenderOutput, cache). The cache holds, on the device, the per-pixel
     final transmittance and last composite; the binning stays in the workspace.
-    The training pair runs on the fp32 path (fp32 scene storage)."""
+    The training pair runs on the fp32 path (fp32 scene storage).
+
+    ``device_outputs=True`` (a device-resident training loop: the scene a
+    ``DeviceScene.from_tensors`` over parameter tensors updated in place, the loss
+    on the device) returns the device images dict (rgb, alpha, depth, count)
+    instead of host arrays."""
     ds = _fp32_scene(scene)
     out, frame = _training_forward(ds, camera, options)
+    if device_outputs:
+        return {k: out[k] for k in ("rgb", "alpha", "depth", "count")}, \
+            dict(options=options, device_out=out, frame=frame, camera=camera)
     H, W = int(camera.height), int(camera.width)
     res = RenderOutput(color=ImageBuffer.trusted(out["rgb"].double().cpu().numpy().reshape(H, W, 3)),
                        alpha=out["alpha"].double().cpu().numpy(), count=out["count"].long().cpu().numpy(),
@@ -211,12 +220,17 @@ def rasterize_cached(scene, camera, options: RasterizeOptions = RasterizeOptions
     return res, dict(options=options, device_out=out, frame=frame, camera=camera)
 
 
-def rasterize_backward(scene, camera, cache: dict, grad_image) -> dict:
+def rasterize_backward(scene, camera, cache: dict, grad_image, *, device: bool = False) -> dict:
     """Analytic gradients of a scalar loss through the rendered image
     (render.py:328-394 + _chain_to_parameters :397-487). ``grad_image`` =
     dL/d(colour image), (H, W, 3). Returns float64 gradients w.r.t. positions,
     sh, log_scales, quaternions, opacity_logits, plus ``mean2d_grad_norm`` and
-    ``touched`` -- the reference's dict, computed by rs_backward in fp32."""
+    ``touched`` -- the reference's dict, computed by rs_backward in fp32.
+
+    ``device=True``: ``grad_image`` may be a CUDA tensor (used in place) and the
+    gradients stay on the device as fp32 tensors (positions (n,3), sh (n,3,16),
+    log_scales (n,3), quaternions (n,4), opacity_logits, mean2d_grad_norm, touched)
+    -- no host round trip per optimizer step."""
     ds = _fp32_scene(scene)
     r = renderer(ds.device)
     options = fp32_options(cache["options"])
@@ -225,11 +239,16 @@ def rasterize_backward(scene, camera, cache: dict, grad_image) -> dict:
         out, cache["frame"] = _training_forward(ds, camera, options)
         cache["device_out"] = out
     H, W = int(camera.height), int(camera.width)
-    g = np.asarray(grad_image, dtype=np.float32)
-    if g.shape != (H, W, 3):
-        raise InvalidParameterError(f"grad_image must be ({H}, {W}, 3)")
     dev = ds.device
-    grad = torch.from_numpy(np.ascontiguousarray(g)).to(dev)
+    if isinstance(grad_image, torch.Tensor):
+        grad = grad_image.to(device=dev, dtype=torch.float32).contiguous()
+        if tuple(grad.shape) != (H, W, 3):
+            raise InvalidParameterError(f"grad_image must be ({H}, {W}, 3)")
+    else:
+        g = np.asarray(grad_image, dtype=np.float32)
+        if g.shape != (H, W, 3):
+            raise InvalidParameterError(f"grad_image must be ({H}, {W}, 3)")
+        grad = torch.from_numpy(np.ascontiguousarray(g)).to(dev)
     n = max(ds.n, 1)
     o = dict(positions=torch.empty((n, 3), device=dev), sh=torch.empty((n, 48), device=dev),
              log_scales=torch.empty((n, 3), device=dev), quaternions=torch.empty((n, 4), device=dev),
@@ -240,6 +259,11 @@ def rasterize_backward(scene, camera, cache: dict, grad_image) -> dict:
                               *(o[k].data_ptr() for k in ("positions", "sh", "log_scales", "quaternions",
                                                          "opacity_logits", "mean2d_grad_norm", "touched")),
                               r.stream), "backward")
+    if device:
+        o = {k: v[:ds.n] for k, v in o.items()}
+        o["sh"] = o["sh"].view(ds.n, 3, 16)
+        o["touched"] = o["touched"].bool()
+        return o
     res = {k: v[:ds.n].cpu().numpy() for k, v in o.items()}
     grads = {k: res[k].astype(np.float64) for k in ("positions", "log_scales", "quaternions", "opacity_logits",
                                                   "mean2d_grad_norm")}

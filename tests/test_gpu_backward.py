@@ -58,3 +58,41 @@ def test_backward_after_other_frames_recomputes_the_forward():
     g2 = rasterize_backward(scene, cam, cache, d[p + "w"])
     for k in KEYS:
         assert np.allclose(g1[k], g2[k], rtol=1e-5, atol=1e-6)
+
+
+def test_device_resident_training_step():
+    """The optimizer's scene as device tensors updated in place (DeviceScene.from_tensors):
+    forward with device outputs, backward with a device dL/dimage and device gradients --
+    the same gradients as the host path, and an in-place parameter update is what the
+    next forward renders (optim.py:336-399 without a host round trip per step)."""
+    import torch
+
+    from paper_2403_13806_b200.device import DeviceScene, pack_planes, pack_sh
+    from paper_2403_13806_b200.render import RasterizeOptions, rasterize_backward, rasterize_cached, render_device
+    from paper_2403_13806_b200.synth import config0
+    scene, cams = config0(0)
+    cam = cams[0]
+    opts = RasterizeOptions(near_limit=0.2, precision="fp32")
+    planes = torch.from_numpy(pack_planes(scene)).cuda()
+    sh = torch.from_numpy(pack_sh(scene)).cuda()
+    ds = DeviceScene.from_tensors(planes, sh, scene.active_sh_degree)
+    img, cache = rasterize_cached(ds, cam, opts, device_outputs=True)
+    target = torch.zeros_like(img["rgb"])
+    gimg = 2.0 * (img["rgb"] - target) / img["rgb"].numel()
+    gd = rasterize_backward(ds, cam, cache, gimg, device=True)
+    host_img, hcache = rasterize_cached(scene, cam, opts)
+    gh = rasterize_backward(scene, cam, hcache, gimg.cpu().numpy())
+    for k in ("positions", "log_scales", "quaternions", "opacity_logits", "mean2d_grad_norm", "sh"):
+        got, ref = gd[k].cpu().numpy().astype(np.float64), gh[k]  # float atomics: order-dependent sums
+        assert np.abs(got - ref).max() <= 1e-5 * np.abs(ref).max() + 1e-12, k
+    assert np.array_equal(gd["touched"].cpu().numpy(), gh["touched"])
+    # in-place SGD step on the device parameters, then the next forward sees it
+    with torch.no_grad():
+        planes[0:3] -= 0.5 * gd["positions"].T
+        planes[3] -= 0.5 * gd["opacity_logits"]
+    img2, _ = render_device(ds, cam, opts)
+    upd = type(scene)(planes[0:3].T.cpu().numpy().copy(), planes[3].cpu().numpy().copy(), scene.sh,
+                      scene.log_scales, scene.quaternions, scene.active_sh_degree)
+    ref, _ = render_device(upd, cam, opts)
+    assert torch.equal(img2["rgb"], ref["rgb"])
+    assert not torch.equal(img2["rgb"], img["rgb"])

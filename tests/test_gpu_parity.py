@@ -307,3 +307,33 @@ def test_score_views_overflow_recovery_matches_per_view_renders(prec):
     over, _ = r.read_overflow()
     assert not over
     r.close()
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
+def test_out_of_range_active_index_rejected(prec):
+    """An index list with an entry outside [0, n) is reported by the device
+    (rs_stats.bad_index / rs_read_sticky) and raised as InvalidParameterError, the
+    reference's error for a bad active mask (render.py:231-234); the bad entries are never
+    read."""
+    from paper_2403_13806_b200.core import InvalidParameterError
+    from paper_2403_13806_b200.device import camera_struct, device_scene, options_struct, renderer
+    from paper_2403_13806_b200.render import RasterizeOptions, render_device
+    s, cam, _ = load_case(golden("suite50"), "c3_")
+    ds = device_scene(s)
+    opts = RasterizeOptions(precision=prec)
+    for bad in ([0, len(s)], [-1], [0, 1, 2 ** 30]):
+        idx = torch.tensor(bad, dtype=torch.int32, device=ds.device)
+        with pytest.raises(InvalidParameterError):
+            render_device(ds, cam, opts, active_idx=idx)
+    # the scoring pass's sticky record too
+    r = renderer(ds.device)
+    r.read_overflow(reset=True)
+    vt = torch.float32 if prec == "fp32" else torch.float64
+    sc = torch.zeros(len(s), dtype=vt, device=ds.device)
+    r.launch(ds, camera_struct(cam), options_struct(opts), {}, sc,
+             torch.tensor([len(s)], dtype=torch.int32, device=ds.device), 1)
+    with pytest.raises(InvalidParameterError):
+        r.read_overflow(reset=True)
+    # a valid list still renders after the errors
+    out, st = render_device(ds, cam, opts, active_idx=torch.arange(len(s), dtype=torch.int32, device=ds.device))
+    assert st.bad_index == 0

@@ -273,3 +273,22 @@ def test_nearest_clusters_device_batch_matches_reference_rule():
     assert np.array_equal(got, ref)
     assert np.array_equal(got, [vis.nearest_cluster(-c.rotation.T @ c.translation) for c in cams])
     assert got[300] == 2 and got[301] == 2
+
+
+@PREC
+def test_config4_full_frame_bit_exact(prec, tier):
+    """A full-size configs[4] view (1M heavy-tailed Gaussians, 1920x1080, ~150M tile pairs)
+    equals the oracle bit for bit: image, counts, scores, E and C."""
+    from oracle import oracle as O
+    from paper_2403_13806_b200.render import RasterizeOptions, render_device
+    from paper_2403_13806_b200.synth import config4
+    scene, cams = config4(0, n=1_000_000, n_views=512)
+    opts = RasterizeOptions(near_limit=0.2, precision=prec)
+    sc = torch.zeros(len(scene), dtype=_vt(prec), device="cuda")
+    out, st = render_device(scene, cams[0], opts, scores=sc, count_evals=True)
+    assert st.n_pairs > 100_000_000
+    ref = O.views(scene, [cams[0]], opts, tier, scores=True, images=True)
+    assert np.array_equal(out["rgb"].cpu().numpy(), ref["img_last"])
+    assert np.array_equal(sc.cpu().numpy(), ref["contrib"])
+    assert st.evals == ref["E"] and st.composites == ref["C"]
+    assert int(out["count"].sum()) == ref["C"]
