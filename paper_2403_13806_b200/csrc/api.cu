@@ -570,7 +570,7 @@ int32_t rs_blend_ex(rs_workspace* ws, const rs_options* opts, const rs_outputs* 
     auto* sc = static_cast<unsigned long long*>(scores_v);
     // exp64_tab's normal range and non-negative thresholds (integer compares, blend64.cuh)
     const bool fast = opts->alpha_cut >= 1e-300 && opts->alpha_max >= 0.0 && opts->alpha_max <= 1e300 &&
-                      opts->tau_stop >= 0.0;
+                      opts->tau_stop >= 0.0 && opts->lowpass >= 0.0;
 #define RS_B64(C, I, K, F) \
   launch(blend64_kernel<C, I, K, F>, T, kBlend64Threads, 0, st, ranges, items, recs, r64, geom, order, ctr, ws->W, \
          ws->H, ws->TW, op, o64, sc, ws->at<double>(ws->L.exptab))

@@ -20,7 +20,7 @@
 // x < lnc (a conservative per-Gaussian bound) proves alpha < alpha_cut. A pixel
 // that does not composite takes alpha = 0 (w = +0, fma(c, 0, rgb) = rgb, tau
 // unchanged: exactly the skipped composite), so the loop has no branches. With
-// FAST (alpha_cut >= 1e-300, alpha_max and tau_stop >= 0) the threshold tests are
+// FAST (alpha_cut >= 1e-300, alpha_max and tau_stop >= 0, lowpass >= 0) the threshold tests are
 // integer compares of the fp64 bit patterns (the thresholds are non-negative, so
 // the signed order of the bits is the value order) -- the FP64 pipe is the
 // kernel's bound. Importance: the warp maximum of w's fp64 bits (two REDUX
@@ -178,7 +178,9 @@ __global__ void __launch_bounds__(kBlend64Threads, RS_BLEND64_MINB) blend64_kern
           const double x1 = __fma_rn(E.nc * dy1, dy1, __fma_rn(E.nb * dy1, dx, qa));
           const bool e0 = bx0[u] && x0 >= E.lnc, e1 = bx1[u] && x1 >= E.lnc;
           // evaluated for every lane (the values of skipped pixels are discarded)
-          const double xc0 = gt_nn(x0, 709.0) ? 709.0 : x0, xc1 = gt_nn(x1, 709.0) ? 709.0 : x1;
+          // the contract clamps the exp argument at 709; with FAST (lowpass >= 0: the conic is
+          // positive definite, -q/2 <= 0 up to rounding) the clamp never binds
+          const double xc0 = FAST ? x0 : (x0 > 709.0 ? 709.0 : x0), xc1 = FAST ? x1 : (x1 > 709.0 ? 709.0 : x1);
           const double raw0 = E.o * exp64_tab<FAST>(xc0, s_exp), raw1 = E.o * exp64_tab<FAST>(xc1, s_exp);
           double a0, a1;
           if (FAST) {
