@@ -89,7 +89,7 @@ constexpr int kMaxDsortCtas = 160;  // cooperative depth sort: one CTA per SM (c
 
 struct Layout {
   // per-frame zeroed region [0, frame_bytes)
-  size_t ctr, hist, proj_lb, ranges, frame_bytes;
+  size_t ctr, hist, proj_lb, ranges, scancls, scanpart, frame_bytes;
   size_t sticky, cam, recs, recs64, exptab, dtab, rows, sgrad, titem, keysA, keysB, valsA, valsB, rowtab, rowcnt, segitem, segspan, geom,
       rowstart, chunkstart, chunkcnt, keysC, chunkinfo, densel, tilecnt, tileord, pitem, lbA, lbB, total;
 };
@@ -126,6 +126,8 @@ Layout make_layout(int64_t n_cap, int64_t pair_cap, int W, int H, int sms) {
   L.proj_lb = take(((size_t)n_cap / kCompactKeys + 2) * sizeof(unsigned long long));
   L.ranges = take(TW * TH * sizeof(uint2));
   L.dtab = take((size_t)4 * std::min(sms, kMaxDsortCtas) * 256 * 4);  // dsort_kernel's per-pass digit tables
+  L.scancls = take(2 * kScanClasses * 4);  // tile scan: list-length class counts and cursors
+  L.scanpart = take(((size_t)TW * TH / kScanTiles + 1) * 8);  // tile scan: 64-tile block sums
   L.frame_bytes = o;
   L.sticky = take(sizeof(Sticky));
   L.cam = take(sizeof(CamPair));
@@ -493,6 +495,11 @@ int32_t rs_bin(rs_workspace* ws, void* stream) {
     const uint32_t seg_cap = (uint32_t)seg_capacity(ws->n_cap, ws->pair_cap);
     const uint32_t tab_stride = (uint32_t)rowtab_stride(ws->n_cap);
     const unsigned rc = (n + kRankChunk - 1) / kRankChunk;
+    const unsigned gx = (unsigned)std::min<int64_t>(seg_cap / kExpandChunk + ws->TH + 1, (int64_t)ws->sms * 16);
+    // expansion: the sparse chunks grid-strided (column groups x chunk slots), the dense ones on
+    // persistent ticketed CTAs on the workspace's second stream, concurrently
+    const dim3 eg((ws->TW + kExpandCols - 1) / kExpandCols, gx), dg(ws->sms * 6);
+    const int T = ws->TW * ws->TH;
     launch(segrows_kernel, rc, 256, 0, st, items_sorted, ws->at<uint32_t>(ws->L.rows), ctr, ws->TH, tab_stride,
            ws->at<uint32_t>(ws->L.rowtab));
     launch(segscan_kernel, ws->TH, 256, 0, st, ws->at<uint32_t>(ws->L.rowtab), tab_stride, ctr, ws->TH, seg_cap,
@@ -501,19 +508,16 @@ int32_t rs_bin(rs_workspace* ws, void* stream) {
     launch(segplace_kernel, rc, 256, 64 * ws->TH, st, items_sorted, ws->at<Rec>(ws->L.recs), ctr, ws->TH,
            ws->at<uint32_t>(ws->L.rowtab), tab_stride, ws->at<uint32_t>(ws->L.rowstart),
            ws->at<uint32_t>(ws->L.segitem), ws->at<uint32_t>(ws->L.segspan), ws->at<float4>(ws->L.geom));
-    const unsigned gx = (unsigned)std::min<int64_t>(seg_cap / kExpandChunk + ws->TH + 1, (int64_t)ws->sms * 16);
-    // expansion: the sparse chunks grid-strided (column groups x chunk slots), the dense ones on
-    // persistent ticketed CTAs on the workspace's second stream, concurrently
-    const dim3 eg((ws->TW + kExpandCols - 1) / kExpandCols, gx), dg(ws->sms * 6);
     launch(chunk_count_kernel, gx, 256, 0, st, ws->at<uint32_t>(ws->L.segspan),
            ws->at<uint32_t>(ws->L.rowstart), ws->at<uint32_t>(ws->L.chunkstart), ws->TH, ws->TW,
            ws->at<uint32_t>(ws->L.chunkcnt), ws->at<uint2>(ws->L.chunkinfo), expand_dense_span(), ctr,
            ws->at<uint32_t>(ws->L.densel));
-    const int T = ws->TW * ws->TH;
     launch(tile_chunks_kernel, (T + 7) / 8, 256, 0, st, ws->at<uint32_t>(ws->L.chunkstart), ws->TH, ws->TW,
-           ws->at<uint32_t>(ws->L.chunkcnt), ws->at<uint32_t>(ws->L.tilecnt));
-    launch(tile_scan_kernel, 1, 1024, 0, st, ws->at<uint32_t>(ws->L.tilecnt), T, ctr, (uint32_t)ws->pair_cap,
-           ws->at<uint2>(ws->L.ranges), ws->at<Sticky>(ws->L.sticky), ws->at<uint32_t>(ws->L.tileord));
+           ws->at<uint32_t>(ws->L.chunkcnt), ws->at<uint32_t>(ws->L.tilecnt),
+           ws->at<unsigned long long>(ws->L.scanpart), ws->at<uint32_t>(ws->L.scancls));
+    launch(tile_scan_kernel, (T + kScanTiles - 1) / kScanTiles, kScanTiles, 0, st, ws->at<uint32_t>(ws->L.tilecnt), T,
+           ctr, (uint32_t)ws->pair_cap, ws->at<uint2>(ws->L.ranges), ws->at<Sticky>(ws->L.sticky),
+           ws->at<uint32_t>(ws->L.tileord), ws->at<unsigned long long>(ws->L.scanpart), ws->at<uint32_t>(ws->L.scancls));
     cudaEventRecord(ws->ev_fork, st);
     cudaStreamWaitEvent(ws->aux, ws->ev_fork, 0);
     g_pdl_class = kPdlExpand;

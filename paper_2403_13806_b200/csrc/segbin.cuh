@@ -20,9 +20,11 @@
 //                    chunk's segments covering it (shared-memory counters);
 //                    the chunk's {first segment, row, count, dense} record and
 //                    the list of dense chunks (>= 8 tiles per segment).
-//   tile_chunks_kernel / tile_scan_kernel  per tile: prefix over its row's
-//                    chunks and its total; exclusive scan over the tiles ->
-//                    ranges [start, end), P, overflow, the blend order.
+//   tile_chunks_kernel  per tile (one warp): prefix over its row's chunks and
+//                    its total; per 64-tile block the sum and list-length class
+//                    counts (atomics).
+//   tile_scan_kernel one CTA per 64-tile block: exclusive scan over the tiles
+//                    -> ranges [start, end), P, overflow, the blend order.
 //   expand_kernel    sparse chunks x 32-column groups: per warp 32 segments'
 //                    column masks, transposed (lane = column), each column's
 //                    covering items appended at its rank.
@@ -51,17 +53,12 @@ __device__ __forceinline__ void box_rows(const int4 cb, int& r0, int& r1) {
 
 // Pass 1: per rank chunk (256 consecutive depth ranks) the number of its Gaussians in each tile
 // row (a per-CTA difference array over the rows), stored row-major: row_tab[ty][chunk].
-__global__ void __launch_bounds__(256) segrows_kernel(const uint32_t* __restrict__ items_sorted,
-                                                      const uint32_t* __restrict__ item_rows,
-                                                      const Counters* __restrict__ ctr, int TH, uint32_t tab_stride,
-                                                      uint32_t* __restrict__ row_tab) {
-  pdl_wait();
-  pdl_trigger();
+__device__ __forceinline__ void segrows_block(uint32_t c, const uint32_t* items_sorted,
+                                              const uint32_t* item_rows, uint32_t nvis, int TH,
+                                              uint32_t tab_stride, uint32_t* row_tab) {
   __shared__ int s_d[kMaxTileRows + 1];
   __shared__ uint32_t s_w[8];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t nvis = ctr->n_visible;
-  const uint32_t c = blockIdx.x;
   if (c * kRankChunk >= nvis) return;
   for (int i = tid; i <= TH; i += 256) s_d[i] = 0;
   __syncthreads();
@@ -101,6 +98,15 @@ __global__ void __launch_bounds__(256) segrows_kernel(const uint32_t* __restrict
     run += v[q];
     if (ty < TH) row_tab[(size_t)ty * tab_stride + c] = (uint32_t)run;
   }
+}
+
+__global__ void __launch_bounds__(256) segrows_kernel(const uint32_t* __restrict__ items_sorted,
+                                                      const uint32_t* __restrict__ item_rows,
+                                                      const Counters* __restrict__ ctr, int TH, uint32_t tab_stride,
+                                                      uint32_t* __restrict__ row_tab) {
+  pdl_wait();
+  pdl_trigger();
+  segrows_block(blockIdx.x, items_sorted, item_rows, ctr->n_visible, TH, tab_stride, row_tab);
 }
 
 // Per-row segment starts and chunk starts (chunks of kExpandChunk segments) of TH <= 2048 rows:
@@ -158,18 +164,12 @@ __device__ __forceinline__ void row_scan_block(const uint32_t* row_count, int TH
 // Pass 2, one CTA per tile row: exclusive prefix of the row's chunk counts (in place) and the
 // row's total. The last CTA: per-row segment starts, expansion chunk starts, S and the
 // segment-capacity verdict.
-__global__ void __launch_bounds__(256) segscan_kernel(uint32_t* __restrict__ row_tab, uint32_t tab_stride,
-                                                      Counters* __restrict__ ctr, int TH, uint32_t seg_cap,
-                                                      uint32_t* __restrict__ row_total,
-                                                      uint32_t* __restrict__ row_start,
-                                                      uint32_t* __restrict__ chunk_start,
-                                                      Sticky* __restrict__ sticky) {
-  pdl_wait();
-  pdl_trigger();
-  __shared__ uint32_t s_w[16], s_last;
+__device__ __forceinline__ void segscan_row(uint32_t ty, uint32_t* row_tab, uint32_t tab_stride,
+                                            uint32_t nvis, uint32_t* row_total) {
+  __shared__ uint32_t s_w[8];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t nc = (ctr->n_visible + kRankChunk - 1) / kRankChunk;
-  uint32_t* tab = row_tab + (size_t)blockIdx.x * tab_stride;
+  const uint32_t nc = (nvis + kRankChunk - 1) / kRankChunk;
+  uint32_t* tab = row_tab + (size_t)ty * tab_stride;
   uint32_t carry = 0;
   constexpr int kPer = 4;
   for (uint32_t base = 0; base < nc; base += 256 * kPer) {
@@ -203,13 +203,17 @@ __global__ void __launch_bounds__(256) segscan_kernel(uint32_t* __restrict__ row
     }
     carry += tot;
   }
-  if (tid == 0) row_total[blockIdx.x] = carry;
-  __threadfence();
+  if (tid == 0) row_total[ty] = carry;
   __syncthreads();
-  if (tid == 0) s_last = atomicAdd(&ctr->emit_done, 1u) == gridDim.x - 1;
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
+}
+
+// The row totals -> per-row segment starts, expansion chunk starts, S and the
+// segment-capacity verdict (one CTA, after every row's total is written).
+__device__ __forceinline__ void segscan_tail(Counters* ctr, int TH, uint32_t seg_cap,
+                                             const uint32_t* row_total, uint32_t* row_start,
+                                             uint32_t* chunk_start, Sticky* sticky) {
+  __shared__ uint32_t s_w[16];
+  const int tid = threadIdx.x;
   row_scan_block(row_total, TH, row_start, chunk_start, s_w);
   const uint32_t S = __ldcg(row_start + TH);
   if (S > seg_cap)  // nothing is placed: no chunks for the later passes either
@@ -227,6 +231,28 @@ __global__ void __launch_bounds__(256) segscan_kernel(uint32_t* __restrict__ row
       atomicMax(&sticky->pairs_needed_max, (unsigned long long)S);
     }
   }
+  __syncthreads();
+}
+
+// Pass 2, one CTA per tile row: exclusive prefix of the row's chunk counts (in place) and the
+// row's total. The last CTA: per-row segment starts, expansion chunk starts, S and the
+// segment-capacity verdict.
+__global__ void __launch_bounds__(256) segscan_kernel(uint32_t* __restrict__ row_tab, uint32_t tab_stride,
+                                                      Counters* __restrict__ ctr, int TH, uint32_t seg_cap,
+                                                      uint32_t* __restrict__ row_total,
+                                                      uint32_t* __restrict__ row_start,
+                                                      uint32_t* __restrict__ chunk_start,
+                                                      Sticky* __restrict__ sticky) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ uint32_t s_last;
+  segscan_row(blockIdx.x, row_tab, tab_stride, ctr->n_visible, row_total);
+  __threadfence();
+  if (threadIdx.x == 0) s_last = atomicAdd(&ctr->emit_done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  segscan_tail(ctr, TH, seg_cap, row_total, row_start, chunk_start, sticky);
 }
 
 // Pass 3, one CTA per rank chunk: every segment written straight to its place in row-major,
@@ -234,14 +260,12 @@ __global__ void __launch_bounds__(256) segscan_kernel(uint32_t* __restrict__ row
 // earlier warps' (a per-row ballot per warp) + the earlier lanes'. The rows of the warp's
 // Gaussians are flattened over the lanes for the span computation (row_span, rows.cuh).
 // Dynamic shared memory: per warp and row the ballot and the offset (2 x 8 x TH words).
-__global__ void __launch_bounds__(256) segplace_kernel(const uint32_t* __restrict__ items_sorted,
-                                                       const Rec* __restrict__ recs, const Counters* __restrict__ ctr,
-                                                       int TH, const uint32_t* __restrict__ row_tab,
-                                                       uint32_t tab_stride, const uint32_t* __restrict__ row_start,
-                                                       uint32_t* __restrict__ seg_item,
-                                                       uint32_t* __restrict__ seg_span, float4* __restrict__ geom) {
-  pdl_wait();
-  pdl_trigger();
+__device__ __forceinline__ void segplace_block(uint32_t c, const uint32_t* items_sorted,
+                                               const Rec* recs, uint32_t nvis, int TH,
+                                               const uint32_t* row_tab, uint32_t tab_stride,
+                                               const uint32_t* row_start,
+                                               uint32_t* seg_item, uint32_t* seg_span,
+                                               float4* geom) {
   extern __shared__ uint32_t s_dyn[];
   uint32_t* s_bal = s_dyn;           // [8][TH]
   uint32_t* s_off = s_dyn + 8 * TH;  // [8][TH]
@@ -249,9 +273,7 @@ __global__ void __launch_bounds__(256) segplace_kernel(const uint32_t* __restric
   __shared__ int4 s_cb[8][32];
   __shared__ int s_pre[8][33];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t nvis = ctr->n_visible;
-  const uint32_t c = blockIdx.x;
-  if (c * kRankChunk >= nvis || ctr->overflow) return;
+  if (c * kRankChunk >= nvis) return;
   const uint32_t r = c * kRankChunk + tid;
   int r0 = 0x7fffffff, r1 = -1, nr = 0;
   uint32_t it = 0;
@@ -328,6 +350,20 @@ __global__ void __launch_bounds__(256) segplace_kernel(const uint32_t* __restric
       seg_span[pos] = ok ? ((uint32_t)t0 | ((uint32_t)t1 << 16)) : kEmptySpan;
     }
   }
+  __syncthreads();  // shared memory reuse by the caller's next block
+}
+
+__global__ void __launch_bounds__(256) segplace_kernel(const uint32_t* __restrict__ items_sorted,
+                                                       const Rec* __restrict__ recs, const Counters* __restrict__ ctr,
+                                                       int TH, const uint32_t* __restrict__ row_tab,
+                                                       uint32_t tab_stride, const uint32_t* __restrict__ row_start,
+                                                       uint32_t* __restrict__ seg_item,
+                                                       uint32_t* __restrict__ seg_span, float4* __restrict__ geom) {
+  pdl_wait();
+  pdl_trigger();
+  if (ctr->overflow) return;
+  segplace_block(blockIdx.x, items_sorted, recs, ctr->n_visible, TH, row_tab, tab_stride, row_start, seg_item,
+                 seg_span, geom);
 }
 
 // (chunk, 32 columns) of a row: which row / which of its chunks (binary search over chunk starts)
@@ -568,19 +604,17 @@ __global__ void __launch_bounds__(256) expand_dense_kernel(const uint32_t* __res
 
 // Expansion counts (order-free): per (chunk, tile column) the number of the chunk's segments
 // covering the column -- shared-memory counters over all the row's columns, one CTA per chunk.
-__global__ void __launch_bounds__(256) chunk_count_kernel(const uint32_t* __restrict__ seg_span,
-                                                          const uint32_t* __restrict__ row_start,
-                                                          const uint32_t* __restrict__ chunk_start, int TH, int TW,
-                                                          uint32_t* __restrict__ chunk_count,
-                                                          uint2* __restrict__ chunk_info, int dense_span,
-                                                          Counters* __restrict__ ctr,
-                                                          uint32_t* __restrict__ dense_list) {
-  pdl_wait();
-  pdl_trigger();
+__device__ __forceinline__ void chunk_count_loop(uint32_t first, uint32_t stride,
+                                                 const uint32_t* seg_span,
+                                                 const uint32_t* row_start,
+                                                 const uint32_t* chunk_start, int TH, int TW,
+                                                 uint32_t* chunk_count,
+                                                 uint2* chunk_info, int dense_span,
+                                                 Counters* ctr, uint32_t* dense_list) {
   __shared__ uint32_t s_cnt[kMaxTileCols];
   __shared__ uint32_t s_tiles;
   const int tid = threadIdx.x;
-  for (uint32_t gc = blockIdx.x;; gc += gridDim.x) {
+  for (uint32_t gc = first;; gc += stride) {
     int ty;
     uint32_t lc;
     if (!chunk_of(chunk_start, TH, gc, ty, lc)) break;
@@ -607,18 +641,30 @@ __global__ void __launch_bounds__(256) chunk_count_kernel(const uint32_t* __rest
     }
     for (int c = tid; c < TW; c += 256) chunk_count[(size_t)gc * TW + c] = s_cnt[c];
   }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) chunk_count_kernel(const uint32_t* __restrict__ seg_span,
+                                                          const uint32_t* __restrict__ row_start,
+                                                          const uint32_t* __restrict__ chunk_start, int TH, int TW,
+                                                          uint32_t* __restrict__ chunk_count,
+                                                          uint2* __restrict__ chunk_info, int dense_span,
+                                                          Counters* __restrict__ ctr,
+                                                          uint32_t* __restrict__ dense_list) {
+  pdl_wait();
+  pdl_trigger();
+  chunk_count_loop(blockIdx.x, gridDim.x, seg_span, row_start, chunk_start, TH, TW, chunk_count, chunk_info,
+                   dense_span, ctr, dense_list);
 }
 
 // Per tile: its chunks' counts -> exclusive prefix over the row's chunks (in place) and the
 // tile's total (one warp per tile, 32 chunks per scan step).
-__global__ void __launch_bounds__(256) tile_chunks_kernel(const uint32_t* __restrict__ chunk_start, int TH, int TW,
-                                                          uint32_t* __restrict__ chunk_count,
-                                                          uint32_t* __restrict__ tile_count) {
-  pdl_wait();
-  pdl_trigger();
+__device__ __forceinline__ uint32_t tile_chunks_block(uint32_t vb, const uint32_t* chunk_start, int TH,
+                                                      int TW, uint32_t* chunk_count,
+                                                      uint32_t* tile_count) {
   const int lane = threadIdx.x & 31;
-  const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (t >= TW * TH) return;
+  const int t = (int)vb * 8 + (threadIdx.x >> 5);
+  if (t >= TW * TH) return 0;
   const int ty = t / TW, tx = t - ty * TW;
   const uint32_t c0 = chunk_start[ty], c1 = chunk_start[ty + 1];
   uint32_t carry = 0;
@@ -635,6 +681,7 @@ __global__ void __launch_bounds__(256) tile_chunks_kernel(const uint32_t* __rest
     carry += __shfl_sync(0xffffffffu, x, 31);
   }
   if (lane == 0) tile_count[t] = carry;
+  return carry;
 }
 
 // Class of a tile's list length for the blend order: floor(log2 v) and the next two bits.
@@ -644,78 +691,62 @@ __device__ __forceinline__ int len_class(uint32_t v) {
   return 4 * (e - 1) + (int)((v >> (e - 2)) & 3u);
 }
 
-// One CTA: exclusive scan of the tile counts (row-major tile ids) -> ranges (empty tiles
-// [0, 0)), P and the overflow verdict, plus the blend order (tiles by list-length class,
-// longest first). Thread t owns ceil(T / 1024) consecutive tiles.
-__global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restrict__ tile_count, int T,
-                                                         Counters* __restrict__ ctr, uint32_t pair_cap,
-                                                         uint2* __restrict__ ranges, Sticky* __restrict__ sticky,
-                                                         uint32_t* __restrict__ tile_order) {
+constexpr int kScanTiles = 64;            // tiles per tile-scan block (8 tile_chunks CTAs)
+constexpr int kScanClasses = 33 * 4;      // list-length classes (len_class)
+
+// One warp per tile (tile_chunks_block), then per CTA (8 consecutive tiles, inside one
+// 64-tile scan block): the block's pair-count sum and the class counts of the blend order,
+// accumulated in the per-frame zeroed scan_part / scan_cls.
+__global__ void __launch_bounds__(256) tile_chunks_kernel(const uint32_t* __restrict__ chunk_start, int TH, int TW,
+                                                          uint32_t* __restrict__ chunk_count,
+                                                          uint32_t* __restrict__ tile_count,
+                                                          unsigned long long* __restrict__ scan_part,
+                                                          uint32_t* __restrict__ scan_cls) {
   pdl_wait();
   pdl_trigger();
-  __shared__ unsigned long long s_w[32];
-  constexpr int kClasses = 33 * 4;  // log2 of the list length, quartered
-  __shared__ uint32_t s_bucket[kClasses], s_cursor[kClasses];
+  __shared__ uint32_t s_v[8];
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const uint32_t v = tile_chunks_block(blockIdx.x, chunk_start, TH, TW, chunk_count, tile_count);
+  if ((tid & 31) == 0) s_v[warp] = v;
+  __syncthreads();
+  const int t0 = (int)blockIdx.x * 8, T = TW * TH;
+  if (tid < 8 && t0 + tid < T && s_v[tid]) atomicAdd(&scan_cls[len_class(s_v[tid])], 1u);
+  if (tid == 0) {
+    unsigned long long sum = 0;
+    uint32_t empties = 0;
+    for (int w = 0; w < 8; ++w) {
+      sum += s_v[w];
+      empties += (t0 + w < T && s_v[w] == 0) ? 1u : 0u;
+    }
+    if (sum) atomicAdd(&scan_part[t0 / kScanTiles], sum);
+    if (empties) atomicAdd(&scan_cls[0], empties);
+  }
+}
+
+// One CTA (64 threads) per 64-tile scan block: the block's exclusive start from the earlier
+// blocks' sums, each tile's range [start, end) (empty tiles [0, 0)), P and the pair-capacity
+// verdict (block 0), and the blend order: tiles by list-length class, longest first (class
+// starts from the frame's class counts, global cursors within a class).
+__global__ void __launch_bounds__(64) tile_scan_kernel(const uint32_t* __restrict__ tile_count, int T,
+                                                       Counters* __restrict__ ctr, uint32_t pair_cap,
+                                                       uint2* __restrict__ ranges, Sticky* __restrict__ sticky,
+                                                       uint32_t* __restrict__ tile_order,
+                                                       const unsigned long long* __restrict__ scan_part,
+                                                       uint32_t* __restrict__ scan_cls) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ uint32_t s_cstart[kScanClasses];
+  __shared__ unsigned long long s_w[2][2];
+  __shared__ uint32_t s_x0;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int per = (T + 1023) / 1024;
-  const int t0 = min(tid * per, T), t1 = min(t0 + per, T);
-  unsigned long long sum = 0;
-  for (int t = t0; t < t1; ++t) sum += tile_count[t];
-  unsigned long long x = sum;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) s_w[warp] = x;
-  __syncthreads();
-  if (warp == 0) {
-    const unsigned long long v = s_w[lane];
-    unsigned long long z = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned long long y = __shfl_up_sync(0xffffffffu, z, o);
-      if (lane >= o) z += y;
-    }
-    s_w[lane] = z - v;  // exclusive warp offsets
-    if (lane == 31) {   // P and the overflow verdict
-      const unsigned long long P = z;
-      ctr->n_pairs = (uint32_t)(P < pair_cap ? P : pair_cap);
-      if (P > ctr->pairs_needed) ctr->pairs_needed = P;
-      if (P > pair_cap) {
-        ctr->overflow = 1u;
-        atomicOr(&sticky->overflowed, 1u);
-        atomicMax(&sticky->pairs_needed_max, P);
-      }
-    }
-  }
-  __syncthreads();
-  unsigned long long st = s_w[warp] + x - sum;
-  if (tid < kClasses) s_bucket[tid] = 0;
-  __syncthreads();
-  for (int k = 0; k < per; ++k) {  // every lane iterates: the class counts are warp-aggregated
-    const int t = t0 + k;
-    const unsigned long long v = t < t1 ? tile_count[t] : 0ull;
-    if (t < t1) {
-      ranges[t] = v ? make_uint2((uint32_t)min(st, (unsigned long long)pair_cap),
-                                 (uint32_t)min(st + v, (unsigned long long)pair_cap))
-                    : make_uint2(0u, 0u);
-      st += v;
-    }
-    // empty tiles (most of a sparse frame: one class, per-tile atomics would serialise) are
-    // counted per warp
-    const uint32_t empties = __ballot_sync(0xffffffffu, t < t1 && v == 0);
-    if (lane == 0 && empties) atomicAdd(&s_bucket[0], (uint32_t)__popc(empties));
-    if (t < t1 && v) atomicAdd(&s_bucket[len_class((uint32_t)v)], 1u);
-  }
-  __syncthreads();
-  if (warp == 0) {  // blend order: longest lists first (the last wave of CTAs holds the short ones)
-    constexpr int kPer = (kClasses + 31) / 32;  // classes per lane, descending
+  const uint32_t k = blockIdx.x, nsb = gridDim.x;
+  if (warp == 0) {  // class starts, classes descending
+    constexpr int kPer = (kScanClasses + 31) / 32;
     uint32_t v[kPer], sum = 0;
 #pragma unroll
     for (int q = 0; q < kPer; ++q) {
-      const int b = kClasses - 1 - (lane * kPer + q);
-      v[q] = b >= 0 ? s_bucket[b] : 0u;
+      const int c = kScanClasses - 1 - (lane * kPer + q);
+      v[q] = c >= 0 ? scan_cls[c] : 0u;
       sum += v[q];
     }
     uint32_t x = sum;
@@ -727,22 +758,62 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restr
     uint32_t run = x - sum;
 #pragma unroll
     for (int q = 0; q < kPer; ++q) {
-      const int b = kClasses - 1 - (lane * kPer + q);
-      if (b >= 0) s_cursor[b] = run;
+      const int c = kScanClasses - 1 - (lane * kPer + q);
+      if (c >= 0) s_cstart[c] = run;
       run += v[q];
     }
   }
+  unsigned long long pre = 0, all = 0;
+  for (uint32_t j = tid; j < nsb; j += 64) {
+    const unsigned long long p = scan_part[j];
+    all += p;
+    pre += j < k ? p : 0ull;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    pre += __shfl_xor_sync(0xffffffffu, pre, o);
+    all += __shfl_xor_sync(0xffffffffu, all, o);
+  }
+  const int t = (int)k * kScanTiles + tid;
+  const bool in = t < T;
+  const uint32_t v = in ? tile_count[t] : 0u;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 0) {
+    s_w[warp][0] = pre;
+    s_w[warp][1] = all;
+  }
+  if (lane == 31 && warp == 0) s_x0 = x;
   __syncthreads();
-  const uint32_t lt = (1u << lane) - 1u;
-  for (int k = 0; k < per; ++k) {
-    const int t = t0 + k;
-    const uint32_t v = t < t1 ? tile_count[t] : 0u;
-    const uint32_t empties = __ballot_sync(0xffffffffu, t < t1 && v == 0);
-    uint32_t base = 0;
-    if (lane == 0 && empties) base = atomicAdd(&s_cursor[0], (uint32_t)__popc(empties));
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (t < t1)
-      tile_order[v ? atomicAdd(&s_cursor[len_class(v)], 1u) : base + __popc(empties & lt)] = (uint32_t)t;
+  pre = s_w[0][0] + s_w[1][0];
+  all = s_w[0][1] + s_w[1][1];
+  if (k == 0 && tid == 0) {  // P and the overflow verdict
+    ctr->n_pairs = (uint32_t)(all < pair_cap ? all : pair_cap);
+    if (all > ctr->pairs_needed) ctr->pairs_needed = all;
+    if (all > pair_cap) {
+      ctr->overflow = 1u;
+      atomicOr(&sticky->overflowed, 1u);
+      atomicMax(&sticky->pairs_needed_max, all);
+    }
+  }
+  const unsigned long long st = pre + (warp ? s_x0 : 0u) + x - v;
+  if (in)
+    ranges[t] = v ? make_uint2((uint32_t)min(st, (unsigned long long)pair_cap),
+                               (uint32_t)min(st + v, (unsigned long long)pair_cap))
+                  : make_uint2(0u, 0u);
+  // empty tiles (most of a sparse frame: one class) take one cursor atomic per warp
+  const uint32_t empties = __ballot_sync(0xffffffffu, in && v == 0);
+  uint32_t base = 0;
+  if (lane == 0 && empties) base = atomicAdd(&scan_cls[kScanClasses], (uint32_t)__popc(empties));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (in) {
+    const int c = v ? len_class(v) : 0;
+    tile_order[s_cstart[c] + (v ? atomicAdd(&scan_cls[kScanClasses + c], 1u)
+                                : base + __popc(empties & ((1u << lane) - 1u)))] = (uint32_t)t;
   }
 }
 
