@@ -85,7 +85,7 @@ namespace {
 
 size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
-constexpr int kMaxDsortCtas = 160;  // cooperative depth sort: one CTA per SM (column_prefix: <= 32 x 5 rows)
+constexpr int kMaxDsortCtas = 160;  // cooperative depth sort: one CTA per SM (column_prefix: <= 32 x 3 rows per half)
 
 struct Layout {
   // per-frame zeroed region [0, frame_bytes)
@@ -125,7 +125,8 @@ Layout make_layout(int64_t n_cap, int64_t pair_cap, int W, int H, int sms) {
   L.hist = take(4 * 256 * sizeof(uint32_t));  // depth passes 0-3
   L.proj_lb = take(((size_t)n_cap / kCompactKeys + 2) * sizeof(unsigned long long));
   L.ranges = take(TW * TH * sizeof(uint2));
-  L.dtab = take((size_t)4 * std::min(sms, kMaxDsortCtas) * 256 * 4);  // dsort_kernel's per-pass digit tables
+  // dsort_kernel's per-pass digit tables (16-bit counts) and digit totals
+  L.dtab = take((size_t)4 * std::min(sms, kMaxDsortCtas) * 128 * 4 + 4 * 256 * 4);
   L.scancls = take(2 * kScanClasses * 4);  // tile scan: list-length class counts and cursors
   L.scanpart = take(((size_t)TW * TH / kScanTiles + 1) * 8);  // tile scan: 64-tile block sums
   L.frame_bytes = o;
@@ -458,8 +459,14 @@ int32_t rs_bin(rs_workspace* ws, void* stream) {
     // one cooperative kernel (compaction fused into pass 0, 4 passes, grid barriers) for frames
     // of up to ~1M items, where the launch chain's per-kernel latency dominates (configs[1]:
     // 52 vs 65 us); larger frames keep the onesweep launches (configs[2]: 112 vs 153 us)
-    if (dsort_mode() == 2 || (dsort_mode() == 1 && n <= kDsortMaxItems)) {
-      const int G = std::min(ws->sms, kMaxDsortCtas);
+    const int G_dsort = std::min(ws->sms, kMaxDsortCtas);
+    // (the per-CTA digit counts are 16-bit: at most ceil(n / G) keys per CTA)
+    if ((n + G_dsort - 1) / G_dsort < 65536 && (dsort_mode() == 2 || (dsort_mode() == 1 && n <= kDsortMaxItems))) {
+      static const int g_env = [] {  // RS_DSORT_CTAS: grid override (A/B measurements)
+        const char* e = std::getenv("RS_DSORT_CTAS");
+        return e ? std::atoi(e) : 0;
+      }();
+      const int G = g_env > 0 ? std::min(g_env, G_dsort) : G_dsort;
       const cudaError_t e = ws->f64
           ? launch_coop(dsort_kernel<true>, G, kDsortThreads, sizeof(DsortSmem), st, ws->at<uint32_t>(ws->L.keysB), n,
                         ws->at<uint32_t>(ws->L.keysA), ws->at<uint32_t>(ws->L.valsA), ws->at<uint32_t>(ws->L.keysC),

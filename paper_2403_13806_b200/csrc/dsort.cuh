@@ -28,28 +28,41 @@
 
 namespace rs {
 
+#ifdef RS_DSORT_PROBE  // tools/dsort_probe.cu: per-CTA globaltimer stamps at the phase boundaries
+__device__ unsigned long long* g_dsort_probe;
+#define DSORT_MARK(k)                                                                   \
+  do {                                                                                  \
+    if (threadIdx.x == 0) {                                                             \
+      unsigned long long t_;                                                            \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                           \
+      g_dsort_probe[blockIdx.x * 32 + (k)] = t_;                                        \
+    }                                                                                   \
+  } while (0)
+#else
+#define DSORT_MARK(k) \
+  do {                \
+  } while (0)
+#endif
+
 constexpr int kDsortThreads = 1024;                           // one CTA of 32 warps per SM
 constexpr int kDsortWarps = kDsortThreads / 32;
 constexpr int kDsortItems = 4;                                // keys per thread per sub-chunk
 constexpr int kDsortChunk = kDsortThreads * kDsortItems;      // 4096
 
-// Grid barrier over the co-resident CTAs of a cooperative launch: arrive on a counter,
-// the last arrival bumps the generation the others spin on. `bar` = {count, gen}, zeroed
-// before the launch (the frame's counter memset).
+// Grid barrier over the co-resident CTAs of a cooperative launch: arrive on a counter that
+// only grows (zeroed before the launch by the frame's counter memset), spin until it reaches
+// the barrier's multiple of the grid size.
 __device__ __forceinline__ void grid_barrier(uint32_t* bar, uint32_t nblocks) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    volatile uint32_t* gen = bar + 1;
-    const uint32_t g = *gen;
     __threadfence();
-    if (atomicAdd(bar, 1u) == nblocks - 1) {
-      bar[0] = 0;
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
-    } else {
-      while (*gen == g) __nanosleep(20);
-    }
-    __threadfence();
+    // the arrival counter only grows: this barrier is complete when it reaches the next
+    // multiple of nblocks (no reset, no second word -- the last arrival releases everyone)
+    const uint32_t target = (atomicAdd(bar, 1u) / nblocks + 1) * nblocks;
+    uint32_t seen;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(bar) : "memory");
+    } while ((int)(seen - target) < 0);
   }
   __syncthreads();
 }
@@ -57,57 +70,66 @@ __device__ __forceinline__ void grid_barrier(uint32_t* bar, uint32_t nblocks) {
 struct DsortSmem {
   uint32_t hist[256];                // running global offset of each digit for this CTA's keys
   uint32_t whist[kDsortWarps][256];  // per-warp digit counts of a sub-chunk, then per-warp starts
-  uint32_t part[2][kDsortWarps][256];  // column-prefix partial sums: [pre | tot][row slice][digit]
+  uint32_t part[1][kDsortWarps][256];  // column-prefix partial sums: [row slice][digit]
+  uint32_t nexth[256];                 // this CTA's keys per next-pass digit (the digit totals)
   uint32_t wsum[8];
 };
 
-// Column prefix of a pass's [G][256] histogram table: pre = sum over rows < b, tot = sum over
-// all rows, for digit tid < 256. Thread (slice w, digit group g) sums rows [w R, (w+1) R) of
-// digits [8 g, 8 g + 8) with two 16-byte loads per row -- every load of the table in flight
-// at once (R <= 5 rows per slice for G <= 160).
-__device__ __forceinline__ void column_prefix(const uint32_t* __restrict__ table, uint32_t G, uint32_t b,
-                                              DsortSmem& S, uint32_t& pre, uint32_t& tot) {
+// Column prefix of a pass's [G][256] digit histogram table (16-bit counts, two per word):
+// pre = sum over rows < b for digit tid < 256. CTAs in the first half sum the rows before
+// them, the others the rows from b on and subtract from the pass's digit totals `gtot`
+// (accumulated separately) -- no CTA reads more than G/2 rows, and the table traffic of the
+// phase (every CTA reading it at once right after the barrier) is a quarter of a full
+// 32-bit read. Thread (slice w, digit group g) sums up to 3 rows of digits [8 g, 8 g + 8)
+// (one 16-byte load per row, all in flight); the 32 slices are combined in shared memory.
+__device__ __forceinline__ void column_prefix(const uint32_t* __restrict__ table, const uint32_t* __restrict__ gtot,
+                                              uint32_t G, uint32_t b, DsortSmem& S, uint32_t& pre,
+                                              uint32_t& tot) {
   const int tid = threadIdx.x, g = tid & 31, w = tid >> 5;
-  const uint32_t R = (G + kDsortWarps - 1) / kDsortWarps;  // <= kColRows (G <= 160)
-  const uint32_t r0 = min(w * R, G), r1 = min(r0 + R, G);
-  uint32_t sp[8] = {0, 0, 0, 0, 0, 0, 0, 0}, st[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  constexpr int kColRows = 5;
-  uint4 xs[kColRows], ys[kColRows];
+  const bool low = 2 * b <= G;
+  const uint32_t ra = low ? 0u : b, rb = low ? b : G;  // rows summed: [ra, rb), rb - ra <= G / 2
+  constexpr int kColRows = 3;                          // 32 slices x 3 rows >= 80 rows (G <= 160)
+  const uint32_t r0 = min(ra + w * kColRows, rb);
+  uint4 xs[kColRows];
 #pragma unroll
   for (int k = 0; k < kColRows; ++k) {  // every load issued before any is used
     const uint32_t r = r0 + k;
-    const uint4* row = reinterpret_cast<const uint4*>(table + (size_t)min(r, G - 1) * 256 + 8 * g);
-    xs[k] = r < r1 ? __ldcg(row) : make_uint4(0, 0, 0, 0);
-    ys[k] = r < r1 ? __ldcg(row + 1) : make_uint4(0, 0, 0, 0);
+    xs[k] = r < rb ? __ldcg(reinterpret_cast<const uint4*>(table + (size_t)r * 128) + g) : make_uint4(0, 0, 0, 0);
   }
+  uint32_t sp[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
   for (int k = 0; k < kColRows; ++k) {
-    const uint32_t v[8] = {xs[k].x, xs[k].y, xs[k].z, xs[k].w, ys[k].x, ys[k].y, ys[k].z, ys[k].w};
-    const bool before = r0 + k < b;
+    const uint32_t v[4] = {xs[k].x, xs[k].y, xs[k].z, xs[k].w};
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      st[q] += v[q];
-      sp[q] += before ? v[q] : 0u;
+    for (int q = 0; q < 4; ++q) {
+      sp[2 * q] += v[q] & 0xffffu;
+      sp[2 * q + 1] += v[q] >> 16;
     }
   }
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    S.part[0][w][8 * g + k] = sp[k];
-    S.part[1][w][8 * g + k] = st[k];
+  for (int k = 0; k < 8; ++k) S.part[0][w][8 * g + k] = sp[k];
+  __syncthreads();
+  {  // the 32 slices of digit d summed by 4 threads (8 slices each), then combined
+    const int d = tid & 255, q = tid >> 8;
+    uint32_t a = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a += S.part[0][8 * q + k][d];
+    S.whist[q][d] = a;  // whist is free until the rank phase
   }
   __syncthreads();
   pre = 0;
   tot = 0;
   if (tid < 256) {
-#pragma unroll 8
-    for (int q = 0; q < kDsortWarps; ++q) {
-      pre += S.part[0][q][tid];
-      tot += S.part[1][q][tid];
-    }
+    uint32_t sum = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) sum += S.whist[q][tid];
+    tot = __ldcg(gtot + tid);
+    pre = low ? sum : tot - sum;
   }
 }
 
-// tables: 4 x [G][256] digit histograms (one per pass), zero on entry (the frame memset).
+// tables: 4 x [G][256] digit histograms (one per pass; 16-bit counts, two per word) and
+// 4 x [256] digit totals, zero on entry (the frame memset).
 // Pass p's table is complete at the barrier that starts pass p: pass 0's from the CTAs'
 // own item ranges, pass p+1's accumulated by pass p's scatter (each key is counted, with a
 // global atomic, for the CTA that owns its new position in pass p+1) -- one grid barrier
@@ -131,10 +153,15 @@ __global__ void __launch_bounds__(kDsortThreads, 1) dsort_kernel(
   uint32_t* vout = vB;
   uint32_t kk[kDsortItems];
   bool one;
+  uint32_t* gtot = tables + (size_t)4 * G * 128;  // [4][256] digit totals per pass
+  DSORT_MARK(0);
   {  // pass 0's histogram: this CTA's item range (valid keys)
     const uint32_t lo = min(b * ci, n_items), hi = min(lo + ci, n_items);
     one = hi - lo <= (uint32_t)kDsortChunk;
-    if (tid < 256) S.hist[tid] = 0;
+    if (tid < 256) {
+      S.hist[tid] = 0;
+      S.nexth[tid] = 0;
+    }
     __syncthreads();
     for (uint32_t base = lo; base < hi; base += kDsortChunk) {
       const uint32_t wbase = base + warp * 32 * kDsortItems;
@@ -148,13 +175,16 @@ __global__ void __launch_bounds__(kDsortThreads, 1) dsort_kernel(
         if (kk[it] != kInvalidKey) atomicAdd(&S.hist[kk[it] & 0xffu], 1u);
     }
     __syncthreads();
-    if (tid < 256) tables[(size_t)b * 256 + tid] = S.hist[tid];
+    if (tid < 128) tables[(size_t)b * 128 + tid] = S.hist[2 * tid] | (S.hist[2 * tid + 1] << 16);
+    if (tid < 256 && S.hist[tid]) atomicAdd(gtot + tid, S.hist[tid]);
   }
+  DSORT_MARK(1);
   for (int p = 0; p < 4; ++p) {
     const int shift = 8 * p;
     grid_barrier(bar, G);
+    DSORT_MARK(2 + 4 * p);
     uint32_t pre, tot;
-    column_prefix(tables + (size_t)p * G * 256, G, b, S, pre, tot);
+    column_prefix(tables + (size_t)p * G * 128, gtot + p * 256, G, b, S, pre, tot);
     uint32_t x = tot;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -183,8 +213,9 @@ __global__ void __launch_bounds__(kDsortThreads, 1) dsort_kernel(
       hi = min(lo + cs, nvis);
       one = hi - lo <= (uint32_t)kDsortChunk;
     }
-    uint32_t* next = p < 3 ? tables + (size_t)(p + 1) * G * 256 : nullptr;
+    uint32_t* next = p < 3 ? tables + (size_t)(p + 1) * G * 128 : nullptr;
     __syncthreads();
+    DSORT_MARK(3 + 4 * p);
     // stable rank + scatter, sub-chunk by sub-chunk (warp-contiguous, item-major, lane-minor)
     for (uint32_t base = lo; base < hi; base += kDsortChunk) {
       const uint32_t wbase = base + warp * 32 * kDsortItems;
@@ -199,6 +230,7 @@ __global__ void __launch_bounds__(kDsortThreads, 1) dsort_kernel(
       }
       for (int i = tid; i < kDsortWarps * 256; i += kDsortThreads) (&S.whist[0][0])[i] = 0;
       __syncthreads();
+      DSORT_MARK(20 + 3 * p);
 #pragma unroll
       for (int it = 0; it < kDsortItems; ++it) {
         const uint32_t d = (kk[it] >> shift) & 0xffu;
@@ -216,6 +248,7 @@ __global__ void __launch_bounds__(kDsortThreads, 1) dsort_kernel(
         rk[it] = r0 + __popc(peers & lt);
       }
       __syncthreads();
+      DSORT_MARK(21 + 3 * p);
       {  // per digit: start of each warp's run = running offset + earlier warps; 4 threads per
          // digit (8 warps each), their totals combined through part[0]
         const int d = tid & 255, qq = tid >> 8;
@@ -239,6 +272,7 @@ __global__ void __launch_bounds__(kDsortThreads, 1) dsort_kernel(
         if (qq == 3) S.hist[d] = run;
       }
       __syncthreads();
+      DSORT_MARK(22 + 3 * p);
 #pragma unroll
       for (int it = 0; it < kDsortItems; ++it) {
         if (!ok[it]) continue;
@@ -247,10 +281,19 @@ __global__ void __launch_bounds__(kDsortThreads, 1) dsort_kernel(
         if (p < 3 || LAST_KEYS) kout[pos] = kk[it];
         vout[pos] = vv[it];
         // next pass: this key belongs to the CTA that owns position pos
-        if (next) atomicAdd(next + (size_t)(pos / cs) * 256 + ((kk[it] >> (shift + 8)) & 0xffu), 1u);
+        if (next) {
+          const uint32_t dn = (kk[it] >> (shift + 8)) & 0xffu;
+          atomicAdd(next + (size_t)(pos / cs) * 128 + (dn >> 1), 1u << (16 * (dn & 1u)));
+          atomicAdd(&S.nexth[dn], 1u);
+        }
       }
       __syncthreads();
     }
+    if (next && tid < 256) {  // the next pass's digit totals
+      if (S.nexth[tid]) atomicAdd(gtot + (p + 1) * 256 + tid, S.nexth[tid]);
+      S.nexth[tid] = 0;
+    }
+    DSORT_MARK(4 + 4 * p);
     kin = kout;
     vin = vout;
     kout = (kout == kB) ? kA : kB;
