@@ -316,12 +316,39 @@ class Renderer:
             scores.data_ptr() if scores is not None else None, flags, self.stream), "render")
 
     @staticmethod
-    def check_scores(scores: torch.Tensor | None, precision: int) -> None:
-        """A score vector holds the frame's value type (float32 / float64, non-negative)."""
+    def check_scores(scores: torch.Tensor | None, precision: int, ds: "DeviceScene | None" = None) -> None:
+        """A score vector holds the frame's value type (float32 / float64, non-negative), one
+        entry per Gaussian of the scene, on the scene's device."""
+        if scores is not None and ds is not None and (scores.numel() < ds.n or not scores.is_contiguous()
+                                                      or scores.device != torch.device(ds.device)):
+            raise InvalidParameterError(f"scores must be a contiguous vector of >= {ds.n} entries on {ds.device}")
         if scores is not None and scores.dtype not in (value_dtype(precision), torch.int32, torch.int64):
             raise InvalidParameterError(f"scores must be {value_dtype(precision)} for this precision")
         if scores is not None and scores.element_size() != (8 if precision == N.RS_F64 else 4):
             raise InvalidParameterError("scores element size does not match the precision")
+
+    @staticmethod
+    def check_outputs(out: dict, cam, precision: int, device) -> None:
+        """Caller-provided images must hold the frame (dtype, element count, contiguity; the
+        float64/int64 reference-typed ones may be pinned host memory) -- the kernels write
+        through the raw pointers."""
+        H, W = int(cam.height), int(cam.width)
+        vt = value_dtype(precision)
+        spec = {"rgb": (vt, 3), "alpha": (vt, 1), "depth": (vt, 1), "count": (torch.int32, 1),
+                "rgb64": (torch.float64, 3), "alpha64": (torch.float64, 1), "count64": (torch.int64, 1),
+                "tau": (torch.float32, 1), "last": (torch.int32, 1)}
+        for k, t in out.items():
+            if k not in spec:
+                raise InvalidParameterError(f"unknown output {k!r}")
+            dt, ch = spec[k]
+            if t.dtype != dt or t.numel() < H * W * ch or not t.is_contiguous():
+                raise InvalidParameterError(f"output {k!r} must be a contiguous {dt} tensor of >= {H * W * ch} "
+                                            f"elements for this frame and precision")
+            if k in ("rgb64", "alpha64", "count64"):
+                if not (t.is_cuda or t.is_pinned()):
+                    raise InvalidParameterError(f"output {k!r} must be device or pinned host memory")
+            elif not t.is_cuda or t.device != torch.device(device):
+                raise InvalidParameterError(f"output {k!r} must live on {device}")
 
     def render(self, ds: DeviceScene, cam, opts, *, color: bool = True, scores: torch.Tensor | None = None,
                active_idx: torch.Tensor | None = None, m: int | None = None, count_evals: bool = False,
@@ -331,7 +358,9 @@ class Renderer:
         W, H = int(cam.width), int(cam.height)
         self.ensure(items, self.caps[1] or max(4 * items, 1 << 20), W, H)
         cam_s, opt_s = camera_struct(cam), options_struct(opts)
-        self.check_scores(scores, opt_s.precision)
+        self.check_scores(scores, opt_s.precision, ds)
+        if out is not None:
+            self.check_outputs(out, cam, opt_s.precision, ds.device)
         out = out if out is not None else self.alloc_outputs(cam, color, opt_s.precision)
         flags = N.RS_FLAG_COUNT_EVALS if count_evals else 0
         snapshot = scores.clone() if scores is not None else None
@@ -359,7 +388,7 @@ class Renderer:
         W, H = max(int(c.width) for c in cams), max(int(c.height) for c in cams)
         self.ensure(ds.n, self.caps[1] or max(4 * ds.n, 1 << 20), W, H)
         opt_s = options_struct(opts)
-        self.check_scores(scores, opt_s.precision)
+        self.check_scores(scores, opt_s.precision, ds)
         structs = [camera_struct(c) for c in cams]
         snapshot = scores.clone()
         self.read_overflow(reset=True)

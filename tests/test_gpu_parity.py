@@ -337,3 +337,23 @@ def test_out_of_range_active_index_rejected(prec):
     # a valid list still renders after the errors
     out, st = render_device(ds, cam, opts, active_idx=torch.arange(len(s), dtype=torch.int32, device=ds.device))
     assert st.bad_index == 0
+
+
+def test_mismatched_caller_outputs_rejected_before_launch():
+    """Caller-provided images of the wrong precision / size raise InvalidParameterError
+    instead of being written past their end; the renderer keeps working afterwards."""
+    from paper_2403_13806_b200.core import InvalidParameterError
+    from paper_2403_13806_b200.device import device_scene, renderer
+    from paper_2403_13806_b200.render import RasterizeOptions
+    from paper_2403_13806_b200 import _native as N
+    s, cam, _ = load_case(golden("suite50"), "c3_")
+    ds = device_scene(s)
+    r = renderer(ds.device)
+    f32 = r.alloc_outputs(cam, precision=N.RS_F32)
+    with pytest.raises(InvalidParameterError):
+        r.render(ds, cam, RasterizeOptions(precision="fp64"), out=f32)
+    with pytest.raises(InvalidParameterError):
+        r.render(ds, cam, RasterizeOptions(precision="fp32"), scores=torch.zeros(len(s) - 1, device=ds.device))
+    out, _ = r.render(ds, cam, RasterizeOptions(precision="fp32"), out=f32)
+    torch.cuda.synchronize()
+    assert torch.isfinite(out["rgb"]).all()

@@ -219,6 +219,39 @@ def test_api_argument_errors_without_gpu():
         bake_visibility(s, cl, [cam], t_cluster=-1.0)
 
 
+def test_caller_outputs_and_scores_are_validated():
+    """Images / score vectors handed to Renderer.render are checked against the frame before
+    any launch (the kernels write through raw pointers): wrong dtype for the precision, too
+    few elements, non-contiguous, unknown keys, wrong device."""
+    import torch
+    from paper_2403_13806_b200 import _native as N
+    from paper_2403_13806_b200.core import InvalidParameterError
+    from paper_2403_13806_b200.device import Renderer
+    cam = load_cam(golden("suite50"), "c0_")
+    H, W = int(cam.height), int(cam.width)
+    f32 = dict(rgb=torch.empty((H, W, 3)), alpha=torch.empty((H, W)), count=torch.empty((H, W), dtype=torch.int32))
+    # CPU tensors: rejected for their device only once dtype and size pass
+    with pytest.raises(InvalidParameterError, match="must live on"):
+        Renderer.check_outputs(f32, cam, N.RS_F32, "cuda:0")
+    with pytest.raises(InvalidParameterError, match="float64"):
+        Renderer.check_outputs(f32, cam, N.RS_F64, "cuda:0")
+    with pytest.raises(InvalidParameterError, match="elements"):
+        Renderer.check_outputs(dict(alpha=torch.empty((H, W - 1))), cam, N.RS_F32, "cuda:0")
+    with pytest.raises(InvalidParameterError, match="contiguous"):
+        Renderer.check_outputs(dict(rgb=torch.empty((W, H, 3)).transpose(0, 1)), cam, N.RS_F32, "cuda:0")
+    with pytest.raises(InvalidParameterError, match="unknown"):
+        Renderer.check_outputs(dict(colour=torch.empty(1)), cam, N.RS_F32, "cuda:0")
+    with pytest.raises(InvalidParameterError, match="pinned"):
+        Renderer.check_outputs(dict(rgb64=torch.empty((H, W, 3), dtype=torch.float64)), cam, N.RS_F32, "cuda:0")
+
+    class _DS:
+        n, device = 10, "cuda:0"
+    with pytest.raises(InvalidParameterError, match="entries"):
+        Renderer.check_scores(torch.zeros(9), N.RS_F32, _DS())
+    with pytest.raises(InvalidParameterError):
+        Renderer.check_scores(torch.zeros(10, dtype=torch.float64), N.RS_F32)
+
+
 def test_contribution_accumulator_merge_commutative():
     from paper_2403_13806_b200.render import ContributionAccumulator
     rng = np.random.default_rng(1234)

@@ -8,7 +8,7 @@ from paper_2403_13806_b200.device import device_scene, renderer
 from paper_2403_13806_b200.render import RasterizeOptions, rasterize
 
 scene, cams = synth.config1(0, n_frames=100)
-opts = RasterizeOptions(near_limit=0.2)
+opts = RasterizeOptions(near_limit=0.2, precision="fp32")
 ds = device_scene(scene)
 r = renderer(ds.device)
 H, W = cams[0].height, cams[0].width
