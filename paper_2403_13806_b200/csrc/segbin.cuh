@@ -603,7 +603,8 @@ __global__ void __launch_bounds__(256) expand_dense_kernel(const uint32_t* __res
 }
 
 // Expansion counts (order-free): per (chunk, tile column) the number of the chunk's segments
-// covering the column -- shared-memory counters over all the row's columns, one CTA per chunk.
+// covering the column -- a shared-memory difference array over the row's columns (two
+// atomics per segment) and its prefix, one CTA per chunk.
 __device__ __forceinline__ void chunk_count_loop(uint32_t first, uint32_t stride,
                                                  const uint32_t* seg_span,
                                                  const uint32_t* row_start,
@@ -611,27 +612,58 @@ __device__ __forceinline__ void chunk_count_loop(uint32_t first, uint32_t stride
                                                  uint32_t* chunk_count,
                                                  uint2* chunk_info, int dense_span,
                                                  Counters* ctr, uint32_t* dense_list) {
-  __shared__ uint32_t s_cnt[kMaxTileCols];
-  __shared__ uint32_t s_tiles;
-  const int tid = threadIdx.x;
+  __shared__ uint32_t s_cnt[kMaxTileCols + 1];
+  __shared__ uint32_t s_tiles, s_w[8];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (uint32_t gc = first;; gc += stride) {
     int ty;
     uint32_t lc;
     if (!chunk_of(chunk_start, TH, gc, ty, lc)) break;
     __syncthreads();
-    for (int c = tid; c < TW; c += 256) s_cnt[c] = 0;
+    for (int c = tid; c <= TW; c += 256) s_cnt[c] = 0;
     if (tid == 0) s_tiles = 0;
     __syncthreads();
     const uint32_t s0 = row_start[ty] + lc * kExpandChunk, s1 = min(row_start[ty + 1], s0 + kExpandChunk);
     int tiles = 0;
-    for (uint32_t sidx = s0 + tid; sidx < s1; sidx += 256) {
+    for (uint32_t sidx = s0 + tid; sidx < s1; sidx += 256) {  // a difference array over the columns
       const uint32_t sp = seg_span[sidx];
       const int t0 = (int)(sp & 0xffffu), t1 = (int)(sp >> 16);
-      for (int c = t0; c <= t1; ++c) atomicAdd(&s_cnt[c], 1u);
+      if (t0 <= t1) {
+        atomicAdd(&s_cnt[t0], 1u);
+        atomicAdd(&s_cnt[t1 + 1], 0xffffffffu);
+      }
       tiles += max(t1 - t0 + 1, 0);
     }
     tiles = __reduce_add_sync(0xffffffffu, tiles);
-    if ((tid & 31) == 0) atomicAdd(&s_tiles, (uint32_t)tiles);
+    if (lane == 0) atomicAdd(&s_tiles, (uint32_t)tiles);
+    __syncthreads();
+    {  // inclusive prefix over the columns: thread t owns columns [8t, 8t + 8)
+      constexpr int kPer = kMaxTileCols / 256;
+      uint32_t v[kPer], sum = 0;
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) {
+        const int c = tid * kPer + q;
+        v[q] = c < TW ? s_cnt[c] : 0u;
+        sum += v[q];
+      }
+      uint32_t x = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane == 31) s_w[warp] = x;
+      __syncthreads();
+      uint32_t run = x - sum;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) run += w < warp ? s_w[w] : 0u;
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) {
+        const int c = tid * kPer + q;
+        run += v[q];
+        if (c < TW) s_cnt[c] = run;
+      }
+    }
     __syncthreads();
     // dense: the segments average >= dense_span tiles (expand_kernel's ballot walk)
     if (tid == 0) {
