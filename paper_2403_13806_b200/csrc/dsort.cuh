@@ -55,10 +55,13 @@ constexpr int kDsortChunk = kDsortThreads * kDsortItems;      // 4096
 __device__ __forceinline__ void grid_barrier(uint32_t* bar, uint32_t nblocks) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
     // the arrival counter only grows: this barrier is complete when it reaches the next
-    // multiple of nblocks (no reset, no second word -- the last arrival releases everyone)
-    const uint32_t target = (atomicAdd(bar, 1u) / nblocks + 1) * nblocks;
+    // multiple of nblocks (no reset, no second word -- the last arrival releases everyone).
+    // Arrival is a release RMW (the CTA's writes, ordered before it by the bar.sync above,
+    // become visible with it), the polling an acquire load.
+    uint32_t arrived;
+    asm volatile("atom.add.release.gpu.global.u32 %0, [%1], 1;" : "=r"(arrived) : "l"(bar) : "memory");
+    const uint32_t target = (arrived / nblocks + 1) * nblocks;
     uint32_t seen;
     do {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(bar) : "memory");
