@@ -981,6 +981,15 @@ def run_train(args, ctx):
         "stages_ms": {"forward_with_cache": float(fwd.mean()), "backward": float(bwd.mean())},
         "gpu_launches": args.steps * (frame_launches(n, False) + 2), "clocks": clk.summary(),
         "e2e": e2e,
+        # the training pair is a widening beyond SURVEY §8's rows: §8d gives no algorithmic
+        # flop/byte model for the backward, and oracle/ has no CPU restatement of it (its
+        # parity is anchored on the reference's own fp64 gradients, tests/golden/grad.npz)
+        "roofline": None,
+        "roofline_note": "no SURVEY §8d algorithmic model for the backward; the forward's blend roofline "
+                         "is the render line's",
+        "cpu_baseline": None,
+        "cpu_baseline_note": "no CPU restatement of the backward in oracle/ (parity vs the reference's "
+                             "fp64 gradients, tests/golden/grad.npz)",
     }
 
 

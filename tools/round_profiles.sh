@@ -22,6 +22,8 @@ for p in fp32 fp64; do   # two frames: the second one is the warm-workspace fram
 done
 ncu --set full --import-source on --clock-control none -c 40 \
     -o $O/${R}_full_configs2_fp32 python tools/profile_frame.py score 2 fp32 > /dev/null 2>&1
+ncu --set full --import-source on --clock-control none -c 40 \
+    -o $O/${R}_full_configs4_fp32 python tools/profile_frame.py batch 2 fp32 > /dev/null 2>&1
 # summaries on the box (the reports themselves are too large to bring back)
 for f in $O/${R}_full_*.ncu-rep; do
   b=${f%.ncu-rep}
