@@ -467,13 +467,17 @@ int32_t rs_bin(rs_workspace* ws, void* stream) {
         return e ? std::atoi(e) : 0;
       }();
       const int G = g_env > 0 ? std::min(g_env, G_dsort) : G_dsort;
+      static const uint32_t red_max = [] {  // RS_DSORT_RED_MAX: the atomics/barrier switch (tests, A/B)
+        const char* e = std::getenv("RS_DSORT_RED_MAX");
+        return e ? (uint32_t)std::strtoul(e, nullptr, 10) : kDsortRedMax;
+      }();
       const cudaError_t e = ws->f64
           ? launch_coop(dsort_kernel<true>, G, kDsortThreads, sizeof(DsortSmem), st, ws->at<uint32_t>(ws->L.keysB), n,
                         ws->at<uint32_t>(ws->L.keysA), ws->at<uint32_t>(ws->L.valsA), ws->at<uint32_t>(ws->L.keysC),
-                        ws->at<uint32_t>(ws->L.valsB), ws->at<uint32_t>(ws->L.dtab), ws->ctr())
+                        ws->at<uint32_t>(ws->L.valsB), ws->at<uint32_t>(ws->L.dtab), ws->ctr(), red_max)
           : launch_coop(dsort_kernel<false>, G, kDsortThreads, sizeof(DsortSmem), st, ws->at<uint32_t>(ws->L.keysB), n,
                         ws->at<uint32_t>(ws->L.keysA), ws->at<uint32_t>(ws->L.valsA), ws->at<uint32_t>(ws->L.keysC),
-                        ws->at<uint32_t>(ws->L.valsB), ws->at<uint32_t>(ws->L.dtab), ws->ctr());
+                        ws->at<uint32_t>(ws->L.valsB), ws->at<uint32_t>(ws->L.dtab), ws->ctr(), red_max);
       if (e == cudaSuccess) {
         keys_res = ws->at<uint32_t>(ws->L.keysA);
         items_sorted = ws->at<uint32_t>(ws->L.valsA);

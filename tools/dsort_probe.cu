@@ -63,7 +63,8 @@ int main(int argc, char** argv) {
     cfg.attrs = at;
     cfg.numAttrs = 1;
     cudaEventRecord(e0);
-    cudaError_t e = cudaLaunchKernelEx(&cfg, dsort_kernel<false>, (const uint32_t*)dk, n, kA, vA, kB, vB, tab, ctr);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, dsort_kernel<false>, (const uint32_t*)dk, n, kA, vA, kB, vB, tab, ctr,
+                                       (uint32_t)(getenv("RS_DSORT_RED_MAX") ? atoi(getenv("RS_DSORT_RED_MAX")) : kDsortRedMax));
     cudaEventRecord(e1);
     cudaDeviceSynchronize();
     if (e != cudaSuccess || cudaGetLastError() != cudaSuccess) {
