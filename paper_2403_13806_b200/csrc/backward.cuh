@@ -166,8 +166,7 @@ __global__ void __launch_bounds__(kBwd2Threads) backward2_kernel(
         const f2 x = f2_pack(fminf(p20, 127.0f), fminf(p21, 127.0f));
         const f2 t = f2_add(x, f2_splat(kMagic));
         const f2 r = f2_sub(x, f2_sub(t, f2_splat(kMagic)));
-        const f2 sc = f2_pack(__int_as_float((__float_as_int(f2_lo(t)) << 23) + 0x3f800000),
-                              __int_as_float((__float_as_int(f2_hi(t)) << 23) + 0x3f800000));
+        const f2 sc = f2_exp2_scale(t);
         f2 pp = f2_fma(f2_splat(fbits(0x3920e999u)), r, f2_splat(fbits(0x3aafa2b5u)));
         pp = f2_fma(pp, r, f2_splat(fbits(0x3c1d96deu)));
         pp = f2_fma(pp, r, f2_splat(fbits(0x3d63576au)));

@@ -41,4 +41,15 @@ __device__ __forceinline__ f2 f2_fma(f2 a, f2 b, f2 c) {
   return d;
 }
 
+// {2^n_lo, 2^n_hi} from the round-to-integer magic sums t = x + 1.5 * 2^23 of an exp2
+// reduction: (bits(t) << 23) + bits(1.0f) per half -- as two 32-bit shift-adds (one LEA each;
+// written on the 64-bit pair in C, ptxas folds the high half into a funnel shift + mask + add)
+__device__ __forceinline__ f2 f2_exp2_scale(f2 t) {
+  f2 r;
+  asm("{\n\t.reg .b32 lo, hi;\n\tmov.b64 {lo, hi}, %1;\n\tshl.b32 lo, lo, 23;\n\tshl.b32 hi, hi, 23;\n\t"
+      "add.u32 lo, lo, 0x3f800000;\n\tadd.u32 hi, hi, 0x3f800000;\n\tmov.b64 %0, {lo, hi};\n\t}"
+      : "=l"(r) : "l"(t));
+  return r;
+}
+
 }  // namespace rs
