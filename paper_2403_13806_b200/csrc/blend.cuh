@@ -215,6 +215,14 @@ constexpr int kBlend2Threads = 128;
 #define RS_BLEND_UNROLL 6
 #endif
 constexpr int kBlendUnroll = RS_BLEND_UNROLL;  // list entries per inner iteration (measured: 2 -> 4 -> 6: -2..-6%, -1.5%)
+// score-only frames (no colour state): 8 entries per iteration at >= 6 CTAs per SM (<= 80
+// registers): configs[2] score blend 216.6 -> 208.0 us (colour frames: 156.7 -> 157.4, kept at 6 / 1)
+#ifndef RS_BLEND_UNROLL_S
+#define RS_BLEND_UNROLL_S 8
+#endif
+#ifndef RS_BLEND_MINB_S
+#define RS_BLEND_MINB_S 6
+#endif
 
 template <bool COLOR, bool STATS, bool FAST>
 __device__ __forceinline__ float blend_px(const float4 ga, const float4 gb, const float4 gc, float xs, float ys,
@@ -251,7 +259,7 @@ template <bool COLOR, bool CONTRIB, bool STATS, bool FAST, bool TRAIN = false>
 #ifndef RS_BLEND_MINB
 #define RS_BLEND_MINB 1
 #endif
-__global__ void __launch_bounds__(kBlend2Threads, RS_BLEND_MINB) blend2_kernel(
+__global__ void __launch_bounds__(kBlend2Threads, COLOR ? RS_BLEND_MINB : RS_BLEND_MINB_S) blend2_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ pair_items, const Rec* __restrict__ recs,
     const float4* __restrict__ geom, const uint32_t* __restrict__ tile_order, Counters* __restrict__ ctr, int W,
     int H, int TW, Opt32 o, const Out32 out, uint32_t* __restrict__ scores) {
@@ -262,7 +270,7 @@ __global__ void __launch_bounds__(kBlend2Threads, RS_BLEND_MINB) blend2_kernel(
 #endif
   constexpr int kBatch = RS_BLEND_BATCH;  // entries staged per batch
   constexpr int kPerThread = kBatch / kBlend2Threads;
-  constexpr int U = kBlendUnroll;
+  constexpr int U = COLOR ? kBlendUnroll : RS_BLEND_UNROLL_S;
   // slot kBatch: an empty-box sentinel that pads every warp list to a multiple of U entries
   __shared__ Rec s_rec[kBatch + 1 > 160 ? kBatch + 1 : 160];  // >= 10 KB: the float64 epilogue's staging
   __shared__ uint32_t s_w[CONTRIB ? kBatch + 1 : 1];

@@ -11,7 +11,9 @@ ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 from paper_2403_13806_b200.build import NVCC_FLAGS, nvcc  # noqa: E402
 
+import os  # noqa: E402
 flags = [f for f in NVCC_FLAGS if f not in ("-shared", "-cudart", "static")]
+flags += os.environ.get("RS_NVCC_EXTRA", "").split()  # the same experiment flags as build()
 out = subprocess.run([nvcc(), *flags, "-Xptxas", "-v", "-c", str(ROOT / "paper_2403_13806_b200/csrc/api.cu"),
                       "-o", "/tmp/_ptxas_report.o"], capture_output=True, text=True).stderr
 name, rows = None, []
