@@ -333,6 +333,9 @@ class Ctx:
     def fp32_peak(self) -> float:
         return self.sms * 128 * 2 * self.pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
 
+    def fp64_peak(self) -> float:  # B200: 64 FP64 lanes per SM (tools/fma_peak.cu measures 33.6 of 37.2)
+        return self.sms * 64 * 2 * self.pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+
     def hbm(self) -> float:
         return float(self.pk.get("hbm_gbs", 6650.0))
 
@@ -514,7 +517,7 @@ def measure_score(ctx, scene, cams, opts, steps, warmup, staged_views=6):
     kept = int((scores[:len(scene)] >= 0.01).sum().item())
     stages = staged_times(ctx, ds, sel, opts, [None, None, None, None], scores=scores)
     flops = (16 * E + 5 * C_) / max(len(sel), 1)
-    peak = ctx.fp32_peak()
+    peak = ctx.fp64_peak() if prec == N.RS_F64 else ctx.fp32_peak()
     nv = max(len(mine), 1)
     hw = cams[0].width * cams[0].height
     view_ms = t_max / steps / max(hi - lo, 1)
@@ -534,7 +537,8 @@ def measure_score(ctx, scene, cams, opts, steps, warmup, staged_views=6):
         "traffic": profiled_traffic("score_fp64" if prec == N.RS_F64 else "score_fp32", "blend2_kernel<0, 1, 0, 1, 0>"),
         "traffic_source": TRAFFIC["score_fp32"] + " (ncu --set full, dram read+write bytes per launch)",
         "algorithmic": "16*E + 5*C flops per view (SURVEY §8d), E/C counted on the staged views",
-        "peak_source": "computed: SMs x 128 FP32 lanes x 2 x sm_max_mhz"}
+        "peak_source": "computed: SMs x 64 FP64 lanes x 2 x sm_max_mhz" if prec == N.RS_F64
+        else "computed: SMs x 128 FP32 lanes x 2 x sm_max_mhz"}
     res["view_roofline"] = {"bytes_alg_per_view": byt, "achieved_gbs": byt / (view_ms / 1e3) / 1e9,
                             "peak_gbs": ctx.hbm(), "frac": byt / (view_ms / 1e3) / 1e9 / ctx.hbm()}
     return res
@@ -562,14 +566,17 @@ def e2e_score(ctx, scene, cams, opts):
 
 def roofline_render(ctx, m, prec_fp64: bool) -> dict:
     kern = "blend64_kernel<1, 0, 0, 1>" if prec_fp64 else "blend2_kernel<1, 0, 0, 1, 0>"
+    peak = ctx.fp64_peak() if prec_fp64 else ctx.fp32_peak()
     return {"kernel": kern, "bound": "fp64" if prec_fp64 else "fp32", "achieved": m["blend_tflops"],
-            "peak": ctx.fp32_peak(), "unit": "TFLOP/s", "frac": m["blend_frac_fp32"],
+            "peak": peak, "unit": "TFLOP/s", "frac": m["blend_tflops"] / peak,
             "traffic": profiled_traffic("render_fp64" if prec_fp64 else "render_fp32", kern),
             "traffic_source": TRAFFIC["render_fp64" if prec_fp64 else "render_fp32"]
             + " (ncu --set full: dram read+write bytes per launch)",
             "algorithmic": "16*E + 11*C flops per frame (SURVEY §8d), E/C counted by the device",
-            "peak_source": "computed: SMs x 128 FP32 lanes x 2 x sm_max_mhz (MEASURED_PEAKS.json has no FP32 "
-                           "figure)"}
+            "peak_source": ("computed: SMs x 64 FP64 lanes x 2 x sm_max_mhz" if prec_fp64 else
+                            "computed: SMs x 128 FP32 lanes x 2 x sm_max_mhz")
+                           + " (MEASURED_PEAKS.json has no FP32 / FP64 figure; tools/fma_peak.cu measured "
+                             "72.2 / 33.6 TFLOP/s of FMA issue on this pool's B200)"}
 
 
 # ---------------------------------------------------------------------------
@@ -826,7 +833,8 @@ def run_trajectory(args, ctx):
     # roofline of the dominant kernel (the blend of the unfiltered / batch frames)
     fl, bl = ref_arm["flops_alg_per_frame"], ref_arm["stages_ms"]["blend"]
     ach = fl / (bl / 1e3) / 1e12
-    peak = ctx.fp32_peak()
+    f64 = args.precision == "fp64"
+    peak = ctx.fp64_peak() if f64 else ctx.fp32_peak()
     t_frame = main_arm["ms_per_frame"]
     result = {
         "metric": METRICS[args.workload], "value": main_arm["fps"], "unit": "frames/s", "n_gpus": world,
@@ -839,10 +847,11 @@ def run_trajectory(args, ctx):
         "arms": res_arms, "clocks": main_arm["clocks"],
         "gpu_launches": sum(a["frames"] // world for a in res_arms.values())
         * frame_launches(len(scene), args.precision == "fp64"),
-        "roofline": {"kernel": "blend2_kernel<1, 0, 0, 1, 0>" + (" (unfiltered frames)" if house else ""),
-                     "bound": "fp32", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
-                     "traffic": None, "algorithmic": "16*E + 11*C flops per frame (SURVEY §8d)",
-                     "peak_source": "computed: SMs x 128 FP32 lanes x 2 x sm_max_mhz"},
+        "roofline": {"kernel": ("blend64_kernel<1, 0, 0, 1>" if f64 else "blend2_kernel<1, 0, 0, 1, 0>")
+                     + (" (unfiltered frames)" if house else ""),
+                     "bound": "fp64" if f64 else "fp32", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+                     "frac": ach / peak, "traffic": None, "algorithmic": "16*E + 11*C flops per frame (SURVEY §8d)",
+                     "peak_source": "computed: SMs x %d FP%d lanes x 2 x sm_max_mhz" % ((64, 64) if f64 else (128, 32))},
         "frame_roofline": {"bytes_alg_per_frame": main_arm["bytes_alg_per_frame"],
                            "achieved_gbs": main_arm["bytes_alg_per_frame"] / (t_frame / 1e3) / 1e9,
                            "peak_gbs": ctx.hbm(),
