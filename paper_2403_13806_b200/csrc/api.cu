@@ -27,9 +27,9 @@ using namespace rs;
 // Frame kernels launched straight onto a stream use programmatic stream serialization (PDL):
 // the grid is scheduled while the previous kernel drains and waits in griddepcontrol.wait
 // (pdl_wait, the first statement of each kernel) for its completion -- the launch gaps of the
-// chain of small binning kernels are hidden (configs[2] scoring +3%). Not while a CUDA graph
-// is being captured: replayed graphs already launch back to back, and programmatic edges in
-// them measured 2% slower per configs[1] frame.
+// chain of small binning kernels are hidden (configs[2] scoring +3%). Captured CUDA graphs keep
+// the programmatic edges too (round 1 measured them 2% slower; with this round's chain they
+// are 1.2% faster per configs[1] frame: 3262 -> 3300 frames/s; RS_PDL_GRAPH=0 drops them).
 enum PdlClass { kPdlChain = 1, kPdlExpand = 2, kPdlBlend = 4, kPdlAll = 7 };
 static int pdl_mode() {  // RS_PDL (A/B measurements): bit 0 binning chain, bit 1 expand, bit 2 blend
   static const int m = [] {
@@ -77,7 +77,11 @@ static void launch(void (*k)(KP...), dim3 grid, dim3 block, size_t smem, cudaStr
   cfg.attrs = at;
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(st, &cap);
-  cfg.numAttrs = (cap == cudaStreamCaptureStatusNone && (pdl_mode() & g_pdl_class)) ? 1 : 0;
+  static const bool pdl_graph = [] {  // RS_PDL_GRAPH=0: no PDL edges in captured graphs (A/B)
+    const char* e = std::getenv("RS_PDL_GRAPH");
+    return !e || std::atoi(e) != 0;
+  }();
+  cfg.numAttrs = ((cap == cudaStreamCaptureStatusNone || pdl_graph) && (pdl_mode() & g_pdl_class)) ? 1 : 0;
   cudaLaunchKernelEx(&cfg, k, static_cast<KP>(args)...);
 }
 
