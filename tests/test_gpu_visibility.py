@@ -148,6 +148,28 @@ def test_config2_scoring_subsample_bit_exact(prec, tier):
 
 
 @PREC
+def test_config2_full_size_view_bit_exact_and_pass_invariants(prec, tier):
+    """configs[2] at its full size (3M Gaussians, 1256x828; the onesweep depth sort path): one
+    view's importance table equals the oracle bit for bit, and a multi-view pass is invariant
+    under view order and view duplication (max-merge is commutative and idempotent,
+    test_pruning.py:54-66) -- the same table whatever the order, bit for bit."""
+    from oracle import oracle as O
+    from paper_2403_13806_b200.pruning import score_views_device
+    from paper_2403_13806_b200.render import RasterizeOptions
+    from paper_2403_13806_b200.synth import config2
+    scene, cams = config2(0, n=3_000_000, n_views=200)
+    opts = RasterizeOptions(near_limit=0.2, precision=prec)
+    one = score_views_device(scene, [cams[17]], opts).cpu().numpy()
+    ref = O.views(scene, [cams[17]], opts, tier, scores=True)["contrib"]
+    assert np.array_equal(one, ref)
+    sel = cams[::25]
+    a = score_views_device(scene, sel, opts)
+    b = score_views_device(scene, sel[::-1] + sel[:3], opts)
+    assert torch.equal(a, b)
+    assert int((a >= 0.01).sum()) > 0 and float(a.max()) <= 0.99
+
+
+@PREC
 def test_large_frame_invariants_config4(prec, tier):
     """configs[4] overlap stress at full size (1M Gaussians, 1920x1080): properties that hold at any size."""
     from paper_2403_13806_b200.device import renderer
