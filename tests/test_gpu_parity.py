@@ -357,3 +357,48 @@ def test_mismatched_caller_outputs_rejected_before_launch():
     out, _ = r.render(ds, cam, RasterizeOptions(precision="fp32"), out=f32)
     torch.cuda.synchronize()
     assert torch.isfinite(out["rgb"]).all()
+
+
+@pytest.mark.parametrize("prec,tier", PRECISIONS, ids=PREC_IDS)
+def test_empty_and_fully_culled_frames(prec, tier):
+    """A scene with no Gaussians, and a camera that sees none of them: black image, zero
+    counts and scores, no pairs -- and the renderer keeps producing correct frames after."""
+    from oracle import oracle as O
+    from paper_2403_13806_b200.core import look_at_camera
+    from paper_2403_13806_b200.render import RasterizeOptions, rasterize
+    from paper_2403_13806_b200.synth import config0
+    scene, cams = config0(0)
+    cam = cams[0]
+    opts = RasterizeOptions(near_limit=0.2, precision=prec)
+    empty = scene.subset(np.zeros(len(scene), dtype=bool))
+    host, st, _ = _render_gpu(empty, cam, opts)
+    assert st.n_visible == 0 and st.n_pairs == 0 and not host["rgb"].any() and not host["count"].any()
+    away = look_at_camera(np.array([0.0, -3.0, 0.0]), np.array([0.0, -6.0, 0.0]), width=128, height=128, fov_deg=50.0)
+    host, st, _ = _render_gpu(scene, away, opts)
+    assert st.n_visible == 0 and st.n_pairs == 0 and not host["rgb"].any() and not host["contrib"].any()
+    res = rasterize(scene, cam, opts)  # the next frame is the oracle's
+    assert np.array_equal(res.color.data, O.render(scene, cam, opts, tier)["img"].astype(np.float64))
+
+
+@pytest.mark.parametrize("prec,tier", PRECISIONS, ids=PREC_IDS)
+def test_largest_tile_grid_bit_exact(prec, tier):
+    """The ABI's largest tile grid (4096 x 4096 px = 65,536 tiles): tile lists, ranges and image
+    equal the oracle; one more tile column is refused with InvalidParameterError."""
+    from oracle import oracle as O
+    from paper_2403_13806_b200.core import InvalidParameterError, look_at_camera
+    from paper_2403_13806_b200.device import renderer
+    from paper_2403_13806_b200.synth import config1
+    from paper_2403_13806_b200.render import RasterizeOptions
+    scene, _ = config1(3, n=20_000, n_frames=1)
+    opts = RasterizeOptions(near_limit=0.2, precision=prec)
+    cam = look_at_camera((2.8, -1.1, 0.7), (0.1, 0.0, 0.0), width=4096, height=4096, fov_deg=55.0)
+    host, st, r = _render_gpu(scene, cam, opts)
+    fa = r.frame_arrays()
+    ob = O.bin_tiles(scene, cam, opts, tier)
+    assert st.n_pairs == ob["P"] and np.array_equal(fa["ranges"], ob["ranges"])
+    assert np.array_equal(fa["pair_items"], ob["vals"])
+    ref = O.views(scene, [cam], opts, tier, scores=True, images=True)
+    assert np.array_equal(host["rgb"], ref["img_last"]) and np.array_equal(host["contrib"], ref["contrib"])
+    too_wide = look_at_camera((2.8, -1.1, 0.7), (0.1, 0.0, 0.0), width=4112, height=4096, fov_deg=55.0)
+    with pytest.raises(InvalidParameterError):
+        _render_gpu(scene, too_wide, opts)
