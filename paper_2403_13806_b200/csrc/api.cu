@@ -130,7 +130,7 @@ Layout make_layout(int64_t n_cap, int64_t pair_cap, int W, int H, int sms) {
   L.proj_lb = take(((size_t)n_cap / kCompactKeys + 2) * sizeof(unsigned long long));
   L.ranges = take(TW * TH * sizeof(uint2));
   // dsort_kernel's per-pass digit tables (16-bit counts) and digit totals
-  L.dtab = take((size_t)4 * std::min(sms, kMaxDsortCtas) * 128 * 4 + 4 * 256 * 4);
+  L.dtab = take(dsort_tab_words(std::min(sms, kMaxDsortCtas)) * 4);  // dsort_kernel's digit tables
   L.scancls = take(2 * kScanClasses * 4);  // tile scan: list-length class counts and cursors
   L.scanpart = take(((size_t)TW * TH / kScanTiles + 1) * 8);  // tile scan: 64-tile block sums
   L.frame_bytes = o;
@@ -471,6 +471,10 @@ int32_t rs_bin(rs_workspace* ws, void* stream) {
         return e ? std::atoi(e) : 0;
       }();
       const int G = g_env > 0 ? std::min(g_env, G_dsort) : G_dsort;
+      static const int force_bins = [] {  // RS_DSORT_BINS=256: always 4 passes of 8-bit digits (tests, A/B)
+        const char* e = std::getenv("RS_DSORT_BINS");
+        return e ? std::atoi(e) : 0;
+      }();
       static const uint32_t red_max = [] {  // RS_DSORT_RED_MAX: the atomics/barrier switch (tests, A/B)
         const char* e = std::getenv("RS_DSORT_RED_MAX");
         return e ? (uint32_t)std::strtoul(e, nullptr, 10) : kDsortRedMax;
@@ -478,10 +482,10 @@ int32_t rs_bin(rs_workspace* ws, void* stream) {
       const cudaError_t e = ws->f64
           ? launch_coop(dsort_kernel<true>, G, kDsortThreads, sizeof(DsortSmem), st, ws->at<uint32_t>(ws->L.keysB), n,
                         ws->at<uint32_t>(ws->L.keysA), ws->at<uint32_t>(ws->L.valsA), ws->at<uint32_t>(ws->L.keysC),
-                        ws->at<uint32_t>(ws->L.valsB), ws->at<uint32_t>(ws->L.dtab), ws->ctr(), red_max)
+                        ws->at<uint32_t>(ws->L.valsB), ws->at<uint32_t>(ws->L.dtab), ws->ctr(), red_max, force_bins)
           : launch_coop(dsort_kernel<false>, G, kDsortThreads, sizeof(DsortSmem), st, ws->at<uint32_t>(ws->L.keysB), n,
                         ws->at<uint32_t>(ws->L.keysA), ws->at<uint32_t>(ws->L.valsA), ws->at<uint32_t>(ws->L.keysC),
-                        ws->at<uint32_t>(ws->L.valsB), ws->at<uint32_t>(ws->L.dtab), ws->ctr(), red_max);
+                        ws->at<uint32_t>(ws->L.valsB), ws->at<uint32_t>(ws->L.dtab), ws->ctr(), red_max, force_bins);
       if (e == cudaSuccess) {
         keys_res = ws->at<uint32_t>(ws->L.keysA);
         items_sorted = ws->at<uint32_t>(ws->L.valsA);
@@ -547,6 +551,9 @@ int32_t rs_bin(rs_workspace* ws, void* stream) {
            expand_major_thresh());
     cudaStreamWaitEvent(st, ws->ev_join, 0);
     g_pdl_class = kPdlChain;
+  } else {  // no items: no tile scan ran -- the blends' CTA -> tile map is the identity
+    const int T = ws->TW * ws->TH;
+    launch(tile_order_identity_kernel, (T + 255) / 256, 256, 0, st, ws->at<uint32_t>(ws->L.tileord), T);
   }
   ws->binned = true;
   return cuda_status();

@@ -76,38 +76,44 @@ __device__ __forceinline__ void grid_barrier(uint32_t* bar, uint32_t nblocks) {
   __syncthreads();
 }
 
+constexpr int kDsortMaxBins = 512;  // 9-bit digits (3 passes) when the keys' range allows
+
 struct DsortSmem {
-  uint32_t hist[256];                // running global offset of each digit for this CTA's keys
-  uint32_t whist[kDsortWarps][256];  // per-warp digit counts of a sub-chunk, then per-warp starts
-  uint32_t part[1][kDsortWarps][256];  // column-prefix partial sums: [row slice][digit]
-  uint32_t nexth[256];                 // this CTA's keys per next-pass digit (the digit totals)
-  uint32_t wsum[8];
+  uint32_t hist[kDsortMaxBins];                 // running global offset of each digit for this CTA's keys
+  uint32_t whist[kDsortWarps][kDsortMaxBins];   // per-warp digit counts of a sub-chunk, then per-warp starts
+  uint32_t part[kDsortWarps][kDsortMaxBins];    // column-prefix partial sums: [row slice][digit]
+  uint32_t nexth[kDsortMaxBins];                // this CTA's keys per next-pass digit (the digit totals)
+  uint32_t wsum[16];
 };
 
-// Column prefix of a pass's [G][256] digit histogram table (16-bit counts, two per word):
-// pre = sum over rows < b for digit tid < 256. CTAs in the first half sum the rows before
+// Column prefix of a pass's [G][NB] digit histogram table (16-bit counts, two per word):
+// pre = sum over rows < b for digit tid < NB. CTAs in the first half sum the rows before
 // them, the others the rows from b on and subtract from the pass's digit totals `gtot`
 // (accumulated separately) -- no CTA reads more than G/2 rows, and the table traffic of the
 // phase (every CTA reading it at once right after the barrier) is a quarter of a full
-// 32-bit read. Thread (slice w, digit group g) sums up to 3 rows of digits [8 g, 8 g + 8)
-// (one 16-byte load per row, all in flight); the 32 slices are combined in shared memory.
+// 32-bit read. Thread (slice w, digit group g) sums up to kRows rows of digits [8 g, 8 g + 8)
+// (one 16-byte load per row, all in flight); the slices are combined in shared memory.
+template <int NB>
 __device__ __forceinline__ void column_prefix(const uint32_t* __restrict__ table, const uint32_t* __restrict__ gtot,
                                               uint32_t G, uint32_t b, DsortSmem& S, uint32_t& pre,
                                               uint32_t& tot) {
-  const int tid = threadIdx.x, g = tid & 31, w = tid >> 5;
+  constexpr int kGroups = NB / 8, kSlices = kDsortThreads / kGroups;  // 32 x 32 (NB 256), 64 x 16 (NB 512)
+  constexpr int kRows = (80 + kSlices - 1) / kSlices;                  // slices x rows >= G / 2 (G <= 160)
+  constexpr int kQ = kDsortThreads / NB, kPerQ = kSlices / kQ;         // slice reducers per digit
+  const int tid = threadIdx.x, g = tid % kGroups, w = tid / kGroups;
   const bool low = 2 * b <= G;
   const uint32_t ra = low ? 0u : b, rb = low ? b : G;  // rows summed: [ra, rb), rb - ra <= G / 2
-  constexpr int kColRows = 3;                          // 32 slices x 3 rows >= 80 rows (G <= 160)
-  const uint32_t r0 = min(ra + w * kColRows, rb);
-  uint4 xs[kColRows];
+  const uint32_t r0 = min(ra + w * kRows, rb);
+  uint4 xs[kRows];
 #pragma unroll
-  for (int k = 0; k < kColRows; ++k) {  // every load issued before any is used
+  for (int k = 0; k < kRows; ++k) {  // every load issued before any is used
     const uint32_t r = r0 + k;
-    xs[k] = r < rb ? __ldcg(reinterpret_cast<const uint4*>(table + (size_t)r * 128) + g) : make_uint4(0, 0, 0, 0);
+    xs[k] = r < rb ? __ldcg(reinterpret_cast<const uint4*>(table + (size_t)r * (NB / 2)) + g)
+                   : make_uint4(0, 0, 0, 0);
   }
   uint32_t sp[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
-  for (int k = 0; k < kColRows; ++k) {
+  for (int k = 0; k < kRows; ++k) {
     const uint32_t v[4] = {xs[k].x, xs[k].y, xs[k].z, xs[k].w};
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -116,41 +122,52 @@ __device__ __forceinline__ void column_prefix(const uint32_t* __restrict__ table
     }
   }
 #pragma unroll
-  for (int k = 0; k < 8; ++k) S.part[0][w][8 * g + k] = sp[k];
+  for (int k = 0; k < 8; ++k) S.part[w][8 * g + k] = sp[k];
   __syncthreads();
-  {  // the 32 slices of digit d summed by 4 threads (8 slices each), then combined
-    const int d = tid & 255, q = tid >> 8;
+  {  // the slices of digit d summed by kQ threads (kPerQ slices each), then combined
+    const int d = tid % NB, q = tid / NB;
     uint32_t a = 0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) a += S.part[0][8 * q + k][d];
+    for (int k = 0; k < kPerQ; ++k) a += S.part[kPerQ * q + k][d];
     S.whist[q][d] = a;  // whist is free until the rank phase
   }
   __syncthreads();
   pre = 0;
   tot = 0;
-  if (tid < 256) {
+  if (tid < NB) {
     uint32_t sum = 0;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) sum += S.whist[q][tid];
+    for (int q = 0; q < kQ; ++q) sum += S.whist[q][tid];
     tot = __ldcg(gtot + tid);
     pre = low ? sum : tot - sum;
   }
 }
 
-// tables: 4 x [G][256] digit histograms (one per pass; 16-bit counts, two per word) and
-// 4 x [256] digit totals, zero on entry (the frame memset).
-// Pass p's table is complete at the barrier that starts pass p: pass 0's from the CTAs'
-// own item ranges, pass p+1's accumulated by pass p's scatter (each key is counted, with a
-// global atomic, for the CTA that owns its new position in pass p+1) -- one grid barrier
-// per pass.
-template <bool LAST_KEYS>
-__global__ void __launch_bounds__(kDsortThreads, 1) dsort_kernel(
-    const uint32_t* __restrict__ keys_all, uint32_t n_items, uint32_t* __restrict__ kA, uint32_t* __restrict__ vA,
-    uint32_t* __restrict__ kB, uint32_t* __restrict__ vB, uint32_t* __restrict__ tables,
-    Counters* __restrict__ ctr, uint32_t red_max) {
+// dtab layout (words; zero on entry, the frame memset): the pass-0 table [G][256] of raw
+// 9-bit digit counts (16-bit, two per word), the tables of passes 1.. ([G][NB / 2] each), the
+// digit totals [4][512] and each CTA's {smallest, largest} binned key [G][2].
+__host__ __device__ constexpr size_t dsort_tab_words(uint32_t G) { return (size_t)3 * G * 256 + 4 * 512 + 2 * G; }
+
+// The sort proper for NB-bin digits, after the kernel's pass-0 histogram and first barrier:
+// NB = 256 -> 4 passes of 8 bits over the raw keys; NB = 512 -> 3 passes of 9 bits over
+// key - kbase (the frame's keys span < 2^27). Pass 0's table holds raw 9-bit digit counts:
+// digit (key - kbase) & 511 is a rotation of key & 511 by kbase (NB 512), digit key & 255 a
+// fold of it (NB 256), applied to the column prefix. Pass p + 1's table is accumulated by
+// pass p's scatter (global atomics into the row of the CTA that will own each key's new
+// position; above red_max visible keys each CTA histograms its own range behind a second
+// barrier instead). Passes write A / B alternately so that the last one writes kA / vA.
+template <int NB, bool LAST_KEYS>
+__device__ __forceinline__ void dsort_body(uint32_t n_items, uint32_t* __restrict__ kA, uint32_t* __restrict__ vA,
+                                           uint32_t* __restrict__ kB, uint32_t* __restrict__ vB,
+                                           uint32_t* __restrict__ tables, Counters* __restrict__ ctr,
+                                           uint32_t red_max, uint32_t kbase, DsortSmem& S,
+                                           const uint32_t* __restrict__ keys_all, uint32_t (&kk)[kDsortItems],
+                                           bool one) {
+  constexpr int DB = NB == 512 ? 9 : 8;
+  constexpr int P = NB == 512 ? 3 : 4;
+  constexpr uint32_t M = NB - 1;
+  constexpr int NW = NB / 2;  // table words per row (passes >= 1)
   uint32_t* bar = ctr->gbar;
-  extern __shared__ __align__(16) unsigned char dsort_smem[];
-  DsortSmem& S = *reinterpret_cast<DsortSmem*>(dsort_smem);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t G = gridDim.x, b = blockIdx.x;
   const uint32_t lt = (1u << lane) - 1u;
@@ -158,44 +175,19 @@ __global__ void __launch_bounds__(kDsortThreads, 1) dsort_kernel(
   uint32_t nvis = 0, cs = 1;
   const uint32_t* kin = keys_all;
   const uint32_t* vin = nullptr;  // pass 0: value = item index
-  uint32_t* kout = kB;
-  uint32_t* vout = vB;
-  uint32_t kk[kDsortItems];
-  bool one;
+  uint32_t* kout = (P % 2 == 1) ? kA : kB;
+  uint32_t* vout = (P % 2 == 1) ? vA : vB;
   bool red = true;  // next pass's histograms by atomics during the scatter (set after pass 0's prefix)
-  uint32_t* gtot = tables + (size_t)4 * G * 128;  // [4][256] digit totals per pass
-  DSORT_MARK(0);
-  {  // pass 0's histogram: this CTA's item range (valid keys)
-    const uint32_t lo = min(b * ci, n_items), hi = min(lo + ci, n_items);
-    one = hi - lo <= (uint32_t)kDsortChunk;
-    if (tid < 256) {
-      S.hist[tid] = 0;
-      S.nexth[tid] = 0;
-    }
-    __syncthreads();
-    for (uint32_t base = lo; base < hi; base += kDsortChunk) {
-      const uint32_t wbase = base + warp * 32 * kDsortItems;
-#pragma unroll
-      for (int it = 0; it < kDsortItems; ++it) {
-        const uint32_t i = wbase + it * 32 + lane;
-        kk[it] = i < hi ? __ldcg(kin + i) : kInvalidKey;
-      }
-#pragma unroll
-      for (int it = 0; it < kDsortItems; ++it)
-        if (kk[it] != kInvalidKey) atomicAdd(&S.hist[kk[it] & 0xffu], 1u);
-    }
-    __syncthreads();
-    if (tid < 128) tables[(size_t)b * 128 + tid] = S.hist[2 * tid] | (S.hist[2 * tid + 1] << 16);
-    if (tid < 256 && S.hist[tid]) atomicAdd(gtot + tid, S.hist[tid]);
-  }
-  DSORT_MARK(1);
-  for (int p = 0; p < 4; ++p) {
-    const int shift = 8 * p;
-    grid_barrier(bar, G);
+  uint32_t* gtot = tables + (size_t)3 * G * 256;  // [4][512] digit totals
+  const uint32_t rot = kbase & 511u;
+  auto table_of = [&](int p) { return p == 0 ? tables : tables + (size_t)G * 256 + (size_t)(p - 1) * G * NW; };
+  for (int p = 0; p < P; ++p) {
+    const int shift = DB * p;
+    if (p > 0) grid_barrier(bar, G);
     if (p > 0 && !red) {  // this pass's histogram of the CTA's own range (written by the last scatter)
       const uint32_t lo = min(b * cs, nvis), hi = min(lo + cs, nvis);
       one = hi - lo <= (uint32_t)kDsortChunk;
-      if (tid < 256) S.hist[tid] = 0;
+      for (int i = tid; i < NB; i += kDsortThreads) S.hist[i] = 0;
       __syncthreads();
       for (uint32_t base = lo; base < hi; base += kDsortChunk) {
         const uint32_t wbase = base + warp * 32 * kDsortItems;
@@ -203,29 +195,50 @@ __global__ void __launch_bounds__(kDsortThreads, 1) dsort_kernel(
         for (int it = 0; it < kDsortItems; ++it) {
           const uint32_t i = wbase + it * 32 + lane;
           kk[it] = i < hi ? __ldcg(kin + i) : kInvalidKey;
-          if (i < hi) atomicAdd(&S.hist[(kk[it] >> shift) & 0xffu], 1u);
+          if (i < hi) atomicAdd(&S.hist[((kk[it] - kbase) >> shift) & M], 1u);
         }
       }
       __syncthreads();
-      uint32_t* tp = tables + (size_t)p * G * 128;
-      if (tid < 128) tp[(size_t)b * 128 + tid] = S.hist[2 * tid] | (S.hist[2 * tid + 1] << 16);
-      if (tid < 256 && S.hist[tid]) atomicAdd(gtot + p * 256 + tid, S.hist[tid]);
+      uint32_t* tp = table_of(p);
+      if (tid < NW) tp[(size_t)b * NW + tid] = S.hist[2 * tid] | (S.hist[2 * tid + 1] << 16);
+      if (tid < NB && S.hist[tid]) atomicAdd(gtot + p * 512 + tid, S.hist[tid]);
       grid_barrier(bar, G);
     }
     DSORT_MARK(2 + 4 * p);
     uint32_t pre, tot;
-    column_prefix(tables + (size_t)p * G * 128, gtot + p * 256, G, b, S, pre, tot);
+    if (p == 0) {  // raw 9-bit counts -> this pass's digits (rotation by kbase / fold to 8 bits)
+      uint32_t pr, tr;
+      column_prefix<512>(tables, gtot, G, b, S, pr, tr);
+      if (tid < 512) {
+        S.part[0][tid] = pr;
+        S.part[1][tid] = tr;
+      }
+      __syncthreads();
+      pre = tot = 0;
+      if (tid < NB) {
+        if (NB == 512) {
+          pre = S.part[0][(tid + rot) & 511u];
+          tot = S.part[1][(tid + rot) & 511u];
+        } else {
+          pre = S.part[0][tid] + S.part[0][tid + 256];
+          tot = S.part[1][tid] + S.part[1][tid + 256];
+        }
+      }
+      __syncthreads();
+    } else {
+      column_prefix<NB>(table_of(p), gtot + p * 512, G, b, S, pre, tot);
+    }
     uint32_t x = tot;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
       if (lane >= o) x += y;
     }
-    if (lane == 31 && warp < 8) S.wsum[warp] = x;
+    if (lane == 31 && warp < NB / 32) S.wsum[warp] = x;
     __syncthreads();
     uint32_t dstart = x - tot, all = 0;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) {
+    for (int w = 0; w < NB / 32; ++w) {
       dstart += w < warp ? S.wsum[w] : 0u;
       all += S.wsum[w];
     }
@@ -234,7 +247,7 @@ __global__ void __launch_bounds__(kDsortThreads, 1) dsort_kernel(
       cs = max((nvis + G - 1) / G, 1u);
       red = nvis <= red_max;
     }
-    if (tid < 256) S.hist[tid] = dstart + pre;  // where this CTA's first key of digit tid goes
+    if (tid < NB) S.hist[tid] = dstart + pre;  // where this CTA's first key of digit tid goes
     uint32_t lo, hi;
     if (p == 0) {
       lo = min(b * ci, n_items);
@@ -244,7 +257,7 @@ __global__ void __launch_bounds__(kDsortThreads, 1) dsort_kernel(
       hi = min(lo + cs, nvis);
       one = hi - lo <= (uint32_t)kDsortChunk;
     }
-    uint32_t* next = p < 3 && red ? tables + (size_t)(p + 1) * G * 128 : nullptr;
+    uint32_t* next = p < P - 1 && red ? table_of(p + 1) : nullptr;
     __syncthreads();
     DSORT_MARK(3 + 4 * p);
     // stable rank + scatter, sub-chunk by sub-chunk (warp-contiguous, item-major, lane-minor)
@@ -259,15 +272,15 @@ __global__ void __launch_bounds__(kDsortThreads, 1) dsort_kernel(
         vv[it] = vin ? (i < hi ? __ldcg(vin + i) : 0u) : i;  // values loaded with the keys
         ok[it] = i < hi && (p > 0 || kk[it] != kInvalidKey);
       }
-      for (int i = tid; i < kDsortWarps * 256; i += kDsortThreads) (&S.whist[0][0])[i] = 0;
+      for (int i = tid; i < kDsortWarps * NB; i += kDsortThreads) S.whist[i / NB][i % NB] = 0;
       __syncthreads();
       DSORT_MARK(20 + 3 * p);
 #pragma unroll
       for (int it = 0; it < kDsortItems; ++it) {
-        const uint32_t d = (kk[it] >> shift) & 0xffu;
+        const uint32_t d = ((kk[it] - kbase) >> shift) & M;
         uint32_t peers = __ballot_sync(0xffffffffu, ok[it]);
 #pragma unroll
-        for (int bt = 0; bt < 8; ++bt) {
+        for (int bt = 0; bt < DB; ++bt) {
           const uint32_t bal = __ballot_sync(0xffffffffu, (d >> bt) & 1u);
           peers &= ((d >> bt) & 1u) ? bal : ~bal;
         }
@@ -280,20 +293,22 @@ __global__ void __launch_bounds__(kDsortThreads, 1) dsort_kernel(
       }
       __syncthreads();
       DSORT_MARK(21 + 3 * p);
-      {  // per digit: start of each warp's run = running offset + earlier warps; 4 threads per
-         // digit (8 warps each), their totals combined through part[0]
-        const int d = tid & 255, qq = tid >> 8;
+      // per digit: start of each warp's run = running offset + earlier warps; 4 threads per
+      // digit (8 warps each), their totals combined through part, 256 digits at a time
+#pragma unroll
+      for (int dh = 0; dh < NB; dh += 256) {
+        const int d = dh + (tid & 255), qq = tid >> 8;
         uint32_t c[8], sum = 0;
 #pragma unroll
         for (int w = 0; w < 8; ++w) {
           c[w] = S.whist[8 * qq + w][d];
           sum += c[w];
         }
-        S.part[0][qq][d] = sum;
+        S.part[qq][d] = sum;
         __syncthreads();
         uint32_t run = S.hist[d];
 #pragma unroll
-        for (int q = 0; q < 3; ++q) run += q < qq ? S.part[0][q][d] : 0u;
+        for (int q = 0; q < 3; ++q) run += q < qq ? S.part[q][d] : 0u;
 #pragma unroll
         for (int w = 0; w < 8; ++w) {
           S.whist[8 * qq + w][d] = run;
@@ -307,22 +322,24 @@ __global__ void __launch_bounds__(kDsortThreads, 1) dsort_kernel(
 #pragma unroll
       for (int it = 0; it < kDsortItems; ++it) {
         if (!ok[it]) continue;
-        const uint32_t d = (kk[it] >> shift) & 0xffu;
+        const uint32_t d = ((kk[it] - kbase) >> shift) & M;
         const uint32_t pos = S.whist[warp][d] + rk[it];
-        if (p < 3 || LAST_KEYS) kout[pos] = kk[it];
+        if (p < P - 1 || LAST_KEYS) kout[pos] = kk[it];
         vout[pos] = vv[it];
         // next pass: this key belongs to the CTA that owns position pos
         if (next) {
-          const uint32_t dn = (kk[it] >> (shift + 8)) & 0xffu;
-          atomicAdd(next + (size_t)(pos / cs) * 128 + (dn >> 1), 1u << (16 * (dn & 1u)));
+          const uint32_t dn = ((kk[it] - kbase) >> (shift + DB)) & M;
+          atomicAdd(next + (size_t)(pos / cs) * NW + (dn >> 1), 1u << (16 * (dn & 1u)));
           atomicAdd(&S.nexth[dn], 1u);
         }
       }
       __syncthreads();
     }
-    if (next && tid < 256) {  // the next pass's digit totals
-      if (S.nexth[tid]) atomicAdd(gtot + (p + 1) * 256 + tid, S.nexth[tid]);
-      S.nexth[tid] = 0;
+    if (next) {  // the next pass's digit totals
+      for (int i = tid; i < NB; i += kDsortThreads) {
+        if (S.nexth[i]) atomicAdd(gtot + (p + 1) * 512 + i, S.nexth[i]);
+        S.nexth[i] = 0;
+      }
     }
     DSORT_MARK(4 + 4 * p);
     kin = kout;
@@ -331,6 +348,98 @@ __global__ void __launch_bounds__(kDsortThreads, 1) dsort_kernel(
     vout = (vout == vB) ? vA : vB;
   }
   if (b == 0 && tid == 0) ctr->n_visible = nvis;
+}
+
+// Pass 0's histogram (raw 9-bit digits) and each CTA's smallest / largest binned key, one grid
+// barrier, then the digit width: keys spanning fewer than 2^27 values -- depths within a
+// factor of ~2^16 of each other -- are sorted in 3 passes of 9-bit digits over key - smallest,
+// others in 4 passes of 8 bits (uniform over the grid: every CTA reduces the same [G][2]).
+template <bool LAST_KEYS>
+__global__ void __launch_bounds__(kDsortThreads, 1) dsort_kernel(
+    const uint32_t* __restrict__ keys_all, uint32_t n_items, uint32_t* __restrict__ kA, uint32_t* __restrict__ vA,
+    uint32_t* __restrict__ kB, uint32_t* __restrict__ vB, uint32_t* __restrict__ tables,
+    Counters* __restrict__ ctr, uint32_t red_max, int force_bins) {
+  extern __shared__ __align__(16) unsigned char dsort_smem[];
+  DsortSmem& S = *reinterpret_cast<DsortSmem*>(dsort_smem);
+  __shared__ uint32_t s_lo[kDsortWarps], s_hi[kDsortWarps];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t G = gridDim.x, b = blockIdx.x;
+  const uint32_t ci = (n_items + G - 1) / G;
+  uint32_t* gtot = tables + (size_t)3 * G * 256;
+  uint32_t* mm = gtot + 4 * 512;
+  uint32_t kk[kDsortItems];
+  bool one;
+  DSORT_MARK(0);
+  {  // pass 0's histogram of this CTA's item range (valid keys, raw 9-bit digits) and key range
+    const uint32_t lo = min(b * ci, n_items), hi = min(lo + ci, n_items);
+    one = hi - lo <= (uint32_t)kDsortChunk;
+    for (int i = tid; i < 512; i += kDsortThreads) {
+      S.hist[i] = 0;
+      S.nexth[i] = 0;
+    }
+    __syncthreads();
+    uint32_t klo = 0xffffffffu, khi = 0;
+    for (uint32_t base = lo; base < hi; base += kDsortChunk) {
+      const uint32_t wbase = base + warp * 32 * kDsortItems;
+#pragma unroll
+      for (int it = 0; it < kDsortItems; ++it) {
+        const uint32_t i = wbase + it * 32 + lane;
+        kk[it] = i < hi ? __ldcg(keys_all + i) : kInvalidKey;
+      }
+#pragma unroll
+      for (int it = 0; it < kDsortItems; ++it)
+        if (kk[it] != kInvalidKey) {
+          atomicAdd(&S.hist[kk[it] & 511u], 1u);
+          klo = min(klo, kk[it]);
+          khi = max(khi, kk[it]);
+        }
+    }
+    klo = __reduce_min_sync(0xffffffffu, klo);
+    khi = __reduce_max_sync(0xffffffffu, khi);
+    if (lane == 0) {
+      s_lo[warp] = klo;
+      s_hi[warp] = khi;
+    }
+    __syncthreads();
+    if (tid < 256) tables[(size_t)b * 256 + tid] = S.hist[2 * tid] | (S.hist[2 * tid + 1] << 16);
+    if (tid < 512 && S.hist[tid]) atomicAdd(gtot + tid, S.hist[tid]);
+    if (warp == 0) {
+      const uint32_t l = __reduce_min_sync(0xffffffffu, s_lo[lane]), h = __reduce_max_sync(0xffffffffu, s_hi[lane]);
+      if (lane == 0) {
+        mm[2 * b] = l;
+        mm[2 * b + 1] = h;
+      }
+    }
+  }
+  DSORT_MARK(1);
+  grid_barrier(ctr->gbar, G);
+  {  // the frame's key range: every CTA reduces the G pairs
+    uint32_t l = 0xffffffffu, h = 0;
+    for (uint32_t r = tid; r < G; r += kDsortThreads) {
+      l = min(l, __ldcg(mm + 2 * r));
+      h = max(h, __ldcg(mm + 2 * r + 1));
+    }
+    l = __reduce_min_sync(0xffffffffu, l);
+    h = __reduce_max_sync(0xffffffffu, h);
+    __syncthreads();  // s_lo / s_hi reuse
+    if (lane == 0) {
+      s_lo[warp] = l;
+      s_hi[warp] = h;
+    }
+    __syncthreads();
+  }
+  uint32_t klo = 0xffffffffu, khi = 0;
+#pragma unroll 8
+  for (int w = 0; w < kDsortWarps; ++w) {
+    klo = min(klo, s_lo[w]);
+    khi = max(khi, s_hi[w]);
+  }
+  const bool nine = force_bins != 256 && (khi < klo || khi - klo < (1u << 27));
+  if (nine)
+    dsort_body<512, LAST_KEYS>(n_items, kA, vA, kB, vB, tables, ctr, red_max, khi >= klo ? klo : 0u, S, keys_all,
+                               kk, one);
+  else
+    dsort_body<256, LAST_KEYS>(n_items, kA, vA, kB, vB, tables, ctr, red_max, 0u, S, keys_all, kk, one);
 }
 
 }  // namespace rs

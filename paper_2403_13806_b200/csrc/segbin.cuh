@@ -755,6 +755,15 @@ __global__ void __launch_bounds__(256) tile_chunks_kernel(const uint32_t* __rest
   }
 }
 
+// A frame without items (no tile scan): every range is empty (the frame memset) and the blend
+// order is the identity.
+__global__ void tile_order_identity_kernel(uint32_t* __restrict__ tile_order, int T) {
+  pdl_wait();
+  pdl_trigger();
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < T) tile_order[t] = (uint32_t)t;
+}
+
 // One CTA (64 threads) per 64-tile scan block: the block's exclusive start from the earlier
 // blocks' sums, each tile's range [start, end) (empty tiles [0, 0)), P and the pair-capacity
 // verdict (block 0), and the blend order: tiles by list-length class, longest first (class

@@ -431,3 +431,33 @@ def test_depth_ties_at_scale_bit_exact(prec, tier):
     # the ties are real: many equal depths among the binned items
     depth = ((pos[:, 1].astype(np.float64) + 4.0))[order]
     assert (np.diff(depth) == 0).mean() > 0.9
+
+
+@pytest.mark.parametrize("prec,tier", PRECISIONS, ids=PREC_IDS)
+def test_wide_depth_range_bit_exact(prec, tier):
+    """Binned depths from ~1 to ~1e6 (keys spanning more than 2^27 values): the cooperative depth
+    sort takes its 4-pass 8-bit-digit path; order, tile lists and image equal the oracle."""
+    from oracle import oracle as O
+    from paper_2403_13806_b200.core import look_at_camera
+    from paper_2403_13806_b200.render import RasterizeOptions
+    from paper_2403_13806_b200.synth import SceneArrays, config1
+    base, _ = config1(7, n=50_000, n_frames=1)
+    pos, ls, lg = base.positions.copy(), base.log_scales.copy(), base.opacity_logits.copy()
+    far = np.arange(0, 50_000, 500)  # 100 huge Gaussians far behind the cloud, on the view axis
+    rng = np.random.default_rng(1)
+    pos[far] = np.stack([rng.uniform(-2e4, 2e4, far.size), rng.uniform(1e5, 1e6, far.size),
+                         rng.uniform(-2e4, 2e4, far.size)], 1).astype(np.float32)
+    ls[far] = np.float32(9.0)
+    lg[far] = np.float32(3.0)
+    scene = SceneArrays(pos, lg, base.sh, ls, base.quaternions, 3)
+    cam = look_at_camera(np.array([0.0, -4.0, 0.0]), np.array([0.0, 0.0, 0.0]), width=320, height=240, fov_deg=60.0)
+    opts = RasterizeOptions(near_limit=0.2, precision=prec)
+    host, st, r = _render_gpu(scene, cam, opts)
+    fa = r.frame_arrays()
+    order = O.order(scene, cam, opts, tier)
+    assert np.array_equal(fa["items_sorted"][:st.n_visible].astype(np.int64), order)
+    assert np.isin(far, order).sum() > 20  # the far Gaussians are binned
+    ob = O.bin_tiles(scene, cam, opts, tier)
+    assert st.n_pairs == ob["P"] and np.array_equal(fa["pair_items"], ob["vals"])
+    ref = O.views(scene, [cam], opts, tier, scores=True, images=True)
+    assert np.array_equal(host["rgb"], ref["img_last"]) and np.array_equal(host["contrib"], ref["contrib"])

@@ -36,7 +36,7 @@ int main(int argc, char** argv) {
   cudaMalloc(&vA, n * 4);
   cudaMalloc(&kB, n * 4);
   cudaMalloc(&vB, n * 4);
-  cudaMalloc(&tab, 4 * 160 * 256 * 4);
+  cudaMalloc(&tab, dsort_tab_words(160) * 4);
   cudaMalloc(&ctr, sizeof(Counters));
   cudaMalloc(&probe, 160 * 32 * 8);
   cudaMemcpyToSymbol(g_dsort_probe, &probe, sizeof(probe));
@@ -50,7 +50,7 @@ int main(int argc, char** argv) {
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   for (int r = 0; r < reps + 3; ++r) {
-    cudaMemset(tab, 0, 4 * 160 * 256 * 4);
+    cudaMemset(tab, 0, dsort_tab_words(160) * 4);
     cudaMemset(ctr, 0, sizeof(Counters));
     cudaMemset(probe, 0, 160 * 32 * 8);
     cudaLaunchConfig_t cfg{};
@@ -64,7 +64,8 @@ int main(int argc, char** argv) {
     cfg.numAttrs = 1;
     cudaEventRecord(e0);
     cudaError_t e = cudaLaunchKernelEx(&cfg, dsort_kernel<false>, (const uint32_t*)dk, n, kA, vA, kB, vB, tab, ctr,
-                                       (uint32_t)(getenv("RS_DSORT_RED_MAX") ? atoi(getenv("RS_DSORT_RED_MAX")) : kDsortRedMax));
+                                       (uint32_t)(getenv("RS_DSORT_RED_MAX") ? atoi(getenv("RS_DSORT_RED_MAX")) : kDsortRedMax),
+                                       getenv("RS_DSORT_BINS") ? atoi(getenv("RS_DSORT_BINS")) : 0);
     cudaEventRecord(e1);
     cudaDeviceSynchronize();
     if (e != cudaSuccess || cudaGetLastError() != cudaSuccess) {
