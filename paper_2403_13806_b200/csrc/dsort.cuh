@@ -51,9 +51,9 @@ constexpr int kDsortChunk = kDsortThreads * kDsortItems;      // 4096
 // Up to kDsortRedMax visible keys (dsort_kernel's red_max; RS_DSORT_RED_MAX overrides it), the next pass's per-CTA histograms are accumulated with global
 // atomics during the scatter (one grid barrier per pass); above it, each CTA histograms its own
 // range after the scatter's barrier and publishes it behind a second barrier -- the per-key
-// atomics cost more than a barrier there (tools/dsort_probe.cu: 200k keys 46.7 vs 48.3 us,
-// 275k 52.0 vs 50.8 us, 500k 68.9 vs 62.4 us, 1M 109.8 vs 93.6 us).
-constexpr uint32_t kDsortRedMax = 240000;
+// atomics cost more than a barrier there (tools/dsort_probe.cu, 9-bit digits: 200k keys 43.3
+// vs 45.1 us, 275k 46.5 vs 47.2, 350k 50.3 vs 49.2, 500k 62.8 vs 58.3 us).
+constexpr uint32_t kDsortRedMax = 300000;
 
 // Grid barrier over the co-resident CTAs of a cooperative launch: arrive on a counter that
 // only grows (zeroed before the launch by the frame's counter memset), spin until it reaches
