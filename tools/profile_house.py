@@ -20,7 +20,7 @@ def main():
     kind = sys.argv[1] if len(sys.argv) > 1 else "filtered"
     frames = int(sys.argv[2]) if len(sys.argv) > 2 else 3
     scene, _, traj = synth.config3(0)
-    opts = RasterizeOptions(near_limit=0.2)
+    opts = RasterizeOptions(near_limit=0.2, precision="fp32")
     ds = device_scene(scene)
     r = renderer(ds.device)
     idx = None
