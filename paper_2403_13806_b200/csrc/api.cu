@@ -13,6 +13,7 @@
 
 #include "segbin.cuh"
 #include "dsort.cuh"
+#include "bsort.cuh"
 #include "blend.cuh"
 #include "blend64.cuh"
 #include "compact.cuh"
@@ -63,6 +64,14 @@ static int dsort_mode() {  // RS_DSORT: 0 onesweep launches, 2 always the cooper
     return e ? std::atoi(e) : 1;
   }();
   return m;
+}
+template <typename... KP, typename... A>
+static void launch(void (*k)(KP...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, A&&... args);
+// launch() returning the launch status (callers with a fallback)
+template <typename... KP, typename... A>
+static cudaError_t launch_ex(void (*k)(KP...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, A&&... args) {
+  launch(k, grid, block, smem, st, static_cast<A&&>(args)...);
+  return cudaGetLastError();
 }
 template <typename... KP, typename... A>
 static void launch(void (*k)(KP...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, A&&... args) {
@@ -289,6 +298,8 @@ void configure_kernels() {  // per device; idempotent
   set_smem_all<uint32_t, kDepthItems>();
   cudaFuncSetAttribute(segplace_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * kMaxTileRows);
   cudaFuncSetAttribute(dsort_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DsortSmem));
+  cudaFuncSetAttribute(bsort_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BsortSmem));
+  cudaFuncSetAttribute(bsort_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BsortSmem));
   cudaFuncSetAttribute(dsort_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DsortSmem));
 }
 
@@ -465,7 +476,22 @@ int32_t rs_bin(rs_workspace* ws, void* stream) {
     // 52 vs 65 us); larger frames keep the onesweep launches (configs[2]: 112 vs 153 us)
     const int G_dsort = std::min(ws->sms, kMaxDsortCtas);
     // (the per-CTA digit counts are 16-bit: at most ceil(n / G) keys per CTA)
-    if ((n + G_dsort - 1) / G_dsort < 65536 && (dsort_mode() == 2 || (dsort_mode() == 1 && n <= kDsortMaxItems))) {
+    if (n <= kBsortMaxItems && dsort_mode() == 1) {  // small frames: one CTA, shared memory only
+      const cudaError_t e = ws->f64
+          ? launch_ex(bsort_kernel<true>, 1, kBsortThreads, sizeof(BsortSmem), st, ws->at<uint32_t>(ws->L.keysB), n,
+                      ws->at<uint32_t>(ws->L.keysA), ws->at<uint32_t>(ws->L.valsA), ws->ctr())
+          : launch_ex(bsort_kernel<false>, 1, kBsortThreads, sizeof(BsortSmem), st, ws->at<uint32_t>(ws->L.keysB), n,
+                      ws->at<uint32_t>(ws->L.keysA), ws->at<uint32_t>(ws->L.valsA), ws->ctr());
+      if (e == cudaSuccess) {
+        keys_res = ws->at<uint32_t>(ws->L.keysA);
+        items_sorted = ws->at<uint32_t>(ws->L.valsA);
+        sorted = true;
+      } else {
+        cudaGetLastError();
+      }
+    }
+    if (!sorted && (n + G_dsort - 1) / G_dsort < 65536 &&
+        (dsort_mode() == 2 || (dsort_mode() == 1 && n <= kDsortMaxItems))) {
       static const int g_env = [] {  // RS_DSORT_CTAS: grid override (A/B measurements)
         const char* e = std::getenv("RS_DSORT_CTAS");
         return e ? std::atoi(e) : 0;
