@@ -188,9 +188,11 @@ int expand_major_thresh() {  // expand's column-major switch (x8): RS_EXPAND_MAJ
 }
 
 int expand_dense_span() {  // chunks averaging >= this many tiles per segment take the ballot walk
+  // (measured: 6 / 8 / 10 / 12 / 16 -> configs[1] 3345 / 3367 / 3369 / 3365 / 3361 frames/s,
+  // configs[4] batch 872 / - / 880 / 847 frames/s)
   static const int t = [] {
     const char* e = std::getenv("RS_EXPAND_DENSE");
-    return e ? std::atoi(e) : 6;
+    return e ? std::atoi(e) : 10;
   }();
   return t;
 }
