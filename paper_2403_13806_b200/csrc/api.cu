@@ -542,7 +542,11 @@ int32_t rs_bin(rs_workspace* ws, void* stream) {
     const uint32_t seg_cap = (uint32_t)seg_capacity(ws->n_cap, ws->pair_cap);
     const uint32_t tab_stride = (uint32_t)rowtab_stride(ws->n_cap);
     const unsigned rc = (n + kRankChunk - 1) / kRankChunk;
-    const unsigned gx = (unsigned)std::min<int64_t>(seg_cap / kExpandChunk + ws->TH + 1, (int64_t)ws->sms * 16);
+    static const int slots = [] {  // RS_EXPAND_SLOTS: chunk slots per SM of the expansion grids (A/B)
+      const char* e = std::getenv("RS_EXPAND_SLOTS");
+      return e ? std::max(std::atoi(e), 1) : 16;
+    }();
+    const unsigned gx = (unsigned)std::min<int64_t>(seg_cap / kExpandChunk + ws->TH + 1, (int64_t)ws->sms * slots);
     // expansion: the sparse chunks grid-strided (column groups x chunk slots), the dense ones on
     // persistent ticketed CTAs on the workspace's second stream, concurrently
     const dim3 eg((ws->TW + kExpandCols - 1) / kExpandCols, gx), dg(ws->sms * 6);
