@@ -55,7 +55,8 @@ WORKLOADS = {"render": "configs[1] orbit render", "score": "configs[2] importanc
 SWEEP_N = (125_000, 250_000, 500_000, 1_000_000, 2_000_000, 3_000_000)
 TRAFFIC = {"render_fp32": "profiles/round2_full_configs1_fp32_traffic.json",
            "render_fp64": "profiles/round2_full_configs1_fp64_traffic.json",
-           "score_fp32": "profiles/round2_full_configs2_fp32_traffic.json"}
+           "score_fp32": "profiles/round2_full_configs2_fp32_traffic.json",
+           "batch_fp32": "profiles/round2_full_configs4_fp32_traffic.json"}
 
 
 def parse():
@@ -220,9 +221,15 @@ def profiled_traffic(which: str, kernel: str):
     """DRAM bytes per launch of `kernel` (the warm-workspace frame's launch) from the committed
     ncu --set full capture of that workload (profiles/round2_full_*.csv), or None."""
     try:
-        return json.loads((ROOT / TRAFFIC[which]).read_text()).get(kernel)
+        table = json.loads((ROOT / TRAFFIC[which]).read_text())
     except (KeyError, OSError, ValueError):
         return None
+    # ncu names carry the namespace ("rs::blend2_kernel<1, 0, 0, 1, 0>"); match without it
+    want = kernel.split(" (")[0].replace(" ", "").removeprefix("rs::")
+    for name, v in table.items():
+        if name.replace(" ", "").removeprefix("rs::") == want:
+            return v
+    return None
 
 
 def make_config(workload: str, scene_n: int, W: int, H: int, world: int) -> dict:
@@ -861,7 +868,10 @@ def run_trajectory(args, ctx):
         "roofline": {"kernel": ("blend64_kernel<1, 0, 0, 1>" if f64 else "blend2_kernel<1, 0, 0, 1, 0>")
                      + (" (unfiltered frames)" if house else ""),
                      "bound": "fp64" if f64 else "fp32", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
-                     "frac": ach / peak, "traffic": None, "algorithmic": "16*E + 11*C flops per frame (SURVEY §8d)",
+                     "frac": ach / peak,
+                     "traffic": None if (house or f64) else profiled_traffic("batch_fp32", "blend2_kernel<1, 0, 0, 1, 0>"),
+                     "traffic_source": None if (house or f64) else TRAFFIC["batch_fp32"],
+                     "algorithmic": "16*E + 11*C flops per frame (SURVEY §8d)",
                      "peak_source": "computed: SMs x %d FP%d lanes x 2 x sm_max_mhz" % ((64, 64) if f64 else (128, 32))},
         "frame_roofline": {"bytes_alg_per_frame": main_arm["bytes_alg_per_frame"],
                            "achieved_gbs": main_arm["bytes_alg_per_frame"] / (t_frame / 1e3) / 1e9,
