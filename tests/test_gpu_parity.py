@@ -461,3 +461,44 @@ def test_wide_depth_range_bit_exact(prec, tier):
     assert st.n_pairs == ob["P"] and np.array_equal(fa["pair_items"], ob["vals"])
     ref = O.views(scene, [cam], opts, tier, scores=True, images=True)
     assert np.array_equal(host["rgb"], ref["img_last"]) and np.array_equal(host["contrib"], ref["contrib"])
+
+
+@pytest.mark.parametrize("prec,tier", PRECISIONS, ids=PREC_IDS)
+def test_precull_border_scene_bit_exact(prec, tier):
+    """Culling and binning at the image border: 60k Gaussians whose centres project into a 300-px band around the image
+    border (and beyond), at depths from just past the near plane to 40, with log-scales from
+    -6 to 4 and strong anisotropy -- order, tile lists and image equal the oracle's; many binned
+    Gaussians have their centre outside the image and many are culled."""
+    from oracle import oracle as O
+    from paper_2403_13806_b200.core import look_at_camera
+    from paper_2403_13806_b200.render import RasterizeOptions
+    from paper_2403_13806_b200.synth import SceneArrays
+    rng = np.random.default_rng(11)
+    n, W, H = 60_000, 320, 240
+    cam = look_at_camera(np.array([0.0, -4.0, 0.0]), np.array([0.0, 0.0, 0.0]), width=W, height=H, fov_deg=60.0)
+    side = rng.integers(0, 4, n)
+    u = rng.uniform(-300.0, 300.0, n)
+    mx = np.where(side == 0, u, np.where(side == 1, W + u, rng.uniform(-300.0, W + 300.0, n)))
+    my = np.where(side == 2, u, np.where(side == 3, H + u, rng.uniform(-300.0, H + 300.0, n)))
+    z = np.where(rng.random(n) < 0.1, rng.uniform(0.15, 0.3, n), np.exp(rng.uniform(np.log(0.3), np.log(40.0), n)))
+    pc = np.stack([(mx - cam.cx) * z / cam.fx, (my - cam.cy) * z / cam.fy, z], 1)
+    pos = ((pc - cam.translation) @ cam.rotation).astype(np.float32)  # R^T (p_cam - t)
+    ls = rng.normal(-2.0, 1.5, (n, 3))
+    ls[:, 0] += rng.normal(0.0, 2.0, n)  # anisotropy
+    ls = np.clip(ls, -6.0, 4.0).astype(np.float32)
+    q = rng.normal(size=(n, 4))
+    q = (q / np.linalg.norm(q, axis=1, keepdims=True)).astype(np.float32)
+    lg = rng.normal(0.0, 2.0, n).astype(np.float32)
+    sh = (rng.normal(0.0, 0.3, (n, 3, 16))).astype(np.float32)
+    scene = SceneArrays(pos, lg, sh, ls, q, 3)
+    opts = RasterizeOptions(near_limit=0.2, precision=prec)
+    host, st, r = _render_gpu(scene, cam, opts)
+    fa = r.frame_arrays()
+    order = O.order(scene, cam, opts, tier)
+    assert np.array_equal(fa["items_sorted"][:st.n_visible].astype(np.int64), order)
+    ob = O.bin_tiles(scene, cam, opts, tier)
+    assert st.n_pairs == ob["P"] and np.array_equal(fa["pair_items"], ob["vals"])
+    ref = O.views(scene, [cam], opts, tier, scores=True, images=True)
+    assert np.array_equal(host["rgb"], ref["img_last"]) and np.array_equal(host["contrib"], ref["contrib"])
+    outside = (mx[order] < 0) | (mx[order] >= W) | (my[order] < 0) | (my[order] >= H)
+    assert outside.sum() > 2000 and len(order) < n - 10_000, (outside.sum(), len(order))
