@@ -224,6 +224,19 @@ constexpr int kBlendUnroll = RS_BLEND_UNROLL;  // list entries per inner iterati
 #define RS_BLEND_MINB_S 6
 #endif
 
+// Record staging of blend2 (RS_BLEND_CPASYNC, colour frames): the {mx,my,na,nb} /
+// {nc,o,cut2,depth} / colour quads go global -> shared with 16-byte cp.async (LDGSTS, no
+// register round trip); only the box quad (and the row geometry for the quarter masks) is
+// loaded into registers.
+#ifndef RS_BLEND_CPASYNC
+#define RS_BLEND_CPASYNC 1
+#endif
+__device__ __forceinline__ void stage16(void* smem, const void* gmem) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void stage_wait() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
 template <bool COLOR, bool STATS, bool FAST>
 __device__ __forceinline__ float blend_px(const float4 ga, const float4 gb, const float4 gc, float xs, float ys,
                                           const Opt32& o, float& tau, float& cr, float& cg, float& cb,
@@ -271,6 +284,9 @@ __global__ void __launch_bounds__(kBlend2Threads, COLOR ? RS_BLEND_MINB : RS_BLE
   constexpr int kBatch = RS_BLEND_BATCH;  // entries staged per batch
   constexpr int kPerThread = kBatch / kBlend2Threads;
   constexpr int U = COLOR ? kBlendUnroll : RS_BLEND_UNROLL_S;
+  // cp.async record staging for colour frames (configs[1] blend 169.8 -> 168.9 us); score-only
+  // frames keep the register path (1557 vs 1555 views/s with cp.async)
+  constexpr bool kCp = RS_BLEND_CPASYNC && COLOR;
   // slot kBatch: an empty-box sentinel that pads every warp list to a multiple of U entries
   __shared__ Rec s_rec[kBatch + 1 > 160 ? kBatch + 1 : 160];  // >= 10 KB: the float64 epilogue's staging
   __shared__ uint32_t s_w[CONTRIB ? kBatch + 1 : 1];
@@ -326,12 +342,19 @@ __global__ void __launch_bounds__(kBlend2Threads, COLOR ? RS_BLEND_MINB : RS_BLE
       if (idx < end) {
         const uint32_t it = __ldg(pair_items + idx);
         const Rec* R = recs + it;
-        const float4 a = __ldg(&R->a);
-        s_rec[slot].a = a;
-        s_rec[slot].b = __ldg(&R->b);
-        const float4 c = __ldg(&R->c);
-        if (COLOR || CONTRIB) s_rec[slot].c = c;
-        gid[h] = (uint32_t)__float_as_int(c.w);
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+        if constexpr (kCp) {
+          stage16(&s_rec[slot].a, &R->a);
+          stage16(&s_rec[slot].b, &R->b);
+          stage16(&s_rec[slot].c, &R->c);
+        } else {
+          a = __ldg(&R->a);
+          s_rec[slot].a = a;
+          s_rec[slot].b = __ldg(&R->b);
+          const float4 c = __ldg(&R->c);
+          if (COLOR || CONTRIB) s_rec[slot].c = c;
+          gid[h] = (uint32_t)__float_as_int(c.w);
+        }
         const int4 dr = __ldg(&R->d);
         const int4 d = cullbox_of(dr);  // only as the s_boxm bits below (the walk never reads E.d)
 #pragma unroll
@@ -352,13 +375,27 @@ __global__ void __launch_bounds__(kBlend2Threads, COLOR ? RS_BLEND_MINB : RS_BLE
           // a box over several quarters: the ones the ellipse strips of the tile's two half-rows
           // reach -- a warp whose quarter no pixel of the entry can composite in never walks it
           // (STATS keeps the box quarters: every in-box pixel is evaluated, the oracle's E count)
-          m = quarter_mask(load_row_geom(geom + 2 * (size_t)it, a.x, a.y), d, ox, oy);
+          RowGeom g = load_row_geom(geom + 2 * (size_t)it, a.x, a.y);
+          if constexpr (kCp) {
+            stage_wait();  // this thread's own copies: mx, my readable from its slot
+            g.mx = s_rec[slot].a.x;
+            g.my = s_rec[slot].a.y;
+          }
+          m = quarter_mask(g, d, ox, oy);
         }
         s_mask[slot] = (uint8_t)m;
       }
       if (CONTRIB) s_w[slot] = 0u;
     }
+    if constexpr (kCp) stage_wait();
     __syncthreads();
+    if constexpr (kCp && CONTRIB) {
+#pragma unroll
+      for (int h = 0; h < kPerThread; ++h) {
+        const int slot = tid + h * kBlend2Threads;
+        gid[h] = base + slot < end ? (uint32_t)__float_as_int(s_rec[slot].c.w) : 0u;
+      }
+    }
     const int n = (int)min((uint32_t)kBatch, end - base);
     if (!__all_sync(0xffffffffu, done0 && done1)) {
       int cntw = 0;
