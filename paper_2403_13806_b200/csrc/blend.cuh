@@ -520,7 +520,9 @@ __global__ void __launch_bounds__(kBlend2Threads, COLOR ? RS_BLEND_MINB : RS_BLE
         if (__all_sync(0xffffffffu, done0 && done1)) break;  // all 64 pixels of the warp terminated
       }
     }
-    __syncthreads();
+    // the batch's score slots are complete once every warp has walked it; without scores the
+    // next batch's __syncthreads_and is the barrier before the slots are restaged
+    if (CONTRIB) __syncthreads();
     if (CONTRIB) {
 #pragma unroll
       for (int h = 0; h < kPerThread; ++h) {

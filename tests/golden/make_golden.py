@@ -237,6 +237,7 @@ def main():
 
     make_io(fs, cf)
     make_grad(fs, cf)
+    make_grad_c0(fs)
     make_metrics(fs, cf)
     make_scale(fs)
     print("golden fixtures written to", HERE)
@@ -307,6 +308,37 @@ def make_grad(fs, conftest):
             d[p + "g_" + k] = np.asarray(g[k])
     d["cases"] = np.array([c[0] for c in cases])
     np.savez_compressed(HERE / "grad.npz", **d)
+
+
+def make_grad_c0(fs):
+    """J': backward pass at BASELINE configs[0] scale (4,096 Gaussians, 128x128, SH degree 3,
+    near_limit 0.2): the reference's fp64 gradients through a seeded random image weight."""
+    R = fs.render
+    from paper_2403_13806_b200.synth import config0
+    arrs, _ = config0(0)
+    scene = fs.GaussianScene(positions=arrs.positions.astype(np.float64),
+                             opacity_logits=arrs.opacity_logits.astype(np.float64),
+                             sh=arrs.sh.astype(np.float64), log_scales=arrs.log_scales.astype(np.float64),
+                             quaternions=arrs.quaternions.astype(np.float64), active_sh_degree=3)
+    cam = fs.look_at_camera((0.0, -3.0, 0.0), (0.0, 0.0, 0.0), width=128, height=128, fov_deg=50.0)
+    opts = R.RasterizeOptions(near_limit=0.2)
+    # the scene is synth.config0(0) and the weight image rng(5).normal: regenerated by the test
+    # (the digest pins them); the gradients of the touched Gaussians are stored as float32
+    # (rounding ~6e-8 relative, far below the test's 2e-5 of scale)
+    import hashlib
+    d = {"scene_sha1": np.array(hashlib.sha1(b"".join(np.ascontiguousarray(a).tobytes() for a in (
+        arrs.positions, arrs.opacity_logits, arrs.sh, arrs.log_scales, arrs.quaternions))).hexdigest())}
+    w = np.random.default_rng(5).normal(size=(cam.height, cam.width, 3))
+    out, cache = R.rasterize_cached(scene, cam, opts)
+    g = R.rasterize_backward(scene, cam, cache, w)
+    t = np.asarray(g["touched"], bool)
+    d["img"] = np.asarray(out.color.data, np.float32)
+    d["touched"] = t
+    for k in ("positions", "sh", "log_scales", "quaternions", "opacity_logits", "mean2d_grad_norm"):
+        a = np.asarray(g[k])
+        assert np.all(a[~t] == 0)
+        d["g_" + k] = a[t].astype(np.float32)
+    np.savez_compressed(HERE / "grad_c0.npz", **d)
 
 
 def make_metrics(fs, conftest):
@@ -407,6 +439,9 @@ if __name__ == "__main__":
     elif sys.argv[1:] == ["grad"]:  # only the backward-pass fixtures
         fs_, conftest_, _ = import_reference()
         make_grad(fs_, conftest_)
+    elif sys.argv[1:] == ["grad_c0"]:  # only the configs[0]-scale backward fixture
+        fs_, _, _ = import_reference()
+        make_grad_c0(fs_)
     elif sys.argv[1:] == ["metrics"]:  # only the image-metric fixtures
         fs_, conftest_, _ = import_reference()
         make_metrics(fs_, conftest_)

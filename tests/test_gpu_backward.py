@@ -96,3 +96,31 @@ def test_device_resident_training_step():
     ref, _ = render_device(upd, cam, opts)
     assert torch.equal(img2["rgb"], ref["rgb"])
     assert not torch.equal(img2["rgb"], img["rgb"])
+
+
+def test_backward_matches_reference_at_config0_scale():
+    """BASELINE configs[0] (4,096 Gaussians, 128x128, SH degree 3, near plane 0.2): every
+    gradient array within REL of its scale of the reference's fp64 gradients
+    (tests/golden/grad_c0.npz: `make_golden.py grad_c0`; the scene is synth.config0(0), pinned
+    by its digest, the weight image rng(5).normal)."""
+    import hashlib
+    from paper_2403_13806_b200.core import look_at_camera
+    from paper_2403_13806_b200.render import RasterizeOptions, rasterize_backward, rasterize_cached
+    from paper_2403_13806_b200.synth import config0
+    d = golden("grad_c0")
+    arrs, _ = config0(0)
+    sha = hashlib.sha1(b"".join(np.ascontiguousarray(a).tobytes() for a in (
+        arrs.positions, arrs.opacity_logits, arrs.sh, arrs.log_scales, arrs.quaternions))).hexdigest()
+    assert sha == str(d["scene_sha1"])
+    cam = look_at_camera((0.0, -3.0, 0.0), (0.0, 0.0, 0.0), width=128, height=128, fov_deg=50.0)
+    out, cache = rasterize_cached(arrs, cam, RasterizeOptions(near_limit=0.2))
+    assert np.abs(out.color.data - d["img"]).max() < 1e-4
+    g = rasterize_backward(arrs, cam, cache, np.random.default_rng(5).normal(size=(128, 128, 3)))
+    t = d["touched"]
+    assert np.array_equal(np.asarray(g["touched"], bool), t)
+    for k in KEYS:
+        ref = d["g_" + k].astype(np.float64)
+        got = np.asarray(g[k])[t]
+        scale = np.abs(ref).max()
+        err = np.abs(got - ref).max()
+        assert err <= REL * scale + 1e-6, f"cfg0.{k}: max err {err} vs scale {scale}"
