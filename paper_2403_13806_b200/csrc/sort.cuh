@@ -203,7 +203,10 @@ __global__ void __launch_bounds__(kSortThreads, 4) onesweep_kernel(
   // decoupled look-back for the exclusive prefix (LB predecessors per round trip)
   uint32_t excl = 0;
   if (c > 0) {
-    constexpr int LB = 4;
+#ifndef RS_SORT_LB
+#define RS_SORT_LB 4  // measured 4 / 8 / 16 / 32: configs[2] 1557 / 1555 / 1537 / 1496 views/s
+#endif
+    constexpr int LB = RS_SORT_LB;
     int j = (int)c - 1;
     for (;;) {
       uint32_t s[LB];
