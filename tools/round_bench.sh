@@ -1,3 +1,5 @@
+# Every bench line of the round (render with its fp64 / score / fps_vs_n blocks, score, batch,
+# train, house, the reference arm) plus the parity tests, into gpurun_out/final/.
 mkdir -p gpurun_out/final
 timeout 600 python -m pytest tests/test_gpu_backward.py tests/test_gpu_parity.py -x -q > gpurun_out/final/tests.log 2>&1
 timeout 500 python bench.py > gpurun_out/final/render.json 2> gpurun_out/final/render.err
