@@ -502,3 +502,64 @@ def test_precull_border_scene_bit_exact(prec, tier):
     assert np.array_equal(host["rgb"], ref["img_last"]) and np.array_equal(host["contrib"], ref["contrib"])
     outside = (mx[order] < 0) | (mx[order] >= W) | (my[order] < 0) | (my[order] >= H)
     assert outside.sum() > 2000 and len(order) < n - 10_000, (outside.sum(), len(order))
+
+
+def _random_frame(seed: int):
+    """A seeded random frame: scene size, distributions (uniform box + clusters, isotropic to
+    strongly anisotropic and heavy-tailed scales, SH degree 0-3), camera (outside or inside the
+    cloud, any aspect, tiny to 1.5k-wide images, narrow to wide fov) and options (near plane,
+    alpha thresholds, low-pass, sigma bound) all drawn from ``seed``."""
+    from paper_2403_13806_b200.core import look_at_camera
+    from paper_2403_13806_b200.synth import SceneArrays
+    rng = np.random.default_rng(1000 + seed)
+    n = int(rng.integers(200, 30_000))
+    box = float(rng.uniform(0.5, 4.0))
+    k = int(rng.integers(1, 40))
+    centers = rng.uniform(-box, box, (k, 3))
+    pick = rng.integers(0, k, n)
+    means = np.where(rng.random((n, 1)) < 0.3, rng.uniform(-box, box, (n, 3)),
+                     centers[pick] + rng.normal(0.0, float(rng.uniform(0.02, 0.5)), (n, 3)))
+    ls = rng.normal(float(rng.uniform(-5.0, -1.5)), float(rng.uniform(0.1, 1.2)), (n, 3))
+    ls[:, 0] += rng.normal(0.0, float(rng.uniform(0.0, 1.5)), n)
+    ls = np.minimum(ls, 1.0)
+    q = rng.normal(size=(n, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    lg = rng.normal(0.0, float(rng.uniform(0.5, 3.0)), n)
+    sh = rng.normal(0.0, 0.1, (n, 3, 16))
+    sh[:, :, 0] = rng.normal(0.0, 0.6, (n, 3))
+    deg = int(rng.integers(0, 4))
+    scene = SceneArrays(means.astype(np.float32), lg.astype(np.float32), sh.astype(np.float32),
+                        ls.astype(np.float32), q.astype(np.float32), deg)
+    inside = rng.random() < 0.25
+    r = float(rng.uniform(0.1, 0.6) * box) if inside else float(rng.uniform(1.2, 3.0) * box)
+    d = rng.normal(size=3)
+    eye = d / np.linalg.norm(d) * r
+    target = rng.normal(0.0, 0.3 * box, 3)
+    W, H = (int(rng.integers(9, 1500)), int(rng.integers(7, 900))) if rng.random() < 0.3 else \
+        (int(rng.integers(9, 400)), int(rng.integers(7, 300)))
+    cam = look_at_camera(eye, target, width=W, height=H, fov_deg=float(rng.uniform(25.0, 110.0)))
+    opts = [float(rng.uniform(0.9, 0.999)), float(rng.choice([1.0 / 255.0, 1e-3, 0.02])),
+            float(rng.choice([1e-4, 1e-3, 0.05])), float(rng.uniform(0.01, 0.5)),
+            float(rng.choice([0.3, 0.1, 1.0])), float(rng.choice([3.0, 2.5, 4.0]))]
+    return scene, cam, opts
+
+
+@pytest.mark.parametrize("prec,tier", PRECISIONS, ids=PREC_IDS)
+@pytest.mark.parametrize("seed", range(64))
+def test_random_frames_bit_exact(seed, prec, tier):
+    """64 seeded random frames (scene, camera and options all drawn per seed: _random_frame):
+    images, counts, scores and tile lists equal the oracle's in both precisions."""
+    scene, cam, vals = _random_frame(seed)
+    opts = options_from(vals, prec)
+    O = _oracle()
+    ref = O.render(scene, cam, opts, tier)
+    got, st, r = _render_gpu(scene, cam, opts)
+    for k in ("img", "alpha", "depth"):
+        g = got["rgb"] if k == "img" else got[k]
+        assert np.array_equal(g, ref[k]), f"seed {seed}: {k} max diff {np.abs(g - ref[k]).max()}"
+    assert np.array_equal(got["count"], ref["count"]), seed
+    assert np.array_equal(got["contrib"], ref["contrib"]), seed
+    ob = O.bin_tiles(scene, cam, opts, tier)
+    fa = r.frame_arrays()
+    assert st.n_pairs == ob["P"] and np.array_equal(fa["pair_items"], ob["vals"]), seed
+    assert np.array_equal(fa["ranges"], ob["ranges"]), seed
