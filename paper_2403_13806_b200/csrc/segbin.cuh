@@ -43,7 +43,10 @@ constexpr int kExpandCols = 32;                // tile columns per expand CTA (8
 constexpr int kMaxTileRows = 2048;             // image height <= 32767 px
 constexpr int kMaxTileCols = 2048;             // image width <= 32767 px
 constexpr int kRankChunk = 256;                // depth ranks per placement chunk (one CTA)
-constexpr int kExpandChunk = 1024;             // segments per expansion chunk (rows cut into chunks)
+#ifndef RS_EXPAND_CHUNK
+#define RS_EXPAND_CHUNK 1024  // measured 512 / 1024 / 2048: render 3375 / 3380 / 3316 fps, score
+#endif                          // 1492 / 1558 / 1564 views/s, configs[4] 859 / 900 / 913 fps
+constexpr int kExpandChunk = RS_EXPAND_CHUNK;  // segments per expansion chunk (rows cut into chunks)
 
 // Tile rows [r0, r1] of a binned record's culling box.
 __device__ __forceinline__ void box_rows(const int4 cb, int& r0, int& r1) {
