@@ -10,6 +10,12 @@ __global__ void stream_out(const double2* __restrict__ src, double2* __restrict_
     dst[i] = src[i];
 }
 
+__global__ void busy(float* p, int iters) {
+  float x = threadIdx.x;
+  for (int i = 0; i < iters; ++i) x = x * 1.0000001f + 0.5f;
+  p[blockIdx.x * blockDim.x + threadIdx.x] = x;
+}
+
 int main() {
   const size_t bytes = 1256ull * 828 * 40;
   void *dev, *host;
@@ -56,6 +62,32 @@ int main() {
     cudaEventDestroy(e);
   }, 20);
   printf("copy engine, 8 bands on 2 streams: %.3f ms  %.1f GB/s\n", ms, bytes / ms / 1e6);
+  // three copies per frame in the rgb / alpha / count split (24 / 8 / 8 B per px), B bands
+  for (int B : {1, 2, 4, 8}) {
+    const size_t np = bytes / 40;
+    ms = timeit([&] {
+      for (int k = 0; k < B; ++k) {
+        const size_t p0 = np * k / B, p1 = np * (k + 1) / B;
+        cudaMemcpyAsync((char*)host + p0 * 24, (char*)dev + p0 * 24, (p1 - p0) * 24, cudaMemcpyDeviceToHost, s[0]);
+        cudaMemcpyAsync((char*)host + np * 24 + p0 * 8, (char*)dev + np * 24 + p0 * 8, (p1 - p0) * 8,
+                        cudaMemcpyDeviceToHost, s[0]);
+        cudaMemcpyAsync((char*)host + np * 32 + p0 * 8, (char*)dev + np * 32 + p0 * 8, (p1 - p0) * 8,
+                        cudaMemcpyDeviceToHost, s[0]);
+      }
+    }, 20);
+    printf("copy engine, 3 arrays x %d bands: %.3f ms  %.1f GB/s\n", B, ms, bytes / ms / 1e6);
+  }
+  // one copy while a compute kernel keeps every SM busy on another stream
+  {
+    void* scratch;
+    cudaMalloc(&scratch, 256 << 20);
+    ms = timeit([&] {
+      busy<<<148 * 4, 256, 0, s[1]>>>((float*)scratch, 4000);
+      cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, s[0]);
+    }, 10);
+    printf("copy engine under a busy kernel (timed on the copy stream): %.3f ms  %.1f GB/s\n", ms, bytes / ms / 1e6);
+    cudaDeviceSynchronize();
+  }
   double2* hd;
   cudaHostGetDevicePointer((void**)&hd, host, 0);
   for (int G : {8, 16, 32, 64, 148, 296, 592}) {

@@ -48,3 +48,17 @@ torch.cuda.synchronize()
 t_dev = sum(a.elapsed_time(b) for a, b in ev) / n / 1e3
 print(f"{prec}: rasterize {t_ras*1e3:.3f} ms ({1/t_ras:.0f} fps) | pinned alloc x3 {t_alloc*1e3:.3f} ms | "
       f"render(prealloc) {t_render*1e3:.3f} ms | device span {t_dev*1e3:.3f} ms")
+# frames launched back to back (no host sync per frame): the device-bound rate of host-output frames
+from paper_2403_13806_b200.device import camera_struct, options_struct  # noqa: E402
+opt_s = options_struct(opts)
+structs = [camera_struct(c) for c in cams[:n]]
+for cs in structs[:3]:
+    r.launch(ds, cs, opt_s, out)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for cs in structs:
+    r.launch(ds, cs, opt_s, out)
+e1.record()
+torch.cuda.synchronize()
+print(f"{prec}: back-to-back host-output frames {e0.elapsed_time(e1) / n:.3f} ms/frame (device-bound)")
