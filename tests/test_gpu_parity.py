@@ -563,3 +563,42 @@ def test_random_frames_bit_exact(seed, prec, tier):
     fa = r.frame_arrays()
     assert st.n_pairs == ob["P"] and np.array_equal(fa["pair_items"], ob["vals"]), seed
     assert np.array_equal(fa["ranges"], ob["ranges"]), seed
+
+
+@pytest.mark.parametrize("prec,tier", PRECISIONS, ids=PREC_IDS)
+@pytest.mark.parametrize("seed", range(16))
+def test_random_filtered_frames_bit_exact(seed, prec, tier):
+    """16 seeded random frames rendered through ``rasterize_filtered`` with a random indicator
+    (5-90% active): colour, alpha and count equal the oracle's render of the same indicator."""
+    from paper_2403_13806_b200.render import rasterize_filtered
+    scene, cam, vals = _random_frame(100 + seed)
+    opts = options_from(vals, prec)
+    rng = np.random.default_rng(seed)
+    active = rng.random(len(scene)) < float(rng.uniform(0.05, 0.9))
+    ref = _oracle().render(scene, cam, opts, tier, active=active)
+    got = rasterize_filtered(scene, cam, active, opts)
+    assert np.array_equal(got.color.data.astype(ref["img"].dtype), ref["img"]), seed
+    assert np.array_equal(got.alpha.astype(ref["alpha"].dtype), ref["alpha"]), seed
+    assert np.array_equal(got.count, ref["count"]), seed
+
+
+@pytest.mark.parametrize("prec,tier", PRECISIONS, ids=PREC_IDS)
+@pytest.mark.parametrize("seed", range(12))
+def test_random_scoring_passes_bit_exact(seed, prec, tier):
+    """12 seeded random scenes scored by ``compute_importance`` from 2-7 random cameras of
+    mixed sizes (one pass, the views launched without a host sync each): the table equals the
+    oracle's per-view max-merge; the keep mask at a random threshold follows."""
+    from paper_2403_13806_b200.pruning import compute_importance
+    scene, _, vals = _random_frame(200 + seed)
+    rng = np.random.default_rng(seed)
+    cams = [_random_frame(300 + 10 * seed + k)[1] for k in range(int(rng.integers(2, 8)))]
+    opts = options_from(vals, prec)
+    table = compute_importance(scene, cams, opts)
+    vt = np.float32 if prec == "fp32" else np.float64
+    exp = np.zeros(len(scene), vt)
+    O = _oracle()
+    for cam in cams:
+        exp = np.maximum(exp, O.render(scene, cam, opts, tier)["contrib"])
+    assert np.array_equal(table.values.astype(vt), exp), seed
+    h = float(rng.choice([1e-4, 1e-3, 1e-2]))
+    assert np.array_equal(table.values >= h, exp.astype(np.float64) >= h)
