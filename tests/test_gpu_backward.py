@@ -129,3 +129,68 @@ def test_backward_matches_reference_at_config0_scale():
         scale = np.abs(ref).max()
         assert (err <= REL * scale + 1e-6).mean() >= 0.998, f"cfg0.{k}"
         assert err.max() <= 2e-3 * scale, f"cfg0.{k}: max err {err.max()} vs scale {scale}"
+
+
+def _fd_scene(seed: int):
+    """A seeded random scene of 300-3,000 Gaussians in front of a 64-128 px camera."""
+    from paper_2403_13806_b200.core import look_at_camera
+    from paper_2403_13806_b200.synth import SceneArrays
+    rng = np.random.default_rng(500 + seed)
+    n = int(rng.integers(300, 3000))
+    means = rng.uniform(-1.0, 1.0, (n, 3))
+    ls = np.minimum(rng.normal(-3.0, 0.5, (n, 3)), -1.0)
+    q = rng.normal(size=(n, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    sh = rng.normal(0.0, 0.1, (n, 3, 16))
+    sh[:, :, 0] = rng.normal(0.0, 0.6, (n, 3))
+    scene = SceneArrays(means.astype(np.float32), rng.normal(0.0, 1.5, n).astype(np.float32),
+                        sh.astype(np.float32), ls.astype(np.float32), q.astype(np.float32), int(rng.integers(0, 4)))
+    d = rng.normal(size=3)
+    cam = look_at_camera(d / np.linalg.norm(d) * float(rng.uniform(2.5, 4.0)), (0.0, 0.0, 0.0),
+                         width=int(rng.integers(64, 129)), height=int(rng.integers(64, 129)),
+                         fov_deg=float(rng.uniform(40.0, 70.0)))
+    return scene, cam, rng
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_backward_matches_central_differences(seed):
+    """Random scenes: the fp32 backward's gradients of L = sum(w * colour) against central
+    differences of the fp64 forward (the same fp32-exact parameters, h = 1e-5) for the
+    Gaussians and parameters with the largest gradients. A perturbation that flips a composite
+    decision (the count image changes) makes L discontinuous and is skipped. Tolerance: 2e-4 of
+    the parameter array's largest gradient (fp32 vs fp64 forward)."""
+    from paper_2403_13806_b200.core import GaussianScene
+    from paper_2403_13806_b200.render import RasterizeOptions, rasterize, rasterize_backward, rasterize_cached
+    scene, cam, rng = _fd_scene(seed)
+    w = rng.normal(size=(cam.height, cam.width, 3))
+    _, cache = rasterize_cached(scene, cam, RasterizeOptions())
+    g = rasterize_backward(scene, cam, cache, w)
+    base = dict(positions=scene.positions.astype(np.float64), log_scales=scene.log_scales.astype(np.float64),
+                quaternions=scene.quaternions.astype(np.float64),
+                opacity_logits=scene.opacity_logits.astype(np.float64), sh=scene.sh.astype(np.float64))
+    o64 = RasterizeOptions(precision="fp64")
+
+    def loss(key, idx, delta):
+        arrs = {k: v.copy() for k, v in base.items()}
+        arrs[key][idx] += delta
+        out = rasterize(GaussianScene(active_sh_degree=scene.active_sh_degree, **arrs), cam, o64)
+        return float((w * out.color.data).sum()), out.count
+
+    h = 1e-5
+    checked = 0
+    for key, comp in (("positions", (0, 1, 2)), ("log_scales", (0, 1, 2)), ("opacity_logits", (None,)),
+                      ("quaternions", (0, 1, 2, 3)), ("sh", ((0, 0), (1, 0), (2, 0)))):
+        ga = np.asarray(g[key], np.float64)
+        scale = np.abs(ga).max()
+        for c in comp:
+            col = ga if c is None else ga[(slice(None),) + (c if isinstance(c, tuple) else (c,))]
+            for i in np.argsort(-np.abs(col))[:2]:
+                idx = (int(i),) if c is None else (int(i),) + (c if isinstance(c, tuple) else (c,))
+                lp, cp = loss(key, idx, h)
+                lm, cm = loss(key, idx, -h)
+                if not np.array_equal(cp, cm):
+                    continue  # a composite decision flipped between the two evaluations
+                fd = (lp - lm) / (2 * h)
+                assert abs(fd - col[int(i)]) <= 2e-4 * scale, (key, idx, fd, col[int(i)], scale)
+                checked += 1
+    assert checked >= 20
