@@ -549,7 +549,8 @@ int32_t rs_bin(rs_workspace* ws, void* stream) {
     const unsigned gx = (unsigned)std::min<int64_t>(seg_cap / kExpandChunk + ws->TH + 1, (int64_t)ws->sms * slots);
     // expansion: the sparse chunks grid-strided (column groups x chunk slots), the dense ones on
     // persistent ticketed CTAs on the workspace's second stream, concurrently
-    const dim3 eg((ws->TW + kExpandCols - 1) / kExpandCols, gx), dg(ws->sms * 6);
+    const unsigned groups = (ws->TW + kExpandCols - 1) / kExpandCols;
+    const dim3 eg((groups + RS_EXPAND_GROUPS - 1) / RS_EXPAND_GROUPS, gx), dg(ws->sms * 6);
     const int T = ws->TW * ws->TH;
     launch(segrows_kernel, rc, 256, 0, st, items_sorted, ws->at<uint32_t>(ws->L.rows), ctr, ws->TH, tab_stride,
            ws->at<uint32_t>(ws->L.rowtab));

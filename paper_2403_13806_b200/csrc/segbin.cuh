@@ -465,6 +465,9 @@ __device__ __forceinline__ void expand_dense_chunk(const uint32_t* __restrict__ 
 }
 
 constexpr int kExpandSub = kExpandChunk / 256;  // 32-segment sub-steps per warp per chunk
+#ifndef RS_EXPAND_GROUPS
+#define RS_EXPAND_GROUPS 4  // column groups per sparse-expansion CTA (measured 1 / 2 / 4: score
+#endif                      // 1545 / 1554 / 1563 views/s, render 3381 / 3390 / 3380 fps)
 
 __global__ void __launch_bounds__(256) expand_kernel(const uint32_t* __restrict__ seg_item,
                                                      const uint32_t* __restrict__ seg_span,
@@ -482,8 +485,8 @@ __global__ void __launch_bounds__(256) expand_kernel(const uint32_t* __restrict_
   if (ctr->overflow) return;
   const uint32_t lt = (1u << lane) - 1u;
   // column group fastest in the grid: a chunk's CTAs run together and share its segments in L2
-  const int g0 = blockIdx.x * kExpandCols;  // this CTA's first tile column
-  const int c = g0 + lane;                  // lane's column (every warp)
+  // (RS_EXPAND_GROUPS > 1: each CTA walks that many column groups of a chunk, the chunk's spans
+  // and items loaded once)
   const uint32_t n_chunks = chunk_start[TH];
   int flip = 0;
   for (uint32_t gc = blockIdx.y; gc < n_chunks; gc += gridDim.y) {  // chunks of all rows, grid-strided
@@ -491,7 +494,6 @@ __global__ void __launch_bounds__(256) expand_kernel(const uint32_t* __restrict_
     if (info.y >> 31) continue;         // dense: expand_dense_kernel (concurrently, on a second stream)
     const int ty = (int)(info.y & 0xffffu);
     const uint32_t cnt = (info.y >> 16) & 0x7fffu;
-    const uint32_t pos = c < TW ? ranges[ty * TW + c].x + chunk_count[(size_t)gc * TW + c] : 0u;
     // warp w: the chunk's segments [128 w, 128 w + 128), 32 per sub-step, all loads issued up front
     uint32_t sid[kExpandSub], m[kExpandSub], item[kExpandSub], cm[kExpandSub];
 #pragma unroll
@@ -502,13 +504,25 @@ __global__ void __launch_bounds__(256) expand_kernel(const uint32_t* __restrict_
     uint32_t sp[kExpandSub];
 #pragma unroll
     for (int k = 0; k < kExpandSub; ++k) sp[k] = seg_span[sid[k] != 0xffffffffu ? sid[k] : 0u];  // all in flight
+#if RS_EXPAND_GROUPS > 1
+    uint32_t it_all[kExpandSub];
+#pragma unroll
+    for (int k = 0; k < kExpandSub; ++k) it_all[k] = sid[k] != 0xffffffffu ? seg_item[sid[k]] : 0u;
+#endif
+    for (int g0 = blockIdx.x * kExpandCols; g0 < TW; g0 += gridDim.x * kExpandCols) {
+    const int c = g0 + lane;  // lane's column (every warp)
+    const uint32_t pos = c < TW ? ranges[ty * TW + c].x + chunk_count[(size_t)gc * TW + c] : 0u;
 #pragma unroll
     for (int k = 0; k < kExpandSub; ++k) {
       const int a = max((int)(sp[k] & 0xffffu) - g0, 0), b = min((int)(sp[k] >> 16) - g0, kExpandCols - 1);
       m[k] = sid[k] != 0xffffffffu && a <= b ? (0xffffffffu >> (31 - b)) & (0xffffffffu << a) : 0u;
     }
 #pragma unroll
+#if RS_EXPAND_GROUPS > 1
+    for (int k = 0; k < kExpandSub; ++k) item[k] = m[k] ? it_all[k] : 0u;
+#else
     for (int k = 0; k < kExpandSub; ++k) item[k] = m[k] ? seg_item[sid[k]] : 0u;
+#endif
     // the warp's segments that reach the CTA's columns, compacted in order (fewer transposes)
     uint32_t nrel = 0;
 #pragma unroll
@@ -568,6 +582,7 @@ __global__ void __launch_bounds__(256) expand_kernel(const uint32_t* __restrict_
         }
       }
     }
+    }  // column groups
   }
 }
 
