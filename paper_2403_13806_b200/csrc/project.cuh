@@ -125,7 +125,12 @@ __device__ __forceinline__ int64_t item_index(const int32_t* __restrict__ active
 }
 
 template <bool FULL, bool COLOR, typename TS>
-__global__ void __launch_bounds__(128) project_kernel(const TS* __restrict__ planes,
+#ifdef RS_PROJ_MINB  // measurement: CTAs per SM the register allocation must allow
+#define RS_PROJ_BOUNDS __launch_bounds__(128, RS_PROJ_MINB)
+#else
+#define RS_PROJ_BOUNDS __launch_bounds__(128)
+#endif
+__global__ void RS_PROJ_BOUNDS project_kernel(const TS* __restrict__ planes,
                                                       const TS* __restrict__ sh, int64_t stride, int deg,
                                                       const int32_t* __restrict__ active_idx, uint32_t n_items,
                                                       int64_t n_scene,
