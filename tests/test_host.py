@@ -411,3 +411,17 @@ def test_cluster_bitset_gather_gloo_world2():
         assert p.exitcode == 0
     for _, got, exp in res:
         assert got == exp
+
+
+def test_bench_roofline_traffic_resolves():
+    """bench.py's roofline.traffic comes from the committed ncu captures: every kernel name the
+    bench lines look up resolves to the warm frame's DRAM bytes (not null)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench_mod", ROOT / "bench.py")
+    b = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(b)
+    for which, kern in (("render_fp32", "blend2_kernel<1, 0, 0, 1, 0>"), ("render_fp64", "blend64_kernel<1, 0, 0, 1>"),
+                        ("score_fp32", "blend2_kernel<0,1,0,1,0> (score)"),
+                        ("batch_fp32", "blend2_kernel<1, 0, 0, 1, 0>")):
+        v = b.profiled_traffic(which, kern)
+        assert v is not None and v > 1e6, (which, kern, v)
